@@ -1,0 +1,161 @@
+/*
+ * ob_api.h -- C ABI of libomega_b200.so, the B200-native Omega serving hot path.
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (streams travel as uint64 handles).  Every call returns an ob_status;
+ * ob_last_error() gives the thread-local message of the last failure.
+ *
+ * Each entry point replaces one piece of the reference's Python serving API
+ * (paths relative to /root/reference/pkg/src/gnnserve):
+ *
+ *   ob_engine_create      ServingEngine.__init__ + ServeConfig      runtime.py:62-82, 258-288
+ *   ob_load_graph         GraphDataset / build_csr (device resident) graphstore.py:40-88
+ *   ob_load_pe            PeStore (device resident)                 graphstore.py:122-171
+ *   ob_load_model         ModelSpec + Weights (weight_matrix_names)  models.py:47-133
+ *   ob_precompute_pe      precompute_embeddings                      graphstore.py:330-365
+ *   ob_read_pe            PeStore.layers[l-1] readback               graphstore.py:143-152
+ *   ob_serve              ServingEngine.serve -> (emb, breakdown)    runtime.py:308-358
+ *   ob_serve_device       same, request already in device memory     (bench: HBM-resident inputs)
+ *   ob_last_plan          RecomputationPlan / CandidateSet (parity)  policy.py:38-61, 64-135
+ *   ob_last_block_sizes   ComputationBlock sizes (parity hook)       compgraph.py:33-57
+ *   ob_last_block         ComputationBlock arrays (parity hook)      compgraph.py:33-57
+ *   ob_nccl_unique_id     bootstrap for one-process-per-GPU CGP      collectives.py:94-137 (World)
+ *
+ * Status -> Python exception mapping:
+ *   OB_EINVAL -> ValueError, OB_ENOTFOUND -> KeyError, OB_ECOMM -> TransportError,
+ *   OB_ECUDA / OB_ENOMEM / OB_ESTATE -> RuntimeError.
+ */
+#ifndef OB_API_H
+#define OB_API_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OB_API_VERSION 1
+
+typedef struct ob_engine ob_engine;
+
+enum ob_status {
+  OB_OK = 0,
+  OB_EINVAL = 1,     /* bad argument / request / config          -> ValueError     */
+  OB_ENOTFOUND = 2,  /* row not stored locally                    -> KeyError       */
+  OB_ECOMM = 3,      /* collective failure                        -> TransportError */
+  OB_ECUDA = 4,      /* CUDA runtime error                        -> RuntimeError   */
+  OB_ENOMEM = 5,     /* device allocation failure                 -> RuntimeError   */
+  OB_ESTATE = 6      /* call out of order (e.g. serve before load) -> RuntimeError  */
+};
+
+/* ServeConfig.strategy (runtime.py:51); "sampled" is out of scope. */
+enum ob_strategy { OB_STRATEGY_FULL = 0, OB_STRATEGY_SRPE = 2, OB_STRATEGY_SRPE_CGP = 3 };
+
+/* ServeConfig.policy (policy.py:29-32); only the ratio policy is on the hot path. */
+enum ob_policy { OB_POLICY_RATIO = 0 };
+
+/* Layer kinds use the reference's on-disk tags (models.py:36 KIND_TAGS). */
+enum ob_kind {
+  OB_KIND_GCN = 0,
+  OB_KIND_SAGE_MEAN = 1,
+  OB_KIND_GAT = 2,
+  OB_KIND_POWER_MEAN = 3,
+  OB_KIND_MOMENTS = 4,
+  OB_KIND_SAGE_MAX = 5
+};
+
+typedef struct {
+  int32_t device;          /* CUDA ordinal                                       */
+  int32_t strategy;        /* enum ob_strategy                                   */
+  double gamma;            /* recompute budget in [0, 1]                         */
+  int32_t policy;          /* enum ob_policy                                     */
+  int32_t num_partitions;  /* CGP partitions P (1 for centralized strategies)    */
+  int32_t rank;            /* this process's partition when nccl_id != NULL      */
+  uint64_t seed;           /* partition hash seed (ServeConfig.seed)             */
+  uint64_t stream;         /* cudaStream_t to launch on; 0 = engine-owned stream */
+  const void* nccl_id;     /* 128-byte ncclUniqueId: one process per GPU / rank;
+                              NULL with P > 1 = all P partitions on this device  */
+} ob_config;
+
+typedef struct {
+  int32_t kind;     /* enum ob_kind */
+  int32_t in_dim;
+  int32_t out_dim;
+  float p;          /* power_mean exponent */
+  int32_t n;        /* moments order */
+} ob_layer;
+
+/* LatencyBreakdown (runtime.py:85-95) plus device-side counters. */
+typedef struct {
+  double fetch_ms;          /* selection + graph construction (device time)          */
+  double transfer_ms;       /* fetch_bytes / bandwidth, as the reference models it   */
+  double compute_ms;        /* per-layer execution (device time)                     */
+  int64_t collective_bytes; /* bytes this engine sent to peers (NVLink)              */
+  int64_t fetch_bytes;      /* graph_fetch_bytes (runtime.py:105-120)                */
+  int64_t num_candidates;
+  int64_t num_targets;
+  int64_t h2d_bytes;        /* request bytes copied host -> device                   */
+  int64_t d2h_bytes;        /* result bytes copied device -> host                    */
+  double total_device_ms;   /* whole request on the device                           */
+} ob_breakdown;
+
+const char* ob_last_error(void);
+int ob_version(void);
+
+int ob_engine_create(const ob_config* cfg, ob_engine** out);
+int ob_engine_destroy(ob_engine* e);
+
+/* In-CSR graph: offsets[N+1], neighbours[E] (sources ascending per destination
+ * after load; duplicates kept), features N x F row-major float32. */
+int ob_load_graph(ob_engine* e, int64_t num_nodes, const int64_t* in_offsets,
+                  const int64_t* in_neighbors, int64_t num_edges, const float* features,
+                  int32_t feature_dim);
+
+/* Stored embeddings for layer `layer` (1-based), N x dim float32. */
+int ob_load_pe(ob_engine* e, int32_t layer, const float* rows, int64_t num_rows, int32_t dim);
+
+/* k layers; mats lists every matrix in weight_matrix_names order per layer
+ * (gcn: w; sage_*: w_self, w_neigh; gat: w, a_src, a_dst; power_mean/moments:
+ * w_self, w), each row-major float32 in_dim x out_dim (a_* are out_dim). */
+int ob_load_model(ob_engine* e, int32_t k, const ob_layer* layers, const float* const* mats);
+
+/* precompute_embeddings on the device: PE layers 1..k-1 from the loaded graph. */
+int ob_precompute_pe(ob_engine* e);
+int ob_read_pe(ob_engine* e, int32_t layer, float* out_rows);
+
+/* Serve one query batch.  Host pointers: query_features B x F, edges m x 2
+ * int64 (src, dst) global ids with queries numbered N..N+B-1.  out: B x H_k
+ * float32 in query-id order.  bd may be NULL.  Under CGP with one process per
+ * GPU every rank calls this with the full request; rank 0 receives `out`. */
+int ob_serve(ob_engine* e, int32_t num_queries, const float* query_features, int64_t num_edges,
+             const int64_t* edges, float* out, ob_breakdown* bd);
+
+/* Same with device pointers (request already resident in HBM); `out` is a
+ * device pointer.  Work is enqueued on the engine stream; with bd == NULL the
+ * call does not synchronise (errors are reported by the next call). */
+int ob_serve_device(ob_engine* e, int32_t num_queries, const float* d_query_features,
+                    int64_t num_edges, const int64_t* d_edges, float* d_out, ob_breakdown* bd);
+
+/* Parity hooks over the last served request (synchronising). */
+int ob_last_plan(ob_engine* e, int64_t* num_candidates, int64_t* num_targets, int64_t* cand_ids,
+                 int64_t* cand_nq, int64_t* cand_total, double* cand_scores, int64_t* targets);
+int ob_last_block_sizes(ob_engine* e, int32_t partition, int32_t layer, int64_t* num_src,
+                        int64_t* num_dst, int64_t* num_edges);
+int ob_last_block(ob_engine* e, int32_t partition, int32_t layer, int64_t* src_ids,
+                  int64_t* dst_ids, int64_t* edge_src, int64_t* edge_dst, uint8_t* bind_kind,
+                  int32_t* bind_pe_layer, int64_t* src_degree, int64_t* dst_self_src);
+
+/* Partition map of a CGP engine (owner per node), for parity checks. */
+int ob_partition_owner(ob_engine* e, int64_t* owner);
+
+/* Kernel-launch counter (own kernels only), for the bench's gpu_launches. */
+int64_t ob_launch_count(ob_engine* e);
+
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 of a CGP group). */
+int ob_nccl_unique_id(void* out128);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OB_API_H */

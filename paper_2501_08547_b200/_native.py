@@ -1,0 +1,123 @@
+"""ctypes binding of libomega_b200.so (include/ob_api.h).
+
+The product path has no CPU fallback: importing this module without the
+built library raises ImportError with the build command.  Status codes map
+to the reference's exception types.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libomega_b200.so")
+
+OB_OK, OB_EINVAL, OB_ENOTFOUND, OB_ECOMM, OB_ECUDA, OB_ENOMEM, OB_ESTATE = range(7)
+STRATEGY = {"full": 0, "srpe": 2, "srpe-cgp": 3}
+POLICY = {"ratio": 0}
+KIND_TAGS = {"gcn": 0, "sage_mean": 1, "gat": 2, "power_mean": 3, "moments": 4, "sage_max": 5}
+
+
+class TransportError(RuntimeError):
+    """Collective failure (collectives.py:31)."""
+
+
+class ObConfig(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32),
+        ("strategy", C.c_int32),
+        ("gamma", C.c_double),
+        ("policy", C.c_int32),
+        ("num_partitions", C.c_int32),
+        ("rank", C.c_int32),
+        ("seed", C.c_uint64),
+        ("stream", C.c_uint64),
+        ("nccl_id", C.c_void_p),
+    ]
+
+
+class ObLayer(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32),
+        ("in_dim", C.c_int32),
+        ("out_dim", C.c_int32),
+        ("p", C.c_float),
+        ("n", C.c_int32),
+    ]
+
+
+class ObBreakdown(C.Structure):
+    _fields_ = [
+        ("fetch_ms", C.c_double),
+        ("transfer_ms", C.c_double),
+        ("compute_ms", C.c_double),
+        ("collective_bytes", C.c_int64),
+        ("fetch_bytes", C.c_int64),
+        ("num_candidates", C.c_int64),
+        ("num_targets", C.c_int64),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
+        ("total_device_ms", C.c_double),
+    ]
+
+
+_P = C.c_void_p
+_I64P = C.POINTER(C.c_int64)
+_SIGS = {
+    "ob_last_error": (C.c_char_p, []),
+    "ob_version": (C.c_int, []),
+    "ob_engine_create": (C.c_int, [C.POINTER(ObConfig), C.POINTER(_P)]),
+    "ob_engine_destroy": (C.c_int, [_P]),
+    "ob_load_graph": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int64, _P, C.c_int32]),
+    "ob_load_pe": (C.c_int, [_P, C.c_int32, _P, C.c_int64, C.c_int32]),
+    "ob_load_model": (C.c_int, [_P, C.c_int32, C.POINTER(ObLayer), C.POINTER(C.c_void_p)]),
+    "ob_precompute_pe": (C.c_int, [_P]),
+    "ob_read_pe": (C.c_int, [_P, C.c_int32, _P]),
+    "ob_serve": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(ObBreakdown)]),
+    "ob_serve_device": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(ObBreakdown)]),
+    "ob_last_plan": (C.c_int, [_P, _I64P, _I64P, _P, _P, _P, _P, _P]),
+    "ob_last_block_sizes": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P, _I64P, _I64P]),
+    "ob_last_block": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ob_partition_owner": (C.c_int, [_P, _P]),
+    "ob_launch_count": (C.c_int64, [_P]),
+    "ob_nccl_unique_id": (C.c_int, [_P]),
+}
+EXPORTED = tuple(_SIGS)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2501_08547_b200.build` "
+            "(the serving path has no CPU fallback)"
+        )
+    # torch (if present) loads libnccl first; our NEEDED entry then resolves to the same copy
+    lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int) -> None:
+    if status == OB_OK:
+        return
+    msg = lib.ob_last_error().decode(errors="replace")
+    if status == OB_EINVAL:
+        raise ValueError(msg)
+    if status == OB_ENOTFOUND:
+        raise KeyError(msg)
+    if status == OB_ECOMM:
+        raise TransportError(msg)
+    raise RuntimeError(f"libomega_b200: {msg} (status {status})")
+
+
+def ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)

@@ -1,0 +1,708 @@
+// ob_api.cu -- engine lifecycle, per-request workspace planning, the serve
+// pipeline and the C ABI (include/ob_api.h).
+//
+// ServingEngine.serve (runtime.py:308-335) becomes one stream-ordered
+// sequence: H2D request -> validate/mark -> candidates -> scores -> radix
+// select -> request CSR -> blocks -> layers -> D2H rows.  Request-dependent
+// sizes never leave the device; the host only sizes the workspace from
+// bounds (m, B, dataset degree profile) and reads the counters back once.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+
+#include "ob_engine.h"
+
+#ifdef OB_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace ob {
+
+static thread_local std::string t_err;
+
+Engine::~Engine() {
+  if (arena.base) cudaFree(arena.base);
+  for (void* p : owned) cudaFree(p);
+  for (auto& ev_ : ev)
+    if (ev_) cudaEventDestroy(ev_);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+// sum of the r largest in-degrees: bound on the CSR edges r destinations can pull
+static int64_t topdeg(const GraphDev& g, int64_t r) {
+  if (g.topdeg_prefix.empty()) return g.E;
+  r = std::max<int64_t>(0, std::min<int64_t>(r, (int64_t)g.topdeg_prefix.size() - 1));
+  return g.topdeg_prefix[r];
+}
+
+struct Plan {
+  int64_t words_N, words_NB, R_max, RB_max, T_max, max_scan_n;
+  std::vector<BlockDev> blocks;
+};
+
+static Plan plan_request(const Engine& e, int B, int64_t m) {
+  Plan p{};
+  const int64_t N = e.g.N;
+  const int k = (int)e.layers.size();
+  p.words_N = (N + 31) / 32;
+  p.words_NB = (N + B + 31) / 32;
+  p.R_max = std::min<int64_t>(N, 2 * m);
+  p.RB_max = p.R_max + B;
+  p.T_max = std::min<int64_t>(p.R_max, (int64_t)std::floor(e.cfg.gamma * (double)p.R_max) + 1);
+  auto mk = [&](int64_t D, int64_t E, bool self) {
+    BlockDev b;
+    b.D_max = std::max<int64_t>(D, 1);
+    b.E_max = std::max<int64_t>(E, 1);
+    int64_t S = std::min<int64_t>(N + B, E + (self ? D : 0));
+    b.S_max = std::max<int64_t>(S, 1);
+    b.items_max = b.E_max / kAggChunk + b.D_max + 1;
+    b.has_self = self;
+    return b;
+  };
+  if (e.cfg.strategy == OB_STRATEGY_FULL) {
+    p.blocks.resize(k);
+    int64_t D = B;
+    for (int l = k; l >= 1; --l) {
+      int64_t E = topdeg(e.g, std::min<int64_t>(N, D)) + m;
+      E = std::min<int64_t>(E, e.g.E + m);
+      p.blocks[l - 1] = mk(D, E, true);
+      D = p.blocks[l - 1].S_max;
+    }
+  } else {
+    int64_t Dm = p.T_max + B;
+    int64_t Em = std::min<int64_t>(topdeg(e.g, std::min<int64_t>(N, p.T_max)) + m, e.g.E + m);
+    p.blocks.push_back(mk(Dm, Em, true));
+    p.blocks.push_back(mk(B, m, true));
+  }
+  p.max_scan_n = std::max<int64_t>(p.words_NB, p.RB_max);
+  for (auto& b : p.blocks) p.max_scan_n = std::max<int64_t>(p.max_scan_n, b.D_max + 1);
+  return p;
+}
+
+// carve the workspace out of an arena (dry-run with base == nullptr to size it)
+static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
+  const int k = (int)e.layers.size();
+  const int64_t m = w.m;
+  const int B = w.B;
+  int maxw = e.g.F;
+  for (auto& L : e.layers) maxw = std::max(maxw, std::max(L.spec.in_dim, L.spec.out_dim));
+  w.words_N = p.words_N;
+  w.words_NB = p.words_NB;
+  w.rc = a.take<ReqCounters>(1);
+  w.qdeg = a.take<int32_t>(B + 1);
+  w.cbits = a.take<uint32_t>(p.words_N + 1);
+  w.cwpre = a.take<int64_t>(p.words_N + 1);
+  w.cand_ids = a.take<int32_t>(p.R_max);
+  w.cand_nq = a.take<int32_t>(p.R_max);
+  w.cand_score = a.take<double>(p.R_max);
+  w.cand_key = a.take<uint64_t>(p.R_max);
+  w.cand_tpos = a.take<int32_t>(p.R_max);
+  w.targets = a.take<int32_t>(p.T_max + 1);
+  w.sel_flag = a.take<int32_t>(p.R_max);
+  w.sel_hist = a.take<uint32_t>(256);
+  w.rq_cnt = a.take<int32_t>(p.RB_max + 1);
+  w.rq_fill = a.take<int32_t>(p.RB_max + 1);
+  w.rq_ptr = a.take<int64_t>(p.RB_max + 1);
+  w.rq_src = a.take<int32_t>(m + 1);
+  w.big_list = a.take<int32_t>(p.RB_max + 1);
+  w.sort_tmp = a.take<int32_t>(m + 1);
+  w.sbits = a.take<uint32_t>(p.words_NB + 1);
+  w.swpre = a.take<int64_t>(p.words_NB + 1);
+  int64_t Emax = 1, Dmax = 1, Smax = 1, Imax = 1;
+  for (auto& b : p.blocks) {
+    Emax = std::max(Emax, b.E_max);
+    Dmax = std::max(Dmax, b.D_max);
+    Smax = std::max(Smax, b.S_max);
+    Imax = std::max(Imax, b.items_max);
+  }
+  w.src_global = a.take<int32_t>(Emax);
+  w.seg_len = a.take<int64_t>(Dmax);
+  w.blocks = p.blocks;
+  for (size_t i = 0; i < w.blocks.size(); ++i) {
+    BlockDev& b = w.blocks[i];
+    b.cnt = a.take<BlockCounters>(1);
+    b.dst_ptr = a.take<int64_t>(b.D_max + 1);
+    b.item_ptr = a.take<int64_t>(b.D_max + 1);
+    b.edge_src = a.take<int32_t>(b.E_max);
+    b.src_ids = a.take<int32_t>(b.S_max);
+    b.self_src = a.take<int32_t>(b.D_max);
+    // full: block l-1's dst list aliases block l's src_ids (set in stage_build_full)
+    b.dst_ids = a.take<int32_t>(b.D_max);
+  }
+  w.block_of_layer.assign(k, 0);
+  for (int l = 1; l <= k; ++l)
+    w.block_of_layer[l - 1] = (e.cfg.strategy == OB_STRATEGY_FULL) ? l - 1 : (l < k ? 0 : 1);
+  w.rowp = a.take<const float*>(Smax);
+  w.gscale = a.take<float>(Smax);
+  w.partial = a.take<float>(Imax * (maxw + 2));
+  w.agg = a.take<float>(Dmax * maxw);
+  bool gat = false, mom = false;
+  for (auto& L : e.layers) {
+    gat |= L.spec.kind == OB_KIND_GAT;
+    mom |= L.spec.kind == OB_KIND_MOMENTS;
+  }
+  w.mean = mom ? a.take<float>(Dmax * maxw) : nullptr;
+  w.z = gat ? a.take<float>(Smax * maxw) : nullptr;
+  w.s_src = gat ? a.take<float>(Smax) : nullptr;
+  w.s_dst = gat ? a.take<float>(Dmax) : nullptr;
+  for (int l = 1; l < k; ++l) {
+    const BlockDev& b = w.blocks[w.block_of_layer[l - 1]];
+    w.outs[l] = a.take<float>(b.D_max * e.layers[l - 1].spec.out_dim);
+  }
+  int64_t tiles = p.max_scan_n / kScanTile + 2;
+  e.scan.tile_sums = a.take<int64_t>(tiles + 1);
+  e.scan.max_tiles = tiles;
+}
+
+struct PinnedReadback {
+  ReqCounters rc;
+  BlockCounters bc[8];
+};
+
+static void prepare_workspace(Engine& e, int B, int64_t m) {
+  Plan p = plan_request(e, B, m);
+  RequestWs& w = e.ws;
+  w.B = B;
+  w.m = m;
+  Arena dry;
+  dry.base = nullptr;
+  dry.cap = (size_t)-1 / 2;
+  carve(e, w, p, dry);
+  size_t need = dry.used + (1u << 20);
+  if (need > e.arena.cap) {
+    OB_CUDA(cudaStreamSynchronize(e.stream));
+    if (e.arena.base) OB_CUDA(cudaFree(e.arena.base));
+    e.arena.base = nullptr;
+    e.arena.cap = 0;
+    size_t cap = std::max(need, (size_t)(e.arena.cap * 3 / 2));
+    void* q = nullptr;
+    OB_CUDA(cudaMalloc(&q, cap));
+    e.arena.base = (char*)q;
+    e.arena.cap = cap;
+  }
+  e.arena.used = 0;
+  carve(e, w, p, e.arena);
+}
+
+static void check_ready(Engine& e) {
+  OB_CHECK(e.g.N > 0, OB_ESTATE, "no graph loaded");
+  OB_CHECK(!e.layers.empty(), OB_ESTATE, "no model loaded");
+  OB_CHECK(e.layers[0].spec.in_dim == e.g.F, OB_EINVAL, "input width does not match layer in_dim");
+  if (e.cfg.strategy != OB_STRATEGY_FULL) {
+    OB_CHECK((int)e.layers.size() >= 2, OB_EINVAL, "reuse graphs need k >= 2");
+    OB_CHECK((int)e.pe.size() >= (int)e.layers.size() - 1 && !e.pe.empty(), OB_EINVAL,
+             "reuse strategy needs stored embeddings");
+    for (int l = 1; l < (int)e.layers.size(); ++l)
+      OB_CHECK(e.pe_dim[l - 1] == e.layers[l].spec.in_dim, OB_EINVAL, "stored embedding width mismatch");
+  }
+}
+
+static void raise_request_errors(const ReqCounters& rc) {
+  if (rc.err & kErrRange) throw Error(OB_EINVAL, "request edge endpoint out of range");
+  if (rc.err & kErrNoQuery) throw Error(OB_EINVAL, "every request edge needs a query endpoint");
+  if (rc.err & kErrNonFinite) throw Error(OB_EINVAL, "query features must be finite");
+  if (rc.err & kErrZeroTotal) throw Error(OB_EINVAL, "candidate with zero total degree");
+}
+
+// fetch-byte accounting per layer (graph_fetch_bytes, runtime.py:105-120)
+static int64_t fetch_bytes(const Engine& e, const RequestWs& w, const std::vector<BlockCounters>& per_layer) {
+  int64_t total = 0;
+  const int k = (int)e.layers.size();
+  for (int l = 1; l <= k; ++l) {
+    const BlockCounters& c = per_layer[l - 1];
+    total += 16 * c.E;
+    total += 4 * (int64_t)e.g.F * c.feat_src;
+    if (l > 1 && !e.pe_dim.empty() && e.cfg.strategy != OB_STRATEGY_FULL) total += 4 * (int64_t)e.pe_dim[l - 2] * c.pe_src;
+  }
+  (void)w;
+  return total;
+}
+
+// The request pipeline.  Inputs/outputs are device pointers.
+static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const int64_t* d_edges, float* d_out,
+                         ob_breakdown* bd) {
+  check_ready(e);
+  OB_CHECK(B >= 0 && m >= 0, OB_EINVAL, "negative request size");
+  OB_CHECK(e.g.N + B < ((int64_t)1 << 31) - 1, OB_EINVAL, "id space exceeds int32");
+  cudaStream_t s = e.stream;
+  prepare_workspace(e, B, m);
+  RequestWs& w = e.ws;
+  w.edges = d_edges;
+  w.qfeat = d_q;
+  const int k = (int)e.layers.size();
+  const bool srpe = e.cfg.strategy != OB_STRATEGY_FULL;
+  OB_CUDA(cudaEventRecord(e.ev[0], s));
+  OB_CUDA(cudaMemsetAsync(w.rc, 0, sizeof(ReqCounters), s));
+  for (auto& b : w.blocks) OB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(BlockCounters), s));
+  stage_request_prep(e, w, srpe);
+  if (srpe) stage_select(e, w);
+  stage_request_csr(e, w);
+  if (srpe) stage_build_srpe(e, w);
+  else stage_build_full(e, w);
+  OB_CUDA(cudaEventRecord(e.ev[1], s));
+  // per-layer fetch counters live in per-layer copies of the block counters
+  stage_forward(e, w, d_out);
+  OB_CUDA(cudaEventRecord(e.ev[2], s));
+  e.have_request = true;
+  if (!bd) return;
+  PinnedReadback hb{};
+  OB_CUDA(cudaMemcpyAsync(&hb.rc, w.rc, sizeof(ReqCounters), cudaMemcpyDeviceToHost, s));
+  for (size_t i = 0; i < w.blocks.size(); ++i)
+    OB_CUDA(cudaMemcpyAsync(&hb.bc[i], w.blocks[i].cnt, sizeof(BlockCounters), cudaMemcpyDeviceToHost, s));
+  OB_CUDA(cudaStreamSynchronize(s));
+  OB_CUDA(cudaGetLastError());
+  for (size_t i = 0; i < w.blocks.size(); ++i) w.blocks[i].host = hb.bc[i];
+  raise_request_errors(hb.rc);
+  float t01 = 0, t12 = 0;
+  OB_CUDA(cudaEventElapsedTime(&t01, e.ev[0], e.ev[1]));
+  OB_CUDA(cudaEventElapsedTime(&t12, e.ev[1], e.ev[2]));
+  std::vector<BlockCounters> per_layer(k);
+  for (int l = 1; l <= k; ++l) per_layer[l - 1] = w.blocks[w.block_of_layer[l - 1]].host;
+  if (srpe) {
+    // the shared mid block accumulated layer 1's FEATURE rows and layers 2..k-1's PE rows
+    const BlockCounters& mid = w.blocks[0].host;
+    for (int l = 1; l < k; ++l) {
+      per_layer[l - 1].feat_src = (l == 1) ? mid.feat_src : 0;
+      per_layer[l - 1].pe_src = (l == 1) ? 0 : mid.pe_src / std::max(1, k - 2);
+    }
+  }
+  std::memset(bd, 0, sizeof(*bd));
+  bd->fetch_ms = t01;
+  bd->compute_ms = t12;
+  bd->fetch_bytes = fetch_bytes(e, w, per_layer);
+  bd->transfer_ms = (double)bd->fetch_bytes / 12e9 * 1e3;
+  bd->num_candidates = hb.rc.R;
+  bd->num_targets = hb.rc.T;
+  bd->total_device_ms = t01 + t12;
+}
+
+// ---------------------------------------------------------------------------
+// loads
+// ---------------------------------------------------------------------------
+static void load_graph(Engine& e, int64_t N, const int64_t* off, const int64_t* nb, int64_t E, const float* feats,
+                       int F) {
+  OB_CHECK(N > 0 && N < ((int64_t)1 << 31) - 4096, OB_EINVAL, "num_nodes out of range");
+  OB_CHECK(off && (E == 0 || nb) && (F == 0 || feats), OB_EINVAL, "null graph array");
+  OB_CHECK(off[0] == 0 && off[N] == E, OB_EINVAL, "offsets inconsistent with num_edges");
+  std::vector<int32_t> nbrs32((size_t)E);
+  std::vector<int32_t> deg((size_t)N);
+  for (int64_t v = 0; v < N; ++v) {
+    int64_t a = off[v], b = off[v + 1];
+    OB_CHECK(b >= a, OB_EINVAL, "offsets must be non-decreasing");
+    deg[v] = (int32_t)(b - a);
+    bool sorted = true;
+    for (int64_t i = a; i < b; ++i) {
+      int64_t u = nb[i];
+      OB_CHECK(u >= 0 && u < N, OB_EINVAL, "edge endpoint out of range");
+      nbrs32[i] = (int32_t)u;
+      if (i > a && nbrs32[i] < nbrs32[i - 1]) sorted = false;
+    }
+    // edges are consumed in (dst, src) order (compgraph.py:197-201): sort rows once at load
+    if (!sorted) std::sort(nbrs32.begin() + a, nbrs32.begin() + b);
+  }
+  GraphDev& g = e.g;
+  g.N = N;
+  g.E = E;
+  g.F = F;
+  g.offsets = (int64_t*)e.dalloc(sizeof(int64_t) * (N + 1));
+  g.nbrs = (int32_t*)e.dalloc(sizeof(int32_t) * std::max<int64_t>(E, 1));
+  g.indeg = (int32_t*)e.dalloc(sizeof(int32_t) * N);
+  g.feats = (float*)e.dalloc(sizeof(float) * std::max<int64_t>(N * F, 1));
+  OB_CUDA(cudaMemcpy(g.offsets, off, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice));
+  if (E) OB_CUDA(cudaMemcpy(g.nbrs, nbrs32.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice));
+  OB_CUDA(cudaMemcpy(g.indeg, deg.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+  if (N * F) OB_CUDA(cudaMemcpy(g.feats, feats, sizeof(float) * N * F, cudaMemcpyHostToDevice));
+  std::sort(deg.begin(), deg.end(), std::greater<int32_t>());
+  g.topdeg_prefix.assign((size_t)N + 1, 0);
+  for (int64_t i = 0; i < N; ++i) g.topdeg_prefix[i + 1] = g.topdeg_prefix[i] + deg[i];
+}
+
+static int nmats(int kind) {
+  switch (kind) {
+    case OB_KIND_GCN: return 1;
+    case OB_KIND_GAT: return 3;
+    default: return 2;
+  }
+}
+
+static void load_model(Engine& e, int k, const ob_layer* layers, const float* const* mats) {
+  OB_CHECK(k >= 1 && k <= 7, OB_EINVAL, "model needs 1..7 layers");
+  std::vector<LayerDev> out(k);
+  int mi = 0;
+  for (int l = 0; l < k; ++l) {
+    const ob_layer& sp = layers[l];
+    OB_CHECK(sp.kind >= 0 && sp.kind <= 5, OB_EINVAL, "unknown layer kind");
+    OB_CHECK(sp.in_dim > 0 && sp.out_dim > 0, OB_EINVAL, "layer dims must be positive");
+    if (l) OB_CHECK(layers[l - 1].out_dim == sp.in_dim, OB_EINVAL, "adjacent layer dimensions do not chain");
+    if (sp.kind == OB_KIND_POWER_MEAN) OB_CHECK(sp.p != 0.f, OB_EINVAL, "power_mean needs p != 0");
+    if (sp.kind == OB_KIND_MOMENTS) OB_CHECK(sp.n >= 2, OB_EINVAL, "moments needs n >= 2");
+    LayerDev& L = out[l];
+    L.spec = sp;
+    const size_t mat = (size_t)sp.in_dim * sp.out_dim;
+    if (sp.kind == OB_KIND_GCN) {
+      L.w = (float*)e.dalloc(sizeof(float) * mat);
+      OB_CUDA(cudaMemcpy(L.w, mats[mi], sizeof(float) * mat, cudaMemcpyHostToDevice));
+    } else if (sp.kind == OB_KIND_GAT) {
+      L.w = (float*)e.dalloc(sizeof(float) * mat);
+      L.a_src = (float*)e.dalloc(sizeof(float) * sp.out_dim);
+      L.a_dst = (float*)e.dalloc(sizeof(float) * sp.out_dim);
+      OB_CUDA(cudaMemcpy(L.w, mats[mi], sizeof(float) * mat, cudaMemcpyHostToDevice));
+      OB_CUDA(cudaMemcpy(L.a_src, mats[mi + 1], sizeof(float) * sp.out_dim, cudaMemcpyHostToDevice));
+      OB_CUDA(cudaMemcpy(L.a_dst, mats[mi + 2], sizeof(float) * sp.out_dim, cudaMemcpyHostToDevice));
+    } else {
+      // [W_self; W_neigh] stacked so the update is one GEMM over [h_v | agg]
+      L.wcat = (float*)e.dalloc(sizeof(float) * 2 * mat);
+      OB_CUDA(cudaMemcpy(L.wcat, mats[mi], sizeof(float) * mat, cudaMemcpyHostToDevice));
+      OB_CUDA(cudaMemcpy(L.wcat + mat, mats[mi + 1], sizeof(float) * mat, cudaMemcpyHostToDevice));
+    }
+    mi += nmats(sp.kind);
+  }
+  e.layers = out;
+}
+
+// ---------------------------------------------------------------------------
+// parity export helpers
+// ---------------------------------------------------------------------------
+__global__ void k_src_degree(const int32_t* __restrict__ src_ids, const BlockCounters* cnt, int64_t N,
+                             const int32_t* indeg, const int32_t* qdeg, int64_t* out) {
+  const int64_t S = cnt->S;
+  OB_GRID_STRIDE(s, S) {
+    int64_t g = src_ids[s];
+    out[s] = g < N ? indeg[g] : qdeg[g - N];
+  }
+}
+
+template <class T>
+static std::vector<T> d2h(const T* d, int64_t n, cudaStream_t s) {
+  std::vector<T> h((size_t)std::max<int64_t>(n, 0));
+  if (n > 0) OB_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(T) * n, cudaMemcpyDeviceToHost, s));
+  OB_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+}  // namespace ob
+
+// =============================================================================
+// C ABI
+// =============================================================================
+using namespace ob;
+
+struct ob_engine {
+  Engine impl;
+  std::mutex mu;  // one in-flight request per engine
+  // persistent request I/O buffers for the host-pointer path
+  int64_t* d_edges = nullptr;
+  float* d_q = nullptr;
+  float* d_out = nullptr;
+  size_t cap_edges = 0, cap_q = 0, cap_out = 0;
+};
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return OB_OK;
+  } catch (const Error& err) {
+    t_err = err.what();
+    return err.code;
+  } catch (const std::exception& ex) {
+    t_err = ex.what();
+    return OB_ECUDA;
+  } catch (...) {
+    t_err = "unknown error";
+    return OB_ECUDA;
+  }
+}
+
+template <class T>
+static void ensure(T*& p, size_t& cap, size_t n) {
+  if (n <= cap && p) return;
+  if (p) OB_CUDA(cudaFree(p));
+  p = nullptr;
+  size_t c = std::max<size_t>(n, 64);
+  OB_CUDA(cudaMalloc(&p, sizeof(T) * c));
+  cap = c;
+}
+
+extern "C" {
+
+const char* ob_last_error(void) { return t_err.c_str(); }
+int ob_version(void) { return OB_API_VERSION; }
+
+int ob_engine_create(const ob_config* cfg, ob_engine** out) {
+  return guarded([&] {
+    OB_CHECK(cfg && out, OB_EINVAL, "null argument");
+    OB_CHECK(cfg->gamma >= 0.0 && cfg->gamma <= 1.0, OB_EINVAL, "gamma must lie in [0, 1]");
+    OB_CHECK(cfg->strategy == OB_STRATEGY_FULL || cfg->strategy == OB_STRATEGY_SRPE ||
+                 cfg->strategy == OB_STRATEGY_SRPE_CGP,
+             OB_EINVAL, "unknown strategy");
+    OB_CHECK(cfg->policy == OB_POLICY_RATIO, OB_EINVAL, "only the ratio policy runs on the device");
+    OB_CHECK(cfg->num_partitions >= 1, OB_EINVAL, "num_partitions must be >= 1");
+    OB_CHECK(cfg->strategy == OB_STRATEGY_SRPE_CGP || cfg->num_partitions == 1, OB_EINVAL,
+             "num_partitions > 1 needs strategy srpe-cgp");
+    OB_CHECK(cfg->strategy != OB_STRATEGY_SRPE_CGP, OB_EINVAL, "srpe-cgp is not built into this library yet");
+    int ndev = 0;
+    OB_CUDA(cudaGetDeviceCount(&ndev));
+    OB_CHECK(cfg->device >= 0 && cfg->device < ndev, OB_EINVAL, "no such CUDA device");
+    OB_CUDA(cudaSetDevice(cfg->device));
+    auto* h = new ob_engine();
+    Engine& e = h->impl;
+    e.cfg = *cfg;
+    if (cfg->stream) {
+      e.stream = (cudaStream_t)(uintptr_t)cfg->stream;
+    } else {
+      OB_CUDA(cudaStreamCreateWithFlags(&e.stream, cudaStreamNonBlocking));
+      e.own_stream = true;
+    }
+    for (auto& ev_ : e.ev) OB_CUDA(cudaEventCreate(&ev_));
+    *out = h;
+  });
+}
+
+int ob_engine_destroy(ob_engine* h) {
+  return guarded([&] {
+    if (!h) return;
+    cudaSetDevice(h->impl.cfg.device);
+    if (h->d_edges) cudaFree(h->d_edges);
+    if (h->d_q) cudaFree(h->d_q);
+    if (h->d_out) cudaFree(h->d_out);
+    delete h;
+  });
+}
+
+int ob_load_graph(ob_engine* h, int64_t N, const int64_t* off, const int64_t* nb, int64_t E, const float* feats,
+                  int32_t F) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    load_graph(h->impl, N, off, nb, E, feats, F);
+  });
+}
+
+int ob_load_pe(ob_engine* h, int32_t layer, const float* rows, int64_t n, int32_t dim) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(e.g.N > 0, OB_ESTATE, "load the graph before stored embeddings");
+    OB_CHECK(layer >= 1 && layer <= 7, OB_EINVAL, "bad stored-embedding layer");
+    OB_CHECK(n == e.g.N, OB_EINVAL, "stored embeddings must cover every node");
+    OB_CHECK(dim > 0 && rows, OB_EINVAL, "bad stored-embedding rows");
+    if ((int)e.pe.size() < layer) {
+      e.pe.resize(layer, nullptr);
+      e.pe_dim.resize(layer, 0);
+    }
+    float* d = (float*)e.dalloc(sizeof(float) * n * dim);
+    OB_CUDA(cudaMemcpy(d, rows, sizeof(float) * n * dim, cudaMemcpyHostToDevice));
+    e.pe[layer - 1] = d;
+    e.pe_dim[layer - 1] = dim;
+  });
+}
+
+int ob_load_model(ob_engine* h, int32_t k, const ob_layer* layers, const float* const* mats) {
+  return guarded([&] {
+    OB_CHECK(h && layers && mats, OB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    load_model(h->impl, k, layers, mats);
+  });
+}
+
+int ob_precompute_pe(ob_engine* h) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    OB_CHECK(!h->impl.layers.empty(), OB_ESTATE, "load a model first");
+    OB_CHECK(h->impl.layers[0].spec.in_dim == h->impl.g.F, OB_EINVAL, "input width does not match layer in_dim");
+    stage_precompute(h->impl);
+    OB_CUDA(cudaGetLastError());
+  });
+}
+
+int ob_read_pe(ob_engine* h, int32_t layer, float* out) {
+  return guarded([&] {
+    OB_CHECK(h && out, OB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(layer >= 1 && layer <= (int)e.pe.size() && e.pe[layer - 1], OB_EINVAL,
+             "no stored embeddings for that layer");
+    OB_CUDA(cudaMemcpy(out, e.pe[layer - 1], sizeof(float) * e.g.N * e.pe_dim[layer - 1], cudaMemcpyDeviceToHost));
+  });
+}
+
+int ob_serve(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* edges, float* out,
+             ob_breakdown* bd) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    check_ready(e);
+    OB_CHECK(B >= 0 && m >= 0, OB_EINVAL, "negative request size");
+    OB_CHECK(m == 0 || edges, OB_EINVAL, "null edges");
+    OB_CHECK(out, OB_EINVAL, "null output");
+    const int H = e.layers.back().spec.out_dim;
+    ensure(h->d_edges, h->cap_edges, (size_t)(2 * m));
+    ensure(h->d_q, h->cap_q, (size_t)B * e.g.F);
+    ensure(h->d_out, h->cap_out, (size_t)B * H);
+    cudaStream_t s = e.stream;
+    if (m) OB_CUDA(cudaMemcpyAsync(h->d_edges, edges, sizeof(int64_t) * 2 * m, cudaMemcpyHostToDevice, s));
+    if ((int64_t)B * e.g.F) OB_CUDA(cudaMemcpyAsync(h->d_q, q, sizeof(float) * B * e.g.F, cudaMemcpyHostToDevice, s));
+    ob_breakdown local{};
+    serve_device(e, B, h->d_q, m, h->d_edges, h->d_out, &local);
+    if ((int64_t)B * H) OB_CUDA(cudaMemcpyAsync(out, h->d_out, sizeof(float) * B * H, cudaMemcpyDeviceToHost, s));
+    OB_CUDA(cudaStreamSynchronize(s));
+    local.h2d_bytes = 16 * m + 4 * (int64_t)B * e.g.F;
+    local.d2h_bytes = 4 * (int64_t)B * H;
+    if (bd) *bd = local;
+  });
+}
+
+int ob_serve_device(ob_engine* h, int32_t B, const float* d_q, int64_t m, const int64_t* d_edges, float* d_out,
+                    ob_breakdown* bd) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    serve_device(h->impl, B, d_q, m, d_edges, d_out, bd);
+  });
+}
+
+int ob_last_plan(ob_engine* h, int64_t* nc, int64_t* nt, int64_t* ids, int64_t* nq, int64_t* total, double* scores,
+                 int64_t* targets) {
+  return guarded([&] {
+    OB_CHECK(h && nc && nt, OB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(e.have_request && e.cfg.strategy != OB_STRATEGY_FULL, OB_ESTATE, "no srpe request served");
+    RequestWs& w = e.ws;
+    cudaStream_t s = e.stream;
+    ReqCounters rc = d2h(w.rc, 1, s)[0];
+    *nc = rc.R;
+    *nt = rc.T;
+    if (ids) {
+      auto a = d2h(w.cand_ids, rc.R, s);
+      auto b = d2h(w.cand_nq, rc.R, s);
+      std::vector<int32_t> deg((size_t)rc.R);
+      // total = training in-degree + nq (policy.py:64-67)
+      std::vector<int32_t> indeg = d2h(e.g.indeg, e.g.N, s);
+      for (int64_t i = 0; i < rc.R; ++i) {
+        ids[i] = a[i];
+        if (nq) nq[i] = b[i];
+        if (total) total[i] = (int64_t)indeg[a[i]] + b[i];
+      }
+      if (scores) {
+        auto c = d2h(w.cand_score, rc.R, s);
+        std::copy(c.begin(), c.end(), scores);
+      }
+    }
+    if (targets) {
+      auto t = d2h(w.targets, rc.T, s);
+      for (int64_t i = 0; i < rc.T; ++i) targets[i] = t[i];
+    }
+  });
+}
+
+int ob_last_block_sizes(ob_engine* h, int32_t part, int32_t layer, int64_t* ns, int64_t* nd, int64_t* ne) {
+  return guarded([&] {
+    OB_CHECK(h && ns && nd && ne, OB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(e.have_request, OB_ESTATE, "no request served");
+    OB_CHECK(part == 0, OB_EINVAL, "partition index out of range");
+    OB_CHECK(layer >= 1 && layer <= (int)e.layers.size(), OB_EINVAL, "layer out of range");
+    BlockDev& b = e.ws.blocks[e.ws.block_of_layer[layer - 1]];
+    BlockCounters c = d2h(b.cnt, 1, e.stream)[0];
+    *ns = c.S;
+    *nd = c.D;
+    *ne = c.E;
+  });
+}
+
+int ob_last_block(ob_engine* h, int32_t part, int32_t layer, int64_t* src_ids, int64_t* dst_ids, int64_t* edge_src,
+                  int64_t* edge_dst, uint8_t* bind_kind, int32_t* bind_pe_layer, int64_t* src_degree,
+                  int64_t* dst_self_src) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(e.have_request, OB_ESTATE, "no request served");
+    OB_CHECK(part == 0, OB_EINVAL, "partition index out of range");
+    OB_CHECK(layer >= 1 && layer <= (int)e.layers.size(), OB_EINVAL, "layer out of range");
+    RequestWs& w = e.ws;
+    BlockDev& b = w.blocks[w.block_of_layer[layer - 1]];
+    cudaStream_t s = e.stream;
+    BlockCounters c = d2h(b.cnt, 1, s)[0];
+    auto cp32 = [&](const int32_t* d, int64_t n, int64_t* o) {
+      if (!o) return;
+      auto v = d2h(d, n, s);
+      for (int64_t i = 0; i < n; ++i) o[i] = v[i];
+    };
+    cp32(b.src_ids, c.S, src_ids);
+    cp32(b.dst_ids, c.D, dst_ids);
+    cp32(b.edge_src, c.E, edge_src);
+    if (b.has_self) cp32(b.self_src, c.D, dst_self_src);
+    if (edge_dst) {
+      auto ptr = d2h(b.dst_ptr, c.D + 1, s);
+      for (int64_t i = 0; i < c.D; ++i)
+        for (int64_t j = ptr[i]; j < ptr[i + 1]; ++j) edge_dst[j] = i;
+    }
+    if (bind_kind || bind_pe_layer || src_degree) {
+      uint8_t* dk = nullptr;
+      int32_t* dp = nullptr;
+      int64_t* dd = nullptr;
+      OB_CUDA(cudaMalloc(&dk, std::max<int64_t>(c.S, 1)));
+      OB_CUDA(cudaMalloc(&dp, sizeof(int32_t) * std::max<int64_t>(c.S, 1)));
+      OB_CUDA(cudaMalloc(&dd, sizeof(int64_t) * std::max<int64_t>(c.S, 1)));
+      export_bindings(e, w, layer, dk, dp);
+      k_src_degree<<<grid_for(std::max<int64_t>(c.S, 1), 256), 256, 0, s>>>(b.src_ids, b.cnt, e.g.N, e.g.indeg,
+                                                                             w.qdeg, dd);
+      OB_LAUNCHED();
+      auto k1 = d2h(dk, c.S, s);
+      auto k2 = d2h(dp, c.S, s);
+      auto k3 = d2h(dd, c.S, s);
+      if (bind_kind) std::copy(k1.begin(), k1.end(), bind_kind);
+      if (bind_pe_layer) std::copy(k2.begin(), k2.end(), bind_pe_layer);
+      if (src_degree) std::copy(k3.begin(), k3.end(), src_degree);
+      cudaFree(dk);
+      cudaFree(dp);
+      cudaFree(dd);
+    }
+  });
+}
+
+int ob_partition_owner(ob_engine* h, int64_t* owner) {
+  return guarded([&] {
+    OB_CHECK(h && owner, OB_EINVAL, "null argument");
+    OB_CHECK(false, OB_ESTATE, "engine is not partitioned");
+  });
+}
+
+int64_t ob_launch_count(ob_engine* h) {
+  (void)h;
+  return g_launches;
+}
+
+int ob_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    OB_CHECK(out128, OB_EINVAL, "null argument");
+#ifdef OB_WITH_NCCL
+    ncclUniqueId id;
+    OB_CHECK(ncclGetUniqueId(&id) == ncclSuccess, OB_ECOMM, "ncclGetUniqueId failed");
+    std::memcpy(out128, &id, sizeof(id));
+#else
+    OB_CHECK(false, OB_ECOMM, "built without NCCL");
+#endif
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,213 @@
+// ob_build.cu -- computation-graph construction on the device.
+//
+// Reference (paths relative to /root/reference/pkg/src/gnnserve):
+//   _serving_in_sources   compgraph.py:216-221  CSR(v) ++ request sources into v
+//   _make_block           compgraph.py:180-213  dedup, relabel, (dst, src) edge order
+//   build_srpe            compgraph.py:308-345  last block = queries; mid = targets U queries
+//   build_full_k_hop      compgraph.py:224-245  k-hop frontier expansion
+//   DegreeView            compgraph.py:124-152  source normaliser degrees
+//
+// One generic builder serves every strategy.  A destination's source list is
+// described by two spans -- a CSR span (training in-neighbours, ascending) and
+// a request span (request sources into it, ascending after the per-slot sort)
+// -- and the concatenation is ascending because request sources of a training
+// destination are queries, which are numbered above every training id.  The
+// builder then: scans the span lengths into dst_ptr, gathers the global
+// source ids edge-parallel (hub destinations are split across warps), marks
+// them (and the destinations' own rows) in a bitmap over [0, N+B), and uses
+// the bitmap's popcount prefix both as the ascending unique source list and
+// as the global -> local relabel.  Edges come out already ordered by
+// (dst, src), so no sort is needed.
+#include "ob_engine.h"
+
+namespace ob {
+
+struct SegSpans {
+  int64_t* cs;  // csr start
+  int32_t* cl;  // csr length
+  int64_t* rs;  // request-span start
+  int32_t* rl;  // request-span length
+};
+
+// spans for a destination list (global ids ascending)
+__global__ void k_block_spans(const int32_t* __restrict__ dst_ids, const BlockCounters* cnt, int64_t N,
+                              const int64_t* __restrict__ offsets, const int32_t* __restrict__ indeg,
+                              const uint32_t* cbits, const int64_t* cwpre, const int64_t* rq_ptr,
+                              const ReqCounters* rc, SegSpans sp, int64_t* seg_len) {
+  const int64_t D = cnt->D;
+  const int64_t R = rc->R;
+  const bool bad = rc->err & (kErrRange | kErrNoQuery);
+  OB_GRID_STRIDE(i, D) {
+    int64_t v = dst_ids[i];
+    int64_t cs = 0, rs = 0;
+    int32_t cl = 0, rl = 0;
+    if (v < N) {
+      cs = offsets[v];
+      cl = indeg[v];
+      if (!bad && bm_test(cbits, v)) {
+        int64_t c = bm_rank(cbits, cwpre, v);
+        rs = rq_ptr[c];
+        rl = (int32_t)(rq_ptr[c + 1] - rs);
+      }
+    } else if (!bad) {
+      int64_t slot = R + (v - N);
+      rs = rq_ptr[slot];
+      rl = (int32_t)(rq_ptr[slot + 1] - rs);
+    }
+    sp.cs[i] = cs;
+    sp.cl[i] = cl;
+    sp.rs[i] = rs;
+    sp.rl[i] = rl;
+    seg_len[i] = (int64_t)cl + rl;
+  }
+}
+
+// same, for a partition's source-split CSR (build_partitioned, compgraph.py:431-447)
+// -- defined in the CGP unit; the centralized path only needs the above.
+
+// largest i with ptr[i] <= e  (ptr ascending, ptr[0] = 0)
+__device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ ptr, int64_t n, int64_t e) {
+  int64_t lo = 0, hi = n;  // answer in [0, n)
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(ptr + mid) <= e) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// gather global source ids edge-parallel; warp-strided so loads coalesce and
+// hub destinations spread over many warps
+constexpr int kFillPerLane = 8;
+__global__ void k_block_fill(const BlockCounters* cnt, const int64_t* __restrict__ dst_ptr, SegSpans sp,
+                             const int32_t* __restrict__ nbrs, const int32_t* __restrict__ rq_src,
+                             int32_t* src_global, uint32_t* sbits) {
+  const int64_t D = cnt->D, E = cnt->E;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t span = 32 * kFillPerLane;
+  for (int64_t base = warp * span; base < E; base += nwarps * span) {
+    int64_t e = base + lane;
+    if (e >= E) continue;
+    int64_t i = seg_of(dst_ptr, D, e);
+    for (int k = 0; k < kFillPerLane && e < E; ++k, e += 32) {
+      while (__ldg(dst_ptr + i + 1) <= e) ++i;
+      int64_t j = e - __ldg(dst_ptr + i);
+      int32_t cl = __ldg(sp.cl + i);
+      int32_t src = j < cl ? __ldg(nbrs + __ldg(sp.cs + i) + j) : __ldg(rq_src + __ldg(sp.rs + i) + (j - cl));
+      src_global[e] = src;
+      bm_set(sbits, src);
+    }
+  }
+}
+
+__global__ void k_mark_ids(const int32_t* __restrict__ ids, const BlockCounters* cnt, uint32_t* sbits) {
+  const int64_t D = cnt->D;
+  OB_GRID_STRIDE(i, D) bm_set(sbits, ids[i]);
+}
+
+__global__ void k_set_S(BlockCounters* cnt, const int64_t* total) { cnt->S = *total; }
+
+__global__ void k_relabel(const BlockCounters* cnt, const int32_t* __restrict__ src_global, const uint32_t* sbits,
+                          const int64_t* swpre, int32_t* edge_src) {
+  const int64_t E = cnt->E;
+  OB_GRID_STRIDE(e, E) edge_src[e] = (int32_t)bm_rank(sbits, swpre, src_global[e]);
+}
+
+__global__ void k_self_rows(const BlockCounters* cnt, const int32_t* __restrict__ dst_ids, const uint32_t* sbits,
+                            const int64_t* swpre, int32_t* self_src) {
+  const int64_t D = cnt->D;
+  OB_GRID_STRIDE(i, D) self_src[i] = (int32_t)bm_rank(sbits, swpre, dst_ids[i]);
+}
+
+// srpe destination lists ------------------------------------------------------
+__global__ void k_mid_dst(const ReqCounters* rc, int64_t N, int B, const int32_t* targets, int32_t* dst_ids,
+                          BlockCounters* cnt) {
+  const int64_t T = rc->T, D = T + B;
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt->D = D;
+  OB_GRID_STRIDE(i, D) dst_ids[i] = i < T ? targets[i] : (int32_t)(N + (i - T));
+}
+
+__global__ void k_query_dst(int64_t N, int B, int32_t* dst_ids, BlockCounters* cnt) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt->D = B;
+  OB_GRID_STRIDE(i, (int64_t)B) dst_ids[i] = (int32_t)(N + i);
+}
+
+__global__ void k_copy_count_D(BlockCounters* dst, const BlockCounters* src) { dst->D = src->S; }
+
+void block_items(Engine& e, BlockDev& b, int64_t chunk) {
+  device_scan(e.stream, e.scan, ItemLoad{b.dst_ptr, chunk}, StoreI64{b.item_ptr}, &b.cnt->D, 0, b.D_max,
+              &b.cnt->items, b.item_ptr);
+}
+
+// generic block assembly over an already written dst list + counts->D
+static void assemble(Engine& e, RequestWs& w, BlockDev& b, const int64_t* offsets, const int32_t* nbrs,
+                     const int32_t* indeg) {
+  cudaStream_t s = e.stream;
+  SegSpans sp;
+  Arena& a = e.arena;
+  size_t mark = a.used;
+  sp.cs = a.take<int64_t>(b.D_max);
+  sp.cl = a.take<int32_t>(b.D_max);
+  sp.rs = a.take<int64_t>(b.D_max);
+  sp.rl = a.take<int32_t>(b.D_max);
+  k_block_spans<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, e.g.N, offsets, indeg, w.cbits, w.cwpre,
+                                                        w.rq_ptr, w.rc, sp, w.seg_len);
+  OB_LAUNCHED();
+  device_scan(s, e.scan, LoadI64{w.seg_len}, StoreI64{b.dst_ptr}, &b.cnt->D, 0, b.D_max, &b.cnt->E, b.dst_ptr);
+  OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
+  k_block_fill<<<grid_for(b.E_max, 32 * kFillPerLane * 8), 256, 0, s>>>(b.cnt, b.dst_ptr, sp, nbrs, w.rq_src,
+                                                                         w.src_global, w.sbits);
+  OB_LAUNCHED();
+  if (b.has_self) {
+    k_mark_ids<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, w.sbits);
+    OB_LAUNCHED();
+  }
+  device_scan(s, e.scan, LoadPopc{w.sbits}, StoreI64{w.swpre}, nullptr, w.words_NB, w.words_NB, &b.cnt->S, w.swpre);
+  k_bitmap_compact_ext(e, w.sbits, w.swpre, w.words_NB, b.src_ids);
+  k_relabel<<<grid_for(b.E_max, 256), 256, 0, s>>>(b.cnt, w.src_global, w.sbits, w.swpre, b.edge_src);
+  OB_LAUNCHED();
+  if (b.has_self) {
+    k_self_rows<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.cnt, b.dst_ids, w.sbits, w.swpre, b.self_src);
+    OB_LAUNCHED();
+  }
+  block_items(e, b, kAggChunk);
+  a.used = mark;  // spans are transient
+}
+
+void stage_build_srpe(Engine& e, RequestWs& w) {
+  cudaStream_t s = e.stream;
+  const int k = (int)e.layers.size();
+  // blocks[0] = shared mid block (layers 1..k-1), blocks[1] = last block (layer k)
+  BlockDev& mid = w.blocks[0];
+  BlockDev& last = w.blocks[1];
+  k_mid_dst<<<grid_for(mid.D_max, 256), 256, 0, s>>>(w.rc, e.g.N, w.B, w.targets, mid.dst_ids, mid.cnt);
+  OB_LAUNCHED();
+  assemble(e, w, mid, e.g.offsets, e.g.nbrs, e.g.indeg);
+  k_query_dst<<<grid_for(w.B, 256), 256, 0, s>>>(e.g.N, w.B, last.dst_ids, last.cnt);
+  OB_LAUNCHED();
+  assemble(e, w, last, e.g.offsets, e.g.nbrs, e.g.indeg);
+  (void)k;
+}
+
+void stage_build_full(Engine& e, RequestWs& w) {
+  cudaStream_t s = e.stream;
+  const int k = (int)e.layers.size();
+  // blocks[l-1] feeds layer l; block k's dst = queries; block l-1's dst = block l's sources
+  BlockDev& top = w.blocks[k - 1];
+  k_query_dst<<<grid_for(w.B, 256), 256, 0, s>>>(e.g.N, w.B, top.dst_ids, top.cnt);
+  OB_LAUNCHED();
+  for (int l = k; l >= 1; --l) {
+    BlockDev& b = w.blocks[l - 1];
+    if (l < k) {
+      BlockDev& up = w.blocks[l];
+      b.dst_ids = up.src_ids;
+      k_copy_count_D<<<1, 1, 0, s>>>(b.cnt, up.cnt);
+      OB_LAUNCHED();
+    }
+    assemble(e, w, b, e.g.offsets, e.g.nbrs, e.g.indeg);
+  }
+}
+
+}  // namespace ob

@@ -1,0 +1,200 @@
+// ob_engine.h -- engine state and stage entry points for libomega_b200.
+//
+// Data layout in HBM:
+//   graph:  in_offsets int64[N+1], in_neighbors int32[E] (ascending per dst),
+//           in_degree int32[N], features f32[N][F] (row-major)
+//   PE:     f32[N][H_l] per stored layer (or owned rows + pos map under CGP)
+//   model:  f32 weights; sage/power/moments keep [W_self; W_neigh] stacked
+//   request workspace: one bump arena sized from per-request bounds, every
+//           request-dependent count lives in a device-side counter block.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "ob_common.cuh"
+
+namespace ob {
+
+enum ErrBits : int64_t {
+  kErrRange = 1,        // request edge endpoint out of range
+  kErrNoQuery = 2,      // request edge without a query endpoint
+  kErrZeroTotal = 4,    // candidate with zero total degree (policy.py:79-80)
+  kErrNonFinite = 8,    // query feature not finite
+};
+
+// Device-side counters of one request (one allocation, read back once).
+struct ReqCounters {
+  int64_t err;
+  int64_t R;           // |candidates|
+  int64_t budget;      // floor(gamma * R)
+  int64_t T;           // |targets|
+  int64_t RB;          // R + B request-CSR slots
+  int64_t n_big;       // segments needing the CTA sort
+  uint64_t sel_prefix; // radix-select state
+  uint64_t sel_mask;
+  int64_t sel_krem;
+  int64_t sel_gt;      // keys strictly above the threshold
+  int64_t sel_eq_take; // threshold-equal keys to take (lowest ids first)
+  int64_t fetch_feat_rows;
+  int64_t pad[4];
+};
+
+struct BlockCounters {
+  int64_t D, E, S, items;
+  int64_t feat_src;    // FEATURE-bound training sources (fetch bytes)
+  int64_t pe_src;      // PE-bound sources (fetch bytes)
+  int64_t pad[2];
+};
+
+// A computation block in device memory (CSR over destinations).
+struct BlockDev {
+  int64_t D_max = 0, E_max = 0, S_max = 0, items_max = 0;
+  BlockCounters* cnt = nullptr;  // device
+  int32_t* dst_ids = nullptr;    // [D] global ids (ascending)
+  int64_t* dst_ptr = nullptr;    // [D+1]
+  int32_t* edge_src = nullptr;   // [E] local source index, ascending within a dst
+  int32_t* src_ids = nullptr;    // [S] ascending global ids
+  int32_t* self_src = nullptr;   // [D] local index of dst's own row (centralized only)
+  int64_t* item_ptr = nullptr;   // [D+1] aggregation work items per dst (edge chunks)
+  bool has_self = true;
+  // host mirror of counts after the request completes
+  BlockCounters host{};
+};
+
+struct LayerDev {
+  ob_layer spec{};
+  float* w = nullptr;       // gcn/gat: W [in x out]
+  float* wcat = nullptr;    // sage/power/moments: [W_self; W_neigh] [(2 in) x out]
+  float* a_src = nullptr;   // gat
+  float* a_dst = nullptr;   // gat
+};
+
+struct GraphDev {
+  int64_t N = 0, E = 0;
+  int F = 0;
+  int64_t* offsets = nullptr;
+  int32_t* nbrs = nullptr;
+  int32_t* indeg = nullptr;
+  float* feats = nullptr;
+  std::vector<int64_t> topdeg_prefix;  // host: prefix sums of in-degrees sorted descending
+};
+
+// Bump allocator over one device allocation (reset per request).
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0;
+  template <class T>
+  T* take(int64_t count) {
+    size_t bytes = ((size_t)(count > 0 ? count : 1) * sizeof(T) + 255) & ~(size_t)255;
+    if (used + bytes > cap) throw Error(OB_ESTATE, "arena overflow");
+    T* p = reinterpret_cast<T*>(base + used);
+    used += bytes;
+    return p;
+  }
+};
+
+// Per-request device workspace for the centralized pipeline.
+struct RequestWs {
+  int B = 0;
+  int64_t m = 0;
+  ReqCounters* rc = nullptr;
+  const int64_t* edges = nullptr;  // device [m][2]
+  const float* qfeat = nullptr;    // device [B][F]
+  int32_t* qdeg = nullptr;         // [B] request in-degree per query
+  // candidate set (bitmap-rank over [0, N))
+  uint32_t* cbits = nullptr;
+  int64_t* cwpre = nullptr;        // [words+1]
+  int32_t* cand_ids = nullptr;     // [R]
+  int32_t* cand_nq = nullptr;      // [R]
+  double* cand_score = nullptr;    // [R]
+  uint64_t* cand_key = nullptr;    // [R]
+  int32_t* cand_tpos = nullptr;    // [R] position in targets or -1
+  int32_t* targets = nullptr;      // [T]
+  int32_t* sel_flag = nullptr;     // [R]
+  int64_t* sel_pos = nullptr;      // [R+1]
+  uint32_t* sel_hist = nullptr;    // [256]
+  // request CSR by destination slot (slot: candidate rank, or R + query)
+  int32_t* rq_cnt = nullptr;       // [RB]
+  int32_t* rq_fill = nullptr;      // [RB]
+  int64_t* rq_ptr = nullptr;       // [RB+1]
+  int32_t* rq_src = nullptr;       // [m] sources, ascending within a slot after sort
+  int32_t* big_list = nullptr;     // segments for the CTA sort
+  int32_t* sort_tmp = nullptr;     // [m] scratch for the big-segment merge
+  // block scratch
+  uint32_t* sbits = nullptr;       // source bitmap over [0, N+B)
+  int64_t* swpre = nullptr;
+  int32_t* src_global = nullptr;   // [E_max] gathered global source ids
+  int64_t* seg_len = nullptr;      // [D_max]
+  // blocks
+  std::vector<BlockDev> blocks;    // blocks[l-1] feeds layer l (mid blocks may alias)
+  std::vector<int> block_of_layer; // layer -> index into blocks
+  // execution scratch
+  const float** rowp = nullptr;    // [S_max] input row per source
+  float* gscale = nullptr;         // [S_max] gcn source normaliser
+  float* partial = nullptr;        // [items_max][w + 2]
+  float* agg = nullptr;            // [D_max][in]
+  float* outs[8] = {};             // per-layer outputs [D_l][out]
+  float* z = nullptr;              // gat: [S_max][out]
+  float* s_src = nullptr;          // gat: [S_max]
+  float* s_dst = nullptr;          // gat: [D_max]
+  float* mean = nullptr;           // moments: [D_max][in]
+  int64_t words_N = 0, words_NB = 0;
+};
+
+// stage entry points ---------------------------------------------------------
+struct Engine;
+
+constexpr int64_t kAggChunk = 128;  // edges per aggregation work item
+
+// aggregation work items: one per kAggChunk edges of a destination (at least one)
+struct ItemLoad {
+  const int64_t* dst_ptr;
+  int64_t chunk;
+  __device__ int64_t operator()(int64_t i) const {
+    int64_t len = dst_ptr[i + 1] - dst_ptr[i];
+    return len > chunk ? (len + chunk - 1) / chunk : 1;
+  }
+};
+
+void export_bindings(Engine& e, RequestWs& w, int layer, uint8_t* d_kind, int32_t* d_pe_layer);
+
+void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, int64_t words, int32_t* out);
+
+void stage_request_prep(Engine& e, RequestWs& w, bool need_scores);
+void stage_select(Engine& e, RequestWs& w);
+void stage_request_csr(Engine& e, RequestWs& w);
+void stage_build_srpe(Engine& e, RequestWs& w);
+void stage_build_full(Engine& e, RequestWs& w);
+void stage_forward(Engine& e, RequestWs& w, float* d_out);
+void stage_precompute(Engine& e);
+void block_items(Engine& e, BlockDev& b, int64_t chunk);
+
+struct Engine {
+  ob_config cfg{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  GraphDev g;
+  std::vector<LayerDev> layers;
+  std::vector<float*> pe;        // per stored layer, N x dim
+  std::vector<int> pe_dim;
+  Arena arena;
+  ScanScratch scan;
+  RequestWs ws;
+  bool have_request = false;
+  cudaEvent_t ev[6] = {};
+  int64_t launches_at_start = 0;
+  std::vector<void*> owned;      // device allocations to free
+  void* dalloc(size_t bytes) {
+    void* p = nullptr;
+    OB_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+    owned.push_back(p);
+    return p;
+  }
+  ~Engine();
+};
+
+}  // namespace ob

@@ -1,0 +1,451 @@
+// ob_select.cu -- SRPE candidate set, ratio scores, budgeted top-k, request CSR.
+//
+// Reference (paths relative to /root/reference/pkg/src/gnnserve):
+//   candidate_arrays / find_candidates  compgraph.py:108-121, policy.py:64-67
+//   score_query_edge_ratio              policy.py:77-81   (IEEE fp64 nq / total)
+//   select_targets                      policy.py:110-135 (floor(gamma*|R|), score desc, id asc)
+//   _EdgeIndex                          compgraph.py:155-171 (request edges by dst, src ascending)
+//
+// B200 design: the candidate set is a bitmap over [0, N) whose word-popcount
+// prefix gives ascending order and an O(1) id -> candidate-rank map.  The
+// top-k is a radix select over the 64-bit score bit patterns (non-negative
+// doubles order like their bits) followed by an ordered compaction, so the
+// (score desc, id asc) order never needs a full sort.  Everything runs off
+// device-side counts.
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/warp/warp_merge_sort.cuh>
+
+#include "ob_engine.h"
+
+namespace ob {
+
+int64_t g_launches = 0;
+
+__global__ void __launch_bounds__(1024) k_scan_tiles(const int64_t* n_dev, int64_t n_host, int64_t* tile_sums,
+                                                     int64_t* total_out, int64_t* out_arr) {
+  using BS = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int64_t carry;
+  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < ntiles; base += 1024) {
+    int64_t i = base + threadIdx.x;
+    int64_t v = i < ntiles ? tile_sums[i] : 0, agg;
+    BS(tmp).ExclusiveSum(v, v, agg);
+    if (i < ntiles) tile_sums[i] = v + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (total_out) *total_out = carry;
+    if (out_arr) out_arr[n] = carry;
+  }
+}
+
+__global__ void k_fill_i32(int32_t* a, const int64_t* n_dev, int64_t n_host, int32_t v) {
+  const int64_t n = dev_count(n_dev, n_host);
+  OB_GRID_STRIDE(i, n) a[i] = v;
+}
+__global__ void k_fill_i64(int64_t* a, const int64_t* n_dev, int64_t n_host, int64_t v) {
+  const int64_t n = dev_count(n_dev, n_host);
+  OB_GRID_STRIDE(i, n) a[i] = v;
+}
+
+// ---------------------------------------------------------------------------
+// 1. validate + mark training endpoints + per-query in-degree
+// ---------------------------------------------------------------------------
+__global__ void k_request_mark(const int64_t* __restrict__ edges, int64_t m, int64_t N, int B,
+                               uint32_t* cbits, int32_t* qdeg, ReqCounters* rc) {
+  const int64_t hi = N + B;
+  int64_t err = 0;
+  OB_GRID_STRIDE(e, m) {
+    int64_t s = edges[2 * e], d = edges[2 * e + 1];
+    if (s < 0 || s >= hi || d < 0 || d >= hi) {
+      err |= kErrRange;
+      continue;
+    }
+    if (s < N && d < N) err |= kErrNoQuery;
+    if (s < N) bm_set(cbits, s);
+    if (d < N) bm_set(cbits, d);
+    else atomicAdd(qdeg + (d - N), 1);
+  }
+  if (err) atomicOr((unsigned long long*)&rc->err, (unsigned long long)err);
+}
+
+__global__ void k_check_finite(const float* __restrict__ q, int64_t n, ReqCounters* rc) {
+  bool bad = false;
+  OB_GRID_STRIDE(i, n) bad |= !isfinite(q[i]);
+  if (bad) atomicOr((unsigned long long*)&rc->err, (unsigned long long)kErrNonFinite);
+}
+
+// ids of set bits in ascending order (bitmap -> sorted unique list)
+__global__ void k_bitmap_compact(const uint32_t* __restrict__ bits, const int64_t* __restrict__ wpre, int64_t words,
+                                 int32_t* out) {
+  OB_GRID_STRIDE(w, words) {
+    uint32_t b = bits[w];
+    int64_t pos = wpre[w];
+    while (b) {
+      int t = __ffs(b) - 1;
+      out[pos++] = (int32_t)(w * 32 + t);
+      b &= b - 1;
+    }
+  }
+}
+
+void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, int64_t words, int32_t* out) {
+  k_bitmap_compact<<<grid_for(words, 256), 256, 0, e.stream>>>(bits, wpre, words, out);
+  OB_LAUNCHED();
+}
+
+__global__ void k_slots_init(ReqCounters* rc, int B) { rc->RB = rc->R + B; }
+
+// request-CSR slot of a destination: candidate rank for training ids, R + q for queries
+__device__ __forceinline__ int64_t rq_slot(int64_t d, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
+                                           int64_t R) {
+  return d < N ? bm_rank(cbits, cwpre, d) : R + (d - N);
+}
+
+__global__ void k_rq_count(const int64_t* __restrict__ edges, int64_t m, int64_t N, const uint32_t* cbits,
+                           const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt) {
+  const int64_t R = rc->R;
+  if (rc->err & (kErrRange | kErrNoQuery)) return;
+  OB_GRID_STRIDE(e, m) atomicAdd(rq_cnt + rq_slot(edges[2 * e + 1], N, cbits, cwpre, R), 1);
+}
+
+// ---------------------------------------------------------------------------
+// 2. ratio scores (policy.py:77-81) and budget
+// ---------------------------------------------------------------------------
+__global__ void k_score(const int32_t* __restrict__ cand_ids, const int32_t* __restrict__ rq_cnt,
+                        const int32_t* __restrict__ indeg, ReqCounters* rc, int32_t* cand_nq, double* score,
+                        uint64_t* key, int32_t* tpos) {
+  const int64_t R = rc->R;
+  bool bad = false;
+  OB_GRID_STRIDE(c, R) {
+    int32_t nq = rq_cnt[c];
+    int64_t total = (int64_t)indeg[cand_ids[c]] + nq;
+    if (total <= 0) bad = true;
+    double s = total > 0 ? (double)nq / (double)total : 0.0;
+    cand_nq[c] = nq;
+    score[c] = s;
+    key[c] = (uint64_t)__double_as_longlong(s);  // s >= +0.0: bit order == value order
+    tpos[c] = -1;
+  }
+  if (bad) atomicOr((unsigned long long*)&rc->err, (unsigned long long)kErrZeroTotal);
+}
+
+__global__ void k_budget(ReqCounters* rc, double gamma, uint32_t* hist) {
+  // budget = int(np.floor(gamma * m)) with gamma a Python float: one IEEE fp64 multiply
+  const int64_t R = rc->R;
+  const int64_t b = (int64_t)floor(gamma * (double)R);
+  if (threadIdx.x == 0) {
+    rc->budget = b;
+    rc->sel_prefix = 0;
+    rc->sel_mask = 0;
+    rc->sel_krem = b;
+    rc->sel_gt = 0;
+    rc->sel_eq_take = 0;
+    rc->T = 0;
+  }
+  if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+}
+
+// radix select, MSB-first 8-bit digits: find the budget-th largest key
+__global__ void k_sel_hist(const uint64_t* __restrict__ key, const ReqCounters* rc, int shift, uint32_t* hist) {
+  __shared__ uint32_t h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t R = rc->R, b = rc->budget;
+  if (b > 0 && b < R) {
+    const uint64_t pre = rc->sel_prefix, msk = rc->sel_mask;
+    OB_GRID_STRIDE(c, R) {
+      uint64_t k = key[c];
+      if ((k & msk) == pre) atomicAdd(&h[(k >> shift) & 255], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(hist + i, h[i]);
+}
+
+__global__ void __launch_bounds__(256) k_sel_pick(ReqCounters* rc, int shift, uint32_t* hist) {
+  using BS = cub::BlockScan<int64_t, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  const int64_t R = rc->R, b = rc->budget;
+  const int d = 255 - threadIdx.x;  // scan from the top digit down
+  int64_t c = hist[d];
+  int64_t excl;
+  BS(tmp).ExclusiveSum(c, excl);  // keys in digits above d
+  hist[d] = 0;
+  if (!(b > 0 && b < R)) return;
+  const int64_t krem = rc->sel_krem;
+  if (excl < krem && krem <= excl + c) {
+    rc->sel_krem = krem - excl;
+    rc->sel_gt += excl;
+    rc->sel_prefix |= (uint64_t)d << shift;
+    rc->sel_mask |= (uint64_t)255 << shift;
+    if (shift == 0) rc->sel_eq_take = krem - excl;
+  }
+}
+
+// 0 = not selected, 1 = selected; ties at the threshold go to the lowest ids
+struct SelFlagLoad {
+  const uint64_t* key;
+  const ReqCounters* rc;
+  __device__ int64_t operator()(int64_t c) const {
+    const int64_t R = rc->R, b = rc->budget;
+    if (b <= 0) return 0;
+    if (b >= R) return 1;
+    return key[c] > rc->sel_prefix ? 1 : 0;
+  }
+};
+struct EqLoad {
+  const uint64_t* key;
+  const ReqCounters* rc;
+  __device__ int64_t operator()(int64_t c) const {
+    const int64_t R = rc->R, b = rc->budget;
+    return (b > 0 && b < R && key[c] == rc->sel_prefix) ? 1 : 0;
+  }
+};
+struct EqStore {
+  int32_t* flag;
+  const uint64_t* key;
+  const ReqCounters* rc;
+  __device__ void operator()(int64_t c, int64_t eqpos) const {
+    const int64_t R = rc->R, b = rc->budget;
+    int sel;
+    if (b <= 0) sel = 0;
+    else if (b >= R) sel = 1;
+    else {
+      uint64_t k = key[c], thr = rc->sel_prefix;
+      sel = (k > thr) || (k == thr && eqpos < rc->sel_eq_take);
+    }
+    flag[c] = sel;
+  }
+};
+struct SelStore {
+  const int32_t* flag;
+  const int32_t* cand_ids;
+  int32_t* targets;
+  int32_t* tpos;
+  __device__ void operator()(int64_t c, int64_t pos) const {
+    if (flag[c]) {
+      targets[pos] = cand_ids[c];
+      tpos[c] = (int32_t)pos;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// 3. request CSR fill + per-slot sort (sources ascending within a destination)
+// ---------------------------------------------------------------------------
+__global__ void k_rq_fill(const int64_t* __restrict__ edges, int64_t m, int64_t N, const uint32_t* cbits,
+                          const int64_t* cwpre, const ReqCounters* rc, const int64_t* rq_ptr, int32_t* rq_fill,
+                          int32_t* rq_src) {
+  const int64_t R = rc->R;
+  if (rc->err & (kErrRange | kErrNoQuery)) return;
+  OB_GRID_STRIDE(e, m) {
+    int64_t slot = rq_slot(edges[2 * e + 1], N, cbits, cwpre, R);
+    int64_t pos = rq_ptr[slot] + atomicAdd(rq_fill + slot, 1);
+    rq_src[pos] = (int32_t)edges[2 * e];
+  }
+}
+
+constexpr int kWarpSortItems = 8;     // warp sort handles <= 256
+constexpr int kBlockSortThreads = 512;
+constexpr int kBlockSortItems = 16;   // CTA sort handles <= 8192 per chunk
+constexpr int kBlockSortTile = kBlockSortThreads * kBlockSortItems;
+
+__device__ __forceinline__ void warp_bitonic32(int32_t& v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      int32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+      bool up = ((lane & k) == 0);
+      bool lower = ((lane & j) == 0);
+      v = (lower == up) ? min(v, o) : max(v, o);
+    }
+  }
+}
+
+struct LessI32 {
+  __device__ bool operator()(const int32_t& a, const int32_t& b) const { return a < b; }
+};
+
+__global__ void __launch_bounds__(256) k_segsort_warp(const int64_t* __restrict__ ptr, const ReqCounters* rc,
+                                                      int32_t* vals, int32_t* big_list, ReqCounters* rcw) {
+  using WS = cub::WarpMergeSort<int32_t, kWarpSortItems, 32>;
+  __shared__ typename WS::TempStorage tmp[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nseg = rc->RB;
+  for (int64_t s = (int64_t)blockIdx.x * 8 + warp; s < nseg; s += (int64_t)gridDim.x * 8) {
+    const int64_t b = ptr[s], len = ptr[s + 1] - b;
+    if (len <= 1) continue;
+    if (len <= 32) {
+      int32_t v = lane < len ? vals[b + lane] : INT32_MAX;
+      warp_bitonic32(v);
+      if (lane < len) vals[b + lane] = v;
+    } else if (len <= 32 * kWarpSortItems) {
+      int32_t k[kWarpSortItems];
+#pragma unroll
+      for (int i = 0; i < kWarpSortItems; ++i) {
+        int64_t idx = (int64_t)lane * kWarpSortItems + i;
+        k[i] = idx < len ? vals[b + idx] : INT32_MAX;
+      }
+      WS(tmp[warp]).Sort(k, LessI32());
+#pragma unroll
+      for (int i = 0; i < kWarpSortItems; ++i) {
+        int64_t idx = (int64_t)lane * kWarpSortItems + i;
+        if (idx < len) vals[b + idx] = k[i];
+      }
+    } else if (lane == 0) {
+      int64_t at = atomicAdd((unsigned long long*)&rcw->n_big, 1ull);
+      big_list[at] = (int32_t)s;
+    }
+  }
+}
+
+// merge sorted runs a[0,na) and b[0,nb) into out with the whole CTA (merge path)
+__device__ void cta_merge(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, int32_t* out) {
+  const int64_t total = na + nb;
+  const int64_t per = (total + blockDim.x - 1) / blockDim.x;
+  int64_t d = min((int64_t)threadIdx.x * per, total);
+  int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= b[d - 1 - mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  int64_t i = lo, j = d - lo;
+  const int64_t end = min(d + per, total);
+  for (int64_t o = d; o < end; ++o) {
+    if (j >= nb || (i < na && a[i] <= b[j])) out[o] = a[i++];
+    else out[o] = b[j++];
+  }
+}
+
+__global__ void __launch_bounds__(kBlockSortThreads) k_segsort_block(const int64_t* __restrict__ ptr,
+                                                                    const ReqCounters* rc, const int32_t* big_list,
+                                                                    int32_t* vals, int32_t* tmpbuf) {
+  using BRS = cub::BlockRadixSort<int32_t, kBlockSortThreads, kBlockSortItems>;
+  __shared__ typename BRS::TempStorage tmp;
+  const int64_t nbig = rc->n_big;
+  for (int64_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    const int64_t s = big_list[bi];
+    const int64_t b = ptr[s], len = ptr[s + 1] - b;
+    int32_t* v = vals + b;
+    int32_t* t = tmpbuf + b;
+    // sort tiles in shared memory
+    for (int64_t c0 = 0; c0 < len; c0 += kBlockSortTile) {
+      int32_t k[kBlockSortItems];
+#pragma unroll
+      for (int i = 0; i < kBlockSortItems; ++i) {
+        int64_t idx = c0 + (int64_t)threadIdx.x * kBlockSortItems + i;
+        k[i] = idx < len ? v[idx] : INT32_MAX;
+      }
+      BRS(tmp).Sort(k);
+#pragma unroll
+      for (int i = 0; i < kBlockSortItems; ++i) {
+        int64_t idx = c0 + (int64_t)threadIdx.x * kBlockSortItems + i;
+        if (idx < len) v[idx] = k[i];
+      }
+      __syncthreads();
+    }
+    // merge rounds, ping-pong between v and t
+    int32_t* src = v;
+    int32_t* dst = t;
+    for (int64_t w = kBlockSortTile; w < len; w <<= 1) {
+      for (int64_t lo = 0; lo < len; lo += 2 * w) {
+        int64_t na = min(w, len - lo);
+        int64_t nb = min(w, len - lo - na);
+        cta_merge(src + lo, na, src + lo + na, nb, dst + lo);
+      }
+      __syncthreads();
+      int32_t* x = src;
+      src = dst;
+      dst = x;
+    }
+    if (src != v) {
+      for (int64_t i = threadIdx.x; i < len; i += blockDim.x) v[i] = src[i];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host drivers
+// ---------------------------------------------------------------------------
+void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
+  cudaStream_t s = e.stream;
+  const int64_t N = e.g.N;
+  const int64_t m = w.m;
+  OB_CUDA(cudaMemsetAsync(w.cbits, 0, sizeof(uint32_t) * (w.words_N + 1), s));
+  OB_CUDA(cudaMemsetAsync(w.qdeg, 0, sizeof(int32_t) * (w.B + 1), s));
+  if (m > 0) {
+    k_request_mark<<<grid_for(m, 256), 256, 0, s>>>(w.edges, m, N, w.B, w.cbits, w.qdeg, w.rc);
+    OB_LAUNCHED();
+  }
+  if ((int64_t)w.B * e.g.F > 0) {
+    k_check_finite<<<grid_for((int64_t)w.B * e.g.F, 256), 256, 0, s>>>(w.qfeat, (int64_t)w.B * e.g.F, w.rc);
+    OB_LAUNCHED();
+  }
+  // candidate set: popcount prefix, ascending ids
+  device_scan(s, e.scan, LoadPopc{w.cbits}, StoreI64{w.cwpre}, nullptr, w.words_N, w.words_N, &w.rc->R, w.cwpre);
+  k_bitmap_compact<<<grid_for(w.words_N, 256), 256, 0, s>>>(w.cbits, w.cwpre, w.words_N, w.cand_ids);
+  OB_LAUNCHED();
+  k_slots_init<<<1, 1, 0, s>>>(w.rc, w.B);
+  OB_LAUNCHED();
+  const int64_t rb_max = std::min<int64_t>(N, 2 * m) + w.B;
+  k_fill_i32<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rq_cnt, &w.rc->RB, 0, 0);
+  k_fill_i32<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rq_fill, &w.rc->RB, 0, 0);
+  g_launches += 2;
+  if (m > 0) {
+    k_rq_count<<<grid_for(m, 256), 256, 0, s>>>(w.edges, m, N, w.cbits, w.cwpre, w.rc, w.rq_cnt);
+    OB_LAUNCHED();
+  }
+  if (need_scores) {
+    const int64_t r_max = std::min<int64_t>(N, 2 * m);
+    k_score<<<grid_for(r_max, 256), 256, 0, s>>>(w.cand_ids, w.rq_cnt, e.g.indeg, w.rc, w.cand_nq, w.cand_score,
+                                                 w.cand_key, w.cand_tpos);
+    OB_LAUNCHED();
+  }
+}
+
+void stage_select(Engine& e, RequestWs& w) {
+  cudaStream_t s = e.stream;
+  const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
+  k_budget<<<1, 256, 0, s>>>(w.rc, e.cfg.gamma, w.sel_hist);
+  OB_LAUNCHED();
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    k_sel_hist<<<grid_for(r_max, 256, kNumSMs * 2), 256, 0, s>>>(w.cand_key, w.rc, shift, w.sel_hist);
+    k_sel_pick<<<1, 256, 0, s>>>(w.rc, shift, w.sel_hist);
+    g_launches += 2;
+  }
+  // ordered compaction: ties at the threshold resolved by ascending id
+  device_scan(s, e.scan, EqLoad{w.cand_key, w.rc}, EqStore{w.sel_flag, w.cand_key, w.rc}, &w.rc->R, 0, r_max,
+              nullptr);
+  device_scan(s, e.scan, LoadI32{w.sel_flag}, SelStore{w.sel_flag, w.cand_ids, w.targets, w.cand_tpos}, &w.rc->R, 0,
+              r_max, &w.rc->T);
+}
+
+void stage_request_csr(Engine& e, RequestWs& w) {
+  cudaStream_t s = e.stream;
+  const int64_t m = w.m;
+  const int64_t rb_max = std::min<int64_t>(e.g.N, 2 * m) + w.B;
+  device_scan(s, e.scan, LoadI32{w.rq_cnt}, StoreI64{w.rq_ptr}, &w.rc->RB, 0, rb_max, nullptr, w.rq_ptr);
+  if (m > 0) {
+    k_rq_fill<<<grid_for(m, 256), 256, 0, s>>>(w.edges, m, e.g.N, w.cbits, w.cwpre, w.rc, w.rq_ptr, w.rq_fill,
+                                               w.rq_src);
+    OB_LAUNCHED();
+    k_segsort_warp<<<grid_for(rb_max, 8), 256, 0, s>>>(w.rq_ptr, w.rc, w.rq_src, w.big_list, w.rc);
+    k_segsort_block<<<kNumSMs, kBlockSortThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.rq_src, w.sort_tmp);
+    g_launches += 2;
+  }
+}
+
+}  // namespace ob

@@ -1,0 +1,234 @@
+"""Serving API: ``ServeConfig``, ``LatencyBreakdown``, ``ServingEngine``.
+
+Drop-in for ``gnnserve/runtime.py:62-358``: same constructor, same
+``serve(request) -> (emb[B, H_k] float32, LatencyBreakdown)`` contract, same
+exception types.  Construction copies the dataset, stored embeddings and
+weights into HBM once; ``serve`` ships only the request (edges + query
+features) to the device and reads back the B x H_k rows.  Selection,
+computation-graph construction and layer execution all run as sm_100a
+kernels in ``libomega_b200.so`` (``_native``); there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .compgraph import ComputationBlock, ComputationGraph, ServingRequest
+from .graphstore import GraphDataset, PeStore
+from .models import ModelSpec, Weights, weight_matrix_names
+
+STRATEGIES = ("full", "sampled", "srpe", "srpe-cgp")
+EDGE_BYTES = 16
+
+METRICS_HEADER = (
+    "request_id,strategy,batch,partitions,fetch_ms,transfer_ms,compute_ms,"
+    "fetch_bytes,collective_bytes,total_ms"
+)
+
+
+@dataclass
+class ServeConfig:
+    """runtime.py:62-82 (plus the CUDA device ordinal)."""
+
+    strategy: str = "full"
+    fanouts: tuple | None = None
+    gamma: float = 0.0
+    policy: str = "ratio"
+    num_partitions: int = 1
+    cache_bytes: int = 0
+    transport: str = "sim"
+    bandwidth_bytes_per_s: float = 12e9
+    seed: int = 0
+    device: int = 0
+
+    def __post_init__(self):
+        if self.strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {self.strategy!r}")
+        if self.strategy == "sampled" and not self.fanouts:
+            raise ValueError("sampled strategy needs fanouts")
+        if not 0.0 <= self.gamma <= 1.0:
+            raise ValueError("gamma must lie in [0, 1]")
+        if self.strategy == "srpe-cgp" and self.policy == "oracle":
+            raise ValueError("oracle policy needs full embeddings; not available under cgp")
+
+
+@dataclass
+class LatencyBreakdown:
+    """runtime.py:85-95; fetch/compute are device times of the request's stages."""
+
+    fetch_ms: float = 0.0
+    transfer_ms: float = 0.0
+    compute_ms: float = 0.0
+    collective_bytes: int = 0
+    fetch_bytes: int = 0
+
+    @property
+    def total_ms(self) -> float:
+        return self.fetch_ms + self.transfer_ms + self.compute_ms
+
+
+def metrics_line(request_id, strategy, batch, partitions, bd: LatencyBreakdown) -> str:
+    return (f"{request_id},{strategy},{batch},{partitions},{bd.fetch_ms:.3f},{bd.transfer_ms:.3f},"
+            f"{bd.compute_ms:.3f},{bd.fetch_bytes},{bd.collective_bytes},{bd.total_ms:.3f}")
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class ServingEngine:
+    """Loaded dataset, stored embeddings and weights, resident on one B200."""
+
+    def __init__(self, dataset: GraphDataset, pe: PeStore | None, model: ModelSpec, weights: Weights,
+                 config: ServeConfig, stream: int = 0, nccl_id: bytes | None = None, rank: int = 0):
+        if config.strategy == "sampled":
+            raise ValueError("the sampled baseline strategy is not part of the B200 serving path")
+        if config.policy != "ratio":
+            raise ValueError(f"policy {config.policy!r} is not on the device path (ratio only)")
+        if config.cache_bytes:
+            raise ValueError("feature caches are subsumed by HBM residency; use cache_bytes=0")
+        self.dataset = dataset
+        self.pe = pe
+        self.model = model
+        self.weights = weights
+        self.config = config
+        cfg = nat.ObConfig(device=config.device, strategy=nat.STRATEGY[config.strategy], gamma=float(config.gamma),
+                           policy=nat.POLICY[config.policy], num_partitions=int(config.num_partitions),
+                           rank=int(rank), seed=int(config.seed) & 0xFFFFFFFFFFFFFFFF, stream=int(stream),
+                           nccl_id=None)
+        self._id_buf = None
+        if nccl_id is not None:
+            self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
+            cfg.nccl_id = C.cast(self._id_buf, C.c_void_p)
+        h = C.c_void_p()
+        nat.check(nat.lib.ob_engine_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+        self._lib = nat.lib
+        try:
+            self._load(dataset, pe, model, weights)
+        except BaseException:
+            self.close()
+            raise
+
+    # -- loading ---------------------------------------------------------------
+    def _load(self, ds, pe, model, weights):
+        off = np.ascontiguousarray(ds.in_offsets, dtype=np.int64)
+        nb = np.ascontiguousarray(ds.in_neighbors, dtype=np.int64)
+        feats = _f32(ds.features)
+        nat.check(self._lib.ob_load_graph(self._h, int(ds.num_nodes), nat.ptr(off), nat.ptr(nb), int(nb.shape[0]),
+                                          nat.ptr(feats), int(feats.shape[1])))
+        layers = (nat.ObLayer * model.k)()
+        mats = []
+        for i, spec in enumerate(model.layers):
+            layers[i] = nat.ObLayer(nat.KIND_TAGS[spec.kind], spec.in_dim, spec.out_dim, float(spec.p), int(spec.n))
+            for name in weight_matrix_names(spec.kind):
+                mats.append(_f32(weights.layers[i][name]))
+        arr = (C.c_void_p * len(mats))(*[m.ctypes.data for m in mats])
+        nat.check(self._lib.ob_load_model(self._h, model.k, layers, arr))
+        if pe is not None:
+            if getattr(pe, "node_ids", None) is not None:
+                raise ValueError("the engine needs a whole-graph stored-embedding store")
+            for l in range(1, pe.num_layers + 1):
+                rows = _f32(pe.layers[l - 1])
+                nat.check(self._lib.ob_load_pe(self._h, l, nat.ptr(rows), int(rows.shape[0]), int(rows.shape[1])))
+
+    def precompute_pe(self) -> None:
+        """GPU precompute_embeddings into HBM (graphstore.py:330-365)."""
+        nat.check(self._lib.ob_precompute_pe(self._h))
+
+    def read_pe(self, layer: int) -> np.ndarray:
+        dim = self.model.layers[layer - 1].out_dim
+        out = np.empty((self.dataset.num_nodes, dim), dtype=np.float32)
+        nat.check(self._lib.ob_read_pe(self._h, layer, nat.ptr(out)))
+        return out
+
+    # -- serving ---------------------------------------------------------------
+    def serve(self, request: ServingRequest) -> tuple[np.ndarray, LatencyBreakdown]:
+        """runtime.py:308-358."""
+        if request.num_base != self.dataset.num_nodes:
+            raise ValueError("request numbered against a different dataset")
+        if self.config.strategy != "full" and self.model.k < 2:
+            raise ValueError("reuse graphs need k >= 2")
+        B = int(request.num_queries)
+        q = _f32(request.query_features)
+        if q.shape != (B, self.dataset.feature_dim):
+            raise ValueError("query features must be B x F")
+        e = np.ascontiguousarray(request.edges, dtype=np.int64)
+        out = np.empty((B, self.model.layers[-1].out_dim), dtype=np.float32)
+        bd = nat.ObBreakdown()
+        nat.check(self._lib.ob_serve(self._h, B, nat.ptr(q), int(e.shape[0]), nat.ptr(e), nat.ptr(out),
+                                     C.byref(bd)))
+        self.last_breakdown = bd
+        lb = LatencyBreakdown(
+            fetch_ms=bd.fetch_ms,
+            transfer_ms=bd.fetch_bytes / self.config.bandwidth_bytes_per_s * 1e3,
+            compute_ms=bd.compute_ms,
+            collective_bytes=int(bd.collective_bytes),
+            fetch_bytes=int(bd.fetch_bytes),
+        )
+        return out, lb
+
+    def serve_device(self, num_queries: int, d_query_features: int, num_edges: int, d_edges: int, d_out: int,
+                     sync: bool = False):
+        """Request already in HBM (device pointers as ints); enqueue only unless sync."""
+        bd = nat.ObBreakdown() if sync else None
+        nat.check(self._lib.ob_serve_device(self._h, int(num_queries), C.c_void_p(d_query_features),
+                                            int(num_edges), C.c_void_p(d_edges), C.c_void_p(d_out),
+                                            C.byref(bd) if bd is not None else None))
+        return bd
+
+    # -- parity hooks ------------------------------------------------------------
+    def last_plan(self) -> dict:
+        nc, nt = C.c_int64(), C.c_int64()
+        nat.check(self._lib.ob_last_plan(self._h, C.byref(nc), C.byref(nt), None, None, None, None, None))
+        ids = np.empty(nc.value, np.int64)
+        nq = np.empty(nc.value, np.int64)
+        tot = np.empty(nc.value, np.int64)
+        sc = np.empty(nc.value, np.float64)
+        tg = np.empty(nt.value, np.int64)
+        nat.check(self._lib.ob_last_plan(self._h, C.byref(nc), C.byref(nt), nat.ptr(ids), nat.ptr(nq),
+                                         nat.ptr(tot), nat.ptr(sc), nat.ptr(tg)))
+        return dict(ids=ids, nq=nq, total=tot, scores=sc, targets=tg)
+
+    def last_block(self, layer: int, partition: int = 0) -> ComputationBlock:
+        ns, nd, ne = C.c_int64(), C.c_int64(), C.c_int64()
+        nat.check(self._lib.ob_last_block_sizes(self._h, partition, layer, C.byref(ns), C.byref(nd), C.byref(ne)))
+        S, D, E = ns.value, nd.value, ne.value
+        b = ComputationBlock(
+            src_ids=np.empty(S, np.int64), dst_ids=np.empty(D, np.int64), edge_src=np.empty(E, np.int64),
+            edge_dst=np.empty(E, np.int64), bind_kind=np.empty(S, np.uint8), bind_pe_layer=np.empty(S, np.int32),
+            src_degree=np.empty(S, np.int64), dst_self_src=np.empty(D, np.int64),
+        )
+        nat.check(self._lib.ob_last_block(self._h, partition, layer, nat.ptr(b.src_ids), nat.ptr(b.dst_ids),
+                                          nat.ptr(b.edge_src), nat.ptr(b.edge_dst), nat.ptr(b.bind_kind),
+                                          nat.ptr(b.bind_pe_layer), nat.ptr(b.src_degree),
+                                          nat.ptr(b.dst_self_src)))
+        if self.config.strategy == "srpe-cgp":
+            b.dst_self_src = None
+        return b
+
+    def last_graph(self, partition: int = 0) -> ComputationGraph:
+        blocks = [self.last_block(l, partition) for l in range(1, self.model.k + 1)]
+        n = self.dataset.num_nodes
+        tg = self.last_plan()["targets"] if self.config.strategy != "full" else np.empty(0, np.int64)
+        B = int(np.sum(blocks[-1].dst_ids >= n))
+        return ComputationGraph(blocks, np.arange(n, n + B, dtype=np.int64), self.config.strategy, n, tg)
+
+    def launch_count(self) -> int:
+        return int(self._lib.ob_launch_count(self._h))
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.ob_engine_destroy(h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,174 @@
+"""CUDA path vs the reference (golden vectors) and the oracle -- needs a B200.
+
+Bars (BASELINE.json north_star): candidates, scores, targets and every block
+array bit-exact; embeddings within max|a-r|/max|r| <= 1e-4 in fp32.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import KINDS, SMALL_CASES, assert_block_equal, golden_weights, load_golden
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def rel(a, r) -> float:
+    from oracle.layers import max_rel_err
+
+    return max_rel_err(a, r)
+
+
+def _engine(g, kind, kw, k, strategy, gamma=0.0, pe=True, H=6):
+    from paper_2501_08547_b200 import graphstore, models, runtime
+
+    N = int(g["N"])
+    F = g["feats"].shape[1]
+    ds = graphstore.GraphDataset(N, g["offsets"], g["nbrs"], g["feats"], np.ones(N, bool), np.zeros(N, bool))
+    model = models.make_model(kind, k, F, H, **kw)
+    w = models.Weights(golden_weights(g, f"w.{kind}.k{k}", kind, k))
+    store = graphstore.PeStore([g[f"pe.{kind}.k{k}.l{l}"] for l in range(1, k)]) if pe else None
+    return runtime.ServingEngine(ds, store, model, w, runtime.ServeConfig(strategy=strategy, gamma=gamma))
+
+
+def _request(g):
+    from paper_2501_08547_b200.compgraph import ServingRequest
+
+    return ServingRequest(int(g["N"]), int(g["B"]), g["qfeat"], g["edges"])
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+@pytest.mark.parametrize("kind,kw", KINDS)
+@pytest.mark.parametrize("k", [2, 3])
+def test_full_strategy(goldens, name, kind, kw, k):
+    g = goldens[name]
+    eng = _engine(g, kind, kw, k, "full", pe=False)
+    emb, bd = eng.serve(_request(g))
+    assert rel(emb, g[f"full.{kind}.k{k}.emb"]) <= TOL
+    if kind == "sage_mean":
+        for l in range(1, k + 1):
+            assert_block_equal(eng.last_block(l), g, f"full.sage_mean.k{k}.b{l}")
+        assert bd.fetch_bytes == int(g[f"full.sage_mean.k{k}.fetch"])
+    eng.close()
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+@pytest.mark.parametrize("kind,kw", KINDS)
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("gamma", [0.0, 0.5, 1.0])
+def test_srpe_strategy(goldens, name, kind, kw, k, gamma):
+    g = goldens[name]
+    if not bool(g["cand.scorable"]):
+        pytest.skip("request has an unscorable candidate")
+    eng = _engine(g, kind, kw, k, "srpe", gamma)
+    emb, bd = eng.serve(_request(g))
+    assert rel(emb, g[f"srpe.{kind}.k{k}.g{gamma}.emb"]) <= TOL
+    assert bd.fetch_bytes == int(g[f"srpe.{kind}.k{k}.g{gamma}.fetch"])
+    plan = eng.last_plan()
+    assert np.array_equal(plan["ids"], g["cand.ids"])
+    assert np.array_equal(plan["nq"], g["cand.nq"])
+    assert np.array_equal(plan["total"], g["cand.total"])
+    assert np.array_equal(plan["scores"].view(np.uint64), g["cand.scores"].view(np.uint64))
+    assert np.array_equal(plan["targets"], g[f"targets.g{gamma}"])
+    if kind == "sage_mean":
+        for l in range(1, k + 1):
+            assert_block_equal(eng.last_block(l), g, f"srpe.sage_mean.k{k}.g{gamma}.b{l}")
+    eng.close()
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+@pytest.mark.parametrize("gamma", [0.1, 0.25, 0.29, 0.57, 0.75])
+def test_selection_gamma_sweep(goldens, name, gamma):
+    g = goldens[name]
+    eng = _engine(g, "sage_mean", {}, 2, "srpe", gamma)
+    eng.serve(_request(g))
+    assert np.array_equal(eng.last_plan()["targets"], g[f"targets.g{gamma}"])
+    eng.close()
+
+
+@pytest.mark.parametrize("kind,kw", KINDS)
+@pytest.mark.parametrize("k", [2, 3])
+def test_gpu_precompute(goldens, kind, kw, k):
+    g = goldens["small_s60"]
+    eng = _engine(g, kind, kw, k, "full", pe=False)
+    eng.precompute_pe()
+    for l in range(1, k):
+        assert rel(eng.read_pe(l), g[f"pe.{kind}.k{k}.l{l}"]) <= TOL
+    eng.close()
+
+
+def test_edge_cases():
+    from paper_2501_08547_b200 import graphstore, models, runtime
+    from paper_2501_08547_b200.compgraph import ServingRequest
+
+    g = load_golden("edge_cases")
+    N = len(g["offsets"]) - 1
+    ds = graphstore.GraphDataset(N, g["offsets"], g["nbrs"], g["feats"], np.ones(N, bool), np.zeros(N, bool))
+    model = models.make_model("sage_mean", 2, 2, 3)
+    w = models.Weights(golden_weights(g, "w", "sage_mean", 2))
+    pe = graphstore.PeStore([np.zeros((N, 3), np.float32)])
+    full = runtime.ServingEngine(ds, None, model, w, runtime.ServeConfig(strategy="full"))
+    srpe = runtime.ServingEngine(ds, pe, model, w, runtime.ServeConfig(strategy="srpe", gamma=0.5))
+    for name in ("empty", "outonly", "dups", "qq"):
+        req = ServingRequest(N, 2, np.ones((2, 2), np.float32), g[f"{name}.edges"].reshape(-1, 2))
+        emb, _ = full.serve(req)
+        assert rel(emb, g[f"{name}.full.emb"]) <= TOL, name
+        for l in (1, 2):
+            assert_block_equal(full.last_block(l), g, f"{name}.full.b{l}")
+        if bool(g[f"{name}.scorable"]):
+            srpe.serve(req)
+            assert np.array_equal(srpe.last_plan()["targets"], g[f"{name}.targets.g0.5"]), name
+        else:
+            with pytest.raises(ValueError, match="zero total degree"):
+                srpe.serve(req)
+    full.close()
+    srpe.close()
+
+
+def _sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def test_config1_against_reference():
+    """BASELINE config 1 end to end: targets, block hashes, fetch bytes, embeddings."""
+    from oracle import layers as OL
+    from paper_2501_08547_b200 import graphstore, models, runtime, workload
+
+    g = load_golden("cfg1")
+    full = workload.gen_powerlaw_graph(100_000, 20.0, 2.1, 64, seed=1)
+    serving, pool = workload.split_holdout(full, 0.25, seed=1)
+    req = workload.make_request(pool, serving, 256, seed=3)
+    model = models.make_model("gcn", 2, 64, 64)
+    w = models.init_weights(model, 2)
+    # PE from the GPU precompute, checked against the reference's spot rows
+    pe_gpu = graphstore.precompute_embeddings(serving, model, w)
+    assert rel(pe_gpu.layers[0][::97], g["pe_l1"]) <= TOL
+    # serve on the reference-equivalent (oracle) PE so embeddings compare like for like
+    pe = graphstore.PeStore(OL.precompute([dict(kind="gcn", in_dim=64, out_dim=64)] * 2, w.layers,
+                                          serving.in_offsets, serving.in_neighbors, serving.features))
+    eng = runtime.ServingEngine(serving, pe, model, w, runtime.ServeConfig(strategy="srpe", gamma=0.1))
+    emb, bd = eng.serve(req)
+    plan = eng.last_plan()
+    assert len(plan["ids"]) == int(g["cand.n"])
+    assert _sha(plan["ids"], plan["scores"]) == str(g["cand_sha"])
+    assert np.array_equal(plan["targets"], g["targets"])
+    fields = ("src_ids", "dst_ids", "edge_src", "edge_dst", "bind_kind", "bind_pe_layer", "src_degree", "dst_self_src")
+    for l in (1, 2):
+        b = eng.last_block(l)
+        assert _sha(*[np.asarray(getattr(b, f), dtype=np.int64) for f in fields]) == str(g[f"b{l}.sha"]), l
+    assert bd.fetch_bytes == int(g["fetch_bytes"])
+    assert rel(emb, g["emb"]) <= TOL
+    # determinism: a second serve is bitwise identical
+    emb2, _ = eng.serve(req)
+    assert np.array_equal(emb, emb2)
+    eng.close()
