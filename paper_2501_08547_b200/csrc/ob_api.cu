@@ -136,14 +136,14 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     w.block_of_layer[l - 1] = (e.cfg.strategy == OB_STRATEGY_FULL) ? l - 1 : (l < k ? 0 : 1);
   w.rowp = a.take<const float*>(Smax);
   w.gscale = a.take<float>(Smax);
-  w.partial = a.take<float>(Imax * (maxw + 2));
-  w.agg = a.take<float>(Dmax * maxw);
   bool gat = false, mom = false;
   for (auto& L : e.layers) {
     gat |= L.spec.kind == OB_KIND_GAT;
     mom |= L.spec.kind == OB_KIND_MOMENTS;
   }
-  w.mean = mom ? a.take<float>(Dmax * maxw) : nullptr;
+  w.partial = a.take<float>(Imax * (maxw + 2) * (mom ? 2 : 1));  // moments partials are float64
+  w.agg = a.take<float>(Dmax * maxw);
+  w.mean = mom ? a.take<float>(2 * Dmax * maxw) : nullptr;
   w.z = gat ? a.take<float>(Smax * maxw) : nullptr;
   w.s_src = gat ? a.take<float>(Smax) : nullptr;
   w.s_dst = gat ? a.take<float>(Dmax) : nullptr;

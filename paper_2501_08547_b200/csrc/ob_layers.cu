@@ -16,11 +16,16 @@
 // deterministic run to run.  Inputs are never materialised: every source
 // carries a row pointer into features / query features / PE / the previous
 // layer's output, and gathers read rows straight from HBM.
+#include <type_traits>
+
 #include "ob_engine.h"
 
 namespace ob {
 
-enum AggOp { kOpSum = 0, kOpMax = 1, kOpPow = 2, kOpMom2 = 3, kOpSoftmax = 4 };
+// kOpDSum / kOpMom2 accumulate in float64: the moments kind takes an n-th root
+// of a central moment near zero, which amplifies float32 rounding (the reference
+// keeps those payloads float64 for the same reason, cgpexec.py:24-28).
+enum AggOp { kOpSum = 0, kOpMax = 1, kOpPow = 2, kOpMom2 = 3, kOpSoftmax = 4, kOpDSum = 5 };
 
 struct RowSrc {
   const float* const* rowp;  // per-source row pointers, or null for dense
@@ -168,7 +173,7 @@ struct AggArgs {
   const float* gscale;   // sum with per-source weight (gcn) or null
   float p;               // power mean exponent
   int n;                 // moments order
-  const float* mean;     // moments phase 2: [D][width]
+  const double* mean;    // moments phase 2: [D][width] (float64)
   const float* s_src;    // softmax
   const float* s_dst;
   float* partial;        // [items][pw]
@@ -190,7 +195,8 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
     const int64_t j = it - a.item_ptr[i];
     const int64_t e0 = a.dst_ptr[i] + j * kAggChunk;
     const int64_t e1 = min(e0 + kAggChunk, a.dst_ptr[i + 1]);
-    float acc[kAggNV][VEC];
+    using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
+    AT acc[kAggNV][VEC];
     float m_run = -INFINITY, den = 0.f;
 #pragma unroll
     for (int q = 0; q < kAggNV; ++q)
@@ -231,11 +237,12 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
 #pragma unroll
             for (int t = 0; t < VEC; ++t) {
               if (OP == kOpSum) acc[q][t] = fmaf(wgt, v[t], acc[q][t]);
+              else if (OP == kOpDSum) acc[q][t] += (double)v[t];
               else if (OP == kOpMax) acc[q][t] = fmaxf(acc[q][t], v[t]);
               else if (OP == kOpPow) acc[q][t] += powf(softplus_f(v[t]), a.p);
               else if (OP == kOpMom2) {
-                float dlt = v[t] - a.mean[i * a.width + col + t];
-                float pw = dlt;
+                double dlt = (double)v[t] - a.mean[i * a.width + col + t];
+                double pw = dlt;
                 for (int r2 = 1; r2 < a.n; ++r2) pw *= dlt;
                 acc[q][t] += pw;
               } else {
@@ -246,7 +253,7 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
         }
       }
     }
-    float* out = a.partial + it * (int64_t)a.pw;
+    AT* out = reinterpret_cast<AT*>(a.partial) + it * (int64_t)a.pw;
     if (OP == kOpSoftmax) {
       if (blockIdx.y == 0 && lane == 0) {
         out[0] = (e1 > e0) ? m_run : -INFINITY;
@@ -261,6 +268,28 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
 #pragma unroll
         for (int t = 0; t < VEC; ++t) out[col + t] = acc[q][t];
       }
+    }
+  }
+}
+
+// moments finalize in float64: phase 1 -> mean (double), phase 2 -> signed root (float)
+__global__ void k_finalize_moments(const BlockCounters* cnt_, const int64_t* dst_ptr, const int64_t* item_ptr,
+                                   const double* partial, int width, int phase, int n, double* mean,
+                                   float* agg) {
+  const int64_t D = cnt_->D;
+  const int64_t total = D * width;
+  OB_GRID_STRIDE(idx, total) {
+    const int64_t i = idx / width;
+    const int col = (int)(idx - i * width);
+    const int64_t cnt = dst_ptr[i + 1] - dst_ptr[i];
+    double s = 0.0;
+    for (int64_t it = item_ptr[i]; it < item_ptr[i + 1]; ++it) s += partial[it * (int64_t)width + col];
+    double m = cnt > 0 ? s / (double)cnt : 0.0;
+    if (phase == 1) {
+      mean[idx] = m;
+    } else {
+      double r = (n & 1) ? copysign(pow(fabs(m), 1.0 / n), m) : pow(fmax(m, 0.0), 1.0 / n);  // densemath.py:37-41
+      agg[idx] = (float)r;
     }
   }
 }
@@ -527,6 +556,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     finalize(s, f, r.D_max);
     return;
   }
+  bool finalize_skip = false;
   if (sp.kind == OB_KIND_GCN) {
     a.gscale = r.gscale;
     launch_agg<kOpSum>(s, a, r.items_max);
@@ -535,18 +565,22 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   } else if (sp.kind == OB_KIND_POWER_MEAN) {
     launch_agg<kOpPow>(s, a, r.items_max);
   } else if (sp.kind == OB_KIND_MOMENTS) {
-    launch_agg<kOpSum>(s, a, r.items_max);
-    f.phase = 1;
-    f.out = sc.mean;
-    finalize(s, f, r.D_max);
-    a.mean = sc.mean;
+    double* mean = reinterpret_cast<double*>(sc.mean);
+    launch_agg<kOpDSum>(s, a, r.items_max);
+    k_finalize_moments<<<grid_for(r.D_max * in, 256), 256, 0, s>>>(r.cnt, r.dst_ptr, r.item_ptr,
+                                                                     (const double*)sc.partial, in, 1, sp.n, mean,
+                                                                     nullptr);
+    a.mean = mean;
     launch_agg<kOpMom2>(s, a, r.items_max);
-    f.phase = 2;
-    f.out = sc.agg;
+    k_finalize_moments<<<grid_for(r.D_max * in, 256), 256, 0, s>>>(r.cnt, r.dst_ptr, r.item_ptr,
+                                                                     (const double*)sc.partial, in, 2, sp.n, nullptr,
+                                                                     sc.agg);
+    g_launches += 2;
+    finalize_skip = true;
   } else {
     launch_agg<kOpSum>(s, a, r.items_max);  // sage_mean
   }
-  finalize(s, f, r.D_max);
+  if (!finalize_skip) finalize(s, f, r.D_max);
   GemmArgs g{};
   g.M_dev = r.D_dev;
   g.Nc = outd;
@@ -663,7 +697,9 @@ void stage_precompute(Engine& e) {
   hc.S = N;
   OB_CUDA(cudaMemcpyAsync(cnt, &hc, sizeof(hc), cudaMemcpyHostToDevice, s));
   int64_t* item_ptr = (int64_t*)e.dalloc(sizeof(int64_t) * (N + 1));
-  float* partial = (float*)e.dalloc(sizeof(float) * items_max * maxw);
+  bool mom = false;
+  for (auto& L : e.layers) mom |= L.spec.kind == OB_KIND_MOMENTS;
+  float* partial = (float*)e.dalloc(sizeof(float) * items_max * maxw * (mom ? 2 : 1));
   float* agg = (float*)e.dalloc(sizeof(float) * N * maxw);
   float* mean = nullptr;
   float* z = nullptr;
@@ -673,7 +709,7 @@ void stage_precompute(Engine& e) {
   k_node_scale<<<grid_for(N, 256), 256, 0, s>>>(e.g.indeg, N, gscale);
   OB_LAUNCHED();
   for (auto& L : e.layers) {
-    if (L.spec.kind == OB_KIND_MOMENTS && !mean) mean = (float*)e.dalloc(sizeof(float) * N * maxw);
+    if (L.spec.kind == OB_KIND_MOMENTS && !mean) mean = (float*)e.dalloc(sizeof(double) * N * maxw);
     if (L.spec.kind == OB_KIND_GAT && !z) {
       z = (float*)e.dalloc(sizeof(float) * N * maxw);
       s_src = (float*)e.dalloc(sizeof(float) * N);
