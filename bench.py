@@ -1,0 +1,385 @@
+"""Serving benchmark: p50/p99 query-batch latency and queries/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the largest single-GPU config): 3-layer
+GraphSAGE-mean on the Reddit-shaped synthetic graph (233K nodes, 103.6M
+edges after the 25% test hold-out, 602-d features, hidden 128), B = 1024
+query batches, SRPE ratio policy gamma = 0.1.  The graph, hold-out pool,
+requests and weights are the reference generator's own (bit-identical numpy
+streams, seeds from SURVEY.md 8(d)); PE comes from the GPU precompute.
+
+One step = one query batch through ServingEngine: selection, graph
+construction and all three layers.  ``value`` times the device path with the
+request already in HBM; ``e2e`` times the public host-pointer API (pinned
+request H2D + D2H of the B x 128 rows inside the region).  L2 is flushed
+(512 MB write) before every timed step.  Under torchrun (N > 1) each rank
+serves its own request stream on its own GPU (replicas; CGP is DESIGN.md's
+next row) and the time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n, avg_degree, F, kind, k, hidden, B, gamma, description)
+    "cfg1": (100_000, 20.0, 64, "gcn", 2, 64, 256, 0.1,
+             "2-layer GCN, 100K-node/2M-edge power-law graph, F=64, B=256, SRPE ratio 0.1"),
+    "cfg2": (233_000, 493.0, 602, "sage_mean", 3, 128, 1024, 0.1,
+             "3-layer GraphSAGE-mean, Reddit-shaped 233K nodes / 103.6M edges, F=602, H=128, B=1024, SRPE ratio 0.1"),
+    "cfg3": (2_400_000, 26.0, 100, "gat", 3, 128, 1024, 0.1,
+             "3-layer GAT, ogbn-products-shaped 2.4M nodes / 55.9M edges, F=100, H=128, B=1024, SRPE ratio 0.1"),
+}
+METRIC = "queries/s (B-query batches, p50/p99 batch latency in ms alongside)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def make_inputs(cfg, rank, world, n_req, seed_base=3):
+    """Reference-generator graph + requests; rank 0 builds, others map the same files."""
+    from paper_2501_08547_b200 import workload
+    from paper_2501_08547_b200.graphstore import GraphDataset
+
+    n, avg, F, kind, k, H, B, gamma, _ = CONFIGS[cfg]
+    shm = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+    path = os.path.join(shm, f"omega_bench_{cfg}")
+    t0 = time.time()
+    if rank == 0 or world == 1:
+        full = workload.gen_powerlaw_graph(n, avg, 2.1, F, seed=1)
+        serving, pool = workload.split_holdout(full, 0.25, seed=1)
+        del full
+        if world > 1:
+            np.savez(path, off=serving.in_offsets, nb=serving.in_neighbors, feats=serving.features,
+                     ids=pool.ids, inc=pool.incident_edges)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        if rank != 0:
+            z = np.load(path + ".npz", mmap_mode="r")
+            serving = GraphDataset(n, z["off"], z["nb"], z["feats"], np.ones(n, bool), np.zeros(n, bool))
+            removed = np.zeros(n, bool)
+            removed[z["ids"]] = True
+            pool = workload.HoldoutPool(z["ids"], removed, serving.features[z["ids"]], z["inc"])
+    log(f"[bench] rank {rank}: graph ready in {time.time() - t0:.1f}s (E={serving.num_edges})")
+    reqs = [workload.make_request(pool, serving, B, seed=seed_base + 1000 * rank + i) for i in range(n_req)]
+    return serving, pool, reqs
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, device):
+        self.path = os.path.join(tempfile.gettempdir(), f"clocks_{os.getpid()}.csv")
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the aggregation kernel from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_agg_traffic.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_sample(serving, pe_layers, model, weights, pool, cfg, budget_s=12.0, batch=16):
+    """The oracle (numpy/scipy port of the reference) on bounded sub-batches of the same workload."""
+    from oracle import layers as OL
+    from paper_2501_08547_b200 import workload
+
+    n, avg, F, kind, k, H, B, gamma, _ = CONFIGS[cfg]
+    specs = [dict(kind=s.kind, in_dim=s.in_dim, out_dim=s.out_dim, p=s.p, n=s.n) for s in model.layers]
+    done, q, t_all, lat = 0, 0, 0.0, []
+    while True:
+        req = workload.make_request(pool, serving, batch, seed=777 + done)
+        t0 = time.perf_counter()
+        OL.serve("srpe", specs, weights.layers, serving.num_nodes, batch, serving.in_offsets, serving.in_neighbors,
+                 serving.features, req.query_features, req.edges, pe_layers=pe_layers, gamma=gamma)
+        dt = time.perf_counter() - t0
+        lat.append(dt * 1e3)
+        t_all += dt
+        q += batch
+        done += 1
+        if t_all >= budget_s:
+            break
+    return q / t_all, done, lat
+
+
+def run_reference(args):
+    """--impl reference: the oracle port of the reference CPU path, rank 0 only."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2501_08547_b200 import models
+
+    cfg = args.config
+    n, avg, F, kind, k, H, B, gamma, desc = CONFIGS[cfg]
+    serving, pool, _ = make_inputs(cfg, 0, 1, 0)
+    model = models.make_model(kind, k, F, H)
+    w = models.init_weights(model, 2)
+    rng = np.random.default_rng(9)
+    # stored embeddings: value-independent for timing; fabricated as in SURVEY.md 6 (reference precompute
+    # would need E x F float64 temporaries)
+    pe = [rng.standard_normal((serving.num_nodes, H)).astype(np.float32) * 0.1 for _ in range(k - 1)]
+    batch = args.ref_batch
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_sample(serving, pe, model, w, pool, cfg, budget_s=0.0, batch=batch)
+    qps, nreq, lat = [], 0, []
+    t_total, q_total = 0.0, 0
+    for _ in range(args.steps):
+        v, nr, l = cpu_sample(serving, pe, model, w, pool, cfg, budget_s=0.0, batch=batch)
+        lat += l
+        t_total += sum(l) / 1e3
+        q_total += batch * nr
+        nreq += nr
+    value = q_total / t_total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_total * 1e3 / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "sample_batch": batch, "policy": "ratio", "gamma": gamma},
+        "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+        "cpu_baseline": {"value": round(value, 3), "unit": "queries/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{args.steps} requests of {batch} queries each (bounded sub-batches of the "
+                                   f"{cfg} workload; numpy/scipy port of the reference, oracle/)"},
+        "e2e": {"value": round(value, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--gamma", type=float, default=None)
+    ap.add_argument("--ref-batch", type=int, default=16)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2501_08547_b200 import models, runtime
+
+    cfg = args.config
+    n, avg, F, kind, k, H, B, gamma, desc = CONFIGS[cfg]
+    if args.gamma is not None:
+        gamma = args.gamma
+    nreq = args.warmup + args.steps
+    serving, pool, reqs = make_inputs(cfg, rank, world, nreq)
+    model = models.make_model(kind, k, F, H)
+    w = models.init_weights(model, 2)
+    stream = torch.cuda.Stream(device=local)
+    t0 = time.time()
+    eng = runtime.ServingEngine(serving, None, model, w,
+                                runtime.ServeConfig(strategy="srpe", gamma=gamma, device=local),
+                                stream=stream.cuda_stream)
+    eng.precompute_pe()
+    log(f"[bench] rank {rank}: engine loaded + GPU PE precompute in {time.time() - t0:.1f}s")
+    lib = eng._lib
+    max_m = max(r.edges.shape[0] for r in reqs)
+    from paper_2501_08547_b200 import _native as nat
+
+    nat.check(lib.ob_reserve(eng._h, B, max_m))
+    dev = torch.device("cuda", local)
+    d_edges = [torch.from_numpy(r.edges).to(dev) for r in reqs]
+    d_q = [torch.from_numpy(r.query_features).to(dev) for r in reqs]
+    d_out = torch.empty((B, H), dtype=torch.float32, device=dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def step(i):
+        eng.serve_device(B, d_q[i].data_ptr(), d_edges[i].shape[0], d_edges[i].data_ptr(), d_out.data_ptr())
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    stream.synchronize()
+    # correctness guard on a warm request: errors surface here, not silently
+    eng.serve_device(B, d_q[0].data_ptr(), d_edges[0].shape[0], d_edges[0].data_ptr(), d_out.data_ptr(), sync=True)
+
+    nat.check(lib.ob_profile(eng._h, 1))
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = eng.launch_count()
+    clocks = Clocks(local)
+    with torch.cuda.stream(stream):
+        for j in range(args.steps):
+            flush.fill_(j & 0xFF)  # evict L2 (512 MB > 126 MB) outside the timed events
+            ev_s[j].record(stream)
+            step(args.warmup + j)
+            ev_e[j].record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = eng.launch_count() - launches0
+    lat = np.array([ev_s[j].elapsed_time(ev_e[j]) for j in range(args.steps)])
+    total_ms = float(lat.sum())
+    agg = _read_prof(lib, eng, nat, 0)
+    gemm = _read_prof(lib, eng, nat, 1)
+    fin = _read_prof(lib, eng, nat, 2)
+    reqp = _read_prof(lib, eng, nat, 6)
+    nat.check(lib.ob_profile(eng._h, 0))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * B * args.steps / (total_ms / 1e3)
+
+    # end to end through the public host-pointer API (pinned buffers, H2D + D2H inside the region)
+    e2e = None
+    if not args.no_e2e:
+        pin_e = [torch.from_numpy(r.edges).pin_memory() for r in reqs]
+        pin_q = [torch.from_numpy(r.query_features).pin_memory() for r in reqs]
+        out_h = torch.empty((B, H), dtype=torch.float32).pin_memory()
+        import ctypes as C
+
+        e2e_ms = []
+        h2d = d2h = 0
+        for j in range(args.steps):
+            i = args.warmup + j
+            flush.fill_(j & 0xFF)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            bd = nat.ObBreakdown()
+            nat.check(lib.ob_serve(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
+                                   C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(out_h.data_ptr()), C.byref(bd)))
+            b.record(stream)
+            b.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+            h2d += bd.h2d_bytes
+            d2h += bd.d2h_bytes
+        et = float(np.sum(e2e_ms))
+        if world > 1:
+            t = torch.tensor([et], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            et = float(t.item())
+        e2e = {"value": round(world * B * args.steps / (et / 1e3), 3), "unit": "queries/s",
+               "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
+               "p50_ms": float(np.percentile(e2e_ms, 50)), "p99_ms": float(np.percentile(e2e_ms, 99))}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        pe_host = [eng.read_pe(l) for l in range(1, k)]
+        qps, nr, cl = cpu_sample(serving, pe_host, model, w, pool, cfg, budget_s=12.0, batch=args.ref_batch)
+        cpu = {"value": round(qps, 3), "unit": "queries/s", "cores": 1, "kind": "port",
+               "sample": f"{nr} requests of {args.ref_batch} queries (bounded sub-batches of the {cfg} workload, "
+                         f"same graph/PE/weights; numpy+scipy port of the reference, oracle/)"}
+
+    hbm, tf, which = peaks()
+    agg_gbs = agg["bytes"] / (agg["ms"] / 1e3) / 1e9 if agg["ms"] > 0 else 0.0
+    roof = {"bound": "hbm", "kernel": "k_agg (edge-chunk gather + segment reduce)",
+            "achieved": round(agg_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(agg_gbs / hbm, 4),
+            "peak_source": which, "traffic": ncu_traffic(),
+            "launches": agg["n"], "avg_launch_us": round(agg["ms"] * 1e3 / max(agg["n"], 1), 2),
+            "share_of_step": round(agg["ms"] / max(reqp["ms"], 1e-9), 3)}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+        "p50_ms": round(float(np.percentile(lat, 50)), 4), "p99_ms": round(float(np.percentile(lat, 99)), 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": desc, "batch": B, "policy": "ratio", "gamma": gamma, "strategy": "srpe",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "l2": "flushed (512 MB write) before every timed step",
+                   "inputs": "reference generator (bit-identical numpy streams), PE from GPU precompute"},
+        "roofline": roof,
+        "kernels_ms_per_step": {"agg": round(agg["ms"] / args.steps, 4), "gemm": round(gemm["ms"] / args.steps, 4),
+                                "finalize": round(fin["ms"] / args.steps, 4)},
+        "gemm_tflops": round(gemm["flops"] / (gemm["ms"] / 1e3) / 1e12, 2) if gemm["ms"] > 0 else None,
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def _read_prof(lib, eng, nat, cls):
+    import ctypes as C
+
+    ms, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+    nat.check(lib.ob_profile_read(eng._h, cls, C.byref(ms), C.byref(n), C.byref(by), C.byref(fl)))
+    return {"ms": ms.value, "n": n.value, "bytes": by.value, "flops": fl.value}
+
+
+if __name__ == "__main__":
+    main()

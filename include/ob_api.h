@@ -20,6 +20,8 @@
  *   ob_last_block_sizes   ComputationBlock sizes (parity hook)       compgraph.py:33-57
  *   ob_last_block         ComputationBlock arrays (parity hook)      compgraph.py:33-57
  *   ob_nccl_unique_id     bootstrap for one-process-per-GPU CGP      collectives.py:94-137 (World)
+ *   ob_reserve / ob_profile / ob_profile_read   measurement support (no reference counterpart;
+ *                         the reference only has perf_counter phase timers, runtime.py:312-334)
  *
  * Status -> Python exception mapping:
  *   OB_EINVAL -> ValueError, OB_ENOTFOUND -> KeyError, OB_ECOMM -> TransportError,
@@ -144,6 +146,21 @@ int ob_last_block_sizes(ob_engine* e, int32_t partition, int32_t layer, int64_t*
 int ob_last_block(ob_engine* e, int32_t partition, int32_t layer, int64_t* src_ids,
                   int64_t* dst_ids, int64_t* edge_src, int64_t* edge_dst, uint8_t* bind_kind,
                   int32_t* bind_pe_layer, int64_t* src_degree, int64_t* dst_self_src);
+
+/* Size the request workspace for batches up to (num_queries, num_edges) so
+ * later serves never allocate (bench warm-up). */
+int ob_reserve(ob_engine* e, int32_t num_queries, int64_t num_edges);
+
+/* In-library kernel profiler: CUDA events around the hot launches on the
+ * engine stream.  enable != 0 resets the records.  ob_profile_read sums the
+ * launches of one class since enabling: device time, count, algorithmic bytes
+ * (aggregation: 4*E + 4*w*S + 4*pw*items; finalize: partials in + rows out;
+ * gemm: operands + result) and flops (gemm). */
+enum ob_prof_class { OB_PROF_AGG = 0, OB_PROF_GEMM = 1, OB_PROF_FINALIZE = 2, OB_PROF_BUILD = 3,
+                     OB_PROF_SELECT = 4, OB_PROF_RESOLVE = 5, OB_PROF_REQUEST = 6 };
+int ob_profile(ob_engine* e, int32_t enable);
+int ob_profile_read(ob_engine* e, int32_t kernel_class, double* total_ms, int64_t* launches,
+                    double* alg_bytes, double* flops);
 
 /* Partition map of a CGP engine (owner per node), for parity checks. */
 int ob_partition_owner(ob_engine* e, int64_t* owner);

@@ -81,6 +81,10 @@ _SIGS = {
     "ob_last_plan": (C.c_int, [_P, _I64P, _I64P, _P, _P, _P, _P, _P]),
     "ob_last_block_sizes": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P, _I64P, _I64P]),
     "ob_last_block": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ob_reserve": (C.c_int, [_P, C.c_int32, C.c_int64]),
+    "ob_profile": (C.c_int, [_P, C.c_int32]),
+    "ob_profile_read": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), _I64P, C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double)]),
     "ob_partition_owner": (C.c_int, [_P, _P]),
     "ob_launch_count": (C.c_int64, [_P]),
     "ob_nccl_unique_id": (C.c_int, [_P]),

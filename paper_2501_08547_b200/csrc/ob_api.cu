@@ -233,6 +233,8 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   w.qfeat = d_q;
   const int k = (int)e.layers.size();
   const bool srpe = e.cfg.strategy != OB_STRATEGY_FULL;
+  g_prof = e.prof.on ? &e.prof : nullptr;
+  cudaEvent_t preq = prof_begin(s);
   OB_CUDA(cudaEventRecord(e.ev[0], s));
   OB_CUDA(cudaMemsetAsync(w.rc, 0, sizeof(ReqCounters), s));
   for (auto& b : w.blocks) OB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(BlockCounters), s));
@@ -245,6 +247,9 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   // per-layer fetch counters live in per-layer copies of the block counters
   stage_forward(e, w, d_out);
   OB_CUDA(cudaEventRecord(e.ev[2], s));
+  prof_end(s, preq, kProfRequest, nullptr, 0, 0, 0, 0, 0);
+  if (g_prof) g_prof->request_end(s);
+  g_prof = nullptr;
   e.have_request = true;
   if (!bd) return;
   PinnedReadback hb{};
@@ -677,6 +682,68 @@ int ob_last_block(ob_engine* h, int32_t part, int32_t layer, int64_t* src_ids, i
       cudaFree(dp);
       cudaFree(dd);
     }
+  });
+}
+
+int ob_reserve(ob_engine* h, int32_t B, int64_t m) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    check_ready(e);
+    prepare_workspace(e, B, m);
+    const int H = e.layers.back().spec.out_dim;
+    ensure(h->d_edges, h->cap_edges, (size_t)(2 * m));
+    ensure(h->d_q, h->cap_q, (size_t)B * e.g.F);
+    ensure(h->d_out, h->cap_out, (size_t)B * H);
+  });
+}
+
+int ob_profile(ob_engine* h, int32_t enable) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    OB_CUDA(cudaStreamSynchronize(h->impl.stream));
+    h->impl.prof.reset();
+    h->impl.prof.on = enable != 0;
+  });
+}
+
+int ob_profile_read(ob_engine* h, int32_t cls, double* total_ms, int64_t* launches, double* alg_bytes,
+                    double* flops) {
+  return guarded([&] {
+    OB_CHECK(h && total_ms && launches && alg_bytes && flops, OB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CUDA(cudaStreamSynchronize(e.stream));
+    double ms = 0, by = 0, fl = 0;
+    int64_t n = 0;
+    for (const ProfRec& r : e.prof.recs) {
+      if (r.cls != cls) continue;
+      float t = 0;
+      OB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      ms += t;
+      ++n;
+      if (r.slot < 0) continue;
+      const BlockCounters& c = e.prof.pinned[r.slot];
+      if (cls == kProfAgg) {
+        // edge list + every source row once + partial rows out
+        by += 4.0 * c.E + 4.0 * r.width * c.S + 4.0 * r.pw * c.items;
+      } else if (cls == kProfFinalize) {
+        by += 4.0 * r.pw * c.items + 4.0 * r.width * c.D;
+      } else if (cls == kProfGemm) {
+        double M = r.gemm_rows ? c.S : c.D;
+        fl += 2.0 * M * r.K * r.Nc;
+        by += 4.0 * (M * r.K + (double)r.K * r.Nc + M * r.Nc);
+      }
+    }
+    *total_ms = ms;
+    *launches = n;
+    *alg_bytes = by;
+    *flops = fl;
   });
 }
 

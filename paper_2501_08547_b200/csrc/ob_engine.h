@@ -145,6 +145,38 @@ struct RequestWs {
   int64_t words_N = 0, words_NB = 0;
 };
 
+// in-library kernel profiler (CUDA events on the launching stream) -------------
+// Used by bench.py to time the dominant kernel live inside the timed region.
+enum ProfClass { kProfAgg = 0, kProfGemm = 1, kProfFinalize = 2, kProfBuild = 3, kProfSelect = 4,
+                 kProfResolve = 5, kProfRequest = 6, kProfClasses = 7 };
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  int slot;           // pinned snapshot of the block counters (-1: none)
+  int width, pw;      // aggregation row width / partial width
+  int K, Nc;          // gemm shape (M from the counters)
+  int gemm_rows;      // 0 = D, 1 = S
+};
+
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  std::vector<ProfRec> recs;
+  BlockCounters* pinned = nullptr;  // snapshot slots
+  int nslots = 0, used_slots = 0;
+  std::vector<std::pair<const BlockCounters*, int>> pending;  // this request's snapshots
+  cudaEvent_t take();
+  int slot_for(const BlockCounters* d);
+  void request_end(cudaStream_t s);
+  void reset();
+};
+extern Profiler* g_prof;
+cudaEvent_t prof_begin(cudaStream_t s);
+void prof_end(cudaStream_t s, cudaEvent_t a, int cls, const BlockCounters* cnt, int width, int pw, int K, int Nc,
+              int gemm_rows);
+
 // stage entry points ---------------------------------------------------------
 struct Engine;
 
@@ -187,6 +219,7 @@ struct Engine {
   bool have_request = false;
   cudaEvent_t ev[6] = {};
   int64_t launches_at_start = 0;
+  Profiler prof;
   std::vector<void*> owned;      // device allocations to free
   void* dalloc(size_t bytes) {
     void* p = nullptr;

@@ -494,21 +494,27 @@ static void launch_agg(cudaStream_t s, const AggArgs& a, int64_t items_max) {
   // and rows are width*4 bytes apart, so width % VEC == 0 suffices.
   int slice = 32 * vec * kAggNV;
   dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a.width + slice - 1) / slice);
+  cudaEvent_t pa = prof_begin(s);
   if (vec == 4) k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a);
   else if (vec == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a);
   else k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a);
   OB_LAUNCHED();
+  prof_end(s, pa, kProfAgg, a.cnt, a.width, a.pw, 0, 0, 0);
 }
 
 static void finalize(cudaStream_t s, FinArgs f, int64_t D_max) {
+  cudaEvent_t pa = prof_begin(s);
   k_finalize<<<grid_for(D_max * f.width, 256), 256, 0, s>>>(f);
   OB_LAUNCHED();
+  prof_end(s, pa, kProfFinalize, f.cnt, f.width, f.pw, 0, 0, 0);
 }
 
-static void gemm(cudaStream_t s, const GemmArgs& g, int64_t M_max) {
+static void gemm(cudaStream_t s, const GemmArgs& g, int64_t M_max, const BlockCounters* cnt = nullptr) {
   int64_t tiles = ((M_max + GBM - 1) / GBM) * ((g.Nc + GBN - 1) / GBN);
+  cudaEvent_t pa = prof_begin(s);
   k_gemm<<<grid_for(tiles, 1, kNumSMs * 4), 256, 0, s>>>(g);
   OB_LAUNCHED();
+  prof_end(s, pa, kProfGemm, cnt, 0, 0, g.K1 + g.K2, g.Nc, (cnt && g.M_dev == &cnt->S) ? 1 : 0);
 }
 
 void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc, float* out) {
@@ -539,7 +545,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   if (sp.kind == OB_KIND_GAT) {
     // z = X @ W over every source row, then scores and the edge softmax
     GemmArgs g{r.S_dev, r.x, nullptr, in, nullptr, 0, L.w, outd, sc.z, false};
-    gemm(s, g, r.S_max);
+    gemm(s, g, r.S_max, r.cnt);
     k_rowdot<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, sc.z, nullptr, outd, L.a_src, sc.s_src);
     k_rowdot<<<grid_for(r.D_max, 8), 256, 0, s>>>(r.D_dev, sc.z, r.self, outd, L.a_dst, sc.s_dst);
     g_launches += 2;
@@ -599,7 +605,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     g.K2 = in;
     g.W = L.wcat;
   }
-  gemm(s, g, r.D_max);
+  gemm(s, g, r.D_max, r.cnt);
 }
 
 // ---------------------------------------------------------------------------
