@@ -107,6 +107,7 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.rq_ptr = a.take<int64_t>(p.RB_max + 1);
   w.rq_src = a.take<int32_t>(m + 1);
   w.big_list = a.take<int32_t>(p.RB_max + 1);
+  w.big_cptr = a.take<int64_t>(p.RB_max + 2);
   w.sort_tmp = a.take<int32_t>(m + 1);
   w.sbits = a.take<uint32_t>(p.words_NB + 1);
   w.swpre = a.take<int64_t>(p.words_NB + 1);
@@ -136,20 +137,23 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     w.block_of_layer[l - 1] = (e.cfg.strategy == OB_STRATEGY_FULL) ? l - 1 : (l < k ? 0 : 1);
   w.rowp = a.take<const float*>(Smax);
   w.gscale = a.take<float>(Smax);
-  bool gat = false, mom = false;
+  bool gat = false, mom = false, wide = false;
   for (auto& L : e.layers) {
     gat |= L.spec.kind == OB_KIND_GAT;
     mom |= L.spec.kind == OB_KIND_MOMENTS;
+    wide |= L.spec.kind == OB_KIND_GAT || L.transform_first;
   }
-  w.partial = a.take<float>(Imax * (maxw + 2) * (mom ? 2 : 1));  // moments partials are float64
-  w.agg = a.take<float>(Dmax * maxw);
-  w.mean = mom ? a.take<float>(2 * Dmax * maxw) : nullptr;
-  w.z = gat ? a.take<float>(Smax * maxw) : nullptr;
+  const int64_t wl = ld4(maxw) + 4;
+  w.qpad = a.take<float>((int64_t)B * e.g.F_ld + 4);
+  w.partial = a.take<float>(Imax * wl * (mom ? 2 : 1));  // moments partials are float64
+  w.agg = a.take<float>(Dmax * wl);
+  w.mean = mom ? a.take<float>(2 * Dmax * wl) : nullptr;
+  w.z = wide ? a.take<float>(Smax * wl) : nullptr;
   w.s_src = gat ? a.take<float>(Smax) : nullptr;
   w.s_dst = gat ? a.take<float>(Dmax) : nullptr;
   for (int l = 1; l < k; ++l) {
     const BlockDev& b = w.blocks[w.block_of_layer[l - 1]];
-    w.outs[l] = a.take<float>(b.D_max * e.layers[l - 1].spec.out_dim);
+    w.outs[l] = a.take<float>(b.D_max * ld4(e.layers[l - 1].spec.out_dim));
   }
   int64_t tiles = p.max_scan_n / kScanTile + 2;
   e.scan.tile_sums = a.take<int64_t>(tiles + 1);
@@ -314,11 +318,16 @@ static void load_graph(Engine& e, int64_t N, const int64_t* off, const int64_t* 
   g.offsets = (int64_t*)e.dalloc(sizeof(int64_t) * (N + 1));
   g.nbrs = (int32_t*)e.dalloc(sizeof(int32_t) * std::max<int64_t>(E, 1));
   g.indeg = (int32_t*)e.dalloc(sizeof(int32_t) * N);
-  g.feats = (float*)e.dalloc(sizeof(float) * std::max<int64_t>(N * F, 1));
+  g.F_ld = ld4(std::max(F, 1));
+  g.feats = (float*)e.dalloc(sizeof(float) * std::max<int64_t>(N * g.F_ld, 1));
   OB_CUDA(cudaMemcpy(g.offsets, off, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice));
   if (E) OB_CUDA(cudaMemcpy(g.nbrs, nbrs32.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice));
   OB_CUDA(cudaMemcpy(g.indeg, deg.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
-  if (N * F) OB_CUDA(cudaMemcpy(g.feats, feats, sizeof(float) * N * F, cudaMemcpyHostToDevice));
+  // rows padded to 16 B for cp.async / float4 staging
+  OB_CUDA(cudaMemset(g.feats, 0, sizeof(float) * N * g.F_ld));
+  if (N * F)
+    OB_CUDA(cudaMemcpy2D(g.feats, sizeof(float) * g.F_ld, feats, sizeof(float) * F, sizeof(float) * F, N,
+                         cudaMemcpyHostToDevice));
   std::sort(deg.begin(), deg.end(), std::greater<int32_t>());
   g.topdeg_prefix.assign((size_t)N + 1, 0);
   for (int64_t i = 0; i < N; ++i) g.topdeg_prefix[i + 1] = g.topdeg_prefix[i] + deg[i];
@@ -343,24 +352,26 @@ static void load_model(Engine& e, int k, const ob_layer* layers, const float* co
     if (l) OB_CHECK(layers[l - 1].out_dim == sp.in_dim, OB_EINVAL, "adjacent layer dimensions do not chain");
     if (sp.kind == OB_KIND_POWER_MEAN) OB_CHECK(sp.p != 0.f, OB_EINVAL, "power_mean needs p != 0");
     if (sp.kind == OB_KIND_MOMENTS) OB_CHECK(sp.n >= 2, OB_EINVAL, "moments needs n >= 2");
+    OB_CHECK(sp.out_dim <= 256, OB_EINVAL, "layer out_dim above 256 is not supported");
     LayerDev& L = out[l];
     L.spec = sp;
-    const size_t mat = (size_t)sp.in_dim * sp.out_dim;
+    const int in = sp.in_dim, o = sp.out_dim;
+    // narrowing linear layers aggregate X W instead of X (fewer gathered bytes)
+    L.transform_first = (sp.kind == OB_KIND_GCN || sp.kind == OB_KIND_SAGE_MEAN) && in > o;
     if (sp.kind == OB_KIND_GCN) {
-      L.w = (float*)e.dalloc(sizeof(float) * mat);
-      OB_CUDA(cudaMemcpy(L.w, mats[mi], sizeof(float) * mat, cudaMemcpyHostToDevice));
+      prep_tc_weights(e, {mats[mi]}, {in}, o, &L.tw_main);
     } else if (sp.kind == OB_KIND_GAT) {
-      L.w = (float*)e.dalloc(sizeof(float) * mat);
-      L.a_src = (float*)e.dalloc(sizeof(float) * sp.out_dim);
-      L.a_dst = (float*)e.dalloc(sizeof(float) * sp.out_dim);
-      OB_CUDA(cudaMemcpy(L.w, mats[mi], sizeof(float) * mat, cudaMemcpyHostToDevice));
-      OB_CUDA(cudaMemcpy(L.a_src, mats[mi + 1], sizeof(float) * sp.out_dim, cudaMemcpyHostToDevice));
-      OB_CUDA(cudaMemcpy(L.a_dst, mats[mi + 2], sizeof(float) * sp.out_dim, cudaMemcpyHostToDevice));
+      prep_tc_weights(e, {mats[mi]}, {in}, o, &L.tw_main);
+      L.a_src = (float*)e.dalloc(sizeof(float) * o);
+      L.a_dst = (float*)e.dalloc(sizeof(float) * o);
+      OB_CUDA(cudaMemcpy(L.a_src, mats[mi + 1], sizeof(float) * o, cudaMemcpyHostToDevice));
+      OB_CUDA(cudaMemcpy(L.a_dst, mats[mi + 2], sizeof(float) * o, cudaMemcpyHostToDevice));
+    } else if (L.transform_first) {
+      prep_tc_weights(e, {mats[mi + 1]}, {in}, o, &L.tw_main);  // X W_neigh
+      prep_tc_weights(e, {mats[mi]}, {in}, o, &L.tw_self);      // h_v W_self (+ mean(X W_neigh))
     } else {
-      // [W_self; W_neigh] stacked so the update is one GEMM over [h_v | agg]
-      L.wcat = (float*)e.dalloc(sizeof(float) * 2 * mat);
-      OB_CUDA(cudaMemcpy(L.wcat, mats[mi], sizeof(float) * mat, cudaMemcpyHostToDevice));
-      OB_CUDA(cudaMemcpy(L.wcat + mat, mats[mi + 1], sizeof(float) * mat, cudaMemcpyHostToDevice));
+      // [W_self; W_neigh] so the update is one GEMM over [h_v | agg]
+      prep_tc_weights(e, {mats[mi], mats[mi + 1]}, {in, in}, o, &L.tw_main);
     }
     mi += nmats(sp.kind);
   }
@@ -501,8 +512,11 @@ int ob_load_pe(ob_engine* h, int32_t layer, const float* rows, int64_t n, int32_
       e.pe.resize(layer, nullptr);
       e.pe_dim.resize(layer, 0);
     }
-    float* d = (float*)e.dalloc(sizeof(float) * n * dim);
-    OB_CUDA(cudaMemcpy(d, rows, sizeof(float) * n * dim, cudaMemcpyHostToDevice));
+    const int ld = ld4(dim);
+    float* d = (float*)e.dalloc(sizeof(float) * n * ld);
+    OB_CUDA(cudaMemset(d, 0, sizeof(float) * n * ld));
+    OB_CUDA(cudaMemcpy2D(d, sizeof(float) * ld, rows, sizeof(float) * dim, sizeof(float) * dim, n,
+                         cudaMemcpyHostToDevice));
     e.pe[layer - 1] = d;
     e.pe_dim[layer - 1] = dim;
   });
@@ -537,7 +551,9 @@ int ob_read_pe(ob_engine* h, int32_t layer, float* out) {
     OB_CUDA(cudaSetDevice(e.cfg.device));
     OB_CHECK(layer >= 1 && layer <= (int)e.pe.size() && e.pe[layer - 1], OB_EINVAL,
              "no stored embeddings for that layer");
-    OB_CUDA(cudaMemcpy(out, e.pe[layer - 1], sizeof(float) * e.g.N * e.pe_dim[layer - 1], cudaMemcpyDeviceToHost));
+    const int dim = e.pe_dim[layer - 1];
+    OB_CUDA(cudaMemcpy2D(out, sizeof(float) * dim, e.pe[layer - 1], sizeof(float) * ld4(dim), sizeof(float) * dim,
+                         e.g.N, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -40,7 +40,8 @@ struct ReqCounters {
   int64_t sel_gt;      // keys strictly above the threshold
   int64_t sel_eq_take; // threshold-equal keys to take (lowest ids first)
   int64_t fetch_feat_rows;
-  int64_t pad[4];
+  int64_t n_chunks;    // 4096-element sort chunks over the long segments
+  int64_t pad[3];
 };
 
 struct BlockCounters {
@@ -65,23 +66,68 @@ struct BlockDev {
   BlockCounters host{};
 };
 
+// Every row table in HBM uses a row stride padded to 4 floats (16 B) so rows
+// can be staged with 16-byte cp.async and read with float4 vectors.
+inline int ld4(int w) { return (w + 3) & ~3; }
+
+// A row source: per-row pointers (gathered inputs) or a dense strided matrix.
+struct RowSrc {
+  const float* const* rowp;
+  const float* base;
+  int64_t ld;
+  __device__ __forceinline__ const float* row(int64_t s) const { return rowp ? rowp[s] : base + s * ld; }
+};
+
+// Weights staged for the tensor-core GEMM: B^T (Np x Kp, K-major, zero padded)
+// plus its 3xTF32 low part; K is the concatenation of 32-padded segments.
+struct TcWeights {
+  float* hi = nullptr;
+  float* lo = nullptr;
+  int N = 0, Np = 0, Kp = 0;
+};
+
+struct TcGemmArgs {
+  const int64_t* M_dev;   // rows (device count)
+  RowSrc a1;              // A1 rows (gathered), K1 wide
+  const int32_t* self;    // A1 row index per output row (null = identity)
+  int K1;
+  const float* a2;        // dense A2 [M][lda2], K2 wide
+  int64_t lda2;
+  int K2;
+  const float* Bt;
+  const float* Bt_lo;
+  int N, Np;
+  float* C;
+  int64_t ldc;
+  const float* E;         // optional addend [M][lde] (before the activation)
+  int64_t lde;
+  bool relu;
+};
+
 struct LayerDev {
   ob_layer spec{};
-  float* w = nullptr;       // gcn/gat: W [in x out]
-  float* wcat = nullptr;    // sage/power/moments: [W_self; W_neigh] [(2 in) x out]
   float* a_src = nullptr;   // gat
   float* a_dst = nullptr;   // gat
+  bool transform_first = false;  // gcn / sage_mean with in > out: aggregate X W instead of X
+  TcWeights tw_main;        // aggregate-first update ([W_self; W_neigh] or W) / gcn-gat W / tf: W_neigh
+  TcWeights tw_self;        // transform-first sage_mean: W_self
 };
 
 struct GraphDev {
   int64_t N = 0, E = 0;
   int F = 0;
+  int F_ld = 0;             // padded feature row stride
   int64_t* offsets = nullptr;
   int32_t* nbrs = nullptr;
   int32_t* indeg = nullptr;
-  float* feats = nullptr;
+  float* feats = nullptr;   // N x F_ld
   std::vector<int64_t> topdeg_prefix;  // host: prefix sums of in-degrees sorted descending
 };
+
+void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max);
+struct Engine;
+void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std::vector<int>& seg_k, int N,
+                     TcWeights* out);
 
 // Bump allocator over one device allocation (reset per request).
 struct Arena {
@@ -103,7 +149,8 @@ struct RequestWs {
   int64_t m = 0;
   ReqCounters* rc = nullptr;
   const int64_t* edges = nullptr;  // device [m][2]
-  const float* qfeat = nullptr;    // device [B][F]
+  const float* qfeat = nullptr;    // device [B][F] as given
+  float* qpad = nullptr;           // device [B][F_ld] staged copy (16 B aligned rows)
   int32_t* qdeg = nullptr;         // [B] request in-degree per query
   // candidate set (bitmap-rank over [0, N))
   uint32_t* cbits = nullptr;
@@ -123,6 +170,7 @@ struct RequestWs {
   int64_t* rq_ptr = nullptr;       // [RB+1]
   int32_t* rq_src = nullptr;       // [m] sources, ascending within a slot after sort
   int32_t* big_list = nullptr;     // segments for the CTA sort
+  int64_t* big_cptr = nullptr;     // chunk prefix over big_list
   int32_t* sort_tmp = nullptr;     // [m] scratch for the big-segment merge
   // block scratch
   uint32_t* sbits = nullptr;       // source bitmap over [0, N+B)
@@ -136,9 +184,9 @@ struct RequestWs {
   const float** rowp = nullptr;    // [S_max] input row per source
   float* gscale = nullptr;         // [S_max] gcn source normaliser
   float* partial = nullptr;        // [items_max][w + 2]
-  float* agg = nullptr;            // [D_max][in]
-  float* outs[8] = {};             // per-layer outputs [D_l][out]
-  float* z = nullptr;              // gat: [S_max][out]
+  float* agg = nullptr;            // [D_max][ld4(w)]
+  float* outs[8] = {};             // per-layer outputs [D_l][ld4(out)]
+  float* z = nullptr;              // gat / transform-first: [S_max][ld4(out)]
   float* s_src = nullptr;          // gat: [S_max]
   float* s_dst = nullptr;          // gat: [D_max]
   float* mean = nullptr;           // moments: [D_max][in]
@@ -211,7 +259,7 @@ struct Engine {
   bool own_stream = false;
   GraphDev g;
   std::vector<LayerDev> layers;
-  std::vector<float*> pe;        // per stored layer, N x dim
+  std::vector<float*> pe;        // per stored layer, N x ld4(dim)
   std::vector<int> pe_dim;
   Arena arena;
   ScanScratch scan;

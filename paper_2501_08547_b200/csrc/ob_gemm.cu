@@ -1,0 +1,349 @@
+// ob_gemm.cu -- dense layer transforms on the 5th-gen tensor cores (tcgen05).
+//
+// C[M x N] = epi( [A1 | A2] @ B ), M device-resident, K = K1 + K2, N <= 256.
+//   A1 rows are gathered through per-row pointers (features / query features /
+//   stored embeddings / previous layer rows -- never materialised), A2 rows are
+//   a dense matrix (the aggregation result).
+//
+// Precision: the reference accumulates in float64 (models.py:214-228) and the
+// parity bar is 1e-4 relative in fp32, which single-pass TF32 (10-bit mantissa)
+// misses.  We use the 3xTF32 split: A = A_hi + A_lo, B = B_hi + B_lo, and
+// D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in an fp32 TMEM tile.  The
+// tensor core truncates fp32 operands to TF32, so the raw fp32 tile *is* A_hi;
+// A_lo = a - trunc(a) is formed in shared memory per k-block, B_lo is prepared
+// once at model load (weights are static).
+//
+// Structure (one CTA per SM, persistent over 128-row tiles):
+//   * 128 threads stage A/B k-blocks (32 fp32 = one 128-byte row) with cp.async
+//     into the canonical K-major SWIZZLE_128B layout, 3-stage ring;
+//   * one elected thread issues 12 tcgen05.mma.kind::tf32 (3 products x 4 K=8
+//     steps) per k-block and tcgen05.commit's an mbarrier per stage;
+//   * epilogue: tcgen05.ld 32x32b -> registers -> activation -> global.
+#include <algorithm>
+#include <cstring>
+
+#include "ob_engine.h"
+
+namespace ob {
+
+namespace {
+
+constexpr int kTcThreads = 128;
+constexpr int kTcBM = 128;
+constexpr int kTcBK = 32;  // fp32 per k-block: one 128-byte swizzle row
+constexpr int kTileA = kTcBM * kTcBK * 4;  // 16 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (sm_100 "version 1")
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);  // start address
+  d |= (uint64_t)1 << 16;                   // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;         // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                   // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;                   // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: fp32 accumulate, K-major A and B, M = 128
+__host__ __device__ constexpr uint32_t tf32_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+}  // namespace
+
+// Shared-memory budget per stage: A, A_lo (16 KB each) + B, B_lo (Np x 128 B each)
+template <int NP>
+struct TcSmem {
+  static constexpr int kTileB = NP * kTcBK * 4;
+  static constexpr int kStage = 2 * kTileA + 2 * kTileB;
+  static constexpr int kStages = (3 * kStage <= 200 * 1024) ? 3 : 2;
+  static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 256 /*bars, rows*/ + kTcBM * 8;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
+  using SM = TcSmem<NP>;
+  constexpr int S = SM::kStages;
+  constexpr uint32_t kCols = NP <= 32 ? 32 : (NP <= 64 ? 64 : (NP <= 128 ? 128 : 256));
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + S * SM::kStage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S + 1);
+  const float** rows = reinterpret_cast<const float**>(base + S * SM::kStage + 256);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t M = *g.M_dev;
+  const int64_t tiles = (M + kTcBM - 1) / kTcBM;
+  const int KB1 = (g.K1 + kTcBK - 1) / kTcBK, KB2 = (g.K2 + kTcBK - 1) / kTcBK, KB = KB1 + KB2;
+  const int Kp = KB * kTcBK;
+
+  if (tid == 0) {
+    for (int i = 0; i < S + 1; ++i) mbar_init(bars + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = tf32_idesc(NP);
+
+  uint32_t it = 0;  // global k-block counter across tiles (stage / phase bookkeeping)
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t m0 = tile * kTcBM;
+    // per-tile A1 row pointers
+    {
+      const int64_t r = m0 + tid;
+      const float* p = nullptr;
+      if (r < M && g.K1) p = g.a1.row(g.self ? (int64_t)g.self[r] : r);
+      rows[tid] = p;
+    }
+    __syncthreads();
+
+    auto load = [&](int kb, int stage) {
+      uint8_t* sA = base + stage * SM::kStage;
+      uint8_t* sB = sA + 2 * kTileA;
+      uint8_t* sBl = sB + SM::kTileB;
+      const uint32_t a_s = smem_u32(sA), b_s = smem_u32(sB), bl_s = smem_u32(sBl);
+      const bool first = kb < KB1;
+      const int k0 = (first ? kb : kb - KB1) * kTcBK;
+      const int Kv = first ? g.K1 : g.K2;
+#pragma unroll
+      for (int i = 0; i < (kTcBM * 8) / kTcThreads; ++i) {
+        const int q = tid + i * kTcThreads;
+        const int r = q >> 3, c = q & 7;
+        const int k = k0 + c * 4;
+        const float* src = nullptr;
+        int bytes = 0;
+        if (m0 + r < M) {
+          const float* rowp = first ? rows[r] : g.a2 + (m0 + r) * g.lda2;
+          int rem = Kv - k;
+          bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
+          src = rowp + (bytes ? k : 0);
+        }
+        if (!src) src = g.Bt;  // any valid address; 0 bytes are read
+        cp_async16(a_s + r * 128 + ((c ^ (r & 7)) << 4), src, bytes);
+      }
+#pragma unroll
+      for (int i = 0; i < (NP * 8) / kTcThreads; ++i) {
+        const int q = tid + i * kTcThreads;
+        const int n = q >> 3, c = q & 7;
+        const int64_t off = (int64_t)n * Kp + kb * kTcBK + c * 4;
+        const uint32_t so = n * 128 + ((c ^ (n & 7)) << 4);
+        cp_async16(b_s + so, g.Bt + off, 16);
+        cp_async16(bl_s + so, g.Bt_lo + off, 16);
+      }
+    };
+
+    // prologue
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) {
+      if (s < KB) load(s, (it + s) % S);
+      cp_async_commit();
+    }
+    for (int kb = 0; kb < KB; ++kb) {
+      const uint32_t gk = it + kb;
+      const int stage = gk % S;
+      cp_async_wait<S - 2>();
+      __syncthreads();
+      // A_lo = a - trunc_tf32(a) (the raw tile doubles as A_hi: the MMA truncates)
+      {
+        float* a = reinterpret_cast<float*>(base + stage * SM::kStage);
+        float* alo = a + kTcBM * kTcBK;
+#pragma unroll 8
+        for (int i = tid; i < kTcBM * kTcBK; i += kTcThreads) {
+          float v = a[i];
+          alo[i] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        }
+      }
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        uint8_t* sA = base + stage * SM::kStage;
+        const uint32_t a_s = smem_u32(sA), alo_s = a_s + kTileA;
+        const uint32_t b_s = a_s + 2 * kTileA, blo_s = b_s + SM::kTileB;
+#pragma unroll
+        for (int kk = 0; kk < kTcBK / 8; ++kk) {
+          const uint32_t off = kk * 32;  // 8 tf32 per MMA
+          const uint64_t da = sw128_desc(a_s + off), dal = sw128_desc(alo_s + off);
+          const uint64_t db = sw128_desc(b_s + off), dbl = sw128_desc(blo_s + off);
+          const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+          mma_tf32(tmem, da, db, idesc, acc0);
+          mma_tf32(tmem, da, dbl, idesc, 1u);
+          mma_tf32(tmem, dal, db, idesc, 1u);
+        }
+        mma_commit(bars + stage);
+      }
+      // refill the stage consumed by the previous k-block once its MMAs retired
+      const int nk = kb + S - 1;
+      if (nk < KB) {
+        const uint32_t gprev = gk + S - 1 - S;  // == gk - 1: last user of stage (gk + S - 1) % S
+        if (kb > 0) mbar_wait(bars + (gprev % S), (gprev / S) & 1);
+        load(nk, (gk + S - 1) % S);
+      }
+      cp_async_commit();
+    }
+    // accumulator complete when the last k-block's commit lands
+    {
+      const uint32_t glast = it + KB - 1;
+      mbar_wait(bars + (glast % S), (glast / S) & 1);
+    }
+    it += KB;
+    tc_fence_after();
+    // epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows
+    const int64_t row = m0 + warp * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < NP; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      if (row < M) {
+        float* crow = g.C + row * g.ldc;
+        const float* erow = g.E ? g.E + row * g.lde : nullptr;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = c0 + j;
+          if (col < g.N) {
+            float o = v[j];
+            if (erow) o += erow[col];
+            if (g.relu) o = fmaxf(o, 0.f);
+            crow[col] = o;
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+  }
+}
+
+void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max) {
+  OB_CHECK(g.N >= 1 && g.N <= 256, OB_ESTATE, "tc_gemm: N out of range");
+  const int64_t tiles = (M_max + kTcBM - 1) / kTcBM;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs));
+  const int np = g.Np;
+  auto go = [&](auto kern, int bytes) {
+    static bool configured[4] = {false, false, false, false};
+    int slot = np <= 32 ? 0 : np <= 64 ? 1 : np <= 128 ? 2 : 3;
+    if (!configured[slot]) {
+      OB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      configured[slot] = true;
+    }
+    kern<<<grid, kTcThreads, bytes, s>>>(g);
+  };
+  if (np == 32) go(k_tc_gemm<32>, TcSmem<32>::kBytes);
+  else if (np == 64) go(k_tc_gemm<64>, TcSmem<64>::kBytes);
+  else if (np == 128) go(k_tc_gemm<128>, TcSmem<128>::kBytes);
+  else if (np == 256) go(k_tc_gemm<256>, TcSmem<256>::kBytes);
+  else throw Error(OB_ESTATE, "tc_gemm: padded N must be 32/64/128/256");
+  OB_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
+// weight preparation: W (K x N row-major) blocks -> Bt / Bt_lo (Np x Kp, K-major,
+// zero padded), K-blocks of each operand segment padded to 32
+// ---------------------------------------------------------------------------
+void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std::vector<int>& seg_k, int N,
+                     TcWeights* out) {
+  int Np = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  OB_CHECK(N <= 256, OB_EINVAL, "layer width above 256 is not supported by the tensor-core path");
+  int Kp = 0;
+  for (int k : seg_k) Kp += (k + kTcBK - 1) / kTcBK * kTcBK;
+  std::vector<float> hi((size_t)Np * Kp, 0.f), lo((size_t)Np * Kp, 0.f);
+  int kbase = 0;
+  for (size_t si = 0; si < segs.size(); ++si) {
+    const float* W = segs[si];
+    const int K = seg_k[si];
+    for (int k = 0; k < K; ++k)
+      for (int n = 0; n < N; ++n) {
+        float v = W[(size_t)k * N + n];
+        uint32_t b;
+        std::memcpy(&b, &v, 4);
+        b &= 0xFFFFE000u;
+        float h;
+        std::memcpy(&h, &b, 4);
+        hi[(size_t)n * Kp + kbase + k] = v;
+        lo[(size_t)n * Kp + kbase + k] = v - h;
+      }
+    kbase += (K + kTcBK - 1) / kTcBK * kTcBK;
+  }
+  out->N = N;
+  out->Np = Np;
+  out->Kp = Kp;
+  out->hi = (float*)e.dalloc(sizeof(float) * hi.size());
+  out->lo = (float*)e.dalloc(sizeof(float) * lo.size());
+  OB_CUDA(cudaMemcpy(out->hi, hi.data(), sizeof(float) * hi.size(), cudaMemcpyHostToDevice));
+  OB_CUDA(cudaMemcpy(out->lo, lo.data(), sizeof(float) * lo.size(), cudaMemcpyHostToDevice));
+}
+
+}  // namespace ob

@@ -10,7 +10,11 @@
 // prefix gives ascending order and an O(1) id -> candidate-rank map.  The
 // top-k is a radix select over the 64-bit score bit patterns (non-negative
 // doubles order like their bits) followed by an ordered compaction, so the
-// (score desc, id asc) order never needs a full sort.  Everything runs off
+// (score desc, id asc) order never needs a full sort.  Request edges are
+// bucketed by destination slot with shared-memory aggregation for the hot
+// query slots (every query receives hundreds of edges), then each bucket is
+// sorted: warp sorts for short buckets, and a chunked CTA radix sort plus
+// multi-CTA merge-path levels for long ones.  Everything runs off
 // device-side counts.
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
@@ -55,23 +59,54 @@ __global__ void k_fill_i64(int64_t* a, const int64_t* n_dev, int64_t n_host, int
   OB_GRID_STRIDE(i, n) a[i] = v;
 }
 
+// warp-aggregated atomicAdd of 1 on base[slot]; returns this lane's old value
+__device__ __forceinline__ int32_t warp_agg_inc(int32_t* base, int64_t slot) {
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, (unsigned long long)slot);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  int32_t old = 0;
+  if (lane == leader) old = atomicAdd(base + slot, __popc(peers));
+  old = __shfl_sync(peers, old, leader);
+  return old + __popc(peers & ((1u << lane) - 1u));
+}
+
 // ---------------------------------------------------------------------------
 // 1. validate + mark training endpoints + per-query in-degree
 // ---------------------------------------------------------------------------
-__global__ void k_request_mark(const int64_t* __restrict__ edges, int64_t m, int64_t N, int B,
-                               uint32_t* cbits, int32_t* qdeg, ReqCounters* rc) {
+constexpr int kEdgeTile = 4096;  // request edges per CTA pass
+constexpr int kMaxSmemQueries = 12288;
+
+__global__ void __launch_bounds__(256) k_request_mark(const int64_t* __restrict__ edges, int64_t m, int64_t N, int B,
+                                                      uint32_t* cbits, int32_t* qdeg, ReqCounters* rc) {
+  extern __shared__ int32_t sq[];  // per-CTA query in-degree histogram (B entries) when B fits
+  const bool smem = B <= kMaxSmemQueries;
   const int64_t hi = N + B;
   int64_t err = 0;
-  OB_GRID_STRIDE(e, m) {
-    int64_t s = edges[2 * e], d = edges[2 * e + 1];
-    if (s < 0 || s >= hi || d < 0 || d >= hi) {
-      err |= kErrRange;
-      continue;
+  for (int64_t t0 = (int64_t)blockIdx.x * kEdgeTile; t0 < m; t0 += (int64_t)gridDim.x * kEdgeTile) {
+    if (smem) {
+      for (int q = threadIdx.x; q < B; q += blockDim.x) sq[q] = 0;
+      __syncthreads();
     }
-    if (s < N && d < N) err |= kErrNoQuery;
-    if (s < N) bm_set(cbits, s);
-    if (d < N) bm_set(cbits, d);
-    else atomicAdd(qdeg + (d - N), 1);
+    const int64_t t1 = min(t0 + kEdgeTile, m);
+    for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
+      int64_t s = edges[2 * e], d = edges[2 * e + 1];
+      if (s < 0 || s >= hi || d < 0 || d >= hi) {
+        err |= kErrRange;
+        continue;
+      }
+      if (s < N && d < N) err |= kErrNoQuery;
+      if (s < N) bm_set(cbits, s);
+      if (d < N) bm_set(cbits, d);
+      else if (smem) atomicAdd(sq + (d - N), 1);
+      else atomicAdd(qdeg + (d - N), 1);
+    }
+    if (smem) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < B; q += blockDim.x)
+        if (sq[q]) atomicAdd(qdeg + q, sq[q]);
+      __syncthreads();
+    }
   }
   if (err) atomicOr((unsigned long long*)&rc->err, (unsigned long long)err);
 }
@@ -101,19 +136,24 @@ void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, 
   OB_LAUNCHED();
 }
 
-__global__ void k_slots_init(ReqCounters* rc, int B) { rc->RB = rc->R + B; }
-
-// request-CSR slot of a destination: candidate rank for training ids, R + q for queries
-__device__ __forceinline__ int64_t rq_slot(int64_t d, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
-                                           int64_t R) {
-  return d < N ? bm_rank(cbits, cwpre, d) : R + (d - N);
+// RB = R + B slots; query slots take their counts from the per-query in-degrees
+__global__ void k_slots_init(ReqCounters* rc, int B, const int32_t* qdeg, int32_t* rq_cnt, int32_t* rq_fill) {
+  const int64_t R = rc->R;
+  if (blockIdx.x == 0 && threadIdx.x == 0) rc->RB = R + B;
+  const int64_t RB = R + B;
+  OB_GRID_STRIDE(i, RB) {
+    rq_cnt[i] = i < R ? 0 : qdeg[i - R];
+    rq_fill[i] = 0;
+  }
 }
 
 __global__ void k_rq_count(const int64_t* __restrict__ edges, int64_t m, int64_t N, const uint32_t* cbits,
                            const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt) {
-  const int64_t R = rc->R;
   if (rc->err & (kErrRange | kErrNoQuery)) return;
-  OB_GRID_STRIDE(e, m) atomicAdd(rq_cnt + rq_slot(edges[2 * e + 1], N, cbits, cwpre, R), 1);
+  OB_GRID_STRIDE(e, m) {
+    int64_t d = edges[2 * e + 1];
+    if (d < N) warp_agg_inc(rq_cnt, bm_rank(cbits, cwpre, d));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -191,17 +231,6 @@ __global__ void __launch_bounds__(256) k_sel_pick(ReqCounters* rc, int shift, ui
   }
 }
 
-// 0 = not selected, 1 = selected; ties at the threshold go to the lowest ids
-struct SelFlagLoad {
-  const uint64_t* key;
-  const ReqCounters* rc;
-  __device__ int64_t operator()(int64_t c) const {
-    const int64_t R = rc->R, b = rc->budget;
-    if (b <= 0) return 0;
-    if (b >= R) return 1;
-    return key[c] > rc->sel_prefix ? 1 : 0;
-  }
-};
 struct EqLoad {
   const uint64_t* key;
   const ReqCounters* rc;
@@ -210,6 +239,7 @@ struct EqLoad {
     return (b > 0 && b < R && key[c] == rc->sel_prefix) ? 1 : 0;
   }
 };
+// selected = above the threshold, or at it among the lowest ids (score desc, id asc)
 struct EqStore {
   int32_t* flag;
   const uint64_t* key;
@@ -240,24 +270,57 @@ struct SelStore {
 };
 
 // ---------------------------------------------------------------------------
-// 3. request CSR fill + per-slot sort (sources ascending within a destination)
+// 3. request CSR fill: per-CTA reservation for query slots, warp-aggregated
+//    atomics for candidate slots
 // ---------------------------------------------------------------------------
-__global__ void k_rq_fill(const int64_t* __restrict__ edges, int64_t m, int64_t N, const uint32_t* cbits,
-                          const int64_t* cwpre, const ReqCounters* rc, const int64_t* rq_ptr, int32_t* rq_fill,
-                          int32_t* rq_src) {
-  const int64_t R = rc->R;
+__global__ void __launch_bounds__(256) k_rq_fill(const int64_t* __restrict__ edges, int64_t m, int64_t N, int B,
+                                                 const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc,
+                                                 const int64_t* rq_ptr, int32_t* rq_fill, int32_t* rq_src) {
+  extern __shared__ int32_t sm[];  // [B] counts, then [B] base offsets
+  const bool smem = B <= kMaxSmemQueries / 2;
   if (rc->err & (kErrRange | kErrNoQuery)) return;
-  OB_GRID_STRIDE(e, m) {
-    int64_t slot = rq_slot(edges[2 * e + 1], N, cbits, cwpre, R);
-    int64_t pos = rq_ptr[slot] + atomicAdd(rq_fill + slot, 1);
-    rq_src[pos] = (int32_t)edges[2 * e];
+  const int64_t R = rc->R;
+  int32_t* cnt = sm;
+  int32_t* base = sm + B;
+  for (int64_t t0 = (int64_t)blockIdx.x * kEdgeTile; t0 < m; t0 += (int64_t)gridDim.x * kEdgeTile) {
+    const int64_t t1 = min(t0 + kEdgeTile, m);
+    if (smem) {
+      for (int q = threadIdx.x; q < B; q += blockDim.x) cnt[q] = 0;
+      __syncthreads();
+      for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
+        int64_t d = edges[2 * e + 1];
+        if (d >= N) atomicAdd(cnt + (d - N), 1);
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < B; q += blockDim.x) {
+        base[q] = cnt[q] ? atomicAdd(rq_fill + R + q, cnt[q]) : 0;
+        cnt[q] = 0;
+      }
+      __syncthreads();
+    }
+    for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
+      int64_t s = edges[2 * e], d = edges[2 * e + 1];
+      int64_t pos;
+      if (d >= N) {
+        int64_t q = d - N;
+        pos = rq_ptr[R + q] + (smem ? base[q] + atomicAdd(cnt + q, 1) : atomicAdd(rq_fill + R + q, 1));
+      } else {
+        int64_t c = bm_rank(cbits, cwpre, d);
+        pos = rq_ptr[c] + warp_agg_inc(rq_fill, c);
+      }
+      rq_src[pos] = (int32_t)s;
+    }
+    if (smem) __syncthreads();
   }
 }
 
+// ---------------------------------------------------------------------------
+// 4. per-slot sort of request sources
+// ---------------------------------------------------------------------------
 constexpr int kWarpSortItems = 8;     // warp sort handles <= 256
-constexpr int kBlockSortThreads = 512;
-constexpr int kBlockSortItems = 16;   // CTA sort handles <= 8192 per chunk
-constexpr int kBlockSortTile = kBlockSortThreads * kBlockSortItems;
+constexpr int kChunkThreads = 512;
+constexpr int kChunkItems = 8;
+constexpr int kChunk = kChunkThreads * kChunkItems;  // 4096-element CTA sort tiles
 
 __device__ __forceinline__ void warp_bitonic32(int32_t& v) {
   const int lane = threadIdx.x & 31;
@@ -277,8 +340,8 @@ struct LessI32 {
   __device__ bool operator()(const int32_t& a, const int32_t& b) const { return a < b; }
 };
 
-__global__ void __launch_bounds__(256) k_segsort_warp(const int64_t* __restrict__ ptr, const ReqCounters* rc,
-                                                      int32_t* vals, int32_t* big_list, ReqCounters* rcw) {
+__global__ void __launch_bounds__(256) k_segsort_warp(const int64_t* __restrict__ ptr, ReqCounters* rc, int32_t* vals,
+                                                      int32_t* big_list) {
   using WS = cub::WarpMergeSort<int32_t, kWarpSortItems, 32>;
   __shared__ typename WS::TempStorage tmp[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -304,75 +367,117 @@ __global__ void __launch_bounds__(256) k_segsort_warp(const int64_t* __restrict_
         if (idx < len) vals[b + idx] = k[i];
       }
     } else if (lane == 0) {
-      int64_t at = atomicAdd((unsigned long long*)&rcw->n_big, 1ull);
+      int64_t at = atomicAdd((unsigned long long*)&rc->n_big, 1ull);
       big_list[at] = (int32_t)s;
     }
   }
 }
 
-// merge sorted runs a[0,na) and b[0,nb) into out with the whole CTA (merge path)
-__device__ void cta_merge(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, int32_t* out) {
-  const int64_t total = na + nb;
-  const int64_t per = (total + blockDim.x - 1) / blockDim.x;
-  int64_t d = min((int64_t)threadIdx.x * per, total);
-  int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
-  while (lo < hi) {
+struct ChunkLoad {
+  const int32_t* big_list;
+  const int64_t* ptr;
+  __device__ int64_t operator()(int64_t i) const {
+    int64_t s = big_list[i];
+    return (ptr[s + 1] - ptr[s] + kChunk - 1) / kChunk;
+  }
+};
+
+// (big segment, chunk) of chunk index ci
+__device__ __forceinline__ void chunk_of(const int64_t* cptr, int64_t nbig, int64_t ci, int64_t* seg, int64_t* j) {
+  int64_t lo = 0, hi = nbig;
+  while (hi - lo > 1) {
     int64_t mid = (lo + hi) >> 1;
-    if (a[mid] <= b[d - 1 - mid]) lo = mid + 1;
+    if (cptr[mid] <= ci) lo = mid;
     else hi = mid;
   }
-  int64_t i = lo, j = d - lo;
-  const int64_t end = min(d + per, total);
-  for (int64_t o = d; o < end; ++o) {
-    if (j >= nb || (i < na && a[i] <= b[j])) out[o] = a[i++];
-    else out[o] = b[j++];
+  *seg = lo;
+  *j = ci - cptr[lo];
+}
+
+// sort every 4096-element chunk of every long segment in shared memory
+__global__ void __launch_bounds__(kChunkThreads) k_chunk_sort(const int64_t* __restrict__ ptr, const ReqCounters* rc,
+                                                              const int32_t* big_list, const int64_t* cptr,
+                                                              int32_t* vals) {
+  using BRS = cub::BlockRadixSort<int32_t, kChunkThreads, kChunkItems>;
+  __shared__ typename BRS::TempStorage tmp;
+  const int64_t nbig = rc->n_big, nch = rc->n_chunks;
+  for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
+    int64_t bi, j;
+    chunk_of(cptr, nbig, ci, &bi, &j);
+    const int64_t s = big_list[bi];
+    const int64_t b = ptr[s] + j * kChunk, len = min((int64_t)kChunk, ptr[s + 1] - b);
+    int32_t k[kChunkItems];
+#pragma unroll
+    for (int i = 0; i < kChunkItems; ++i) {
+      int64_t idx = (int64_t)threadIdx.x * kChunkItems + i;
+      k[i] = idx < len ? vals[b + idx] : INT32_MAX;
+    }
+    BRS(tmp).Sort(k);
+#pragma unroll
+    for (int i = 0; i < kChunkItems; ++i) {
+      int64_t idx = (int64_t)threadIdx.x * kChunkItems + i;
+      if (idx < len) vals[b + idx] = k[i];
+    }
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kBlockSortThreads) k_segsort_block(const int64_t* __restrict__ ptr,
-                                                                    const ReqCounters* rc, const int32_t* big_list,
-                                                                    int32_t* vals, int32_t* tmpbuf) {
-  using BRS = cub::BlockRadixSort<int32_t, kBlockSortThreads, kBlockSortItems>;
-  __shared__ typename BRS::TempStorage tmp;
-  const int64_t nbig = rc->n_big;
-  for (int64_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+// number of elements of a[0,na) that are < v (strict) or <= v
+__device__ __forceinline__ int lower_cnt(const int32_t* a, int na, int32_t v, bool inclusive) {
+  int lo = 0, hi = na;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    bool go = inclusive ? (a[mid] <= v) : (a[mid] < v);
+    if (go) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// one merge level: runs of width w merge pairwise; each CTA produces one
+// 4096-element output tile (merge-path split, then rank-merge in shared memory)
+__global__ void __launch_bounds__(kChunkThreads) k_merge_level(const int64_t* __restrict__ ptr, const ReqCounters* rc,
+                                                               const int32_t* big_list, const int64_t* cptr,
+                                                               const int32_t* src, int32_t* dst, int64_t w) {
+  __shared__ int32_t sa[kChunk];
+  __shared__ int32_t sb[kChunk];
+  __shared__ int64_t split[2];
+  const int64_t nbig = rc->n_big, nch = rc->n_chunks;
+  for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
+    int64_t bi, j;
+    chunk_of(cptr, nbig, ci, &bi, &j);
     const int64_t s = big_list[bi];
-    const int64_t b = ptr[s], len = ptr[s + 1] - b;
-    int32_t* v = vals + b;
-    int32_t* t = tmpbuf + b;
-    // sort tiles in shared memory
-    for (int64_t c0 = 0; c0 < len; c0 += kBlockSortTile) {
-      int32_t k[kBlockSortItems];
-#pragma unroll
-      for (int i = 0; i < kBlockSortItems; ++i) {
-        int64_t idx = c0 + (int64_t)threadIdx.x * kBlockSortItems + i;
-        k[i] = idx < len ? v[idx] : INT32_MAX;
-      }
-      BRS(tmp).Sort(k);
-#pragma unroll
-      for (int i = 0; i < kBlockSortItems; ++i) {
-        int64_t idx = c0 + (int64_t)threadIdx.x * kBlockSortItems + i;
-        if (idx < len) v[idx] = k[i];
-      }
+    const int64_t sb0 = ptr[s], len = ptr[s + 1] - sb0;
+    const int64_t o0 = j * kChunk, o1 = min(o0 + kChunk, len);
+    const int64_t ps = (o0 / (2 * w)) * (2 * w);
+    const int64_t na = min(w, len - ps), nb = max((int64_t)0, min(w, len - ps - na));
+    const int32_t* A = src + sb0 + ps;
+    const int32_t* Bp = A + na;
+    if (nb == 0) {  // lone run: copy through
+      for (int64_t o = o0 + threadIdx.x; o < o1; o += blockDim.x) dst[sb0 + o] = src[sb0 + o];
       __syncthreads();
+      continue;
     }
-    // merge rounds, ping-pong between v and t
-    int32_t* src = v;
-    int32_t* dst = t;
-    for (int64_t w = kBlockSortTile; w < len; w <<= 1) {
-      for (int64_t lo = 0; lo < len; lo += 2 * w) {
-        int64_t na = min(w, len - lo);
-        int64_t nb = min(w, len - lo - na);
-        cta_merge(src + lo, na, src + lo + na, nb, dst + lo);
+    if (threadIdx.x < 2) {
+      const int64_t d = (threadIdx.x == 0 ? o0 : o1) - ps;
+      int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
+      while (lo < hi) {  // merge path: A elements precede equal B elements
+        int64_t mid = (lo + hi) >> 1;
+        if (A[mid] <= Bp[d - 1 - mid]) lo = mid + 1;
+        else hi = mid;
       }
-      __syncthreads();
-      int32_t* x = src;
-      src = dst;
-      dst = x;
+      split[threadIdx.x] = lo;
     }
-    if (src != v) {
-      for (int64_t i = threadIdx.x; i < len; i += blockDim.x) v[i] = src[i];
-    }
+    __syncthreads();
+    const int64_t a0 = split[0], a1 = split[1];
+    const int64_t b0 = (o0 - ps) - a0, b1 = (o1 - ps) - a1;
+    const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
+    for (int i = threadIdx.x; i < la; i += blockDim.x) sa[i] = A[a0 + i];
+    for (int i = threadIdx.x; i < lb; i += blockDim.x) sb[i] = Bp[b0 + i];
+    __syncthreads();
+    int32_t* out = dst + sb0 + o0;
+    for (int i = threadIdx.x; i < la; i += blockDim.x) out[i + lower_cnt(sb, lb, sa[i], false)] = sa[i];
+    for (int i = threadIdx.x; i < lb; i += blockDim.x) out[i + lower_cnt(sa, la, sb[i], true)] = sb[i];
     __syncthreads();
   }
 }
@@ -386,8 +491,9 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   const int64_t m = w.m;
   OB_CUDA(cudaMemsetAsync(w.cbits, 0, sizeof(uint32_t) * (w.words_N + 1), s));
   OB_CUDA(cudaMemsetAsync(w.qdeg, 0, sizeof(int32_t) * (w.B + 1), s));
+  const size_t sq = w.B <= kMaxSmemQueries ? sizeof(int32_t) * w.B : 0;
   if (m > 0) {
-    k_request_mark<<<grid_for(m, 256), 256, 0, s>>>(w.edges, m, N, w.B, w.cbits, w.qdeg, w.rc);
+    k_request_mark<<<grid_for(m, kEdgeTile, kNumSMs * 4), 256, sq, s>>>(w.edges, m, N, w.B, w.cbits, w.qdeg, w.rc);
     OB_LAUNCHED();
   }
   if ((int64_t)w.B * e.g.F > 0) {
@@ -398,12 +504,9 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   device_scan(s, e.scan, LoadPopc{w.cbits}, StoreI64{w.cwpre}, nullptr, w.words_N, w.words_N, &w.rc->R, w.cwpre);
   k_bitmap_compact<<<grid_for(w.words_N, 256), 256, 0, s>>>(w.cbits, w.cwpre, w.words_N, w.cand_ids);
   OB_LAUNCHED();
-  k_slots_init<<<1, 1, 0, s>>>(w.rc, w.B);
-  OB_LAUNCHED();
   const int64_t rb_max = std::min<int64_t>(N, 2 * m) + w.B;
-  k_fill_i32<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rq_cnt, &w.rc->RB, 0, 0);
-  k_fill_i32<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rq_fill, &w.rc->RB, 0, 0);
-  g_launches += 2;
+  k_slots_init<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rc, w.B, w.qdeg, w.rq_cnt, w.rq_fill);
+  OB_LAUNCHED();
   if (m > 0) {
     k_rq_count<<<grid_for(m, 256), 256, 0, s>>>(w.edges, m, N, w.cbits, w.cwpre, w.rc, w.rq_cnt);
     OB_LAUNCHED();
@@ -438,13 +541,32 @@ void stage_request_csr(Engine& e, RequestWs& w) {
   const int64_t m = w.m;
   const int64_t rb_max = std::min<int64_t>(e.g.N, 2 * m) + w.B;
   device_scan(s, e.scan, LoadI32{w.rq_cnt}, StoreI64{w.rq_ptr}, &w.rc->RB, 0, rb_max, nullptr, w.rq_ptr);
-  if (m > 0) {
-    k_rq_fill<<<grid_for(m, 256), 256, 0, s>>>(w.edges, m, e.g.N, w.cbits, w.cwpre, w.rc, w.rq_ptr, w.rq_fill,
-                                               w.rq_src);
+  if (m <= 0) return;
+  const size_t sm = w.B <= kMaxSmemQueries / 2 ? 2 * sizeof(int32_t) * w.B : 0;
+  k_rq_fill<<<grid_for(m, kEdgeTile, kNumSMs * 4), 256, sm, s>>>(w.edges, m, e.g.N, w.B, w.cbits, w.cwpre, w.rc,
+                                                                   w.rq_ptr, w.rq_fill, w.rq_src);
+  k_segsort_warp<<<grid_for(rb_max, 8), 256, 0, s>>>(w.rq_ptr, w.rc, w.rq_src, w.big_list);
+  g_launches += 2;
+  // long segments: chunk sort + merge levels (ping-pong rq_src <-> sort_tmp)
+  device_scan(s, e.scan, ChunkLoad{w.big_list, w.rq_ptr}, StoreI64{w.big_cptr}, &w.rc->n_big, 0, rb_max,
+              &w.rc->n_chunks, w.big_cptr);
+  const int64_t ch_max = m / kChunk + rb_max / 256 + 2;
+  const int g = grid_for(ch_max, 1, kNumSMs * 4);
+  k_chunk_sort<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, w.rq_src);
+  OB_LAUNCHED();
+  int32_t* a = w.rq_src;
+  int32_t* b = w.sort_tmp;
+  int levels = 0;
+  for (int64_t wd = kChunk; wd < m; wd *= 2) {
+    k_merge_level<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, a, b, wd);
     OB_LAUNCHED();
-    k_segsort_warp<<<grid_for(rb_max, 8), 256, 0, s>>>(w.rq_ptr, w.rc, w.rq_src, w.big_list, w.rc);
-    k_segsort_block<<<kNumSMs, kBlockSortThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.rq_src, w.sort_tmp);
-    g_launches += 2;
+    std::swap(a, b);
+    ++levels;
+  }
+  if (levels & 1) {
+    // result sits in sort_tmp for the long segments: one more copy-through level
+    k_merge_level<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, a, b, (int64_t)1 << 40);
+    OB_LAUNCHED();
   }
 }
 
