@@ -126,6 +126,7 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     b.cnt = a.take<BlockCounters>(1);
     b.dst_ptr = a.take<int64_t>(b.D_max + 1);
     b.item_ptr = a.take<int64_t>(b.D_max + 1);
+    b.group_ptr = a.take<int64_t>(b.D_max + 1);
     b.edge_src = a.take<int32_t>(b.E_max);
     b.src_ids = a.take<int32_t>(b.S_max);
     b.self_src = a.take<int32_t>(b.D_max);
@@ -146,6 +147,7 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   const int64_t wl = ld4(maxw) + 4;
   w.qpad = a.take<float>((int64_t)B * e.g.F_ld + 4);
   w.partial = a.take<float>(Imax * wl * (mom ? 2 : 1));  // moments partials are float64
+  w.partial2 = a.take<float>((Imax / kItemGroup + Dmax + 1) * wl);
   w.agg = a.take<float>(Dmax * wl);
   w.mean = mom ? a.take<float>(2 * Dmax * wl) : nullptr;
   w.z = wide ? a.take<float>(Smax * wl) : nullptr;

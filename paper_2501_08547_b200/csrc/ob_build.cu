@@ -97,7 +97,7 @@ __global__ void k_block_fill(const BlockCounters* cnt, const int64_t* __restrict
       int32_t cl = __ldg(sp.cl + i);
       int32_t src = j < cl ? __ldg(nbrs + __ldg(sp.cs + i) + j) : __ldg(rq_src + __ldg(sp.rs + i) + (j - cl));
       src_global[e] = src;
-      bm_set(sbits, src);
+      bm_set_warp(sbits, src);
     }
   }
 }
@@ -139,6 +139,8 @@ __global__ void k_copy_count_D(BlockCounters* dst, const BlockCounters* src) { d
 void block_items(Engine& e, BlockDev& b, int64_t chunk) {
   device_scan(e.stream, e.scan, ItemLoad{b.dst_ptr, chunk}, StoreI64{b.item_ptr}, &b.cnt->D, 0, b.D_max,
               &b.cnt->items, b.item_ptr);
+  device_scan(e.stream, e.scan, GroupLoad{b.item_ptr}, StoreI64{b.group_ptr}, &b.cnt->D, 0, b.D_max,
+              &b.cnt->groups, b.group_ptr);
 }
 
 // generic block assembly over an already written dst list + counts->D

@@ -65,6 +65,14 @@ __device__ __forceinline__ void bm_set(uint32_t* bits, int64_t v) {
 __device__ __forceinline__ bool bm_test(const uint32_t* bits, int64_t v) {
   return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
 }
+// warp-aggregated bm_set: lanes hitting the same word OR their bits first
+__device__ __forceinline__ void bm_set_warp(uint32_t* bits, int64_t v) {
+  const unsigned act = __activemask();
+  const uint32_t word = (uint32_t)(v >> 5);
+  const unsigned peers = __match_any_sync(act, word);
+  const uint32_t orv = __reduce_or_sync(peers, 1u << (v & 31));
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(bits + word, orv);
+}
 // rank of v among set bits (v need not be set: counts set bits below v)
 __device__ __forceinline__ int64_t bm_rank(const uint32_t* bits, const int64_t* wpre, int64_t v) {
   uint32_t w = __ldg(bits + (v >> 5));

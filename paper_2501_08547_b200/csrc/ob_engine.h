@@ -48,7 +48,8 @@ struct BlockCounters {
   int64_t D, E, S, items;
   int64_t feat_src;    // FEATURE-bound training sources (fetch bytes)
   int64_t pe_src;      // PE-bound sources (fetch bytes)
-  int64_t pad[2];
+  int64_t groups;      // second-level partial groups (hub destinations)
+  int64_t pad;
 };
 
 // A computation block in device memory (CSR over destinations).
@@ -61,6 +62,7 @@ struct BlockDev {
   int32_t* src_ids = nullptr;    // [S] ascending global ids
   int32_t* self_src = nullptr;   // [D] local index of dst's own row (centralized only)
   int64_t* item_ptr = nullptr;   // [D+1] aggregation work items per dst (edge chunks)
+  int64_t* group_ptr = nullptr;  // [D+1] groups of kItemGroup items (hub destinations only)
   bool has_self = true;
   // host mirror of counts after the request completes
   BlockCounters host{};
@@ -184,6 +186,7 @@ struct RequestWs {
   const float** rowp = nullptr;    // [S_max] input row per source
   float* gscale = nullptr;         // [S_max] gcn source normaliser
   float* partial = nullptr;        // [items_max][w + 2]
+  float* partial2 = nullptr;       // [groups_max][w + 2] second-level partials of hub destinations
   float* agg = nullptr;            // [D_max][ld4(w)]
   float* outs[8] = {};             // per-layer outputs [D_l][ld4(out)]
   float* z = nullptr;              // gat / transform-first: [S_max][ld4(out)]
@@ -229,6 +232,7 @@ void prof_end(cudaStream_t s, cudaEvent_t a, int cls, const BlockCounters* cnt, 
 struct Engine;
 
 constexpr int64_t kAggChunk = 128;  // edges per aggregation work item
+constexpr int64_t kItemGroup = 16;  // items merged per second-level partial (hub destinations)
 
 // aggregation work items: one per kAggChunk edges of a destination (at least one)
 struct ItemLoad {
@@ -237,6 +241,14 @@ struct ItemLoad {
   __device__ int64_t operator()(int64_t i) const {
     int64_t len = dst_ptr[i + 1] - dst_ptr[i];
     return len > chunk ? (len + chunk - 1) / chunk : 1;
+  }
+};
+// second-level groups: only destinations with more than kItemGroup items get them
+struct GroupLoad {
+  const int64_t* item_ptr;
+  __device__ int64_t operator()(int64_t i) const {
+    int64_t n = item_ptr[i + 1] - item_ptr[i];
+    return n > kItemGroup ? (n + kItemGroup - 1) / kItemGroup : 0;
   }
 };
 

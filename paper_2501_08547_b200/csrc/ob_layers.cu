@@ -154,13 +154,14 @@ struct AggArgs {
   int pw;                // partial row width (softmax: width + 2)
 };
 
-template <int OP>
+template <int OP, int NV>
 __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
+  constexpr int kU = 4;  // edges whose rows are in flight together
   const int lane = threadIdx.x & 31;
   const int64_t D = a.cnt->D;
   const int64_t items = a.cnt->items;
-  const int col0 = blockIdx.y * kAggSlice;
+  const int col0 = blockIdx.y * (32 * 4 * NV);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = gw; it < items; it += nw) {
@@ -168,10 +169,10 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
     const int64_t j = it - a.item_ptr[i];
     const int64_t e0 = a.dst_ptr[i] + j * kAggChunk;
     const int64_t e1 = min(e0 + kAggChunk, a.dst_ptr[i + 1]);
-    AT acc[kAggNV][4];
+    AT acc[NV][4];
     float m_run = -INFINITY, den = 0.f;
 #pragma unroll
-    for (int q = 0; q < kAggNV; ++q)
+    for (int q = 0; q < NV; ++q)
 #pragma unroll
       for (int t = 0; t < 4; ++t) acc[q][t] = (OP == kOpMax) ? -INFINITY : 0.f;
     const float sd = (OP == kOpSoftmax) ? a.s_dst[i] : 0.f;
@@ -189,44 +190,53 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
         }
       }
       const int cnt = (int)min((int64_t)32, e1 - eb);
-#pragma unroll 2
-      for (int u = 0; u < cnt; ++u) {
-        const float* r = (const float*)__shfl_sync(0xffffffffu, (unsigned long long)r_l, u);
-        const float wgt = __shfl_sync(0xffffffffu, w_l, u);
-        float scale_old = 1.f, pe = 1.f;
-        if (OP == kOpSoftmax) {
-          float mn = fmaxf(m_run, wgt);
-          scale_old = __expf(m_run - mn);
-          pe = __expf(wgt - mn);
-          den = den * scale_old + pe;
-          m_run = mn;
-        }
-        float4 v[kAggNV];
+      for (int u = 0; u < cnt; u += kU) {
+        float4 v[kU][NV];
+        float wg[kU];
 #pragma unroll
-        for (int q = 0; q < kAggNV; ++q) {
-          const int col = col0 + (q * 32 + lane) * 4;
-          v[q] = col < a.width ? __ldg(reinterpret_cast<const float4*>(r + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int x = 0; x < kU; ++x) {  // issue kU row loads before consuming any
+          const int uu = min(u + x, cnt - 1);
+          const float* r = (const float*)__shfl_sync(0xffffffffu, (unsigned long long)r_l, uu);
+          wg[x] = __shfl_sync(0xffffffffu, w_l, uu);
+#pragma unroll
+          for (int q = 0; q < NV; ++q) {
+            const int col = col0 + (q * 32 + lane) * 4;
+            v[x][q] = col < a.width ? __ldg(reinterpret_cast<const float4*>(r + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
 #pragma unroll
-        for (int q = 0; q < kAggNV; ++q) {
-          const int col = col0 + (q * 32 + lane) * 4;
-          if (col < a.width) {
-            const float vv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+        for (int x = 0; x < kU; ++x) {
+          if (u + x >= cnt) break;
+          const float wgt = wg[x];
+          float scale_old = 1.f, pe = 1.f;
+          if (OP == kOpSoftmax) {
+            float mn = fmaxf(m_run, wgt);
+            scale_old = __expf(m_run - mn);
+            pe = __expf(wgt - mn);
+            den = den * scale_old + pe;
+            m_run = mn;
+          }
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              if (OP == kOpSum) acc[q][t] = fmaf(wgt, vv[t], acc[q][t]);
-              else if (OP == kOpDSum) acc[q][t] += (double)vv[t];
-              else if (OP == kOpMax) acc[q][t] = fmaxf(acc[q][t], vv[t]);
-              else if (OP == kOpPow) acc[q][t] += powf(softplus_f(vv[t]), a.p);
-              else if (OP == kOpMom2) {
-                if (col + t < a.width) {
-                  double dlt = (double)vv[t] - a.mean[i * a.width + col + t];
-                  double pw = dlt;
-                  for (int r2 = 1; r2 < a.n; ++r2) pw *= dlt;
-                  acc[q][t] += pw;
+          for (int q = 0; q < NV; ++q) {
+            const int col = col0 + (q * 32 + lane) * 4;
+            if (col < a.width) {
+              const float vv[4] = {v[x][q].x, v[x][q].y, v[x][q].z, v[x][q].w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                if (OP == kOpSum) acc[q][t] = fmaf(wgt, vv[t], acc[q][t]);
+                else if (OP == kOpDSum) acc[q][t] += (double)vv[t];
+                else if (OP == kOpMax) acc[q][t] = fmaxf(acc[q][t], vv[t]);
+                else if (OP == kOpPow) acc[q][t] += powf(softplus_f(vv[t]), a.p);
+                else if (OP == kOpMom2) {
+                  if (col + t < a.width) {
+                    double dlt = (double)vv[t] - a.mean[i * a.width + col + t];
+                    double pw = dlt;
+                    for (int r2 = 1; r2 < a.n; ++r2) pw *= dlt;
+                    acc[q][t] += pw;
+                  }
+                } else {
+                  acc[q][t] = fmaf(pe, vv[t], acc[q][t] * scale_old);
                 }
-              } else {
-                acc[q][t] = fmaf(pe, vv[t], acc[q][t] * scale_old);
               }
             }
           }
@@ -242,7 +252,7 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
       out += 2;
     }
 #pragma unroll
-    for (int q = 0; q < kAggNV; ++q) {
+    for (int q = 0; q < NV; ++q) {
       const int col = col0 + (q * 32 + lane) * 4;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -259,6 +269,8 @@ struct FinArgs {
   const int64_t* dst_ptr;
   const int64_t* item_ptr;
   const float* partial;
+  const int64_t* group_ptr;  // hub destinations: second-level partials in partial2
+  const float* partial2;
   int pw;
   int width;
   int kind;   // ob_kind
@@ -270,18 +282,91 @@ struct FinArgs {
   bool gcn_norm;  // divide by sqrt(count + 1) (gcn)
 };
 
+// Hub destinations (more than kItemGroup items): merge each group of
+// kItemGroup consecutive items into one second-level partial of the same form
+// (sum / max / softmax triple), one warp per group, fixed association.
+__global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a, float* partial2) {
+  const int64_t D = a.cnt->D, G = a.cnt->groups;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = gw; g < G; g += nw) {
+    int64_t lo = 0, hi = D;  // dst with group_ptr[i] <= g < group_ptr[i+1]
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (a.group_ptr[mid] <= g) lo = mid;
+      else hi = mid;
+    }
+    const int64_t i = lo;
+    const int64_t it0 = a.item_ptr[i] + (g - a.group_ptr[i]) * kItemGroup;
+    const int64_t it1 = min(it0 + kItemGroup, a.item_ptr[i + 1]);
+    float* out = partial2 + g * (int64_t)a.pw;
+    if (a.kind == OB_KIND_GAT) {
+      float ms = -INFINITY;
+      for (int64_t it = it0; it < it1; ++it) {
+        const float* pp = a.partial + it * (int64_t)a.pw;
+        if (pp[1] > 0.f) ms = fmaxf(ms, pp[0]);
+      }
+      float den = 0.f;
+      for (int64_t it = it0; it < it1; ++it) {
+        const float* pp = a.partial + it * (int64_t)a.pw;
+        if (pp[1] > 0.f) den += pp[1] * __expf(pp[0] - ms);
+      }
+      if (lane == 0) {
+        out[0] = ms;
+        out[1] = den;
+      }
+      for (int col = lane; col < a.width; col += 32) {
+        float num = 0.f;
+        for (int64_t it = it0; it < it1; ++it) {
+          const float* pp = a.partial + it * (int64_t)a.pw;
+          if (pp[1] > 0.f) num += pp[2 + col] * __expf(pp[0] - ms);
+        }
+        out[2 + col] = num;
+      }
+    } else {
+      for (int col = lane; col < a.width; col += 32) {
+        float r0, r1, r2, r3;
+        const bool mx = a.kind == OB_KIND_SAGE_MAX;
+        r0 = r1 = r2 = r3 = mx ? -INFINITY : 0.f;
+        int64_t it = it0;
+        for (; it + 3 < it1; it += 4) {
+          const float v0 = a.partial[it * (int64_t)a.pw + col], v1 = a.partial[(it + 1) * (int64_t)a.pw + col];
+          const float v2 = a.partial[(it + 2) * (int64_t)a.pw + col], v3 = a.partial[(it + 3) * (int64_t)a.pw + col];
+          if (mx) {
+            r0 = fmaxf(r0, v0), r1 = fmaxf(r1, v1), r2 = fmaxf(r2, v2), r3 = fmaxf(r3, v3);
+          } else {
+            r0 += v0, r1 += v1, r2 += v2, r3 += v3;
+          }
+        }
+        for (; it < it1; ++it) {
+          const float v = a.partial[it * (int64_t)a.pw + col];
+          r0 = mx ? fmaxf(r0, v) : r0 + v;
+        }
+        out[col] = mx ? fmaxf(fmaxf(r0, r1), fmaxf(r2, r3)) : (r0 + r1) + (r2 + r3);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
   const int64_t D = a.cnt->D;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = gw; i < D; i += nw) {
-    const int64_t i0 = a.item_ptr[i], i1 = a.item_ptr[i + 1];
+    int64_t i0 = a.item_ptr[i], i1 = a.item_ptr[i + 1];
     const int64_t cnt = a.dst_ptr[i + 1] - a.dst_ptr[i];
+    const float* part = a.partial;
+    if (a.group_ptr && a.group_ptr[i + 1] > a.group_ptr[i]) {  // hub: merge the group partials
+      i0 = a.group_ptr[i];
+      i1 = a.group_ptr[i + 1];
+      part = a.partial2;
+    }
     float ms = -INFINITY;
     if (a.kind == OB_KIND_GAT) {
       for (int64_t it = i0; it < i1; ++it) {
-        const float* pp = a.partial + it * (int64_t)a.pw;
+        const float* pp = part + it * (int64_t)a.pw;
         if (pp[1] > 0.f) ms = fmaxf(ms, pp[0]);
       }
     }
@@ -291,7 +376,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
         // (max, sum exp, sum exp*z) merge in item order (cgpexec.py:225-239)
         float den = 0.f, num = 0.f;
         for (int64_t it = i0; it < i1; ++it) {
-          const float* pp = a.partial + it * (int64_t)a.pw;
+          const float* pp = part + it * (int64_t)a.pw;
           if (pp[1] > 0.f) {
             float sc = __expf(pp[0] - ms);
             den += pp[1] * sc;
@@ -303,22 +388,22 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
         float m0 = -INFINITY, m1 = -INFINITY;
         int64_t it = i0;
         for (; it + 1 < i1; it += 2) {
-          m0 = fmaxf(m0, a.partial[it * (int64_t)a.pw + col]);
-          m1 = fmaxf(m1, a.partial[(it + 1) * (int64_t)a.pw + col]);
+          m0 = fmaxf(m0, part[it * (int64_t)a.pw + col]);
+          m1 = fmaxf(m1, part[(it + 1) * (int64_t)a.pw + col]);
         }
-        if (it < i1) m0 = fmaxf(m0, a.partial[it * (int64_t)a.pw + col]);
+        if (it < i1) m0 = fmaxf(m0, part[it * (int64_t)a.pw + col]);
         r = cnt > 0 ? fmaxf(m0, m1) : 0.f;
       } else {
         // four independent partial sums (fixed association -> deterministic)
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         int64_t it = i0;
         for (; it + 3 < i1; it += 4) {
-          s0 += a.partial[it * (int64_t)a.pw + col];
-          s1 += a.partial[(it + 1) * (int64_t)a.pw + col];
-          s2 += a.partial[(it + 2) * (int64_t)a.pw + col];
-          s3 += a.partial[(it + 3) * (int64_t)a.pw + col];
+          s0 += part[it * (int64_t)a.pw + col];
+          s1 += part[(it + 1) * (int64_t)a.pw + col];
+          s2 += part[(it + 2) * (int64_t)a.pw + col];
+          s3 += part[(it + 3) * (int64_t)a.pw + col];
         }
-        for (; it < i1; ++it) s0 += a.partial[it * (int64_t)a.pw + col];
+        for (; it < i1; ++it) s0 += part[it * (int64_t)a.pw + col];
         const float s = (s0 + s1) + (s2 + s3);
         if (a.gcn_norm) {
           r = s / sqrtf((float)cnt + 1.f);  // agg / sqrt(|N(v)|+1) (models.py:217-218)
@@ -379,15 +464,22 @@ __global__ void k_rowdot(const int64_t* M_dev, const float* __restrict__ z, int6
 // ---------------------------------------------------------------------------
 template <int OP>
 static void launch_agg(cudaStream_t s, const AggArgs& a, int64_t items_max) {
-  dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a.width + kAggSlice - 1) / kAggSlice);
+  const int nv = a.width <= 128 ? 1 : (a.width <= 256 ? 2 : 4);
+  dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a.width + 128 * nv - 1) / (128 * nv));
   cudaEvent_t pa = prof_begin(s);
-  k_agg<OP><<<grid, 32 * kAggWarps, 0, s>>>(a);
+  if (nv == 1) k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a);
+  else if (nv == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a);
+  else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a);
   OB_LAUNCHED();
   prof_end(s, pa, kProfAgg, a.cnt, a.width, a.pw, 0, 0, 0);
 }
 
-static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max) {
+static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t items_max) {
   cudaEvent_t pa = prof_begin(s);
+  if (f.group_ptr) {
+    k_reduce_groups<<<grid_for(items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f, (float*)f.partial2);
+    OB_LAUNCHED();
+  }
   k_finalize<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(f);
   OB_LAUNCHED();
   prof_end(s, pa, kProfFinalize, f.cnt, f.width, f.pw, 0, 0, 0);
@@ -413,10 +505,12 @@ struct LayerRun {
   const int32_t* self;       // null = identity
   RowSrc x;                  // bound inputs
   const float* gscale;       // gcn
+  const int64_t* group_ptr;  // second-level partial groups (hub destinations)
 };
 
 struct LayerScratch {
   float* partial;
+  float* partial2;
   float* agg;     // [D][ld4(w)]
   float* mean;    // moments (float64 [D][in])
   float* z;       // [S][ld4(out)]
@@ -458,6 +552,8 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   f.dst_ptr = r.dst_ptr;
   f.item_ptr = r.item_ptr;
   f.partial = sc.partial;
+  f.partial2 = sc.partial2;
+  f.group_ptr = r.group_ptr;
   f.pw = in;
   f.width = in;
   f.kind = sp.kind;
@@ -477,6 +573,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     a.pw = outd;
     f.width = outd;
     f.pw = outd;
+    f.ldo = ld_out;
   }
   if (sp.kind == OB_KIND_GAT) {
     k_rowdot<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, sc.z, ld_out, nullptr, outd, L.a_src, sc.s_src);
@@ -490,7 +587,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     f.out = out;
     f.ldo = ldo;
     f.relu = true;
-    finalize(s, f, r.D_max);
+    finalize(s, f, r.D_max, r.items_max);
     return;
   }
   if (sp.kind == OB_KIND_GCN) {
@@ -501,10 +598,10 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
       f.out = out;
       f.ldo = ldo;
       f.relu = true;
-      finalize(s, f, r.D_max);
+      finalize(s, f, r.D_max, r.items_max);
       return;
     }
-    finalize(s, f, r.D_max);
+    finalize(s, f, r.D_max, r.items_max);
     TcGemmArgs g = gemm_args(r.D_dev, L.tw_main, out, ldo, true);
     g.a2 = sc.agg;
     g.lda2 = ld4(in);
@@ -514,7 +611,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   }
   if (sp.kind == OB_KIND_SAGE_MEAN && L.transform_first) {
     launch_agg<kOpSum>(s, a, r.items_max);
-    finalize(s, f, r.D_max);  // mean over Y = X W_neigh rows -> agg [D][ld_out]
+    finalize(s, f, r.D_max, r.items_max);  // mean over Y = X W_neigh rows -> agg [D][ld_out]
     TcGemmArgs g = gemm_args(r.D_dev, L.tw_self, out, ldo, true);
     g.a1 = r.x;
     g.self = r.self;
@@ -526,10 +623,10 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   }
   if (sp.kind == OB_KIND_SAGE_MAX) {
     launch_agg<kOpMax>(s, a, r.items_max);
-    finalize(s, f, r.D_max);
+    finalize(s, f, r.D_max, r.items_max);
   } else if (sp.kind == OB_KIND_POWER_MEAN) {
     launch_agg<kOpPow>(s, a, r.items_max);
-    finalize(s, f, r.D_max);
+    finalize(s, f, r.D_max, r.items_max);
   } else if (sp.kind == OB_KIND_MOMENTS) {
     double* mean = reinterpret_cast<double*>(sc.mean);
     launch_agg<kOpDSum>(s, a, r.items_max);
@@ -542,7 +639,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     g_launches += 2;
   } else {  // sage_mean aggregate-first
     launch_agg<kOpSum>(s, a, r.items_max);
-    finalize(s, f, r.D_max);
+    finalize(s, f, r.D_max, r.items_max);
   }
   // relu([h_v | agg] @ [W_self; W_neigh])
   TcGemmArgs g = gemm_args(r.D_dev, L.tw_main, out, ldo, true);
@@ -614,7 +711,8 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     r.self = b.self_src;
     r.x = RowSrc{w.rowp, nullptr, 0};
     r.gscale = w.gscale;
-    LayerScratch sc{w.partial, w.agg, w.mean, w.z, w.s_src, w.s_dst};
+    r.group_ptr = b.group_ptr;
+    LayerScratch sc{w.partial, w.partial2, w.agg, w.mean, w.z, w.s_src, w.s_dst};
     const bool last = l == k;
     float* out = last ? d_out : w.outs[l];
     run_layer(s, L, r, sc, out, last ? L.spec.out_dim : ld4(L.spec.out_dim));
@@ -666,6 +764,8 @@ void stage_precompute(Engine& e) {
     OB_CUDA(cudaMemcpyAsync(cnt, &hc, sizeof(hc), cudaMemcpyHostToDevice, s));
     int64_t* item_ptr = (int64_t*)talloc(sizeof(int64_t) * (N + 1));
     float* partial = (float*)talloc(sizeof(float) * items_max * maxw * (mom ? 2 : 1));
+    float* partial2 = (float*)talloc(sizeof(float) * (items_max / kItemGroup + N + 1) * maxw);
+    int64_t* group_ptr = (int64_t*)talloc(sizeof(int64_t) * (N + 1));
     float* agg = (float*)talloc(sizeof(float) * N * maxw);
     float* mean = mom ? (float*)talloc(sizeof(double) * N * maxw) : nullptr;
     float* z = wide ? (float*)talloc(sizeof(float) * N * maxw) : nullptr;
@@ -679,6 +779,7 @@ void stage_precompute(Engine& e) {
     sc_scan.tile_sums = (int64_t*)talloc(sizeof(int64_t) * (sc_scan.max_tiles + 1));
     device_scan(s, sc_scan, ItemLoad{e.g.offsets, kAggChunk}, StoreI64{item_ptr}, nullptr, N, N, &cnt->items,
                 item_ptr);
+    device_scan(s, sc_scan, GroupLoad{item_ptr}, StoreI64{group_ptr}, nullptr, N, N, &cnt->groups, group_ptr);
     e.pe.assign(k - 1, nullptr);
     e.pe_dim.assign(k - 1, 0);
     const float* h = e.g.feats;
@@ -703,7 +804,8 @@ void stage_precompute(Engine& e) {
       r.self = nullptr;
       r.x = RowSrc{nullptr, h, hld};
       r.gscale = gscale;
-      LayerScratch scr{partial, agg, mean, z, s_src, s_dst};
+      r.group_ptr = group_ptr;
+      LayerScratch scr{partial, partial2, agg, mean, z, s_src, s_dst};
       run_layer(s, L, r, scr, out, old);
       e.pe[l - 1] = out;
       e.pe_dim[l - 1] = L.spec.out_dim;

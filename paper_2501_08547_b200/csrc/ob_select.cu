@@ -434,20 +434,33 @@ __device__ __forceinline__ int lower_cnt(const int32_t* a, int na, int32_t v, bo
   return lo;
 }
 
-// one merge level: runs of width w merge pairwise; each CTA produces one
-// 4096-element output tile (merge-path split, then rank-merge in shared memory)
+// merge levels a segment of `len` needs after the 4096-element chunk sort
+__device__ __forceinline__ int levels_for(int64_t len) {
+  int l = 0;
+  for (int64_t w = kChunk; w < len; w *= 2) ++l;
+  return l;
+}
+
+// merge level `level` (run width 4096 << level): runs merge pairwise from the
+// buffer the segment's data currently sits in (parity of the level) into the
+// other; segments that need fewer levels are skipped.  Each CTA produces one
+// 4096-element output tile (merge-path split, then rank-merge in shared memory).
 __global__ void __launch_bounds__(kChunkThreads) k_merge_level(const int64_t* __restrict__ ptr, const ReqCounters* rc,
                                                                const int32_t* big_list, const int64_t* cptr,
-                                                               const int32_t* src, int32_t* dst, int64_t w) {
+                                                               int32_t* vals, int32_t* tmp, int level) {
   __shared__ int32_t sa[kChunk];
   __shared__ int32_t sb[kChunk];
   __shared__ int64_t split[2];
   const int64_t nbig = rc->n_big, nch = rc->n_chunks;
+  const int64_t w = (int64_t)kChunk << level;
   for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
     int64_t bi, j;
     chunk_of(cptr, nbig, ci, &bi, &j);
     const int64_t s = big_list[bi];
     const int64_t sb0 = ptr[s], len = ptr[s + 1] - sb0;
+    if (level >= levels_for(len)) continue;  // uniform per CTA
+    const int32_t* src = (level & 1) ? tmp : vals;
+    int32_t* dst = (level & 1) ? vals : tmp;
     const int64_t o0 = j * kChunk, o1 = min(o0 + kChunk, len);
     const int64_t ps = (o0 / (2 * w)) * (2 * w);
     const int64_t na = min(w, len - ps), nb = max((int64_t)0, min(w, len - ps - na));
@@ -479,6 +492,23 @@ __global__ void __launch_bounds__(kChunkThreads) k_merge_level(const int64_t* __
     for (int i = threadIdx.x; i < la; i += blockDim.x) out[i + lower_cnt(sb, lb, sa[i], false)] = sa[i];
     for (int i = threadIdx.x; i < lb; i += blockDim.x) out[i + lower_cnt(sa, la, sb[i], true)] = sb[i];
     __syncthreads();
+  }
+}
+
+// segments whose level count is odd finished in tmp: copy their tiles back
+__global__ void __launch_bounds__(kChunkThreads) k_merge_copyback(const int64_t* __restrict__ ptr,
+                                                                  const ReqCounters* rc, const int32_t* big_list,
+                                                                  const int64_t* cptr, int32_t* vals,
+                                                                  const int32_t* tmp) {
+  const int64_t nbig = rc->n_big, nch = rc->n_chunks;
+  for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
+    int64_t bi, j;
+    chunk_of(cptr, nbig, ci, &bi, &j);
+    const int64_t s = big_list[bi];
+    const int64_t sb0 = ptr[s], len = ptr[s + 1] - sb0;
+    if (!(levels_for(len) & 1)) continue;
+    const int64_t o0 = j * kChunk, o1 = min(o0 + kChunk, len);
+    for (int64_t o = o0 + threadIdx.x; o < o1; o += blockDim.x) vals[sb0 + o] = tmp[sb0 + o];
   }
 }
 
@@ -554,18 +584,15 @@ void stage_request_csr(Engine& e, RequestWs& w) {
   const int g = grid_for(ch_max, 1, kNumSMs * 4);
   k_chunk_sort<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, w.rq_src);
   OB_LAUNCHED();
-  int32_t* a = w.rq_src;
-  int32_t* b = w.sort_tmp;
-  int levels = 0;
-  for (int64_t wd = kChunk; wd < m; wd *= 2) {
-    k_merge_level<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, a, b, wd);
+  // the longest possible segment is the whole request; levels past a segment's
+  // own count exit immediately
+  int level = 0;
+  for (int64_t wd = kChunk; wd < m; wd *= 2, ++level) {
+    k_merge_level<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, w.rq_src, w.sort_tmp, level);
     OB_LAUNCHED();
-    std::swap(a, b);
-    ++levels;
   }
-  if (levels & 1) {
-    // result sits in sort_tmp for the long segments: one more copy-through level
-    k_merge_level<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, a, b, (int64_t)1 << 40);
+  if (level > 0) {
+    k_merge_copyback<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, w.rq_src, w.sort_tmp);
     OB_LAUNCHED();
   }
 }
