@@ -14,11 +14,13 @@
 // once at model load (weights are static).
 //
 // Structure (one CTA per SM, persistent over 128-row tiles):
-//   * 128 threads stage A/B k-blocks (32 fp32 = one 128-byte row) with cp.async
-//     into the canonical K-major SWIZZLE_128B layout, 3-stage ring;
+//   * 256 threads stage A/B k-blocks (32 fp32 = one 128-byte row) with cp.async
+//     into the canonical K-major SWIZZLE_128B layout, up to a 4-stage ring;
+//     A_lo lives in its own double buffer so the ring holds only raw loads;
 //   * one elected thread issues 12 tcgen05.mma.kind::tf32 (3 products x 4 K=8
 //     steps) per k-block and tcgen05.commit's an mbarrier per stage;
-//   * epilogue: tcgen05.ld 32x32b -> registers -> activation -> global.
+//   * epilogue: 8 warps tcgen05.ld 32x32b (lane quadrant x column half) ->
+//     registers -> optional addend + activation -> global.
 #include <algorithm>
 #include <cstring>
 
@@ -28,7 +30,7 @@ namespace ob {
 
 namespace {
 
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;
 constexpr int kTcBM = 128;
 constexpr int kTcBK = 32;  // fp32 per k-block: one 128-byte swizzle row
 constexpr int kTileA = kTcBM * kTcBK * 4;  // 16 KB
@@ -113,13 +115,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
 
 }  // namespace
 
-// Shared-memory budget per stage: A, A_lo (16 KB each) + B, B_lo (Np x 128 B each)
+// Shared memory: S-stage ring of {A, B, B_lo} k-blocks + a double-buffered A_lo.
 template <int NP>
 struct TcSmem {
   static constexpr int kTileB = NP * kTcBK * 4;
-  static constexpr int kStage = 2 * kTileA + 2 * kTileB;
-  static constexpr int kStages = (3 * kStage <= 200 * 1024) ? 3 : 2;
-  static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 256 /*bars, rows*/ + kTcBM * 8;
+  static constexpr int kStage = kTileA + 2 * kTileB;
+  static constexpr int kBudget = 227 * 1024 - 2 * kTileA - (1024 + 256 + kTcBM * 8);
+  static constexpr int kStages = (kBudget / kStage) >= 4 ? 4 : ((kBudget / kStage) >= 3 ? 3 : 2);
+  static constexpr int kBytes = kStages * kStage + 2 * kTileA + 1024 /*align*/ + 256 /*bars*/ + kTcBM * 8;
 };
 
 template <int NP>
@@ -129,9 +132,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
   constexpr uint32_t kCols = NP <= 32 ? 32 : (NP <= 64 ? 64 : (NP <= 128 ? 128 : 256));
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + S * SM::kStage);
+  uint8_t* alo_base = base + S * SM::kStage;  // 2 x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(alo_base + 2 * kTileA);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S + 1);
-  const float** rows = reinterpret_cast<const float**>(base + S * SM::kStage + 256);
+  const float** rows = reinterpret_cast<const float**>(alo_base + 2 * kTileA + 256);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t M = *g.M_dev;
@@ -157,8 +161,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
   uint32_t it = 0;  // global k-block counter across tiles (stage / phase bookkeeping)
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t m0 = tile * kTcBM;
-    // per-tile A1 row pointers
-    {
+    if (tid < kTcBM) {  // per-tile A1 row pointers
       const int64_t r = m0 + tid;
       const float* p = nullptr;
       if (r < M && g.K1) p = g.a1.row(g.self ? (int64_t)g.self[r] : r);
@@ -168,9 +171,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
 
     auto load = [&](int kb, int stage) {
       uint8_t* sA = base + stage * SM::kStage;
-      uint8_t* sB = sA + 2 * kTileA;
-      uint8_t* sBl = sB + SM::kTileB;
-      const uint32_t a_s = smem_u32(sA), b_s = smem_u32(sB), bl_s = smem_u32(sBl);
+      const uint32_t a_s = smem_u32(sA), b_s = a_s + kTileA, bl_s = b_s + SM::kTileB;
       const bool first = kb < KB1;
       const int k0 = (first ? kb : kb - KB1) * kTcBK;
       const int Kv = first ? g.K1 : g.K2;
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
         int bytes = 0;
         if (m0 + r < M) {
           const float* rowp = first ? rows[r] : g.a2 + (m0 + r) * g.lda2;
-          int rem = Kv - k;
+          const int rem = Kv - k;
           bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
           src = rowp + (bytes ? k : 0);
         }
@@ -191,17 +192,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
         cp_async16(a_s + r * 128 + ((c ^ (r & 7)) << 4), src, bytes);
       }
 #pragma unroll
-      for (int i = 0; i < (NP * 8) / kTcThreads; ++i) {
+      for (int i = 0; i < (NP * 8 + kTcThreads - 1) / kTcThreads; ++i) {
         const int q = tid + i * kTcThreads;
-        const int n = q >> 3, c = q & 7;
-        const int64_t off = (int64_t)n * Kp + kb * kTcBK + c * 4;
-        const uint32_t so = n * 128 + ((c ^ (n & 7)) << 4);
-        cp_async16(b_s + so, g.Bt + off, 16);
-        cp_async16(bl_s + so, g.Bt_lo + off, 16);
+        if (q < NP * 8) {
+          const int n = q >> 3, c = q & 7;
+          const int64_t off = (int64_t)n * Kp + kb * kTcBK + c * 4;
+          const uint32_t so = n * 128 + ((c ^ (n & 7)) << 4);
+          cp_async16(b_s + so, g.Bt + off, 16);
+          cp_async16(bl_s + so, g.Bt_lo + off, 16);
+        }
       }
     };
 
-    // prologue
 #pragma unroll
     for (int s = 0; s < S - 1; ++s) {
       if (s < KB) load(s, (it + s) % S);
@@ -212,30 +214,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
       const int stage = gk % S;
       cp_async_wait<S - 2>();
       __syncthreads();
-      // A_lo = a - trunc_tf32(a) (the raw tile doubles as A_hi: the MMA truncates)
+      // A_lo = a - trunc_tf32(a) into the double buffer (MMAs of k-block gk-2 have retired:
+      // we waited for gk-2 before refilling its stage one iteration ago)
       {
-        float* a = reinterpret_cast<float*>(base + stage * SM::kStage);
-        float* alo = a + kTcBM * kTcBK;
-#pragma unroll 8
-        for (int i = tid; i < kTcBM * kTcBK; i += kTcThreads) {
-          float v = a[i];
-          alo[i] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        const float* a = reinterpret_cast<const float*>(base + stage * SM::kStage);
+        float* alo = reinterpret_cast<float*>(alo_base + (gk & 1) * kTileA);
+#pragma unroll 4
+        for (int i = tid * 4; i < kTcBM * kTcBK; i += kTcThreads * 4) {
+          const float4 v = *reinterpret_cast<const float4*>(a + i);
+          float4 o;
+          o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          *reinterpret_cast<float4*>(alo + i) = o;
         }
       }
       fence_proxy_async();
       __syncthreads();
       if (tid == 0) {
         tc_fence_after();
-        uint8_t* sA = base + stage * SM::kStage;
-        const uint32_t a_s = smem_u32(sA), alo_s = a_s + kTileA;
-        const uint32_t b_s = a_s + 2 * kTileA, blo_s = b_s + SM::kTileB;
+        const uint32_t a_s = smem_u32(base + stage * SM::kStage);
+        const uint32_t b_s = a_s + kTileA, blo_s = b_s + SM::kTileB;
+        const uint32_t alo_s = smem_u32(alo_base + (gk & 1) * kTileA);
 #pragma unroll
         for (int kk = 0; kk < kTcBK / 8; ++kk) {
           const uint32_t off = kk * 32;  // 8 tf32 per MMA
           const uint64_t da = sw128_desc(a_s + off), dal = sw128_desc(alo_s + off);
           const uint64_t db = sw128_desc(b_s + off), dbl = sw128_desc(blo_s + off);
-          const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem, da, db, idesc, acc0);
+          mma_tf32(tmem, da, db, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
           mma_tf32(tmem, da, dbl, idesc, 1u);
           mma_tf32(tmem, dal, db, idesc, 1u);
         }
@@ -244,36 +251,40 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
       // refill the stage consumed by the previous k-block once its MMAs retired
       const int nk = kb + S - 1;
       if (nk < KB) {
-        const uint32_t gprev = gk + S - 1 - S;  // == gk - 1: last user of stage (gk + S - 1) % S
-        if (kb > 0) mbar_wait(bars + (gprev % S), (gprev / S) & 1);
+        if (kb > 0) mbar_wait(bars + ((gk - 1) % S), ((gk - 1) / S) & 1);
         load(nk, (gk + S - 1) % S);
       }
       cp_async_commit();
     }
-    // accumulator complete when the last k-block's commit lands
     {
       const uint32_t glast = it + KB - 1;
       mbar_wait(bars + (glast % S), (glast / S) & 1);
     }
     it += KB;
     tc_fence_after();
-    // epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows
-    const int64_t row = m0 + warp * 32 + lane;
+    // epilogue: warp w reads TMEM lanes [32(w%4), +32) = tile rows, column half w/4
+    {
+      const int quad = warp & 3, half = warp >> 2;
+      const int64_t row = m0 + quad * 32 + lane;
+      constexpr int kHalf = NP >= 64 ? NP / 2 : NP;
+      if (NP >= 64 || half == 0) {
 #pragma unroll 1
-    for (int c0 = 0; c0 < NP; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-      if (row < M) {
-        float* crow = g.C + row * g.ldc;
-        const float* erow = g.E ? g.E + row * g.lde : nullptr;
+        for (int c0 = half * kHalf; c0 < (half + 1) * kHalf; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + c0, v);
+          if (row < M) {
+            float* crow = g.C + row * g.ldc;
+            const float* erow = g.E ? g.E + row * g.lde : nullptr;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = c0 + j;
-          if (col < g.N) {
-            float o = v[j];
-            if (erow) o += erow[col];
-            if (g.relu) o = fmaxf(o, 0.f);
-            crow[col] = o;
+            for (int j = 0; j < 32; ++j) {
+              const int col = c0 + j;
+              if (col < g.N) {
+                float o = v[j];
+                if (erow) o += erow[col];
+                if (g.relu) o = fmaxf(o, 0.f);
+                crow[col] = o;
+              }
+            }
           }
         }
       }
