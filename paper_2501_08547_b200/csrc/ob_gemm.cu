@@ -130,8 +130,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
   using SM = TcSmem<NP>;
   constexpr int S = SM::kStages;
   constexpr uint32_t kCols = NP <= 32 ? 32 : (NP <= 64 ? 64 : (NP <= 128 ? 128 : 256));
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // offset (not an integer cast) keeps the pointer in the shared window -> LDS/STS
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* alo_base = base + S * SM::kStage;  // 2 x 16 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(alo_base + 2 * kTileA);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S + 1);
@@ -262,30 +263,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
     }
     it += KB;
     tc_fence_after();
-    // epilogue: warp w reads TMEM lanes [32(w%4), +32) = tile rows, column half w/4
+    // epilogue: warp w reads TMEM lanes [32(w%4), +32) = tile rows, column half w/4;
+    // each 32x32 block is transposed through shared memory (the free A_lo buffers,
+    // XOR-swizzled) so E loads and C stores run with lanes along a row (coalesced)
     {
       const int quad = warp & 3, half = warp >> 2;
-      const int64_t row = m0 + quad * 32 + lane;
       constexpr int kHalf = NP >= 64 ? NP / 2 : NP;
+      float* buf = reinterpret_cast<float*>(alo_base) + warp * 1024;
       if (NP >= 64 || half == 0) {
 #pragma unroll 1
         for (int c0 = half * kHalf; c0 < (half + 1) * kHalf; c0 += 32) {
           float v[32];
           tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + c0, v);
-          if (row < M) {
-            float* crow = g.C + row * g.ldc;
-            const float* erow = g.E ? g.E + row * g.lde : nullptr;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int col = c0 + j;
-              if (col < g.N) {
-                float o = v[j];
-                if (erow) o += erow[col];
-                if (g.relu) o = fmaxf(o, 0.f);
-                crow[col] = o;
-              }
+          for (int j = 0; j < 32; ++j) buf[lane * 32 + (j ^ lane)] = v[j];
+          __syncwarp();
+          const int col = c0 + lane;
+#pragma unroll 4
+          for (int r = 0; r < 32; ++r) {
+            const int64_t row = m0 + quad * 32 + r;
+            if (row < M && col < g.N) {
+              float o = buf[r * 32 + (lane ^ r)];
+              if (g.E) o += g.E[row * g.lde + col];
+              if (g.relu) o = fmaxf(o, 0.f);
+              g.C[row * g.ldc + col] = o;
             }
           }
+          __syncwarp();
         }
       }
     }

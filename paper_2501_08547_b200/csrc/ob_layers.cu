@@ -157,7 +157,7 @@ struct AggArgs {
 template <int OP, int NV>
 __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
-  constexpr int kU = 4;  // edges whose rows are in flight together
+  constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   const int lane = threadIdx.x & 31;
   const int64_t D = a.cnt->D;
   const int64_t items = a.cnt->items;
