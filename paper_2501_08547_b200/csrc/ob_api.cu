@@ -23,6 +23,7 @@ namespace ob {
 static thread_local std::string t_err;
 
 Engine::~Engine() {
+  cgp_destroy(*this);
   if (arena.base) cudaFree(arena.base);
   for (void* p : owned) cudaFree(p);
   for (auto& ev_ : ev)
@@ -108,6 +109,7 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.rq_src = a.take<int32_t>(m + 1);
   w.big_list = a.take<int32_t>(p.RB_max + 1);
   w.big_cptr = a.take<int64_t>(p.RB_max + 2);
+  w.rq_ctr = a.take<int64_t>(4);
   w.sort_tmp = a.take<int32_t>(m + 1);
   w.sbits = a.take<uint32_t>(p.words_NB + 1);
   w.swpre = a.take<int64_t>(p.words_NB + 1);
@@ -176,6 +178,7 @@ static void prepare_workspace(Engine& e, int B, int64_t m) {
   dry.base = nullptr;
   dry.cap = (size_t)-1 / 2;
   carve(e, w, p, dry);
+  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) carve_cgp(e, w, dry);
   size_t need = dry.used + (1u << 20);
   if (need > e.arena.cap) {
     OB_CUDA(cudaStreamSynchronize(e.stream));
@@ -190,6 +193,7 @@ static void prepare_workspace(Engine& e, int B, int64_t m) {
   }
   e.arena.used = 0;
   carve(e, w, p, e.arena);
+  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) carve_cgp(e, w, e.arena);
 }
 
 static void check_ready(Engine& e) {
@@ -244,14 +248,18 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   OB_CUDA(cudaEventRecord(e.ev[0], s));
   OB_CUDA(cudaMemsetAsync(w.rc, 0, sizeof(ReqCounters), s));
   for (auto& b : w.blocks) OB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(BlockCounters), s));
-  stage_request_prep(e, w, srpe);
-  if (srpe) stage_select(e, w);
-  stage_request_csr(e, w);
-  if (srpe) stage_build_srpe(e, w);
-  else stage_build_full(e, w);
-  OB_CUDA(cudaEventRecord(e.ev[1], s));
-  // per-layer fetch counters live in per-layer copies of the block counters
-  stage_forward(e, w, d_out);
+  const bool cgp = e.cfg.strategy == OB_STRATEGY_SRPE_CGP;
+  if (cgp) {
+    serve_cgp(e, d_out);  // records ev[1] between build and layers
+  } else {
+    stage_request_prep(e, w, srpe);
+    if (srpe) stage_select(e, w);
+    stage_request_csr(e, w);
+    if (srpe) stage_build_srpe(e, w);
+    else stage_build_full(e, w);
+    OB_CUDA(cudaEventRecord(e.ev[1], s));
+    stage_forward(e, w, d_out);
+  }
   OB_CUDA(cudaEventRecord(e.ev[2], s));
   prof_end(s, preq, kProfRequest, nullptr, 0, 0, 0, 0, 0);
   if (g_prof) g_prof->request_end(s);
@@ -260,29 +268,51 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   if (!bd) return;
   PinnedReadback hb{};
   OB_CUDA(cudaMemcpyAsync(&hb.rc, w.rc, sizeof(ReqCounters), cudaMemcpyDeviceToHost, s));
-  for (size_t i = 0; i < w.blocks.size(); ++i)
-    OB_CUDA(cudaMemcpyAsync(&hb.bc[i], w.blocks[i].cnt, sizeof(BlockCounters), cudaMemcpyDeviceToHost, s));
+  std::vector<BlockDev*> all;  // centralized blocks, or every partition's (mid, last)
+  if (cgp) {
+    for (auto& pw : e.cgp.ws) all.insert(all.end(), {&pw.blocks[0], &pw.blocks[1]});
+  } else {
+    for (auto& b : w.blocks) all.push_back(&b);
+  }
+  std::vector<BlockCounters> hc(all.size());
+  for (size_t i = 0; i < all.size(); ++i)
+    OB_CUDA(cudaMemcpyAsync(&hc[i], all[i]->cnt, sizeof(BlockCounters), cudaMemcpyDeviceToHost, s));
   OB_CUDA(cudaStreamSynchronize(s));
   OB_CUDA(cudaGetLastError());
-  for (size_t i = 0; i < w.blocks.size(); ++i) w.blocks[i].host = hb.bc[i];
+  for (size_t i = 0; i < all.size(); ++i) all[i]->host = hc[i];
   raise_request_errors(hb.rc);
   float t01 = 0, t12 = 0;
   OB_CUDA(cudaEventElapsedTime(&t01, e.ev[0], e.ev[1]));
   OB_CUDA(cudaEventElapsedTime(&t12, e.ev[1], e.ev[2]));
-  std::vector<BlockCounters> per_layer(k);
-  for (int l = 1; l <= k; ++l) per_layer[l - 1] = w.blocks[w.block_of_layer[l - 1]].host;
-  if (srpe) {
-    // the shared mid block accumulated layer 1's FEATURE rows and layers 2..k-1's PE rows
-    const BlockCounters& mid = w.blocks[0].host;
-    for (int l = 1; l < k; ++l) {
-      per_layer[l - 1].feat_src = (l == 1) ? mid.feat_src : 0;
-      per_layer[l - 1].pe_src = (l == 1) ? 0 : mid.pe_src / std::max(1, k - 2);
+  // graph_fetch_bytes per block set (runtime.py:105-120; CGP: _shard_fetch_bytes summed, :224-247)
+  auto set_bytes = [&](const BlockCounters* blocks_of_layer[], const BlockCounters& mid) {
+    std::vector<BlockCounters> per_layer(k);
+    for (int l = 1; l <= k; ++l) per_layer[l - 1] = *blocks_of_layer[l - 1];
+    if (srpe) {
+      // the shared mid block accumulated layer 1's FEATURE rows and layers 2..k-1's PE rows
+      for (int l = 1; l < k; ++l) {
+        per_layer[l - 1].feat_src = (l == 1) ? mid.feat_src : 0;
+        per_layer[l - 1].pe_src = (l == 1) ? 0 : mid.pe_src / std::max(1, k - 2);
+      }
     }
+    return fetch_bytes(e, w, per_layer);
+  };
+  int64_t fb = 0;
+  std::vector<const BlockCounters*> bl(k);
+  if (cgp) {
+    for (auto& pw : e.cgp.ws) {
+      for (int l = 1; l <= k; ++l) bl[l - 1] = &pw.blocks[l < k ? 0 : 1].host;
+      fb += set_bytes(bl.data(), pw.blocks[0].host);
+    }
+  } else {
+    for (int l = 1; l <= k; ++l) bl[l - 1] = &w.blocks[w.block_of_layer[l - 1]].host;
+    fb = set_bytes(bl.data(), w.blocks[0].host);
   }
   std::memset(bd, 0, sizeof(*bd));
   bd->fetch_ms = t01;
   bd->compute_ms = t12;
-  bd->fetch_bytes = fetch_bytes(e, w, per_layer);
+  bd->fetch_bytes = fb;
+  bd->collective_bytes = e.cgp.collective_bytes;
   bd->transfer_ms = (double)bd->fetch_bytes / 12e9 * 1e3;
   bd->num_candidates = hb.rc.R;
   bd->num_targets = hb.rc.T;
@@ -366,6 +396,16 @@ static void load_model(Engine& e, int k, const ob_layer* layers, const float* co
       prep_tc_weights(e, {mats[mi]}, {in}, o, &L.tw_main);
       L.a_src = (float*)e.dalloc(sizeof(float) * o);
       L.a_dst = (float*)e.dalloc(sizeof(float) * o);
+      {  // W a_dst for owner-side destination scores under CGP (models.py:199-200 reassociated)
+        std::vector<float> wa(in);
+        for (int i = 0; i < in; ++i) {
+          double acc = 0.0;
+          for (int j = 0; j < o; ++j) acc += (double)mats[mi][(size_t)i * o + j] * (double)mats[mi + 2][j];
+          wa[i] = (float)acc;
+        }
+        L.wa_dst = (float*)e.dalloc(sizeof(float) * in);
+        OB_CUDA(cudaMemcpy(L.wa_dst, wa.data(), sizeof(float) * in, cudaMemcpyHostToDevice));
+      }
       OB_CUDA(cudaMemcpy(L.a_src, mats[mi + 1], sizeof(float) * o, cudaMemcpyHostToDevice));
       OB_CUDA(cudaMemcpy(L.a_dst, mats[mi + 2], sizeof(float) * o, cudaMemcpyHostToDevice));
     } else if (L.transform_first) {
@@ -460,7 +500,8 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
     OB_CHECK(cfg->num_partitions >= 1, OB_EINVAL, "num_partitions must be >= 1");
     OB_CHECK(cfg->strategy == OB_STRATEGY_SRPE_CGP || cfg->num_partitions == 1, OB_EINVAL,
              "num_partitions > 1 needs strategy srpe-cgp");
-    OB_CHECK(cfg->strategy != OB_STRATEGY_SRPE_CGP, OB_EINVAL, "srpe-cgp is not built into this library yet");
+    OB_CHECK(cfg->nccl_id == nullptr || (cfg->rank >= 0 && cfg->rank < cfg->num_partitions), OB_EINVAL,
+             "rank out of range");
     int ndev = 0;
     OB_CUDA(cudaGetDeviceCount(&ndev));
     OB_CHECK(cfg->device >= 0 && cfg->device < ndev, OB_EINVAL, "no such CUDA device");
@@ -475,6 +516,14 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
       e.own_stream = true;
     }
     for (auto& ev_ : e.ev) OB_CUDA(cudaEventCreate(&ev_));
+    if (cfg->nccl_id && cfg->strategy == OB_STRATEGY_SRPE_CGP) {
+      try {
+        cgp_init_comm(e);
+      } catch (...) {
+        delete h;
+        throw;
+      }
+    }
     *out = h;
   });
 }
@@ -497,6 +546,7 @@ int ob_load_graph(ob_engine* h, int64_t N, const int64_t* off, const int64_t* nb
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
     load_graph(h->impl, N, off, nb, E, feats, F);
+    if (h->impl.cfg.strategy == OB_STRATEGY_SRPE_CGP) cgp_build_partitions(h->impl);
   });
 }
 
@@ -633,16 +683,30 @@ int ob_last_plan(ob_engine* h, int64_t* nc, int64_t* nt, int64_t* ids, int64_t* 
   });
 }
 
+// the block that fed `layer` on partition `part` (centralized: part 0)
+static BlockDev& block_of(Engine& e, int part, int layer) {
+  OB_CHECK(e.have_request, OB_ESTATE, "no request served");
+  OB_CHECK(layer >= 1 && layer <= (int)e.layers.size(), OB_EINVAL, "layer out of range");
+  const int k = (int)e.layers.size();
+  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) {
+    const CgpState& c = e.cgp;
+    int idx = -1;
+    for (size_t i = 0; i < c.parts.size(); ++i)
+      if (c.parts[i].rank == part) idx = (int)i;
+    OB_CHECK(idx >= 0, OB_EINVAL, "partition not held by this engine");
+    return e.cgp.ws[idx].blocks[layer < k ? 0 : 1];
+  }
+  OB_CHECK(part == 0, OB_EINVAL, "partition index out of range");
+  return e.ws.blocks[e.ws.block_of_layer[layer - 1]];
+}
+
 int ob_last_block_sizes(ob_engine* h, int32_t part, int32_t layer, int64_t* ns, int64_t* nd, int64_t* ne) {
   return guarded([&] {
     OB_CHECK(h && ns && nd && ne, OB_EINVAL, "null argument");
     std::lock_guard<std::mutex> lk(h->mu);
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
-    OB_CHECK(e.have_request, OB_ESTATE, "no request served");
-    OB_CHECK(part == 0, OB_EINVAL, "partition index out of range");
-    OB_CHECK(layer >= 1 && layer <= (int)e.layers.size(), OB_EINVAL, "layer out of range");
-    BlockDev& b = e.ws.blocks[e.ws.block_of_layer[layer - 1]];
+    BlockDev& b = block_of(e, part, layer);
     BlockCounters c = d2h(b.cnt, 1, e.stream)[0];
     *ns = c.S;
     *nd = c.D;
@@ -658,11 +722,8 @@ int ob_last_block(ob_engine* h, int32_t part, int32_t layer, int64_t* src_ids, i
     std::lock_guard<std::mutex> lk(h->mu);
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
-    OB_CHECK(e.have_request, OB_ESTATE, "no request served");
-    OB_CHECK(part == 0, OB_EINVAL, "partition index out of range");
-    OB_CHECK(layer >= 1 && layer <= (int)e.layers.size(), OB_EINVAL, "layer out of range");
     RequestWs& w = e.ws;
-    BlockDev& b = w.blocks[w.block_of_layer[layer - 1]];
+    BlockDev& b = block_of(e, part, layer);
     cudaStream_t s = e.stream;
     BlockCounters c = d2h(b.cnt, 1, s)[0];
     auto cp32 = [&](const int32_t* d, int64_t n, int64_t* o) {
@@ -686,7 +747,7 @@ int ob_last_block(ob_engine* h, int32_t part, int32_t layer, int64_t* src_ids, i
       OB_CUDA(cudaMalloc(&dk, std::max<int64_t>(c.S, 1)));
       OB_CUDA(cudaMalloc(&dp, sizeof(int32_t) * std::max<int64_t>(c.S, 1)));
       OB_CUDA(cudaMalloc(&dd, sizeof(int64_t) * std::max<int64_t>(c.S, 1)));
-      export_bindings(e, w, layer, dk, dp);
+      export_bindings(e, w, b, layer, dk, dp);
       k_src_degree<<<grid_for(std::max<int64_t>(c.S, 1), 256), 256, 0, s>>>(b.src_ids, b.cnt, e.g.N, e.g.indeg,
                                                                              w.qdeg, dd);
       OB_LAUNCHED();
@@ -768,7 +829,12 @@ int ob_profile_read(ob_engine* h, int32_t cls, double* total_ms, int64_t* launch
 int ob_partition_owner(ob_engine* h, int64_t* owner) {
   return guarded([&] {
     OB_CHECK(h && owner, OB_EINVAL, "null argument");
-    OB_CHECK(false, OB_ESTATE, "engine is not partitioned");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(e.cfg.strategy == OB_STRATEGY_SRPE_CGP && e.cgp.owner, OB_ESTATE, "engine is not partitioned");
+    auto v = d2h(e.cgp.owner, e.g.N, e.stream);
+    for (int64_t i = 0; i < e.g.N; ++i) owner[i] = v[i];
   });
 }
 

@@ -143,9 +143,10 @@ void block_items(Engine& e, BlockDev& b, int64_t chunk) {
               &b.cnt->groups, b.group_ptr);
 }
 
-// generic block assembly over an already written dst list + counts->D
-static void assemble(Engine& e, RequestWs& w, BlockDev& b, const int64_t* offsets, const int32_t* nbrs,
-                     const int32_t* indeg) {
+// generic block assembly over an already written dst list + counts->D.
+// `src` names the CSR the destinations pull from (the whole graph, or a CGP
+// rank's source-split CSR) and the request CSR (whole request or the rank's slice).
+void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
   cudaStream_t s = e.stream;
   SegSpans sp;
   Arena& a = e.arena;
@@ -154,12 +155,12 @@ static void assemble(Engine& e, RequestWs& w, BlockDev& b, const int64_t* offset
   sp.cl = a.take<int32_t>(b.D_max);
   sp.rs = a.take<int64_t>(b.D_max);
   sp.rl = a.take<int32_t>(b.D_max);
-  k_block_spans<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, e.g.N, offsets, indeg, w.cbits, w.cwpre,
-                                                        w.rq_ptr, w.rc, sp, w.seg_len);
+  k_block_spans<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, e.g.N, src.offsets, src.deg, w.cbits,
+                                                        w.cwpre, src.rq_ptr, w.rc, sp, w.seg_len);
   OB_LAUNCHED();
   device_scan(s, e.scan, LoadI64{w.seg_len}, StoreI64{b.dst_ptr}, &b.cnt->D, 0, b.D_max, &b.cnt->E, b.dst_ptr);
   OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
-  k_block_fill<<<grid_for(b.E_max, 32 * kFillPerLane * 8), 256, 0, s>>>(b.cnt, b.dst_ptr, sp, nbrs, w.rq_src,
+  k_block_fill<<<grid_for(b.E_max, 32 * kFillPerLane * 8), 256, 0, s>>>(b.cnt, b.dst_ptr, sp, src.nbrs, src.rq_src,
                                                                          w.src_global, w.sbits);
   OB_LAUNCHED();
   if (b.has_self) {
@@ -178,28 +179,31 @@ static void assemble(Engine& e, RequestWs& w, BlockDev& b, const int64_t* offset
   a.used = mark;  // spans are transient
 }
 
+void write_mid_dst(Engine& e, RequestWs& w, BlockDev& b) {
+  k_mid_dst<<<grid_for(b.D_max, 256), 256, 0, e.stream>>>(w.rc, e.g.N, w.B, w.targets, b.dst_ids, b.cnt);
+  OB_LAUNCHED();
+}
+
+void write_query_dst(Engine& e, RequestWs& w, BlockDev& b) {
+  k_query_dst<<<grid_for(w.B, 256), 256, 0, e.stream>>>(e.g.N, w.B, b.dst_ids, b.cnt);
+  OB_LAUNCHED();
+}
+
 void stage_build_srpe(Engine& e, RequestWs& w) {
-  cudaStream_t s = e.stream;
-  const int k = (int)e.layers.size();
   // blocks[0] = shared mid block (layers 1..k-1), blocks[1] = last block (layer k)
-  BlockDev& mid = w.blocks[0];
-  BlockDev& last = w.blocks[1];
-  k_mid_dst<<<grid_for(mid.D_max, 256), 256, 0, s>>>(w.rc, e.g.N, w.B, w.targets, mid.dst_ids, mid.cnt);
-  OB_LAUNCHED();
-  assemble(e, w, mid, e.g.offsets, e.g.nbrs, e.g.indeg);
-  k_query_dst<<<grid_for(w.B, 256), 256, 0, s>>>(e.g.N, w.B, last.dst_ids, last.cnt);
-  OB_LAUNCHED();
-  assemble(e, w, last, e.g.offsets, e.g.nbrs, e.g.indeg);
-  (void)k;
+  const SpanSrc src{e.g.offsets, e.g.nbrs, e.g.indeg, w.rq_ptr, w.rq_src};
+  write_mid_dst(e, w, w.blocks[0]);
+  assemble(e, w, w.blocks[0], src);
+  write_query_dst(e, w, w.blocks[1]);
+  assemble(e, w, w.blocks[1], src);
 }
 
 void stage_build_full(Engine& e, RequestWs& w) {
   cudaStream_t s = e.stream;
   const int k = (int)e.layers.size();
+  const SpanSrc src{e.g.offsets, e.g.nbrs, e.g.indeg, w.rq_ptr, w.rq_src};
   // blocks[l-1] feeds layer l; block k's dst = queries; block l-1's dst = block l's sources
-  BlockDev& top = w.blocks[k - 1];
-  k_query_dst<<<grid_for(w.B, 256), 256, 0, s>>>(e.g.N, w.B, top.dst_ids, top.cnt);
-  OB_LAUNCHED();
+  write_query_dst(e, w, w.blocks[k - 1]);
   for (int l = k; l >= 1; --l) {
     BlockDev& b = w.blocks[l - 1];
     if (l < k) {
@@ -208,7 +212,7 @@ void stage_build_full(Engine& e, RequestWs& w) {
       k_copy_count_D<<<1, 1, 0, s>>>(b.cnt, up.cnt);
       OB_LAUNCHED();
     }
-    assemble(e, w, b, e.g.offsets, e.g.nbrs, e.g.indeg);
+    assemble(e, w, b, src);
   }
 }
 

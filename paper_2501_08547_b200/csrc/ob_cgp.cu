@@ -1,0 +1,409 @@
+// ob_cgp.cu -- computation-graph parallelism (CGP) on B200s.
+//
+// Reference (paths relative to /root/reference/pkg/src/gnnserve):
+//   partition_random_hash    graphstore.py:219-263  owner = splitmix64(v ^ splitmix64(seed)) % P,
+//                                                   edges stored at their source's owner
+//   partition_request        compgraph.py:367-392   request edge -> owner of its source
+//   select_targets_distributed runtime.py:151-192   identical plan on every rank
+//   build_partitioned        compgraph.py:395-459   global dst lists, local sources only
+//   execute_layer/_model     cgpexec.py:308-439     local partials -> owner merge -> update
+//
+// B200 mapping.  Every rank receives the whole request (it is small next to the
+// graph), so candidate scoring and the top-k run redundantly and identically on
+// every rank -- the reference's stats all-gather disappears.  A rank builds the
+// part of both blocks whose sources it owns (its source-split CSR + its request
+// slice) with the same device builder as the centralized path, aggregates
+// locally into one raw partial per destination (sum / max / softmax triple), and
+// the partials are combined across ranks:
+//   * NCCL mode (one process per GPU, ob_config.nccl_id): ncclAllReduce over
+//     NVLink/NVSwitch on destination-indexed buffers padded to the request bound
+//     (sum; max for sage_max; max-then-rescaled-sum for the softmax triple), so no
+//     host-side sizes are needed; owners then update their destinations and the
+//     query rows reduce to rank 0;
+//   * emulation (nccl_id == NULL, P > 1): all P partitions run on this device and
+//     the merge walks the P partials in ascending rank order (cgpexec.py:189-240).
+#include <algorithm>
+#include <cmath>
+
+#include "ob_engine.h"
+
+#ifdef OB_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace ob {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser (graphstore.py:25-30)
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_owner(int64_t N, int P, uint64_t seed, int32_t* owner) {
+  const uint64_t key = mix64(seed);
+  OB_GRID_STRIDE(v, N) owner[v] = (int32_t)(mix64((uint64_t)v ^ key) % (uint64_t)P);
+}
+
+// per destination row: number of in-neighbours owned by partition r (warp per row)
+__global__ void k_part_deg(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
+                           const int32_t* __restrict__ owner, int r, int32_t* deg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = gw; v < N; v += nw) {
+    int c = 0;
+    for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) c += owner[nbrs[e]] == r;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) deg[v] = c;
+  }
+}
+
+// ordered compaction of the owned in-neighbours (ascending order preserved)
+__global__ void k_part_fill(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
+                            const int32_t* __restrict__ owner, int r, const int64_t* __restrict__ poff,
+                            int32_t* psrc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = gw; v < N; v += nw) {
+    int64_t out = poff[v];
+    for (int64_t e0 = off[v]; e0 < off[v + 1]; e0 += 32) {
+      const int64_t e = e0 + lane;
+      const bool keep = e < off[v + 1] && owner[nbrs[e]] == r;
+      const unsigned b = __ballot_sync(0xffffffffu, keep);
+      if (keep) psrc[out + __popc(b & ((1u << lane) - 1u))] = nbrs[e];
+      out += __popc(b);
+    }
+  }
+}
+
+void cgp_build_partitions(Engine& e) {
+  CgpState& c = e.cgp;
+  cudaStream_t s = e.stream;
+  const int64_t N = e.g.N;
+  c.P = e.cfg.num_partitions;
+  c.nccl = e.cfg.nccl_id != nullptr;
+  c.my_rank = c.nccl ? e.cfg.rank : 0;
+  c.owner = (int32_t*)e.dalloc(sizeof(int32_t) * N);
+  k_owner<<<grid_for(N, 256), 256, 0, s>>>(N, c.P, e.cfg.seed, c.owner);
+  OB_LAUNCHED();
+  ScanScratch sc;
+  sc.max_tiles = N / kScanTile + 2;
+  sc.tile_sums = (int64_t*)e.dalloc(sizeof(int64_t) * (sc.max_tiles + 1));
+  int64_t* total = (int64_t*)e.dalloc(sizeof(int64_t));
+  c.parts.clear();
+  for (int r = 0; r < c.P; ++r) {
+    if (c.nccl && r != c.my_rank) continue;
+    PartitionDev p;
+    p.rank = r;
+    p.deg = (int32_t*)e.dalloc(sizeof(int32_t) * N);
+    p.off = (int64_t*)e.dalloc(sizeof(int64_t) * (N + 1));
+    k_part_deg<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, c.owner, r, p.deg);
+    OB_LAUNCHED();
+    device_scan(s, sc, LoadI32{p.deg}, StoreI64{p.off}, nullptr, N, N, total, p.off);
+    OB_CUDA(cudaMemcpyAsync(&p.E, total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    OB_CUDA(cudaStreamSynchronize(s));
+    p.src = (int32_t*)e.dalloc(sizeof(int32_t) * std::max<int64_t>(p.E, 1));
+    k_part_fill<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, c.owner, r, p.off, p.src);
+    OB_LAUNCHED();
+    c.parts.push_back(p);
+  }
+  OB_CUDA(cudaStreamSynchronize(s));
+}
+
+// request slice of partition r: edges whose source it owns (queries: round robin)
+__global__ void k_filter_slice(const int64_t* __restrict__ edges, int64_t m, int64_t N, int P, int r,
+                               const int32_t* __restrict__ owner, const ReqCounters* rc, int64_t* out,
+                               int64_t* count) {
+  if (rc->err & (kErrRange | kErrNoQuery)) return;
+  OB_GRID_STRIDE(e, m) {
+    const int64_t s = edges[2 * e];
+    const int o = s >= N ? (int)((s - N) % P) : owner[s];
+    const bool keep = o == r;
+    const unsigned act = __activemask();
+    const unsigned b = __ballot_sync(act, keep);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(act) - 1;
+    int64_t base = 0;
+    if (lane == leader && b) base = (int64_t)atomicAdd((unsigned long long*)count, (unsigned long long)__popc(b));
+    base = __shfl_sync(act, base, leader);
+    if (keep) {
+      const int64_t at = base + __popc(b & ((1u << lane) - 1u));
+      out[2 * at] = s;
+      out[2 * at + 1] = edges[2 * e + 1];
+    }
+  }
+}
+
+// destination rows h_v for a layer (dst-indexed); non-owned rows read a zero row
+__global__ void k_dst_rows(const int32_t* __restrict__ dst_ids, const int64_t* D_dev, int64_t N, int layer, int k,
+                           const float* feats, const float* qpad, int64_t F_ld, const float* prev, int64_t in_ld,
+                           const int64_t* T_dev, const int32_t* owner, int P, int rank, const float* zero,
+                           const float** hvp) {
+  const int64_t D = *D_dev, T = *T_dev;
+  OB_GRID_STRIDE(i, D) {
+    const int64_t g = dst_ids[i];
+    bool mine = true;
+    if (owner) mine = (g >= N ? (int)((g - N) % P) : owner[g]) == rank;
+    const float* r;
+    if (!mine) r = zero;
+    else if (layer == 1) r = g < N ? feats + g * F_ld : qpad + (g - N) * F_ld;
+    else if (layer == k) r = prev + (T + (g - N)) * in_ld;  // last block: queries in the mid table
+    else r = prev + i * in_ld;                              // mid blocks share one destination list
+    hvp[i] = r;
+  }
+}
+
+__global__ void k_rowdot_ptr(const int64_t* M_dev, const float* const* rows, int w, const float* __restrict__ av,
+                             float* out) {
+  const int64_t M = *M_dev;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < M; r += nw) {
+    const float* row = rows[r];
+    float s = 0.f;
+    for (int c = lane; c < w; c += 32) s = fmaf(row[c], av[c], s);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[r] = s;
+  }
+}
+
+// softmax exchange: pull the max-logit column out, then rescale (den, num) to the
+// global max so the triples can be summed (cgpexec.py:225-239)
+__global__ void k_sm_extract(const int64_t* D_dev, const float* lp, int64_t ldp, float* lmax) {
+  const int64_t D = *D_dev;
+  OB_GRID_STRIDE(i, D) lmax[i] = lp[i * ldp + 1] > 0.f ? lp[i * ldp] : -INFINITY;
+}
+__global__ void k_sm_rescale(const int64_t* D_dev, float* lp, int64_t ldp, int w, const float* gmax) {
+  const int64_t D = *D_dev;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < D; i += nw) {
+    float* o = lp + i * ldp;
+    const float sc = o[1] > 0.f ? __expf(o[0] - gmax[i]) : 0.f;
+    __syncwarp();
+    for (int c = lane; c < w; c += 32) o[2 + c] *= sc;
+    __syncwarp();
+    if (lane == 0) {
+      o[1] *= sc;
+      o[0] = 0.f;
+    }
+  }
+}
+__global__ void k_sm_restore(const int64_t* D_dev, float* lp, int64_t ldp, const float* gmax) {
+  const int64_t D = *D_dev;
+  OB_GRID_STRIDE(i, D) lp[i * ldp] = gmax[i];
+}
+
+// final rows: zero the queries this rank does not own before the reduce to rank 0
+__global__ void k_zero_foreign_queries(float* rows, int B, int H, int P, int rank) {
+  const int64_t n = (int64_t)B * H;
+  OB_GRID_STRIDE(i, n) if ((int)((i / H) % P) != rank) rows[i] = 0.f;
+}
+
+void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
+  CgpState& c = e.cgp;
+  const int np = (int)c.parts.size();
+  const BlockDev& mid = w.blocks[0];
+  const BlockDev& last = w.blocks[1];
+  c.ws.assign(np, CgpPartWs{});
+  const int64_t RB_max = std::min<int64_t>(e.g.N, 2 * w.m) + w.B;
+  for (int p = 0; p < np; ++p) {
+    CgpPartWs& pw = c.ws[p];
+    pw.ledges = a.take<int64_t>(2 * w.m + 2);
+    pw.rq.cnt = a.take<int32_t>(RB_max + 1);
+    pw.rq.fill = a.take<int32_t>(RB_max + 1);
+    pw.rq.ptr = a.take<int64_t>(RB_max + 1);
+    pw.rq.src = a.take<int32_t>(w.m + 1);
+    pw.rq.big_list = a.take<int32_t>(RB_max + 1);
+    pw.rq.big_cptr = a.take<int64_t>(RB_max + 2);
+    pw.rq.sort_tmp = a.take<int32_t>(w.m + 1);
+    pw.rq.ctr = a.take<int64_t>(4);
+    for (int bi = 0; bi < 2; ++bi) {
+      BlockDev b = bi == 0 ? mid : last;
+      b.has_self = false;
+      b.cnt = a.take<BlockCounters>(1);
+      b.dst_ptr = a.take<int64_t>(b.D_max + 1);
+      b.item_ptr = a.take<int64_t>(b.D_max + 1);
+      b.group_ptr = a.take<int64_t>(b.D_max + 1);
+      b.edge_src = a.take<int32_t>(b.E_max);
+      b.src_ids = a.take<int32_t>(b.S_max);
+      b.self_src = nullptr;
+      b.dst_ids = a.take<int32_t>(b.D_max);
+      pw.blocks[bi] = b;
+    }
+  }
+  int maxw = 4;
+  bool mom = false;
+  for (auto& L : e.layers) {
+    maxw = std::max(maxw, cgp_partial_width(L));
+    mom |= L.spec.kind == OB_KIND_MOMENTS;
+  }
+  c.D_max = mid.D_max;
+  c.ldp = ld4(maxw);
+  const int64_t part_elems = c.D_max * c.ldp * (mom ? 2 : 1);
+  c.lp = a.take<float>(np * part_elems);
+  c.lcnt = a.take<float>(np * c.D_max);
+  c.hvp = a.take<const float*>(c.D_max);
+  c.zero_row = a.take<float>(ld4(std::max(e.g.F, 4)) + 512);
+  c.sdst = a.take<float>(c.D_max);
+  c.lmax = a.take<float>(c.D_max);
+  c.mean = mom ? a.take<double>(c.D_max * ld4(maxw)) : nullptr;
+  c.fin = a.take<float>((int64_t)w.B * e.layers.back().spec.out_dim + 4);
+}
+
+#ifdef OB_WITH_NCCL
+#define OB_NCCL(x)                                                                               \
+  do {                                                                                           \
+    ncclResult_t _r = (x);                                                                       \
+    if (_r != ncclSuccess) throw Error(OB_ECOMM, std::string(#x) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+#endif
+
+static void allreduce(Engine& e, void* buf, size_t count, bool is_double, bool max) {
+#ifdef OB_WITH_NCCL
+  CgpState& c = e.cgp;
+  OB_NCCL(ncclAllReduce(buf, buf, count, is_double ? ncclDouble : ncclFloat, max ? ncclMax : ncclSum,
+                        (ncclComm_t)c.comm, e.stream));
+  c.collective_bytes += (int64_t)(2.0 * (c.P - 1) / c.P * count * (is_double ? 8 : 4));
+#else
+  (void)e, (void)buf, (void)count, (void)is_double, (void)max;
+  throw Error(OB_ECOMM, "built without NCCL");
+#endif
+}
+
+void serve_cgp(Engine& e, float* d_out) {
+  CgpState& c = e.cgp;
+  RequestWs& w = e.ws;
+  cudaStream_t s = e.stream;
+  const int k = (int)e.layers.size();
+  const int np = (int)c.parts.size();
+  const int64_t N = e.g.N;
+  c.collective_bytes = 0;
+  // identical plan on every rank from the whole request (runtime.py:151-192)
+  stage_request_prep(e, w, true);
+  stage_select(e, w);
+  for (int p = 0; p < np; ++p) {
+    CgpPartWs& pw = c.ws[p];
+    const PartitionDev& part = c.parts[p];
+    OB_CUDA(cudaMemsetAsync(pw.rq.ctr, 0, sizeof(int64_t) * 4, s));
+    OB_CUDA(cudaMemsetAsync(pw.blocks[0].cnt, 0, sizeof(BlockCounters), s));
+    OB_CUDA(cudaMemsetAsync(pw.blocks[1].cnt, 0, sizeof(BlockCounters), s));
+    if (w.m > 0) {
+      k_filter_slice<<<grid_for(w.m, 256), 256, 0, s>>>(w.edges, w.m, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
+                                                         pw.rq.ctr);
+      OB_LAUNCHED();
+    }
+    build_rq_csr(e, w, pw.ledges, w.m, pw.rq.ctr, pw.rq, /*counts_ready=*/false);
+    const SpanSrc src{part.off, part.src, part.deg, pw.rq.ptr, pw.rq.src};
+    write_mid_dst(e, w, pw.blocks[0]);
+    assemble(e, w, pw.blocks[0], src);
+    write_query_dst(e, w, pw.blocks[1]);
+    assemble(e, w, pw.blocks[1], src);
+  }
+  OB_CUDA(cudaEventRecord(e.ev[1], s));
+  stage_qpad(e, w);
+  OB_CUDA(cudaMemsetAsync(c.zero_row, 0, sizeof(float) * (ld4(std::max(e.g.F, 4)) + 512), s));
+  const int64_t part_stride_f = c.D_max * c.ldp;  // floats between partitions (x2 for float64 partials)
+  for (int l = 1; l <= k; ++l) {
+    const LayerDev& L = e.layers[l - 1];
+    const int bi = l < k ? 0 : 1;
+    const BlockDev& b0 = c.ws[0].blocks[bi];
+    const int64_t* D_dev = &b0.cnt->D;
+    const int64_t D_max = b0.D_max;
+    const bool mom = L.spec.kind == OB_KIND_MOMENTS;
+    const int64_t pstride = mom ? 2 * part_stride_f : part_stride_f;
+    BindCtx bc = bind_ctx(e, w, l);
+    // destination rows h_v (owned ones; zero row elsewhere under NCCL)
+    k_dst_rows<<<grid_for(D_max, 256), 256, 0, s>>>(b0.dst_ids, D_dev, N, l, k, e.g.feats, w.qpad, e.g.F_ld,
+                                                    l > 1 ? w.outs[l - 1] : nullptr, ld4(L.spec.in_dim), &w.rc->T,
+                                                    c.nccl ? c.owner : nullptr, c.P, c.my_rank, c.zero_row, c.hvp);
+    OB_LAUNCHED();
+    if (L.spec.kind == OB_KIND_GAT) {  // s_dst = h_v . (W a_dst), computed by the owner
+      k_rowdot_ptr<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.hvp, L.spec.in_dim, L.wa_dst, c.sdst);
+      OB_LAUNCHED();
+      if (c.nccl) allreduce(e, c.sdst, D_max, false, false);
+    }
+    const int phases = mom ? 2 : 1;
+    for (int ph = 1; ph <= phases; ++ph) {
+      for (int p = 0; p < np; ++p) {
+        const BlockDev& b = c.ws[p].blocks[bi];
+        launch_resolve(s, bc, b.cnt, b.S_max, b.src_ids, w.rowp, w.gscale);
+        LayerRun r{};
+        r.cnt = b.cnt;
+        r.D_dev = &b.cnt->D;
+        r.S_dev = &b.cnt->S;
+        r.D_max = b.D_max;
+        r.S_max = b.S_max;
+        r.items_max = b.items_max;
+        r.dst_ptr = b.dst_ptr;
+        r.item_ptr = b.item_ptr;
+        r.edge_src = b.edge_src;
+        r.self = nullptr;
+        r.x = RowSrc{w.rowp, nullptr, 0};
+        r.gscale = w.gscale;
+        r.group_ptr = b.group_ptr;
+        LayerScratch sc{w.partial, w.partial2, w.agg, w.mean, w.z, w.s_src, w.s_dst};
+        cgp_local_partial(s, L, r, sc, c.sdst, c.lp + p * pstride, c.ldp, c.lcnt + p * c.D_max, ph, c.mean);
+      }
+      int Pm = np;
+      if (c.nccl) {
+        const int64_t pw = cgp_partial_width(L);
+        if (L.spec.kind == OB_KIND_GAT) {
+          k_sm_extract<<<grid_for(D_max, 256), 256, 0, s>>>(D_dev, c.lp, c.ldp, c.lmax);
+          OB_LAUNCHED();
+          allreduce(e, c.lmax, D_max, false, true);
+          k_sm_rescale<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.lp, c.ldp, (int)pw - 2, c.lmax);
+          OB_LAUNCHED();
+          allreduce(e, c.lp, D_max * c.ldp, false, false);
+          k_sm_restore<<<grid_for(D_max, 256), 256, 0, s>>>(D_dev, c.lp, c.ldp, c.lmax);
+          OB_LAUNCHED();
+        } else if (L.spec.kind == OB_KIND_SAGE_MAX) {
+          allreduce(e, c.lp, D_max * c.ldp, false, true);  // empty partials hold -inf
+        } else {
+          allreduce(e, c.lp, D_max * c.ldp, mom, false);
+        }
+        allreduce(e, c.lcnt, D_max, false, false);
+        Pm = 1;
+      }
+      const bool last = l == k;
+      float* out = last ? (c.nccl ? c.fin : d_out) : w.outs[l];
+      const int64_t ldo = last ? L.spec.out_dim : ld4(L.spec.out_dim);
+      cgp_merge(s, L, Pm, c.lp, pstride, c.ldp, c.lcnt, c.D_max, D_dev, D_max, w.agg, out, ldo, ph, c.mean);
+      if (ph == phases) cgp_update(s, L, D_dev, D_max, c.hvp, w.agg, out, ldo);
+    }
+  }
+#ifdef OB_WITH_NCCL
+  if (c.nccl) {
+    const int H = e.layers.back().spec.out_dim;
+    k_zero_foreign_queries<<<grid_for((int64_t)w.B * H, 256), 256, 0, s>>>(c.fin, w.B, H, c.P, c.my_rank);
+    OB_LAUNCHED();
+    OB_NCCL(ncclReduce(c.fin, d_out, (size_t)w.B * H, ncclFloat, ncclSum, 0, (ncclComm_t)c.comm, s));
+    c.collective_bytes += (int64_t)w.B * H * 4;
+  }
+#endif
+}
+
+void cgp_init_comm(Engine& e) {
+#ifdef OB_WITH_NCCL
+  ncclUniqueId id;
+  std::memcpy(&id, e.cfg.nccl_id, sizeof(id));
+  ncclComm_t comm;
+  OB_NCCL(ncclCommInitRank(&comm, e.cfg.num_partitions, id, e.cfg.rank));
+  e.cgp.comm = comm;
+#else
+  throw Error(OB_ECOMM, "built without NCCL");
+#endif
+}
+
+void cgp_destroy(Engine& e) {
+#ifdef OB_WITH_NCCL
+  if (e.cgp.comm) ncclCommDestroy((ncclComm_t)e.cgp.comm);
+#endif
+  e.cgp.comm = nullptr;
+}
+
+}  // namespace ob

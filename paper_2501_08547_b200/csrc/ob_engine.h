@@ -110,6 +110,7 @@ struct LayerDev {
   ob_layer spec{};
   float* a_src = nullptr;   // gat
   float* a_dst = nullptr;   // gat
+  float* wa_dst = nullptr;  // gat: W a_dst (in_dim), s_dst = h_v . (W a_dst) for CGP owners
   bool transform_first = false;  // gcn / sage_mean with in > out: aggregate X W instead of X
   TcWeights tw_main;        // aggregate-first update ([W_self; W_neigh] or W) / gcn-gat W / tf: W_neigh
   TcWeights tw_self;        // transform-first sage_mean: W_self
@@ -145,6 +146,18 @@ struct Arena {
   }
 };
 
+// Request sources bucketed by destination slot (slot: candidate rank, or R + query).
+struct RqCsr {
+  int32_t* cnt = nullptr;       // [RB]
+  int32_t* fill = nullptr;      // [RB]
+  int64_t* ptr = nullptr;       // [RB+1]
+  int32_t* src = nullptr;       // [m] ascending within a slot after the sort
+  int32_t* big_list = nullptr;  // long segments
+  int64_t* big_cptr = nullptr;  // chunk prefix over big_list
+  int32_t* sort_tmp = nullptr;  // [m]
+  int64_t* ctr = nullptr;       // device [4]: m (edge count), n_big, n_chunks, spare
+};
+
 // Per-request device workspace for the centralized pipeline.
 struct RequestWs {
   int B = 0;
@@ -174,6 +187,19 @@ struct RequestWs {
   int32_t* big_list = nullptr;     // segments for the CTA sort
   int64_t* big_cptr = nullptr;     // chunk prefix over big_list
   int32_t* sort_tmp = nullptr;     // [m] scratch for the big-segment merge
+  int64_t* rq_ctr = nullptr;       // [4] csr counters
+  RqCsr rq_view() const {
+    RqCsr c;
+    c.cnt = rq_cnt;
+    c.fill = rq_fill;
+    c.ptr = rq_ptr;
+    c.src = rq_src;
+    c.big_list = big_list;
+    c.big_cptr = big_cptr;
+    c.sort_tmp = sort_tmp;
+    c.ctr = rq_ctr;
+    return c;
+  }
   // block scratch
   uint32_t* sbits = nullptr;       // source bitmap over [0, N+B)
   int64_t* swpre = nullptr;
@@ -228,6 +254,68 @@ cudaEvent_t prof_begin(cudaStream_t s);
 void prof_end(cudaStream_t s, cudaEvent_t a, int cls, const BlockCounters* cnt, int width, int pw, int K, int Nc,
               int gemm_rows);
 
+
+// layer execution building blocks (ob_layers.cu), shared with CGP (ob_cgp.cu) ---------
+struct BindCtx {
+  int mode;             // 0 = srpe, 1 = full (computed rows follow the source order)
+  int layer;            // 1-based
+  int64_t N;
+  int64_t F_ld;
+  const float* feats;   // N x F_ld
+  const float* qfeat;   // B x F_ld
+  const float* pe;      // stored layer (layer-1) rows, N x in_ld
+  const float* prev;    // previous layer output, rows x in_ld
+  int64_t in_ld;
+  const int64_t* T_dev; // srpe: computed rows = [targets..., queries...]
+  const uint32_t* cbits;
+  const int64_t* cwpre;
+  const int32_t* tpos;
+  const int32_t* indeg;
+  const int32_t* qdeg;
+};
+
+struct LayerRun {
+  const BlockCounters* cnt;  // D, E, S, items (device)
+  const int64_t* D_dev;
+  const int64_t* S_dev;
+  int64_t D_max, S_max, items_max;
+  const int64_t* dst_ptr;
+  const int64_t* item_ptr;
+  const int32_t* edge_src;
+  const int32_t* self;       // null = identity
+  RowSrc x;                  // bound inputs
+  const float* gscale;       // gcn
+  const int64_t* group_ptr;  // second-level partial groups (hub destinations)
+};
+
+struct LayerScratch {
+  float* partial;
+  float* partial2;
+  float* agg;     // [D][ld4(w)]
+  float* mean;    // moments (float64 [D][in])
+  float* z;       // [S][ld4(out)]
+  float* s_src;
+  float* s_dst;
+};
+
+void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc, float* out,
+               int64_t ldo);
+void launch_resolve(cudaStream_t s, const BindCtx& c, BlockCounters* cnt, int64_t S_max, const int32_t* src_ids,
+                    const float** rowp, float* gscale);
+// CGP: this partition's raw per-destination partial (cgpexec.py:111-164, not normalised)
+void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc,
+                       const float* s_dst, float* lp, int64_t ldp, float* lcnt, int moments_phase,
+                       const double* mean);
+// CGP: merge P raw partials in partition order (cgpexec.py:189-240) and normalise; GAT and
+// transform-first GCN write the layer output, the others the aggregate for cgp_update
+void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const float* lp, int64_t part_stride, int64_t ldp,
+               const float* lcnt, int64_t cnt_stride, const int64_t* D_dev, int64_t D_max, float* agg,
+               float* out, int64_t ldo, int moments_phase, double* mean);
+// CGP: apply_update with explicit destination rows h_v (models.py:214-228)
+void cgp_update(cudaStream_t s, const LayerDev& L, const int64_t* D_dev, int64_t D_max, const float* const* hvp,
+                const float* agg, float* out, int64_t ldo);
+int cgp_partial_width(const LayerDev& L);  // raw partial row width (pw)
+
 // stage entry points ---------------------------------------------------------
 struct Engine;
 
@@ -252,21 +340,81 @@ struct GroupLoad {
   }
 };
 
-void export_bindings(Engine& e, RequestWs& w, int layer, uint8_t* d_kind, int32_t* d_pe_layer);
+void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d_kind, int32_t* d_pe_layer);
+BindCtx bind_ctx(Engine& e, RequestWs& w, int l);
+void stage_qpad(Engine& e, RequestWs& w);
 
 void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, int64_t words, int32_t* out);
 
 void stage_request_prep(Engine& e, RequestWs& w, bool need_scores);
 void stage_select(Engine& e, RequestWs& w);
 void stage_request_csr(Engine& e, RequestWs& w);
+void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound, const int64_t* m_dev, RqCsr& c,
+                  bool counts_ready);
+// where a block's destinations pull their sources from
+struct SpanSrc {
+  const int64_t* offsets;  // CSR over all N destinations (whole graph or a rank's source-split CSR)
+  const int32_t* nbrs;
+  const int32_t* deg;      // CSR row lengths
+  const int64_t* rq_ptr;   // request CSR (whole request or the rank's slice)
+  const int32_t* rq_src;
+};
+void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src);
+void write_mid_dst(Engine& e, RequestWs& w, BlockDev& b);
+void write_query_dst(Engine& e, RequestWs& w, BlockDev& b);
 void stage_build_srpe(Engine& e, RequestWs& w);
 void stage_build_full(Engine& e, RequestWs& w);
 void stage_forward(Engine& e, RequestWs& w, float* d_out);
 void stage_precompute(Engine& e);
 void block_items(Engine& e, BlockDev& b, int64_t chunk);
 
+// ---------------------------------------------------------------------------
+// computation-graph parallelism (CGP): hash partitions and per-partition work
+// ---------------------------------------------------------------------------
+struct PartitionDev {
+  int rank = 0;
+  int64_t* off = nullptr;  // source-split CSR over all N destinations (graphstore.py:233-262)
+  int32_t* src = nullptr;
+  int32_t* deg = nullptr;
+  int64_t E = 0;
+};
+
+struct CgpPartWs {
+  int64_t* ledges = nullptr;  // this partition's request slice [m][2]
+  RqCsr rq;                   // slice bucketed by destination slot (rq.ctr[0] = slice size)
+  BlockDev blocks[2];         // mid (layers 1..k-1), last (layer k); no self rows
+};
+
+struct CgpState {
+  int P = 1;
+  int my_rank = 0;
+  bool nccl = false;
+  void* comm = nullptr;       // ncclComm_t
+  int32_t* owner = nullptr;   // [N]
+  std::vector<PartitionDev> parts;  // emulation: all P; NCCL: this rank's
+  std::vector<CgpPartWs> ws;
+  // per request
+  const float** hvp = nullptr;  // [D_max] destination rows h_v (owned; zero row otherwise)
+  float* zero_row = nullptr;
+  float* lp = nullptr;          // raw partials [nparts][D_max][ldp] (float64 for moments)
+  float* lcnt = nullptr;        // [nparts][D_max]
+  float* sdst = nullptr;        // [D_max]
+  float* lmax = nullptr;        // [D_max] softmax max exchange
+  double* mean = nullptr;       // moments [D_max][in]
+  float* fin = nullptr;         // [B][H] last-layer rows before the reduce to rank 0
+  int64_t D_max = 0, ldp = 0;
+  int64_t collective_bytes = 0;
+};
+
+void cgp_build_partitions(Engine& e);
+void carve_cgp(Engine& e, RequestWs& w, Arena& a);
+void serve_cgp(Engine& e, float* d_out);
+void cgp_destroy(Engine& e);
+void cgp_init_comm(Engine& e);
+
 struct Engine {
   ob_config cfg{};
+  CgpState cgp;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   GraphDev g;

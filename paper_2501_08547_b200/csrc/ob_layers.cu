@@ -41,23 +41,6 @@ __device__ __forceinline__ float softplus_f(float x) {
 // ---------------------------------------------------------------------------
 // binding (resolve_block_inputs)
 // ---------------------------------------------------------------------------
-struct BindCtx {
-  int mode;             // 0 = srpe, 1 = full (computed rows follow the source order)
-  int layer;            // 1-based
-  int64_t N;
-  int64_t F_ld;
-  const float* feats;   // N x F_ld
-  const float* qfeat;   // B x F_ld
-  const float* pe;      // stored layer (layer-1) rows, N x in_ld
-  const float* prev;    // previous layer output, rows x in_ld
-  int64_t in_ld;
-  const int64_t* T_dev; // srpe: computed rows = [targets..., queries...]
-  const uint32_t* cbits;
-  const int64_t* cwpre;
-  const int32_t* tpos;
-  const int32_t* indeg;
-  const int32_t* qdeg;
-};
 
 // returns BIND_* kind and the row pointer (compgraph.py:287-305 binding rule)
 __device__ __forceinline__ int bind_row(const BindCtx& c, int64_t T, int64_t s, int64_t g, const float** row,
@@ -494,29 +477,7 @@ static void gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max, const Block
 // ---------------------------------------------------------------------------
 // one layer over one block (shared by serving and precompute)
 // ---------------------------------------------------------------------------
-struct LayerRun {
-  const BlockCounters* cnt;  // D, E, S, items (device)
-  const int64_t* D_dev;
-  const int64_t* S_dev;
-  int64_t D_max, S_max, items_max;
-  const int64_t* dst_ptr;
-  const int64_t* item_ptr;
-  const int32_t* edge_src;
-  const int32_t* self;       // null = identity
-  RowSrc x;                  // bound inputs
-  const float* gscale;       // gcn
-  const int64_t* group_ptr;  // second-level partial groups (hub destinations)
-};
 
-struct LayerScratch {
-  float* partial;
-  float* partial2;
-  float* agg;     // [D][ld4(w)]
-  float* mean;    // moments (float64 [D][in])
-  float* z;       // [S][ld4(out)]
-  float* s_src;
-  float* s_dst;
-};
 
 static TcGemmArgs gemm_args(const int64_t* M_dev, const TcWeights& w, float* C, int64_t ldc, bool relu) {
   TcGemmArgs g{};
@@ -653,9 +614,326 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
 }
 
 // ---------------------------------------------------------------------------
+// CGP building blocks (cgpexec.py:111-240): raw local partials, partition-
+// ordered merge, update with explicit destination rows
+// ---------------------------------------------------------------------------
+int cgp_partial_width(const LayerDev& L) {
+  const int w = (L.spec.kind == OB_KIND_GAT || L.transform_first) ? L.spec.out_dim : L.spec.in_dim;
+  return L.spec.kind == OB_KIND_GAT ? w + 2 : w;
+}
+
+// merge a destination's items (or hub groups) into one raw partial: sum / max /
+// (max logit, sum exp, sum exp*z); count = local in-edges
+__global__ void __launch_bounds__(256) k_local_raw(FinArgs a, float* lp, int64_t ldp, float* lcnt) {
+  const int64_t D = a.cnt->D;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < D; i += nw) {
+    int64_t i0 = a.item_ptr[i], i1 = a.item_ptr[i + 1];
+    const float* part = a.partial;
+    if (a.group_ptr && a.group_ptr[i + 1] > a.group_ptr[i]) {
+      i0 = a.group_ptr[i];
+      i1 = a.group_ptr[i + 1];
+      part = a.partial2;
+    }
+    float* o = lp + i * ldp;
+    if (lane == 0) lcnt[i] = (float)(a.dst_ptr[i + 1] - a.dst_ptr[i]);
+    if (a.kind == OB_KIND_GAT) {
+      float ms = -INFINITY;
+      for (int64_t it = i0; it < i1; ++it) {
+        const float* pp = part + it * (int64_t)a.pw;
+        if (pp[1] > 0.f) ms = fmaxf(ms, pp[0]);
+      }
+      float den = 0.f;
+      for (int64_t it = i0; it < i1; ++it) {
+        const float* pp = part + it * (int64_t)a.pw;
+        if (pp[1] > 0.f) den += pp[1] * __expf(pp[0] - ms);
+      }
+      if (lane == 0) {
+        o[0] = ms;
+        o[1] = den;
+      }
+      for (int col = lane; col < a.width; col += 32) {
+        float num = 0.f;
+        for (int64_t it = i0; it < i1; ++it) {
+          const float* pp = part + it * (int64_t)a.pw;
+          if (pp[1] > 0.f) num += pp[2 + col] * __expf(pp[0] - ms);
+        }
+        o[2 + col] = num;
+      }
+      continue;
+    }
+    const bool mx = a.kind == OB_KIND_SAGE_MAX;
+    for (int col = lane; col < a.width; col += 32) {
+      float r0 = mx ? -INFINITY : 0.f, r1 = r0;
+      int64_t it = i0;
+      for (; it + 1 < i1; it += 2) {
+        const float v0 = part[it * (int64_t)a.pw + col], v1 = part[(it + 1) * (int64_t)a.pw + col];
+        if (mx) r0 = fmaxf(r0, v0), r1 = fmaxf(r1, v1);
+        else r0 += v0, r1 += v1;
+      }
+      if (it < i1) {
+        const float v = part[it * (int64_t)a.pw + col];
+        r0 = mx ? fmaxf(r0, v) : r0 + v;
+      }
+      o[col] = mx ? fmaxf(r0, r1) : r0 + r1;
+    }
+  }
+}
+
+// float64 raw sums for the moments kind (items carry float64 partials)
+__global__ void __launch_bounds__(256) k_local_raw_f64(const BlockCounters* cnt_, const int64_t* dst_ptr,
+                                                       const int64_t* item_ptr, const double* partial, int width,
+                                                       double* lp, int64_t ldp, float* lcnt) {
+  const int64_t D = cnt_->D;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < D; i += nw) {
+    if (lane == 0) lcnt[i] = (float)(dst_ptr[i + 1] - dst_ptr[i]);
+    for (int col = lane; col < width; col += 32) {
+      double s = 0.0;
+      for (int64_t it = item_ptr[i]; it < item_ptr[i + 1]; ++it) s += partial[it * (int64_t)width + col];
+      lp[i * ldp + col] = s;
+    }
+  }
+}
+
+struct MergeArgs {
+  int P;
+  const float* lp;
+  int64_t part_stride, ldp;
+  const float* lcnt;
+  int64_t cnt_stride;
+  const int64_t* D_dev;
+  int width, kind;
+  float p;
+  int n;
+  bool gcn_norm, relu;
+  float* out;
+  int64_t ldo;
+};
+
+// merge in ascending partition order (cgpexec.py:189-240): sum / mean / max / powmean /
+// softmax rescale, empty destinations aggregate to zero
+__global__ void __launch_bounds__(256) k_merge_parts(MergeArgs m) {
+  const int64_t D = *m.D_dev;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < D; i += nw) {
+    float c = 0.f;
+    for (int p = 0; p < m.P; ++p) c += m.lcnt[p * m.cnt_stride + i];
+    float ms = -INFINITY;
+    if (m.kind == OB_KIND_GAT) {
+      for (int p = 0; p < m.P; ++p) {
+        const float* o = m.lp + p * m.part_stride + i * m.ldp;
+        if (o[1] > 0.f) ms = fmaxf(ms, o[0]);
+      }
+    }
+    for (int col = lane; col < m.width; col += 32) {
+      float r;
+      if (m.kind == OB_KIND_GAT) {
+        float den = 0.f, num = 0.f;
+        for (int p = 0; p < m.P; ++p) {
+          const float* o = m.lp + p * m.part_stride + i * m.ldp;
+          if (o[1] > 0.f) {
+            const float sc = __expf(o[0] - ms);
+            den += o[1] * sc;
+            num += o[2 + col] * sc;
+          }
+        }
+        r = den > 0.f ? num / den : 0.f;
+      } else if (m.kind == OB_KIND_SAGE_MAX) {
+        float mx = -INFINITY;
+        for (int p = 0; p < m.P; ++p)
+          if (m.lcnt[p * m.cnt_stride + i] > 0.f) mx = fmaxf(mx, m.lp[p * m.part_stride + i * m.ldp + col]);
+        r = c > 0.f ? mx : 0.f;
+      } else {
+        float s = 0.f;
+        for (int p = 0; p < m.P; ++p) s += m.lp[p * m.part_stride + i * m.ldp + col];
+        if (m.gcn_norm) r = s / sqrtf(c + 1.f);
+        else if (m.kind == OB_KIND_POWER_MEAN) r = c > 0.f ? powf(s / c, 1.f / m.p) : 0.f;
+        else r = c > 0.f ? s / c : 0.f;
+      }
+      if (m.relu) r = fmaxf(r, 0.f);
+      m.out[i * m.ldo + col] = r;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_merge_moments(int P, const double* lp, int64_t part_stride, int64_t ldp,
+                                                       const float* lcnt, int64_t cnt_stride, const int64_t* D_dev,
+                                                       int width, int phase, int n, double* mean, float* agg,
+                                                       int64_t ldo) {
+  const int64_t D = *D_dev;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < D; i += nw) {
+    float c = 0.f;
+    for (int p = 0; p < P; ++p) c += lcnt[p * cnt_stride + i];
+    for (int col = lane; col < width; col += 32) {
+      double s = 0.0;
+      for (int p = 0; p < P; ++p) s += lp[p * part_stride + i * ldp + col];
+      const double v = c > 0.f ? s / (double)c : 0.0;
+      if (phase == 1) {
+        mean[i * width + col] = v;
+      } else {
+        const double r = (n & 1) ? copysign(pow(fabs(v), 1.0 / n), v) : pow(fmax(v, 0.0), 1.0 / n);
+        agg[i * ldo + col] = (float)r;
+      }
+    }
+  }
+}
+
+void launch_resolve(cudaStream_t s, const BindCtx& c, BlockCounters* cnt, int64_t S_max, const int32_t* src_ids,
+                    const float** rowp, float* gscale) {
+  k_resolve<<<grid_for(S_max, 256), 256, 0, s>>>(c, cnt, src_ids, rowp, gscale, nullptr, nullptr);
+  OB_LAUNCHED();
+}
+
+void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc,
+                       const float* s_dst, float* lp, int64_t ldp, float* lcnt, int moments_phase,
+                       const double* mean) {
+  const ob_layer& sp = L.spec;
+  const int in = sp.in_dim, outd = sp.out_dim;
+  const int64_t ld_out = ld4(outd);
+  AggArgs a{};
+  a.cnt = r.cnt;
+  a.dst_ptr = r.dst_ptr;
+  a.item_ptr = r.item_ptr;
+  a.edge_src = r.edge_src;
+  a.x = r.x;
+  a.width = in;
+  a.pw = in;
+  a.partial = sc.partial;
+  a.p = sp.p;
+  a.n = sp.n;
+  if (sp.kind == OB_KIND_GAT || L.transform_first) {
+    TcGemmArgs g = gemm_args(r.S_dev, L.tw_main, sc.z, ld_out, false);
+    g.a1 = r.x;
+    g.K1 = in;
+    gemm(s, g, r.S_max, r.cnt);
+    a.x = RowSrc{nullptr, sc.z, ld_out};
+    a.width = outd;
+    a.pw = outd;
+  }
+  if (sp.kind == OB_KIND_MOMENTS) {
+    a.mean = mean;
+    if (moments_phase == 1) launch_agg<kOpDSum>(s, a, r.items_max);
+    else launch_agg<kOpMom2>(s, a, r.items_max);
+    k_local_raw_f64<<<grid_for(r.D_max, 8, kNumSMs * 16), 256, 0, s>>>(r.cnt, r.dst_ptr, r.item_ptr,
+                                                                        (const double*)sc.partial, in, (double*)lp,
+                                                                        ldp, lcnt);
+    OB_LAUNCHED();
+    return;
+  }
+  if (sp.kind == OB_KIND_GAT) {
+    k_rowdot<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, sc.z, ld_out, nullptr, outd, L.a_src, sc.s_src);
+    OB_LAUNCHED();
+    a.pw = outd + 2;
+    a.s_src = sc.s_src;
+    a.s_dst = s_dst;
+    launch_agg<kOpSoftmax>(s, a, r.items_max);
+  } else if (sp.kind == OB_KIND_GCN) {
+    a.gscale = r.gscale;
+    launch_agg<kOpSum>(s, a, r.items_max);
+  } else if (sp.kind == OB_KIND_SAGE_MAX) {
+    launch_agg<kOpMax>(s, a, r.items_max);
+  } else if (sp.kind == OB_KIND_POWER_MEAN) {
+    launch_agg<kOpPow>(s, a, r.items_max);
+  } else {
+    launch_agg<kOpSum>(s, a, r.items_max);
+  }
+  FinArgs f{};
+  f.cnt = r.cnt;
+  f.dst_ptr = r.dst_ptr;
+  f.item_ptr = r.item_ptr;
+  f.partial = sc.partial;
+  f.partial2 = sc.partial2;
+  f.group_ptr = r.group_ptr;
+  f.pw = a.pw;
+  f.width = a.width;
+  f.kind = sp.kind;
+  k_reduce_groups<<<grid_for(r.items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f, sc.partial2);
+  k_local_raw<<<grid_for(r.D_max, 8, kNumSMs * 16), 256, 0, s>>>(f, lp, ldp, lcnt);
+  g_launches += 2;
+}
+
+void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const float* lp, int64_t part_stride, int64_t ldp,
+               const float* lcnt, int64_t cnt_stride, const int64_t* D_dev, int64_t D_max, float* agg, float* out,
+               int64_t ldo, int moments_phase, double* mean) {
+  const ob_layer& sp = L.spec;
+  if (sp.kind == OB_KIND_MOMENTS) {
+    k_merge_moments<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(P, (const double*)lp, part_stride, ldp, lcnt,
+                                                                      cnt_stride, D_dev, sp.in_dim, moments_phase,
+                                                                      sp.n, mean, agg, ld4(sp.in_dim));
+    OB_LAUNCHED();
+    return;
+  }
+  MergeArgs m{};
+  m.P = P;
+  m.lp = lp;
+  m.part_stride = part_stride;
+  m.ldp = ldp;
+  m.lcnt = lcnt;
+  m.cnt_stride = cnt_stride;
+  m.D_dev = D_dev;
+  m.kind = sp.kind;
+  m.p = sp.p;
+  m.n = sp.n;
+  const bool narrow = sp.kind == OB_KIND_GAT || L.transform_first;
+  m.width = narrow ? sp.out_dim : sp.in_dim;
+  m.gcn_norm = sp.kind == OB_KIND_GCN;
+  if (sp.kind == OB_KIND_GAT || (sp.kind == OB_KIND_GCN && L.transform_first)) {
+    m.relu = true;  // relu(agg) is the layer output
+    m.out = out;
+    m.ldo = ldo;
+  } else {
+    m.out = agg;
+    m.ldo = ld4(m.width);
+  }
+  k_merge_parts<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(m);
+  OB_LAUNCHED();
+}
+
+void cgp_update(cudaStream_t s, const LayerDev& L, const int64_t* D_dev, int64_t D_max, const float* const* hvp,
+                const float* agg, float* out, int64_t ldo) {
+  const ob_layer& sp = L.spec;
+  const int in = sp.in_dim;
+  if (sp.kind == OB_KIND_GAT || (sp.kind == OB_KIND_GCN && L.transform_first)) return;  // merged directly
+  if (sp.kind == OB_KIND_GCN) {
+    TcGemmArgs g = gemm_args(D_dev, L.tw_main, out, ldo, true);
+    g.a2 = agg;
+    g.lda2 = ld4(in);
+    g.K2 = in;
+    gemm(s, g, D_max, nullptr);
+    return;
+  }
+  if (sp.kind == OB_KIND_SAGE_MEAN && L.transform_first) {
+    TcGemmArgs g = gemm_args(D_dev, L.tw_self, out, ldo, true);
+    g.a1 = RowSrc{hvp, nullptr, 0};
+    g.K1 = in;
+    g.E = agg;
+    g.lde = ld4(sp.out_dim);
+    gemm(s, g, D_max, nullptr);
+    return;
+  }
+  TcGemmArgs g = gemm_args(D_dev, L.tw_main, out, ldo, true);
+  g.a1 = RowSrc{hvp, nullptr, 0};
+  g.K1 = in;
+  g.a2 = agg;
+  g.lda2 = ld4(in);
+  g.K2 = in;
+  gemm(s, g, D_max, nullptr);
+}
+
+// ---------------------------------------------------------------------------
 // serving forward over the request's blocks
 // ---------------------------------------------------------------------------
-static BindCtx bind_ctx(Engine& e, RequestWs& w, int l) {
+BindCtx bind_ctx(Engine& e, RequestWs& w, int l) {
   const bool full = e.cfg.strategy == OB_STRATEGY_FULL;
   const LayerDev& L = e.layers[l - 1];
   BindCtx c{};
@@ -719,9 +997,13 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
   }
 }
 
+void stage_qpad(Engine& e, RequestWs& w) {
+  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, e.stream>>>(w.qfeat, w.B, e.g.F, w.qpad, e.g.F_ld);
+  OB_LAUNCHED();
+}
+
 // parity export of bind_kind / bind_pe_layer with the same binding rule
-void export_bindings(Engine& e, RequestWs& w, int layer, uint8_t* d_kind, int32_t* d_pe_layer) {
-  BlockDev& b = w.blocks[w.block_of_layer[layer - 1]];
+void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d_kind, int32_t* d_pe_layer) {
   BindCtx c = bind_ctx(e, w, layer);
   k_resolve<<<grid_for(b.S_max, 256), 256, 0, e.stream>>>(c, b.cnt, b.src_ids, w.rowp, nullptr, d_kind, d_pe_layer);
   OB_LAUNCHED();

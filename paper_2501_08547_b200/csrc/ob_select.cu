@@ -156,6 +156,25 @@ __global__ void k_rq_count(const int64_t* __restrict__ edges, int64_t m, int64_t
   }
 }
 
+// request-CSR slot of a destination: candidate rank for training ids, R + q for queries
+__device__ __forceinline__ int64_t rq_slot(int64_t d, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
+                                           int64_t R) {
+  return d < N ? bm_rank(cbits, cwpre, d) : R + (d - N);
+}
+
+// every slot (candidate and query) of an edge subset -- a CGP rank's slice
+__global__ void k_rq_count_all(const int64_t* __restrict__ edges, int64_t m_host, const int64_t* m_dev, int64_t N,
+                               const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt) {
+  if (rc->err & (kErrRange | kErrNoQuery)) return;
+  const int64_t R = rc->R, m = dev_count(m_dev, m_host);
+  OB_GRID_STRIDE(e, m) warp_agg_inc(rq_cnt, rq_slot(edges[2 * e + 1], N, cbits, cwpre, R));
+}
+
+__global__ void k_zero_slots(const ReqCounters* rc, int B, int32_t* a, int32_t* b) {
+  const int64_t RB = rc->R + B;
+  OB_GRID_STRIDE(i, RB) a[i] = b[i] = 0;
+}
+
 // ---------------------------------------------------------------------------
 // 2. ratio scores (policy.py:77-81) and budget
 // ---------------------------------------------------------------------------
@@ -273,13 +292,15 @@ struct SelStore {
 // 3. request CSR fill: per-CTA reservation for query slots, warp-aggregated
 //    atomics for candidate slots
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_rq_fill(const int64_t* __restrict__ edges, int64_t m, int64_t N, int B,
-                                                 const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc,
-                                                 const int64_t* rq_ptr, int32_t* rq_fill, int32_t* rq_src) {
+__global__ void __launch_bounds__(256) k_rq_fill(const int64_t* __restrict__ edges, int64_t m_host,
+                                                 const int64_t* m_dev, int64_t N, int B, const uint32_t* cbits,
+                                                 const int64_t* cwpre, const ReqCounters* rc, const int64_t* rq_ptr,
+                                                 int32_t* rq_fill, int32_t* rq_src) {
   extern __shared__ int32_t sm[];  // [B] counts, then [B] base offsets
   const bool smem = B <= kMaxSmemQueries / 2;
   if (rc->err & (kErrRange | kErrNoQuery)) return;
   const int64_t R = rc->R;
+  const int64_t m = dev_count(m_dev, m_host);
   int32_t* cnt = sm;
   int32_t* base = sm + B;
   for (int64_t t0 = (int64_t)blockIdx.x * kEdgeTile; t0 < m; t0 += (int64_t)gridDim.x * kEdgeTile) {
@@ -340,8 +361,8 @@ struct LessI32 {
   __device__ bool operator()(const int32_t& a, const int32_t& b) const { return a < b; }
 };
 
-__global__ void __launch_bounds__(256) k_segsort_warp(const int64_t* __restrict__ ptr, ReqCounters* rc, int32_t* vals,
-                                                      int32_t* big_list) {
+__global__ void __launch_bounds__(256) k_segsort_warp(const int64_t* __restrict__ ptr, const ReqCounters* rc,
+                                                      int64_t* ctr, int32_t* vals, int32_t* big_list) {
   using WS = cub::WarpMergeSort<int32_t, kWarpSortItems, 32>;
   __shared__ typename WS::TempStorage tmp[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -367,7 +388,7 @@ __global__ void __launch_bounds__(256) k_segsort_warp(const int64_t* __restrict_
         if (idx < len) vals[b + idx] = k[i];
       }
     } else if (lane == 0) {
-      int64_t at = atomicAdd((unsigned long long*)&rc->n_big, 1ull);
+      int64_t at = atomicAdd((unsigned long long*)&ctr[1], 1ull);
       big_list[at] = (int32_t)s;
     }
   }
@@ -395,12 +416,12 @@ __device__ __forceinline__ void chunk_of(const int64_t* cptr, int64_t nbig, int6
 }
 
 // sort every 4096-element chunk of every long segment in shared memory
-__global__ void __launch_bounds__(kChunkThreads) k_chunk_sort(const int64_t* __restrict__ ptr, const ReqCounters* rc,
+__global__ void __launch_bounds__(kChunkThreads) k_chunk_sort(const int64_t* __restrict__ ptr, const int64_t* ctr,
                                                               const int32_t* big_list, const int64_t* cptr,
                                                               int32_t* vals) {
   using BRS = cub::BlockRadixSort<int32_t, kChunkThreads, kChunkItems>;
   __shared__ typename BRS::TempStorage tmp;
-  const int64_t nbig = rc->n_big, nch = rc->n_chunks;
+  const int64_t nbig = ctr[1], nch = ctr[2];
   for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
     int64_t bi, j;
     chunk_of(cptr, nbig, ci, &bi, &j);
@@ -445,13 +466,13 @@ __device__ __forceinline__ int levels_for(int64_t len) {
 // buffer the segment's data currently sits in (parity of the level) into the
 // other; segments that need fewer levels are skipped.  Each CTA produces one
 // 4096-element output tile (merge-path split, then rank-merge in shared memory).
-__global__ void __launch_bounds__(kChunkThreads) k_merge_level(const int64_t* __restrict__ ptr, const ReqCounters* rc,
+__global__ void __launch_bounds__(kChunkThreads) k_merge_level(const int64_t* __restrict__ ptr, const int64_t* ctr,
                                                                const int32_t* big_list, const int64_t* cptr,
                                                                int32_t* vals, int32_t* tmp, int level) {
   __shared__ int32_t sa[kChunk];
   __shared__ int32_t sb[kChunk];
   __shared__ int64_t split[2];
-  const int64_t nbig = rc->n_big, nch = rc->n_chunks;
+  const int64_t nbig = ctr[1], nch = ctr[2];
   const int64_t w = (int64_t)kChunk << level;
   for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
     int64_t bi, j;
@@ -497,10 +518,10 @@ __global__ void __launch_bounds__(kChunkThreads) k_merge_level(const int64_t* __
 
 // segments whose level count is odd finished in tmp: copy their tiles back
 __global__ void __launch_bounds__(kChunkThreads) k_merge_copyback(const int64_t* __restrict__ ptr,
-                                                                  const ReqCounters* rc, const int32_t* big_list,
+                                                                  const int64_t* ctr, const int32_t* big_list,
                                                                   const int64_t* cptr, int32_t* vals,
                                                                   const int32_t* tmp) {
-  const int64_t nbig = rc->n_big, nch = rc->n_chunks;
+  const int64_t nbig = ctr[1], nch = ctr[2];
   for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
     int64_t bi, j;
     chunk_of(cptr, nbig, ci, &bi, &j);
@@ -566,35 +587,52 @@ void stage_select(Engine& e, RequestWs& w) {
               r_max, &w.rc->T);
 }
 
-void stage_request_csr(Engine& e, RequestWs& w) {
+// Request CSR over an edge set (the whole request, or one CGP rank's slice):
+// bucket by destination slot, then sort each slot's sources ascending.
+void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound, const int64_t* m_dev, RqCsr& c,
+                  bool counts_ready) {
   cudaStream_t s = e.stream;
-  const int64_t m = w.m;
-  const int64_t rb_max = std::min<int64_t>(e.g.N, 2 * m) + w.B;
-  device_scan(s, e.scan, LoadI32{w.rq_cnt}, StoreI64{w.rq_ptr}, &w.rc->RB, 0, rb_max, nullptr, w.rq_ptr);
-  if (m <= 0) return;
+  const int64_t rb_max = std::min<int64_t>(e.g.N, 2 * w.m) + w.B;
+  OB_CUDA(cudaMemsetAsync(c.ctr + 1, 0, 2 * sizeof(int64_t), s));
+  if (!counts_ready) {
+    k_zero_slots<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rc, w.B, c.cnt, c.fill);
+    OB_LAUNCHED();
+    if (m_bound > 0) {
+      k_rq_count_all<<<grid_for(m_bound, 256), 256, 0, s>>>(edges, m_bound, m_dev, e.g.N, w.cbits, w.cwpre, w.rc,
+                                                              c.cnt);
+      OB_LAUNCHED();
+    }
+  }
+  device_scan(s, e.scan, LoadI32{c.cnt}, StoreI64{c.ptr}, &w.rc->RB, 0, rb_max, nullptr, c.ptr);
+  if (m_bound <= 0) return;
   const size_t sm = w.B <= kMaxSmemQueries / 2 ? 2 * sizeof(int32_t) * w.B : 0;
-  k_rq_fill<<<grid_for(m, kEdgeTile, kNumSMs * 4), 256, sm, s>>>(w.edges, m, e.g.N, w.B, w.cbits, w.cwpre, w.rc,
-                                                                   w.rq_ptr, w.rq_fill, w.rq_src);
-  k_segsort_warp<<<grid_for(rb_max, 8), 256, 0, s>>>(w.rq_ptr, w.rc, w.rq_src, w.big_list);
+  k_rq_fill<<<grid_for(m_bound, kEdgeTile, kNumSMs * 4), 256, sm, s>>>(edges, m_bound, m_dev, e.g.N, w.B, w.cbits,
+                                                                         w.cwpre, w.rc, c.ptr, c.fill, c.src);
+  k_segsort_warp<<<grid_for(rb_max, 8), 256, 0, s>>>(c.ptr, w.rc, c.ctr, c.src, c.big_list);
   g_launches += 2;
-  // long segments: chunk sort + merge levels (ping-pong rq_src <-> sort_tmp)
-  device_scan(s, e.scan, ChunkLoad{w.big_list, w.rq_ptr}, StoreI64{w.big_cptr}, &w.rc->n_big, 0, rb_max,
-              &w.rc->n_chunks, w.big_cptr);
-  const int64_t ch_max = m / kChunk + rb_max / 256 + 2;
+  // long segments: chunk sort + merge levels (ping-pong src <-> sort_tmp)
+  device_scan(s, e.scan, ChunkLoad{c.big_list, c.ptr}, StoreI64{c.big_cptr}, c.ctr + 1, 0, rb_max, c.ctr + 2,
+              c.big_cptr);
+  const int64_t ch_max = m_bound / kChunk + rb_max / 256 + 2;
   const int g = grid_for(ch_max, 1, kNumSMs * 4);
-  k_chunk_sort<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, w.rq_src);
+  k_chunk_sort<<<g, kChunkThreads, 0, s>>>(c.ptr, c.ctr, c.big_list, c.big_cptr, c.src);
   OB_LAUNCHED();
-  // the longest possible segment is the whole request; levels past a segment's
+  // the longest possible segment is the whole edge set; levels past a segment's
   // own count exit immediately
   int level = 0;
-  for (int64_t wd = kChunk; wd < m; wd *= 2, ++level) {
-    k_merge_level<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, w.rq_src, w.sort_tmp, level);
+  for (int64_t wd = kChunk; wd < m_bound; wd *= 2, ++level) {
+    k_merge_level<<<g, kChunkThreads, 0, s>>>(c.ptr, c.ctr, c.big_list, c.big_cptr, c.src, c.sort_tmp, level);
     OB_LAUNCHED();
   }
   if (level > 0) {
-    k_merge_copyback<<<g, kChunkThreads, 0, s>>>(w.rq_ptr, w.rc, w.big_list, w.big_cptr, w.rq_src, w.sort_tmp);
+    k_merge_copyback<<<g, kChunkThreads, 0, s>>>(c.ptr, c.ctr, c.big_list, c.big_cptr, c.src, c.sort_tmp);
     OB_LAUNCHED();
   }
+}
+
+void stage_request_csr(Engine& e, RequestWs& w) {
+  RqCsr c = w.rq_view();
+  build_rq_csr(e, w, w.edges, w.m, nullptr, c, /*counts_ready=*/true);
 }
 
 }  // namespace ob

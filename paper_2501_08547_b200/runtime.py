@@ -80,6 +80,13 @@ def _f32(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float32)
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for a one-process-per-GPU CGP group (call on rank 0, broadcast)."""
+    buf = C.create_string_buffer(128)
+    nat.check(nat.lib.ob_nccl_unique_id(buf))
+    return buf.raw
+
+
 class ServingEngine:
     """Loaded dataset, stored embeddings and weights, resident on one B200."""
 
@@ -163,9 +170,10 @@ class ServingEngine:
         nat.check(self._lib.ob_serve(self._h, B, nat.ptr(q), int(e.shape[0]), nat.ptr(e), nat.ptr(out),
                                      C.byref(bd)))
         self.last_breakdown = bd
+        parts = self.config.num_partitions if self.config.strategy == "srpe-cgp" else 1
         lb = LatencyBreakdown(
             fetch_ms=bd.fetch_ms,
-            transfer_ms=bd.fetch_bytes / self.config.bandwidth_bytes_per_s * 1e3,
+            transfer_ms=bd.fetch_bytes / parts / self.config.bandwidth_bytes_per_s * 1e3,
             compute_ms=bd.compute_ms,
             collective_bytes=int(bd.collective_bytes),
             fetch_bytes=int(bd.fetch_bytes),
@@ -217,6 +225,12 @@ class ServingEngine:
         tg = self.last_plan()["targets"] if self.config.strategy != "full" else np.empty(0, np.int64)
         B = int(np.sum(blocks[-1].dst_ids >= n))
         return ComputationGraph(blocks, np.arange(n, n + B, dtype=np.int64), self.config.strategy, n, tg)
+
+    def partition_owner(self) -> np.ndarray:
+        """PartitionMap.owner of a CGP engine (graphstore.py:177-181)."""
+        out = np.empty(self.dataset.num_nodes, np.int64)
+        nat.check(self._lib.ob_partition_owner(self._h, nat.ptr(out)))
+        return out
 
     def launch_count(self) -> int:
         return int(self._lib.ob_launch_count(self._h))

@@ -1,0 +1,101 @@
+"""CGP on the device vs the reference's partitioned execution -- needs a B200.
+
+Single-process emulation (num_partitions = P, no NCCL id): all P partitions run
+on one GPU and partials merge in ascending rank order, which is exactly the
+reference's sim-transport semantics (runtime.py:337-358, cgpexec.py:373-439).
+Bars: partition owners and every per-rank shard array bit-exact against the
+reference (golden), targets identical to the centralized plan, embeddings
+within 1e-4 of the reference's CGP output.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import KINDS, SMALL_CASES, assert_block_equal, golden_weights
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+SHARD_FIELDS = ("src_ids", "dst_ids", "edge_src", "edge_dst", "bind_kind", "bind_pe_layer", "src_degree")
+
+
+def rel(a, r):
+    from oracle.layers import max_rel_err
+
+    return max_rel_err(a, r)
+
+
+def _engine(g, kind, kw, k, P, gamma=0.5, seed=11):
+    from paper_2501_08547_b200 import graphstore, models, runtime
+
+    N = int(g["N"])
+    F = g["feats"].shape[1]
+    ds = graphstore.GraphDataset(N, g["offsets"], g["nbrs"], g["feats"], np.ones(N, bool), np.zeros(N, bool))
+    model = models.make_model(kind, k, F, 6, **kw)
+    w = models.Weights(golden_weights(g, f"w.{kind}.k{k}", kind, k))
+    pe = graphstore.PeStore([g[f"pe.{kind}.k{k}.l{l}"] for l in range(1, k)])
+    cfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=gamma, num_partitions=P, seed=seed)
+    return runtime.ServingEngine(ds, pe, model, w, cfg)
+
+
+def _request(g):
+    from paper_2501_08547_b200.compgraph import ServingRequest
+
+    return ServingRequest(int(g["N"]), int(g["B"]), g["qfeat"], g["edges"])
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+@pytest.mark.parametrize("kind,kw", KINDS)
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("P", [2, 3])
+def test_cgp_embeddings(goldens, name, kind, kw, k, P):
+    g = goldens[name]
+    if not bool(g["cand.scorable"]):
+        pytest.skip("request has an unscorable candidate")
+    eng = _engine(g, kind, kw, k, P)
+    emb, bd = eng.serve(_request(g))
+    assert rel(emb, g[f"cgp.{kind}.k{k}.P{P}.emb"]) <= TOL
+    assert np.array_equal(eng.last_plan()["targets"], g["targets.g0.5"])
+    if kind == "sage_mean":
+        assert np.array_equal(eng.partition_owner(), g[f"cgp.P{P}.owner"])
+        for r in range(P):
+            for l in range(1, k + 1):
+                assert_block_equal(eng.last_block(l, partition=r), g, f"cgp.{kind}.k{k}.P{P}.r{r}.b{l}",
+                                   fields=SHARD_FIELDS)
+    eng.close()
+
+
+def test_cgp_single_partition_equals_centralized(goldens):
+    """P = 1 shards equal the centralized srpe blocks (pkg/tests/test_compgraph.py:275-292)."""
+    from paper_2501_08547_b200 import runtime
+
+    g = goldens["small_s60"]
+    eng = _engine(g, "sage_mean", {}, 3, 1)
+    emb, _ = eng.serve(_request(g))
+    assert rel(emb, g["srpe.sage_mean.k3.g0.5.emb"]) <= TOL
+    for l in (1, 2, 3):
+        assert_block_equal(eng.last_block(l), g, f"srpe.sage_mean.k3.g0.5.b{l}", fields=SHARD_FIELDS)
+    eng.close()
+    _ = runtime
+
+
+def test_cgp_union_of_shards_is_the_centralized_graph(goldens):
+    """Union over ranks of the shard edge multisets == centralized block (test_compgraph.py:335-352)."""
+    from collections import Counter
+
+    g = goldens["small_s3"]
+    P, k = 3, 2
+    eng = _engine(g, "sage_mean", {}, k, P)
+    eng.serve(_request(g))
+    for l in range(1, k + 1):
+        union = Counter()
+        for r in range(P):
+            b = eng.last_block(l, partition=r)
+            union += Counter((int(b.src_ids[s]), int(b.dst_ids[d])) for s, d in zip(b.edge_src, b.edge_dst))
+        src = g[f"srpe.sage_mean.k{k}.g0.5.b{l}.src_ids"]
+        dst = g[f"srpe.sage_mean.k{k}.g0.5.b{l}.dst_ids"]
+        es = g[f"srpe.sage_mean.k{k}.g0.5.b{l}.edge_src"]
+        ed = g[f"srpe.sage_mean.k{k}.g0.5.b{l}.edge_dst"]
+        assert union == Counter((int(src[s]), int(dst[d])) for s, d in zip(es, ed))
+    eng.close()
