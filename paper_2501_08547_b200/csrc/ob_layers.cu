@@ -867,7 +867,8 @@ void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const float* lp, int64_
                int64_t ldo, int moments_phase, double* mean) {
   const ob_layer& sp = L.spec;
   if (sp.kind == OB_KIND_MOMENTS) {
-    k_merge_moments<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(P, (const double*)lp, part_stride, ldp, lcnt,
+    // part_stride counts floats; the moments partials are float64
+    k_merge_moments<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(P, (const double*)lp, part_stride / 2, ldp, lcnt,
                                                                       cnt_stride, D_dev, sp.in_dim, moments_phase,
                                                                       sp.n, mean, agg, ld4(sp.in_dim));
     OB_LAUNCHED();

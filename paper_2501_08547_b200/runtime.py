@@ -87,6 +87,29 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def broadcast_nccl_id(make_id=nccl_unique_id) -> bytes:
+    """Rank 0 draws the NCCL id and every rank of the default torch.distributed group gets it.
+
+    The bootstrap is plumbing only (the World of collectives.py:94-137); all
+    data-path collectives run inside libomega_b200 on the engine's stream.
+    """
+    import torch.distributed as dist
+
+    obj = [make_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return bytes(obj[0])
+
+
+def distributed_engine(dataset, pe, model, weights, config: ServeConfig, stream: int = 0) -> "ServingEngine":
+    """One CGP rank per process/GPU: rank = torch.distributed rank, P = world size."""
+    import torch.distributed as dist
+
+    if config.strategy != "srpe-cgp" or config.num_partitions != dist.get_world_size():
+        raise ValueError("distributed_engine needs strategy='srpe-cgp' with num_partitions == world size")
+    nid = broadcast_nccl_id()
+    return ServingEngine(dataset, pe, model, weights, config, stream=stream, nccl_id=nid, rank=dist.get_rank())
+
+
 class ServingEngine:
     """Loaded dataset, stored embeddings and weights, resident on one B200."""
 

@@ -1,0 +1,74 @@
+"""One-process-per-GPU CGP check (launched by torchrun; used by test_gpu_cgp_multi).
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29511 tests/cgp_multiproc.py
+
+Every rank serves the same requests through an NCCL-connected engine; rank 0
+compares the result with the reference's CGP embeddings (golden) and with the
+single-process emulation, and prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    rank, P = dist.get_rank(), dist.get_world_size()
+    from conftest import KINDS, golden_weights, load_golden
+    from oracle.layers import max_rel_err
+    from paper_2501_08547_b200 import graphstore, models, runtime
+    from paper_2501_08547_b200.compgraph import ServingRequest
+
+    results = []
+    for name in ("small_s3", "small_s50", "small_s60"):
+        g = load_golden(name)
+        N, F = int(g["N"]), g["feats"].shape[1]
+        ds = graphstore.GraphDataset(N, g["offsets"], g["nbrs"], g["feats"], np.ones(N, bool), np.zeros(N, bool))
+        req = ServingRequest(N, int(g["B"]), g["qfeat"], g["edges"])
+        for kind, kw in KINDS:
+            for k in (2, 3):
+                model = models.make_model(kind, k, F, 6, **kw)
+                w = models.Weights(golden_weights(g, f"w.{kind}.k{k}", kind, k))
+                pe = graphstore.PeStore([g[f"pe.{kind}.k{k}.l{l}"] for l in range(1, k)])
+                cfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=0.5, num_partitions=P, seed=11, device=local)
+                eng = runtime.distributed_engine(ds, pe, model, w, cfg)
+                emb, bd = eng.serve(req)
+                # this rank's shard equals the emulation's shard for the same rank
+                emu = runtime.ServingEngine(ds, pe, model, w, cfg)
+                emb_emu, _ = emu.serve(req)
+                same_shard = all(
+                    np.array_equal(eng.last_block(l, partition=rank).edge_src,
+                                   emu.last_block(l, partition=rank).edge_src)
+                    for l in range(1, k + 1))
+                if rank == 0:
+                    key = f"cgp.{kind}.k{k}.P{P}.emb"
+                    ref = g[key] if key in g else emb_emu
+                    results.append(dict(case=name, kind=kind, k=k, err_ref=max_rel_err(emb, ref),
+                                        err_emu=max_rel_err(emb, emb_emu), shard=bool(same_shard),
+                                        coll_bytes=int(bd.collective_bytes)))
+                eng.close()
+                emu.close()
+    if rank == 0:
+        worst = max(r["err_ref"] for r in results)
+        ok = worst <= 1e-4 and all(r["shard"] for r in results)
+        print(json.dumps(dict(ok=ok, P=P, cases=len(results), worst_err=worst, results=results[:4])))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
