@@ -108,3 +108,24 @@ def test_cgp_union_of_shards_is_the_centralized_graph(goldens):
         ed = g[f"srpe.sage_mean.k{k}.g0.5.b{l}.edge_dst"]
         assert union == Counter((int(src[s]), int(dst[d])) for s, d in zip(es, ed))
     eng.close()
+
+
+def test_cgp_multi_process_nccl():
+    """One process per GPU over NCCL (needs >= 2 GPUs): tests/cgp_multiproc.py under torchrun."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+           "--master-port", "29517", os.path.join(root, "tests", "cgp_multiproc.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
+    res = json.loads(line)
+    assert res["ok"], res
