@@ -53,7 +53,7 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def make_inputs(cfg, rank, world, n_req, seed_base=3):
+def make_inputs(cfg, rank, world, n_req, seed_base=3, same_requests=False):
     """Reference-generator graph + requests; rank 0 builds, others map the same files."""
     from paper_2501_08547_b200 import workload
     from paper_2501_08547_b200.graphstore import GraphDataset
@@ -80,7 +80,8 @@ def make_inputs(cfg, rank, world, n_req, seed_base=3):
             removed[z["ids"]] = True
             pool = workload.HoldoutPool(z["ids"], removed, serving.features[z["ids"]], z["inc"])
     log(f"[bench] rank {rank}: graph ready in {time.time() - t0:.1f}s (E={serving.num_edges})")
-    reqs = [workload.make_request(pool, serving, B, seed=seed_base + 1000 * rank + i) for i in range(n_req)]
+    rs = 0 if same_requests else rank  # CGP: every rank serves the same request stream
+    reqs = [workload.make_request(pool, serving, B, seed=seed_base + 1000 * rs + i) for i in range(n_req)]
     return serving, pool, reqs
 
 
@@ -227,6 +228,8 @@ def main():
     ap.add_argument("--ref-batch", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--parallel", default=None, choices=["cgp", "replicas"],
+                    help="N > 1: computation-graph parallelism (default) or independent replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -248,14 +251,19 @@ def main():
     if args.gamma is not None:
         gamma = args.gamma
     nreq = args.warmup + args.steps
-    serving, pool, reqs = make_inputs(cfg, rank, world, nreq)
+    mode = args.parallel or ("cgp" if world > 1 else "single")
+    cgp = mode == "cgp" and world > 1
+    serving, pool, reqs = make_inputs(cfg, rank, world, nreq, same_requests=cgp)
     model = models.make_model(kind, k, F, H)
     w = models.init_weights(model, 2)
     stream = torch.cuda.Stream(device=local)
     t0 = time.time()
-    eng = runtime.ServingEngine(serving, None, model, w,
-                                runtime.ServeConfig(strategy="srpe", gamma=gamma, device=local),
-                                stream=stream.cuda_stream)
+    if cgp:
+        scfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=gamma, num_partitions=world, seed=0, device=local)
+        eng = runtime.distributed_engine(serving, None, model, w, scfg, stream=stream.cuda_stream)
+    else:
+        scfg = runtime.ServeConfig(strategy="srpe", gamma=gamma, device=local)
+        eng = runtime.ServingEngine(serving, None, model, w, scfg, stream=stream.cuda_stream)
     eng.precompute_pe()
     log(f"[bench] rank {rank}: engine loaded + GPU PE precompute in {time.time() - t0:.1f}s")
     lib = eng._lib
@@ -311,7 +319,8 @@ def main():
         t = torch.tensor([total_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = world * B * args.steps / (total_ms / 1e3)
+    served = B if cgp else world * B  # CGP: all ranks serve the same batch together
+    value = served * args.steps / (total_ms / 1e3)
 
     # end to end through the public host-pointer API (pinned buffers, H2D + D2H inside the region)
     e2e = None
@@ -343,7 +352,7 @@ def main():
             t = torch.tensor([et], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             et = float(t.item())
-        e2e = {"value": round(world * B * args.steps / (et / 1e3), 3), "unit": "queries/s",
+        e2e = {"value": round(served * args.steps / (et / 1e3), 3), "unit": "queries/s",
                "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
                "p50_ms": float(np.percentile(e2e_ms, 50)), "p99_ms": float(np.percentile(e2e_ms, 99))}
 
@@ -366,9 +375,12 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
         "p50_ms": round(float(np.percentile(lat, 50)), 4), "p99_ms": round(float(np.percentile(lat, 99)), 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": desc, "batch": B, "policy": "ratio", "gamma": gamma, "strategy": "srpe",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single",
+        "higher_is_better": True, "scaling": "strong" if cgp else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": desc, "batch": B, "policy": "ratio", "gamma": gamma,
+                   "strategy": "srpe-cgp" if cgp else "srpe",
+                   "parallelism": (f"cgp x{world} (NCCL over NVLink)" if cgp else
+                                   (f"replicas x{world}" if world > 1 else "single")),
                    "l2": "flushed (512 MB write) before every timed step",
                    "inputs": "reference generator (bit-identical numpy streams), PE from GPU precompute"},
         "roofline": roof,
