@@ -76,26 +76,28 @@ __device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ ptr, int64
   return lo;
 }
 
-// gather global source ids edge-parallel; warp-strided so loads coalesce and
-// hub destinations spread over many warps
-constexpr int kFillPerLane = 8;
-__global__ void k_block_fill(const BlockCounters* cnt, const int64_t* __restrict__ dst_ptr, SegSpans sp,
-                             const int32_t* __restrict__ nbrs, const int32_t* __restrict__ rq_src,
-                             int32_t* src_global, uint32_t* sbits) {
-  const int64_t D = cnt->D, E = cnt->E;
+// gather global source ids: one warp per aggregation work item (kAggChunk edges
+// of one destination), so a destination's CSR row and request span are copied
+// with contiguous, coalesced loads and hub destinations spread over many warps
+__global__ void __launch_bounds__(256) k_block_fill(const BlockCounters* cnt, const int64_t* __restrict__ dst_ptr,
+                                                    const int64_t* __restrict__ item_ptr, SegSpans sp,
+                                                    const int32_t* __restrict__ nbrs,
+                                                    const int32_t* __restrict__ rq_src, int32_t* src_global,
+                                                    uint32_t* sbits) {
+  const int64_t D = cnt->D, items = cnt->items;
   const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t span = 32 * kFillPerLane;
-  for (int64_t base = warp * span; base < E; base += nwarps * span) {
-    int64_t e = base + lane;
-    if (e >= E) continue;
-    int64_t i = seg_of(dst_ptr, D, e);
-    for (int k = 0; k < kFillPerLane && e < E; ++k, e += 32) {
-      while (__ldg(dst_ptr + i + 1) <= e) ++i;
-      int64_t j = e - __ldg(dst_ptr + i);
-      int32_t cl = __ldg(sp.cl + i);
-      int32_t src = j < cl ? __ldg(nbrs + __ldg(sp.cs + i) + j) : __ldg(rq_src + __ldg(sp.rs + i) + (j - cl));
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = gw; it < items; it += nw) {
+    const int64_t i = seg_of(item_ptr, D, it);
+    const int64_t d0 = __ldg(dst_ptr + i);
+    const int64_t e0 = d0 + (it - __ldg(item_ptr + i)) * kAggChunk;
+    const int64_t e1 = min(e0 + kAggChunk, __ldg(dst_ptr + i + 1));
+    const int64_t cs = __ldg(sp.cs + i), rs = __ldg(sp.rs + i);
+    const int32_t cl = __ldg(sp.cl + i);
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int64_t j = e - d0;
+      const int32_t src = j < cl ? __ldg(nbrs + cs + j) : __ldg(rq_src + rs + (j - cl));
       src_global[e] = src;
       bm_set_warp(sbits, src);
     }
@@ -159,9 +161,10 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
                                                         w.cwpre, src.rq_ptr, w.rc, sp, w.seg_len);
   OB_LAUNCHED();
   device_scan(s, e.scan, LoadI64{w.seg_len}, StoreI64{b.dst_ptr}, &b.cnt->D, 0, b.D_max, &b.cnt->E, b.dst_ptr);
+  block_items(e, b, kAggChunk);  // work items double as the fill's edge chunks
   OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
-  k_block_fill<<<grid_for(b.E_max, 32 * kFillPerLane * 8), 256, 0, s>>>(b.cnt, b.dst_ptr, sp, src.nbrs, src.rq_src,
-                                                                         w.src_global, w.sbits);
+  k_block_fill<<<grid_for(b.items_max, 8, kNumSMs * 16), 256, 0, s>>>(b.cnt, b.dst_ptr, b.item_ptr, sp, src.nbrs,
+                                                                       src.rq_src, w.src_global, w.sbits);
   OB_LAUNCHED();
   if (b.has_self) {
     k_mark_ids<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, w.sbits);
@@ -175,7 +178,6 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
     k_self_rows<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.cnt, b.dst_ids, w.sbits, w.swpre, b.self_src);
     OB_LAUNCHED();
   }
-  block_items(e, b, kAggChunk);
   a.used = mark;  // spans are transient
 }
 

@@ -86,6 +86,9 @@ struct TcWeights {
   float* hi = nullptr;
   float* lo = nullptr;
   int N = 0, Np = 0, Kp = 0;
+  alignas(64) unsigned char map_hi[128] = {};  // CUtensorMap (TMA, 128B swizzle, box 32 x Np)
+  alignas(64) unsigned char map_lo[128] = {};
+  bool map_ready = false;
 };
 
 struct TcGemmArgs {
@@ -98,6 +101,7 @@ struct TcGemmArgs {
   int K2;
   const float* Bt;
   const float* Bt_lo;
+  const TcWeights* w;     // staged weights (TMA maps)
   int N, Np;
   float* C;
   int64_t ldc;

@@ -8,19 +8,26 @@
 // Precision: the reference accumulates in float64 (models.py:214-228) and the
 // parity bar is 1e-4 relative in fp32, which single-pass TF32 (10-bit mantissa)
 // misses.  We use the 3xTF32 split: A = A_hi + A_lo, B = B_hi + B_lo, and
-// D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in an fp32 TMEM tile.  The
-// tensor core truncates fp32 operands to TF32, so the raw fp32 tile *is* A_hi;
-// A_lo = a - trunc(a) is formed in shared memory per k-block, B_lo is prepared
-// once at model load (weights are static).
+// D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in an fp32 TMEM tile.
+// B_hi / B_lo are prepared once at model load (weights are static).
 //
-// Structure (one CTA per SM, persistent over 128-row tiles):
-//   * 256 threads stage A/B k-blocks (32 fp32 = one 128-byte row) with cp.async
-//     into the canonical K-major SWIZZLE_128B layout, up to a 4-stage ring;
-//     A_lo lives in its own double buffer so the ring holds only raw loads;
-//   * one elected thread issues 12 tcgen05.mma.kind::tf32 (3 products x 4 K=8
-//     steps) per k-block and tcgen05.commit's an mbarrier per stage;
-//   * epilogue: 8 warps tcgen05.ld 32x32b (lane quadrant x column half) ->
-//     registers -> optional addend + activation -> global.
+// Warp-specialized persistent kernel, one CTA per SM, 128-row tiles:
+//   warps 0-3  producers: gather A k-blocks (32 fp32 = one 128-byte row per
+//              tile row) with cp.async into the canonical K-major SWIZZLE_128B
+//              layout, completion signalled on the stage's mbarrier
+//              (cp.async.mbarrier.arrive.noinc); one elected thread loads the
+//              B_hi / B_lo k-blocks with TMA (cp.async.bulk.tensor, 128B swizzle)
+//   warps 4-7  transform: rewrite the A tile in place as trunc_tf32(a) and
+//              write A_lo = a - trunc_tf32(a); their own generic-proxy writes +
+//              fence.proxy.async publish the operands to the tensor core
+//   warp 12    MMA issuer: 12 x tcgen05.mma.kind::tf32 (3 products x 4 K=8
+//              steps) per k-block into one of two TMEM accumulators,
+//              tcgen05.commit frees the stage / publishes the accumulator
+//   warps 8-11 epilogue: tcgen05.ld 32x32b -> smem transpose -> coalesced
+//              addend + activation + store, overlapping the next tile's MMAs
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstring>
 
@@ -30,10 +37,12 @@ namespace ob {
 
 namespace {
 
-constexpr int kTcThreads = 256;
 constexpr int kTcBM = 128;
-constexpr int kTcBK = 32;  // fp32 per k-block: one 128-byte swizzle row
+constexpr int kTcBK = 32;                  // fp32 per k-block: one 128-byte swizzle row
 constexpr int kTileA = kTcBM * kTcBK * 4;  // 16 KB
+constexpr int kWarpsProd = 4, kWarpsXf = 4, kWarpsEpi = 4;
+constexpr int kTcThreads = (kWarpsProd + kWarpsXf + kWarpsEpi + 1) * 32;  // 416
+constexpr int kMmaWarp = kWarpsProd + kWarpsXf + kWarpsEpi;               // 12
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -55,13 +64,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+// arrive on the barrier when all of this thread's prior cp.async have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -115,219 +139,250 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
 
 }  // namespace
 
-// Shared memory: S-stage ring of {A, B, B_lo} k-blocks + a double-buffered A_lo.
+// Shared memory: S-stage ring of {A, A_lo, B, B_lo} + epilogue transpose tiles.
 template <int NP>
 struct TcSmem {
   static constexpr int kTileB = NP * kTcBK * 4;
-  static constexpr int kStage = kTileA + 2 * kTileB;
-  static constexpr int kBudget = 227 * 1024 - 2 * kTileA - (1024 + 256 + kTcBM * 8);
-  static constexpr int kStages = (kBudget / kStage) >= 4 ? 4 : ((kBudget / kStage) >= 3 ? 3 : 2);
-  static constexpr int kBytes = kStages * kStage + 2 * kTileA + 1024 /*align*/ + 256 /*bars*/ + kTcBM * 8;
+  static constexpr int kStage = 2 * kTileA + 2 * kTileB;
+  static constexpr int kEpi = kWarpsEpi * 32 * 32 * 4;  // 16 KB
+  static constexpr int kFixed = kEpi + 1024 /*align*/ + 512 /*bars*/;
+  static constexpr int kStages = ((227 * 1024 - kFixed) / kStage) >= 4 ? 4
+                                 : (((227 * 1024 - kFixed) / kStage) >= 3 ? 3 : 2);
+  static constexpr int kBytes = kStages * kStage + kFixed;
+  static constexpr uint32_t kCols = NP <= 32 ? 64 : (NP <= 64 ? 128 : (NP <= 128 ? 256 : 512));  // 2 accumulators
 };
 
 template <int NP>
-__global__ void __launch_bounds__(kTcThreads, 1) k_tc_gemm(TcGemmArgs g) {
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_tc_gemm(TcGemmArgs g, const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo) {
   using SM = TcSmem<NP>;
   constexpr int S = SM::kStages;
-  constexpr uint32_t kCols = NP <= 32 ? 32 : (NP <= 64 ? 64 : (NP <= 128 ? 128 : 256));
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // offset (not an integer cast) keeps the pointer in the shared window -> LDS/STS
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* alo_base = base + S * SM::kStage;  // 2 x 16 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(alo_base + 2 * kTileA);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S + 1);
-  const float** rows = reinterpret_cast<const float**>(alo_base + 2 * kTileA + 256);
+  float* epi_buf = reinterpret_cast<float*>(base + S * SM::kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + S * SM::kStage + SM::kEpi);
+  uint64_t* ready = full + S;
+  uint64_t* empty = ready + S;
+  uint64_t* tfull = empty + S;   // [2]
+  uint64_t* tempty = tfull + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t M = *g.M_dev;
   const int64_t tiles = (M + kTcBM - 1) / kTcBM;
   const int KB1 = (g.K1 + kTcBK - 1) / kTcBK, KB2 = (g.K2 + kTcBK - 1) / kTcBK, KB = KB1 + KB2;
-  const int Kp = KB * kTcBK;
 
   if (tid == 0) {
-    for (int i = 0; i < S + 1; ++i) mbar_init(bars + i, 1);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, kWarpsProd * 32 + 1);  // cp.async arrivals + the TMA expect_tx arrival
+      mbar_init(ready + i, kWarpsXf * 32);
+      mbar_init(empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull + i, 1);
+      mbar_init(tempty + i, kWarpsEpi * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(kCols));
+                 "r"(SM::kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = tf32_idesc(NP);
 
-  uint32_t it = 0;  // global k-block counter across tiles (stage / phase bookkeeping)
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t m0 = tile * kTcBM;
-    if (tid < kTcBM) {  // per-tile A1 row pointers
-      const int64_t r = m0 + tid;
-      const float* p = nullptr;
-      if (r < M && g.K1) p = g.a1.row(g.self ? (int64_t)g.self[r] : r);
-      rows[tid] = p;
-    }
-    __syncthreads();
-
-    auto load = [&](int kb, int stage) {
-      uint8_t* sA = base + stage * SM::kStage;
-      const uint32_t a_s = smem_u32(sA), b_s = a_s + kTileA, bl_s = b_s + SM::kTileB;
-      const bool first = kb < KB1;
-      const int k0 = (first ? kb : kb - KB1) * kTcBK;
-      const int Kv = first ? g.K1 : g.K2;
+  if (warp < kWarpsProd) {
+    // ---------------- producers ----------------
+    uint32_t gk = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int64_t row = tile * kTcBM + tid;  // one tile row per producer thread
+      const float* p1 = nullptr;
+      const float* p2 = nullptr;
+      if (row < M) {
+        if (g.K1) p1 = g.a1.row(g.self ? (int64_t)g.self[row] : row);
+        if (g.K2) p2 = g.a2 + row * g.lda2;
+      }
+      for (int kb = 0; kb < KB; ++kb, ++gk) {
+        const int s = gk % S;
+        if (gk >= (uint32_t)S) mbar_wait(empty + s, ((gk / S) - 1) & 1);
+        uint8_t* st = base + s * SM::kStage;
+        const uint32_t a_s = smem_u32(st);
+        const bool first = kb < KB1;
+        const int k0 = (first ? kb : kb - KB1) * kTcBK;
+        const int Kv = first ? g.K1 : g.K2;
+        const float* rp = first ? p1 : p2;
 #pragma unroll
-      for (int i = 0; i < (kTcBM * 8) / kTcThreads; ++i) {
-        const int q = tid + i * kTcThreads;
-        const int r = q >> 3, c = q & 7;
-        const int k = k0 + c * 4;
-        const float* src = nullptr;
-        int bytes = 0;
-        if (m0 + r < M) {
-          const float* rowp = first ? rows[r] : g.a2 + (m0 + r) * g.lda2;
+        for (int c = 0; c < 8; ++c) {
+          const int k = k0 + c * 4;
           const int rem = Kv - k;
-          bytes = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
-          src = rowp + (bytes ? k : 0);
+          const int bytes = rp ? (rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0)) : 0;
+          const float* src = bytes ? rp + k : g.Bt;  // any valid address when 0 bytes are read
+          cp_async16(a_s + tid * 128 + ((c ^ (tid & 7)) << 4), src, bytes);
         }
-        if (!src) src = g.Bt;  // any valid address; 0 bytes are read
-        cp_async16(a_s + r * 128 + ((c ^ (r & 7)) << 4), src, bytes);
-      }
-#pragma unroll
-      for (int i = 0; i < (NP * 8 + kTcThreads - 1) / kTcThreads; ++i) {
-        const int q = tid + i * kTcThreads;
-        if (q < NP * 8) {
-          const int n = q >> 3, c = q & 7;
-          const int64_t off = (int64_t)n * Kp + kb * kTcBK + c * 4;
-          const uint32_t so = n * 128 + ((c ^ (n & 7)) << 4);
-          cp_async16(b_s + so, g.Bt + off, 16);
-          cp_async16(bl_s + so, g.Bt_lo + off, 16);
+        cp_async_arrive(full + s);
+        if (tid == 0) {
+          mbar_expect_tx(full + s, 2 * SM::kTileB);
+          const uint32_t b_s = a_s + 2 * kTileA;
+          tma_load_2d(b_s, &map_hi, kb * kTcBK, 0, full + s);
+          tma_load_2d(b_s + SM::kTileB, &map_lo, kb * kTcBK, 0, full + s);
         }
       }
-    };
-
-#pragma unroll
-    for (int s = 0; s < S - 1; ++s) {
-      if (s < KB) load(s, (it + s) % S);
-      cp_async_commit();
     }
-    for (int kb = 0; kb < KB; ++kb) {
-      const uint32_t gk = it + kb;
-      const int stage = gk % S;
-      cp_async_wait<S - 2>();
-      __syncthreads();
-      // A_lo = a - trunc_tf32(a) into the double buffer (MMAs of k-block gk-2 have retired:
-      // we waited for gk-2 before refilling its stage one iteration ago)
-      {
-        const float* a = reinterpret_cast<const float*>(base + stage * SM::kStage);
-        float* alo = reinterpret_cast<float*>(alo_base + (gk & 1) * kTileA);
-#pragma unroll 4
-        for (int i = tid * 4; i < kTcBM * kTcBK; i += kTcThreads * 4) {
+  } else if (warp < kWarpsProd + kWarpsXf) {
+    // ---------------- transform: A -> (trunc A, A - trunc A) ----------------
+    const int t = tid - kWarpsProd * 32;
+    uint32_t gk = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int kb = 0; kb < KB; ++kb, ++gk) {
+        const int s = gk % S;
+        mbar_wait(full + s, (gk / S) & 1);
+        float* a = reinterpret_cast<float*>(base + s * SM::kStage);
+        float* alo = a + kTcBM * kTcBK;
+#pragma unroll
+        for (int i = t * 4; i < kTcBM * kTcBK; i += kWarpsXf * 32 * 4) {
           const float4 v = *reinterpret_cast<const float4*>(a + i);
-          float4 o;
-          o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-          o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-          o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-          o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          float4 h, o;
+          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          o.x = v.x - h.x, o.y = v.y - h.y, o.z = v.z - h.z, o.w = v.w - h.w;
+          *reinterpret_cast<float4*>(a + i) = h;
           *reinterpret_cast<float4*>(alo + i) = o;
         }
+        fence_proxy_async();
+        mbar_arrive(ready + s);
       }
-      fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc_fence_after();
-        const uint32_t a_s = smem_u32(base + stage * SM::kStage);
-        const uint32_t b_s = a_s + kTileA, blo_s = b_s + SM::kTileB;
-        const uint32_t alo_s = smem_u32(alo_base + (gk & 1) * kTileA);
-#pragma unroll
-        for (int kk = 0; kk < kTcBK / 8; ++kk) {
-          const uint32_t off = kk * 32;  // 8 tf32 per MMA
-          const uint64_t da = sw128_desc(a_s + off), dal = sw128_desc(alo_s + off);
-          const uint64_t db = sw128_desc(b_s + off), dbl = sw128_desc(blo_s + off);
-          mma_tf32(tmem, da, db, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-          mma_tf32(tmem, da, dbl, idesc, 1u);
-          mma_tf32(tmem, dal, db, idesc, 1u);
-        }
-        mma_commit(bars + stage);
-      }
-      // refill the stage consumed by the previous k-block once its MMAs retired
-      const int nk = kb + S - 1;
-      if (nk < KB) {
-        if (kb > 0) mbar_wait(bars + ((gk - 1) % S), ((gk - 1) / S) & 1);
-        load(nk, (gk + S - 1) % S);
-      }
-      cp_async_commit();
     }
-    {
-      const uint32_t glast = it + KB - 1;
-      mbar_wait(bars + (glast % S), (glast / S) & 1);
-    }
-    it += KB;
-    tc_fence_after();
-    // epilogue: warp w reads TMEM lanes [32(w%4), +32) = tile rows, column half w/4;
-    // each 32x32 block is transposed through shared memory (the free A_lo buffers,
-    // XOR-swizzled) so E loads and C stores run with lanes along a row (coalesced)
-    {
-      const int quad = warp & 3, half = warp >> 2;
-      constexpr int kHalf = NP >= 64 ? NP / 2 : NP;
-      float* buf = reinterpret_cast<float*>(alo_base) + warp * 1024;
-      if (NP >= 64 || half == 0) {
+  } else if (warp < kMmaWarp) {
+    // ---------------- epilogue: TMEM -> smem transpose -> global ----------------
+    const int q = warp - (kWarpsProd + kWarpsXf);  // TMEM lane quadrant (warp % 4)
+    float* buf = epi_buf + q * 1024;
+    uint32_t ti = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++ti) {
+      const int acc = ti & 1;
+      mbar_wait(tfull + acc, (ti >> 1) & 1);
+      tc_fence_after();
+      const int64_t m0 = tile * kTcBM;
 #pragma unroll 1
-        for (int c0 = half * kHalf; c0 < (half + 1) * kHalf; c0 += 32) {
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + c0, v);
+      for (int c0 = 0; c0 < NP; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * NP + c0, v);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) buf[lane * 32 + (j ^ lane)] = v[j];
-          __syncwarp();
-          const int col = c0 + lane;
+        for (int j = 0; j < 32; ++j) buf[lane * 32 + (j ^ lane)] = v[j];
+        __syncwarp();
+        const int col = c0 + lane;
 #pragma unroll 4
-          for (int r = 0; r < 32; ++r) {
-            const int64_t row = m0 + quad * 32 + r;
-            if (row < M && col < g.N) {
-              float o = buf[r * 32 + (lane ^ r)];
-              if (g.E) o += g.E[row * g.lde + col];
-              if (g.relu) o = fmaxf(o, 0.f);
-              g.C[row * g.ldc + col] = o;
-            }
+        for (int r = 0; r < 32; ++r) {
+          const int64_t row = m0 + q * 32 + r;
+          if (row < M && col < g.N) {
+            float o = buf[r * 32 + (lane ^ r)];
+            if (g.E) o += __ldg(g.E + row * g.lde + col);
+            if (g.relu) o = fmaxf(o, 0.f);
+            g.C[row * g.ldc + col] = o;
           }
-          __syncwarp();
         }
+        __syncwarp();
+      }
+      tc_fence_before();
+      mbar_arrive(tempty + acc);
+    }
+  } else {
+    // ---------------- MMA issuer (one elected thread) ----------------
+    if (lane == 0) {
+      const uint32_t idesc = tf32_idesc(NP);
+      uint32_t gk = 0, ti = 0;
+      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++ti) {
+        const int acc = ti & 1;
+        if (ti >= 2) mbar_wait(tempty + acc, ((ti >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem + acc * NP;
+        for (int kb = 0; kb < KB; ++kb, ++gk) {
+          const int s = gk % S;
+          mbar_wait(ready + s, (gk / S) & 1);
+          tc_fence_after();
+          const uint32_t a_s = smem_u32(base + s * SM::kStage);
+          const uint32_t alo_s = a_s + kTileA, b_s = a_s + 2 * kTileA, blo_s = b_s + SM::kTileB;
+#pragma unroll
+          for (int kk = 0; kk < kTcBK / 8; ++kk) {
+            const uint32_t off = kk * 32;  // 8 tf32 per MMA
+            const uint64_t da = sw128_desc(a_s + off), dal = sw128_desc(alo_s + off);
+            const uint64_t db = sw128_desc(b_s + off), dbl = sw128_desc(blo_s + off);
+            mma_tf32(dcol, da, db, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32(dcol, da, dbl, idesc, 1u);
+            mma_tf32(dcol, dal, db, idesc, 1u);
+          }
+          mma_commit(empty + s);  // stage free once these MMAs retire
+        }
+        mma_commit(tfull + acc);  // accumulator complete
       }
     }
-    tc_fence_before();
-    __syncthreads();
+    __syncwarp();
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(SM::kCols));
   }
 }
 
 void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max) {
   OB_CHECK(g.N >= 1 && g.N <= 256, OB_ESTATE, "tc_gemm: N out of range");
+  OB_CHECK(g.w && g.w->map_ready, OB_ESTATE, "tc_gemm: weights not staged");
   const int64_t tiles = (M_max + kTcBM - 1) / kTcBM;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs));
   const int np = g.Np;
-  auto go = [&](auto kern, int bytes) {
+  const CUtensorMap& mh = *reinterpret_cast<const CUtensorMap*>(g.w->map_hi);
+  const CUtensorMap& ml = *reinterpret_cast<const CUtensorMap*>(g.w->map_lo);
+  auto go = [&](auto kern, int bytes, int slot) {
     static bool configured[4] = {false, false, false, false};
-    int slot = np <= 32 ? 0 : np <= 64 ? 1 : np <= 128 ? 2 : 3;
     if (!configured[slot]) {
       OB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       configured[slot] = true;
     }
-    kern<<<grid, kTcThreads, bytes, s>>>(g);
+    kern<<<grid, kTcThreads, bytes, s>>>(g, mh, ml);
   };
-  if (np == 32) go(k_tc_gemm<32>, TcSmem<32>::kBytes);
-  else if (np == 64) go(k_tc_gemm<64>, TcSmem<64>::kBytes);
-  else if (np == 128) go(k_tc_gemm<128>, TcSmem<128>::kBytes);
-  else if (np == 256) go(k_tc_gemm<256>, TcSmem<256>::kBytes);
+  if (np == 32) go(k_tc_gemm<32>, TcSmem<32>::kBytes, 0);
+  else if (np == 64) go(k_tc_gemm<64>, TcSmem<64>::kBytes, 1);
+  else if (np == 128) go(k_tc_gemm<128>, TcSmem<128>::kBytes, 2);
+  else if (np == 256) go(k_tc_gemm<256>, TcSmem<256>::kBytes, 3);
   else throw Error(OB_ESTATE, "tc_gemm: padded N must be 32/64/128/256");
   OB_LAUNCHED();
 }
 
 // ---------------------------------------------------------------------------
-// weight preparation: W (K x N row-major) blocks -> Bt / Bt_lo (Np x Kp, K-major,
-// zero padded), K-blocks of each operand segment padded to 32
+// weight preparation: W (K x N row-major) segments -> Bt / Bt_lo (Np x Kp, K-major,
+// zero padded), each K segment padded to 32; TMA maps over both (128B swizzle)
 // ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    OB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    OB_CHECK(p && q == cudaDriverEntryPointSuccess, OB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static void make_map(void* out, float* base, int Np, int Kp) {
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out);
+  const cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)Np};
+  const cuuint64_t strides[1] = {(cuuint64_t)Kp * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)Np};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  OB_CHECK(r == CUDA_SUCCESS, OB_ECUDA, "cuTensorMapEncodeTiled failed");
+}
+
 void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std::vector<int>& seg_k, int N,
                      TcWeights* out) {
   int Np = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
@@ -347,7 +402,7 @@ void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std
         b &= 0xFFFFE000u;
         float h;
         std::memcpy(&h, &b, 4);
-        hi[(size_t)n * Kp + kbase + k] = v;
+        hi[(size_t)n * Kp + kbase + k] = h;
         lo[(size_t)n * Kp + kbase + k] = v - h;
       }
     kbase += (K + kTcBK - 1) / kTcBK * kTcBK;
@@ -359,6 +414,9 @@ void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std
   out->lo = (float*)e.dalloc(sizeof(float) * lo.size());
   OB_CUDA(cudaMemcpy(out->hi, hi.data(), sizeof(float) * hi.size(), cudaMemcpyHostToDevice));
   OB_CUDA(cudaMemcpy(out->lo, lo.data(), sizeof(float) * lo.size(), cudaMemcpyHostToDevice));
+  make_map(out->map_hi, out->hi, Np, Kp);
+  make_map(out->map_lo, out->lo, Np, Kp);
+  out->map_ready = true;
 }
 
 }  // namespace ob

@@ -484,6 +484,7 @@ static TcGemmArgs gemm_args(const int64_t* M_dev, const TcWeights& w, float* C, 
   g.M_dev = M_dev;
   g.Bt = w.hi;
   g.Bt_lo = w.lo;
+  g.w = &w;
   g.N = w.N;
   g.Np = w.Np;
   g.C = C;

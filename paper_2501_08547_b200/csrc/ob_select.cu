@@ -416,9 +416,13 @@ __device__ __forceinline__ void chunk_of(const int64_t* cptr, int64_t nbig, int6
 }
 
 // sort every 4096-element chunk of every long segment in shared memory
-__global__ void __launch_bounds__(kChunkThreads) k_chunk_sort(const int64_t* __restrict__ ptr, const int64_t* ctr,
+__device__ __forceinline__ int levels_for(int64_t len);
+
+// ids are < 2^end_bit, so only end_bit radix bits are sorted; the merge levels the
+// longest segment needs are published in ctr[3] (later levels exit at once)
+__global__ void __launch_bounds__(kChunkThreads) k_chunk_sort(const int64_t* __restrict__ ptr, int64_t* ctr,
                                                               const int32_t* big_list, const int64_t* cptr,
-                                                              int32_t* vals) {
+                                                              int32_t* vals, int end_bit) {
   using BRS = cub::BlockRadixSort<int32_t, kChunkThreads, kChunkItems>;
   __shared__ typename BRS::TempStorage tmp;
   const int64_t nbig = ctr[1], nch = ctr[2];
@@ -427,13 +431,15 @@ __global__ void __launch_bounds__(kChunkThreads) k_chunk_sort(const int64_t* __r
     chunk_of(cptr, nbig, ci, &bi, &j);
     const int64_t s = big_list[bi];
     const int64_t b = ptr[s] + j * kChunk, len = min((int64_t)kChunk, ptr[s + 1] - b);
+    if (j == 0 && threadIdx.x == 0)
+      atomicMax((unsigned long long*)&ctr[3], (unsigned long long)levels_for(ptr[s + 1] - ptr[s]));
     int32_t k[kChunkItems];
 #pragma unroll
     for (int i = 0; i < kChunkItems; ++i) {
       int64_t idx = (int64_t)threadIdx.x * kChunkItems + i;
-      k[i] = idx < len ? vals[b + idx] : INT32_MAX;
+      k[i] = idx < len ? vals[b + idx] : INT32_MAX;  // padding sorts last (stable, all-ones low bits)
     }
-    BRS(tmp).Sort(k);
+    BRS(tmp).Sort(k, 0, end_bit);
 #pragma unroll
     for (int i = 0; i < kChunkItems; ++i) {
       int64_t idx = (int64_t)threadIdx.x * kChunkItems + i;
@@ -473,6 +479,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_merge_level(const int64_t* __
   __shared__ int32_t sb[kChunk];
   __shared__ int64_t split[2];
   const int64_t nbig = ctr[1], nch = ctr[2];
+  if (level >= ctr[3]) return;  // no segment needs this level
   const int64_t w = (int64_t)kChunk << level;
   for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
     int64_t bi, j;
@@ -593,7 +600,7 @@ void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound
                   bool counts_ready) {
   cudaStream_t s = e.stream;
   const int64_t rb_max = std::min<int64_t>(e.g.N, 2 * w.m) + w.B;
-  OB_CUDA(cudaMemsetAsync(c.ctr + 1, 0, 2 * sizeof(int64_t), s));
+  OB_CUDA(cudaMemsetAsync(c.ctr + 1, 0, 3 * sizeof(int64_t), s));
   if (!counts_ready) {
     k_zero_slots<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rc, w.B, c.cnt, c.fill);
     OB_LAUNCHED();
@@ -615,7 +622,9 @@ void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound
               c.big_cptr);
   const int64_t ch_max = m_bound / kChunk + rb_max / 256 + 2;
   const int g = grid_for(ch_max, 1, kNumSMs * 4);
-  k_chunk_sort<<<g, kChunkThreads, 0, s>>>(c.ptr, c.ctr, c.big_list, c.big_cptr, c.src);
+  int end_bit = 1;
+  while (end_bit < 31 && ((int64_t)1 << end_bit) <= e.g.N + w.B) ++end_bit;
+  k_chunk_sort<<<g, kChunkThreads, 0, s>>>(c.ptr, c.ctr, c.big_list, c.big_cptr, c.src, end_bit);
   OB_LAUNCHED();
   // the longest possible segment is the whole edge set; levels past a segment's
   // own count exit immediately
