@@ -276,12 +276,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int j = 0; j < 32; ++j) buf[lane * 32 + (j ^ lane)] = v[j];
         __syncwarp();
         const int col = c0 + lane;
-#pragma unroll 4
+        const int64_t r0 = m0 + q * 32;
+        if (g.E) {  // all 32 addend loads in flight before any is consumed
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            v[r] = (r0 + r < M && col < g.N) ? __ldg(g.E + (r0 + r) * g.lde + col) : 0.f;
+        }
+#pragma unroll
         for (int r = 0; r < 32; ++r) {
-          const int64_t row = m0 + q * 32 + r;
+          const int64_t row = r0 + r;
           if (row < M && col < g.N) {
             float o = buf[r * 32 + (lane ^ r)];
-            if (g.E) o += __ldg(g.E + row * g.lde + col);
+            if (g.E) o += v[r];
             if (g.relu) o = fmaxf(o, 0.f);
             g.C[row * g.ldc + col] = o;
           }
