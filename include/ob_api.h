@@ -148,7 +148,8 @@ int ob_last_block(ob_engine* e, int32_t partition, int32_t layer, int64_t* src_i
                   int32_t* bind_pe_layer, int64_t* src_degree, int64_t* dst_self_src);
 
 /* Size the request workspace for batches up to (num_queries, num_edges) so
- * later serves never allocate (bench warm-up). */
+ * later serves never allocate, and plan every later request at that edge
+ * bound so all of them replay one captured graph (serving warm-up). */
 int ob_reserve(ob_engine* e, int32_t num_queries, int64_t num_edges);
 
 /* In-library kernel profiler: CUDA events around the hot launches on the
@@ -159,6 +160,12 @@ int ob_reserve(ob_engine* e, int32_t num_queries, int64_t num_edges);
 enum ob_prof_class { OB_PROF_AGG = 0, OB_PROF_GEMM = 1, OB_PROF_FINALIZE = 2, OB_PROF_BUILD = 3,
                      OB_PROF_SELECT = 4, OB_PROF_RESOLVE = 5, OB_PROF_REQUEST = 6 };
 int ob_profile(ob_engine* e, int32_t enable);
+/* Request graphs: by default each (B, edge-count bucket) request shape is
+ * captured once into a CUDA graph and replayed (the request itself is read
+ * from a device parameter block, so any request of that shape reuses it).
+ * enable == 0 launches every stage eagerly; profiling always runs eagerly.
+ * The environment variable OB_NO_GRAPHS=1 sets the default to off. */
+int ob_set_graphs(ob_engine* e, int32_t enable);
 int ob_profile_read(ob_engine* e, int32_t kernel_class, double* total_ms, int64_t* launches,
                     double* alg_bytes, double* flops);
 

@@ -83,6 +83,7 @@ _SIGS = {
     "ob_last_block": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ob_reserve": (C.c_int, [_P, C.c_int32, C.c_int64]),
     "ob_profile": (C.c_int, [_P, C.c_int32]),
+    "ob_set_graphs": (C.c_int, [_P, C.c_int32]),
     "ob_profile_read": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), _I64P, C.POINTER(C.c_double),
                                   C.POINTER(C.c_double)]),
     "ob_partition_owner": (C.c_int, [_P, _P]),
@@ -98,7 +99,19 @@ def _load():
             f"{LIB_PATH} is missing: build it with `python -m paper_2501_08547_b200.build` "
             "(the serving path has no CPU fallback)"
         )
-    # torch (if present) loads libnccl first; our NEEDED entry then resolves to the same copy
+    # One libnccl per process: pre-load the copy torch is built against (the
+    # wheel's nvidia/nccl) so our NEEDED libnccl.so.2 resolves to it whether or
+    # not torch is imported before or after us.
+    try:
+        import nvidia.nccl as _nccl
+
+        for d in _nccl.__path__:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                C.CDLL(p, mode=C.RTLD_GLOBAL)
+                break
+    except ImportError:
+        pass
     lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
     for name, (res, args) in _SIGS.items():
         fn = getattr(lib, name)

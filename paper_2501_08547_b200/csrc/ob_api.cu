@@ -8,6 +8,7 @@
 // bounds (m, B, dataset degree profile) and reads the counters back once.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -23,6 +24,7 @@ namespace ob {
 static thread_local std::string t_err;
 
 Engine::~Engine() {
+  drop_graphs();
   cgp_destroy(*this);
   if (arena.base) cudaFree(arena.base);
   for (void* p : owned) cudaFree(p);
@@ -122,6 +124,10 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   }
   w.src_global = a.take<int32_t>(Emax);
   w.seg_len = a.take<int64_t>(Dmax);
+  w.span_cs = a.take<int64_t>(Dmax);
+  w.span_cl = a.take<int32_t>(Dmax);
+  w.span_rs = a.take<int64_t>(Dmax);
+  w.span_rl = a.take<int32_t>(Dmax);
   w.blocks = p.blocks;
   for (size_t i = 0; i < w.blocks.size(); ++i) {
     BlockDev& b = w.blocks[i];
@@ -132,9 +138,11 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     b.edge_src = a.take<int32_t>(b.E_max);
     b.src_ids = a.take<int32_t>(b.S_max);
     b.self_src = a.take<int32_t>(b.D_max);
-    // full: block l-1's dst list aliases block l's src_ids (set in stage_build_full)
+    // full: block l-1's dst list aliases block l's src_ids (set below)
     b.dst_ids = a.take<int32_t>(b.D_max);
   }
+  if (e.cfg.strategy == OB_STRATEGY_FULL)  // block l-1's destinations are block l's sources
+    for (int l = k - 1; l >= 1; --l) w.blocks[l - 1].dst_ids = w.blocks[l].src_ids;
   w.block_of_layer.assign(k, 0);
   for (int l = 1; l <= k; ++l)
     w.block_of_layer[l - 1] = (e.cfg.strategy == OB_STRATEGY_FULL) ? l - 1 : (l < k ? 0 : 1);
@@ -182,10 +190,11 @@ static void prepare_workspace(Engine& e, int B, int64_t m) {
   size_t need = dry.used + (1u << 20);
   if (need > e.arena.cap) {
     OB_CUDA(cudaStreamSynchronize(e.stream));
+    e.drop_graphs();  // captured graphs point into the old arena
+    const size_t cap = std::max(need, e.arena.cap * 3 / 2);
     if (e.arena.base) OB_CUDA(cudaFree(e.arena.base));
     e.arena.base = nullptr;
     e.arena.cap = 0;
-    size_t cap = std::max(need, (size_t)(e.arena.cap * 3 / 2));
     void* q = nullptr;
     OB_CUDA(cudaMalloc(&q, cap));
     e.arena.base = (char*)q;
@@ -230,6 +239,81 @@ static int64_t fetch_bytes(const Engine& e, const RequestWs& w, const std::vecto
   return total;
 }
 
+// request-size bucket: grids and the workspace are sized from this bound so
+// one captured graph serves every request up to it (<= 25 % slack)
+static int64_t bucket_m(int64_t m) {
+  int64_t b = 1024;
+  while (b < m) b = (b + b / 4 + 1023) / 1024 * 1024;
+  return b;
+}
+
+__global__ void k_set_params(ReqParams* p, const int64_t* edges, const float* q, int64_t m) {
+  p->edges = edges;
+  p->qfeat = q;
+  p->m = m;
+}
+
+// every stage of one request, enqueued on e.stream (eagerly or under capture)
+static void enqueue_request(Engine& e, float* d_out) {
+  cudaStream_t s = e.stream;
+  RequestWs& w = e.ws;
+  const bool srpe = e.cfg.strategy != OB_STRATEGY_FULL;
+  OB_CUDA(cudaMemsetAsync(w.rc, 0, sizeof(ReqCounters), s));
+  for (auto& b : w.blocks) OB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(BlockCounters), s));
+  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) {
+    serve_cgp(e, d_out);  // marks ev[1] between build and layers
+    return;
+  }
+  stage_request_prep(e, w, srpe);
+  if (srpe) stage_select(e, w);
+  stage_request_csr(e, w);
+  if (srpe) stage_build_srpe(e, w);
+  else stage_build_full(e, w);
+  record_mark(e.ev[1], s);
+  stage_forward(e, w, d_out);
+}
+
+static RequestGraph& request_graph(Engine& e, float* d_out) {
+  const RequestWs& w = e.ws;
+  for (auto& gr : e.graphs)
+    if (gr.B == w.B && gr.m_bound == w.m && gr.arena == e.arena.base && gr.out == d_out) return gr;
+  cudaStream_t s = e.stream;
+  const int64_t l0 = g_launches;
+  OB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  cudaGraph_t graph = nullptr;
+  try {
+    enqueue_request(e, d_out);
+  } catch (...) {
+    cudaStreamEndCapture(s, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    g_launches = l0;
+    throw;
+  }
+  OB_CUDA(cudaStreamEndCapture(s, &graph));
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t err = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  OB_CUDA(err);
+  if (e.graphs.size() >= 16) {  // evict the least recently used
+    auto lru = std::min_element(e.graphs.begin(), e.graphs.end(),
+                                [](const RequestGraph& a, const RequestGraph& b) { return a.last_use < b.last_use; });
+    cudaGraphExecDestroy(lru->exec);
+    e.graphs.erase(lru);
+  }
+  RequestGraph gr;
+  gr.B = w.B;
+  gr.m_bound = w.m;
+  gr.arena = e.arena.base;
+  gr.out = d_out;
+  gr.exec = exec;
+  gr.kernels = g_launches - l0;
+  gr.collective_bytes = e.cgp.collective_bytes;
+  g_launches = l0;  // counted per replay
+  e.graphs.push_back(gr);
+  return e.graphs.back();
+}
+
 // The request pipeline.  Inputs/outputs are device pointers.
 static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const int64_t* d_edges, float* d_out,
                          ob_breakdown* bd) {
@@ -237,33 +321,39 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   OB_CHECK(B >= 0 && m >= 0, OB_EINVAL, "negative request size");
   OB_CHECK(e.g.N + B < ((int64_t)1 << 31) - 1, OB_EINVAL, "id space exceeds int32");
   cudaStream_t s = e.stream;
-  prepare_workspace(e, B, m);
+  prepare_workspace(e, B, std::max(bucket_m(m), e.m_reserved));
   RequestWs& w = e.ws;
+  if (!e.params) e.params = (ReqParams*)e.dalloc(sizeof(ReqParams));
+  w.rp = e.params;
   w.edges = d_edges;
   w.qfeat = d_q;
   const int k = (int)e.layers.size();
   const bool srpe = e.cfg.strategy != OB_STRATEGY_FULL;
-  g_prof = e.prof.on ? &e.prof : nullptr;
-  cudaEvent_t preq = prof_begin(s);
-  OB_CUDA(cudaEventRecord(e.ev[0], s));
-  OB_CUDA(cudaMemsetAsync(w.rc, 0, sizeof(ReqCounters), s));
-  for (auto& b : w.blocks) OB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(BlockCounters), s));
   const bool cgp = e.cfg.strategy == OB_STRATEGY_SRPE_CGP;
-  if (cgp) {
-    serve_cgp(e, d_out);  // records ev[1] between build and layers
+  // kernel arguments are copied at launch: the block is stream-ordered with no host staging
+  k_set_params<<<1, 1, 0, s>>>(e.params, d_edges, d_q, m);
+  OB_LAUNCHED();
+  OB_CUDA(cudaEventRecord(e.ev[0], s));
+  if (e.prof.on || !e.use_graphs) {
+    g_prof = e.prof.on ? &e.prof : nullptr;
+    cudaEvent_t preq = prof_begin(s);
+    try {
+      enqueue_request(e, d_out);
+    } catch (...) {
+      g_prof = nullptr;
+      throw;
+    }
+    prof_end(s, preq, kProfRequest, nullptr, 0, 0, 0, 0, 0);
+    if (g_prof) g_prof->request_end(s);
+    g_prof = nullptr;
   } else {
-    stage_request_prep(e, w, srpe);
-    if (srpe) stage_select(e, w);
-    stage_request_csr(e, w);
-    if (srpe) stage_build_srpe(e, w);
-    else stage_build_full(e, w);
-    OB_CUDA(cudaEventRecord(e.ev[1], s));
-    stage_forward(e, w, d_out);
+    RequestGraph& gr = request_graph(e, d_out);
+    gr.last_use = ++e.graph_clock;
+    OB_CUDA(cudaGraphLaunch(gr.exec, s));
+    g_launches += gr.kernels;
+    e.cgp.collective_bytes = gr.collective_bytes;
   }
   OB_CUDA(cudaEventRecord(e.ev[2], s));
-  prof_end(s, preq, kProfRequest, nullptr, 0, 0, 0, 0, 0);
-  if (g_prof) g_prof->request_end(s);
-  g_prof = nullptr;
   e.have_request = true;
   if (!bd) return;
   PinnedReadback hb{};
@@ -516,6 +606,7 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
       e.own_stream = true;
     }
     for (auto& ev_ : e.ev) OB_CUDA(cudaEventCreate(&ev_));
+    if (const char* v = std::getenv("OB_NO_GRAPHS")) e.use_graphs = !(v[0] && v[0] != '0');
     if (cfg->nccl_id && cfg->strategy == OB_STRATEGY_SRPE_CGP) {
       try {
         cgp_init_comm(e);
@@ -771,11 +862,23 @@ int ob_reserve(ob_engine* h, int32_t B, int64_t m) {
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
     check_ready(e);
-    prepare_workspace(e, B, m);
+    e.m_reserved = bucket_m(m);
+    prepare_workspace(e, B, e.m_reserved);
     const int H = e.layers.back().spec.out_dim;
     ensure(h->d_edges, h->cap_edges, (size_t)(2 * m));
     ensure(h->d_q, h->cap_q, (size_t)B * e.g.F);
     ensure(h->d_out, h->cap_out, (size_t)B * H);
+  });
+}
+
+int ob_set_graphs(ob_engine* h, int32_t enable) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    OB_CUDA(cudaStreamSynchronize(h->impl.stream));
+    h->impl.use_graphs = enable != 0;
+    if (!enable) h->impl.drop_graphs();
   });
 }
 
@@ -787,6 +890,7 @@ int ob_profile(ob_engine* h, int32_t enable) {
     OB_CUDA(cudaStreamSynchronize(h->impl.stream));
     h->impl.prof.reset();
     h->impl.prof.on = enable != 0;
+    if (enable) h->impl.prof.prime(8192);
   });
 }
 

@@ -150,13 +150,11 @@ void block_items(Engine& e, BlockDev& b, int64_t chunk) {
 // rank's source-split CSR) and the request CSR (whole request or the rank's slice).
 void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
   cudaStream_t s = e.stream;
-  SegSpans sp;
-  Arena& a = e.arena;
-  size_t mark = a.used;
-  sp.cs = a.take<int64_t>(b.D_max);
-  sp.cl = a.take<int32_t>(b.D_max);
-  sp.rs = a.take<int64_t>(b.D_max);
-  sp.rl = a.take<int32_t>(b.D_max);
+  SegSpans sp;  // transient, shared by every block of the request
+  sp.cs = w.span_cs;
+  sp.cl = w.span_cl;
+  sp.rs = w.span_rs;
+  sp.rl = w.span_rl;
   k_block_spans<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, e.g.N, src.offsets, src.deg, w.cbits,
                                                         w.cwpre, src.rq_ptr, w.rc, sp, w.seg_len);
   OB_LAUNCHED();
@@ -178,7 +176,6 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
     k_self_rows<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.cnt, b.dst_ids, w.sbits, w.swpre, b.self_src);
     OB_LAUNCHED();
   }
-  a.used = mark;  // spans are transient
 }
 
 void write_mid_dst(Engine& e, RequestWs& w, BlockDev& b) {
@@ -209,8 +206,7 @@ void stage_build_full(Engine& e, RequestWs& w) {
   for (int l = k; l >= 1; --l) {
     BlockDev& b = w.blocks[l - 1];
     if (l < k) {
-      BlockDev& up = w.blocks[l];
-      b.dst_ids = up.src_ids;
+      BlockDev& up = w.blocks[l];  // b.dst_ids aliases up.src_ids (carve)
       k_copy_count_D<<<1, 1, 0, s>>>(b.cnt, up.cnt);
       OB_LAUNCHED();
     }

@@ -113,10 +113,11 @@ void cgp_build_partitions(Engine& e) {
 }
 
 // request slice of partition r: edges whose source it owns (queries: round robin)
-__global__ void k_filter_slice(const int64_t* __restrict__ edges, int64_t m, int64_t N, int P, int r,
-                               const int32_t* __restrict__ owner, const ReqCounters* rc, int64_t* out,
-                               int64_t* count) {
+__global__ void k_filter_slice(const ReqParams* rp, int64_t N, int P, int r, const int32_t* __restrict__ owner,
+                               const ReqCounters* rc, int64_t* out, int64_t* count) {
   if (rc->err & (kErrRange | kErrNoQuery)) return;
+  const int64_t* __restrict__ edges = rp->edges;
+  const int64_t m = rp->m;
   OB_GRID_STRIDE(e, m) {
     const int64_t s = edges[2 * e];
     const int o = s >= N ? (int)((s - N) % P) : owner[s];
@@ -293,7 +294,7 @@ void serve_cgp(Engine& e, float* d_out) {
     OB_CUDA(cudaMemsetAsync(pw.blocks[0].cnt, 0, sizeof(BlockCounters), s));
     OB_CUDA(cudaMemsetAsync(pw.blocks[1].cnt, 0, sizeof(BlockCounters), s));
     if (w.m > 0) {
-      k_filter_slice<<<grid_for(w.m, 256), 256, 0, s>>>(w.edges, w.m, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
+      k_filter_slice<<<grid_for(w.m, 256), 256, 0, s>>>(w.rp, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
                                                          pw.rq.ctr);
       OB_LAUNCHED();
     }
@@ -304,7 +305,7 @@ void serve_cgp(Engine& e, float* d_out) {
     write_query_dst(e, w, pw.blocks[1]);
     assemble(e, w, pw.blocks[1], src);
   }
-  OB_CUDA(cudaEventRecord(e.ev[1], s));
+  record_mark(e.ev[1], s);
   stage_qpad(e, w);
   OB_CUDA(cudaMemsetAsync(c.zero_row, 0, sizeof(float) * (ld4(std::max(e.g.F, 4)) + 512), s));
   const int64_t part_stride_f = c.D_max * c.ldp;  // floats between partitions (x2 for float64 partials)

@@ -162,10 +162,21 @@ struct RqCsr {
   int64_t* ctr = nullptr;       // device [4]: m (edge count), n_big, n_chunks, spare
 };
 
+// Request inputs as seen by the kernels: written (16 bytes of pointers + m) before
+// each request so a captured CUDA graph can be replayed for any request whose
+// size fits the graph's bucket.
+struct ReqParams {
+  const int64_t* edges;  // device [m][2]
+  const float* qfeat;    // device [B][F]
+  int64_t m;             // edge count of this request
+  int64_t pad;
+};
+
 // Per-request device workspace for the centralized pipeline.
 struct RequestWs {
   int B = 0;
-  int64_t m = 0;
+  int64_t m = 0;                   // bucket bound on the edge count (sizes grids and buffers)
+  const ReqParams* rp = nullptr;   // device
   ReqCounters* rc = nullptr;
   const int64_t* edges = nullptr;  // device [m][2]
   const float* qfeat = nullptr;    // device [B][F] as given
@@ -209,6 +220,10 @@ struct RequestWs {
   int64_t* swpre = nullptr;
   int32_t* src_global = nullptr;   // [E_max] gathered global source ids
   int64_t* seg_len = nullptr;      // [D_max]
+  int64_t* span_cs = nullptr;      // [Dmax] block-assembly spans (CSR start/len, request start/len)
+  int32_t* span_cl = nullptr;
+  int64_t* span_rs = nullptr;
+  int32_t* span_rl = nullptr;
   // blocks
   std::vector<BlockDev> blocks;    // blocks[l-1] feeds layer l (mid blocks may alias)
   std::vector<int> block_of_layer; // layer -> index into blocks
@@ -252,6 +267,7 @@ struct Profiler {
   int slot_for(const BlockCounters* d);
   void request_end(cudaStream_t s);
   void reset();
+  void prime(size_t events);  // allocate up front so profiled requests do no allocation
 };
 extern Profiler* g_prof;
 cudaEvent_t prof_begin(cudaStream_t s);
@@ -416,6 +432,29 @@ void serve_cgp(Engine& e, float* d_out);
 void cgp_destroy(Engine& e);
 void cgp_init_comm(Engine& e);
 
+// One instantiated CUDA graph of the whole request pipeline.  Kernels read
+// the request through the fixed ReqParams block and size their grids from
+// the bucketed bound, so one graph serves every request with the same
+// (B, m bucket) while the arena and output pointer stay put.
+struct RequestGraph {
+  int B = 0;
+  int64_t m_bound = 0;
+  const char* arena = nullptr;
+  const float* out = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;           // kernel launches per replay (ob_launch_count)
+  int64_t collective_bytes = 0;  // CGP accounting captured with the graph
+  uint64_t last_use = 0;
+};
+
+// stage boundary marks: recorded as event nodes when the stream is being captured
+inline void record_mark(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  OB_CUDA(cudaStreamIsCapturing(s, &st));
+  if (st == cudaStreamCaptureStatusActive) OB_CUDA(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal));
+  else OB_CUDA(cudaEventRecord(ev, s));
+}
+
 struct Engine {
   ob_config cfg{};
   CgpState cgp;
@@ -432,6 +471,16 @@ struct Engine {
   cudaEvent_t ev[6] = {};
   int64_t launches_at_start = 0;
   Profiler prof;
+  ReqParams* params = nullptr;   // device parameter block of the in-flight request
+  bool use_graphs = true;        // replay captured request graphs (eager when profiling)
+  int64_t m_reserved = 0;        // ob_reserve: edge-count bound every request is planned at (one graph)
+  std::vector<RequestGraph> graphs;
+  uint64_t graph_clock = 0;
+  void drop_graphs() {
+    for (auto& gr : graphs)
+      if (gr.exec) cudaGraphExecDestroy(gr.exec);
+    graphs.clear();
+  }
   std::vector<void*> owned;      // device allocations to free
   void* dalloc(size_t bytes) {
     void* p = nullptr;

@@ -345,20 +345,22 @@ void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max) {
   const int np = g.Np;
   const CUtensorMap& mh = *reinterpret_cast<const CUtensorMap*>(g.w->map_hi);
   const CUtensorMap& ml = *reinterpret_cast<const CUtensorMap*>(g.w->map_lo);
-  auto go = [&](auto kern, int bytes, int slot) {
-    static bool configured[4] = {false, false, false, false};
-    if (!configured[slot]) {
-      OB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      configured[slot] = true;
-    }
-    kern<<<grid, kTcThreads, bytes, s>>>(g, mh, ml);
-  };
-  if (np == 32) go(k_tc_gemm<32>, TcSmem<32>::kBytes, 0);
-  else if (np == 64) go(k_tc_gemm<64>, TcSmem<64>::kBytes, 1);
-  else if (np == 128) go(k_tc_gemm<128>, TcSmem<128>::kBytes, 2);
-  else if (np == 256) go(k_tc_gemm<256>, TcSmem<256>::kBytes, 3);
+  // smem opt-in is set at weight preparation (tc_gemm_configure), never while a
+  // request is being captured into a CUDA graph
+  auto go = [&](auto kern, int bytes) { kern<<<grid, kTcThreads, bytes, s>>>(g, mh, ml); };
+  if (np == 32) go(k_tc_gemm<32>, TcSmem<32>::kBytes);
+  else if (np == 64) go(k_tc_gemm<64>, TcSmem<64>::kBytes);
+  else if (np == 128) go(k_tc_gemm<128>, TcSmem<128>::kBytes);
+  else if (np == 256) go(k_tc_gemm<256>, TcSmem<256>::kBytes);
   else throw Error(OB_ESTATE, "tc_gemm: padded N must be 32/64/128/256");
   OB_LAUNCHED();
+}
+
+static void tc_gemm_configure() {
+  OB_CUDA(cudaFuncSetAttribute(k_tc_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<32>::kBytes));
+  OB_CUDA(cudaFuncSetAttribute(k_tc_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<64>::kBytes));
+  OB_CUDA(cudaFuncSetAttribute(k_tc_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<128>::kBytes));
+  OB_CUDA(cudaFuncSetAttribute(k_tc_gemm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<256>::kBytes));
 }
 
 // ---------------------------------------------------------------------------
@@ -391,6 +393,7 @@ static void make_map(void* out, float* base, int Np, int Kp) {
 
 void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std::vector<int>& seg_k, int N,
                      TcWeights* out) {
+  tc_gemm_configure();
   int Np = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   OB_CHECK(N <= 256, OB_EINVAL, "layer width above 256 is not supported by the tensor-core path");
   int Kp = 0;

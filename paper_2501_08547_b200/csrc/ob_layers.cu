@@ -957,7 +957,8 @@ BindCtx bind_ctx(Engine& e, RequestWs& w, int l) {
   return c;
 }
 
-__global__ void k_pad_rows(const float* __restrict__ src, int64_t rows, int w, float* dst, int64_t ld) {
+__global__ void k_pad_rows(const ReqParams* rp, int64_t rows, int w, float* dst, int64_t ld) {
+  const float* __restrict__ src = rp->qfeat;
   const int64_t n = rows * ld;
   OB_GRID_STRIDE(i, n) {
     const int64_t r = i / ld;
@@ -970,7 +971,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
   cudaStream_t s = e.stream;
   const int k = (int)e.layers.size();
   // stage query features with 16 B aligned rows
-  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, s>>>(w.qfeat, w.B, e.g.F, w.qpad, e.g.F_ld);
+  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, s>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
   OB_LAUNCHED();
   for (int l = 1; l <= k; ++l) {
     const LayerDev& L = e.layers[l - 1];
@@ -1000,7 +1001,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
 }
 
 void stage_qpad(Engine& e, RequestWs& w) {
-  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, e.stream>>>(w.qfeat, w.B, e.g.F, w.qpad, e.g.F_ld);
+  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, e.stream>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
   OB_LAUNCHED();
 }
 

@@ -38,6 +38,18 @@ void Profiler::request_end(cudaStream_t s) {
   pending.clear();
 }
 
+void Profiler::prime(size_t events) {
+  while (pool.size() < events) {
+    cudaEvent_t ev;
+    OB_CUDA(cudaEventCreate(&ev));
+    pool.push_back(ev);
+  }
+  if (!pinned) {
+    nslots = 1 << 14;
+    OB_CUDA(cudaMallocHost(&pinned, sizeof(BlockCounters) * nslots));
+  }
+}
+
 void Profiler::reset() {
   next = 0;
   recs.clear();

@@ -77,9 +77,11 @@ __device__ __forceinline__ int32_t warp_agg_inc(int32_t* base, int64_t slot) {
 constexpr int kEdgeTile = 4096;  // request edges per CTA pass
 constexpr int kMaxSmemQueries = 12288;
 
-__global__ void __launch_bounds__(256) k_request_mark(const int64_t* __restrict__ edges, int64_t m, int64_t N, int B,
-                                                      uint32_t* cbits, int32_t* qdeg, ReqCounters* rc) {
+__global__ void __launch_bounds__(256) k_request_mark(const ReqParams* rp, int64_t N, int B, uint32_t* cbits,
+                                                      int32_t* qdeg, ReqCounters* rc) {
   extern __shared__ int32_t sq[];  // per-CTA query in-degree histogram (B entries) when B fits
+  const int64_t* __restrict__ edges = rp->edges;
+  const int64_t m = rp->m;
   const bool smem = B <= kMaxSmemQueries;
   const int64_t hi = N + B;
   int64_t err = 0;
@@ -111,7 +113,8 @@ __global__ void __launch_bounds__(256) k_request_mark(const int64_t* __restrict_
   if (err) atomicOr((unsigned long long*)&rc->err, (unsigned long long)err);
 }
 
-__global__ void k_check_finite(const float* __restrict__ q, int64_t n, ReqCounters* rc) {
+__global__ void k_check_finite(const ReqParams* rp, int64_t n, ReqCounters* rc) {
+  const float* __restrict__ q = rp->qfeat;
   bool bad = false;
   OB_GRID_STRIDE(i, n) bad |= !isfinite(q[i]);
   if (bad) atomicOr((unsigned long long*)&rc->err, (unsigned long long)kErrNonFinite);
@@ -147,9 +150,11 @@ __global__ void k_slots_init(ReqCounters* rc, int B, const int32_t* qdeg, int32_
   }
 }
 
-__global__ void k_rq_count(const int64_t* __restrict__ edges, int64_t m, int64_t N, const uint32_t* cbits,
-                           const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt) {
+__global__ void k_rq_count(const ReqParams* rp, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
+                           const ReqCounters* rc, int32_t* rq_cnt) {
   if (rc->err & (kErrRange | kErrNoQuery)) return;
+  const int64_t* __restrict__ edges = rp->edges;
+  const int64_t m = rp->m;
   OB_GRID_STRIDE(e, m) {
     int64_t d = edges[2 * e + 1];
     if (d < N) warp_agg_inc(rq_cnt, bm_rank(cbits, cwpre, d));
@@ -166,7 +171,7 @@ __device__ __forceinline__ int64_t rq_slot(int64_t d, int64_t N, const uint32_t*
 __global__ void k_rq_count_all(const int64_t* __restrict__ edges, int64_t m_host, const int64_t* m_dev, int64_t N,
                                const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt) {
   if (rc->err & (kErrRange | kErrNoQuery)) return;
-  const int64_t R = rc->R, m = dev_count(m_dev, m_host);
+  const int64_t R = rc->R, m = dev_count(m_dev, m_host);  // a CGP slice: edges live in the arena
   OB_GRID_STRIDE(e, m) warp_agg_inc(rq_cnt, rq_slot(edges[2 * e + 1], N, cbits, cwpre, R));
 }
 
@@ -292,15 +297,17 @@ struct SelStore {
 // 3. request CSR fill: per-CTA reservation for query slots, warp-aggregated
 //    atomics for candidate slots
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_rq_fill(const int64_t* __restrict__ edges, int64_t m_host,
-                                                 const int64_t* m_dev, int64_t N, int B, const uint32_t* cbits,
-                                                 const int64_t* cwpre, const ReqCounters* rc, const int64_t* rq_ptr,
-                                                 int32_t* rq_fill, int32_t* rq_src) {
+__global__ void __launch_bounds__(256) k_rq_fill(const int64_t* __restrict__ edges_arg, int64_t m_host,
+                                                 const int64_t* m_dev, const ReqParams* rp, int64_t N, int B,
+                                                 const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc,
+                                                 const int64_t* rq_ptr, int32_t* rq_fill, int32_t* rq_src) {
   extern __shared__ int32_t sm[];  // [B] counts, then [B] base offsets
   const bool smem = B <= kMaxSmemQueries / 2;
   if (rc->err & (kErrRange | kErrNoQuery)) return;
   const int64_t R = rc->R;
-  const int64_t m = dev_count(m_dev, m_host);
+  // the whole request (edges from the parameter block) or a CGP slice in the arena
+  const int64_t* __restrict__ edges = rp ? rp->edges : edges_arg;
+  const int64_t m = rp ? rp->m : dev_count(m_dev, m_host);
   int32_t* cnt = sm;
   int32_t* base = sm + B;
   for (int64_t t0 = (int64_t)blockIdx.x * kEdgeTile; t0 < m; t0 += (int64_t)gridDim.x * kEdgeTile) {
@@ -551,11 +558,11 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   OB_CUDA(cudaMemsetAsync(w.qdeg, 0, sizeof(int32_t) * (w.B + 1), s));
   const size_t sq = w.B <= kMaxSmemQueries ? sizeof(int32_t) * w.B : 0;
   if (m > 0) {
-    k_request_mark<<<grid_for(m, kEdgeTile, kNumSMs * 4), 256, sq, s>>>(w.edges, m, N, w.B, w.cbits, w.qdeg, w.rc);
+    k_request_mark<<<grid_for(m, kEdgeTile, kNumSMs * 4), 256, sq, s>>>(w.rp, N, w.B, w.cbits, w.qdeg, w.rc);
     OB_LAUNCHED();
   }
   if ((int64_t)w.B * e.g.F > 0) {
-    k_check_finite<<<grid_for((int64_t)w.B * e.g.F, 256), 256, 0, s>>>(w.qfeat, (int64_t)w.B * e.g.F, w.rc);
+    k_check_finite<<<grid_for((int64_t)w.B * e.g.F, 256), 256, 0, s>>>(w.rp, (int64_t)w.B * e.g.F, w.rc);
     OB_LAUNCHED();
   }
   // candidate set: popcount prefix, ascending ids
@@ -566,7 +573,7 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   k_slots_init<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rc, w.B, w.qdeg, w.rq_cnt, w.rq_fill);
   OB_LAUNCHED();
   if (m > 0) {
-    k_rq_count<<<grid_for(m, 256), 256, 0, s>>>(w.edges, m, N, w.cbits, w.cwpre, w.rc, w.rq_cnt);
+    k_rq_count<<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt);
     OB_LAUNCHED();
   }
   if (need_scores) {
@@ -594,10 +601,12 @@ void stage_select(Engine& e, RequestWs& w) {
               r_max, &w.rc->T);
 }
 
-// Request CSR over an edge set (the whole request, or one CGP rank's slice):
-// bucket by destination slot, then sort each slot's sources ascending.
+// Request CSR over an edge set (the whole request via the parameter block when
+// edges == nullptr, or one CGP rank's slice in the arena): bucket by destination
+// slot, then sort each slot's sources ascending.
 void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound, const int64_t* m_dev, RqCsr& c,
                   bool counts_ready) {
+  const ReqParams* rp = edges ? nullptr : w.rp;
   cudaStream_t s = e.stream;
   const int64_t rb_max = std::min<int64_t>(e.g.N, 2 * w.m) + w.B;
   OB_CUDA(cudaMemsetAsync(c.ctr + 1, 0, 3 * sizeof(int64_t), s));
@@ -613,8 +622,8 @@ void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound
   device_scan(s, e.scan, LoadI32{c.cnt}, StoreI64{c.ptr}, &w.rc->RB, 0, rb_max, nullptr, c.ptr);
   if (m_bound <= 0) return;
   const size_t sm = w.B <= kMaxSmemQueries / 2 ? 2 * sizeof(int32_t) * w.B : 0;
-  k_rq_fill<<<grid_for(m_bound, kEdgeTile, kNumSMs * 4), 256, sm, s>>>(edges, m_bound, m_dev, e.g.N, w.B, w.cbits,
-                                                                         w.cwpre, w.rc, c.ptr, c.fill, c.src);
+  k_rq_fill<<<grid_for(m_bound, kEdgeTile, kNumSMs * 4), 256, sm, s>>>(edges, m_bound, m_dev, rp, e.g.N, w.B,
+                                                                         w.cbits, w.cwpre, w.rc, c.ptr, c.fill, c.src);
   k_segsort_warp<<<grid_for(rb_max, 8), 256, 0, s>>>(c.ptr, w.rc, c.ctr, c.src, c.big_list);
   g_launches += 2;
   // long segments: chunk sort + merge levels (ping-pong src <-> sort_tmp)
@@ -641,7 +650,7 @@ void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound
 
 void stage_request_csr(Engine& e, RequestWs& w) {
   RqCsr c = w.rq_view();
-  build_rq_csr(e, w, w.edges, w.m, nullptr, c, /*counts_ready=*/true);
+  build_rq_csr(e, w, nullptr, w.m, nullptr, c, /*counts_ready=*/true);
 }
 
 }  // namespace ob

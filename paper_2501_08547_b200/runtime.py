@@ -258,6 +258,10 @@ class ServingEngine:
     def launch_count(self) -> int:
         return int(self._lib.ob_launch_count(self._h))
 
+    def set_graphs(self, enable: bool) -> None:
+        """Replay captured per-shape CUDA graphs (default) or launch every stage eagerly."""
+        nat.check(self._lib.ob_set_graphs(self._h, int(bool(enable))))
+
     def close(self) -> None:
         h = getattr(self, "_h", None)
         if h is not None and h.value:

@@ -214,3 +214,43 @@ def test_config1_against_reference():
     emb2, _ = eng.serve(req)
     assert np.array_equal(emb, emb2)
     eng.close()
+
+
+@pytest.mark.parametrize("strategy", ["srpe", "full"])
+def test_graph_replay_matches_eager(strategy):
+    """Requests of different sizes (several sharing one edge-count bucket) served
+    through captured graph replays equal the eager launches bit for bit, and
+    the oracle within the fp32 bar; a replay never sees the previous request."""
+    from oracle import layers as OL
+    from paper_2501_08547_b200 import graphstore, models, runtime, workload
+    from paper_2501_08547_b200.compgraph import ServingRequest
+
+    full = workload.gen_powerlaw_graph(6000, 6.0, 2.1, 8, seed=3)
+    serving, pool = workload.split_holdout(full, 0.25, seed=3)
+    N = serving.num_nodes
+    model = models.make_model("sage_mean", 2, 8, 8)
+    w = models.init_weights(model, 5)
+    layers = [dict(kind="sage_mean", in_dim=8, out_dim=8)] * 2
+    pe = graphstore.PeStore(OL.precompute(layers, w.layers, serving.in_offsets, serving.in_neighbors,
+                                          serving.features))
+    cfg = runtime.ServeConfig(strategy=strategy, gamma=0.3)
+    graph = runtime.ServingEngine(serving, pe, model, w, cfg)
+    eager = runtime.ServingEngine(serving, pe, model, w, cfg)
+    eager.set_graphs(False)
+    rng = np.random.default_rng(9)
+    live = np.flatnonzero(np.diff(serving.in_offsets) > 0)
+    for B, per in [(4, 200), (4, 230), (4, 150), (7, 90), (4, 210), (4, 0)]:
+        e = [np.stack([live[rng.integers(0, len(live), per)], N + rng.integers(0, B, per)], 1)]
+        e.append(np.stack([N + rng.integers(0, B, per // 3), rng.integers(0, N, per // 3)], 1))
+        e = np.concatenate(e).astype(np.int64)
+        req = ServingRequest(N, B, rng.standard_normal((B, 8)).astype(np.float32), e)
+        a, bda = graph.serve(req)
+        b, bdb = eager.serve(req)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (B, per)
+        assert bda.fetch_bytes == bdb.fetch_bytes
+        ref = OL.serve(strategy, layers, w.layers, N, B, serving.in_offsets, serving.in_neighbors,
+                       serving.features, req.query_features, req.edges, pe_layers=pe.layers, gamma=0.3)
+        assert rel(a, ref["emb"]) <= TOL
+        assert bda.fetch_bytes == ref["fetch_bytes"]
+    graph.close()
+    eager.close()
