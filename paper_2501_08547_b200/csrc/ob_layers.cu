@@ -107,6 +107,7 @@ __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restri
 // edge-chunk aggregation: one warp per (work item, 512-column slice)
 // ---------------------------------------------------------------------------
 constexpr int kAggWarps = 4;
+constexpr int kSmHdr = 4;    // softmax partial rows: [max logit, sum exp, pad, pad | values]
 constexpr int kAggNV = 4;    // float4 vectors per lane per slice
 constexpr int kAggSlice = 32 * 4 * kAggNV;
 
@@ -134,7 +135,7 @@ struct AggArgs {
   const float* s_src;    // softmax
   const float* s_dst;
   float* partial;        // [items][pw]
-  int pw;                // partial row width (softmax: width + 2)
+  int pw;                // partial row stride: ld4(width), softmax kSmHdr + ld4(width)
 };
 
 template <int OP, int NV>
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
         out[0] = (e1 > e0) ? m_run : -INFINITY;
         out[1] = den;
       }
-      out += 2;
+      out += kSmHdr;
     }
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
@@ -254,7 +255,7 @@ struct FinArgs {
   const float* partial;
   const int64_t* group_ptr;  // hub destinations: second-level partials in partial2
   const float* partial2;
-  int pw;
+  int pw;     // partial row stride: ld4(width) (+ kSmHdr for softmax)
   int width;
   int kind;   // ob_kind
   float p;
@@ -265,70 +266,108 @@ struct FinArgs {
   bool gcn_norm;  // divide by sqrt(count + 1) (gcn)
 };
 
+__device__ __forceinline__ float4 ld4f(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// softmax partial header over items [i0, i1): running max logit and the
+// rescaled sum of exps, lanes over items, fixed butterfly order
+__device__ __forceinline__ void sm_header(const float* part, int64_t pw, int64_t i0, int64_t i1, float& ms,
+                                          float& den) {
+  const int lane = threadIdx.x & 31;
+  float m = -INFINITY;
+  for (int64_t it = i0 + lane; it < i1; it += 32) {
+    const float2 h = __ldg(reinterpret_cast<const float2*>(part + it * pw));
+    if (h.y > 0.f) m = fmaxf(m, h.x);
+  }
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float d = 0.f;
+  for (int64_t it = i0 + lane; it < i1; it += 32) {
+    const float2 h = __ldg(reinterpret_cast<const float2*>(part + it * pw));
+    if (h.y > 0.f) d += h.y * __expf(h.x - m);
+  }
+  for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  ms = m;
+  den = d;
+}
+
+enum MergeKind { kMergeSum = 0, kMergeMax = 1, kMergeSoftmax = 2 };
+
+__device__ __forceinline__ float4 f4_op(int mk, float4 a, float4 v, float sc) {
+  if (mk == kMergeMax) return make_float4(fmaxf(a.x, v.x), fmaxf(a.y, v.y), fmaxf(a.z, v.z), fmaxf(a.w, v.w));
+  if (mk == kMergeSoftmax) return make_float4(fmaf(sc, v.x, a.x), fmaf(sc, v.y, a.y), fmaf(sc, v.z, a.z), fmaf(sc, v.w, a.w));
+  return make_float4(a.x + v.x, a.y + v.y, a.z + v.z, a.w + v.w);
+}
+
+// four columns [c4, c4+4) of items [i0, i1) merged with a fixed association:
+// four interleaved accumulators, 4 rows in flight per lane
+__device__ __forceinline__ float4 merge_cols(int mk, const float* part, int64_t pw, int64_t i0, int64_t i1, int hdr,
+                                             int c4, float ms) {
+  const float z = mk == kMergeMax ? -INFINITY : 0.f;
+  float4 acc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = make_float4(z, z, z, z);
+  int64_t it = i0;
+  for (; it + 3 < i1; it += 4) {
+    float4 v[4];
+    float sc[4] = {1.f, 1.f, 1.f, 1.f};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = ld4f(part + (it + j) * pw + hdr + c4);
+    if (mk == kMergeSoftmax) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 h = __ldg(reinterpret_cast<const float2*>(part + (it + j) * pw));
+        sc[j] = h.y > 0.f ? __expf(h.x - ms) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = f4_op(mk, acc[j], v[j], sc[j]);
+  }
+  for (; it < i1; ++it) {
+    float sc = 1.f;
+    if (mk == kMergeSoftmax) {
+      const float2 h = __ldg(reinterpret_cast<const float2*>(part + it * pw));
+      sc = h.y > 0.f ? __expf(h.x - ms) : 0.f;
+    }
+    acc[0] = f4_op(mk, acc[0], ld4f(part + it * pw + hdr + c4), sc);
+  }
+  const int cm = mk == kMergeMax ? kMergeMax : kMergeSum;
+  return f4_op(cm, f4_op(cm, acc[0], acc[1], 1.f), f4_op(cm, acc[2], acc[3], 1.f), 1.f);
+}
+
+__device__ __forceinline__ int merge_kind(int kind) {
+  return kind == OB_KIND_GAT ? kMergeSoftmax : (kind == OB_KIND_SAGE_MAX ? kMergeMax : kMergeSum);
+}
+
 // Hub destinations (more than kItemGroup items): merge each group of
 // kItemGroup consecutive items into one second-level partial of the same form
-// (sum / max / softmax triple), one warp per group, fixed association.
+// (sum / max / softmax header + values), one warp per group, fixed association.
 __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a, float* partial2) {
   const int64_t D = a.cnt->D, G = a.cnt->groups;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int mk = merge_kind(a.kind);
+  const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
   for (int64_t g = gw; g < G; g += nw) {
     int64_t lo = 0, hi = D;  // dst with group_ptr[i] <= g < group_ptr[i+1]
     while (hi - lo > 1) {
       int64_t mid = (lo + hi) >> 1;
-      if (a.group_ptr[mid] <= g) lo = mid;
+      if (__ldg(a.group_ptr + mid) <= g) lo = mid;
       else hi = mid;
     }
     const int64_t i = lo;
     const int64_t it0 = a.item_ptr[i] + (g - a.group_ptr[i]) * kItemGroup;
     const int64_t it1 = min(it0 + kItemGroup, a.item_ptr[i + 1]);
     float* out = partial2 + g * (int64_t)a.pw;
-    if (a.kind == OB_KIND_GAT) {
-      float ms = -INFINITY;
-      for (int64_t it = it0; it < it1; ++it) {
-        const float* pp = a.partial + it * (int64_t)a.pw;
-        if (pp[1] > 0.f) ms = fmaxf(ms, pp[0]);
-      }
-      float den = 0.f;
-      for (int64_t it = it0; it < it1; ++it) {
-        const float* pp = a.partial + it * (int64_t)a.pw;
-        if (pp[1] > 0.f) den += pp[1] * __expf(pp[0] - ms);
-      }
+    float ms = 0.f, den = 0.f;
+    if (mk == kMergeSoftmax) {
+      sm_header(a.partial, a.pw, it0, it1, ms, den);
       if (lane == 0) {
         out[0] = ms;
         out[1] = den;
       }
-      for (int col = lane; col < a.width; col += 32) {
-        float num = 0.f;
-        for (int64_t it = it0; it < it1; ++it) {
-          const float* pp = a.partial + it * (int64_t)a.pw;
-          if (pp[1] > 0.f) num += pp[2 + col] * __expf(pp[0] - ms);
-        }
-        out[2 + col] = num;
-      }
-    } else {
-      for (int col = lane; col < a.width; col += 32) {
-        float r0, r1, r2, r3;
-        const bool mx = a.kind == OB_KIND_SAGE_MAX;
-        r0 = r1 = r2 = r3 = mx ? -INFINITY : 0.f;
-        int64_t it = it0;
-        for (; it + 3 < it1; it += 4) {
-          const float v0 = a.partial[it * (int64_t)a.pw + col], v1 = a.partial[(it + 1) * (int64_t)a.pw + col];
-          const float v2 = a.partial[(it + 2) * (int64_t)a.pw + col], v3 = a.partial[(it + 3) * (int64_t)a.pw + col];
-          if (mx) {
-            r0 = fmaxf(r0, v0), r1 = fmaxf(r1, v1), r2 = fmaxf(r2, v2), r3 = fmaxf(r3, v3);
-          } else {
-            r0 += v0, r1 += v1, r2 += v2, r3 += v3;
-          }
-        }
-        for (; it < it1; ++it) {
-          const float v = a.partial[it * (int64_t)a.pw + col];
-          r0 = mx ? fmaxf(r0, v) : r0 + v;
-        }
-        out[col] = mx ? fmaxf(fmaxf(r0, r1), fmaxf(r2, r3)) : (r0 + r1) + (r2 + r3);
-      }
     }
+    for (int c4 = lane * 4; c4 < a.width; c4 += 128)
+      *reinterpret_cast<float4*>(out + hdr + c4) = merge_cols(mk, a.partial, a.pw, it0, it1, hdr, c4, ms);
   }
 }
 
@@ -337,6 +376,8 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int mk = merge_kind(a.kind);
+  const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
   for (int64_t i = gw; i < D; i += nw) {
     int64_t i0 = a.item_ptr[i], i1 = a.item_ptr[i + 1];
     const int64_t cnt = a.dst_ptr[i + 1] - a.dst_ptr[i];
@@ -346,58 +387,24 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
       i1 = a.group_ptr[i + 1];
       part = a.partial2;
     }
-    float ms = -INFINITY;
-    if (a.kind == OB_KIND_GAT) {
-      for (int64_t it = i0; it < i1; ++it) {
-        const float* pp = part + it * (int64_t)a.pw;
-        if (pp[1] > 0.f) ms = fmaxf(ms, pp[0]);
+    float ms = 0.f, den = 0.f;
+    // (max, sum exp, sum exp*z) merge in item order (cgpexec.py:225-239)
+    if (mk == kMergeSoftmax) sm_header(part, a.pw, i0, i1, ms, den);
+    for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
+      const float4 v = merge_cols(mk, part, a.pw, i0, i1, hdr, c4, ms);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (c4 + t >= a.width) break;
+        float r;
+        if (mk == kMergeSoftmax) r = den > 0.f ? vv[t] / den : 0.f;
+        else if (mk == kMergeMax) r = cnt > 0 ? vv[t] : 0.f;
+        else if (a.gcn_norm) r = vv[t] / sqrtf((float)cnt + 1.f);  // agg / sqrt(|N(v)|+1) (models.py:217-218)
+        else if (a.kind == OB_KIND_POWER_MEAN) r = cnt > 0 ? powf(vv[t] / (float)cnt, 1.f / a.p) : 0.f;
+        else r = cnt > 0 ? vv[t] / (float)cnt : 0.f;  // mean
+        if (a.relu) r = fmaxf(r, 0.f);
+        a.out[i * a.ldo + c4 + t] = r;
       }
-    }
-    for (int col = lane; col < a.width; col += 32) {
-      float r;
-      if (a.kind == OB_KIND_GAT) {
-        // (max, sum exp, sum exp*z) merge in item order (cgpexec.py:225-239)
-        float den = 0.f, num = 0.f;
-        for (int64_t it = i0; it < i1; ++it) {
-          const float* pp = part + it * (int64_t)a.pw;
-          if (pp[1] > 0.f) {
-            float sc = __expf(pp[0] - ms);
-            den += pp[1] * sc;
-            num += pp[2 + col] * sc;
-          }
-        }
-        r = den > 0.f ? num / den : 0.f;
-      } else if (a.kind == OB_KIND_SAGE_MAX) {
-        float m0 = -INFINITY, m1 = -INFINITY;
-        int64_t it = i0;
-        for (; it + 1 < i1; it += 2) {
-          m0 = fmaxf(m0, part[it * (int64_t)a.pw + col]);
-          m1 = fmaxf(m1, part[(it + 1) * (int64_t)a.pw + col]);
-        }
-        if (it < i1) m0 = fmaxf(m0, part[it * (int64_t)a.pw + col]);
-        r = cnt > 0 ? fmaxf(m0, m1) : 0.f;
-      } else {
-        // four independent partial sums (fixed association -> deterministic)
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        int64_t it = i0;
-        for (; it + 3 < i1; it += 4) {
-          s0 += part[it * (int64_t)a.pw + col];
-          s1 += part[(it + 1) * (int64_t)a.pw + col];
-          s2 += part[(it + 2) * (int64_t)a.pw + col];
-          s3 += part[(it + 3) * (int64_t)a.pw + col];
-        }
-        for (; it < i1; ++it) s0 += part[it * (int64_t)a.pw + col];
-        const float s = (s0 + s1) + (s2 + s3);
-        if (a.gcn_norm) {
-          r = s / sqrtf((float)cnt + 1.f);  // agg / sqrt(|N(v)|+1) (models.py:217-218)
-        } else if (a.kind == OB_KIND_POWER_MEAN) {
-          r = cnt > 0 ? powf(s / (float)cnt, 1.f / a.p) : 0.f;
-        } else {
-          r = cnt > 0 ? s / (float)cnt : 0.f;  // mean
-        }
-      }
-      if (a.relu) r = fmaxf(r, 0.f);
-      a.out[i * a.ldo + col] = r;
     }
   }
 }
@@ -505,7 +512,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   a.edge_src = r.edge_src;
   a.x = r.x;
   a.width = in;
-  a.pw = in;
+  a.pw = sp.kind == OB_KIND_MOMENTS ? in : ld4(in);  // moments: float64 rows, unpadded
   a.partial = sc.partial;
   a.p = sp.p;
   a.n = sp.n;
@@ -516,7 +523,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   f.partial = sc.partial;
   f.partial2 = sc.partial2;
   f.group_ptr = r.group_ptr;
-  f.pw = in;
+  f.pw = a.pw;
   f.width = in;
   f.kind = sp.kind;
   f.p = sp.p;
@@ -532,20 +539,20 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     gemm(s, g, r.S_max, r.cnt);
     a.x = RowSrc{nullptr, sc.z, ld_out};
     a.width = outd;
-    a.pw = outd;
+    a.pw = ld4(outd);
     f.width = outd;
-    f.pw = outd;
+    f.pw = ld4(outd);
     f.ldo = ld_out;
   }
   if (sp.kind == OB_KIND_GAT) {
     k_rowdot<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, sc.z, ld_out, nullptr, outd, L.a_src, sc.s_src);
     k_rowdot<<<grid_for(r.D_max, 8), 256, 0, s>>>(r.D_dev, sc.z, ld_out, r.self, outd, L.a_dst, sc.s_dst);
     g_launches += 2;
-    a.pw = outd + 2;
+    a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
     a.s_dst = sc.s_dst;
     launch_agg<kOpSoftmax>(s, a, r.items_max);
-    f.pw = outd + 2;
+    f.pw = a.pw;
     f.out = out;
     f.ldo = ldo;
     f.relu = true;
@@ -640,45 +647,23 @@ __global__ void __launch_bounds__(256) k_local_raw(FinArgs a, float* lp, int64_t
     }
     float* o = lp + i * ldp;
     if (lane == 0) lcnt[i] = (float)(a.dst_ptr[i + 1] - a.dst_ptr[i]);
-    if (a.kind == OB_KIND_GAT) {
-      float ms = -INFINITY;
-      for (int64_t it = i0; it < i1; ++it) {
-        const float* pp = part + it * (int64_t)a.pw;
-        if (pp[1] > 0.f) ms = fmaxf(ms, pp[0]);
-      }
-      float den = 0.f;
-      for (int64_t it = i0; it < i1; ++it) {
-        const float* pp = part + it * (int64_t)a.pw;
-        if (pp[1] > 0.f) den += pp[1] * __expf(pp[0] - ms);
-      }
+    const int mk = merge_kind(a.kind);
+    const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
+    const int oh = mk == kMergeSoftmax ? 2 : 0;  // rank-partial layout: [max, sum exp | values]
+    float ms = 0.f, den = 0.f;
+    if (mk == kMergeSoftmax) {
+      sm_header(part, a.pw, i0, i1, ms, den);
       if (lane == 0) {
         o[0] = ms;
         o[1] = den;
       }
-      for (int col = lane; col < a.width; col += 32) {
-        float num = 0.f;
-        for (int64_t it = i0; it < i1; ++it) {
-          const float* pp = part + it * (int64_t)a.pw;
-          if (pp[1] > 0.f) num += pp[2 + col] * __expf(pp[0] - ms);
-        }
-        o[2 + col] = num;
-      }
-      continue;
     }
-    const bool mx = a.kind == OB_KIND_SAGE_MAX;
-    for (int col = lane; col < a.width; col += 32) {
-      float r0 = mx ? -INFINITY : 0.f, r1 = r0;
-      int64_t it = i0;
-      for (; it + 1 < i1; it += 2) {
-        const float v0 = part[it * (int64_t)a.pw + col], v1 = part[(it + 1) * (int64_t)a.pw + col];
-        if (mx) r0 = fmaxf(r0, v0), r1 = fmaxf(r1, v1);
-        else r0 += v0, r1 += v1;
-      }
-      if (it < i1) {
-        const float v = part[it * (int64_t)a.pw + col];
-        r0 = mx ? fmaxf(r0, v) : r0 + v;
-      }
-      o[col] = mx ? fmaxf(r0, r1) : r0 + r1;
+    for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
+      const float4 v = merge_cols(mk, part, a.pw, i0, i1, hdr, c4, ms);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (c4 + t < a.width) o[oh + c4 + t] = vv[t];
     }
   }
 }
@@ -808,7 +793,7 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   a.edge_src = r.edge_src;
   a.x = r.x;
   a.width = in;
-  a.pw = in;
+  a.pw = sp.kind == OB_KIND_MOMENTS ? in : ld4(in);
   a.partial = sc.partial;
   a.p = sp.p;
   a.n = sp.n;
@@ -819,7 +804,7 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
     gemm(s, g, r.S_max, r.cnt);
     a.x = RowSrc{nullptr, sc.z, ld_out};
     a.width = outd;
-    a.pw = outd;
+    a.pw = ld4(outd);
   }
   if (sp.kind == OB_KIND_MOMENTS) {
     a.mean = mean;
@@ -834,7 +819,7 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   if (sp.kind == OB_KIND_GAT) {
     k_rowdot<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, sc.z, ld_out, nullptr, outd, L.a_src, sc.s_src);
     OB_LAUNCHED();
-    a.pw = outd + 2;
+    a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
     a.s_dst = s_dst;
     launch_agg<kOpSoftmax>(s, a, r.items_max);
@@ -1028,7 +1013,7 @@ void stage_precompute(Engine& e) {
   int maxw = 0;
   bool mom = false, wide = false;
   for (auto& L : e.layers) {
-    maxw = std::max(maxw, ld4(std::max(L.spec.in_dim, L.spec.out_dim)) + 2);
+    maxw = std::max(maxw, ld4(std::max(L.spec.in_dim, L.spec.out_dim)) + kSmHdr);
     mom |= L.spec.kind == OB_KIND_MOMENTS;
     wide |= L.spec.kind == OB_KIND_GAT || L.transform_first;
   }
