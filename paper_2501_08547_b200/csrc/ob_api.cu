@@ -27,6 +27,7 @@ Engine::~Engine() {
   drop_graphs();
   cgp_destroy(*this);
   if (arena.base) cudaFree(arena.base);
+  if (scan.pool) cudaFree(scan.pool);
   for (void* p : owned) cudaFree(p);
   for (auto& ev_ : ev)
     if (ev_) cudaEventDestroy(ev_);
@@ -167,9 +168,6 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     const BlockDev& b = w.blocks[w.block_of_layer[l - 1]];
     w.outs[l] = a.take<float>(b.D_max * ld4(e.layers[l - 1].spec.out_dim));
   }
-  int64_t tiles = p.max_scan_n / kScanTile + 2;
-  e.scan.tile_sums = a.take<int64_t>(tiles + 1);
-  e.scan.max_tiles = tiles;
 }
 
 struct PinnedReadback {
@@ -199,6 +197,22 @@ static void prepare_workspace(Engine& e, int B, int64_t m) {
     OB_CUDA(cudaMalloc(&q, cap));
     e.arena.base = (char*)q;
     e.arena.cap = cap;
+  }
+  // scan state pool: its own allocation at a fixed address, zeroed once here
+  // and by every request after use (graphs bake in its slices)
+  const int nscans = 24 + 8 * std::max(1, e.cfg.num_partitions);
+  const size_t pool = ScanScratch::bytes_for(p.max_scan_n, nscans);
+  if (pool > e.scan.cap) {
+    OB_CUDA(cudaStreamSynchronize(e.stream));
+    e.drop_graphs();
+    if (e.scan.pool) OB_CUDA(cudaFree(e.scan.pool));
+    e.scan.pool = nullptr;
+    e.scan.cap = 0;
+    void* q = nullptr;
+    OB_CUDA(cudaMalloc(&q, pool));
+    OB_CUDA(cudaMemset(q, 0, pool));
+    e.scan.pool = (char*)q;
+    e.scan.cap = pool;
   }
   e.arena.used = 0;
   carve(e, w, p, e.arena);
@@ -254,7 +268,23 @@ __global__ void k_set_params(ReqParams* p, const int64_t* edges, const float* q,
 }
 
 // every stage of one request, enqueued on e.stream (eagerly or under capture)
+static void enqueue_stages(Engine& e, float* d_out);
+
 static void enqueue_request(Engine& e, float* d_out) {
+  e.scan.cursor = 0;
+  try {
+    enqueue_stages(e, d_out);
+  } catch (...) {
+    // the pool must be all zero for the next request whatever was enqueued
+    cudaStreamSynchronize(e.stream);
+    cudaMemset(e.scan.pool, 0, e.scan.cap);
+    e.scan.cursor = 0;
+    throw;
+  }
+  e.scan.clear(e.stream);  // zero the scan state this request used
+}
+
+static void enqueue_stages(Engine& e, float* d_out) {
   cudaStream_t s = e.stream;
   RequestWs& w = e.ws;
   const bool srpe = e.cfg.strategy != OB_STRATEGY_FULL;

@@ -138,13 +138,6 @@ __global__ void k_query_dst(int64_t N, int B, int32_t* dst_ids, BlockCounters* c
 
 __global__ void k_copy_count_D(BlockCounters* dst, const BlockCounters* src) { dst->D = src->S; }
 
-void block_items(Engine& e, BlockDev& b, int64_t chunk) {
-  device_scan(e.stream, e.scan, ItemLoad{b.dst_ptr, chunk}, StoreI64{b.item_ptr}, &b.cnt->D, 0, b.D_max,
-              &b.cnt->items, b.item_ptr);
-  device_scan(e.stream, e.scan, GroupLoad{b.item_ptr}, StoreI64{b.group_ptr}, &b.cnt->D, 0, b.D_max,
-              &b.cnt->groups, b.group_ptr);
-}
-
 // generic block assembly over an already written dst list + counts->D.
 // `src` names the CSR the destinations pull from (the whole graph, or a CGP
 // rank's source-split CSR) and the request CSR (whole request or the rank's slice).
@@ -158,8 +151,10 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
   k_block_spans<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, e.g.N, src.offsets, src.deg, w.cbits,
                                                         w.cwpre, src.rq_ptr, w.rc, sp, w.seg_len);
   OB_LAUNCHED();
-  device_scan(s, e.scan, LoadI64{w.seg_len}, StoreI64{b.dst_ptr}, &b.cnt->D, 0, b.D_max, &b.cnt->E, b.dst_ptr);
-  block_items(e, b, kAggChunk);  // work items double as the fill's edge chunks
+  // dst_ptr / item_ptr / group_ptr (+ E, items, groups) in one pass; the work
+  // items double as the fill's edge chunks
+  const BlockStore3 st{b.dst_ptr, b.item_ptr, b.group_ptr};
+  device_scan_t<I3>(s, e.scan, SegLenLoad3{w.seg_len}, st, BlockTotal3{st, b.cnt}, &b.cnt->D, 0, b.D_max);
   OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
   k_block_fill<<<grid_for(b.items_max, 8, kNumSMs * 16), 256, 0, s>>>(b.cnt, b.dst_ptr, b.item_ptr, sp, src.nbrs,
                                                                        src.rq_src, w.src_global, w.sbits);

@@ -89,8 +89,9 @@ void cgp_build_partitions(Engine& e) {
   k_owner<<<grid_for(N, 256), 256, 0, s>>>(N, c.P, e.cfg.seed, c.owner);
   OB_LAUNCHED();
   ScanScratch sc;
-  sc.max_tiles = N / kScanTile + 2;
-  sc.tile_sums = (int64_t*)e.dalloc(sizeof(int64_t) * (sc.max_tiles + 1));
+  sc.cap = ScanScratch::bytes_for(N, c.P);
+  sc.pool = (char*)e.dalloc(sc.cap);
+  OB_CUDA(cudaMemsetAsync(sc.pool, 0, sc.cap, s));
   int64_t* total = (int64_t*)e.dalloc(sizeof(int64_t));
   c.parts.clear();
   for (int r = 0; r < c.P; ++r) {

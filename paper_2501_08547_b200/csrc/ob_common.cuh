@@ -59,8 +59,11 @@ __device__ __forceinline__ int64_t dev_count(const int64_t* p, int64_t fallback)
 // ---------------------------------------------------------------------------
 // bitmap-rank set over [0, n_bits)
 // ---------------------------------------------------------------------------
+// test before set: re-marking an already set bit (the common case when a
+// source feeds many destinations) costs an L2 read instead of an L2 atomic
 __device__ __forceinline__ void bm_set(uint32_t* bits, int64_t v) {
-  atomicOr(bits + (v >> 5), 1u << (v & 31));
+  const uint32_t m = 1u << (v & 31);
+  if (!(__ldcg(bits + (v >> 5)) & m)) atomicOr(bits + (v >> 5), m);
 }
 __device__ __forceinline__ bool bm_test(const uint32_t* bits, int64_t v) {
   return (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
@@ -71,7 +74,7 @@ __device__ __forceinline__ void bm_set_warp(uint32_t* bits, int64_t v) {
   const uint32_t word = (uint32_t)(v >> 5);
   const unsigned peers = __match_any_sync(act, word);
   const uint32_t orv = __reduce_or_sync(peers, 1u << (v & 31));
-  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(bits + word, orv);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1 && (__ldcg(bits + word) & orv) != orv) atomicOr(bits + word, orv);
 }
 // rank of v among set bits (v need not be set: counts set bits below v)
 __device__ __forceinline__ int64_t bm_rank(const uint32_t* bits, const int64_t* wpre, int64_t v) {
@@ -80,78 +83,180 @@ __device__ __forceinline__ int64_t bm_rank(const uint32_t* bits, const int64_t* 
 }
 
 // ---------------------------------------------------------------------------
-// 3-phase exclusive scan with a device-resident item count
-//   out[i] = sum_{j<i} load(j) for i in [0, n]; *total = out[n]
+// Single-pass exclusive scan (decoupled look-back) with a device-resident count
+//   out[i] = sum_{j<i} load(j) for i in [0, n]; total(n, out[n])
+// Tiles are claimed in order from an atomic ticket, so every predecessor of a
+// tile is already resident and the look-back cannot deadlock.  Each tile
+// publishes its aggregate, then its inclusive prefix; warp 0 of a tile walks
+// back 32 predecessors at a time until it meets an inclusive prefix.
+// The per-scan state (ticket, flags, aggregates, prefixes) is a slice of a
+// zeroed pool; the request zeroes what it used when it finishes.
 // ---------------------------------------------------------------------------
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-template <class Load>
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Load load, const int64_t* n_dev, int64_t n_host,
-                                                              int64_t* tile_sums) {
-  using BR = cub::BlockReduce<int64_t, kScanThreads>;
-  __shared__ typename BR::TempStorage tmp;
-  const int64_t n = dev_count(n_dev, n_host);
-  const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    int64_t base = t * kScanTile;
-    int64_t s = 0;
-#pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-      int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
-      if (idx < n) s += load(idx);
-    }
-    int64_t r = BR(tmp).Sum(s);
-    if (threadIdx.x == 0) tile_sums[t] = r;
-    __syncthreads();
-  }
+// three running sums scanned together (block assembly: edges, items, groups)
+struct I3 {
+  int64_t a, b, c;
+  I3() = default;
+  __host__ __device__ constexpr I3(int64_t x) : a(x), b(x), c(x) {}
+  __host__ __device__ constexpr I3(int64_t x, int64_t y, int64_t z) : a(x), b(y), c(z) {}
+};
+__host__ __device__ inline I3 operator+(const I3& x, const I3& y) { return I3(x.a + y.a, x.b + y.b, x.c + y.c); }
+
+__device__ __forceinline__ int64_t shfl_xor_t(int64_t v, int o) {
+  return (int64_t)__shfl_xor_sync(0xffffffffu, (long long)v, o);
+}
+__device__ __forceinline__ I3 shfl_xor_t(const I3& v, int o) {
+  return I3(shfl_xor_t(v.a, o), shfl_xor_t(v.b, o), shfl_xor_t(v.c, o));
+}
+__device__ __forceinline__ int64_t ldcg_t(const int64_t* p) { return __ldcg(reinterpret_cast<const long long*>(p)); }
+__device__ __forceinline__ I3 ldcg_t(const I3* p) {
+  const long long* q = reinterpret_cast<const long long*>(p);
+  return I3(__ldcg(q), __ldcg(q + 1), __ldcg(q + 2));
 }
 
-__global__ void __launch_bounds__(1024) k_scan_tiles(const int64_t* n_dev, int64_t n_host, int64_t* tile_sums,
-                                                     int64_t* total_out, int64_t* out_arr);
+template <class T>
+struct ScanTiles {
+  unsigned long long* ticket;
+  int* flag;  // 0 empty, 1 aggregate published, 2 inclusive prefix published
+  T* agg;
+  T* incl;
+};
 
-template <class Load, class Store>
-__global__ void __launch_bounds__(kScanThreads) k_scan_downsweep(Load load, Store store, const int64_t* n_dev,
-                                                                 int64_t n_host, const int64_t* tile_sums) {
-  using BS = cub::BlockScan<int64_t, kScanThreads>;
+template <class T, class Load, class Store, class Total>
+__global__ void __launch_bounds__(kScanThreads) k_scan(Load load, Store store, Total total, const int64_t* n_dev,
+                                                       int64_t n_host, ScanTiles<T> st) {
+  using BS = cub::BlockScan<T, kScanThreads>;
   __shared__ typename BS::TempStorage tmp;
+  __shared__ int64_t s_tile;
+  __shared__ T s_prefix;
   const int64_t n = dev_count(n_dev, n_host);
   const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    int64_t base = t * kScanTile + (int64_t)threadIdx.x * kScanItems;  // blocked arrangement
-    int64_t v[kScanItems];
+  const int lane = threadIdx.x & 31;
+  if (n <= 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) total(0, T(0));
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(st.ticket, 1ull);
+    __syncthreads();
+    const int64_t t = s_tile;
+    if (t >= ntiles) break;
+    const int64_t base = t * kScanTile + (int64_t)threadIdx.x * kScanItems;  // blocked arrangement
+    T v[kScanItems];
 #pragma unroll
-    for (int i = 0; i < kScanItems; ++i) v[i] = (base + i < n) ? load(base + i) : 0;
-    int64_t agg;
+    for (int i = 0; i < kScanItems; ++i) v[i] = (base + i < n) ? T(load(base + i)) : T(0);
+    T agg;
     BS(tmp).ExclusiveSum(v, v, agg);
-    int64_t off = tile_sums[t];
+    if (threadIdx.x < 32) {
+      T excl(0);
+      volatile int* vf = st.flag;
+      if (t == 0) {
+        if (lane == 0) {
+          st.incl[0] = agg;
+          __threadfence();
+          vf[0] = 2;
+        }
+      } else {
+        if (lane == 0) {
+          st.agg[t] = agg;
+          __threadfence();
+          vf[t] = 1;
+        }
+        for (int64_t hi = t - 1;;) {
+          const int64_t j = hi - lane;
+          int f = j >= 0 ? vf[j] : 2;
+          const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
+          const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
+          const unsigned need = first == 32 ? 0xffffffffu : (first == 31 ? 0xffffffffu : ((2u << first) - 1u));
+          if (__ballot_sync(0xffffffffu, f == 0) & need) continue;  // a predecessor has not published yet
+          __threadfence();
+          T x(0);
+          if (j >= 0 && lane < first) x = ldcg_t(st.agg + j);
+          else if (j >= 0 && lane == first) x = ldcg_t(st.incl + j);
+#pragma unroll
+          for (int o = 16; o; o >>= 1) x = x + shfl_xor_t(x, o);
+          excl = excl + x;
+          if (first < 32) break;
+          hi -= 32;
+        }
+        if (lane == 0) {
+          st.incl[t] = excl + agg;
+          __threadfence();
+          vf[t] = 2;
+        }
+      }
+      if (lane == 0) s_prefix = excl;
+    }
+    __syncthreads();
+    const T off = s_prefix;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i)
       if (base + i < n) store(base + i, v[i] + off);
-    __syncthreads();
+    if (t == ntiles - 1 && threadIdx.x == 0) total(n, off + agg);
+    __syncthreads();  // s_tile / s_prefix / tmp are reused by the next tile
   }
 }
 
-// Host driver.  `max_n` bounds the device count (sizes tile_sums).  Writes
-// out[n] via the tile kernel (out_total) and optionally a second copy.
+// Pool of zeroed per-scan state.  `cursor` advances per scan on the host (so a
+// captured graph bakes in fixed slices); clear() zeroes the used part.
 struct ScanScratch {
-  int64_t* tile_sums = nullptr;  // >= max_tiles + 1
-  int64_t max_tiles = 0;
+  char* pool = nullptr;
+  size_t cap = 0;
+  size_t cursor = 0;
+  static size_t slice_bytes(int64_t max_n) {
+    const size_t tiles = (size_t)(max_n / kScanTile + 2);
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    return 256 + al(tiles * sizeof(int)) + 2 * al(tiles * sizeof(I3));
+  }
+  static size_t bytes_for(int64_t max_n, int scans) { return slice_bytes(max_n) * (size_t)scans; }
+  template <class T>
+  ScanTiles<T> take(int64_t max_n) {
+    const size_t tiles = (size_t)(max_n / kScanTile + 2);
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t need = 256 + al(tiles * sizeof(int)) + 2 * al(tiles * sizeof(T));
+    if (cursor + need > cap) throw Error(OB_ESTATE, "scan pool too small");
+    char* p = pool + cursor;
+    cursor += need;
+    ScanTiles<T> st;
+    st.ticket = reinterpret_cast<unsigned long long*>(p);
+    st.flag = reinterpret_cast<int*>(p + 256);
+    st.agg = reinterpret_cast<T*>(p + 256 + al(tiles * sizeof(int)));
+    st.incl = reinterpret_cast<T*>(p + 256 + al(tiles * sizeof(int)) + al(tiles * sizeof(T)));
+    return st;
+  }
+  void clear(cudaStream_t s) {
+    if (cursor) OB_CUDA(cudaMemsetAsync(pool, 0, cursor, s));
+    cursor = 0;
+  }
 };
 
-// out_arr (optional): the plain array behind `store`; out_arr[n] = total is written.
-template <class Load, class Store>
-void device_scan(cudaStream_t s, const ScanScratch& sc, Load load, Store store, const int64_t* n_dev,
-                 int64_t n_host, int64_t max_n, int64_t* total_out, int64_t* out_arr = nullptr) {
+struct TotalI64 {
+  int64_t* total_out;
+  int64_t* out_arr;
+  __device__ void operator()(int64_t n, int64_t v) const {
+    if (total_out) *total_out = v;
+    if (out_arr) out_arr[n] = v;
+  }
+};
+
+template <class T, class Load, class Store, class Total>
+void device_scan_t(cudaStream_t s, ScanScratch& sc, Load load, Store store, Total total, const int64_t* n_dev,
+                   int64_t n_host, int64_t max_n) {
+  ScanTiles<T> st = sc.take<T>(max_n);
   int64_t tiles = (max_n + kScanTile - 1) / kScanTile;
-  if (tiles < 1) tiles = 1;
-  OB_CHECK(tiles <= sc.max_tiles, OB_ESTATE, "scan scratch too small");
-  int g = grid_for(tiles, 1, kNumSMs * 2);
-  k_scan_reduce<<<g, kScanThreads, 0, s>>>(load, n_dev, n_host, sc.tile_sums);
-  k_scan_tiles<<<1, 1024, 0, s>>>(n_dev, n_host, sc.tile_sums, total_out, out_arr);
-  k_scan_downsweep<<<g, kScanThreads, 0, s>>>(load, store, n_dev, n_host, sc.tile_sums);
-  g_launches += 3;
+  const int g = grid_for(tiles < 1 ? 1 : tiles, 1, kNumSMs * 2);
+  k_scan<T><<<g, kScanThreads, 0, s>>>(load, store, total, n_dev, n_host, st);
+  ++g_launches;
+}
+
+// int64 scan; out_arr (optional): the plain array behind `store`, out_arr[n] = total.
+template <class Load, class Store>
+void device_scan(cudaStream_t s, ScanScratch& sc, Load load, Store store, const int64_t* n_dev, int64_t n_host,
+                 int64_t max_n, int64_t* total_out, int64_t* out_arr = nullptr) {
+  device_scan_t<int64_t>(s, sc, load, store, TotalI64{total_out, out_arr}, n_dev, n_host, max_n);
 }
 
 // Common loaders / stores.

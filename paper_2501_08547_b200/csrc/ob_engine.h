@@ -172,6 +172,18 @@ struct ReqParams {
   int64_t pad;
 };
 
+// one (src, dst) request edge: a single 16-byte load when the array allows it
+__device__ __forceinline__ void ld_edge(const int64_t* __restrict__ edges, int64_t e, int64_t& s, int64_t& d) {
+  if ((reinterpret_cast<uintptr_t>(edges) & 15) == 0) {
+    const longlong2 v = __ldg(reinterpret_cast<const longlong2*>(edges) + e);
+    s = v.x;
+    d = v.y;
+  } else {
+    s = __ldg(edges + 2 * e);
+    d = __ldg(edges + 2 * e + 1);
+  }
+}
+
 // Per-request device workspace for the centralized pipeline.
 struct RequestWs {
   int B = 0;
@@ -343,20 +355,41 @@ constexpr int64_t kAggChunk = 128;  // edges per aggregation work item
 constexpr int64_t kItemGroup = 16;  // items merged per second-level partial (hub destinations)
 
 // aggregation work items: one per kAggChunk edges of a destination (at least one)
-struct ItemLoad {
-  const int64_t* dst_ptr;
-  int64_t chunk;
-  __device__ int64_t operator()(int64_t i) const {
-    int64_t len = dst_ptr[i + 1] - dst_ptr[i];
-    return len > chunk ? (len + chunk - 1) / chunk : 1;
+// Block offsets in one scan: (edges, aggregation work items, second-level
+// groups) per destination.  A destination gets ceil(len / kAggChunk) items
+// (at least one, so empty destinations still finalize), and destinations with
+// more than kItemGroup items get ceil(items / kItemGroup) groups.
+__device__ __forceinline__ I3 block_counts(int64_t len) {
+  const int64_t items = len > kAggChunk ? (len + kAggChunk - 1) / kAggChunk : 1;
+  const int64_t groups = items > kItemGroup ? (items + kItemGroup - 1) / kItemGroup : 0;
+  return I3(len, items, groups);
+}
+struct SegLenLoad3 {  // from per-destination lengths
+  const int64_t* seg_len;
+  __device__ I3 operator()(int64_t i) const { return block_counts(seg_len[i]); }
+};
+struct OffsetsLoad3 {  // from an existing CSR offsets array
+  const int64_t* off;
+  __device__ I3 operator()(int64_t i) const { return block_counts(off[i + 1] - off[i]); }
+};
+struct BlockStore3 {
+  int64_t* dst_ptr;  // null: offsets already exist
+  int64_t* item_ptr;
+  int64_t* group_ptr;
+  __device__ void operator()(int64_t i, const I3& v) const {
+    if (dst_ptr) dst_ptr[i] = v.a;
+    item_ptr[i] = v.b;
+    group_ptr[i] = v.c;
   }
 };
-// second-level groups: only destinations with more than kItemGroup items get them
-struct GroupLoad {
-  const int64_t* item_ptr;
-  __device__ int64_t operator()(int64_t i) const {
-    int64_t n = item_ptr[i + 1] - item_ptr[i];
-    return n > kItemGroup ? (n + kItemGroup - 1) / kItemGroup : 0;
+struct BlockTotal3 {
+  BlockStore3 st;
+  BlockCounters* cnt;
+  __device__ void operator()(int64_t n, const I3& v) const {
+    st(n, v);
+    cnt->E = v.a;
+    cnt->items = v.b;
+    cnt->groups = v.c;
   }
 };
 
@@ -386,7 +419,6 @@ void stage_build_srpe(Engine& e, RequestWs& w);
 void stage_build_full(Engine& e, RequestWs& w);
 void stage_forward(Engine& e, RequestWs& w, float* d_out);
 void stage_precompute(Engine& e);
-void block_items(Engine& e, BlockDev& b, int64_t chunk);
 
 // ---------------------------------------------------------------------------
 // computation-graph parallelism (CGP): hash partitions and per-partition work

@@ -1045,11 +1045,11 @@ void stage_precompute(Engine& e) {
     k_node_scale<<<grid_for(N, 256), 256, 0, s>>>(e.g.indeg, N, gscale);
     OB_LAUNCHED();
     ScanScratch sc_scan;
-    sc_scan.max_tiles = N / kScanTile + 2;
-    sc_scan.tile_sums = (int64_t*)talloc(sizeof(int64_t) * (sc_scan.max_tiles + 1));
-    device_scan(s, sc_scan, ItemLoad{e.g.offsets, kAggChunk}, StoreI64{item_ptr}, nullptr, N, N, &cnt->items,
-                item_ptr);
-    device_scan(s, sc_scan, GroupLoad{item_ptr}, StoreI64{group_ptr}, nullptr, N, N, &cnt->groups, group_ptr);
+    sc_scan.cap = ScanScratch::bytes_for(N, 1);
+    sc_scan.pool = (char*)talloc(sc_scan.cap);
+    OB_CUDA(cudaMemsetAsync(sc_scan.pool, 0, sc_scan.cap, s));
+    const BlockStore3 bst{nullptr, item_ptr, group_ptr};  // dst_ptr = the graph's offsets
+    device_scan_t<I3>(s, sc_scan, OffsetsLoad3{e.g.offsets}, bst, BlockTotal3{bst, cnt}, nullptr, N, N);
     e.pe.assign(k - 1, nullptr);
     e.pe_dim.assign(k - 1, 0);
     const float* h = e.g.feats;

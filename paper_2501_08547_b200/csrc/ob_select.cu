@@ -26,30 +26,6 @@ namespace ob {
 
 int64_t g_launches = 0;
 
-__global__ void __launch_bounds__(1024) k_scan_tiles(const int64_t* n_dev, int64_t n_host, int64_t* tile_sums,
-                                                     int64_t* total_out, int64_t* out_arr) {
-  using BS = cub::BlockScan<int64_t, 1024>;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ int64_t carry;
-  const int64_t n = dev_count(n_dev, n_host);
-  const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < ntiles; base += 1024) {
-    int64_t i = base + threadIdx.x;
-    int64_t v = i < ntiles ? tile_sums[i] : 0, agg;
-    BS(tmp).ExclusiveSum(v, v, agg);
-    if (i < ntiles) tile_sums[i] = v + carry;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += agg;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    if (total_out) *total_out = carry;
-    if (out_arr) out_arr[n] = carry;
-  }
-}
-
 __global__ void k_fill_i32(int32_t* a, const int64_t* n_dev, int64_t n_host, int32_t v) {
   const int64_t n = dev_count(n_dev, n_host);
   OB_GRID_STRIDE(i, n) a[i] = v;
@@ -92,7 +68,8 @@ __global__ void __launch_bounds__(256) k_request_mark(const ReqParams* rp, int64
     }
     const int64_t t1 = min(t0 + kEdgeTile, m);
     for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-      int64_t s = edges[2 * e], d = edges[2 * e + 1];
+      int64_t s, d;
+      ld_edge(edges, e, s, d);
       if (s < 0 || s >= hi || d < 0 || d >= hi) {
         err |= kErrRange;
         continue;
@@ -327,7 +304,8 @@ __global__ void __launch_bounds__(256) k_rq_fill(const int64_t* __restrict__ edg
       __syncthreads();
     }
     for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-      int64_t s = edges[2 * e], d = edges[2 * e + 1];
+      int64_t s, d;
+      ld_edge(edges, e, s, d);
       int64_t pos;
       if (d >= N) {
         int64_t q = d - N;

@@ -7,14 +7,16 @@ import csv
 import sys
 
 
-def main(path, marker="k_request_mark"):
+def main(path, marker="k_set_params"):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
     ks = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[hi + 1:] if len(r) > vi and r[vi]]
     starts = [i for i, (n, _) in enumerate(ks) if marker in n]
-    seg = ks[starts[-1]:] if starts else ks
+    # the last complete request: between the last two markers (else from the last one)
+    seg = ks[starts[-2]:starts[-1]] if len(starts) >= 2 else (ks[starts[-1]:] if starts else ks)
+    seg = [(n, v) for n, v in seg if "ob::" in n]
     agg = collections.OrderedDict()
     for n, v in seg:
         s = n.split("(")[0].replace("void ", "")[:70]
