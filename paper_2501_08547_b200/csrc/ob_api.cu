@@ -135,6 +135,8 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     b.cnt = a.take<BlockCounters>(1);
     b.dst_ptr = a.take<int64_t>(b.D_max + 1);
     b.item_ptr = a.take<int64_t>(b.D_max + 1);
+    b.item_dst = a.take<int32_t>(b.items_max);
+    b.group_dst = a.take<int32_t>(b.items_max / kItemGroup + b.D_max + 1);
     b.group_ptr = a.take<int64_t>(b.D_max + 1);
     b.edge_src = a.take<int32_t>(b.E_max);
     b.src_ids = a.take<int32_t>(b.S_max);

@@ -80,7 +80,8 @@ __device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ ptr, int64
 // of one destination), so a destination's CSR row and request span are copied
 // with contiguous, coalesced loads and hub destinations spread over many warps
 __global__ void __launch_bounds__(256) k_block_fill(const BlockCounters* cnt, const int64_t* __restrict__ dst_ptr,
-                                                    const int64_t* __restrict__ item_ptr, SegSpans sp,
+                                                    const int64_t* __restrict__ item_ptr,
+                                                    const int32_t* __restrict__ item_dst, SegSpans sp,
                                                     const int32_t* __restrict__ nbrs,
                                                     const int32_t* __restrict__ rq_src, int32_t* src_global,
                                                     uint32_t* sbits) {
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(256) k_block_fill(const BlockCounters* cnt, co
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = gw; it < items; it += nw) {
-    const int64_t i = seg_of(item_ptr, D, it);
+    const int64_t i = __ldg(item_dst + it);
     const int64_t d0 = __ldg(dst_ptr + i);
     const int64_t e0 = d0 + (it - __ldg(item_ptr + i)) * kAggChunk;
     const int64_t e1 = min(e0 + kAggChunk, __ldg(dst_ptr + i + 1));
@@ -153,10 +154,11 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
   OB_LAUNCHED();
   // dst_ptr / item_ptr / group_ptr (+ E, items, groups) in one pass; the work
   // items double as the fill's edge chunks
-  const BlockStore3 st{b.dst_ptr, b.item_ptr, b.group_ptr};
-  device_scan_t<I3>(s, e.scan, SegLenLoad3{w.seg_len}, st, BlockTotal3{st, b.cnt}, &b.cnt->D, 0, b.D_max);
+  const BlockStore3<SegLenLoad3> st{SegLenLoad3{w.seg_len}, b.dst_ptr, b.item_ptr, b.group_ptr, b.item_dst, b.group_dst};
+  device_scan_t<I3>(s, e.scan, SegLenLoad3{w.seg_len}, st, BlockTotal3<SegLenLoad3>{st, b.cnt}, &b.cnt->D, 0,
+                    b.D_max);
   OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
-  k_block_fill<<<grid_for(b.items_max, 8, kNumSMs * 16), 256, 0, s>>>(b.cnt, b.dst_ptr, b.item_ptr, sp, src.nbrs,
+  k_block_fill<<<grid_for(b.items_max, 8, kNumSMs * 16), 256, 0, s>>>(b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs,
                                                                        src.rq_src, w.src_global, w.sbits);
   OB_LAUNCHED();
   if (b.has_self) {

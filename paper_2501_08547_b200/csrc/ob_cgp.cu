@@ -230,6 +230,8 @@ void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
       b.cnt = a.take<BlockCounters>(1);
       b.dst_ptr = a.take<int64_t>(b.D_max + 1);
       b.item_ptr = a.take<int64_t>(b.D_max + 1);
+      b.item_dst = a.take<int32_t>(b.items_max);
+      b.group_dst = a.take<int32_t>(b.items_max / kItemGroup + b.D_max + 1);
       b.group_ptr = a.take<int64_t>(b.D_max + 1);
       b.edge_src = a.take<int32_t>(b.E_max);
       b.src_ids = a.take<int32_t>(b.S_max);
@@ -343,6 +345,8 @@ void serve_cgp(Engine& e, float* d_out) {
         r.items_max = b.items_max;
         r.dst_ptr = b.dst_ptr;
         r.item_ptr = b.item_ptr;
+        r.item_dst = b.item_dst;
+        r.group_dst = b.group_dst;
         r.edge_src = b.edge_src;
         r.self = nullptr;
         r.x = RowSrc{w.rowp, nullptr, 0};

@@ -62,6 +62,8 @@ struct BlockDev {
   int32_t* src_ids = nullptr;    // [S] ascending global ids
   int32_t* self_src = nullptr;   // [D] local index of dst's own row (centralized only)
   int64_t* item_ptr = nullptr;   // [D+1] aggregation work items per dst (edge chunks)
+  int32_t* item_dst = nullptr;   // [items] destination of each work item
+  int32_t* group_dst = nullptr;  // [groups] destination of each second-level group
   int64_t* group_ptr = nullptr;  // [D+1] groups of kItemGroup items (hub destinations only)
   bool has_self = true;
   // host mirror of counts after the request completes
@@ -313,6 +315,8 @@ struct LayerRun {
   int64_t D_max, S_max, items_max;
   const int64_t* dst_ptr;
   const int64_t* item_ptr;
+  const int32_t* item_dst;   // destination per work item
+  const int32_t* group_dst;  // destination per second-level group
   const int32_t* edge_src;
   const int32_t* self;       // null = identity
   RowSrc x;                  // bound inputs
@@ -372,21 +376,36 @@ struct OffsetsLoad3 {  // from an existing CSR offsets array
   const int64_t* off;
   __device__ I3 operator()(int64_t i) const { return block_counts(off[i + 1] - off[i]); }
 };
+// Stores the three offsets and expands the item -> destination and
+// group -> destination maps (the counts are recomputed from the source).
+template <class Src>
 struct BlockStore3 {
+  Src src;
   int64_t* dst_ptr;  // null: offsets already exist
   int64_t* item_ptr;
   int64_t* group_ptr;
+  int32_t* item_dst;
+  int32_t* group_dst;
   __device__ void operator()(int64_t i, const I3& v) const {
     if (dst_ptr) dst_ptr[i] = v.a;
     item_ptr[i] = v.b;
     group_ptr[i] = v.c;
+    const I3 c = src(i);
+    for (int64_t k = 0; k < c.b; ++k) item_dst[v.b + k] = (int32_t)i;
+    for (int64_t k = 0; k < c.c; ++k) group_dst[v.c + k] = (int32_t)i;
+  }
+  __device__ void end(int64_t n, const I3& v) const {
+    if (dst_ptr) dst_ptr[n] = v.a;
+    item_ptr[n] = v.b;
+    group_ptr[n] = v.c;
   }
 };
+template <class Src>
 struct BlockTotal3 {
-  BlockStore3 st;
+  BlockStore3<Src> st;
   BlockCounters* cnt;
   __device__ void operator()(int64_t n, const I3& v) const {
-    st(n, v);
+    st.end(n, v);
     cnt->E = v.a;
     cnt->items = v.b;
     cnt->groups = v.c;

@@ -111,20 +111,11 @@ constexpr int kSmHdr = 4;    // softmax partial rows: [max logit, sum exp, pad, 
 constexpr int kAggNV = 4;    // float4 vectors per lane per slice
 constexpr int kAggSlice = 32 * 4 * kAggNV;
 
-__device__ __forceinline__ int64_t item_dst(const int64_t* __restrict__ item_ptr, int64_t D, int64_t it) {
-  int64_t lo = 0, hi = D;
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (__ldg(item_ptr + mid) <= it) lo = mid;
-    else hi = mid;
-  }
-  return lo;
-}
-
 struct AggArgs {
   const BlockCounters* cnt;
   const int64_t* dst_ptr;
   const int64_t* item_ptr;
+  const int32_t* item_dst;
   const int32_t* edge_src;
   RowSrc x;              // input rows (16 B aligned, stride multiple of 4)
   int width;
@@ -149,7 +140,7 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = gw; it < items; it += nw) {
-    const int64_t i = item_dst(a.item_ptr, D, it);
+    const int64_t i = __ldg(a.item_dst + it);
     const int64_t j = it - a.item_ptr[i];
     const int64_t e0 = a.dst_ptr[i] + j * kAggChunk;
     const int64_t e1 = min(e0 + kAggChunk, a.dst_ptr[i + 1]);
@@ -252,6 +243,7 @@ struct FinArgs {
   const BlockCounters* cnt;
   const int64_t* dst_ptr;
   const int64_t* item_ptr;
+  const int32_t* group_dst;  // destination per second-level group
   const float* partial;
   const int64_t* group_ptr;  // hub destinations: second-level partials in partial2
   const float* partial2;
@@ -348,13 +340,7 @@ __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a, float* partial
   const int mk = merge_kind(a.kind);
   const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
   for (int64_t g = gw; g < G; g += nw) {
-    int64_t lo = 0, hi = D;  // dst with group_ptr[i] <= g < group_ptr[i+1]
-    while (hi - lo > 1) {
-      int64_t mid = (lo + hi) >> 1;
-      if (__ldg(a.group_ptr + mid) <= g) lo = mid;
-      else hi = mid;
-    }
-    const int64_t i = lo;
+    const int64_t i = __ldg(a.group_dst + g);
     const int64_t it0 = a.item_ptr[i] + (g - a.group_ptr[i]) * kItemGroup;
     const int64_t it1 = min(it0 + kItemGroup, a.item_ptr[i + 1]);
     float* out = partial2 + g * (int64_t)a.pw;
@@ -509,6 +495,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   a.cnt = r.cnt;
   a.dst_ptr = r.dst_ptr;
   a.item_ptr = r.item_ptr;
+  a.item_dst = r.item_dst;
   a.edge_src = r.edge_src;
   a.x = r.x;
   a.width = in;
@@ -520,6 +507,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   f.cnt = r.cnt;
   f.dst_ptr = r.dst_ptr;
   f.item_ptr = r.item_ptr;
+  f.group_dst = r.group_dst;
   f.partial = sc.partial;
   f.partial2 = sc.partial2;
   f.group_ptr = r.group_ptr;
@@ -790,6 +778,7 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   a.cnt = r.cnt;
   a.dst_ptr = r.dst_ptr;
   a.item_ptr = r.item_ptr;
+  a.item_dst = r.item_dst;
   a.edge_src = r.edge_src;
   a.x = r.x;
   a.width = in;
@@ -837,6 +826,7 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   f.cnt = r.cnt;
   f.dst_ptr = r.dst_ptr;
   f.item_ptr = r.item_ptr;
+  f.group_dst = r.group_dst;
   f.partial = sc.partial;
   f.partial2 = sc.partial2;
   f.group_ptr = r.group_ptr;
@@ -973,6 +963,8 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     r.items_max = b.items_max;
     r.dst_ptr = b.dst_ptr;
     r.item_ptr = b.item_ptr;
+    r.item_dst = b.item_dst;
+    r.group_dst = b.group_dst;
     r.edge_src = b.edge_src;
     r.self = b.self_src;
     r.x = RowSrc{w.rowp, nullptr, 0};
@@ -1036,6 +1028,8 @@ void stage_precompute(Engine& e) {
     float* partial = (float*)talloc(sizeof(float) * items_max * maxw * (mom ? 2 : 1));
     float* partial2 = (float*)talloc(sizeof(float) * (items_max / kItemGroup + N + 1) * maxw);
     int64_t* group_ptr = (int64_t*)talloc(sizeof(int64_t) * (N + 1));
+    int32_t* item_dst = (int32_t*)talloc(sizeof(int32_t) * items_max);
+    int32_t* group_dst = (int32_t*)talloc(sizeof(int32_t) * (items_max / kItemGroup + N + 1));
     float* agg = (float*)talloc(sizeof(float) * N * maxw);
     float* mean = mom ? (float*)talloc(sizeof(double) * N * maxw) : nullptr;
     float* z = wide ? (float*)talloc(sizeof(float) * N * maxw) : nullptr;
@@ -1048,8 +1042,9 @@ void stage_precompute(Engine& e) {
     sc_scan.cap = ScanScratch::bytes_for(N, 1);
     sc_scan.pool = (char*)talloc(sc_scan.cap);
     OB_CUDA(cudaMemsetAsync(sc_scan.pool, 0, sc_scan.cap, s));
-    const BlockStore3 bst{nullptr, item_ptr, group_ptr};  // dst_ptr = the graph's offsets
-    device_scan_t<I3>(s, sc_scan, OffsetsLoad3{e.g.offsets}, bst, BlockTotal3{bst, cnt}, nullptr, N, N);
+    // dst_ptr = the graph's offsets
+    const BlockStore3<OffsetsLoad3> bst{OffsetsLoad3{e.g.offsets}, nullptr, item_ptr, group_ptr, item_dst, group_dst};
+    device_scan_t<I3>(s, sc_scan, OffsetsLoad3{e.g.offsets}, bst, BlockTotal3<OffsetsLoad3>{bst, cnt}, nullptr, N, N);
     e.pe.assign(k - 1, nullptr);
     e.pe_dim.assign(k - 1, 0);
     const float* h = e.g.feats;
@@ -1070,6 +1065,8 @@ void stage_precompute(Engine& e) {
       r.items_max = items_max;
       r.dst_ptr = e.g.offsets;
       r.item_ptr = item_ptr;
+      r.item_dst = item_dst;
+      r.group_dst = group_dst;
       r.edge_src = e.g.nbrs;
       r.self = nullptr;
       r.x = RowSrc{nullptr, h, hld};
