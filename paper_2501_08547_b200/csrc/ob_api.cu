@@ -80,7 +80,7 @@ static Plan plan_request(const Engine& e, int B, int64_t m) {
     p.blocks.push_back(mk(Dm, Em, true));
     p.blocks.push_back(mk(B, m, true));
   }
-  p.max_scan_n = std::max<int64_t>(p.words_NB, p.RB_max);
+  p.max_scan_n = std::max<int64_t>(std::max<int64_t>(p.words_NB, p.RB_max), 256 * rx_tiles(m));
   for (auto& b : p.blocks) p.max_scan_n = std::max<int64_t>(p.max_scan_n, b.D_max + 1);
   return p;
 }
@@ -110,10 +110,11 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.rq_fill = a.take<int32_t>(p.RB_max + 1);
   w.rq_ptr = a.take<int64_t>(p.RB_max + 1);
   w.rq_src = a.take<int32_t>(m + 1);
-  w.big_list = a.take<int32_t>(p.RB_max + 1);
-  w.big_cptr = a.take<int64_t>(p.RB_max + 2);
+  w.rq_keys = a.take<uint64_t>(m + 1);
+  w.rq_keys2 = a.take<uint64_t>(m + 1);
+  w.rx_cnt = a.take<int32_t>(256 * rx_tiles(m));
+  w.rx_off = a.take<int64_t>(256 * rx_tiles(m) + 1);
   w.rq_ctr = a.take<int64_t>(4);
-  w.sort_tmp = a.take<int32_t>(m + 1);
   w.sbits = a.take<uint32_t>(p.words_NB + 1);
   w.swpre = a.take<int64_t>(p.words_NB + 1);
   int64_t Emax = 1, Dmax = 1, Smax = 1, Imax = 1;

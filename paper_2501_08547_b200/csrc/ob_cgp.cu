@@ -220,9 +220,10 @@ void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
     pw.rq.fill = a.take<int32_t>(RB_max + 1);
     pw.rq.ptr = a.take<int64_t>(RB_max + 1);
     pw.rq.src = a.take<int32_t>(w.m + 1);
-    pw.rq.big_list = a.take<int32_t>(RB_max + 1);
-    pw.rq.big_cptr = a.take<int64_t>(RB_max + 2);
-    pw.rq.sort_tmp = a.take<int32_t>(w.m + 1);
+    pw.rq.keys = a.take<uint64_t>(w.m + 1);
+    pw.rq.keys2 = a.take<uint64_t>(w.m + 1);
+    pw.rq.rx_cnt = a.take<int32_t>(256 * rx_tiles(w.m));
+    pw.rq.rx_off = a.take<int64_t>(256 * rx_tiles(w.m) + 1);
     pw.rq.ctr = a.take<int64_t>(4);
     for (int bi = 0; bi < 2; ++bi) {
       BlockDev b = bi == 0 ? mid : last;

@@ -152,17 +152,34 @@ struct Arena {
   }
 };
 
-// Request sources bucketed by destination slot (slot: candidate rank, or R + query).
+// Request sources bucketed by destination slot (slot: candidate rank, or R + query),
+// ascending within a slot.  Built by an LSD radix sort of one packed key per
+// edge (see RqKeyFmt); the slot offsets come from the per-slot counts.
 struct RqCsr {
   int32_t* cnt = nullptr;       // [RB]
   int32_t* fill = nullptr;      // [RB]
   int64_t* ptr = nullptr;       // [RB+1]
-  int32_t* src = nullptr;       // [m] ascending within a slot after the sort
-  int32_t* big_list = nullptr;  // long segments
-  int64_t* big_cptr = nullptr;  // chunk prefix over big_list
-  int32_t* sort_tmp = nullptr;  // [m]
-  int64_t* ctr = nullptr;       // device [4]: m (edge count), n_big, n_chunks, spare
+  int32_t* src = nullptr;       // [m] ascending within a slot
+  uint64_t* keys = nullptr;     // [m] packed keys (u32 or u64), radix ping
+  uint64_t* keys2 = nullptr;    // [m] radix pong
+  int32_t* rx_cnt = nullptr;    // [256 x tiles] digit counts per 4096-key tile (digit-major)
+  int64_t* rx_off = nullptr;    // [256 x tiles + 1] their exclusive scan
+  int64_t* ctr = nullptr;       // device [4]: m (slice edge count), spare
 };
+
+// Packed request-edge key: (population, slot, source) so that ascending key
+// order is the request CSR order.  Edges into a training candidate carry a
+// query source (every edge has a query endpoint), edges into a query carry
+// any source:
+//   candidate slot:  [0 | rank (bR bits) | src - N (bB bits)]
+//   query slot:      [1 | q (bB bits)    | src (bN bits)]   (population bit at `body`)
+struct RqKeyFmt {
+  int bB, bN, bR, body, total;
+  bool wide() const { return total > 32; }
+  int passes() const { return (total + 7) / 8; }
+};
+constexpr int kRxTile = 4096;  // keys per radix tile (512 threads x 8)
+inline int64_t rx_tiles(int64_t m_bound) { return m_bound / kRxTile + 1; }
 
 // Request inputs as seen by the kernels: written (16 bytes of pointers + m) before
 // each request so a captured CUDA graph can be replayed for any request whose
@@ -213,9 +230,10 @@ struct RequestWs {
   int32_t* rq_fill = nullptr;      // [RB]
   int64_t* rq_ptr = nullptr;       // [RB+1]
   int32_t* rq_src = nullptr;       // [m] sources, ascending within a slot after sort
-  int32_t* big_list = nullptr;     // segments for the CTA sort
-  int64_t* big_cptr = nullptr;     // chunk prefix over big_list
-  int32_t* sort_tmp = nullptr;     // [m] scratch for the big-segment merge
+  uint64_t* rq_keys = nullptr;     // [m] radix keys (ping)
+  uint64_t* rq_keys2 = nullptr;    // [m] radix keys (pong)
+  int32_t* rx_cnt = nullptr;       // radix digit counts
+  int64_t* rx_off = nullptr;       // radix digit offsets
   int64_t* rq_ctr = nullptr;       // [4] csr counters
   RqCsr rq_view() const {
     RqCsr c;
@@ -223,9 +241,10 @@ struct RequestWs {
     c.fill = rq_fill;
     c.ptr = rq_ptr;
     c.src = rq_src;
-    c.big_list = big_list;
-    c.big_cptr = big_cptr;
-    c.sort_tmp = sort_tmp;
+    c.keys = rq_keys;
+    c.keys2 = rq_keys2;
+    c.rx_cnt = rx_cnt;
+    c.rx_off = rx_off;
     c.ctr = rq_ctr;
     return c;
   }

@@ -10,15 +10,13 @@
 // prefix gives ascending order and an O(1) id -> candidate-rank map.  The
 // top-k is a radix select over the 64-bit score bit patterns (non-negative
 // doubles order like their bits) followed by an ordered compaction, so the
-// (score desc, id asc) order never needs a full sort.  Request edges are
-// bucketed by destination slot with shared-memory aggregation for the hot
-// query slots (every query receives hundreds of edges), then each bucket is
-// sorted: warp sorts for short buckets, and a chunked CTA radix sort plus
-// multi-CTA merge-path levels for long ones.  Everything runs off
-// device-side counts.
-#include <cub/block/block_radix_sort.cuh>
+// (score desc, id asc) order never needs a full sort.  The request CSR
+// (sources by destination slot, ascending) is one stable LSD radix sort of a
+// packed (population, slot, source) key per edge -- usually 29 bits, so four
+// 8-bit passes over 32-bit keys -- which handles hub queries with 10^5 in-edges
+// and the ~10^5 tiny candidate slots alike.  Everything runs off device-side
+// counts.
 #include <cub/block/block_scan.cuh>
-#include <cub/warp/warp_merge_sort.cuh>
 
 #include "ob_engine.h"
 
@@ -127,14 +125,26 @@ __global__ void k_slots_init(ReqCounters* rc, int B, const int32_t* qdeg, int32_
   }
 }
 
+// packed request-edge key (RqKeyFmt); candidate ranks come from the bitmap
+template <class K>
+__device__ __forceinline__ K rq_key(int64_t s, int64_t d, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
+                                    const RqKeyFmt& f) {
+  if (d < N) return ((K)bm_rank(cbits, cwpre, d) << f.bB) | (K)(s - N);
+  return ((K)1 << f.body) | ((K)(d - N) << f.bN) | (K)s;
+}
+
+// candidate-slot counts (query slots take qdeg) + one radix key per edge
+template <class K>
 __global__ void k_rq_count(const ReqParams* rp, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
-                           const ReqCounters* rc, int32_t* rq_cnt) {
+                           const ReqCounters* rc, int32_t* rq_cnt, K* keys, RqKeyFmt f) {
   if (rc->err & (kErrRange | kErrNoQuery)) return;
   const int64_t* __restrict__ edges = rp->edges;
   const int64_t m = rp->m;
   OB_GRID_STRIDE(e, m) {
-    int64_t d = edges[2 * e + 1];
+    int64_t s, d;
+    ld_edge(edges, e, s, d);
     if (d < N) warp_agg_inc(rq_cnt, bm_rank(cbits, cwpre, d));
+    keys[e] = rq_key<K>(s, d, N, cbits, cwpre, f);
   }
 }
 
@@ -144,12 +154,19 @@ __device__ __forceinline__ int64_t rq_slot(int64_t d, int64_t N, const uint32_t*
   return d < N ? bm_rank(cbits, cwpre, d) : R + (d - N);
 }
 
-// every slot (candidate and query) of an edge subset -- a CGP rank's slice
-__global__ void k_rq_count_all(const int64_t* __restrict__ edges, int64_t m_host, const int64_t* m_dev, int64_t N,
-                               const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt) {
+// every slot (candidate and query) of an edge subset -- a CGP rank's slice -- + keys
+template <class K>
+__global__ void k_rq_count_all(const int64_t* __restrict__ edges, const int64_t* m_dev, int64_t N,
+                               const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt,
+                               K* keys, RqKeyFmt f) {
   if (rc->err & (kErrRange | kErrNoQuery)) return;
-  const int64_t R = rc->R, m = dev_count(m_dev, m_host);  // a CGP slice: edges live in the arena
-  OB_GRID_STRIDE(e, m) warp_agg_inc(rq_cnt, rq_slot(edges[2 * e + 1], N, cbits, cwpre, R));
+  const int64_t R = rc->R, m = *m_dev;  // a CGP slice: edges live in the arena
+  OB_GRID_STRIDE(e, m) {
+    int64_t s, d;
+    ld_edge(edges, e, s, d);
+    warp_agg_inc(rq_cnt, rq_slot(d, N, cbits, cwpre, R));
+    keys[e] = rq_key<K>(s, d, N, cbits, cwpre, f);
+  }
 }
 
 __global__ void k_zero_slots(const ReqCounters* rc, int B, int32_t* a, int32_t* b) {
@@ -271,258 +288,154 @@ struct SelStore {
 };
 
 // ---------------------------------------------------------------------------
-// 3. request CSR fill: per-CTA reservation for query slots, warp-aggregated
-//    atomics for candidate slots
+// 3. request CSR order: stable LSD radix sort of the packed keys, 8-bit digits,
+//    4096-key tiles.  Per pass: digit counts per tile (digit-major), one scan,
+//    then a stable scatter -- keys are ranked inside the tile warp by warp
+//    (match_any over the digit, items in index order), exchanged through shared
+//    memory into tile order and written out in coalesced runs.  The last pass
+//    writes the decoded source ids straight into the CSR.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_rq_fill(const int64_t* __restrict__ edges_arg, int64_t m_host,
-                                                 const int64_t* m_dev, const ReqParams* rp, int64_t N, int B,
-                                                 const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc,
-                                                 const int64_t* rq_ptr, int32_t* rq_fill, int32_t* rq_src) {
-  extern __shared__ int32_t sm[];  // [B] counts, then [B] base offsets
-  const bool smem = B <= kMaxSmemQueries / 2;
-  if (rc->err & (kErrRange | kErrNoQuery)) return;
-  const int64_t R = rc->R;
-  // the whole request (edges from the parameter block) or a CGP slice in the arena
-  const int64_t* __restrict__ edges = rp ? rp->edges : edges_arg;
-  const int64_t m = rp ? rp->m : dev_count(m_dev, m_host);
-  int32_t* cnt = sm;
-  int32_t* base = sm + B;
-  for (int64_t t0 = (int64_t)blockIdx.x * kEdgeTile; t0 < m; t0 += (int64_t)gridDim.x * kEdgeTile) {
-    const int64_t t1 = min(t0 + kEdgeTile, m);
-    if (smem) {
-      for (int q = threadIdx.x; q < B; q += blockDim.x) cnt[q] = 0;
-      __syncthreads();
-      for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-        int64_t d = edges[2 * e + 1];
-        if (d >= N) atomicAdd(cnt + (d - N), 1);
-      }
-      __syncthreads();
-      for (int q = threadIdx.x; q < B; q += blockDim.x) {
-        base[q] = cnt[q] ? atomicAdd(rq_fill + R + q, cnt[q]) : 0;
-        cnt[q] = 0;
-      }
-      __syncthreads();
+constexpr int kRxThreads = 512;
+constexpr int kRxWarps = kRxThreads / 32;
+constexpr int kRxItems = kRxTile / kRxThreads;  // 8 keys per thread, warp-striped
+
+template <class K>
+__global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* __restrict__ keys, const int64_t* m_dev, int shift,
+                                                        int64_t tiles_b, int32_t* cnt) {
+  __shared__ int32_t h[256];
+  const int64_t m = *m_dev;
+  const int64_t tiles = (m + kRxTile - 1) / kRxTile;
+  for (int64_t t = blockIdx.x; t < tiles_b; t += gridDim.x) {
+    if (threadIdx.x < 256) h[threadIdx.x] = 0;
+    __syncthreads();
+    if (t < tiles) {
+      const int64_t e1 = min((t + 1) * kRxTile, m);
+      for (int64_t e = t * kRxTile + threadIdx.x; e < e1; e += kRxThreads) atomicAdd(&h[(keys[e] >> shift) & 255], 1);
     }
-    for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-      int64_t s, d;
-      ld_edge(edges, e, s, d);
-      int64_t pos;
-      if (d >= N) {
-        int64_t q = d - N;
-        pos = rq_ptr[R + q] + (smem ? base[q] + atomicAdd(cnt + q, 1) : atomicAdd(rq_fill + R + q, 1));
-      } else {
-        int64_t c = bm_rank(cbits, cwpre, d);
-        pos = rq_ptr[c] + warp_agg_inc(rq_fill, c);
-      }
-      rq_src[pos] = (int32_t)s;
-    }
-    if (smem) __syncthreads();
+    __syncthreads();
+    if (threadIdx.x < 256) cnt[(int64_t)threadIdx.x * tiles_b + t] = h[threadIdx.x];
+    __syncthreads();
   }
 }
 
-// ---------------------------------------------------------------------------
-// 4. per-slot sort of request sources
-// ---------------------------------------------------------------------------
-constexpr int kWarpSortItems = 8;     // warp sort handles <= 256
-constexpr int kChunkThreads = 512;
-constexpr int kChunkItems = 8;
-constexpr int kChunk = kChunkThreads * kChunkItems;  // 4096-element CTA sort tiles
-
-__device__ __forceinline__ void warp_bitonic32(int32_t& v) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      int32_t o = __shfl_xor_sync(0xffffffffu, v, j);
-      bool up = ((lane & k) == 0);
-      bool lower = ((lane & j) == 0);
-      v = (lower == up) ? min(v, o) : max(v, o);
-    }
-  }
-}
-
-struct LessI32 {
-  __device__ bool operator()(const int32_t& a, const int32_t& b) const { return a < b; }
-};
-
-__global__ void __launch_bounds__(256) k_segsort_warp(const int64_t* __restrict__ ptr, const ReqCounters* rc,
-                                                      int64_t* ctr, int32_t* vals, int32_t* big_list) {
-  using WS = cub::WarpMergeSort<int32_t, kWarpSortItems, 32>;
-  __shared__ typename WS::TempStorage tmp[8];
+template <class K, bool FINAL>
+__global__ void __launch_bounds__(kRxThreads) k_rx_scatter(const K* __restrict__ in, K* out, int32_t* src_out,
+                                                           const int64_t* m_dev, int shift, int64_t tiles_b,
+                                                           const int64_t* __restrict__ off, RqKeyFmt f, int64_t N) {
+  using BS = cub::BlockScan<int32_t, kRxThreads>;
+  __shared__ union {
+    int32_t wcnt[kRxWarps][256];  // per-warp digit counts, then per-warp offsets
+    K exch[kRxTile];              // the tile in (digit, index) order
+  } u;
+  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ int32_t bstart[256];
+  __shared__ int64_t gofs[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nseg = rc->RB;
-  for (int64_t s = (int64_t)blockIdx.x * 8 + warp; s < nseg; s += (int64_t)gridDim.x * 8) {
-    const int64_t b = ptr[s], len = ptr[s + 1] - b;
-    if (len <= 1) continue;
-    if (len <= 32) {
-      int32_t v = lane < len ? vals[b + lane] : INT32_MAX;
-      warp_bitonic32(v);
-      if (lane < len) vals[b + lane] = v;
-    } else if (len <= 32 * kWarpSortItems) {
-      int32_t k[kWarpSortItems];
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t m = *m_dev;
+  const int64_t tiles = (m + kRxTile - 1) / kRxTile;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int i = threadIdx.x; i < kRxWarps * 256; i += kRxThreads) (&u.wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t base = t * kRxTile + warp * 256;
+    K k[kRxItems];
+    int dg[kRxItems], rk[kRxItems];
 #pragma unroll
-      for (int i = 0; i < kWarpSortItems; ++i) {
-        int64_t idx = (int64_t)lane * kWarpSortItems + i;
-        k[i] = idx < len ? vals[b + idx] : INT32_MAX;
+    for (int i = 0; i < kRxItems; ++i) {
+      const int64_t idx = base + i * 32 + lane;
+      k[i] = idx < m ? in[idx] : (K)0;
+      dg[i] = idx < m ? (int)((k[i] >> shift) & 255) : 256 + lane;  // padding never matches
+    }
+#pragma unroll
+    for (int i = 0; i < kRxItems; ++i) {
+      const unsigned peers = __match_any_sync(0xffffffffu, dg[i]);
+      const int leader = __ffs(peers) - 1;
+      int b0 = 0;
+      if (lane == leader && dg[i] < 256) {
+        b0 = u.wcnt[warp][dg[i]];
+        u.wcnt[warp][dg[i]] = b0 + __popc(peers);
       }
-      WS(tmp[warp]).Sort(k, LessI32());
-#pragma unroll
-      for (int i = 0; i < kWarpSortItems; ++i) {
-        int64_t idx = (int64_t)lane * kWarpSortItems + i;
-        if (idx < len) vals[b + idx] = k[i];
+      rk[i] = __shfl_sync(0xffffffffu, b0, leader) + __popc(peers & lt);
+      __syncwarp();
+    }
+    __syncthreads();
+    int32_t tot = 0;
+    if (threadIdx.x < 256) {  // per digit: warps' exclusive offsets, tile total
+      for (int w2 = 0; w2 < kRxWarps; ++w2) {
+        const int32_t c = u.wcnt[w2][threadIdx.x];
+        u.wcnt[w2][threadIdx.x] = tot;
+        tot += c;
       }
-    } else if (lane == 0) {
-      int64_t at = atomicAdd((unsigned long long*)&ctr[1], 1ull);
-      big_list[at] = (int32_t)s;
     }
-  }
-}
-
-struct ChunkLoad {
-  const int32_t* big_list;
-  const int64_t* ptr;
-  __device__ int64_t operator()(int64_t i) const {
-    int64_t s = big_list[i];
-    return (ptr[s + 1] - ptr[s] + kChunk - 1) / kChunk;
-  }
-};
-
-// (big segment, chunk) of chunk index ci
-__device__ __forceinline__ void chunk_of(const int64_t* cptr, int64_t nbig, int64_t ci, int64_t* seg, int64_t* j) {
-  int64_t lo = 0, hi = nbig;
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (cptr[mid] <= ci) lo = mid;
-    else hi = mid;
-  }
-  *seg = lo;
-  *j = ci - cptr[lo];
-}
-
-// sort every 4096-element chunk of every long segment in shared memory
-__device__ __forceinline__ int levels_for(int64_t len);
-
-// ids are < 2^end_bit, so only end_bit radix bits are sorted; the merge levels the
-// longest segment needs are published in ctr[3] (later levels exit at once)
-__global__ void __launch_bounds__(kChunkThreads) k_chunk_sort(const int64_t* __restrict__ ptr, int64_t* ctr,
-                                                              const int32_t* big_list, const int64_t* cptr,
-                                                              int32_t* vals, int end_bit) {
-  using BRS = cub::BlockRadixSort<int32_t, kChunkThreads, kChunkItems>;
-  __shared__ typename BRS::TempStorage tmp;
-  const int64_t nbig = ctr[1], nch = ctr[2];
-  for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
-    int64_t bi, j;
-    chunk_of(cptr, nbig, ci, &bi, &j);
-    const int64_t s = big_list[bi];
-    const int64_t b = ptr[s] + j * kChunk, len = min((int64_t)kChunk, ptr[s + 1] - b);
-    if (j == 0 && threadIdx.x == 0)
-      atomicMax((unsigned long long*)&ctr[3], (unsigned long long)levels_for(ptr[s + 1] - ptr[s]));
-    int32_t k[kChunkItems];
-#pragma unroll
-    for (int i = 0; i < kChunkItems; ++i) {
-      int64_t idx = (int64_t)threadIdx.x * kChunkItems + i;
-      k[i] = idx < len ? vals[b + idx] : INT32_MAX;  // padding sorts last (stable, all-ones low bits)
-    }
-    BRS(tmp).Sort(k, 0, end_bit);
-#pragma unroll
-    for (int i = 0; i < kChunkItems; ++i) {
-      int64_t idx = (int64_t)threadIdx.x * kChunkItems + i;
-      if (idx < len) vals[b + idx] = k[i];
+    int32_t start;
+    BS(scan_tmp).ExclusiveSum(tot, start);
+    if (threadIdx.x < 256) {
+      bstart[threadIdx.x] = start;
+      gofs[threadIdx.x] = off[(int64_t)threadIdx.x * tiles_b + t];
     }
     __syncthreads();
-  }
-}
-
-// number of elements of a[0,na) that are < v (strict) or <= v
-__device__ __forceinline__ int lower_cnt(const int32_t* a, int na, int32_t v, bool inclusive) {
-  int lo = 0, hi = na;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    bool go = inclusive ? (a[mid] <= v) : (a[mid] < v);
-    if (go) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-// merge levels a segment of `len` needs after the 4096-element chunk sort
-__device__ __forceinline__ int levels_for(int64_t len) {
-  int l = 0;
-  for (int64_t w = kChunk; w < len; w *= 2) ++l;
-  return l;
-}
-
-// merge level `level` (run width 4096 << level): runs merge pairwise from the
-// buffer the segment's data currently sits in (parity of the level) into the
-// other; segments that need fewer levels are skipped.  Each CTA produces one
-// 4096-element output tile (merge-path split, then rank-merge in shared memory).
-__global__ void __launch_bounds__(kChunkThreads) k_merge_level(const int64_t* __restrict__ ptr, const int64_t* ctr,
-                                                               const int32_t* big_list, const int64_t* cptr,
-                                                               int32_t* vals, int32_t* tmp, int level) {
-  __shared__ int32_t sa[kChunk];
-  __shared__ int32_t sb[kChunk];
-  __shared__ int64_t split[2];
-  const int64_t nbig = ctr[1], nch = ctr[2];
-  if (level >= ctr[3]) return;  // no segment needs this level
-  const int64_t w = (int64_t)kChunk << level;
-  for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
-    int64_t bi, j;
-    chunk_of(cptr, nbig, ci, &bi, &j);
-    const int64_t s = big_list[bi];
-    const int64_t sb0 = ptr[s], len = ptr[s + 1] - sb0;
-    if (level >= levels_for(len)) continue;  // uniform per CTA
-    const int32_t* src = (level & 1) ? tmp : vals;
-    int32_t* dst = (level & 1) ? vals : tmp;
-    const int64_t o0 = j * kChunk, o1 = min(o0 + kChunk, len);
-    const int64_t ps = (o0 / (2 * w)) * (2 * w);
-    const int64_t na = min(w, len - ps), nb = max((int64_t)0, min(w, len - ps - na));
-    const int32_t* A = src + sb0 + ps;
-    const int32_t* Bp = A + na;
-    if (nb == 0) {  // lone run: copy through
-      for (int64_t o = o0 + threadIdx.x; o < o1; o += blockDim.x) dst[sb0 + o] = src[sb0 + o];
-      __syncthreads();
-      continue;
-    }
-    if (threadIdx.x < 2) {
-      const int64_t d = (threadIdx.x == 0 ? o0 : o1) - ps;
-      int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
-      while (lo < hi) {  // merge path: A elements precede equal B elements
-        int64_t mid = (lo + hi) >> 1;
-        if (A[mid] <= Bp[d - 1 - mid]) lo = mid + 1;
-        else hi = mid;
+#pragma unroll
+    for (int i = 0; i < kRxItems; ++i)
+      if (dg[i] < 256) rk[i] += bstart[dg[i]] + u.wcnt[warp][dg[i]];
+    __syncthreads();  // offsets read before the exchange overwrites them
+#pragma unroll
+    for (int i = 0; i < kRxItems; ++i)
+      if (dg[i] < 256) u.exch[rk[i]] = k[i];
+    __syncthreads();
+    const int n = (int)min((int64_t)kRxTile, m - t * kRxTile);
+    for (int p = threadIdx.x; p < n; p += kRxThreads) {
+      const K kk = u.exch[p];
+      const int d = (int)((kk >> shift) & 255);
+      const int64_t pos = gofs[d] + (p - bstart[d]);
+      if (FINAL) {
+        const bool query_slot = (kk >> f.body) & 1;
+        src_out[pos] = query_slot ? (int32_t)(kk & (((K)1 << f.bN) - 1)) : (int32_t)(N + (kk & (((K)1 << f.bB) - 1)));
+      } else {
+        out[pos] = kk;
       }
-      split[threadIdx.x] = lo;
     }
-    __syncthreads();
-    const int64_t a0 = split[0], a1 = split[1];
-    const int64_t b0 = (o0 - ps) - a0, b1 = (o1 - ps) - a1;
-    const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
-    for (int i = threadIdx.x; i < la; i += blockDim.x) sa[i] = A[a0 + i];
-    for (int i = threadIdx.x; i < lb; i += blockDim.x) sb[i] = Bp[b0 + i];
-    __syncthreads();
-    int32_t* out = dst + sb0 + o0;
-    for (int i = threadIdx.x; i < la; i += blockDim.x) out[i + lower_cnt(sb, lb, sa[i], false)] = sa[i];
-    for (int i = threadIdx.x; i < lb; i += blockDim.x) out[i + lower_cnt(sa, la, sb[i], true)] = sb[i];
     __syncthreads();
   }
 }
 
-// segments whose level count is odd finished in tmp: copy their tiles back
-__global__ void __launch_bounds__(kChunkThreads) k_merge_copyback(const int64_t* __restrict__ ptr,
-                                                                  const int64_t* ctr, const int32_t* big_list,
-                                                                  const int64_t* cptr, int32_t* vals,
-                                                                  const int32_t* tmp) {
-  const int64_t nbig = ctr[1], nch = ctr[2];
-  for (int64_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
-    int64_t bi, j;
-    chunk_of(cptr, nbig, ci, &bi, &j);
-    const int64_t s = big_list[bi];
-    const int64_t sb0 = ptr[s], len = ptr[s + 1] - sb0;
-    if (!(levels_for(len) & 1)) continue;
-    const int64_t o0 = j * kChunk, o1 = min(o0 + kChunk, len);
-    for (int64_t o = o0 + threadIdx.x; o < o1; o += blockDim.x) vals[sb0 + o] = tmp[sb0 + o];
+template <class K>
+static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int64_t m_bound, const RqKeyFmt& f) {
+  cudaStream_t s = e.stream;
+  const int64_t tiles_b = rx_tiles(m_bound);
+  const int g = grid_for(tiles_b, 1, kNumSMs * 2);
+  K* a = reinterpret_cast<K*>(c.keys);
+  K* b = reinterpret_cast<K*>(c.keys2);
+  const int passes = f.passes();
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    k_rx_hist<K><<<g, kRxThreads, 0, s>>>(a, m_dev, shift, tiles_b, c.rx_cnt);
+    OB_LAUNCHED();
+    device_scan(s, e.scan, LoadI32{c.rx_cnt}, StoreI64{c.rx_off}, nullptr, 256 * tiles_b, 256 * tiles_b, nullptr);
+    if (p + 1 == passes) {
+      k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, c.rx_off, f, e.g.N);
+    } else {
+      k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, c.rx_off, f, e.g.N);
+      std::swap(a, b);
+    }
+    OB_LAUNCHED();
   }
+}
+
+static int bits_for(int64_t n) {  // bits to hold values in [0, n)
+  int b = 1;
+  while (b < 62 && ((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+RqKeyFmt rq_key_fmt(const Engine& e, const RequestWs& w) {
+  RqKeyFmt f;
+  f.bB = bits_for(std::max(w.B, 1));
+  f.bN = bits_for(e.g.N + w.B);
+  f.bR = bits_for(std::max<int64_t>(1, std::min<int64_t>(e.g.N, 2 * w.m)));
+  f.body = std::max(f.bR + f.bB, f.bB + f.bN);
+  f.total = f.body + 1;
+  OB_CHECK(f.total <= 64, OB_EINVAL, "request key does not fit 64 bits");
+  return f;
 }
 
 // ---------------------------------------------------------------------------
@@ -550,8 +463,13 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   const int64_t rb_max = std::min<int64_t>(N, 2 * m) + w.B;
   k_slots_init<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rc, w.B, w.qdeg, w.rq_cnt, w.rq_fill);
   OB_LAUNCHED();
-  if (m > 0) {
-    k_rq_count<<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt);
+  if (m > 0) {  // candidate-slot counts + the request CSR's radix keys
+    const RqKeyFmt f = rq_key_fmt(e, w);
+    if (f.wide())
+      k_rq_count<uint64_t><<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt, w.rq_keys, f);
+    else
+      k_rq_count<uint32_t><<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt,
+                                                            reinterpret_cast<uint32_t*>(w.rq_keys), f);
     OB_LAUNCHED();
   }
   if (need_scores) {
@@ -580,50 +498,31 @@ void stage_select(Engine& e, RequestWs& w) {
 }
 
 // Request CSR over an edge set (the whole request via the parameter block when
-// edges == nullptr, or one CGP rank's slice in the arena): bucket by destination
-// slot, then sort each slot's sources ascending.
+// edges == nullptr, or one CGP rank's slice in the arena): slot offsets from
+// the per-slot counts, source order from the radix sort of the packed keys.
 void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound, const int64_t* m_dev, RqCsr& c,
                   bool counts_ready) {
-  const ReqParams* rp = edges ? nullptr : w.rp;
   cudaStream_t s = e.stream;
   const int64_t rb_max = std::min<int64_t>(e.g.N, 2 * w.m) + w.B;
-  OB_CUDA(cudaMemsetAsync(c.ctr + 1, 0, 3 * sizeof(int64_t), s));
+  const RqKeyFmt f = rq_key_fmt(e, w);
+  if (!edges) m_dev = &w.rp->m;  // the whole request: its edge count lives in the parameter block
   if (!counts_ready) {
     k_zero_slots<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rc, w.B, c.cnt, c.fill);
     OB_LAUNCHED();
     if (m_bound > 0) {
-      k_rq_count_all<<<grid_for(m_bound, 256), 256, 0, s>>>(edges, m_bound, m_dev, e.g.N, w.cbits, w.cwpre, w.rc,
-                                                              c.cnt);
+      if (f.wide())
+        k_rq_count_all<uint64_t><<<grid_for(m_bound, 256), 256, 0, s>>>(edges, m_dev, e.g.N, w.cbits, w.cwpre, w.rc,
+                                                                          c.cnt, c.keys, f);
+      else
+        k_rq_count_all<uint32_t><<<grid_for(m_bound, 256), 256, 0, s>>>(
+            edges, m_dev, e.g.N, w.cbits, w.cwpre, w.rc, c.cnt, reinterpret_cast<uint32_t*>(c.keys), f);
       OB_LAUNCHED();
     }
   }
   device_scan(s, e.scan, LoadI32{c.cnt}, StoreI64{c.ptr}, &w.rc->RB, 0, rb_max, nullptr, c.ptr);
   if (m_bound <= 0) return;
-  const size_t sm = w.B <= kMaxSmemQueries / 2 ? 2 * sizeof(int32_t) * w.B : 0;
-  k_rq_fill<<<grid_for(m_bound, kEdgeTile, kNumSMs * 4), 256, sm, s>>>(edges, m_bound, m_dev, rp, e.g.N, w.B,
-                                                                         w.cbits, w.cwpre, w.rc, c.ptr, c.fill, c.src);
-  k_segsort_warp<<<grid_for(rb_max, 8), 256, 0, s>>>(c.ptr, w.rc, c.ctr, c.src, c.big_list);
-  g_launches += 2;
-  // long segments: chunk sort + merge levels (ping-pong src <-> sort_tmp)
-  device_scan(s, e.scan, ChunkLoad{c.big_list, c.ptr}, StoreI64{c.big_cptr}, c.ctr + 1, 0, rb_max, c.ctr + 2,
-              c.big_cptr);
-  const int64_t ch_max = m_bound / kChunk + rb_max / 256 + 2;
-  const int g = grid_for(ch_max, 1, kNumSMs * 4);
-  int end_bit = 1;
-  while (end_bit < 31 && ((int64_t)1 << end_bit) <= e.g.N + w.B) ++end_bit;
-  k_chunk_sort<<<g, kChunkThreads, 0, s>>>(c.ptr, c.ctr, c.big_list, c.big_cptr, c.src, end_bit);
-  OB_LAUNCHED();
-  // the longest possible segment is the whole edge set; levels past a segment's
-  // own count exit immediately
-  int level = 0;
-  for (int64_t wd = kChunk; wd < m_bound; wd *= 2, ++level) {
-    k_merge_level<<<g, kChunkThreads, 0, s>>>(c.ptr, c.ctr, c.big_list, c.big_cptr, c.src, c.sort_tmp, level);
-    OB_LAUNCHED();
-  }
-  if (level > 0) {
-    k_merge_copyback<<<g, kChunkThreads, 0, s>>>(c.ptr, c.ctr, c.big_list, c.big_cptr, c.src, c.sort_tmp);
-    OB_LAUNCHED();
-  }
+  if (f.wide()) rx_sort<uint64_t>(e, w, c, m_dev, m_bound, f);
+  else rx_sort<uint32_t>(e, w, c, m_dev, m_bound, f);
 }
 
 void stage_request_csr(Engine& e, RequestWs& w) {
