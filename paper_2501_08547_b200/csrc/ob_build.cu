@@ -96,13 +96,38 @@ __global__ void __launch_bounds__(256) k_block_fill(const BlockCounters* cnt, co
     const int64_t e1 = min(e0 + kAggChunk, __ldg(dst_ptr + i + 1));
     const int64_t cs = __ldg(sp.cs + i), rs = __ldg(sp.rs + i);
     const int32_t cl = __ldg(sp.cl + i);
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
-      const int64_t j = e - d0;
-      const int32_t src = j < cl ? __ldg(nbrs + cs + j) : __ldg(rq_src + rs + (j - cl));
-      src_global[e] = src;
-      bm_set_warp(sbits, src);
+    int32_t v[kAggChunk / 32];
+#pragma unroll
+    for (int u = 0; u < kAggChunk / 32; ++u) {  // all loads in flight first
+      const int64_t e = e0 + u * 32 + lane, j = e - d0;
+      v[u] = e < e1 ? (j < cl ? __ldg(nbrs + cs + j) : __ldg(rq_src + rs + (j - cl))) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kAggChunk / 32; ++u) {
+      if (v[u] < 0) continue;
+      src_global[e0 + u * 32 + lane] = v[u];
+      bm_set(sbits, v[u]);  // test before set: a re-marked source costs a read, not an atomic
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_expand_items(const BlockCounters* cnt, const int64_t* __restrict__ item_ptr,
+                                                      const int64_t* __restrict__ group_ptr, int32_t* item_dst,
+                                                      int32_t* group_dst) {
+  const int64_t D = cnt->D;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < D; i += nw) {
+    for (int64_t it = item_ptr[i] + lane; it < item_ptr[i + 1]; it += 32) item_dst[it] = (int32_t)i;
+    for (int64_t g = group_ptr[i] + lane; g < group_ptr[i + 1]; g += 32) group_dst[g] = (int32_t)i;
+  }
+}
+
+void expand_items(cudaStream_t s, const BlockCounters* cnt, int64_t D_max, const int64_t* item_ptr,
+                  const int64_t* group_ptr, int32_t* item_dst, int32_t* group_dst) {
+  k_expand_items<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(cnt, item_ptr, group_ptr, item_dst, group_dst);
+  OB_LAUNCHED();
 }
 
 __global__ void k_mark_ids(const int32_t* __restrict__ ids, const BlockCounters* cnt, uint32_t* sbits) {
@@ -154,9 +179,9 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
   OB_LAUNCHED();
   // dst_ptr / item_ptr / group_ptr (+ E, items, groups) in one pass; the work
   // items double as the fill's edge chunks
-  const BlockStore3<SegLenLoad3> st{SegLenLoad3{w.seg_len}, b.dst_ptr, b.item_ptr, b.group_ptr, b.item_dst, b.group_dst};
-  device_scan_t<I3>(s, e.scan, SegLenLoad3{w.seg_len}, st, BlockTotal3<SegLenLoad3>{st, b.cnt}, &b.cnt->D, 0,
-                    b.D_max);
+  const BlockStore3 st{b.dst_ptr, b.item_ptr, b.group_ptr};
+  device_scan_t<I3>(s, e.scan, SegLenLoad3{w.seg_len}, st, BlockTotal3{st, b.cnt}, &b.cnt->D, 0, b.D_max);
+  expand_items(s, b.cnt, b.D_max, b.item_ptr, b.group_ptr, b.item_dst, b.group_dst);
   OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
   k_block_fill<<<grid_for(b.items_max, 8, kNumSMs * 16), 256, 0, s>>>(b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs,
                                                                        src.rq_src, w.src_global, w.sbits);

@@ -395,42 +395,30 @@ struct OffsetsLoad3 {  // from an existing CSR offsets array
   const int64_t* off;
   __device__ I3 operator()(int64_t i) const { return block_counts(off[i + 1] - off[i]); }
 };
-// Stores the three offsets and expands the item -> destination and
-// group -> destination maps (the counts are recomputed from the source).
-template <class Src>
 struct BlockStore3 {
-  Src src;
   int64_t* dst_ptr;  // null: offsets already exist
   int64_t* item_ptr;
   int64_t* group_ptr;
-  int32_t* item_dst;
-  int32_t* group_dst;
   __device__ void operator()(int64_t i, const I3& v) const {
     if (dst_ptr) dst_ptr[i] = v.a;
     item_ptr[i] = v.b;
     group_ptr[i] = v.c;
-    const I3 c = src(i);
-    for (int64_t k = 0; k < c.b; ++k) item_dst[v.b + k] = (int32_t)i;
-    for (int64_t k = 0; k < c.c; ++k) group_dst[v.c + k] = (int32_t)i;
-  }
-  __device__ void end(int64_t n, const I3& v) const {
-    if (dst_ptr) dst_ptr[n] = v.a;
-    item_ptr[n] = v.b;
-    group_ptr[n] = v.c;
   }
 };
-template <class Src>
 struct BlockTotal3 {
-  BlockStore3<Src> st;
+  BlockStore3 st;
   BlockCounters* cnt;
   __device__ void operator()(int64_t n, const I3& v) const {
-    st.end(n, v);
+    st(n, v);
     cnt->E = v.a;
     cnt->items = v.b;
     cnt->groups = v.c;
   }
 };
 
+// item -> destination and group -> destination maps (warp per destination)
+void expand_items(cudaStream_t s, const BlockCounters* cnt, int64_t D_max, const int64_t* item_ptr,
+                  const int64_t* group_ptr, int32_t* item_dst, int32_t* group_dst);
 void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d_kind, int32_t* d_pe_layer);
 BindCtx bind_ctx(Engine& e, RequestWs& w, int l);
 void stage_qpad(Engine& e, RequestWs& w);

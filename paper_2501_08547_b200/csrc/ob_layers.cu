@@ -1043,8 +1043,9 @@ void stage_precompute(Engine& e) {
     sc_scan.pool = (char*)talloc(sc_scan.cap);
     OB_CUDA(cudaMemsetAsync(sc_scan.pool, 0, sc_scan.cap, s));
     // dst_ptr = the graph's offsets
-    const BlockStore3<OffsetsLoad3> bst{OffsetsLoad3{e.g.offsets}, nullptr, item_ptr, group_ptr, item_dst, group_dst};
-    device_scan_t<I3>(s, sc_scan, OffsetsLoad3{e.g.offsets}, bst, BlockTotal3<OffsetsLoad3>{bst, cnt}, nullptr, N, N);
+    const BlockStore3 bst{nullptr, item_ptr, group_ptr};
+    device_scan_t<I3>(s, sc_scan, OffsetsLoad3{e.g.offsets}, bst, BlockTotal3{bst, cnt}, nullptr, N, N);
+    expand_items(s, cnt, N, item_ptr, group_ptr, item_dst, group_dst);
     e.pe.assign(k - 1, nullptr);
     e.pe_dim.assign(k - 1, 0);
     const float* h = e.g.feats;

@@ -65,18 +65,29 @@ __global__ void __launch_bounds__(256) k_request_mark(const ReqParams* rp, int64
       __syncthreads();
     }
     const int64_t t1 = min(t0 + kEdgeTile, m);
-    for (int64_t e = t0 + threadIdx.x; e < t1; e += blockDim.x) {
-      int64_t s, d;
-      ld_edge(edges, e, s, d);
-      if (s < 0 || s >= hi || d < 0 || d >= hi) {
-        err |= kErrRange;
-        continue;
+    constexpr int kU = 4;  // edges per thread with their loads in flight together
+    for (int64_t e00 = t0 + threadIdx.x; e00 < t1; e00 += (int64_t)kU * blockDim.x) {
+      int64_t sv[kU], dv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t e = e00 + (int64_t)u * blockDim.x;
+        sv[u] = dv[u] = 0;
+        if (e < t1) ld_edge(edges, e, sv[u], dv[u]);
       }
-      if (s < N && d < N) err |= kErrNoQuery;
-      if (s < N) bm_set(cbits, s);
-      if (d < N) bm_set(cbits, d);
-      else if (smem) atomicAdd(sq + (d - N), 1);
-      else atomicAdd(qdeg + (d - N), 1);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (e00 + (int64_t)u * blockDim.x >= t1) break;
+        const int64_t s = sv[u], d = dv[u];
+        if (s < 0 || s >= hi || d < 0 || d >= hi) {
+          err |= kErrRange;
+          continue;
+        }
+        if (s < N && d < N) err |= kErrNoQuery;
+        if (s < N) bm_set(cbits, s);
+        if (d < N) bm_set(cbits, d);
+        else if (smem) atomicAdd(sq + (d - N), 1);
+        else atomicAdd(qdeg + (d - N), 1);
+      }
     }
     if (smem) {
       __syncthreads();
