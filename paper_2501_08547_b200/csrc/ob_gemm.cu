@@ -142,15 +142,41 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
 // Shared memory: S-stage ring of {A, A_lo, B, B_lo} + epilogue transpose tiles.
 template <int NP>
 struct TcSmem {
+  // A_lo lives in TMEM (written by the transform warps with tcgen05.st) when the
+  // two accumulators leave room: frees 16 KB of shared memory per stage
+  static constexpr bool kLoTmem = NP <= 128;
   static constexpr int kTileB = NP * kTcBK * 4;
-  static constexpr int kStage = 2 * kTileA + 2 * kTileB;
+  static constexpr int kStage = (kLoTmem ? 1 : 2) * kTileA + 2 * kTileB;
   static constexpr int kEpi = kWarpsEpi * 32 * 32 * 4;  // 16 KB
   static constexpr int kFixed = kEpi + 1024 /*align*/ + 512 /*bars*/;
-  static constexpr int kStages = ((227 * 1024 - kFixed) / kStage) >= 4 ? 4
-                                 : (((227 * 1024 - kFixed) / kStage) >= 3 ? 3 : 2);
+  static constexpr int kFit = (227 * 1024 - kFixed) / kStage;
+  static constexpr int kStages = kFit >= 6 ? 6 : (kFit < 2 ? 2 : kFit);
   static constexpr int kBytes = kStages * kStage + kFixed;
-  static constexpr uint32_t kCols = NP <= 32 ? 64 : (NP <= 64 ? 128 : (NP <= 128 ? 256 : 512));  // 2 accumulators
+  static constexpr uint32_t kAccCols = 2 * (NP < 32 ? 32 : NP);  // two accumulators
+  static constexpr uint32_t kLoCol = kAccCols;                     // then kStages x 32 A_lo columns
+  static constexpr uint32_t kNeed = kAccCols + (kLoTmem ? kStages * kTcBK : 0);
+  static constexpr uint32_t kCols = kNeed <= 64 ? 64 : (kNeed <= 128 ? 128 : (kNeed <= 256 ? 256 : 512));
+  static_assert(kNeed <= 512, "TMEM budget");
 };
+
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// A operand from TMEM (the A_lo x B_hi product)
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(tmem_d), "r"(tmem_a), "l"(bdesc),
+      "r"(idesc));
+}
 
 template <int NP>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -197,14 +223,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   if (warp < kWarpsProd) {
     // ---------------- producers ----------------
+    // thread t copies 16-byte chunk (t & 7) of rows (t >> 3) + 16 i: each warp
+    // instruction moves four whole 128-byte row segments (coalesced), not 32
+    // scattered 16-byte pieces
+    constexpr int kRowsPer = kTcBM / (kWarpsProd * 32 / 8);  // 8 rows per thread
+    const int c = tid & 7, r0 = tid >> 3;
     uint32_t gk = 0;
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int64_t row = tile * kTcBM + tid;  // one tile row per producer thread
-      const float* p1 = nullptr;
-      const float* p2 = nullptr;
-      if (row < M) {
-        if (g.K1) p1 = g.a1.row(g.self ? (int64_t)g.self[row] : row);
-        if (g.K2) p2 = g.a2 + row * g.lda2;
+      const float* p1[kRowsPer];
+      const float* p2[kRowsPer];
+#pragma unroll
+      for (int i = 0; i < kRowsPer; ++i) {
+        const int64_t row = tile * kTcBM + r0 + 16 * i;
+        p1[i] = (row < M && g.K1) ? g.a1.row(g.self ? (int64_t)g.self[row] : row) : nullptr;
+        p2[i] = (row < M && g.K2) ? g.a2 + row * g.lda2 : nullptr;
       }
       for (int kb = 0; kb < KB; ++kb, ++gk) {
         const int s = gk % S;
@@ -212,21 +244,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint8_t* st = base + s * SM::kStage;
         const uint32_t a_s = smem_u32(st);
         const bool first = kb < KB1;
-        const int k0 = (first ? kb : kb - KB1) * kTcBK;
-        const int Kv = first ? g.K1 : g.K2;
-        const float* rp = first ? p1 : p2;
+        const int k = (first ? kb : kb - KB1) * kTcBK + c * 4;
+        const int rem = (first ? g.K1 : g.K2) - k;
+        const int vb = rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int k = k0 + c * 4;
-          const int rem = Kv - k;
-          const int bytes = rp ? (rem >= 4 ? 16 : (rem > 0 ? rem * 4 : 0)) : 0;
+        for (int i = 0; i < kRowsPer; ++i) {
+          const int r = r0 + 16 * i;
+          const float* rp = first ? p1[i] : p2[i];
+          const int bytes = rp ? vb : 0;
           const float* src = bytes ? rp + k : g.Bt;  // any valid address when 0 bytes are read
-          cp_async16(a_s + tid * 128 + ((c ^ (tid & 7)) << 4), src, bytes);
+          cp_async16(a_s + r * 128 + ((c ^ (r & 7)) << 4), src, bytes);
         }
         cp_async_arrive(full + s);
         if (tid == 0) {
           mbar_expect_tx(full + s, 2 * SM::kTileB);
-          const uint32_t b_s = a_s + 2 * kTileA;
+          const uint32_t b_s = a_s + (SM::kLoTmem ? 1 : 2) * kTileA;
           tma_load_2d(b_s, &map_hi, kb * kTcBK, 0, full + s);
           tma_load_2d(b_s + SM::kTileB, &map_lo, kb * kTcBK, 0, full + s);
         }
@@ -236,6 +268,30 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- transform: A -> (trunc A, A - trunc A) ----------------
     const int t = tid - kWarpsProd * 32;
     uint32_t gk = 0;
+    if constexpr (SM::kLoTmem) {
+      // row r = this warp's TMEM lane quadrant x 32 + lane: read the (swizzled)
+      // 128-byte row, write a - trunc_tf32(a) to this stage's A_lo columns
+      const int q = warp & 3, r = q * 32 + lane;
+      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < KB; ++kb, ++gk) {
+          const int s = gk % S;
+          mbar_wait(full + s, (gk / S) & 1);
+          const uint8_t* rowp = base + s * SM::kStage + r * 128;
+          float lo[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) lo[c * 4 + j] = vv[j] - __uint_as_float(__float_as_uint(vv[j]) & 0xFFFFE000u);
+          }
+          tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + SM::kLoCol + s * kTcBK, lo);
+          fence_proxy_async();  // the cp.async-written A tile is read by the tensor core
+          tc_fence_before();
+          mbar_arrive(ready + s);
+        }
+      }
+    } else
     for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       for (int kb = 0; kb < KB; ++kb, ++gk) {
         const int s = gk % S;
@@ -312,15 +368,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait(ready + s, (gk / S) & 1);
           tc_fence_after();
           const uint32_t a_s = smem_u32(base + s * SM::kStage);
-          const uint32_t alo_s = a_s + kTileA, b_s = a_s + 2 * kTileA, blo_s = b_s + SM::kTileB;
+          const uint32_t alo_s = a_s + kTileA;
+          const uint32_t b_s = a_s + (SM::kLoTmem ? 1 : 2) * kTileA, blo_s = b_s + SM::kTileB;
 #pragma unroll
           for (int kk = 0; kk < kTcBK / 8; ++kk) {
             const uint32_t off = kk * 32;  // 8 tf32 per MMA
-            const uint64_t da = sw128_desc(a_s + off), dal = sw128_desc(alo_s + off);
+            const uint64_t da = sw128_desc(a_s + off);
             const uint64_t db = sw128_desc(b_s + off), dbl = sw128_desc(blo_s + off);
             mma_tf32(dcol, da, db, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
             mma_tf32(dcol, da, dbl, idesc, 1u);
-            mma_tf32(dcol, dal, db, idesc, 1u);
+            if constexpr (SM::kLoTmem) mma_tf32_ta(dcol, tmem + SM::kLoCol + s * kTcBK + kk * 8, db, idesc);
+            else mma_tf32(dcol, sw128_desc(alo_s + off), db, idesc, 1u);
           }
           mma_commit(empty + s);  // stage free once these MMAs retire
         }
