@@ -11,11 +11,19 @@ streams, seeds from SURVEY.md 8(d)); PE comes from the GPU precompute.
 
 One step = one query batch through ServingEngine: selection, graph
 construction and all three layers.  ``value`` times the device path with the
-request already in HBM; ``e2e`` times the public host-pointer API (pinned
+request already in HBM (every request replays the one CUDA graph captured for
+the reserved request shape); ``e2e`` times the public host-pointer API (pinned
 request H2D + D2H of the B x 128 rows inside the region).  L2 is flushed
-(512 MB write) before every timed step.  Under torchrun (N > 1) each rank
-serves its own request stream on its own GPU (replicas; CGP is DESIGN.md's
-next row) and the time is the max over ranks.
+(512 MB write) before every timed step.  A second, eager pass over the same
+requests with per-kernel CUDA events gives the roofline and kernel split.
+
+Under torchrun (N > 1) the default is independent replicas: every rank holds
+the whole graph and serves its own request stream (query batches are
+independent units, no data-path collective; weak scaling, time = max over
+ranks).  ``--parallel cgp`` runs computation-graph parallelism instead: the
+graph is hash-partitioned, every rank aggregates the part of each batch whose
+sources it owns and partials meet at the owners over NCCL (strong scaling on
+one shared batch stream) -- DESIGN.md "Multi-GPU".
 """
 
 from __future__ import annotations
@@ -229,7 +237,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--parallel", default=None, choices=["cgp", "replicas"],
-                    help="N > 1: computation-graph parallelism (default) or independent replicas")
+                    help="N > 1: independent replicas (default) or computation-graph parallelism")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -251,7 +259,7 @@ def main():
     if args.gamma is not None:
         gamma = args.gamma
     nreq = args.warmup + args.steps
-    mode = args.parallel or ("cgp" if world > 1 else "single")
+    mode = args.parallel or ("replicas" if world > 1 else "single")
     cgp = mode == "cgp" and world > 1
     serving, pool, reqs = make_inputs(cfg, rank, world, nreq, same_requests=cgp)
     model = models.make_model(kind, k, F, H)

@@ -12,17 +12,19 @@
 // B_hi / B_lo are prepared once at model load (weights are static).
 //
 // Warp-specialized persistent kernel, one CTA per SM, 128-row tiles:
-//   warps 0-3  producers: gather A k-blocks (32 fp32 = one 128-byte row per
-//              tile row) with cp.async into the canonical K-major SWIZZLE_128B
-//              layout, completion signalled on the stage's mbarrier
-//              (cp.async.mbarrier.arrive.noinc); one elected thread loads the
-//              B_hi / B_lo k-blocks with TMA (cp.async.bulk.tensor, 128B swizzle)
-//   warps 4-7  transform: rewrite the A tile in place as trunc_tf32(a) and
-//              write A_lo = a - trunc_tf32(a); their own generic-proxy writes +
-//              fence.proxy.async publish the operands to the tensor core
-//   warp 12    MMA issuer: 12 x tcgen05.mma.kind::tf32 (3 products x 4 K=8
-//              steps) per k-block into one of two TMEM accumulators,
-//              tcgen05.commit frees the stage / publishes the accumulator
+//   warps 0-3  A producers: gather A k-blocks (32 fp32 = one 128-byte row
+//              segment per tile row; 8 threads per segment, coalesced) with
+//              cp.async into the canonical K-major SWIZZLE_128B layout of an
+//              SA-deep ring, completion via cp.async.mbarrier.arrive.noinc
+//   warp 13    weight tiles: B_hi / B_lo k-blocks by TMA (cp.async.bulk.tensor,
+//              128B swizzle) into a separate, shorter SB-deep ring
+//   warps 4-7  transform: A_lo = a - trunc_tf32(a) written to TMEM with
+//              tcgen05.st (N <= 128; in place in shared memory for N = 256);
+//              the tensor core truncates the raw tile to A_hi itself
+//   warp 12    MMA issuer: 12 x tcgen05.mma.kind::tf32 (A B_hi, A B_lo from
+//              shared memory, A_lo B_hi with A from TMEM; 4 K=8 steps) per
+//              k-block into one of two TMEM accumulators; tcgen05.commit frees
+//              the A and B stages / publishes the accumulator
 //   warps 8-11 epilogue: tcgen05.ld 32x32b -> smem transpose -> coalesced
 //              addend + activation + store, overlapping the next tile's MMAs
 #include <cuda.h>
@@ -41,7 +43,7 @@ constexpr int kTcBM = 128;
 constexpr int kTcBK = 32;                  // fp32 per k-block: one 128-byte swizzle row
 constexpr int kTileA = kTcBM * kTcBK * 4;  // 16 KB
 constexpr int kWarpsProd = 4, kWarpsXf = 4, kWarpsEpi = 4;
-constexpr int kTcThreads = (kWarpsProd + kWarpsXf + kWarpsEpi + 1) * 32;  // 416
+constexpr int kTcThreads = (kWarpsProd + kWarpsXf + kWarpsEpi + 2) * 32;  // 448: + MMA warp + TMA warp
 constexpr int kMmaWarp = kWarpsProd + kWarpsXf + kWarpsEpi;               // 12
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -139,24 +141,35 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
 
 }  // namespace
 
-// Shared memory: S-stage ring of {A, A_lo, B, B_lo} + epilogue transpose tiles.
+// Shared memory: an SA-stage ring of gathered A tiles (+ A_lo when it cannot
+// live in TMEM), a separate SB-stage ring of {B_hi, B_lo} tiles, and the
+// epilogue transpose tiles.  Splitting the rings lets the A gather (HBM
+// latency, the long pole) run up to SA k-blocks ahead while the weight tiles
+// (L2-resident, shared by every CTA) only need a short ring.
+constexpr int cmin(int a, int b) { return a < b ? a : b; }
+
 template <int NP>
 struct TcSmem {
   // A_lo lives in TMEM (written by the transform warps with tcgen05.st) when the
-  // two accumulators leave room: frees 16 KB of shared memory per stage
+  // two accumulators leave room for it
   static constexpr bool kLoTmem = NP <= 128;
   static constexpr int kTileB = NP * kTcBK * 4;
-  static constexpr int kStage = (kLoTmem ? 1 : 2) * kTileA + 2 * kTileB;
+  static constexpr int kStageA = (kLoTmem ? 1 : 2) * kTileA;
+  static constexpr int kStageB = 2 * kTileB;
   static constexpr int kEpi = kWarpsEpi * 32 * 32 * 4;  // 16 KB
-  static constexpr int kFixed = kEpi + 1024 /*align*/ + 512 /*bars*/;
-  static constexpr int kFit = (227 * 1024 - kFixed) / kStage;
-  static constexpr int kStages = kFit >= 6 ? 6 : (kFit < 2 ? 2 : kFit);
-  static constexpr int kBytes = kStages * kStage + kFixed;
-  static constexpr uint32_t kAccCols = 2 * (NP < 32 ? 32 : NP);  // two accumulators
-  static constexpr uint32_t kLoCol = kAccCols;                     // then kStages x 32 A_lo columns
-  static constexpr uint32_t kNeed = kAccCols + (kLoTmem ? kStages * kTcBK : 0);
+  static constexpr int kFixed = kEpi + 1024 /*align*/ + 1024 /*bars*/;
+  static constexpr int kBudget = 227 * 1024 - kFixed;
+  static constexpr int kSB = NP >= 256 ? 2 : 3;
+  static constexpr uint32_t kAccCols = 2 * NP;  // two accumulators
+  static constexpr int kSA0 = cmin(8, cmin((kBudget - kSB * kStageB) / kStageA,
+                                           kLoTmem ? (int)((512 - kAccCols) / kTcBK) : 8));
+  static constexpr int kSA = kSA0 < 2 ? 2 : kSA0;
+  static constexpr int kBytes = kSA * kStageA + kSB * kStageB + kFixed;
+  static constexpr uint32_t kLoCol = kAccCols;  // then kSA x 32 A_lo columns
+  static constexpr uint32_t kNeed = kAccCols + (kLoTmem ? kSA * kTcBK : 0);
   static constexpr uint32_t kCols = kNeed <= 64 ? 64 : (kNeed <= 128 ? 128 : (kNeed <= 256 ? 256 : 512));
   static_assert(kNeed <= 512, "TMEM budget");
+  static_assert(kBytes <= 227 * 1024, "shared memory budget");
 };
 
 __device__ __forceinline__ void tmem_st32(uint32_t addr, const float* v) {
@@ -182,16 +195,20 @@ template <int NP>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_tc_gemm(TcGemmArgs g, const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo) {
   using SM = TcSmem<NP>;
-  constexpr int S = SM::kStages;
+  constexpr int SA = SM::kSA, SB = SM::kSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // offset (not an integer cast) keeps the pointer in the shared window -> LDS/STS
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* epi_buf = reinterpret_cast<float*>(base + S * SM::kStage);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + S * SM::kStage + SM::kEpi);
-  uint64_t* ready = full + S;
-  uint64_t* empty = ready + S;
-  uint64_t* tfull = empty + S;   // [2]
-  uint64_t* tempty = tfull + 2;  // [2]
+  uint8_t* ring_a = base;
+  uint8_t* ring_b = base + SA * SM::kStageA;
+  float* epi_buf = reinterpret_cast<float*>(ring_b + SB * SM::kStageB);
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(ring_b + SB * SM::kStageB + SM::kEpi);
+  uint64_t* ready_a = full_a + SA;
+  uint64_t* empty_a = ready_a + SA;
+  uint64_t* full_b = empty_a + SA;
+  uint64_t* empty_b = full_b + SB;
+  uint64_t* tfull = empty_b + SB;  // [2]
+  uint64_t* tempty = tfull + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -200,10 +217,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int KB1 = (g.K1 + kTcBK - 1) / kTcBK, KB2 = (g.K2 + kTcBK - 1) / kTcBK, KB = KB1 + KB2;
 
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(full + i, kWarpsProd * 32 + 1);  // cp.async arrivals + the TMA expect_tx arrival
-      mbar_init(ready + i, kWarpsXf * 32);
-      mbar_init(empty + i, 1);
+    for (int i = 0; i < SA; ++i) {
+      mbar_init(full_a + i, kWarpsProd * 32);  // cp.async arrivals
+      mbar_init(ready_a + i, kWarpsXf * 32);
+      mbar_init(empty_a + i, 1);
+    }
+    for (int i = 0; i < SB; ++i) {
+      mbar_init(full_b + i, 1);  // the TMA expect_tx arrival
+      mbar_init(empty_b + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tfull + i, 1);
@@ -222,7 +243,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < kWarpsProd) {
-    // ---------------- producers ----------------
+    // ---------------- A producers ----------------
     // thread t copies 16-byte chunk (t & 7) of rows (t >> 3) + 16 i: each warp
     // instruction moves four whole 128-byte row segments (coalesced), not 32
     // scattered 16-byte pieces
@@ -239,10 +260,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         p2[i] = (row < M && g.K2) ? g.a2 + row * g.lda2 : nullptr;
       }
       for (int kb = 0; kb < KB; ++kb, ++gk) {
-        const int s = gk % S;
-        if (gk >= (uint32_t)S) mbar_wait(empty + s, ((gk / S) - 1) & 1);
-        uint8_t* st = base + s * SM::kStage;
-        const uint32_t a_s = smem_u32(st);
+        const int s = gk % SA;
+        if (gk >= (uint32_t)SA) mbar_wait(empty_a + s, ((gk / SA) - 1) & 1);
+        const uint32_t a_s = smem_u32(ring_a + s * SM::kStageA);
         const bool first = kb < KB1;
         const int k = (first ? kb : kb - KB1) * kTcBK + c * 4;
         const int rem = (first ? g.K1 : g.K2) - k;
@@ -255,28 +275,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const float* src = bytes ? rp + k : g.Bt;  // any valid address when 0 bytes are read
           cp_async16(a_s + r * 128 + ((c ^ (r & 7)) << 4), src, bytes);
         }
-        cp_async_arrive(full + s);
-        if (tid == 0) {
-          mbar_expect_tx(full + s, 2 * SM::kTileB);
-          const uint32_t b_s = a_s + (SM::kLoTmem ? 1 : 2) * kTileA;
-          tma_load_2d(b_s, &map_hi, kb * kTcBK, 0, full + s);
-          tma_load_2d(b_s + SM::kTileB, &map_lo, kb * kTcBK, 0, full + s);
-        }
+        cp_async_arrive(full_a + s);
       }
     }
   } else if (warp < kWarpsProd + kWarpsXf) {
-    // ---------------- transform: A -> (trunc A, A - trunc A) ----------------
-    const int t = tid - kWarpsProd * 32;
+    // ---------------- transform: A_lo = a - trunc_tf32(a) ----------------
     uint32_t gk = 0;
     if constexpr (SM::kLoTmem) {
       // row r = this warp's TMEM lane quadrant x 32 + lane: read the (swizzled)
-      // 128-byte row, write a - trunc_tf32(a) to this stage's A_lo columns
+      // 128-byte row, write A_lo to this stage's TMEM columns
       const int q = warp & 3, r = q * 32 + lane;
       for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         for (int kb = 0; kb < KB; ++kb, ++gk) {
-          const int s = gk % S;
-          mbar_wait(full + s, (gk / S) & 1);
-          const uint8_t* rowp = base + s * SM::kStage + r * 128;
+          const int s = gk % SA;
+          mbar_wait(full_a + s, (gk / SA) & 1);
+          const uint8_t* rowp = ring_a + s * SM::kStageA + r * 128;
           float lo[32];
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -288,30 +301,33 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + SM::kLoCol + s * kTcBK, lo);
           fence_proxy_async();  // the cp.async-written A tile is read by the tensor core
           tc_fence_before();
-          mbar_arrive(ready + s);
+          mbar_arrive(ready_a + s);
         }
       }
-    } else
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      for (int kb = 0; kb < KB; ++kb, ++gk) {
-        const int s = gk % S;
-        mbar_wait(full + s, (gk / S) & 1);
-        float* a = reinterpret_cast<float*>(base + s * SM::kStage);
-        float* alo = a + kTcBM * kTcBK;
+    } else {
+      // in place: trunc_tf32(a) in the A tile, A_lo in the stage's second tile
+      const int t = tid - kWarpsProd * 32;
+      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < KB; ++kb, ++gk) {
+          const int s = gk % SA;
+          mbar_wait(full_a + s, (gk / SA) & 1);
+          float* a = reinterpret_cast<float*>(ring_a + s * SM::kStageA);
+          float* alo = a + kTcBM * kTcBK;
 #pragma unroll
-        for (int i = t * 4; i < kTcBM * kTcBK; i += kWarpsXf * 32 * 4) {
-          const float4 v = *reinterpret_cast<const float4*>(a + i);
-          float4 h, o;
-          h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-          o.x = v.x - h.x, o.y = v.y - h.y, o.z = v.z - h.z, o.w = v.w - h.w;
-          *reinterpret_cast<float4*>(a + i) = h;
-          *reinterpret_cast<float4*>(alo + i) = o;
+          for (int i = t * 4; i < kTcBM * kTcBK; i += kWarpsXf * 32 * 4) {
+            const float4 v = *reinterpret_cast<const float4*>(a + i);
+            float4 h, o;
+            h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+            h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+            h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+            h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+            o.x = v.x - h.x, o.y = v.y - h.y, o.z = v.z - h.z, o.w = v.w - h.w;
+            *reinterpret_cast<float4*>(a + i) = h;
+            *reinterpret_cast<float4*>(alo + i) = o;
+          }
+          fence_proxy_async();
+          mbar_arrive(ready_a + s);
         }
-        fence_proxy_async();
-        mbar_arrive(ready + s);
       }
     }
   } else if (warp < kMmaWarp) {
@@ -353,7 +369,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_before();
       mbar_arrive(tempty + acc);
     }
-  } else {
+  } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer (one elected thread) ----------------
     if (lane == 0) {
       const uint32_t idesc = tf32_idesc(NP);
@@ -364,12 +380,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tc_fence_after();
         const uint32_t dcol = tmem + acc * NP;
         for (int kb = 0; kb < KB; ++kb, ++gk) {
-          const int s = gk % S;
-          mbar_wait(ready + s, (gk / S) & 1);
+          const int sa = gk % SA, sb = gk % SB;
+          mbar_wait(ready_a + sa, (gk / SA) & 1);
+          mbar_wait(full_b + sb, (gk / SB) & 1);
           tc_fence_after();
-          const uint32_t a_s = smem_u32(base + s * SM::kStage);
-          const uint32_t alo_s = a_s + kTileA;
-          const uint32_t b_s = a_s + (SM::kLoTmem ? 1 : 2) * kTileA, blo_s = b_s + SM::kTileB;
+          const uint32_t a_s = smem_u32(ring_a + sa * SM::kStageA), alo_s = a_s + kTileA;
+          const uint32_t b_s = smem_u32(ring_b + sb * SM::kStageB), blo_s = b_s + SM::kTileB;
 #pragma unroll
           for (int kk = 0; kk < kTcBK / 8; ++kk) {
             const uint32_t off = kk * 32;  // 8 tf32 per MMA
@@ -377,12 +393,29 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const uint64_t db = sw128_desc(b_s + off), dbl = sw128_desc(blo_s + off);
             mma_tf32(dcol, da, db, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
             mma_tf32(dcol, da, dbl, idesc, 1u);
-            if constexpr (SM::kLoTmem) mma_tf32_ta(dcol, tmem + SM::kLoCol + s * kTcBK + kk * 8, db, idesc);
+            if constexpr (SM::kLoTmem) mma_tf32_ta(dcol, tmem + SM::kLoCol + sa * kTcBK + kk * 8, db, idesc);
             else mma_tf32(dcol, sw128_desc(alo_s + off), db, idesc, 1u);
           }
-          mma_commit(empty + s);  // stage free once these MMAs retire
+          mma_commit(empty_a + sa);  // stages free once these MMAs retire
+          mma_commit(empty_b + sb);
         }
         mma_commit(tfull + acc);  // accumulator complete
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- weight tiles: TMA into the B ring ----------------
+    if (lane == 0) {
+      uint32_t gk = 0;
+      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < KB; ++kb, ++gk) {
+          const int s = gk % SB;
+          if (gk >= (uint32_t)SB) mbar_wait(empty_b + s, ((gk / SB) - 1) & 1);
+          const uint32_t b_s = smem_u32(ring_b + s * SM::kStageB);
+          mbar_expect_tx(full_b + s, SM::kStageB);
+          tma_load_2d(b_s, &map_hi, kb * kTcBK, 0, full_b + s);
+          tma_load_2d(b_s + SM::kTileB, &map_lo, kb * kTcBK, 0, full_b + s);
+        }
       }
     }
     __syncwarp();
