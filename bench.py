@@ -49,7 +49,12 @@ CONFIGS = {
              "3-layer GraphSAGE-mean, Reddit-shaped 233K nodes / 103.6M edges, F=602, H=128, B=1024, SRPE ratio 0.1"),
     "cfg3": (2_400_000, 26.0, 100, "gat", 3, 128, 1024, 0.1,
              "3-layer GAT, ogbn-products-shaped 2.4M nodes / 55.9M edges, F=100, H=128, B=1024, SRPE ratio 0.1"),
+    # BASELINE configs[3]: generated on the GPUs (ob_generate_graph), partitioned by CGP; N >= 2 only
+    "cfg4": (111_059_956, 14.55, 128, "sage_mean", 3, 128, 1024, 0.1,
+             "3-layer GraphSAGE-mean, ogbn-papers100M-shaped 111M nodes / ~1.6B edges generated on the GPUs, "
+             "F=128, H=128, B=1024, SRPE ratio 0.1, CGP-partitioned"),
 }
+SYNTHETIC = {"cfg4"}  # device-generated graph + synthetic stored embeddings (never on the host)
 METRIC = "queries/s (B-query batches, p50/p99 batch latency in ms alongside)"
 
 
@@ -192,6 +197,10 @@ def run_reference(args):
 
     cfg = args.config
     n, avg, F, kind, k, H, B, gamma, desc = CONFIGS[cfg]
+    if cfg in SYNTHETIC:
+        print(json.dumps({"impl": "reference", "unavailable": f"{cfg}: the ~1.6B-edge graph exists only on the GPUs "
+                                                             "(generated per rank); the CPU port cannot hold it"}))
+        return
     serving, pool, _ = make_inputs(cfg, 0, 1, 0)
     model = models.make_model(kind, k, F, H)
     w = models.init_weights(model, 2)
@@ -259,21 +268,38 @@ def main():
     if args.gamma is not None:
         gamma = args.gamma
     nreq = args.warmup + args.steps
-    mode = args.parallel or ("replicas" if world > 1 else "single")
+    synthetic = cfg in SYNTHETIC
+    mode = args.parallel or ("cgp" if synthetic and world > 1 else ("replicas" if world > 1 else "single"))
     cgp = mode == "cgp" and world > 1
-    serving, pool, reqs = make_inputs(cfg, rank, world, nreq, same_requests=cgp)
+    if synthetic and not cgp:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": f"{cfg} needs --parallel cgp on >= 2 GPUs "
+                                                               "(one B200 cannot hold its graph + stored rows)"}))
+        return
+    if synthetic:
+        from paper_2501_08547_b200 import graphstore, workload
+
+        serving = graphstore.SyntheticGraph(n, avg, 2.1, F, seed=1)
+        pool = None
+        reqs = [workload.make_request_synthetic(n, avg, 2.1, F, B, seed=3 + i) for i in range(nreq)]
+        pe_src = graphstore.SyntheticPe([H] * (k - 1), seed=2)
+    else:
+        serving, pool, reqs = make_inputs(cfg, rank, world, nreq, same_requests=cgp)
+        pe_src = None
     model = models.make_model(kind, k, F, H)
     w = models.init_weights(model, 2)
     stream = torch.cuda.Stream(device=local)
     t0 = time.time()
     if cgp:
         scfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=gamma, num_partitions=world, seed=0, device=local)
-        eng = runtime.distributed_engine(serving, None, model, w, scfg, stream=stream.cuda_stream)
+        eng = runtime.distributed_engine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream)
     else:
         scfg = runtime.ServeConfig(strategy="srpe", gamma=gamma, device=local)
-        eng = runtime.ServingEngine(serving, None, model, w, scfg, stream=stream.cuda_stream)
-    eng.precompute_pe()
-    log(f"[bench] rank {rank}: engine loaded + GPU PE precompute in {time.time() - t0:.1f}s")
+        eng = runtime.ServingEngine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream)
+    if not synthetic:
+        eng.precompute_pe()
+    info = eng.graph_info()
+    log(f"[bench] rank {rank}: engine loaded in {time.time() - t0:.1f}s ({info})")
     lib = eng._lib
     max_m = max(r.edges.shape[0] for r in reqs)
     from paper_2501_08547_b200 import _native as nat
@@ -294,7 +320,8 @@ def main():
             step(i)
     stream.synchronize()
     # correctness guard on a warm request: errors surface here, not silently
-    eng.serve_device(B, d_q[0].data_ptr(), d_edges[0].shape[0], d_edges[0].data_ptr(), d_out.data_ptr(), sync=True)
+    bd0 = eng.serve_device(B, d_q[0].data_ptr(), d_edges[0].shape[0], d_edges[0].data_ptr(), d_out.data_ptr(),
+                           sync=True)
 
     def timed_pass(profile):
         """K requests, L2 flushed before each, device events around each request."""
@@ -376,7 +403,10 @@ def main():
                "p50_ms": float(np.percentile(e2e_ms, 50)), "p99_ms": float(np.percentile(e2e_ms, 99))}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if synthetic:
+        cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "port",
+               "sample": f"none: the {cfg} graph exists only on the GPUs; see the cfg2 line for the CPU baseline"}
+    elif rank == 0 and world == 1 and not args.no_cpu:
         pe_host = [eng.read_pe(l) for l in range(1, k)]
         qps, nr, cl = cpu_sample(serving, pe_host, model, w, pool, cfg, budget_s=12.0, batch=args.ref_batch)
         cpu = {"value": round(qps, 3), "unit": "queries/s", "cores": 1, "kind": "port",
@@ -401,13 +431,19 @@ def main():
                    "parallelism": (f"cgp x{world} (NCCL over NVLink)" if cgp else
                                    (f"replicas x{world}" if world > 1 else "single")),
                    "l2": "flushed (512 MB write) before every timed step",
-                   "inputs": "reference generator (bit-identical numpy streams), PE from GPU precompute"},
+                   "inputs": ("device generator (ob_generate_graph: the reference degree law, not its numpy "
+                              "stream), synthetic N(0,1) stored embeddings, host-drawn request batches")
+                   if synthetic else "reference generator (bit-identical numpy streams), PE from GPU precompute",
+                   "graph": info},
         "roofline": roof,
         "eager_ms_per_step": round(float(lat_eager.mean()), 4),
         "kernels_ms_per_step": {"agg": round(agg["ms"] / args.steps, 4), "gemm": round(gemm["ms"] / args.steps, 4),
                                 "finalize": round(fin["ms"] / args.steps, 4)},
         "gemm_tflops": round(gemm["flops"] / (gemm["ms"] / 1e3) / 1e12, 2) if gemm["ms"] > 0 else None,
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
+        "request": {"edges": int(reqs[0].edges.shape[0]), "candidates": int(bd0.num_candidates),
+                    "targets": int(bd0.num_targets), "fetch_bytes": int(bd0.fetch_bytes),
+                    "nvlink_bytes_per_step": int(bd0.collective_bytes) if cgp else 0},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

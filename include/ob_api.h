@@ -113,6 +113,27 @@ int ob_load_graph(ob_engine* e, int64_t num_nodes, const int64_t* in_offsets,
                   const int64_t* in_neighbors, int64_t num_edges, const float* features,
                   int32_t feature_dim);
 
+/* Device-generated synthetic graph (the power law of
+ * workload.py:119-168, drawn on the GPU -- not the numpy stream): N nodes,
+ * average in-degree avg_degree, degree exponent, F-wide N(0,1) features.  An
+ * NCCL-mode CGP engine builds only its rank's share (source-split CSR, owned
+ * feature rows); other engines build the whole in-CSR.  Replaces
+ * ob_load_graph for graphs that cannot exist on the host. */
+int ob_generate_graph(ob_engine* e, int64_t num_nodes, double avg_degree, double exponent,
+                      int32_t feature_dim, uint64_t seed);
+/* Synthetic N(0,1) stored embeddings for layer `layer` (rows this engine stores). */
+int ob_generate_pe(ob_engine* e, int32_t layer, int32_t dim, uint64_t seed);
+/* Sizes of the loaded graph: global nodes/edges, rows and edges held here. */
+int ob_graph_info(ob_engine* e, int64_t* num_nodes, int64_t* num_edges, int64_t* local_rows,
+                  int64_t* local_edges);
+/* Copy out the whole in-CSR (partition < 0) or partition p's source-split CSR,
+ * plus the global in-degrees; any pointer may be NULL. */
+int ob_graph_csr(ob_engine* e, int32_t partition, int64_t* offsets, int64_t* neighbors,
+                 int32_t* in_degree);
+/* Copy out rows of the feature table (table 0) or stored layer `table` for
+ * global ids; OB_ENOTFOUND for rows another rank stores. */
+int ob_read_rows(ob_engine* e, int32_t table, int64_t n, const int64_t* ids, float* out);
+
 /* Stored embeddings for layer `layer` (1-based), N x dim float32. */
 int ob_load_pe(ob_engine* e, int32_t layer, const float* rows, int64_t num_rows, int32_t dim);
 

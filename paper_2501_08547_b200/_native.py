@@ -73,6 +73,11 @@ _SIGS = {
     "ob_engine_destroy": (C.c_int, [_P]),
     "ob_load_graph": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int64, _P, C.c_int32]),
     "ob_load_pe": (C.c_int, [_P, C.c_int32, _P, C.c_int64, C.c_int32]),
+    "ob_generate_graph": (C.c_int, [_P, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_uint64]),
+    "ob_generate_pe": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_uint64]),
+    "ob_graph_info": (C.c_int, [_P, _I64P, _I64P, _I64P, _I64P]),
+    "ob_graph_csr": (C.c_int, [_P, C.c_int32, _P, _P, _P]),
+    "ob_read_rows": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P]),
     "ob_load_model": (C.c_int, [_P, C.c_int32, C.POINTER(ObLayer), C.POINTER(C.c_void_p)]),
     "ob_precompute_pe": (C.c_int, [_P]),
     "ob_read_pe": (C.c_int, [_P, C.c_int32, _P]),

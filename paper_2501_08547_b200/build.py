@@ -21,7 +21,7 @@ OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libomega_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["ob_select.cu", "ob_build.cu", "ob_layers.cu", "ob_gemm.cu", "ob_cgp.cu", "ob_prof.cu", "ob_api.cu"]
+SOURCES = ["ob_select.cu", "ob_build.cu", "ob_layers.cu", "ob_gemm.cu", "ob_cgp.cu", "ob_gen.cu", "ob_prof.cu", "ob_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]

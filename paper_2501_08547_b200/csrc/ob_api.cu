@@ -37,6 +37,7 @@ Engine::~Engine() {
 // sum of the r largest in-degrees: bound on the CSR edges r destinations can pull
 static int64_t topdeg(const GraphDev& g, int64_t r) {
   if (g.topdeg_prefix.empty()) return g.E;
+  if (r >= (int64_t)g.topdeg_prefix.size() - 1 && (int64_t)g.topdeg_prefix.size() - 1 < g.N) return g.E;
   r = std::max<int64_t>(0, std::min<int64_t>(r, (int64_t)g.topdeg_prefix.size() - 1));
   return g.topdeg_prefix[r];
 }
@@ -353,6 +354,7 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   check_ready(e);
   OB_CHECK(B >= 0 && m >= 0, OB_EINVAL, "negative request size");
   OB_CHECK(e.g.N + B < ((int64_t)1 << 31) - 1, OB_EINVAL, "id space exceeds int32");
+  cgp_localize_storage(e);  // NCCL CGP: keep only the owned rows (no-op otherwise)
   cudaStream_t s = e.stream;
   prepare_workspace(e, B, std::max(bucket_m(m), e.m_reserved));
   RequestWs& w = e.ws;
@@ -674,6 +676,98 @@ int ob_load_graph(ob_engine* h, int64_t N, const int64_t* off, const int64_t* nb
   });
 }
 
+int ob_generate_graph(ob_engine* h, int64_t N, double avg_degree, double exponent, int32_t F, uint64_t seed) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    generate_graph(h->impl, N, avg_degree, exponent, F, seed);
+  });
+}
+
+int ob_generate_pe(ob_engine* h, int32_t layer, int32_t dim, uint64_t seed) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    generate_pe(h->impl, layer, dim, seed);
+  });
+}
+
+int ob_graph_info(ob_engine* h, int64_t* num_nodes, int64_t* num_edges, int64_t* local_rows, int64_t* local_edges) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    const Engine& e = h->impl;
+    if (num_nodes) *num_nodes = e.g.N;
+    if (num_edges) *num_edges = e.g.E;
+    if (local_rows) *local_rows = e.g.pos ? e.g.N_local : e.g.N;
+    if (local_edges) {
+      int64_t le = 0;
+      if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP && e.cgp.nccl)
+        for (const auto& p : e.cgp.parts) le += p.E;
+      else
+        le = e.g.E;
+      *local_edges = le;
+    }
+  });
+}
+
+int ob_graph_csr(ob_engine* h, int32_t partition, int64_t* offsets, int64_t* nbrs, int32_t* indeg) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    const int64_t N = e.g.N;
+    OB_CHECK(N > 0, OB_ESTATE, "no graph loaded");
+    const int64_t* off = e.g.offsets;
+    const int32_t* nb = e.g.nbrs;
+    int64_t E = e.g.E;
+    if (partition >= 0) {
+      const PartitionDev* p = nullptr;
+      for (const auto& q : e.cgp.parts)
+        if (q.rank == partition) p = &q;
+      OB_CHECK(p, OB_EINVAL, "partition not held by this engine");
+      off = p->off;
+      nb = p->src;
+      E = p->E;
+    }
+    OB_CHECK(off, OB_ESTATE, "the whole in-CSR is not held by this engine");
+    if (offsets) OB_CUDA(cudaMemcpy(offsets, off, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost));
+    if (nbrs && E) {
+      std::vector<int32_t> t((size_t)E);
+      OB_CUDA(cudaMemcpy(t.data(), nb, sizeof(int32_t) * E, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < E; ++i) nbrs[i] = t[i];
+    }
+    if (indeg) OB_CUDA(cudaMemcpy(indeg, e.g.indeg, sizeof(int32_t) * N, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ob_read_rows(ob_engine* h, int32_t table, int64_t n, const int64_t* ids, float* out) {
+  return guarded([&] {
+    OB_CHECK(h && (n == 0 || (ids && out)), OB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(table >= 0 && table <= (int)e.pe.size(), OB_EINVAL, "table: 0 = features, l = stored layer l");
+    const float* base = table == 0 ? e.g.feats : e.pe[table - 1];
+    const int w = table == 0 ? e.g.F : e.pe_dim[table - 1];
+    OB_CHECK(base, OB_EINVAL, "table not loaded");
+    std::vector<int32_t> pos;
+    if (e.g.pos) {
+      pos.resize((size_t)e.g.N);
+      OB_CUDA(cudaMemcpy(pos.data(), e.g.pos, sizeof(int32_t) * e.g.N, cudaMemcpyDeviceToHost));
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      OB_CHECK(ids[i] >= 0 && ids[i] < e.g.N, OB_EINVAL, "row id out of range");
+      const int64_t r = e.g.pos ? pos[ids[i]] : ids[i];
+      OB_CHECK(r >= 0, OB_ENOTFOUND, "row not stored on this rank");
+      OB_CUDA(cudaMemcpy(out + i * w, base + r * ld4(w), sizeof(float) * w, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
 int ob_load_pe(ob_engine* h, int32_t layer, const float* rows, int64_t n, int32_t dim) {
   return guarded([&] {
     OB_CHECK(h, OB_EINVAL, "null engine");
@@ -688,13 +782,16 @@ int ob_load_pe(ob_engine* h, int32_t layer, const float* rows, int64_t n, int32_
       e.pe.resize(layer, nullptr);
       e.pe_dim.resize(layer, 0);
     }
+    OB_CHECK(!e.g.generated || !e.g.pos, OB_ESTATE, "partitioned generated graph: use ob_generate_pe");
     const int ld = ld4(dim);
     float* d = (float*)e.dalloc(sizeof(float) * n * ld);
     OB_CUDA(cudaMemset(d, 0, sizeof(float) * n * ld));
     OB_CUDA(cudaMemcpy2D(d, sizeof(float) * ld, rows, sizeof(float) * dim, sizeof(float) * dim, n,
                          cudaMemcpyHostToDevice));
+    e.dfree(e.pe[layer - 1]);
     e.pe[layer - 1] = d;
     e.pe_dim[layer - 1] = dim;
+    if (e.localized) localize_table(e, e.pe[layer - 1], ld);  // keep the owned rows only
   });
 }
 
@@ -714,6 +811,8 @@ int ob_precompute_pe(ob_engine* h) {
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
     OB_CHECK(!h->impl.layers.empty(), OB_ESTATE, "load a model first");
     OB_CHECK(h->impl.layers[0].spec.in_dim == h->impl.g.F, OB_EINVAL, "input width does not match layer in_dim");
+    OB_CHECK(h->impl.g.offsets && !h->impl.g.pos, OB_ESTATE,
+             "precompute needs the whole graph on this device (partitioned engines: precompute before serving)");
     stage_precompute(h->impl);
     OB_CUDA(cudaGetLastError());
   });
@@ -727,6 +826,7 @@ int ob_read_pe(ob_engine* h, int32_t layer, float* out) {
     OB_CUDA(cudaSetDevice(e.cfg.device));
     OB_CHECK(layer >= 1 && layer <= (int)e.pe.size() && e.pe[layer - 1], OB_EINVAL,
              "no stored embeddings for that layer");
+    OB_CHECK(!e.g.pos, OB_ESTATE, "stored embeddings are partitioned across ranks on this engine");
     const int dim = e.pe_dim[layer - 1];
     OB_CUDA(cudaMemcpy2D(out, sizeof(float) * dim, e.pe[layer - 1], sizeof(float) * ld4(dim), sizeof(float) * dim,
                          e.g.N, cudaMemcpyDeviceToHost));
@@ -895,6 +995,7 @@ int ob_reserve(ob_engine* h, int32_t B, int64_t m) {
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
     check_ready(e);
+    cgp_localize_storage(e);
     e.m_reserved = bucket_m(m);
     prepare_workspace(e, B, e.m_reserved);
     const int H = e.layers.back().spec.out_dim;

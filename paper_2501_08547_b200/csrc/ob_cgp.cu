@@ -40,7 +40,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
   return z ^ (z >> 31);
 }
 
-__global__ void k_owner(int64_t N, int P, uint64_t seed, int32_t* owner) {
+__global__ void k_owner(int64_t N, int P, uint64_t seed, int32_t* owner) {  // declared in ob_engine.h
   const uint64_t key = mix64(seed);
   OB_GRID_STRIDE(v, N) owner[v] = (int32_t)(mix64((uint64_t)v ^ key) % (uint64_t)P);
 }
@@ -113,6 +113,81 @@ void cgp_build_partitions(Engine& e) {
   OB_CUDA(cudaStreamSynchronize(s));
 }
 
+__global__ void k_flag_owned(int64_t N, const int32_t* owner, int rank, int32_t* flag) {
+  OB_GRID_STRIDE(v, N) flag[v] = owner[v] == rank;
+}
+__global__ void k_pos_owned(int64_t N, const int32_t* owner, int rank, const int64_t* excl, int32_t* pos) {
+  OB_GRID_STRIDE(v, N) pos[v] = owner[v] == rank ? (int32_t)excl[v] : -1;
+}
+__global__ void k_gather_owned(int64_t N, int64_t ld, const int32_t* __restrict__ pos, const float* __restrict__ full,
+                               float* local) {
+  const int64_t n = N * ld;
+  OB_GRID_STRIDE(i, n) {
+    const int64_t v = i / ld;
+    const int32_t p = pos[v];
+    if (p >= 0) local[(int64_t)p * ld + (i - v * ld)] = full[i];
+  }
+}
+
+// owned-row map of this rank: pos[v] = local row of v, -1 when another rank owns it
+void owned_positions(Engine& e) {
+  CgpState& c = e.cgp;
+  cudaStream_t s = e.stream;
+  const int64_t N = e.g.N;
+  int32_t* flag = (int32_t*)e.dalloc(sizeof(int32_t) * N);
+  int64_t* excl = (int64_t*)e.dalloc(sizeof(int64_t) * (N + 1));
+  ScanScratch sc;
+  sc.cap = ScanScratch::bytes_for(N, 1);
+  sc.pool = (char*)e.dalloc(sc.cap);
+  OB_CUDA(cudaMemsetAsync(sc.pool, 0, sc.cap, s));
+  k_flag_owned<<<grid_for(N, 256), 256, 0, s>>>(N, c.owner, c.my_rank, flag);
+  device_scan(s, sc, LoadI32{flag}, StoreI64{excl}, nullptr, N, N, nullptr, excl);
+  e.g.pos = (int32_t*)e.dalloc(sizeof(int32_t) * N);
+  k_pos_owned<<<grid_for(N, 256), 256, 0, s>>>(N, c.owner, c.my_rank, excl, e.g.pos);
+  g_launches += 2;
+  OB_CUDA(cudaMemcpyAsync(&e.g.N_local, excl + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  OB_CUDA(cudaStreamSynchronize(s));
+  e.dfree(flag);
+  e.dfree(excl);
+  e.dfree(sc.pool);
+}
+
+// replace a full (N x ld) row table by this rank's owned rows (g.pos order)
+void localize_table(Engine& e, float*& table, int64_t ld) {
+  if (!table) return;
+  cudaStream_t s = e.stream;
+  const int64_t N = e.g.N;
+  float* local = (float*)e.dalloc(sizeof(float) * std::max<int64_t>(e.g.N_local, 1) * ld);
+  k_gather_owned<<<grid_for(N * ld, 256), 256, 0, s>>>(N, ld, e.g.pos, table, local);
+  OB_LAUNCHED();
+  OB_CUDA(cudaStreamSynchronize(s));
+  e.dfree(table);
+  table = local;
+}
+
+// NCCL-mode CGP: every rank keeps only the feature and stored-embedding rows of
+// the nodes it owns (graphstore.py:233-262); aggregation sources are always
+// owned (source-split edges) and destinations are updated by their owner, so
+// no request ever needs another rank's rows.  The full in-CSR is dropped too
+// (the rank's source-split CSR replaces it).
+void cgp_localize_storage(Engine& e) {
+  if (e.localized || !e.cgp.nccl || e.cfg.strategy != OB_STRATEGY_SRPE_CGP) return;
+  cudaStream_t s = e.stream;
+  const int64_t N = e.g.N;
+  if (!e.g.pos) owned_positions(e);
+  (void)s;
+  (void)N;
+  if (!e.g.generated) {
+    localize_table(e, e.g.feats, e.g.F_ld);
+    for (size_t l = 0; l < e.pe.size(); ++l) localize_table(e, e.pe[l], ld4(e.pe_dim[l]));
+    e.dfree(e.g.offsets);
+    e.dfree(e.g.nbrs);
+    e.g.offsets = nullptr;
+    e.g.nbrs = nullptr;
+  }
+  e.localized = true;
+}
+
 // request slice of partition r: edges whose source it owns (queries: round robin)
 __global__ void k_filter_slice(const ReqParams* rp, int64_t N, int P, int r, const int32_t* __restrict__ owner,
                                const ReqCounters* rc, int64_t* out, int64_t* count) {
@@ -140,7 +215,8 @@ __global__ void k_filter_slice(const ReqParams* rp, int64_t N, int P, int r, con
 
 // destination rows h_v for a layer (dst-indexed); non-owned rows read a zero row
 __global__ void k_dst_rows(const int32_t* __restrict__ dst_ids, const int64_t* D_dev, int64_t N, int layer, int k,
-                           const float* feats, const float* qpad, int64_t F_ld, const float* prev, int64_t in_ld,
+                           const int32_t* pos, const float* feats, const float* qpad, int64_t F_ld,
+                           const float* prev, int64_t in_ld,
                            const int64_t* T_dev, const int32_t* owner, int P, int rank, const float* zero,
                            const float** hvp) {
   const int64_t D = *D_dev, T = *T_dev;
@@ -150,7 +226,7 @@ __global__ void k_dst_rows(const int32_t* __restrict__ dst_ids, const int64_t* D
     if (owner) mine = (g >= N ? (int)((g - N) % P) : owner[g]) == rank;
     const float* r;
     if (!mine) r = zero;
-    else if (layer == 1) r = g < N ? feats + g * F_ld : qpad + (g - N) * F_ld;
+    else if (layer == 1) r = g < N ? feats + (pos ? (int64_t)pos[g] : g) * F_ld : qpad + (g - N) * F_ld;
     else if (layer == k) r = prev + (T + (g - N)) * in_ld;  // last block: queries in the mid table
     else r = prev + i * in_ld;                              // mid blocks share one destination list
     hvp[i] = r;
@@ -323,7 +399,7 @@ void serve_cgp(Engine& e, float* d_out) {
     const int64_t pstride = mom ? 2 * part_stride_f : part_stride_f;
     BindCtx bc = bind_ctx(e, w, l);
     // destination rows h_v (owned ones; zero row elsewhere under NCCL)
-    k_dst_rows<<<grid_for(D_max, 256), 256, 0, s>>>(b0.dst_ids, D_dev, N, l, k, e.g.feats, w.qpad, e.g.F_ld,
+    k_dst_rows<<<grid_for(D_max, 256), 256, 0, s>>>(b0.dst_ids, D_dev, N, l, k, e.g.pos, e.g.feats, w.qpad, e.g.F_ld,
                                                     l > 1 ? w.outs[l - 1] : nullptr, ld4(L.spec.in_dim), &w.rc->T,
                                                     c.nccl ? c.owner : nullptr, c.P, c.my_rank, c.zero_row, c.hvp);
     OB_LAUNCHED();

@@ -129,8 +129,14 @@ struct GraphDev {
   int64_t* offsets = nullptr;
   int32_t* nbrs = nullptr;
   int32_t* indeg = nullptr;
-  float* feats = nullptr;   // N x F_ld
-  std::vector<int64_t> topdeg_prefix;  // host: prefix sums of in-degrees sorted descending
+  float* feats = nullptr;   // N x F_ld (or N_local x F_ld with pos)
+  // CGP with partitioned storage: stored rows (features, PE) are the rank's
+  // owned nodes only; pos maps a global id to its local row (-1: not stored).
+  // Null: every row is stored at its global index.
+  int32_t* pos = nullptr;
+  int64_t N_local = 0;
+  bool generated = false;   // built by the device generator (no host copy)
+  std::vector<int64_t> topdeg_prefix;  // host: prefix sums of the largest in-degrees (descending)
 };
 
 void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max);
@@ -314,7 +320,8 @@ struct BindCtx {
   int layer;            // 1-based
   int64_t N;
   int64_t F_ld;
-  const float* feats;   // N x F_ld
+  const int32_t* pos;   // global -> stored row (null: identity)
+  const float* feats;   // stored rows x F_ld
   const float* qfeat;   // B x F_ld
   const float* pe;      // stored layer (layer-1) rows, N x in_ld
   const float* prev;    // previous layer output, rows x in_ld
@@ -485,6 +492,22 @@ struct CgpState {
 };
 
 void cgp_build_partitions(Engine& e);
+// NCCL-mode CGP on a host-loaded graph: keep only this rank's feature / PE rows
+// (called before the first request; precompute must come first)
+void cgp_localize_storage(Engine& e);
+void owned_positions(Engine& e);
+void localize_table(Engine& e, float*& table, int64_t ld);  // g.pos / g.N_local from cgp.owner and cgp.my_rank
+
+// device generator (ob_gen.cu)
+struct GenLaw {
+  int64_t N;
+  double s, inv1ms, c1, E, H;
+  uint64_t seed, a, b;
+};
+GenLaw make_law(int64_t N, double avg, double exponent, uint64_t seed, cudaStream_t s, double* d_acc);
+void generate_graph(Engine& e, int64_t N, double avg, double exponent, int F, uint64_t seed);
+void generate_pe(Engine& e, int layer, int dim, uint64_t seed);
+__global__ void k_owner(int64_t N, int P, uint64_t seed, int32_t* owner);
 void carve_cgp(Engine& e, RequestWs& w, Arena& a);
 void serve_cgp(Engine& e, float* d_out);
 void cgp_destroy(Engine& e);
@@ -546,6 +569,17 @@ struct Engine {
     owned.push_back(p);
     return p;
   }
+  void dfree(void* p) {
+    if (!p) return;
+    for (auto& q : owned)
+      if (q == p) {
+        cudaFree(q);
+        q = owned.back();
+        owned.pop_back();
+        return;
+      }
+  }
+  bool localized = false;  // NCCL-mode CGP storage reduced to the owned rows
   ~Engine();
 };
 

@@ -47,7 +47,7 @@ __device__ __forceinline__ int bind_row(const BindCtx& c, int64_t T, int64_t s, 
                                         int* pe_layer) {
   *pe_layer = 0;
   if (c.layer == 1) {
-    *row = g < c.N ? c.feats + g * c.F_ld : c.qfeat + (g - c.N) * c.F_ld;
+    *row = g < c.N ? c.feats + (c.pos ? (int64_t)c.pos[g] : g) * c.F_ld : c.qfeat + (g - c.N) * c.F_ld;
     return 0;  // FEATURE
   }
   if (c.mode == 1) {
@@ -65,7 +65,7 @@ __device__ __forceinline__ int bind_row(const BindCtx& c, int64_t T, int64_t s, 
       return 2;
     }
   }
-  *row = c.pe + g * c.in_ld;
+  *row = c.pe + (c.pos ? (int64_t)c.pos[g] : g) * c.in_ld;
   *pe_layer = c.layer - 1;
   return 1;  // PE
 }
@@ -918,6 +918,7 @@ BindCtx bind_ctx(Engine& e, RequestWs& w, int l) {
   c.layer = l;
   c.N = e.g.N;
   c.F_ld = e.g.F_ld;
+  c.pos = e.g.pos;
   c.feats = e.g.feats;
   c.qfeat = w.qpad;
   c.pe = (!full && l > 1) ? e.pe[l - 2] : nullptr;

@@ -87,6 +87,36 @@ def export_edges(dataset: GraphDataset) -> np.ndarray:
     return np.stack([dataset.in_neighbors, dst], axis=1)
 
 
+@dataclass
+class SyntheticGraph:
+    """A power-law graph generated on the device.
+
+    Same degree law as ``workload.gen_powerlaw_graph`` (workload.py:119-168) but
+    drawn by ``ob_generate_graph`` on the GPU, so papers-scale graphs never exist
+    on the host; it is *not* the reference's numpy stream.  Under NCCL-mode CGP
+    each rank generates only its own share (source-split CSR + owned rows).
+    """
+
+    num_nodes: int
+    avg_degree: float
+    exponent: float
+    feature_dim: int
+    seed: int = 1
+
+
+@dataclass
+class SyntheticPe:
+    """N(0, 1) stored embeddings generated on the device for layers 1..k-1 (bench inputs only:
+    the serving kernels are data-independent; parity uses precomputed PEs)."""
+
+    dims: list
+    seed: int = 2
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.dims)
+
+
 class PeStore:
     """Per-layer stored embeddings for layers 1..k-1 (graphstore.py:122-171)."""
 

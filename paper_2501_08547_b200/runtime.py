@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as nat
 from .compgraph import ComputationBlock, ComputationGraph, ServingRequest
-from .graphstore import GraphDataset, PeStore
+from .graphstore import GraphDataset, PeStore, SyntheticGraph, SyntheticPe
 from .models import ModelSpec, Weights, weight_matrix_names
 
 STRATEGIES = ("full", "sampled", "srpe", "srpe-cgp")
@@ -146,11 +146,16 @@ class ServingEngine:
 
     # -- loading ---------------------------------------------------------------
     def _load(self, ds, pe, model, weights):
-        off = np.ascontiguousarray(ds.in_offsets, dtype=np.int64)
-        nb = np.ascontiguousarray(ds.in_neighbors, dtype=np.int64)
-        feats = _f32(ds.features)
-        nat.check(self._lib.ob_load_graph(self._h, int(ds.num_nodes), nat.ptr(off), nat.ptr(nb), int(nb.shape[0]),
-                                          nat.ptr(feats), int(feats.shape[1])))
+        if isinstance(ds, SyntheticGraph):
+            nat.check(self._lib.ob_generate_graph(self._h, int(ds.num_nodes), float(ds.avg_degree),
+                                                  float(ds.exponent), int(ds.feature_dim),
+                                                  int(ds.seed) & 0xFFFFFFFFFFFFFFFF))
+        else:
+            off = np.ascontiguousarray(ds.in_offsets, dtype=np.int64)
+            nb = np.ascontiguousarray(ds.in_neighbors, dtype=np.int64)
+            feats = _f32(ds.features)
+            nat.check(self._lib.ob_load_graph(self._h, int(ds.num_nodes), nat.ptr(off), nat.ptr(nb),
+                                              int(nb.shape[0]), nat.ptr(feats), int(feats.shape[1])))
         layers = (nat.ObLayer * model.k)()
         mats = []
         for i, spec in enumerate(model.layers):
@@ -159,7 +164,10 @@ class ServingEngine:
                 mats.append(_f32(weights.layers[i][name]))
         arr = (C.c_void_p * len(mats))(*[m.ctypes.data for m in mats])
         nat.check(self._lib.ob_load_model(self._h, model.k, layers, arr))
-        if pe is not None:
+        if isinstance(pe, SyntheticPe):
+            for l, dim in enumerate(pe.dims, start=1):
+                nat.check(self._lib.ob_generate_pe(self._h, l, int(dim), int(pe.seed) + l))
+        elif pe is not None:
             if getattr(pe, "node_ids", None) is not None:
                 raise ValueError("the engine needs a whole-graph stored-embedding store")
             for l in range(1, pe.num_layers + 1):
@@ -253,6 +261,36 @@ class ServingEngine:
         """PartitionMap.owner of a CGP engine (graphstore.py:177-181)."""
         out = np.empty(self.dataset.num_nodes, np.int64)
         nat.check(self._lib.ob_partition_owner(self._h, nat.ptr(out)))
+        return out
+
+    def graph_info(self) -> dict:
+        """Global nodes/edges and the rows/edges this engine holds (partitioned under NCCL CGP)."""
+        v = [C.c_int64() for _ in range(4)]
+        nat.check(self._lib.ob_graph_info(self._h, *[C.byref(x) for x in v]))
+        return dict(num_nodes=v[0].value, num_edges=v[1].value, local_rows=v[2].value, local_edges=v[3].value)
+
+    def graph_csr(self, partition: int = -1) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """(offsets, neighbours, in-degrees) of the held in-CSR or of one partition's source-split CSR."""
+        info = self.graph_info()
+        n = info["num_nodes"]
+        if partition < 0:
+            ne = info["num_edges"]
+        else:
+            off = np.empty(n + 1, np.int64)
+            nat.check(self._lib.ob_graph_csr(self._h, partition, nat.ptr(off), None, None))
+            ne = int(off[-1])
+        off = np.empty(n + 1, np.int64)
+        nb = np.empty(ne, np.int64)
+        deg = np.empty(n, np.int32)
+        nat.check(self._lib.ob_graph_csr(self._h, partition, nat.ptr(off), nat.ptr(nb), nat.ptr(deg)))
+        return off, nb, deg
+
+    def read_rows(self, table: int, ids) -> np.ndarray:
+        """Rows of the feature table (0) or stored layer ``table`` for global ids held here."""
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        w = self.dataset.feature_dim if table == 0 else self.model.layers[table - 1].out_dim
+        out = np.empty((len(ids), w), np.float32)
+        nat.check(self._lib.ob_read_rows(self._h, table, len(ids), nat.ptr(ids), nat.ptr(out)))
         return out
 
     def launch_count(self) -> int:

@@ -8,9 +8,11 @@ requests are bit-identical to the reference's for the same seeds
 change is speed: CSR construction sorts one combined key instead of a
 two-key lexsort, and the hold-out split reuses the already-sorted CSR order.
 
-``gen_powerlaw_graph_gpu`` draws the same degree law on the GPU for
-configurations too large for the host generator (SURVEY.md 8(d) configs 2-4);
-it is *not* bit-identical to the numpy stream and says so in its output.
+For graphs too large for the host, the engine
+generates the graph on the device from a ``graphstore.SyntheticGraph``
+descriptor (``ob_generate_graph``: same degree law, Zipf-rank sampling, *not*
+the numpy stream); ``make_request_synthetic`` draws query batches against such
+a graph from the same law on the host.
 """
 
 from __future__ import annotations
@@ -129,3 +131,39 @@ def make_request(pool: HoldoutPool, serving_graph: GraphDataset, batch_size: int
     d = np.where(qid[b] >= 0, qid[b], b)
     edges = np.concatenate([np.stack([s, d], axis=1), np.stack([d, s], axis=1)])
     return ServingRequest(base, batch_size, pool.features[np.searchsorted(pool.ids, selected)], edges)
+
+
+def _zipf_norm(n: int, s: float) -> float:
+    """sum_{r=1..n} r^-s in float64 (chunked), the generator's normaliser."""
+    tot = 0.0
+    step = 1 << 24
+    for a in range(1, n + 1, step):
+        r = np.arange(a, min(n, a + step - 1) + 1, dtype=np.float64)
+        tot += float(np.sum(r ** -s))
+    return tot
+
+
+def make_request_synthetic(num_nodes: int, avg_degree: float, exponent: float, feature_dim: int,
+                           batch_size: int, seed: int) -> ServingRequest:
+    """A query batch against a device-generated graph (ob_generate_graph's law).
+
+    Each query is a new node (ids N..N+B-1, like a re-attached hold-out node in
+    make_request, workload.py:78-116) whose degree is drawn from the in-degree
+    law and whose neighbours are drawn by popularity rank; every incident edge
+    is added in both directions, as the reference does.
+    """
+    n = int(num_nodes)
+    s = 1.0 / (exponent - 1.0)
+    c1 = (n + 1.0) ** (1.0 - s) - 1.0
+    E = avg_degree * n
+    H = _zipf_norm(n, s)
+    rng = np.random.default_rng(seed)
+    # incident edges of a held-out node: one in-degree and one out-degree draw
+    r = rng.integers(0, n, size=(2, batch_size)).astype(np.float64)
+    deg = np.clip(np.floor(E * (r + 1.0) ** -s / H + 0.5), 1, n - 1).astype(np.int64).sum(axis=0)
+    q = np.repeat(np.arange(batch_size, dtype=np.int64), deg) + n
+    x = rng.random(int(deg.sum()))
+    u = np.clip(np.floor((1.0 + x * c1) ** (1.0 / (1.0 - s))).astype(np.int64) - 1, 0, n - 1)
+    edges = np.concatenate([np.stack([u, q], axis=1), np.stack([q, u], axis=1)])
+    feats = rng.standard_normal((batch_size, feature_dim)).astype(np.float32)
+    return ServingRequest(n, batch_size, feats, edges)

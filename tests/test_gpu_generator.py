@@ -1,0 +1,107 @@
+"""Device graph generator (ob_generate_graph) -- needs a B200.
+
+The generator is not the reference's numpy stream, so parity here is against
+the oracle run on the generated graph itself (CSR, features and PE read back
+from the device): structure bit-exact, embeddings within 1e-4.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def _engine(strategy, P=1, N=6000, avg=8.0, F=16, H=8, k=3, kind="sage_mean", gamma=0.3, seed=5, pe="precompute"):
+    from paper_2501_08547_b200 import graphstore, models, runtime
+
+    ds = graphstore.SyntheticGraph(N, avg, 2.1, F, seed=seed)
+    model = models.make_model(kind, k, F, H)
+    w = models.init_weights(model, 3)
+    cfg = runtime.ServeConfig(strategy=strategy, gamma=gamma, num_partitions=P, seed=11)
+    store = graphstore.SyntheticPe([H] * (k - 1), seed=9) if pe == "synthetic" else None
+    eng = runtime.ServingEngine(ds, store, model, w, cfg)
+    if pe == "precompute":
+        eng.precompute_pe()
+    return eng, ds, model, w
+
+
+def test_generated_csr_is_a_valid_sorted_in_csr():
+    eng, ds, _, _ = _engine("srpe")
+    off, nb, deg = eng.graph_csr()
+    info = eng.graph_info()
+    assert info["num_nodes"] == ds.num_nodes and info["num_edges"] == len(nb) == off[-1]
+    assert np.array_equal(np.diff(off), deg)
+    assert nb.min() >= 0 and nb.max() < ds.num_nodes
+    for v in range(ds.num_nodes):  # rows ascending: the (dst, src) edge order
+        row = nb[off[v]:off[v + 1]]
+        assert np.all(row[1:] >= row[:-1])
+    assert abs(len(nb) / ds.num_nodes - 8.0) < 2.0  # the requested average degree (rounding aside)
+    # heavy-tailed in- and out-degrees
+    assert deg.max() > 20 * np.median(deg)
+    outd = np.bincount(nb, minlength=ds.num_nodes)
+    assert outd.max() > 20 * max(1, np.median(outd))
+    # deterministic in the seed
+    eng2, _, _, _ = _engine("srpe")
+    o2, n2, d2 = eng2.graph_csr()
+    assert np.array_equal(off, o2) and np.array_equal(nb, n2)
+    f1 = eng.read_rows(0, np.arange(50))
+    assert np.array_equal(f1, eng2.read_rows(0, np.arange(50)))
+    assert abs(float(eng.read_rows(0, np.arange(ds.num_nodes)).std()) - 1.0) < 0.05
+    eng.close()
+    eng2.close()
+
+
+@pytest.mark.parametrize("strategy", ["srpe", "full"])
+def test_generated_graph_serving_matches_oracle(strategy):
+    from oracle import layers as OL
+    from paper_2501_08547_b200 import workload
+
+    eng, ds, model, w = _engine(strategy)
+    off, nb, _ = eng.graph_csr()
+    feats = eng.read_rows(0, np.arange(ds.num_nodes))
+    layers = [dict(kind=s.kind, in_dim=s.in_dim, out_dim=s.out_dim) for s in model.layers]
+    pe = OL.precompute(layers, w.layers, off, nb, feats)
+    for l in range(1, model.k):
+        assert OL.max_rel_err(eng.read_pe(l), pe[l - 1]) <= TOL
+    req = workload.make_request_synthetic(ds.num_nodes, ds.avg_degree, ds.exponent, ds.feature_dim, 48, seed=4)
+    emb, bd = eng.serve(req)
+    ref = OL.serve(strategy, layers, w.layers, ds.num_nodes, 48, off, nb, feats, req.query_features, req.edges,
+                   pe_layers=[eng.read_pe(l) for l in range(1, model.k)], gamma=0.3)
+    assert OL.max_rel_err(emb, ref["emb"]) <= TOL
+    assert bd.fetch_bytes == ref["fetch_bytes"]
+    for l, rb in enumerate(ref["blocks"], start=1):
+        gb = eng.last_block(l)
+        for f in ("src_ids", "dst_ids", "edge_src", "edge_dst", "bind_kind", "src_degree"):
+            assert np.array_equal(np.asarray(getattr(gb, f), np.int64), np.asarray(getattr(rb, f), np.int64)), (l, f)
+    eng.close()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_generated_graph_cgp_emulation_matches_centralized(P):
+    from paper_2501_08547_b200 import workload
+
+    cen, ds, _, _ = _engine("srpe", pe="synthetic")
+    cgp, _, _, _ = _engine("srpe-cgp", P=P, pe="synthetic")
+    req = workload.make_request_synthetic(ds.num_nodes, ds.avg_degree, ds.exponent, ds.feature_dim, 64, seed=8)
+    a, _ = cen.serve(req)
+    b, _ = cgp.serve(req)
+    from oracle.layers import max_rel_err
+
+    assert max_rel_err(b, a) <= TOL
+    # the P source-split CSRs partition the whole in-CSR
+    off, nb, _ = cen.graph_csr()
+    owner = cgp.partition_owner()
+    tot = 0
+    for r in range(P):
+        po, pn, _ = cgp.graph_csr(partition=r)
+        tot += len(pn)
+        assert np.all(owner[pn] == r)
+        for v in (0, 1, int(np.argmax(np.diff(off)))):
+            want = nb[off[v]:off[v + 1]]
+            assert np.array_equal(pn[po[v]:po[v + 1]], want[owner[want] == r])
+    assert tot == len(nb)
+    cen.close()
+    cgp.close()
