@@ -301,10 +301,14 @@ def main():
     info = eng.graph_info()
     log(f"[bench] rank {rank}: engine loaded in {time.time() - t0:.1f}s ({info})")
     lib = eng._lib
-    max_m = max(r.edges.shape[0] for r in reqs)
+    ms = np.array([r.edges.shape[0] for r in reqs])
     from paper_2501_08547_b200 import _native as nat
 
-    nat.check(lib.ob_reserve(eng._h, B, max_m))
+    # plan requests at the p90 edge count (one captured graph serves them); larger ones take
+    # their own bucket's graph, captured during warm-up below
+    nat.check(lib.ob_reserve(eng._h, B, int(np.percentile(ms, 90))))
+    above = sorted(set(int(np.argmax(ms == v)) for v in np.unique(ms) if v > np.percentile(ms, 90)),
+                   key=lambda i: -ms[i])
     dev = torch.device("cuda", local)
     d_edges = [torch.from_numpy(r.edges).to(dev) for r in reqs]
     d_q = [torch.from_numpy(r.query_features).to(dev) for r in reqs]
@@ -316,6 +320,8 @@ def main():
         eng.serve_device(B, d_q[i].data_ptr(), d_edges[i].shape[0], d_edges[i].data_ptr(), d_out.data_ptr())
 
     with torch.cuda.stream(stream):
+        for i in above:  # largest first: the arena reaches its final size before any capture we keep
+            step(i)  # capture the graphs of the above-bound buckets outside the timed region
         for i in range(args.warmup):
             step(i)
     stream.synchronize()
@@ -357,6 +363,8 @@ def main():
     gemm = _read_prof(lib, eng, nat, 1)
     fin = _read_prof(lib, eng, nat, 2)
     reqp = _read_prof(lib, eng, nat, 6)
+    st = {name: _read_prof(lib, eng, nat, cls) for name, cls in
+          (("select", 4), ("request_csr", 7), ("build", 3), ("resolve", 5), ("collectives", 8))}
     nat.check(lib.ob_profile(eng._h, 0))
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -375,9 +383,10 @@ def main():
 
         e2e_ms = []
         h2d = d2h = 0
-        bd = nat.ObBreakdown()  # first host-path call captures its graph (output buffer differs)
-        nat.check(lib.ob_serve(eng._h, B, C.c_void_p(pin_q[0].data_ptr()), pin_e[0].shape[0],
-                               C.c_void_p(pin_e[0].data_ptr()), C.c_void_p(out_h.data_ptr()), C.byref(bd)))
+        bd = nat.ObBreakdown()  # host-path calls capture their own graphs (output buffer differs)
+        for i in above + [0]:
+            nat.check(lib.ob_serve(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
+                                   C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(out_h.data_ptr()), C.byref(bd)))
         for j in range(args.steps):
             i = args.warmup + j
             flush.fill_(j & 0xFF)
@@ -438,7 +447,8 @@ def main():
         "roofline": roof,
         "eager_ms_per_step": round(float(lat_eager.mean()), 4),
         "kernels_ms_per_step": {"agg": round(agg["ms"] / args.steps, 4), "gemm": round(gemm["ms"] / args.steps, 4),
-                                "finalize": round(fin["ms"] / args.steps, 4)},
+                                "finalize": round(fin["ms"] / args.steps, 4),
+                                **{name: round(st[name]["ms"] / args.steps, 4) for name in st}},
         "gemm_tflops": round(gemm["flops"] / (gemm["ms"] / 1e3) / 1e12, 2) if gemm["ms"] > 0 else None,
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
         "request": {"edges": int(reqs[0].edges.shape[0]), "candidates": int(bd0.num_candidates),

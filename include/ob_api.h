@@ -179,7 +179,8 @@ int ob_reserve(ob_engine* e, int32_t num_queries, int64_t num_edges);
  * (aggregation: 4*E + 4*w*S + 4*pw*items; finalize: partials in + rows out;
  * gemm: operands + result) and flops (gemm). */
 enum ob_prof_class { OB_PROF_AGG = 0, OB_PROF_GEMM = 1, OB_PROF_FINALIZE = 2, OB_PROF_BUILD = 3,
-                     OB_PROF_SELECT = 4, OB_PROF_RESOLVE = 5, OB_PROF_REQUEST = 6 };
+                     OB_PROF_SELECT = 4, OB_PROF_RESOLVE = 5, OB_PROF_REQUEST = 6, OB_PROF_CSR = 7,
+                     OB_PROF_COMM = 8 };
 int ob_profile(ob_engine* e, int32_t enable);
 /* Request graphs: by default each (B, edge-count bucket) request shape is
  * captured once into a CUDA graph and replayed (the request itself is read

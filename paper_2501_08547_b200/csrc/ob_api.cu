@@ -298,11 +298,17 @@ static void enqueue_stages(Engine& e, float* d_out) {
     serve_cgp(e, d_out);  // marks ev[1] between build and layers
     return;
   }
+  cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, srpe);
   if (srpe) stage_select(e, w);
+  prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
+  p0 = prof_begin(s);
   stage_request_csr(e, w);
+  prof_end(s, p0, kProfCsr, nullptr, 0, 0, 0, 0, 0);
+  p0 = prof_begin(s);
   if (srpe) stage_build_srpe(e, w);
   else stage_build_full(e, w);
+  prof_end(s, p0, kProfBuild, nullptr, 0, 0, 0, 0, 0);
   record_mark(e.ev[1], s);
   stage_forward(e, w, d_out);
 }

@@ -347,8 +347,10 @@ void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
 static void allreduce(Engine& e, void* buf, size_t count, bool is_double, bool max) {
 #ifdef OB_WITH_NCCL
   CgpState& c = e.cgp;
+  cudaEvent_t p0 = prof_begin(e.stream);
   OB_NCCL(ncclAllReduce(buf, buf, count, is_double ? ncclDouble : ncclFloat, max ? ncclMax : ncclSum,
                         (ncclComm_t)c.comm, e.stream));
+  prof_end(e.stream, p0, kProfComm, nullptr, 0, 0, 0, 0, 0);
   c.collective_bytes += (int64_t)(2.0 * (c.P - 1) / c.P * count * (is_double ? 8 : 4));
 #else
   (void)e, (void)buf, (void)count, (void)is_double, (void)max;
@@ -365,8 +367,11 @@ void serve_cgp(Engine& e, float* d_out) {
   const int64_t N = e.g.N;
   c.collective_bytes = 0;
   // identical plan on every rank from the whole request (runtime.py:151-192)
+  cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, true);
   stage_select(e, w);
+  prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
+  p0 = prof_begin(s);
   for (int p = 0; p < np; ++p) {
     CgpPartWs& pw = c.ws[p];
     const PartitionDev& part = c.parts[p];
@@ -385,6 +390,7 @@ void serve_cgp(Engine& e, float* d_out) {
     write_query_dst(e, w, pw.blocks[1]);
     assemble(e, w, pw.blocks[1], src);
   }
+  prof_end(s, p0, kProfBuild, nullptr, 0, 0, 0, 0, 0);
   record_mark(e.ev[1], s);
   stage_qpad(e, w);
   OB_CUDA(cudaMemsetAsync(c.zero_row, 0, sizeof(float) * (ld4(std::max(e.g.F, 4)) + 512), s));

@@ -12,7 +12,10 @@
 #include <stdint.h>
 
 #include <cub/block/block_reduce.cuh>
+#include <cub/block/block_exchange.cuh>
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <type_traits>
 #include <stdexcept>
 #include <string>
 
@@ -125,15 +128,25 @@ struct ScanTiles {
   T* incl;
 };
 
-template <class T, class Load, class Store, class Total>
+template <class T, int ITEMS, class Load, class Store, class Total>
 __global__ void __launch_bounds__(kScanThreads) k_scan(Load load, Store store, Total total, const int64_t* n_dev,
                                                        int64_t n_host, ScanTiles<T> st) {
   using BS = cub::BlockScan<T, kScanThreads>;
-  __shared__ typename BS::TempStorage tmp;
+  using BX = cub::BlockExchange<T, kScanThreads, ITEMS>;
+  // 8-byte values move warp-striped (coalesced loads and stores) and are
+  // transposed to the blocked order the scan needs through shared memory
+  constexpr bool kStriped = sizeof(T) == 8;
+  struct NoExchange {};
+  using XT = typename std::conditional<kStriped, typename BX::TempStorage, NoExchange>::type;
+  constexpr int64_t kTile = (int64_t)kScanThreads * ITEMS;
+  __shared__ union {
+    typename BS::TempStorage scan;
+    XT ex;
+  } tmp;
   __shared__ int64_t s_tile;
   __shared__ T s_prefix;
   const int64_t n = dev_count(n_dev, n_host);
-  const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  const int64_t ntiles = (n + kTile - 1) / kTile;
   const int lane = threadIdx.x & 31;
   if (n <= 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) total(0, T(0));
@@ -144,12 +157,22 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Load load, Store store, T
     __syncthreads();
     const int64_t t = s_tile;
     if (t >= ntiles) break;
-    const int64_t base = t * kScanTile + (int64_t)threadIdx.x * kScanItems;  // blocked arrangement
-    T v[kScanItems];
+    T v[ITEMS];
+    if constexpr (kStriped) {
 #pragma unroll
-    for (int i = 0; i < kScanItems; ++i) v[i] = (base + i < n) ? T(load(base + i)) : T(0);
+      for (int i = 0; i < ITEMS; ++i) {
+        const int64_t idx = t * kTile + (int64_t)i * kScanThreads + threadIdx.x;
+        v[i] = idx < n ? T(load(idx)) : T(0);
+      }
+      BX(tmp.ex).StripedToBlocked(v);
+      __syncthreads();
+    } else {
+      const int64_t base = t * kTile + (int64_t)threadIdx.x * ITEMS;  // blocked arrangement
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) v[i] = (base + i < n) ? T(load(base + i)) : T(0);
+    }
     T agg;
-    BS(tmp).ExclusiveSum(v, v, agg);
+    BS(tmp.scan).ExclusiveSum(v, v, agg);
     if (threadIdx.x < 32) {
       T excl(0);
       volatile int* vf = st.flag;
@@ -193,8 +216,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Load load, Store store, T
     __syncthreads();
     const T off = s_prefix;
 #pragma unroll
-    for (int i = 0; i < kScanItems; ++i)
-      if (base + i < n) store(base + i, v[i] + off);
+    for (int i = 0; i < ITEMS; ++i) v[i] = v[i] + off;
+    if constexpr (kStriped) {
+      BX(tmp.ex).BlockedToStriped(v);
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int64_t idx = t * kTile + (int64_t)i * kScanThreads + threadIdx.x;
+        if (idx < n) store(idx, v[i]);
+      }
+    } else {
+      const int64_t base = t * kTile + (int64_t)threadIdx.x * ITEMS;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (base + i < n) store(base + i, v[i]);
+    }
     if (t == ntiles - 1 && threadIdx.x == 0) total(n, off + agg);
     __syncthreads();  // s_tile / s_prefix / tmp are reused by the next tile
   }
@@ -242,13 +277,90 @@ struct TotalI64 {
   }
 };
 
+// Reduce-then-scan variant for very long inputs (bitmaps over 10^8 ids): with
+// thousands of 4096-element tiles the single-pass look-back chain, not
+// bandwidth, sets the time; three bandwidth-bound passes are shorter.
+template <class Load>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Load load, const int64_t* n_dev, int64_t n_host,
+                                                              int64_t* tile_sums) {
+  using BR = cub::BlockReduce<int64_t, kScanThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int64_t v = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      const int64_t idx = t * kScanTile + (int64_t)i * kScanThreads + threadIdx.x;
+      if (idx < n) v += load(idx);
+    }
+    const int64_t r = BR(tmp).Sum(v);
+    if (threadIdx.x == 0) tile_sums[t] = r;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_spine(const int64_t* n_dev, int64_t n_host, int64_t* tile_sums);
+
+template <class Load, class Store, class Total>
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(Load load, Store store, Total total,
+                                                            const int64_t* n_dev, int64_t n_host,
+                                                            const int64_t* tile_off) {
+  using BS = cub::BlockScan<int64_t, kScanThreads>;
+  using BX = cub::BlockExchange<int64_t, kScanThreads, kScanItems>;
+  __shared__ union {
+    typename BS::TempStorage scan;
+    typename BX::TempStorage ex;
+  } tmp;
+  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  if (n <= 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) total(0, 0);
+    return;
+  }
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int64_t v[kScanItems];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      const int64_t idx = t * kScanTile + (int64_t)i * kScanThreads + threadIdx.x;
+      v[i] = idx < n ? (int64_t)load(idx) : 0;
+    }
+    BX(tmp.ex).StripedToBlocked(v);
+    __syncthreads();
+    int64_t agg;
+    BS(tmp.scan).ExclusiveSum(v, v, agg);
+    const int64_t off = tile_off[t];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) v[i] += off;
+    __syncthreads();
+    BX(tmp.ex).BlockedToStriped(v);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      const int64_t idx = t * kScanTile + (int64_t)i * kScanThreads + threadIdx.x;
+      if (idx < n) store(idx, v[i]);
+    }
+    if (t == ntiles - 1 && threadIdx.x == 0) total(n, off + agg);
+    __syncthreads();
+  }
+}
+
 template <class T, class Load, class Store, class Total>
 void device_scan_t(cudaStream_t s, ScanScratch& sc, Load load, Store store, Total total, const int64_t* n_dev,
                    int64_t n_host, int64_t max_n) {
   ScanTiles<T> st = sc.take<T>(max_n);
-  int64_t tiles = (max_n + kScanTile - 1) / kScanTile;
+  const int64_t tiles = (max_n + kScanTile - 1) / kScanTile;
   const int g = grid_for(tiles < 1 ? 1 : tiles, 1, kNumSMs * 2);
-  k_scan<T><<<g, kScanThreads, 0, s>>>(load, store, total, n_dev, n_host, st);
+  if constexpr (std::is_same<T, int64_t>::value) {
+    if (tiles > 4 * kNumSMs) {  // long input: reduce, spine, downsweep
+      int64_t* sums = reinterpret_cast<int64_t*>(st.agg);
+      k_scan_reduce<<<g, kScanThreads, 0, s>>>(load, n_dev, n_host, sums);
+      k_scan_spine<<<1, 1024, 0, s>>>(n_dev, n_host, sums);
+      k_scan_down<<<g, kScanThreads, 0, s>>>(load, store, total, n_dev, n_host, sums);
+      g_launches += 3;
+      return;
+    }
+  }
+  k_scan<T, kScanItems><<<g, kScanThreads, 0, s>>>(load, store, total, n_dev, n_host, st);
   ++g_launches;
 }
 

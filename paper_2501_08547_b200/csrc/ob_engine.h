@@ -283,7 +283,7 @@ struct RequestWs {
 // in-library kernel profiler (CUDA events on the launching stream) -------------
 // Used by bench.py to time the dominant kernel live inside the timed region.
 enum ProfClass { kProfAgg = 0, kProfGemm = 1, kProfFinalize = 2, kProfBuild = 3, kProfSelect = 4,
-                 kProfResolve = 5, kProfRequest = 6, kProfClasses = 7 };
+                 kProfResolve = 5, kProfRequest = 6, kProfCsr = 7, kProfComm = 8, kProfClasses = 9 };
 
 struct ProfRec {
   int cls;

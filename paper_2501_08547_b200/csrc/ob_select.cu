@@ -24,6 +24,26 @@ namespace ob {
 
 int64_t g_launches = 0;
 
+// exclusive scan of the tile sums in place (one CTA; long scans only)
+__global__ void __launch_bounds__(1024) k_scan_spine(const int64_t* n_dev, int64_t n_host, int64_t* tile_sums) {
+  using BS = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int64_t carry;
+  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b = 0; b < ntiles; b += 1024) {
+    const int64_t i = b + threadIdx.x;
+    int64_t v = i < ntiles ? tile_sums[i] : 0, agg;
+    BS(tmp).ExclusiveSum(v, v, agg);
+    if (i < ntiles) tile_sums[i] = v + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+}
+
 __global__ void k_fill_i32(int32_t* a, const int64_t* n_dev, int64_t n_host, int32_t v) {
   const int64_t n = dev_count(n_dev, n_host);
   OB_GRID_STRIDE(i, n) a[i] = v;
