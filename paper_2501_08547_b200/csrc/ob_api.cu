@@ -220,7 +220,10 @@ static void prepare_workspace(Engine& e, int B, int64_t m) {
   }
   e.arena.used = 0;
   carve(e, w, p, e.arena);
-  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) carve_cgp(e, w, e.arena);
+  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) {
+    carve_cgp(e, w, e.arena);
+    cgp_ensure_exchange(e);  // NCCL mode: NVLink exchange buffers for this plan
+  }
 }
 
 static void check_ready(Engine& e) {
@@ -241,6 +244,7 @@ static void raise_request_errors(const ReqCounters& rc) {
   if (rc.err & kErrNoQuery) throw Error(OB_EINVAL, "every request edge needs a query endpoint");
   if (rc.err & kErrNonFinite) throw Error(OB_EINVAL, "query features must be finite");
   if (rc.err & kErrZeroTotal) throw Error(OB_EINVAL, "candidate with zero total degree");
+  if (rc.err & kErrComm) throw Error(OB_ECOMM, "CGP exchange: a peer rank did not signal within 2 s");
 }
 
 // fetch-byte accounting per layer (graph_fetch_bytes, runtime.py:105-120)

@@ -23,6 +23,7 @@
 //   * emulation (nccl_id == NULL, P > 1): all P partitions run on this device and
 //     the merge walks the P partials in ascending rank order (cgpexec.py:189-240).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "ob_engine.h"
@@ -334,6 +335,13 @@ void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
   c.lmax = a.take<float>(c.D_max);
   c.mean = mom ? a.take<double>(c.D_max * ld4(maxw)) : nullptr;
   c.fin = a.take<float>((int64_t)w.B * e.layers.back().spec.out_dim + 4);
+  // exchange region: the largest single-step payload (partials + counts, s_dst,
+  // moments means, final query rows)
+  const int64_t esz = mom ? 8 : 4;
+  const size_t parts_b = (((size_t)c.D_max * c.ldp * esz + 255) & ~(size_t)255) + (size_t)c.D_max * 4;
+  const size_t mean_b = mom ? (size_t)c.D_max * ld4(maxw) * 8 : 0;
+  const size_t fin_b = (size_t)w.B * e.layers.back().spec.out_dim * 4;
+  c.x_need_region = (std::max(std::max(parts_b, mean_b), std::max(fin_b, (size_t)c.D_max * 4)) + 4095) & ~(size_t)4095;
 }
 
 #ifdef OB_WITH_NCCL
@@ -343,6 +351,107 @@ void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
     if (_r != ncclSuccess) throw Error(OB_ECOMM, std::string(#x) + ": " + ncclGetErrorString(_r)); \
   } while (0)
 #endif
+
+// ---------------------------------------------------------------------------
+// NVLink exchange over CUDA-IPC-mapped peer buffers (NCCL mode)
+//
+// Buffer of rank r: ready[p] (int64, written by rank p when its step-k data is
+// in p's region), done[p] (written by rank p when it has read r's step-k data),
+// then one region per exchange step of a request.  One step:
+//   x_begin    wait until every peer finished reading the previous step
+//   producer   kernels write this rank's region (local stores)
+//   x_publish  fence; bump the device step counter k; ready[me] = k at every peer
+//   x_wait     spin until ready[p] >= k for every peer (acquire, system scope)
+//   consumer   kernels read peers' regions with ld.global.cg over NVLink
+//   x_done     done[me] = k at every peer
+// The step counter lives on the device, so a replayed CUDA graph keeps
+// counting; spins give up after ~2 s and raise OB_ECOMM instead of hanging.
+// ---------------------------------------------------------------------------
+struct XCtx {
+  char* peer[kMaxParts];
+  int P, rank;
+  int64_t* ep;
+  int64_t* err;     // the request's error word (kErrComm on a flag timeout)
+};
+constexpr size_t kXFlags = 256;  // ready[8] @0, done[8] @64
+
+__device__ __forceinline__ int64_t ld_acq_sys(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_sys(int64_t* p, int64_t v) {
+  asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void spin_geq(const int64_t* f, int64_t k, int64_t* err) {
+  const long long t0 = clock64();
+  while (ld_acq_sys(f) < k) {
+    if (clock64() - t0 > (1ll << 32)) {  // ~2 s at 1.9 GHz: a peer is gone
+      atomicOr((unsigned long long*)err, (unsigned long long)kErrComm);
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+
+__global__ void k_x_begin(XCtx x) {  // peers done with the previous step
+  const int q = threadIdx.x;
+  if (q >= x.P || q == x.rank) return;
+  const int64_t k = *x.ep;
+  if (k > 0) spin_geq(reinterpret_cast<const int64_t*>(x.peer[x.rank] + 64) + q, k, x.err);
+}
+__global__ void k_x_publish(XCtx x) {
+  __threadfence_system();
+  const int64_t k = *x.ep + 1;
+  __syncthreads();
+  if (threadIdx.x == 0) *x.ep = k;
+  const int q = threadIdx.x;
+  if (q < x.P && q != x.rank) st_rel_sys(reinterpret_cast<int64_t*>(x.peer[q]) + x.rank, k);
+}
+__global__ void k_x_wait(XCtx x) {
+  const int p = threadIdx.x;
+  if (p >= x.P || p == x.rank) return;
+  spin_geq(reinterpret_cast<const int64_t*>(x.peer[x.rank]) + p, *x.ep, x.err);
+}
+__global__ void k_x_done(XCtx x) {
+  const int q = threadIdx.x;
+  if (q < x.P && q != x.rank)
+    st_rel_sys(reinterpret_cast<int64_t*>(x.peer[q] + 64) + x.rank, *x.ep);
+}
+
+// rows[i] of destination i from its owner's copy (s_dst, moments means, final rows)
+__global__ void k_x_gather_rows(XCtx x, size_t off, const int32_t* dst_ids, const int64_t* D_dev, int64_t D_fixed,
+                                int64_t N, const int32_t* owner, int esize, int64_t width_el, float* out) {
+  const int64_t D = D_dev ? *D_dev : D_fixed;
+  const int64_t words = width_el * esize / 4;  // 4-byte words per row
+  const int64_t n = D * words;
+  OB_GRID_STRIDE(t, n) {
+    const int64_t i = t / words;
+    const int64_t g = dst_ids ? (int64_t)dst_ids[i] : N + i;
+    const int o = g >= N ? (int)((g - N) % x.P) : owner[g];
+    const float* src = reinterpret_cast<const float*>(x.peer[o] + kXFlags + off);
+    out[t] = __ldcg(src + t);
+  }
+}
+
+static XCtx xctx(Engine& e) {
+  CgpState& c = e.cgp;
+  XCtx x{};
+  for (int p = 0; p < c.P; ++p) x.peer[p] = c.xpeer[p];
+  x.P = c.P;
+  x.rank = c.my_rank;
+  x.ep = c.xep;
+  x.err = &e.ws.rc->err;
+  return x;
+}
+static void x_launch(cudaStream_t s, void (*kern)(XCtx), const XCtx& x) {
+  kern<<<1, 32, 0, s>>>(x);
+  OB_LAUNCHED();
+}
+
+// offset (from the region base past the flags) of step j's region
+static size_t xoff(const CgpState& c, int j) { return (size_t)j * c.xregion; }
+static char* xregion_ptr(const CgpState& c, int j) { return c.xbuf + kXFlags + xoff(c, j); }
 
 static void allreduce(Engine& e, void* buf, size_t count, bool is_double, bool max) {
 #ifdef OB_WITH_NCCL
@@ -395,6 +504,28 @@ void serve_cgp(Engine& e, float* d_out) {
   stage_qpad(e, w);
   OB_CUDA(cudaMemsetAsync(c.zero_row, 0, sizeof(float) * (ld4(std::max(e.g.F, 4)) + 512), s));
   const int64_t part_stride_f = c.D_max * c.ldp;  // floats between partitions (x2 for float64 partials)
+  const bool p2p = c.nccl && c.p2p;
+  const XCtx x = p2p ? xctx(e) : XCtx{};
+  int xj = 0;  // exchange step within this request (selects the region)
+  c.nvlink_bytes = 0;
+  OwnerFilter own{};
+  if (p2p) {
+    own.owner = c.owner;
+    own.N = N;
+    own.P = c.P;
+    own.rank = c.my_rank;
+  }
+  auto x_begin = [&] { x_launch(s, k_x_begin, x); };
+  auto x_exchange = [&] {  // publish this rank's region, wait for everyone's
+    cudaEvent_t pc = prof_begin(s);
+    x_launch(s, k_x_publish, x);
+    x_launch(s, k_x_wait, x);
+    prof_end(s, pc, kProfComm, nullptr, 0, 0, 0, 0, 0);
+  };
+  auto x_done = [&] {
+    x_launch(s, k_x_done, x);
+    ++xj;
+  };
   for (int l = 1; l <= k; ++l) {
     const LayerDev& L = e.layers[l - 1];
     const int bi = l < k ? 0 : 1;
@@ -404,18 +535,41 @@ void serve_cgp(Engine& e, float* d_out) {
     const bool mom = L.spec.kind == OB_KIND_MOMENTS;
     const int64_t pstride = mom ? 2 * part_stride_f : part_stride_f;
     BindCtx bc = bind_ctx(e, w, l);
+    own.dst_ids = b0.dst_ids;
     // destination rows h_v (owned ones; zero row elsewhere under NCCL)
     k_dst_rows<<<grid_for(D_max, 256), 256, 0, s>>>(b0.dst_ids, D_dev, N, l, k, e.g.pos, e.g.feats, w.qpad, e.g.F_ld,
                                                     l > 1 ? w.outs[l - 1] : nullptr, ld4(L.spec.in_dim), &w.rc->T,
                                                     c.nccl ? c.owner : nullptr, c.P, c.my_rank, c.zero_row, c.hvp);
     OB_LAUNCHED();
     if (L.spec.kind == OB_KIND_GAT) {  // s_dst = h_v . (W a_dst), computed by the owner
-      k_rowdot_ptr<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.hvp, L.spec.in_dim, L.wa_dst, c.sdst);
-      OB_LAUNCHED();
-      if (c.nccl) allreduce(e, c.sdst, D_max, false, false);
+      if (p2p) {
+        x_begin();
+        float* reg = reinterpret_cast<float*>(xregion_ptr(c, xj));
+        k_rowdot_ptr<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.hvp, L.spec.in_dim, L.wa_dst, reg);
+        OB_LAUNCHED();
+        x_exchange();
+        k_x_gather_rows<<<grid_for(D_max, 256), 256, 0, s>>>(x, xoff(c, xj), b0.dst_ids, D_dev, 0, N, c.owner, 4, 1,
+                                                             c.sdst);
+        OB_LAUNCHED();
+        x_done();
+        c.nvlink_bytes += (int64_t)(D_max * 4 * (c.P - 1) / c.P);
+      } else {
+        k_rowdot_ptr<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.hvp, L.spec.in_dim, L.wa_dst, c.sdst);
+        OB_LAUNCHED();
+        if (c.nccl) allreduce(e, c.sdst, D_max, false, false);
+      }
     }
     const int phases = mom ? 2 : 1;
     for (int ph = 1; ph <= phases; ++ph) {
+      // this rank's raw partials: into its exchange region (p2p) or the arena
+      float* lp0 = c.lp;
+      float* cnt0 = c.lcnt;
+      if (p2p) {
+        x_begin();
+        char* reg = xregion_ptr(c, xj);
+        lp0 = reinterpret_cast<float*>(reg);
+        cnt0 = reinterpret_cast<float*>(reg + (((size_t)c.D_max * c.ldp * (mom ? 8 : 4) + 255) & ~(size_t)255));
+      }
       for (int p = 0; p < np; ++p) {
         const BlockDev& b = c.ws[p].blocks[bi];
         launch_resolve(s, bc, b.cnt, b.S_max, b.src_ids, w.rowp, w.gscale);
@@ -436,43 +590,159 @@ void serve_cgp(Engine& e, float* d_out) {
         r.gscale = w.gscale;
         r.group_ptr = b.group_ptr;
         LayerScratch sc{w.partial, w.partial2, w.agg, w.mean, w.z, w.s_src, w.s_dst};
-        cgp_local_partial(s, L, r, sc, c.sdst, c.lp + p * pstride, c.ldp, c.lcnt + p * c.D_max, ph, c.mean);
+        cgp_local_partial(s, L, r, sc, c.sdst, lp0 + p * pstride, c.ldp, cnt0 + p * c.D_max, ph, c.mean);
       }
+      PartPtrs pp{};
       int Pm = np;
-      if (c.nccl) {
-        const int64_t pw = cgp_partial_width(L);
-        if (L.spec.kind == OB_KIND_GAT) {
-          k_sm_extract<<<grid_for(D_max, 256), 256, 0, s>>>(D_dev, c.lp, c.ldp, c.lmax);
-          OB_LAUNCHED();
-          allreduce(e, c.lmax, D_max, false, true);
-          k_sm_rescale<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.lp, c.ldp, (int)pw - 2, c.lmax);
-          OB_LAUNCHED();
-          allreduce(e, c.lp, D_max * c.ldp, false, false);
-          k_sm_restore<<<grid_for(D_max, 256), 256, 0, s>>>(D_dev, c.lp, c.ldp, c.lmax);
-          OB_LAUNCHED();
-        } else if (L.spec.kind == OB_KIND_SAGE_MAX) {
-          allreduce(e, c.lp, D_max * c.ldp, false, true);  // empty partials hold -inf
-        } else {
-          allreduce(e, c.lp, D_max * c.ldp, mom, false);
+      const size_t cnt_off = (((size_t)c.D_max * c.ldp * (mom ? 8 : 4) + 255) & ~(size_t)255);
+      if (p2p) {
+        x_exchange();
+        Pm = c.P;
+        for (int q = 0; q < c.P; ++q) {  // every rank's partials, read in place over NVLink
+          const char* reg = c.xpeer[q] + kXFlags + xoff(c, xj);
+          pp.lp[q] = reinterpret_cast<const float*>(reg);
+          pp.cnt[q] = reinterpret_cast<const float*>(reg + cnt_off);
         }
-        allreduce(e, c.lcnt, D_max, false, false);
-        Pm = 1;
+        c.nvlink_bytes += (int64_t)((double)D_max / c.P * (c.P - 1) * ((double)cgp_partial_width(L) * (mom ? 8 : 4) + 4));
+      } else {
+        if (c.nccl) {
+          const int64_t pw = cgp_partial_width(L);
+          if (L.spec.kind == OB_KIND_GAT) {
+            k_sm_extract<<<grid_for(D_max, 256), 256, 0, s>>>(D_dev, c.lp, c.ldp, c.lmax);
+            OB_LAUNCHED();
+            allreduce(e, c.lmax, D_max, false, true);
+            k_sm_rescale<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.lp, c.ldp, (int)pw - 2, c.lmax);
+            OB_LAUNCHED();
+            allreduce(e, c.lp, D_max * c.ldp, false, false);
+            k_sm_restore<<<grid_for(D_max, 256), 256, 0, s>>>(D_dev, c.lp, c.ldp, c.lmax);
+            OB_LAUNCHED();
+          } else if (L.spec.kind == OB_KIND_SAGE_MAX) {
+            allreduce(e, c.lp, D_max * c.ldp, false, true);  // empty partials hold -inf
+          } else {
+            allreduce(e, c.lp, D_max * c.ldp, mom, false);
+          }
+          allreduce(e, c.lcnt, D_max, false, false);
+          Pm = 1;
+        }
+        for (int q = 0; q < Pm; ++q) {
+          pp.lp[q] = c.lp + q * pstride;
+          pp.cnt[q] = c.lcnt + q * c.D_max;
+        }
       }
       const bool last = l == k;
       float* out = last ? (c.nccl ? c.fin : d_out) : w.outs[l];
       const int64_t ldo = last ? L.spec.out_dim : ld4(L.spec.out_dim);
-      cgp_merge(s, L, Pm, c.lp, pstride, c.ldp, c.lcnt, c.D_max, D_dev, D_max, w.agg, out, ldo, ph, c.mean);
+      cgp_merge(s, L, Pm, pp, c.ldp, own, D_dev, D_max, w.agg, out, ldo, ph, c.mean);
+      if (p2p) x_done();
+      if (mom && ph == 1 && p2p) {  // owners' means to every rank (phase 2 needs them for all destinations)
+        x_begin();
+        const int64_t mw = L.spec.in_dim;  // mean rows are in_dim float64 wide (k_merge_moments)
+        OB_CUDA(cudaMemcpyAsync(xregion_ptr(c, xj), c.mean, sizeof(double) * D_max * mw, cudaMemcpyDeviceToDevice, s));
+        x_exchange();
+        k_x_gather_rows<<<grid_for(D_max * mw * 2, 256), 256, 0, s>>>(x, xoff(c, xj), b0.dst_ids, D_dev, 0, N, c.owner,
+                                                                      8, mw, reinterpret_cast<float*>(c.mean));
+        OB_LAUNCHED();
+        x_done();
+        c.nvlink_bytes += (int64_t)(D_max * mw * 8 * (c.P - 1) / c.P);
+      }
       if (ph == phases) cgp_update(s, L, D_dev, D_max, c.hvp, w.agg, out, ldo);
     }
   }
 #ifdef OB_WITH_NCCL
-  if (c.nccl) {
+  if (p2p) {  // rank 0 collects every query row from its owner
+    const int H = e.layers.back().spec.out_dim;
+    x_begin();
+    OB_CUDA(cudaMemcpyAsync(xregion_ptr(c, xj), c.fin, sizeof(float) * w.B * H, cudaMemcpyDeviceToDevice, s));
+    x_exchange();
+    if (c.my_rank == 0) {
+      k_x_gather_rows<<<grid_for((int64_t)w.B * H, 256), 256, 0, s>>>(x, xoff(c, xj), nullptr, nullptr, w.B, N,
+                                                                      c.owner, 4, H, d_out);
+      OB_LAUNCHED();
+    }
+    x_done();
+    c.nvlink_bytes += (int64_t)w.B * H * 4 * (c.P - 1) / c.P;
+    c.collective_bytes = c.nvlink_bytes;
+  } else if (c.nccl) {
     const int H = e.layers.back().spec.out_dim;
     k_zero_foreign_queries<<<grid_for((int64_t)w.B * H, 256), 256, 0, s>>>(c.fin, w.B, H, c.P, c.my_rank);
     OB_LAUNCHED();
     OB_NCCL(ncclReduce(c.fin, d_out, (size_t)w.B * H, ncclFloat, ncclSum, 0, (ncclComm_t)c.comm, s));
     c.collective_bytes += (int64_t)w.B * H * 4;
   }
+#endif
+}
+
+#ifdef OB_WITH_NCCL
+static void comm_barrier(Engine& e) {
+  CgpState& c = e.cgp;
+  int* d = (int*)e.dalloc(sizeof(int));
+  OB_CUDA(cudaMemsetAsync(d, 0, sizeof(int), e.stream));
+  OB_NCCL(ncclAllReduce(d, d, 1, ncclInt, ncclSum, (ncclComm_t)c.comm, e.stream));
+  OB_CUDA(cudaStreamSynchronize(e.stream));
+  e.dfree(d);
+}
+#endif
+
+static void close_exchange(Engine& e) {
+  CgpState& c = e.cgp;
+  for (int p = 0; p < c.P && p < kMaxParts; ++p) {
+    if (c.xpeer[p] && c.xpeer[p] != c.xbuf) cudaIpcCloseMemHandle(c.xpeer[p]);
+    c.xpeer[p] = nullptr;
+  }
+  if (c.xbuf) cudaFree(c.xbuf);
+  c.xbuf = nullptr;
+  c.xregion = 0;
+  c.xsteps = 0;
+}
+
+void cgp_ensure_exchange(Engine& e) {
+#ifdef OB_WITH_NCCL
+  CgpState& c = e.cgp;
+  if (!c.nccl || !c.p2p) return;
+  const int steps = 4 * (int)e.layers.size() + 2;
+  if (c.xbuf && c.x_need_region <= c.xregion && steps <= c.xsteps) return;
+  cudaStream_t s = e.stream;
+  OB_CUDA(cudaStreamSynchronize(s));
+  e.drop_graphs();  // captured graphs hold the old buffer addresses
+  comm_barrier(e);  // every peer stopped using the old buffers
+  close_exchange(e);
+  comm_barrier(e);
+  const size_t region = std::max(c.x_need_region, c.xregion * 3 / 2);
+  const size_t bytes = kXFlags + (size_t)steps * region;
+  void* q = nullptr;
+  OB_CUDA(cudaMalloc(&q, bytes));
+  OB_CUDA(cudaMemset(q, 0, bytes));
+  c.xbuf = (char*)q;
+  c.xregion = region;
+  c.xsteps = steps;
+  if (!c.xep) {
+    c.xep = (int64_t*)e.dalloc(sizeof(int64_t));
+    c.xerr = (int64_t*)e.dalloc(sizeof(int64_t));
+  }
+  OB_CUDA(cudaMemset(c.xep, 0, sizeof(int64_t)));
+  OB_CUDA(cudaMemset(c.xerr, 0, sizeof(int64_t)));
+  // everyone's IPC handle to everyone
+  cudaIpcMemHandle_t mine;
+  OB_CUDA(cudaIpcGetMemHandle(&mine, c.xbuf));
+  char* dh = (char*)e.dalloc(sizeof(cudaIpcMemHandle_t) * c.P);
+  OB_CUDA(cudaMemcpy(dh + sizeof(mine) * c.my_rank, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  OB_NCCL(ncclAllGather(dh + sizeof(mine) * c.my_rank, dh, sizeof(mine), ncclChar, (ncclComm_t)c.comm, s));
+  std::vector<cudaIpcMemHandle_t> all(c.P);
+  OB_CUDA(cudaMemcpyAsync(all.data(), dh, sizeof(mine) * c.P, cudaMemcpyDeviceToHost, s));
+  OB_CUDA(cudaStreamSynchronize(s));
+  e.dfree(dh);
+  for (int p = 0; p < c.P; ++p) {
+    if (p == c.my_rank) {
+      c.xpeer[p] = c.xbuf;
+      continue;
+    }
+    void* ptr = nullptr;
+    OB_CUDA(cudaIpcOpenMemHandle(&ptr, all[p], cudaIpcMemLazyEnablePeerAccess));
+    c.xpeer[p] = (char*)ptr;
+  }
+  comm_barrier(e);  // every peer mapped before any request uses the flags
+#else
+  (void)e;
 #endif
 }
 
@@ -483,6 +753,10 @@ void cgp_init_comm(Engine& e) {
   ncclComm_t comm;
   OB_NCCL(ncclCommInitRank(&comm, e.cfg.num_partitions, id, e.cfg.rank));
   e.cgp.comm = comm;
+  // partial exchange over CUDA-IPC-mapped peer buffers unless OB_CGP_NCCL=1 asks for
+  // the padded ncclAllReduce path
+  const char* v = std::getenv("OB_CGP_NCCL");
+  e.cgp.p2p = !(v && v[0] && v[0] != '0') && e.cfg.num_partitions <= kMaxParts;
 #else
   throw Error(OB_ECOMM, "built without NCCL");
 #endif
@@ -490,6 +764,16 @@ void cgp_init_comm(Engine& e) {
 
 void cgp_destroy(Engine& e) {
 #ifdef OB_WITH_NCCL
+  if (e.cgp.comm && e.cgp.xbuf) {
+    try {
+      cudaStreamSynchronize(e.stream);
+      comm_barrier(e);  // no peer still reads this rank's buffer
+      close_exchange(e);
+      comm_barrier(e);
+    } catch (...) {
+      close_exchange(e);
+    }
+  }
   if (e.cgp.comm) ncclCommDestroy((ncclComm_t)e.cgp.comm);
 #endif
   e.cgp.comm = nullptr;

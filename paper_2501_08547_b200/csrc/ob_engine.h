@@ -24,6 +24,7 @@ enum ErrBits : int64_t {
   kErrNoQuery = 2,      // request edge without a query endpoint
   kErrZeroTotal = 4,    // candidate with zero total degree (policy.py:79-80)
   kErrNonFinite = 8,    // query feature not finite
+  kErrComm = 16,        // a CGP peer never signalled (NVLink exchange timeout)
 };
 
 // Device-side counters of one request (one allocation, read back once).
@@ -350,6 +351,27 @@ struct LayerRun {
   const int64_t* group_ptr;  // second-level partial groups (hub destinations)
 };
 
+// CGP merge inputs: partition p's raw partial rows and local in-edge counts
+// (contiguous in the single-process emulation, peers' exchange buffers over
+// NVLink in NCCL mode); read with ld.global.cg so peer data is never stale in L1
+constexpr int kMaxParts = 8;
+struct PartPtrs {
+  const float* lp[kMaxParts];
+  const float* cnt[kMaxParts];
+};
+// NCCL mode: a rank merges / updates only the destinations it owns
+struct OwnerFilter {
+  const int32_t* owner = nullptr;  // null: every destination
+  const int32_t* dst_ids = nullptr;
+  int64_t N = 0;
+  int P = 1, rank = 0;
+  __device__ __forceinline__ bool mine(int64_t i) const {
+    if (!owner) return true;
+    const int64_t g = dst_ids[i];
+    return (g >= N ? (int)((g - N) % P) : owner[g]) == rank;
+  }
+};
+
 struct LayerScratch {
   float* partial;
   float* partial2;
@@ -370,9 +392,9 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
                        const double* mean);
 // CGP: merge P raw partials in partition order (cgpexec.py:189-240) and normalise; GAT and
 // transform-first GCN write the layer output, the others the aggregate for cgp_update
-void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const float* lp, int64_t part_stride, int64_t ldp,
-               const float* lcnt, int64_t cnt_stride, const int64_t* D_dev, int64_t D_max, float* agg,
-               float* out, int64_t ldo, int moments_phase, double* mean);
+void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const PartPtrs& parts, int64_t ldp, const OwnerFilter& own,
+               const int64_t* D_dev, int64_t D_max, float* agg, float* out, int64_t ldo, int moments_phase,
+               double* mean);
 // CGP: apply_update with explicit destination rows h_v (models.py:214-228)
 void cgp_update(cudaStream_t s, const LayerDev& L, const int64_t* D_dev, int64_t D_max, const float* const* hvp,
                 const float* agg, float* out, int64_t ldo);
@@ -489,7 +511,23 @@ struct CgpState {
   float* fin = nullptr;         // [B][H] last-layer rows before the reduce to rank 0
   int64_t D_max = 0, ldp = 0;
   int64_t collective_bytes = 0;
+  // NVLink exchange (NCCL mode): every rank's exchange buffer is mapped into
+  // every peer (CUDA IPC); partials move with P2P loads, step flags with
+  // system-scope stores -- only real rows, no padding, owner-only merges
+  bool p2p = false;             // use the exchange (else padded ncclAllReduce)
+  char* xbuf = nullptr;         // [flags 256 B][steps x region]
+  size_t xregion = 0;           // bytes per step region
+  int xsteps = 0;               // regions
+  size_t x_need_region = 0;     // this plan's region bytes (carve_cgp)
+  char* xpeer[kMaxParts] = {};  // every rank's buffer in this address space (own = xbuf)
+  int64_t* xep = nullptr;       // device step counter
+  int64_t* xerr = nullptr;      // device error word (flag wait timeouts)
+  int64_t nvlink_bytes = 0;     // per request, real-row bytes read from peers (host estimate)
 };
+
+// (re)build the NVLink exchange when the plan needs bigger regions (all ranks
+// call it at the same request: plans are identical); outside any capture
+void cgp_ensure_exchange(Engine& e);
 
 void cgp_build_partitions(Engine& e);
 // NCCL-mode CGP on a host-loaded graph: keep only this rank's feature / PE rows

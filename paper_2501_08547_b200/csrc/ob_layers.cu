@@ -676,11 +676,10 @@ __global__ void __launch_bounds__(256) k_local_raw_f64(const BlockCounters* cnt_
 
 struct MergeArgs {
   int P;
-  const float* lp;
-  int64_t part_stride, ldp;
-  const float* lcnt;
-  int64_t cnt_stride;
+  PartPtrs parts;             // partition p's partial rows / counts (local or a peer's, over NVLink)
+  int64_t ldp;
   const int64_t* D_dev;
+  OwnerFilter own;            // NCCL mode: merge only the destinations this rank owns
   int width, kind;
   float p;
   int n;
@@ -697,13 +696,14 @@ __global__ void __launch_bounds__(256) k_merge_parts(MergeArgs m) {
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = gw; i < D; i += nw) {
+    if (!m.own.mine(i)) continue;
     float c = 0.f;
-    for (int p = 0; p < m.P; ++p) c += m.lcnt[p * m.cnt_stride + i];
+    for (int p = 0; p < m.P; ++p) c += __ldcg(m.parts.cnt[p] + i);
     float ms = -INFINITY;
     if (m.kind == OB_KIND_GAT) {
       for (int p = 0; p < m.P; ++p) {
-        const float* o = m.lp + p * m.part_stride + i * m.ldp;
-        if (o[1] > 0.f) ms = fmaxf(ms, o[0]);
+        const float* o = m.parts.lp[p] + i * m.ldp;
+        if (__ldcg(o + 1) > 0.f) ms = fmaxf(ms, __ldcg(o));
       }
     }
     for (int col = lane; col < m.width; col += 32) {
@@ -711,22 +711,22 @@ __global__ void __launch_bounds__(256) k_merge_parts(MergeArgs m) {
       if (m.kind == OB_KIND_GAT) {
         float den = 0.f, num = 0.f;
         for (int p = 0; p < m.P; ++p) {
-          const float* o = m.lp + p * m.part_stride + i * m.ldp;
-          if (o[1] > 0.f) {
-            const float sc = __expf(o[0] - ms);
-            den += o[1] * sc;
-            num += o[2 + col] * sc;
+          const float* o = m.parts.lp[p] + i * m.ldp;
+          if (__ldcg(o + 1) > 0.f) {
+            const float sc = __expf(__ldcg(o) - ms);
+            den += __ldcg(o + 1) * sc;
+            num += __ldcg(o + 2 + col) * sc;
           }
         }
         r = den > 0.f ? num / den : 0.f;
       } else if (m.kind == OB_KIND_SAGE_MAX) {
         float mx = -INFINITY;
         for (int p = 0; p < m.P; ++p)
-          if (m.lcnt[p * m.cnt_stride + i] > 0.f) mx = fmaxf(mx, m.lp[p * m.part_stride + i * m.ldp + col]);
+          if (__ldcg(m.parts.cnt[p] + i) > 0.f) mx = fmaxf(mx, __ldcg(m.parts.lp[p] + i * m.ldp + col));
         r = c > 0.f ? mx : 0.f;
       } else {
         float s = 0.f;
-        for (int p = 0; p < m.P; ++p) s += m.lp[p * m.part_stride + i * m.ldp + col];
+        for (int p = 0; p < m.P; ++p) s += __ldcg(m.parts.lp[p] + i * m.ldp + col);
         if (m.gcn_norm) r = s / sqrtf(c + 1.f);
         else if (m.kind == OB_KIND_POWER_MEAN) r = c > 0.f ? powf(s / c, 1.f / m.p) : 0.f;
         else r = c > 0.f ? s / c : 0.f;
@@ -737,20 +737,21 @@ __global__ void __launch_bounds__(256) k_merge_parts(MergeArgs m) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_merge_moments(int P, const double* lp, int64_t part_stride, int64_t ldp,
-                                                       const float* lcnt, int64_t cnt_stride, const int64_t* D_dev,
-                                                       int width, int phase, int n, double* mean, float* agg,
-                                                       int64_t ldo) {
+__global__ void __launch_bounds__(256) k_merge_moments(int P, PartPtrs parts, int64_t ldp, const int64_t* D_dev,
+                                                       OwnerFilter own, int width, int phase, int n, double* mean,
+                                                       float* agg, int64_t ldo) {
   const int64_t D = *D_dev;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = gw; i < D; i += nw) {
+    if (!own.mine(i)) continue;
     float c = 0.f;
-    for (int p = 0; p < P; ++p) c += lcnt[p * cnt_stride + i];
+    for (int p = 0; p < P; ++p) c += __ldcg(parts.cnt[p] + i);
     for (int col = lane; col < width; col += 32) {
       double s = 0.0;
-      for (int p = 0; p < P; ++p) s += lp[p * part_stride + i * ldp + col];
+      for (int p = 0; p < P; ++p)
+        s += __ldcg(reinterpret_cast<const double*>(parts.lp[p]) + i * ldp + col);
       const double v = c > 0.f ? s / (double)c : 0.0;
       if (phase == 1) {
         mean[i * width + col] = v;
@@ -838,25 +839,21 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   g_launches += 2;
 }
 
-void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const float* lp, int64_t part_stride, int64_t ldp,
-               const float* lcnt, int64_t cnt_stride, const int64_t* D_dev, int64_t D_max, float* agg, float* out,
-               int64_t ldo, int moments_phase, double* mean) {
+void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const PartPtrs& parts, int64_t ldp, const OwnerFilter& own,
+               const int64_t* D_dev, int64_t D_max, float* agg, float* out, int64_t ldo, int moments_phase,
+               double* mean) {
   const ob_layer& sp = L.spec;
-  if (sp.kind == OB_KIND_MOMENTS) {
-    // part_stride counts floats; the moments partials are float64
-    k_merge_moments<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(P, (const double*)lp, part_stride / 2, ldp, lcnt,
-                                                                      cnt_stride, D_dev, sp.in_dim, moments_phase,
-                                                                      sp.n, mean, agg, ld4(sp.in_dim));
+  if (sp.kind == OB_KIND_MOMENTS) {  // float64 partials, ldp counts float64 elements
+    k_merge_moments<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(P, parts, ldp, D_dev, own, sp.in_dim,
+                                                                      moments_phase, sp.n, mean, agg, ld4(sp.in_dim));
     OB_LAUNCHED();
     return;
   }
   MergeArgs m{};
   m.P = P;
-  m.lp = lp;
-  m.part_stride = part_stride;
+  m.parts = parts;
   m.ldp = ldp;
-  m.lcnt = lcnt;
-  m.cnt_stride = cnt_stride;
+  m.own = own;
   m.D_dev = D_dev;
   m.kind = sp.kind;
   m.p = sp.p;
