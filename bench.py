@@ -156,11 +156,12 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the aggregation kernel from the committed ncu capture, if any."""
+def ncu_traffic(cfg):
+    """dram bytes per launch (averaged over one request's launches, like roofline.achieved) of the
+    aggregation kernel from the committed ncu capture of this config, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_agg_traffic.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f).get(cfg, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -426,7 +427,7 @@ def main():
     agg_gbs = agg["bytes"] / (agg["ms"] / 1e3) / 1e9 if agg["ms"] > 0 else 0.0
     roof = {"bound": "hbm", "kernel": "k_agg (edge-chunk gather + segment reduce)",
             "achieved": round(agg_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(agg_gbs / hbm, 4),
-            "peak_source": which, "traffic": ncu_traffic(),
+            "peak_source": which, "traffic": ncu_traffic(cfg),
             "launches": agg["n"], "avg_launch_us": round(agg["ms"] * 1e3 / max(agg["n"], 1), 2),
             "share_of_step": round(agg["ms"] / max(reqp["ms"], 1e-9), 3)}
     line = {

@@ -16,7 +16,7 @@ def main(path, marker="k_set_params"):
     starts = [i for i, (n, _) in enumerate(ks) if marker in n]
     # the last complete request: between the last two markers (else from the last one)
     seg = ks[starts[-2]:starts[-1]] if len(starts) >= 2 else (ks[starts[-1]:] if starts else ks)
-    seg = [(n, v) for n, v in seg if "ob::" in n]
+    seg = [(n, v) for n, v in seg if "at::" not in n]  # drop torch's L2-flush kernels
     agg = collections.OrderedDict()
     for n, v in seg:
         s = n.split("(")[0].replace("void ", "")[:70]
