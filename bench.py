@@ -429,6 +429,9 @@ def main():
             "achieved": round(agg_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(agg_gbs / hbm, 4),
             "peak_source": which, "traffic": ncu_traffic(cfg),
             "launches": agg["n"], "avg_launch_us": round(agg["ms"] * 1e3 / max(agg["n"], 1), 2),
+            "gathered_row_gbs": round(agg["flops"] / (agg["ms"] / 1e3) / 1e9, 1) if agg["ms"] > 0 else None,
+            "note": "rows are re-read once per edge (avg source out-degree in the block), mostly from L2; "
+                    "gathered_row_gbs is that served traffic, the kernel's real limiter (L2 fabric)",
             "share_of_step": round(agg["ms"] / max(reqp["ms"], 1e-9), 3)}
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,

@@ -177,7 +177,8 @@ int ob_reserve(ob_engine* e, int32_t num_queries, int64_t num_edges);
  * engine stream.  enable != 0 resets the records.  ob_profile_read sums the
  * launches of one class since enabling: device time, count, algorithmic bytes
  * (aggregation: 4*E + 4*w*S + 4*pw*items; finalize: partials in + rows out;
- * gemm: operands + result) and flops (gemm). */
+ * gemm: operands + result) and flops (gemm; for the aggregation class this slot returns the
+ * gathered row bytes 4*w*E, i.e. the traffic the gather actually serves). */
 enum ob_prof_class { OB_PROF_AGG = 0, OB_PROF_GEMM = 1, OB_PROF_FINALIZE = 2, OB_PROF_BUILD = 3,
                      OB_PROF_SELECT = 4, OB_PROF_RESOLVE = 5, OB_PROF_REQUEST = 6, OB_PROF_CSR = 7,
                      OB_PROF_COMM = 8 };

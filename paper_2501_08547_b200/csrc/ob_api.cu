@@ -1059,6 +1059,7 @@ int ob_profile_read(ob_engine* h, int32_t cls, double* total_ms, int64_t* launch
       if (cls == kProfAgg) {
         // edge list + every source row once + partial rows out
         by += 4.0 * c.E + 4.0 * r.width * c.S + 4.0 * r.pw * c.items;
+        fl += 4.0 * r.width * c.E;  // gathered row bytes (rows are re-read once per edge, mostly from L2)
       } else if (cls == kProfFinalize) {
         by += 4.0 * r.pw * c.items + 4.0 * r.width * c.D;
       } else if (cls == kProfGemm) {
