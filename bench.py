@@ -430,6 +430,7 @@ def main():
             "peak_source": which, "traffic": ncu_traffic(cfg),
             "launches": agg["n"], "avg_launch_us": round(agg["ms"] * 1e3 / max(agg["n"], 1), 2),
             "gathered_row_gbs": round(agg["flops"] / (agg["ms"] / 1e3) / 1e9, 1) if agg["ms"] > 0 else None,
+            "gather_ceiling_gbs": 15200.0,  # measured random 512-B row gather, L2-sized table (profiles/r01_gather_ceiling.md)
             "note": "rows are re-read once per edge (avg source out-degree in the block), mostly from L2; "
                     "gathered_row_gbs is that served traffic, the kernel's real limiter (L2 fabric)",
             "share_of_step": round(agg["ms"] / max(reqp["ms"], 1e-9), 3)}
