@@ -117,6 +117,7 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.rx_off = a.take<int64_t>(256 * rx_tiles(m) + 1);
   w.rq_ctr = a.take<int64_t>(4);
   w.sbits = a.take<uint32_t>(p.words_NB + 1);
+  w.fill_bits = p.words_NB <= 48 * 1024 ? a.take<uint32_t>(kNumSMs * (p.words_NB + 1)) : nullptr;
   w.swpre = a.take<int64_t>(p.words_NB + 1);
   int64_t Emax = 1, Dmax = 1, Smax = 1, Imax = 1;
   for (auto& b : p.blocks) {
@@ -651,6 +652,7 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
       e.own_stream = true;
     }
     for (auto& ev_ : e.ev) OB_CUDA(cudaEventCreate(&ev_));
+    configure_fill();
     if (const char* v = std::getenv("OB_NO_GRAPHS")) e.use_graphs = !(v[0] && v[0] != '0');
     if (cfg->nccl_id && cfg->strategy == OB_STRATEGY_SRPE_CGP) {
       try {

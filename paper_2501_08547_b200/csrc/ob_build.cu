@@ -79,14 +79,24 @@ __device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ ptr, int64
 // gather global source ids: one warp per aggregation work item (kAggChunk edges
 // of one destination), so a destination's CSR row and request span are copied
 // with contiguous, coalesced loads and hub destinations spread over many warps
-__global__ void __launch_bounds__(256) k_block_fill(const BlockCounters* cnt, const int64_t* __restrict__ dst_ptr,
-                                                    const int64_t* __restrict__ item_ptr,
-                                                    const int32_t* __restrict__ item_dst, SegSpans sp,
-                                                    const int32_t* __restrict__ nbrs,
-                                                    const int32_t* __restrict__ rq_src, int32_t* src_global,
-                                                    uint32_t* sbits) {
-  const int64_t D = cnt->D, items = cnt->items;
+// SMEM variant (source bitmap fits in shared memory): each CTA marks its
+// sources in a private shared bitmap and writes it out once; k_bitmap_or
+// merges the per-CTA bitmaps.  Hub sources that appear in thousands of rows
+// then cost shared-memory atomics instead of serialised L2 atomics on one word.
+template <bool SMEM>
+__global__ void __launch_bounds__(1024) k_block_fill(const BlockCounters* cnt, const int64_t* __restrict__ dst_ptr,
+                                                     const int64_t* __restrict__ item_ptr,
+                                                     const int32_t* __restrict__ item_dst, SegSpans sp,
+                                                     const int32_t* __restrict__ nbrs,
+                                                     const int32_t* __restrict__ rq_src, int32_t* src_global,
+                                                     uint32_t* sbits, int64_t words, uint32_t* part_bits) {
+  extern __shared__ uint32_t sbm[];
+  const int64_t items = cnt->items;
   const int lane = threadIdx.x & 31;
+  if (SMEM) {
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) sbm[w] = 0u;
+    __syncthreads();
+  }
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = gw; it < items; it += nw) {
@@ -106,9 +116,34 @@ __global__ void __launch_bounds__(256) k_block_fill(const BlockCounters* cnt, co
     for (int u = 0; u < kAggChunk / 32; ++u) {
       if (v[u] < 0) continue;
       src_global[e0 + u * 32 + lane] = v[u];
-      bm_set(sbits, v[u]);  // test before set: a re-marked source costs a read, not an atomic
+      if (SMEM) {
+        const uint32_t m = 1u << (v[u] & 31);
+        if (!(sbm[v[u] >> 5] & m)) atomicOr(sbm + (v[u] >> 5), m);
+      } else {
+        bm_set(sbits, v[u]);  // test before set: a re-marked source costs a read, not an atomic
+      }
     }
   }
+  if (SMEM) {
+    __syncthreads();
+    uint32_t* out = part_bits + (int64_t)blockIdx.x * words;
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) out[w] = sbm[w];
+  }
+}
+
+__global__ void k_bitmap_or(const uint32_t* __restrict__ part_bits, int nparts, int64_t words, uint32_t* sbits) {
+  OB_GRID_STRIDE(w, words) {
+    uint32_t v = 0;
+    for (int p = 0; p < nparts; ++p) v |= __ldg(part_bits + (int64_t)p * words + w);
+    sbits[w] = v;
+  }
+}
+
+constexpr int64_t kFillSmemWords = 48 * 1024;  // 192 KB: source bitmaps up to 1.5M ids stay on chip
+
+void configure_fill() {
+  OB_CUDA(cudaFuncSetAttribute(k_block_fill<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(kFillSmemWords * 4)));
 }
 
 __global__ void __launch_bounds__(256) k_expand_items(const BlockCounters* cnt, const int64_t* __restrict__ item_ptr,
@@ -182,10 +217,18 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
   const BlockStore3 st{b.dst_ptr, b.item_ptr, b.group_ptr};
   device_scan_t<I3>(s, e.scan, SegLenLoad3{w.seg_len}, st, BlockTotal3{st, b.cnt}, &b.cnt->D, 0, b.D_max);
   expand_items(s, b.cnt, b.D_max, b.item_ptr, b.group_ptr, b.item_dst, b.group_dst);
-  OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
-  k_block_fill<<<grid_for(b.items_max, 8, kNumSMs * 16), 256, 0, s>>>(b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs,
-                                                                       src.rq_src, w.src_global, w.sbits);
-  OB_LAUNCHED();
+  if (w.words_NB <= kFillSmemWords) {  // per-CTA shared bitmaps, then one OR pass
+    const int64_t words = w.words_NB + 1;
+    k_block_fill<true><<<kNumSMs, 1024, words * 4, s>>>(b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs,
+                                                        src.rq_src, w.src_global, nullptr, words, w.fill_bits);
+    k_bitmap_or<<<grid_for(words, 256), 256, 0, s>>>(w.fill_bits, kNumSMs, words, w.sbits);
+    g_launches += 2;
+  } else {
+    OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
+    k_block_fill<false><<<grid_for(b.items_max, 32, kNumSMs * 2), 1024, 0, s>>>(
+        b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs, src.rq_src, w.src_global, w.sbits, 0, nullptr);
+    OB_LAUNCHED();
+  }
   if (b.has_self) {
     k_mark_ids<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, w.sbits);
     OB_LAUNCHED();

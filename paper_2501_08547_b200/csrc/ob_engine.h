@@ -257,6 +257,7 @@ struct RequestWs {
   }
   // block scratch
   uint32_t* sbits = nullptr;       // source bitmap over [0, N+B)
+  uint32_t* fill_bits = nullptr;   // [148][words_NB+1] per-CTA source bitmaps (small N only)
   int64_t* swpre = nullptr;
   int32_t* src_global = nullptr;   // [E_max] gathered global source ids
   int64_t* seg_len = nullptr;      // [D_max]
@@ -446,6 +447,7 @@ struct BlockTotal3 {
 };
 
 // item -> destination and group -> destination maps (warp per destination)
+void configure_fill();  // shared-memory opt-in of the block fill (outside any capture)
 void expand_items(cudaStream_t s, const BlockCounters* cnt, int64_t D_max, const int64_t* item_ptr,
                   const int64_t* group_ptr, int32_t* item_dst, int32_t* group_dst);
 void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d_kind, int32_t* d_pe_layer);
