@@ -106,7 +106,7 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.cand_tpos = a.take<int32_t>(p.R_max);
   w.targets = a.take<int32_t>(p.T_max + 1);
   w.sel_flag = a.take<int32_t>(p.R_max);
-  w.sel_hist = a.take<uint32_t>(256);
+  w.sel_hist = a.take<uint32_t>(257);  // [256] = round completion counter
   w.rq_cnt = a.take<int32_t>(p.RB_max + 1);
   w.rq_fill = a.take<int32_t>(p.RB_max + 1);
   w.rq_ptr = a.take<int64_t>(p.RB_max + 1);

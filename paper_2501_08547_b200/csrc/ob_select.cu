@@ -240,6 +240,52 @@ __global__ void k_budget(ReqCounters* rc, double gamma, uint32_t* hist) {
     rc->T = 0;
   }
   if (threadIdx.x < 256) hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) hist[256] = 0;
+}
+
+// One radix-select round in one launch: per-CTA digit histograms of the keys that
+// still match the chosen prefix are merged into hist; the last CTA to finish
+// picks this round's digit (scan from the top digit) and clears hist.
+__global__ void __launch_bounds__(256) k_sel_round(const uint64_t* __restrict__ key, ReqCounters* rc, int shift,
+                                                   uint32_t* hist) {
+  using BS = cub::BlockScan<int64_t, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t h[256];
+  __shared__ bool last;
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t R = rc->R, b = rc->budget;
+  const bool active = b > 0 && b < R;
+  if (active) {
+    const uint64_t pre = rc->sel_prefix, msk = rc->sel_mask;
+    OB_GRID_STRIDE(c, R) {
+      const uint64_t k = key[c];
+      if ((k & msk) == pre) atomicAdd(&h[(k >> shift) & 255], 1u);
+    }
+  }
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(hist + threadIdx.x, h[threadIdx.x]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(hist + 256, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int d = 255 - threadIdx.x;  // scan from the top digit down
+  const int64_t c = __ldcg(hist + d);
+  int64_t excl;
+  BS(tmp).ExclusiveSum(c, excl);  // keys in digits above d
+  hist[d] = 0;
+  if (threadIdx.x == 0) hist[256] = 0;
+  if (!active) return;
+  const int64_t krem = rc->sel_krem;
+  if (excl < krem && krem <= excl + c) {
+    rc->sel_krem = krem - excl;
+    rc->sel_gt += excl;
+    rc->sel_prefix |= (uint64_t)d << shift;
+    rc->sel_mask |= (uint64_t)255 << shift;
+    if (shift == 0) rc->sel_eq_take = krem - excl;
+  }
 }
 
 // radix select, MSB-first 8-bit digits: find the budget-th largest key
@@ -517,9 +563,8 @@ void stage_select(Engine& e, RequestWs& w) {
   k_budget<<<1, 256, 0, s>>>(w.rc, e.cfg.gamma, w.sel_hist);
   OB_LAUNCHED();
   for (int shift = 56; shift >= 0; shift -= 8) {
-    k_sel_hist<<<grid_for(r_max, 256, kNumSMs * 2), 256, 0, s>>>(w.cand_key, w.rc, shift, w.sel_hist);
-    k_sel_pick<<<1, 256, 0, s>>>(w.rc, shift, w.sel_hist);
-    g_launches += 2;
+    k_sel_round<<<grid_for(r_max, 256, kNumSMs * 2), 256, 0, s>>>(w.cand_key, w.rc, shift, w.sel_hist);
+    OB_LAUNCHED();
   }
   // ordered compaction: ties at the threshold resolved by ascending id
   device_scan(s, e.scan, EqLoad{w.cand_key, w.rc}, EqStore{w.sel_flag, w.cand_key, w.rc}, &w.rc->R, 0, r_max,
