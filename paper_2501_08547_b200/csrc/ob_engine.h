@@ -179,7 +179,9 @@ struct RqCsr {
 // query source (every edge has a query endpoint), edges into a query carry
 // any source:
 //   candidate slot:  [0 | rank (bR bits) | src - N (bB bits)]
-//   query slot:      [1 | q (bB bits)    | src (bN bits)]   (population bit at `body`)
+//   query slot:      [1 | q (bB bits)    | src' (bN bits)]  (population bit at `body`)
+// with src' = candidate rank of a training source (every training endpoint is a
+// candidate and ranks follow ids) or R + q' for a query source.
 struct RqKeyFmt {
   int bB, bN, bR, body, total;
   bool wide() const { return total > 32; }

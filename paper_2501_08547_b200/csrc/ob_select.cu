@@ -157,11 +157,15 @@ __global__ void k_slots_init(ReqCounters* rc, int B, const int32_t* qdeg, int32_
 }
 
 // packed request-edge key (RqKeyFmt); candidate ranks come from the bitmap
+// Sources into a query slot are stored by candidate rank (every training
+// endpoint of the request is a candidate, and ranks follow id order) or R + q'
+// for a query source, so the key needs bits(R + B) for them, not bits(N + B).
 template <class K>
 __device__ __forceinline__ K rq_key(int64_t s, int64_t d, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
-                                    const RqKeyFmt& f) {
+                                    int64_t R, const RqKeyFmt& f) {
   if (d < N) return ((K)bm_rank(cbits, cwpre, d) << f.bB) | (K)(s - N);
-  return ((K)1 << f.body) | ((K)(d - N) << f.bN) | (K)s;
+  const int64_t sr = s < N ? bm_rank(cbits, cwpre, s) : R + (s - N);
+  return ((K)1 << f.body) | ((K)(d - N) << f.bN) | (K)sr;
 }
 
 // candidate-slot counts (query slots take qdeg) + one radix key per edge
@@ -175,7 +179,7 @@ __global__ void k_rq_count(const ReqParams* rp, int64_t N, const uint32_t* cbits
     int64_t s, d;
     ld_edge(edges, e, s, d);
     if (d < N) warp_agg_inc(rq_cnt, bm_rank(cbits, cwpre, d));
-    keys[e] = rq_key<K>(s, d, N, cbits, cwpre, f);
+    keys[e] = rq_key<K>(s, d, N, cbits, cwpre, rc->R, f);
   }
 }
 
@@ -196,7 +200,7 @@ __global__ void k_rq_count_all(const int64_t* __restrict__ edges, const int64_t*
     int64_t s, d;
     ld_edge(edges, e, s, d);
     warp_agg_inc(rq_cnt, rq_slot(d, N, cbits, cwpre, R));
-    keys[e] = rq_key<K>(s, d, N, cbits, cwpre, f);
+    keys[e] = rq_key<K>(s, d, N, cbits, cwpre, R, f);
   }
 }
 
@@ -398,7 +402,9 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* __restrict__ ke
 template <class K, bool FINAL>
 __global__ void __launch_bounds__(kRxThreads) k_rx_scatter(const K* __restrict__ in, K* out, int32_t* src_out,
                                                            const int64_t* m_dev, int shift, int64_t tiles_b,
-                                                           const int64_t* __restrict__ off, RqKeyFmt f, int64_t N) {
+                                                           const int64_t* __restrict__ off, RqKeyFmt f, int64_t N,
+                                                           const int32_t* __restrict__ cand_ids,
+                                                           const ReqCounters* rc) {
   using BS = cub::BlockScan<int32_t, kRxThreads>;
   __shared__ union {
     int32_t wcnt[kRxWarps][256];  // per-warp digit counts, then per-warp offsets
@@ -466,7 +472,12 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_scatter(const K* __restrict__
       const int64_t pos = gofs[d] + (p - bstart[d]);
       if (FINAL) {
         const bool query_slot = (kk >> f.body) & 1;
-        src_out[pos] = query_slot ? (int32_t)(kk & (((K)1 << f.bN) - 1)) : (int32_t)(N + (kk & (((K)1 << f.bB) - 1)));
+        if (query_slot) {
+          const int64_t sr = (int64_t)(kk & (((K)1 << f.bN) - 1)), R = rc->R;
+          src_out[pos] = sr < R ? cand_ids[sr] : (int32_t)(N + (sr - R));
+        } else {
+          src_out[pos] = (int32_t)(N + (kk & (((K)1 << f.bB) - 1)));
+        }
       } else {
         out[pos] = kk;
       }
@@ -489,9 +500,11 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
     OB_LAUNCHED();
     device_scan(s, e.scan, LoadI32{c.rx_cnt}, StoreI64{c.rx_off}, nullptr, 256 * tiles_b, 256 * tiles_b, nullptr);
     if (p + 1 == passes) {
-      k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, c.rx_off, f, e.g.N);
+      k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, c.rx_off, f, e.g.N,
+                                                      w.cand_ids, w.rc);
     } else {
-      k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, c.rx_off, f, e.g.N);
+      k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, c.rx_off, f, e.g.N,
+                                                       w.cand_ids, w.rc);
       std::swap(a, b);
     }
     OB_LAUNCHED();
@@ -507,8 +520,8 @@ static int bits_for(int64_t n) {  // bits to hold values in [0, n)
 RqKeyFmt rq_key_fmt(const Engine& e, const RequestWs& w) {
   RqKeyFmt f;
   f.bB = bits_for(std::max(w.B, 1));
-  f.bN = bits_for(e.g.N + w.B);
   f.bR = bits_for(std::max<int64_t>(1, std::min<int64_t>(e.g.N, 2 * w.m)));
+  f.bN = bits_for(std::min<int64_t>(e.g.N, 2 * w.m) + w.B);  // query-slot sources by candidate rank
   f.body = std::max(f.bR + f.bB, f.bB + f.bN);
   f.total = f.body + 1;
   OB_CHECK(f.total <= 64, OB_EINVAL, "request key does not fit 64 bits");
