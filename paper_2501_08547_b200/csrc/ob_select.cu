@@ -402,10 +402,13 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* __restrict__ ke
 template <class K, bool FINAL>
 __global__ void __launch_bounds__(kRxThreads) k_rx_scatter(const K* __restrict__ in, K* out, int32_t* src_out,
                                                            const int64_t* m_dev, int shift, int64_t tiles_b,
-                                                           const int64_t* __restrict__ off, RqKeyFmt f, int64_t N,
+                                                           const int64_t* __restrict__ off,
+                                                           const int32_t* __restrict__ cnt, RqKeyFmt f, int64_t N,
                                                            const int32_t* __restrict__ cand_ids,
                                                            const ReqCounters* rc) {
   using BS = cub::BlockScan<int32_t, kRxThreads>;
+  using BS64 = cub::BlockScan<int64_t, kRxThreads>;
+  __shared__ typename BS64::TempStorage scan_tmp64;
   __shared__ union {
     int32_t wcnt[kRxWarps][256];  // per-warp digit counts, then per-warp offsets
     K exch[kRxTile];              // the tile in (digit, index) order
@@ -452,9 +455,29 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_scatter(const K* __restrict__
     }
     int32_t start;
     BS(scan_tmp).ExclusiveSum(tot, start);
-    if (threadIdx.x < 256) {
-      bstart[threadIdx.x] = start;
-      gofs[threadIdx.x] = off[(int64_t)threadIdx.x * tiles_b + t];
+    if (off) {
+      if (threadIdx.x < 256) {
+        bstart[threadIdx.x] = start;
+        gofs[threadIdx.x] = off[(int64_t)threadIdx.x * tiles_b + t];
+      }
+    } else {
+      // few tiles: derive this tile's global digit offsets from the raw counts
+      // (digit d starts after every key of smaller digits, then after digit d's
+      // keys in earlier tiles) instead of a separate grid-wide scan
+      int64_t dtot = 0, before = 0;
+      if (threadIdx.x < 256)
+        for (int64_t t2 = 0; t2 < tiles_b; ++t2) {
+          const int64_t c = cnt[(int64_t)threadIdx.x * tiles_b + t2];
+          dtot += c;
+          if (t2 < t) before += c;
+        }
+      __syncthreads();  // scan_tmp reuse
+      int64_t dstart;
+      BS64(scan_tmp64).ExclusiveSum(dtot, dstart);
+      if (threadIdx.x < 256) {
+        bstart[threadIdx.x] = start;
+        gofs[threadIdx.x] = dstart + before;
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -494,17 +517,20 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
   K* a = reinterpret_cast<K*>(c.keys);
   K* b = reinterpret_cast<K*>(c.keys2);
   const int passes = f.passes();
+  const bool fused = tiles_b <= 32;  // few tiles: offsets come straight from the counts
+  const int64_t* off = fused ? nullptr : c.rx_off;
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
     k_rx_hist<K><<<g, kRxThreads, 0, s>>>(a, m_dev, shift, tiles_b, c.rx_cnt);
     OB_LAUNCHED();
-    device_scan(s, e.scan, LoadI32{c.rx_cnt}, StoreI64{c.rx_off}, nullptr, 256 * tiles_b, 256 * tiles_b, nullptr);
+    if (!fused)
+      device_scan(s, e.scan, LoadI32{c.rx_cnt}, StoreI64{c.rx_off}, nullptr, 256 * tiles_b, 256 * tiles_b, nullptr);
     if (p + 1 == passes) {
-      k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, c.rx_off, f, e.g.N,
-                                                      w.cand_ids, w.rc);
+      k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, off, c.rx_cnt, f,
+                                                      e.g.N, w.cand_ids, w.rc);
     } else {
-      k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, c.rx_off, f, e.g.N,
-                                                       w.cand_ids, w.rc);
+      k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, off, c.rx_cnt, f,
+                                                       e.g.N, w.cand_ids, w.rc);
       std::swap(a, b);
     }
     OB_LAUNCHED();
