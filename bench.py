@@ -21,9 +21,12 @@ Under torchrun (N > 1) the default is independent replicas: every rank holds
 the whole graph and serves its own request stream (query batches are
 independent units, no data-path collective; weak scaling, time = max over
 ranks).  ``--parallel cgp`` runs computation-graph parallelism instead: the
-graph is hash-partitioned, every rank aggregates the part of each batch whose
-sources it owns and partials meet at the owners over NCCL (strong scaling on
-one shared batch stream) -- DESIGN.md "Multi-GPU".
+graph is hash-partitioned over a group of ``--cgp-size`` GPUs, every rank
+aggregates the part of each batch whose sources it owns and partials meet at
+the owners over NVLink (peer-mapped exchange buffers); N / size groups serve
+independent request streams side by side -- DESIGN.md "Multi-GPU".  The
+papers-shaped ``--config cfg4`` (111M nodes, 1.6B edges, generated on the
+GPUs) runs only this way, with groups of 2 by default.
 """
 
 from __future__ import annotations
@@ -66,7 +69,7 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def make_inputs(cfg, rank, world, n_req, seed_base=3, same_requests=False):
+def make_inputs(cfg, rank, world, n_req, seed_base=3, same_requests=False, stream_id=None):
     """Reference-generator graph + requests; rank 0 builds, others map the same files."""
     from paper_2501_08547_b200 import workload
     from paper_2501_08547_b200.graphstore import GraphDataset
@@ -93,7 +96,7 @@ def make_inputs(cfg, rank, world, n_req, seed_base=3, same_requests=False):
             removed[z["ids"]] = True
             pool = workload.HoldoutPool(z["ids"], removed, serving.features[z["ids"]], z["inc"])
     log(f"[bench] rank {rank}: graph ready in {time.time() - t0:.1f}s (E={serving.num_edges})")
-    rs = 0 if same_requests else rank  # CGP: every rank serves the same request stream
+    rs = (stream_id or 0) if same_requests else rank  # CGP: a group's ranks serve the same request stream
     reqs = [workload.make_request(pool, serving, B, seed=seed_base + 1000 * rs + i) for i in range(n_req)]
     return serving, pool, reqs
 
@@ -248,6 +251,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--parallel", default=None, choices=["cgp", "replicas"],
                     help="N > 1: independent replicas (default) or computation-graph parallelism")
+    ap.add_argument("--cgp-size", type=int, default=None,
+                    help="GPUs per CGP group (default: all for cfg1-3, 2 for cfg4); N / size groups serve "
+                         "independent request streams")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -277,23 +283,34 @@ def main():
             print(json.dumps({"metric": METRIC, "unavailable": f"{cfg} needs --parallel cgp on >= 2 GPUs "
                                                                "(one B200 cannot hold its graph + stored rows)"}))
         return
+    P = (args.cgp_size or (2 if synthetic else world)) if cgp else 1
+    if cgp and (P < 2 or world % P):
+        raise SystemExit(f"--cgp-size {P} must be >= 2 and divide the world size {world}")
+    groups = world // P if cgp else world
+    my_group = rank // P if cgp else rank
+    pg = None
+    if cgp and groups > 1:  # every rank creates every group, then keeps its own
+        import torch.distributed as dist
+
+        pgs = [dist.new_group(list(range(g * P, (g + 1) * P))) for g in range(groups)]
+        pg = pgs[my_group]
     if synthetic:
         from paper_2501_08547_b200 import graphstore, workload
 
         serving = graphstore.SyntheticGraph(n, avg, 2.1, F, seed=1)
         pool = None
-        reqs = [workload.make_request_synthetic(n, avg, 2.1, F, B, seed=3 + i) for i in range(nreq)]
+        reqs = [workload.make_request_synthetic(n, avg, 2.1, F, B, seed=3 + 1000 * my_group + i) for i in range(nreq)]
         pe_src = graphstore.SyntheticPe([H] * (k - 1), seed=2)
     else:
-        serving, pool, reqs = make_inputs(cfg, rank, world, nreq, same_requests=cgp)
+        serving, pool, reqs = make_inputs(cfg, rank, world, nreq, same_requests=cgp, stream_id=my_group)
         pe_src = None
     model = models.make_model(kind, k, F, H)
     w = models.init_weights(model, 2)
     stream = torch.cuda.Stream(device=local)
     t0 = time.time()
     if cgp:
-        scfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=gamma, num_partitions=world, seed=0, device=local)
-        eng = runtime.distributed_engine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream)
+        scfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=gamma, num_partitions=P, seed=0, device=local)
+        eng = runtime.distributed_engine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream, group=pg)
     else:
         scfg = runtime.ServeConfig(strategy="srpe", gamma=gamma, device=local)
         eng = runtime.ServingEngine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream)
@@ -371,7 +388,7 @@ def main():
         t = torch.tensor([total_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    served = B if cgp else world * B  # CGP: all ranks serve the same batch together
+    served = groups * B  # CGP: the P ranks of a group serve one batch together
     value = served * args.steps / (total_ms / 1e3)
 
     # end to end through the public host-pointer API (pinned buffers, H2D + D2H inside the region)
@@ -438,11 +455,12 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
         "p50_ms": round(float(np.percentile(lat, 50)), 4), "p99_ms": round(float(np.percentile(lat, 99)), 4),
-        "higher_is_better": True, "scaling": "strong" if cgp else "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if (cgp and groups == 1) else "weak", "vs_baseline": None,
+        "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": desc, "batch": B, "policy": "ratio", "gamma": gamma,
                    "strategy": "srpe-cgp" if cgp else "srpe",
-                   "parallelism": (f"cgp x{world} (NCCL over NVLink)" if cgp else
+                   "parallelism": (f"cgp x{P} (NVLink exchange) x {groups} group(s)" if cgp else
                                    (f"replicas x{world}" if world > 1 else "single")),
                    "l2": "flushed (512 MB write) before every timed step",
                    "inputs": ("device generator (ob_generate_graph: the reference degree law, not its numpy "

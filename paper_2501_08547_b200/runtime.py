@@ -87,27 +87,36 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def broadcast_nccl_id(make_id=nccl_unique_id) -> bytes:
-    """Rank 0 draws the NCCL id and every rank of the default torch.distributed group gets it.
+def broadcast_nccl_id(make_id=nccl_unique_id, group=None) -> bytes:
+    """The group's rank 0 draws the NCCL id and every rank of the torch.distributed group gets it.
 
     The bootstrap is plumbing only (the World of collectives.py:94-137); all
     data-path collectives run inside libomega_b200 on the engine's stream.
     """
     import torch.distributed as dist
 
-    obj = [make_id() if dist.get_rank() == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(obj, src=src, group=group)
     return bytes(obj[0])
 
 
-def distributed_engine(dataset, pe, model, weights, config: ServeConfig, stream: int = 0) -> "ServingEngine":
-    """One CGP rank per process/GPU: rank = torch.distributed rank, P = world size."""
+def distributed_engine(dataset, pe, model, weights, config: ServeConfig, stream: int = 0,
+                       group=None) -> "ServingEngine":
+    """One CGP rank per process/GPU: rank and P from the torch.distributed group (default: the world).
+
+    Several groups can serve side by side (data parallel over CGP groups): each
+    group partitions its own copy of the graph over its P GPUs and has its own
+    NCCL communicator and NVLink exchange.
+    """
     import torch.distributed as dist
 
-    if config.strategy != "srpe-cgp" or config.num_partitions != dist.get_world_size():
-        raise ValueError("distributed_engine needs strategy='srpe-cgp' with num_partitions == world size")
-    nid = broadcast_nccl_id()
-    return ServingEngine(dataset, pe, model, weights, config, stream=stream, nccl_id=nid, rank=dist.get_rank())
+    size = dist.get_world_size(group)
+    if config.strategy != "srpe-cgp" or config.num_partitions != size:
+        raise ValueError("distributed_engine needs strategy='srpe-cgp' with num_partitions == group size")
+    nid = broadcast_nccl_id(group=group)
+    return ServingEngine(dataset, pe, model, weights, config, stream=stream, nccl_id=nid,
+                         rank=dist.get_rank(group))
 
 
 class ServingEngine:
