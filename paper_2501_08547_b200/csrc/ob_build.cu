@@ -62,23 +62,9 @@ __global__ void k_block_spans(const int32_t* __restrict__ dst_ids, const BlockCo
   }
 }
 
-// same, for a partition's source-split CSR (build_partitioned, compgraph.py:431-447)
-// -- defined in the CGP unit; the centralized path only needs the above.
-
-// largest i with ptr[i] <= e  (ptr ascending, ptr[0] = 0)
-__device__ __forceinline__ int64_t seg_of(const int64_t* __restrict__ ptr, int64_t n, int64_t e) {
-  int64_t lo = 0, hi = n;  // answer in [0, n)
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (__ldg(ptr + mid) <= e) lo = mid;
-    else hi = mid;
-  }
-  return lo;
-}
-
 // gather global source ids: one warp per aggregation work item (kAggChunk edges
 // of one destination), so a destination's CSR row and request span are copied
-// with contiguous, coalesced loads and hub destinations spread over many warps
+// with contiguous, coalesced loads and hub destinations spread over many warps.
 // SMEM variant (source bitmap fits in shared memory): each CTA marks its
 // sources in a private shared bitmap and writes it out once; k_bitmap_or
 // merges the per-CTA bitmaps.  Hub sources that appear in thousands of rows
@@ -169,8 +155,6 @@ __global__ void k_mark_ids(const int32_t* __restrict__ ids, const BlockCounters*
   const int64_t D = cnt->D;
   OB_GRID_STRIDE(i, D) bm_set(sbits, ids[i]);
 }
-
-__global__ void k_set_S(BlockCounters* cnt, const int64_t* total) { cnt->S = *total; }
 
 __global__ void k_relabel(const BlockCounters* cnt, const int32_t* __restrict__ src_global, const uint32_t* sbits,
                           const int64_t* swpre, int32_t* edge_src) {

@@ -393,7 +393,5 @@ struct StoreI64 {
 #define OB_GRID_STRIDE(i, n) \
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
-__global__ void k_fill_i32(int32_t* a, const int64_t* n_dev, int64_t n_host, int32_t v);
-__global__ void k_fill_i64(int64_t* a, const int64_t* n_dev, int64_t n_host, int64_t v);
 
 }  // namespace ob

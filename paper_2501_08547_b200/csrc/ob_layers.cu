@@ -108,8 +108,6 @@ __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restri
 // ---------------------------------------------------------------------------
 constexpr int kAggWarps = 4;
 constexpr int kSmHdr = 4;    // softmax partial rows: [max logit, sum exp, pad, pad | values]
-constexpr int kAggNV = 4;    // float4 vectors per lane per slice
-constexpr int kAggSlice = 32 * 4 * kAggNV;
 
 struct AggArgs {
   const BlockCounters* cnt;

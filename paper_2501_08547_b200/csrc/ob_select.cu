@@ -44,15 +44,6 @@ __global__ void __launch_bounds__(1024) k_scan_spine(const int64_t* n_dev, int64
   }
 }
 
-__global__ void k_fill_i32(int32_t* a, const int64_t* n_dev, int64_t n_host, int32_t v) {
-  const int64_t n = dev_count(n_dev, n_host);
-  OB_GRID_STRIDE(i, n) a[i] = v;
-}
-__global__ void k_fill_i64(int64_t* a, const int64_t* n_dev, int64_t n_host, int64_t v) {
-  const int64_t n = dev_count(n_dev, n_host);
-  OB_GRID_STRIDE(i, n) a[i] = v;
-}
-
 // warp-aggregated atomicAdd of 1 on base[slot]; returns this lane's old value
 __device__ __forceinline__ int32_t warp_agg_inc(int32_t* base, int64_t slot) {
   const unsigned act = __activemask();
@@ -282,44 +273,6 @@ __global__ void __launch_bounds__(256) k_sel_round(const uint64_t* __restrict__ 
   hist[d] = 0;
   if (threadIdx.x == 0) hist[256] = 0;
   if (!active) return;
-  const int64_t krem = rc->sel_krem;
-  if (excl < krem && krem <= excl + c) {
-    rc->sel_krem = krem - excl;
-    rc->sel_gt += excl;
-    rc->sel_prefix |= (uint64_t)d << shift;
-    rc->sel_mask |= (uint64_t)255 << shift;
-    if (shift == 0) rc->sel_eq_take = krem - excl;
-  }
-}
-
-// radix select, MSB-first 8-bit digits: find the budget-th largest key
-__global__ void k_sel_hist(const uint64_t* __restrict__ key, const ReqCounters* rc, int shift, uint32_t* hist) {
-  __shared__ uint32_t h[256];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  const int64_t R = rc->R, b = rc->budget;
-  if (b > 0 && b < R) {
-    const uint64_t pre = rc->sel_prefix, msk = rc->sel_mask;
-    OB_GRID_STRIDE(c, R) {
-      uint64_t k = key[c];
-      if ((k & msk) == pre) atomicAdd(&h[(k >> shift) & 255], 1u);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += blockDim.x)
-    if (h[i]) atomicAdd(hist + i, h[i]);
-}
-
-__global__ void __launch_bounds__(256) k_sel_pick(ReqCounters* rc, int shift, uint32_t* hist) {
-  using BS = cub::BlockScan<int64_t, 256>;
-  __shared__ typename BS::TempStorage tmp;
-  const int64_t R = rc->R, b = rc->budget;
-  const int d = 255 - threadIdx.x;  // scan from the top digit down
-  int64_t c = hist[d];
-  int64_t excl;
-  BS(tmp).ExclusiveSum(c, excl);  // keys in digits above d
-  hist[d] = 0;
-  if (!(b > 0 && b < R)) return;
   const int64_t krem = rc->sel_krem;
   if (excl < krem && krem <= excl + c) {
     rc->sel_krem = krem - excl;
