@@ -105,7 +105,6 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.cand_key = a.take<uint64_t>(p.R_max);
   w.cand_tpos = a.take<int32_t>(p.R_max);
   w.targets = a.take<int32_t>(p.T_max + 1);
-  w.sel_flag = a.take<int32_t>(p.R_max);
   w.sel_hist = a.take<uint32_t>(257);  // [256] = round completion counter
   w.rq_cnt = a.take<int32_t>(p.RB_max + 1);
   w.rq_fill = a.take<int32_t>(p.RB_max + 1);

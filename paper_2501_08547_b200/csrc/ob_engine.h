@@ -231,7 +231,6 @@ struct RequestWs {
   uint64_t* cand_key = nullptr;    // [R]
   int32_t* cand_tpos = nullptr;    // [R] position in targets or -1
   int32_t* targets = nullptr;      // [T]
-  int32_t* sel_flag = nullptr;     // [R]
   int64_t* sel_pos = nullptr;      // [R+1]
   uint32_t* sel_hist = nullptr;    // [256]
   // request CSR by destination slot (slot: candidate rank, or R + query)

@@ -283,41 +283,42 @@ __global__ void __launch_bounds__(256) k_sel_round(const uint64_t* __restrict__ 
   }
 }
 
-struct EqLoad {
+// Ordered compaction of the selection in one scan over (above-threshold,
+// at-threshold) counts: candidate c is selected when its key is above the
+// threshold, or equal to it with fewer than eq_take equal keys before it (ties
+// go to the lowest ids, policy.py:131); its target position is then
+// (# above before c) + min(# equal before c, eq_take).
+struct SelLoad {
   const uint64_t* key;
   const ReqCounters* rc;
-  __device__ int64_t operator()(int64_t c) const {
+  __device__ I3 operator()(int64_t c) const {
     const int64_t R = rc->R, b = rc->budget;
-    return (b > 0 && b < R && key[c] == rc->sel_prefix) ? 1 : 0;
+    if (b <= 0) return I3(0);
+    if (b >= R) return I3(1, 0, 0);
+    const uint64_t k = key[c], thr = rc->sel_prefix;
+    return I3(k > thr ? 1 : 0, k == thr ? 1 : 0, 0);
   }
 };
-// selected = above the threshold, or at it among the lowest ids (score desc, id asc)
-struct EqStore {
-  int32_t* flag;
-  const uint64_t* key;
-  const ReqCounters* rc;
-  __device__ void operator()(int64_t c, int64_t eqpos) const {
-    const int64_t R = rc->R, b = rc->budget;
-    int sel;
-    if (b <= 0) sel = 0;
-    else if (b >= R) sel = 1;
-    else {
-      uint64_t k = key[c], thr = rc->sel_prefix;
-      sel = (k > thr) || (k == thr && eqpos < rc->sel_eq_take);
-    }
-    flag[c] = sel;
-  }
-};
-struct SelStore {
-  const int32_t* flag;
+struct SelStore3 {
+  SelLoad ld;
   const int32_t* cand_ids;
   int32_t* targets;
   int32_t* tpos;
-  __device__ void operator()(int64_t c, int64_t pos) const {
-    if (flag[c]) {
+  __device__ void operator()(int64_t c, const I3& pre) const {
+    const I3 me = ld(c);
+    const int64_t take = ld.rc->sel_eq_take;
+    if (me.a || (me.b && pre.b < take)) {
+      const int64_t pos = pre.a + (pre.b < take ? pre.b : take);
       targets[pos] = cand_ids[c];
       tpos[c] = (int32_t)pos;
     }
+  }
+};
+struct SelTotal {
+  ReqCounters* rc;
+  __device__ void operator()(int64_t, const I3& t) const {
+    const int64_t take = rc->sel_eq_take;
+    rc->T = t.a + (t.b < take ? t.b : take);
   }
 };
 
@@ -559,10 +560,9 @@ void stage_select(Engine& e, RequestWs& w) {
     OB_LAUNCHED();
   }
   // ordered compaction: ties at the threshold resolved by ascending id
-  device_scan(s, e.scan, EqLoad{w.cand_key, w.rc}, EqStore{w.sel_flag, w.cand_key, w.rc}, &w.rc->R, 0, r_max,
-              nullptr);
-  device_scan(s, e.scan, LoadI32{w.sel_flag}, SelStore{w.sel_flag, w.cand_ids, w.targets, w.cand_tpos}, &w.rc->R, 0,
-              r_max, &w.rc->T);
+  const SelLoad ld{w.cand_key, w.rc};
+  device_scan_t<I3>(s, e.scan, ld, SelStore3{ld, w.cand_ids, w.targets, w.cand_tpos}, SelTotal{w.rc}, &w.rc->R, 0,
+                    r_max);
 }
 
 // Request CSR over an edge set (the whole request via the parameter block when
