@@ -60,3 +60,36 @@ def test_bench_cgp_config_is_consistent():
     assert (n, F, kind, k, H, B) == (233_000, 602, "sage_mean", 3, 128, 1024)
     with pytest.raises(KeyError):
         bench.CONFIGS["nope"]
+
+
+def _group_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2501_08547_b200 import runtime
+
+    P = 2  # CGP groups of two (bench.py --cgp-size 2): every rank creates every group
+    groups = [dist.new_group(list(range(g * P, (g + 1) * P))) for g in range(world // P)]
+    mine = groups[rank // P]
+    nid = runtime.broadcast_nccl_id(make_id=lambda: bytes([rank]) * 128, group=mine)
+    q.put((rank, dist.get_rank(mine), nid))
+    dist.destroy_process_group()
+
+
+def test_nccl_id_per_cgp_group():
+    """Each CGP group's leader draws its own id; members get their leader's, not rank 0's."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 4
+    procs = [ctx.Process(target=_group_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {r: (gr, nid) for r, gr, nid in (q.get(timeout=180) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [got[r][0] for r in range(world)] == [0, 1, 0, 1]
+    assert got[0][1] == got[1][1] == bytes([0]) * 128
+    assert got[2][1] == got[3][1] == bytes([2]) * 128
