@@ -32,6 +32,9 @@ Engine::~Engine() {
   for (auto& ev_ : ev)
     if (ev_) cudaEventDestroy(ev_);
   if (own_stream && stream) cudaStreamDestroy(stream);
+  if (side) cudaStreamDestroy(side);
+  if (fork_ev) cudaEventDestroy(fork_ev);
+  if (join_ev) cudaEventDestroy(join_ev);
 }
 
 // sum of the r largest in-degrees: bound on the CSR edges r destinations can pull
@@ -304,11 +307,26 @@ static void enqueue_stages(Engine& e, float* d_out) {
   }
   cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, srpe);
+  // the request-index sort (side stream) and the top-k selection (main stream)
+  // only share read-only inputs from here on: run them side by side
+  OB_CUDA(cudaEventRecord(e.fork_ev, s));
+  OB_CUDA(cudaStreamWaitEvent(e.side, e.fork_ev, 0));
+  {
+    e.stream = e.side;  // stage functions launch on e.stream
+    cudaEvent_t pc = prof_begin(e.side);
+    try {
+      stage_request_csr(e, w);
+    } catch (...) {
+      e.stream = s;
+      throw;
+    }
+    prof_end(e.side, pc, kProfCsr, nullptr, 0, 0, 0, 0, 0);
+    e.stream = s;
+  }
   if (srpe) stage_select(e, w);
   prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
-  p0 = prof_begin(s);
-  stage_request_csr(e, w);
-  prof_end(s, p0, kProfCsr, nullptr, 0, 0, 0, 0, 0);
+  OB_CUDA(cudaEventRecord(e.join_ev, e.side));
+  OB_CUDA(cudaStreamWaitEvent(s, e.join_ev, 0));
   p0 = prof_begin(s);
   if (srpe) stage_build_srpe(e, w);
   else stage_build_full(e, w);
@@ -651,6 +669,9 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
       e.own_stream = true;
     }
     for (auto& ev_ : e.ev) OB_CUDA(cudaEventCreate(&ev_));
+    OB_CUDA(cudaStreamCreateWithFlags(&e.side, cudaStreamNonBlocking));
+    OB_CUDA(cudaEventCreateWithFlags(&e.fork_ev, cudaEventDisableTiming));
+    OB_CUDA(cudaEventCreateWithFlags(&e.join_ev, cudaEventDisableTiming));
     configure_fill();
     if (const char* v = std::getenv("OB_NO_GRAPHS")) e.use_graphs = !(v[0] && v[0] != '0');
     if (cfg->nccl_id && cfg->strategy == OB_STRATEGY_SRPE_CGP) {

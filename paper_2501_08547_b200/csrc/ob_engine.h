@@ -582,6 +582,10 @@ struct Engine {
   CgpState cgp;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // side stream for independent request stages (request-index sort next to the
+  // top-k selection); forked and joined with events, so captured graphs branch
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   GraphDev g;
   std::vector<LayerDev> layers;
   std::vector<float*> pe;        // per stored layer, N x ld4(dim)
