@@ -35,6 +35,7 @@ Engine::~Engine() {
   if (side) cudaStreamDestroy(side);
   if (fork_ev) cudaEventDestroy(fork_ev);
   if (join_ev) cudaEventDestroy(join_ev);
+  if (csr_ev) cudaEventDestroy(csr_ev);
 }
 
 // sum of the r largest in-degrees: bound on the CSR edges r destinations can pull
@@ -118,9 +119,6 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.rx_cnt = a.take<int32_t>(256 * rx_tiles(m));
   w.rx_off = a.take<int64_t>(256 * rx_tiles(m) + 1);
   w.rq_ctr = a.take<int64_t>(4);
-  w.sbits = a.take<uint32_t>(p.words_NB + 1);
-  w.fill_bits = p.words_NB <= 48 * 1024 ? a.take<uint32_t>(kNumSMs * (p.words_NB + 1)) : nullptr;
-  w.swpre = a.take<int64_t>(p.words_NB + 1);
   int64_t Emax = 1, Dmax = 1, Smax = 1, Imax = 1;
   for (auto& b : p.blocks) {
     Emax = std::max(Emax, b.E_max);
@@ -128,12 +126,20 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     Smax = std::max(Smax, b.S_max);
     Imax = std::max(Imax, b.items_max);
   }
-  w.src_global = a.take<int32_t>(Emax);
-  w.seg_len = a.take<int64_t>(Dmax);
-  w.span_cs = a.take<int64_t>(Dmax);
-  w.span_cl = a.take<int32_t>(Dmax);
-  w.span_rs = a.take<int64_t>(Dmax);
-  w.span_rl = a.take<int32_t>(Dmax);
+  auto take_scratch = [&](BuildScratch& sc, int64_t D, int64_t E) {
+    sc.sbits = a.take<uint32_t>(p.words_NB + 1);
+    sc.fill_bits = p.words_NB <= 48 * 1024 ? a.take<uint32_t>(kNumSMs * (p.words_NB + 1)) : nullptr;
+    sc.swpre = a.take<int64_t>(p.words_NB + 1);
+    sc.src_global = a.take<int32_t>(E);
+    sc.seg_len = a.take<int64_t>(D);
+    sc.span_cs = a.take<int64_t>(D);
+    sc.span_cl = a.take<int32_t>(D);
+    sc.span_rs = a.take<int64_t>(D);
+    sc.span_rl = a.take<int32_t>(D);
+  };
+  take_scratch(w.bs[0], Dmax, Emax);
+  if (e.cfg.strategy != OB_STRATEGY_FULL) take_scratch(w.bs[1], p.blocks[1].D_max, p.blocks[1].E_max);  // query block
+  else w.bs[1] = w.bs[0];
   w.blocks = p.blocks;
   for (size_t i = 0; i < w.blocks.size(); ++i) {
     BlockDev& b = w.blocks[i];
@@ -309,28 +315,36 @@ static void enqueue_stages(Engine& e, float* d_out) {
   stage_request_prep(e, w, srpe);
   // the request-index sort (side stream) and the top-k selection (main stream)
   // only share read-only inputs from here on: run them side by side
+  // and, under srpe, the query block (it needs only the index) follows the sort there
   OB_CUDA(cudaEventRecord(e.fork_ev, s));
   OB_CUDA(cudaStreamWaitEvent(e.side, e.fork_ev, 0));
   {
     e.stream = e.side;  // stage functions launch on e.stream
-    cudaEvent_t pc = prof_begin(e.side);
     try {
+      cudaEvent_t pc = prof_begin(e.side);
       stage_request_csr(e, w);
+      prof_end(e.side, pc, kProfCsr, nullptr, 0, 0, 0, 0, 0);
+      OB_CUDA(cudaEventRecord(e.csr_ev, e.side));
+      if (srpe) {
+        pc = prof_begin(e.side);
+        build_query_block(e, w);
+        prof_end(e.side, pc, kProfBuild, nullptr, 0, 0, 0, 0, 0);
+      }
     } catch (...) {
       e.stream = s;
       throw;
     }
-    prof_end(e.side, pc, kProfCsr, nullptr, 0, 0, 0, 0, 0);
     e.stream = s;
   }
   if (srpe) stage_select(e, w);
   prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
-  OB_CUDA(cudaEventRecord(e.join_ev, e.side));
-  OB_CUDA(cudaStreamWaitEvent(s, e.join_ev, 0));
+  OB_CUDA(cudaStreamWaitEvent(s, e.csr_ev, 0));
   p0 = prof_begin(s);
-  if (srpe) stage_build_srpe(e, w);
+  if (srpe) build_mid_block(e, w);
   else stage_build_full(e, w);
   prof_end(s, p0, kProfBuild, nullptr, 0, 0, 0, 0, 0);
+  OB_CUDA(cudaEventRecord(e.join_ev, e.side));
+  OB_CUDA(cudaStreamWaitEvent(s, e.join_ev, 0));
   record_mark(e.ev[1], s);
   stage_forward(e, w, d_out);
 }
@@ -672,6 +686,7 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
     OB_CUDA(cudaStreamCreateWithFlags(&e.side, cudaStreamNonBlocking));
     OB_CUDA(cudaEventCreateWithFlags(&e.fork_ev, cudaEventDisableTiming));
     OB_CUDA(cudaEventCreateWithFlags(&e.join_ev, cudaEventDisableTiming));
+    OB_CUDA(cudaEventCreateWithFlags(&e.csr_ev, cudaEventDisableTiming));
     configure_fill();
     if (const char* v = std::getenv("OB_NO_GRAPHS")) e.use_graphs = !(v[0] && v[0] != '0');
     if (cfg->nccl_id && cfg->strategy == OB_STRATEGY_SRPE_CGP) {

@@ -186,43 +186,43 @@ __global__ void k_copy_count_D(BlockCounters* dst, const BlockCounters* src) { d
 // generic block assembly over an already written dst list + counts->D.
 // `src` names the CSR the destinations pull from (the whole graph, or a CGP
 // rank's source-split CSR) and the request CSR (whole request or the rank's slice).
-void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src) {
+void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const BuildScratch& sc) {
   cudaStream_t s = e.stream;
   SegSpans sp;  // transient, shared by every block of the request
-  sp.cs = w.span_cs;
-  sp.cl = w.span_cl;
-  sp.rs = w.span_rs;
-  sp.rl = w.span_rl;
+  sp.cs = sc.span_cs;
+  sp.cl = sc.span_cl;
+  sp.rs = sc.span_rs;
+  sp.rl = sc.span_rl;
   k_block_spans<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, e.g.N, src.offsets, src.deg, w.cbits,
-                                                        w.cwpre, src.rq_ptr, w.rc, sp, w.seg_len);
+                                                        w.cwpre, src.rq_ptr, w.rc, sp, sc.seg_len);
   OB_LAUNCHED();
   // dst_ptr / item_ptr / group_ptr (+ E, items, groups) in one pass; the work
   // items double as the fill's edge chunks
   const BlockStore3 st{b.dst_ptr, b.item_ptr, b.group_ptr};
-  device_scan_t<I3>(s, e.scan, SegLenLoad3{w.seg_len}, st, BlockTotal3{st, b.cnt}, &b.cnt->D, 0, b.D_max);
+  device_scan_t<I3>(s, e.scan, SegLenLoad3{sc.seg_len}, st, BlockTotal3{st, b.cnt}, &b.cnt->D, 0, b.D_max);
   expand_items(s, b.cnt, b.D_max, b.item_ptr, b.group_ptr, b.item_dst, b.group_dst);
   if (w.words_NB <= kFillSmemWords) {  // per-CTA shared bitmaps, then one OR pass
     const int64_t words = w.words_NB + 1;
     k_block_fill<true><<<kNumSMs, 1024, words * 4, s>>>(b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs,
-                                                        src.rq_src, w.src_global, nullptr, words, w.fill_bits);
-    k_bitmap_or<<<grid_for(words, 256), 256, 0, s>>>(w.fill_bits, kNumSMs, words, w.sbits);
+                                                        src.rq_src, sc.src_global, nullptr, words, sc.fill_bits);
+    k_bitmap_or<<<grid_for(words, 256), 256, 0, s>>>(sc.fill_bits, kNumSMs, words, sc.sbits);
     g_launches += 2;
   } else {
-    OB_CUDA(cudaMemsetAsync(w.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
+    OB_CUDA(cudaMemsetAsync(sc.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
     k_block_fill<false><<<grid_for(b.items_max, 32, kNumSMs * 2), 1024, 0, s>>>(
-        b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs, src.rq_src, w.src_global, w.sbits, 0, nullptr);
+        b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs, src.rq_src, sc.src_global, sc.sbits, 0, nullptr);
     OB_LAUNCHED();
   }
   if (b.has_self) {
-    k_mark_ids<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, w.sbits);
+    k_mark_ids<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, sc.sbits);
     OB_LAUNCHED();
   }
-  device_scan(s, e.scan, LoadPopc{w.sbits}, StoreI64{w.swpre}, nullptr, w.words_NB, w.words_NB, &b.cnt->S, w.swpre);
-  k_bitmap_compact_ext(e, w.sbits, w.swpre, w.words_NB, b.src_ids);
-  k_relabel<<<grid_for(b.E_max, 256), 256, 0, s>>>(b.cnt, w.src_global, w.sbits, w.swpre, b.edge_src);
+  device_scan(s, e.scan, LoadPopc{sc.sbits}, StoreI64{sc.swpre}, nullptr, w.words_NB, w.words_NB, &b.cnt->S, sc.swpre);
+  k_bitmap_compact_ext(e, sc.sbits, sc.swpre, w.words_NB, b.src_ids);
+  k_relabel<<<grid_for(b.E_max, 256), 256, 0, s>>>(b.cnt, sc.src_global, sc.sbits, sc.swpre, b.edge_src);
   OB_LAUNCHED();
   if (b.has_self) {
-    k_self_rows<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.cnt, b.dst_ids, w.sbits, w.swpre, b.self_src);
+    k_self_rows<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.cnt, b.dst_ids, sc.sbits, sc.swpre, b.self_src);
     OB_LAUNCHED();
   }
 }
@@ -241,9 +241,22 @@ void stage_build_srpe(Engine& e, RequestWs& w) {
   // blocks[0] = shared mid block (layers 1..k-1), blocks[1] = last block (layer k)
   const SpanSrc src{e.g.offsets, e.g.nbrs, e.g.indeg, w.rq_ptr, w.rq_src};
   write_mid_dst(e, w, w.blocks[0]);
-  assemble(e, w, w.blocks[0], src);
+  assemble(e, w, w.blocks[0], src, w.bs[0]);
   write_query_dst(e, w, w.blocks[1]);
-  assemble(e, w, w.blocks[1], src);
+  assemble(e, w, w.blocks[1], src, w.bs[1]);
+}
+
+// the two srpe blocks separately: the query block needs only the request index,
+// the mid block also the targets (stage_build_srpe = both, in order)
+void build_query_block(Engine& e, RequestWs& w) {
+  const SpanSrc src{e.g.offsets, e.g.nbrs, e.g.indeg, w.rq_ptr, w.rq_src};
+  write_query_dst(e, w, w.blocks[1]);
+  assemble(e, w, w.blocks[1], src, w.bs[1]);
+}
+void build_mid_block(Engine& e, RequestWs& w) {
+  const SpanSrc src{e.g.offsets, e.g.nbrs, e.g.indeg, w.rq_ptr, w.rq_src};
+  write_mid_dst(e, w, w.blocks[0]);
+  assemble(e, w, w.blocks[0], src, w.bs[0]);
 }
 
 void stage_build_full(Engine& e, RequestWs& w) {
@@ -259,7 +272,7 @@ void stage_build_full(Engine& e, RequestWs& w) {
       k_copy_count_D<<<1, 1, 0, s>>>(b.cnt, up.cnt);
       OB_LAUNCHED();
     }
-    assemble(e, w, b, src);
+    assemble(e, w, b, src, w.bs[0]);
   }
 }
 

@@ -495,9 +495,9 @@ void serve_cgp(Engine& e, float* d_out) {
     build_rq_csr(e, w, pw.ledges, w.m, pw.rq.ctr, pw.rq, /*counts_ready=*/false);
     const SpanSrc src{part.off, part.src, part.deg, pw.rq.ptr, pw.rq.src};
     write_mid_dst(e, w, pw.blocks[0]);
-    assemble(e, w, pw.blocks[0], src);
+    assemble(e, w, pw.blocks[0], src, w.bs[0]);
     write_query_dst(e, w, pw.blocks[1]);
-    assemble(e, w, pw.blocks[1], src);
+    assemble(e, w, pw.blocks[1], src, w.bs[0]);
   }
   prof_end(s, p0, kProfBuild, nullptr, 0, 0, 0, 0, 0);
   record_mark(e.ev[1], s);

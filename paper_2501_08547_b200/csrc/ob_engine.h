@@ -212,6 +212,20 @@ __device__ __forceinline__ void ld_edge(const int64_t* __restrict__ edges, int64
   }
 }
 
+// Scratch of one block assembly (two sets: the query block is assembled on the
+// side stream while the mid block is assembled on the main stream).
+struct BuildScratch {
+  uint32_t* sbits = nullptr;       // source bitmap over [0, N+B)
+  uint32_t* fill_bits = nullptr;   // [148][words_NB+1] per-CTA source bitmaps (small N only)
+  int64_t* swpre = nullptr;        // [words_NB+1] popcount prefix
+  int32_t* src_global = nullptr;   // [E] global source id per edge
+  int64_t* seg_len = nullptr;      // [D] CSR span + request span per destination
+  int64_t* span_cs = nullptr;      // [D] CSR start/len, request start/len
+  int32_t* span_cl = nullptr;
+  int64_t* span_rs = nullptr;
+  int32_t* span_rl = nullptr;
+};
+
 // Per-request device workspace for the centralized pipeline.
 struct RequestWs {
   int B = 0;
@@ -257,15 +271,6 @@ struct RequestWs {
     return c;
   }
   // block scratch
-  uint32_t* sbits = nullptr;       // source bitmap over [0, N+B)
-  uint32_t* fill_bits = nullptr;   // [148][words_NB+1] per-CTA source bitmaps (small N only)
-  int64_t* swpre = nullptr;
-  int32_t* src_global = nullptr;   // [E_max] gathered global source ids
-  int64_t* seg_len = nullptr;      // [D_max]
-  int64_t* span_cs = nullptr;      // [Dmax] block-assembly spans (CSR start/len, request start/len)
-  int32_t* span_cl = nullptr;
-  int64_t* span_rs = nullptr;
-  int32_t* span_rl = nullptr;
   // blocks
   std::vector<BlockDev> blocks;    // blocks[l-1] feeds layer l (mid blocks may alias)
   std::vector<int> block_of_layer; // layer -> index into blocks
@@ -281,6 +286,7 @@ struct RequestWs {
   float* s_dst = nullptr;          // gat: [D_max]
   float* mean = nullptr;           // moments: [D_max][in]
   int64_t words_N = 0, words_NB = 0;
+  BuildScratch bs[2];
 };
 
 // in-library kernel profiler (CUDA events on the launching stream) -------------
@@ -470,7 +476,9 @@ struct SpanSrc {
   const int64_t* rq_ptr;   // request CSR (whole request or the rank's slice)
   const int32_t* rq_src;
 };
-void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src);
+void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const BuildScratch& sc);
+void build_query_block(Engine& e, RequestWs& w);
+void build_mid_block(Engine& e, RequestWs& w);
 void write_mid_dst(Engine& e, RequestWs& w, BlockDev& b);
 void write_query_dst(Engine& e, RequestWs& w, BlockDev& b);
 void stage_build_srpe(Engine& e, RequestWs& w);
@@ -585,7 +593,7 @@ struct Engine {
   // side stream for independent request stages (request-index sort next to the
   // top-k selection); forked and joined with events, so captured graphs branch
   cudaStream_t side = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, csr_ev = nullptr;
   GraphDev g;
   std::vector<LayerDev> layers;
   std::vector<float*> pe;        // per stored layer, N x ld4(dim)
