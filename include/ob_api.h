@@ -53,8 +53,10 @@ enum ob_status {
 /* ServeConfig.strategy (runtime.py:51); "sampled" is out of scope. */
 enum ob_strategy { OB_STRATEGY_FULL = 0, OB_STRATEGY_SRPE = 2, OB_STRATEGY_SRPE_CGP = 3 };
 
-/* ServeConfig.policy (policy.py:29-32); only the ratio policy is on the hot path. */
-enum ob_policy { OB_POLICY_RATIO = 0 };
+/* ServeConfig.policy (policy.py:29-32): ratio (policy.py:77-81) and importance
+   (policy.py:84-107; under srpe-cgp the per-partition numerators are summed in
+   rank order, runtime.py:168-175). */
+enum ob_policy { OB_POLICY_RATIO = 0, OB_POLICY_IS = 1 };
 
 /* Layer kinds use the reference's on-disk tags (models.py:36 KIND_TAGS). */
 enum ob_kind {

@@ -193,6 +193,47 @@ def ratio_scores(nq: np.ndarray, total: np.ndarray) -> np.ndarray:
     return nq.astype(np.float64) / total.astype(np.float64)
 
 
+def _is_terms(srcs: np.ndarray, train_deg: np.ndarray) -> np.ndarray:
+    nd = train_deg[srcs].astype(np.float64)
+    return np.where(nd > 0, 1.0 / np.maximum(nd, 1.0), 0.0)
+
+
+def importance_scores(ids: np.ndarray, offsets: np.ndarray, nbrs: np.ndarray, train_deg: np.ndarray) -> np.ndarray:
+    """score_importance (policy.py:84-95): (1/deg v) * sum_{u in N(v)} 1/deg u, fp64.
+
+    The row sum is numpy's pairwise ``np.sum`` over the CSR row in order (the
+    exact association the CUDA path reproduces); zero-in-degree rows score 0.
+    """
+    out = np.zeros(len(ids), dtype=np.float64)
+    deg = np.asarray(train_deg)
+    for i, v in enumerate(np.asarray(ids, dtype=_I64)):
+        d = float(deg[v])
+        if d <= 0:
+            continue
+        out[i] = np.sum(_is_terms(nbrs[offsets[v]:offsets[v + 1]], deg)) / d
+    return out
+
+
+def importance_partial_sums(ids: np.ndarray, part_offsets: np.ndarray, part_srcs: np.ndarray,
+                            train_deg: np.ndarray) -> np.ndarray:
+    """importance_partial_sums (policy.py:98-107): one partition's share of each numerator."""
+    out = np.zeros(len(ids), dtype=np.float64)
+    for i, v in enumerate(np.asarray(ids, dtype=_I64)):
+        srcs = part_srcs[part_offsets[v]:part_offsets[v + 1]]
+        if srcs.size:
+            out[i] = np.sum(_is_terms(srcs, train_deg))
+    return out
+
+
+def importance_scores_distributed(ids: np.ndarray, partials: list, train_deg: np.ndarray) -> np.ndarray:
+    """select_targets_distributed's IS branch (runtime.py:168-175): partials summed in rank order."""
+    sums = np.zeros(len(ids), dtype=np.float64)
+    for p in partials:
+        sums += p
+    deg = np.asarray(train_deg)[np.asarray(ids, dtype=_I64)].astype(np.float64)
+    return np.where(deg > 0, sums / np.maximum(deg, 1.0), 0.0)
+
+
 def select_top(ids: np.ndarray, scores: np.ndarray, gamma: float) -> np.ndarray:
     """select_targets (policy.py:110-135): top floor(gamma*|R|), score desc, id asc."""
     if not 0.0 <= gamma <= 1.0:

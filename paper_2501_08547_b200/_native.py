@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libomega_b200.so")
 
 OB_OK, OB_EINVAL, OB_ENOTFOUND, OB_ECOMM, OB_ECUDA, OB_ENOMEM, OB_ESTATE = range(7)
 STRATEGY = {"full": 0, "srpe": 2, "srpe-cgp": 3}
-POLICY = {"ratio": 0}
+POLICY = {"ratio": 0, "is": 1}
 KIND_TAGS = {"gcn": 0, "sage_mean": 1, "gat": 2, "power_mean": 3, "moments": 4, "sage_max": 5}
 
 

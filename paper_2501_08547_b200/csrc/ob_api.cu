@@ -107,6 +107,9 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.cand_nq = a.take<int32_t>(p.R_max);
   w.cand_score = a.take<double>(p.R_max);
   w.cand_key = a.take<uint64_t>(p.R_max);
+  // IS numerators: one array centralized, one per partition under CGP emulation,
+  // [P][R] for the NCCL all-gather fallback
+  w.is_part = e.cfg.policy == OB_POLICY_IS ? a.take<double>(p.R_max * std::max(1, e.cfg.num_partitions)) : nullptr;
   w.cand_tpos = a.take<int32_t>(p.R_max);
   w.targets = a.take<int32_t>(p.T_max + 1);
   w.sel_hist = a.take<uint32_t>(257);  // [256] = round completion counter
@@ -663,7 +666,8 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
     OB_CHECK(cfg->strategy == OB_STRATEGY_FULL || cfg->strategy == OB_STRATEGY_SRPE ||
                  cfg->strategy == OB_STRATEGY_SRPE_CGP,
              OB_EINVAL, "unknown strategy");
-    OB_CHECK(cfg->policy == OB_POLICY_RATIO, OB_EINVAL, "only the ratio policy runs on the device");
+    OB_CHECK(cfg->policy == OB_POLICY_RATIO || cfg->policy == OB_POLICY_IS, OB_EINVAL,
+             "unknown policy (ratio and is run on the device)");
     OB_CHECK(cfg->num_partitions >= 1, OB_EINVAL, "num_partitions must be >= 1");
     OB_CHECK(cfg->strategy == OB_STRATEGY_SRPE_CGP || cfg->num_partitions == 1, OB_EINVAL,
              "num_partitions > 1 needs strategy srpe-cgp");

@@ -341,7 +341,9 @@ void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
   const size_t parts_b = (((size_t)c.D_max * c.ldp * esz + 255) & ~(size_t)255) + (size_t)c.D_max * 4;
   const size_t mean_b = mom ? (size_t)c.D_max * ld4(maxw) * 8 : 0;
   const size_t fin_b = (size_t)w.B * e.layers.back().spec.out_dim * 4;
-  c.x_need_region = (std::max(std::max(parts_b, mean_b), std::max(fin_b, (size_t)c.D_max * 4)) + 4095) & ~(size_t)4095;
+  const size_t is_b = e.cfg.policy == OB_POLICY_IS ? (size_t)std::min<int64_t>(e.g.N, 2 * w.m) * 8 : 0;
+  c.x_need_region = (std::max(std::max(std::max(parts_b, mean_b), std::max(fin_b, (size_t)c.D_max * 4)), is_b) + 4095) &
+                    ~(size_t)4095;
 }
 
 #ifdef OB_WITH_NCCL
@@ -475,9 +477,53 @@ void serve_cgp(Engine& e, float* d_out) {
   const int np = (int)c.parts.size();
   const int64_t N = e.g.N;
   c.collective_bytes = 0;
+  const bool p2p = c.nccl && c.p2p;
+  const XCtx x = p2p ? xctx(e) : XCtx{};
+  int xj = 0;  // exchange step within this request (selects the region)
+  c.nvlink_bytes = 0;
+  auto x_begin = [&] { x_launch(s, k_x_begin, x); };
+  auto x_exchange = [&] {  // publish this rank's region, wait for everyone's
+    cudaEvent_t pc = prof_begin(s);
+    x_launch(s, k_x_publish, x);
+    x_launch(s, k_x_wait, x);
+    prof_end(s, pc, kProfComm, nullptr, 0, 0, 0, 0, 0);
+  };
+  auto x_done = [&] {
+    x_launch(s, k_x_done, x);
+    ++xj;
+  };
   // identical plan on every rank from the whole request (runtime.py:151-192)
   cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, true);
+  const int64_t r_max = std::min<int64_t>(N, 2 * w.m);
+  if (e.cfg.policy == OB_POLICY_IS && r_max > 0) {
+    // importance numerators per partition over its source-split CSR
+    // (policy.py:98-107), summed in rank order on every rank (runtime.py:168-175)
+    IsParts ip{};
+    ip.P = c.P;
+    if (p2p) {
+      x_begin();
+      launch_is_partial(e, w, c.parts[0].off, c.parts[0].src, reinterpret_cast<double*>(xregion_ptr(c, xj)));
+      x_exchange();
+      for (int q = 0; q < c.P; ++q)
+        ip.part[q] = reinterpret_cast<const double*>(c.xpeer[q] + kXFlags + xoff(c, xj));
+      launch_score_is(e, w, ip);
+      x_done();
+      c.nvlink_bytes += r_max * 8 * (c.P - 1);
+    } else {
+      for (int p = 0; p < np; ++p)
+        launch_is_partial(e, w, c.parts[p].off, c.parts[p].src, w.is_part + (int64_t)c.parts[p].rank * r_max);
+#ifdef OB_WITH_NCCL
+      if (c.nccl) {
+        OB_NCCL(ncclAllGather(w.is_part + (int64_t)c.my_rank * r_max, w.is_part, (size_t)r_max, ncclDouble,
+                              (ncclComm_t)c.comm, s));
+        c.collective_bytes += r_max * 8 * (c.P - 1);
+      }
+#endif
+      for (int q = 0; q < c.P; ++q) ip.part[q] = w.is_part + (int64_t)q * r_max;
+      launch_score_is(e, w, ip);
+    }
+  }
   stage_select(e, w);
   prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
   p0 = prof_begin(s);
@@ -504,10 +550,6 @@ void serve_cgp(Engine& e, float* d_out) {
   stage_qpad(e, w);
   OB_CUDA(cudaMemsetAsync(c.zero_row, 0, sizeof(float) * (ld4(std::max(e.g.F, 4)) + 512), s));
   const int64_t part_stride_f = c.D_max * c.ldp;  // floats between partitions (x2 for float64 partials)
-  const bool p2p = c.nccl && c.p2p;
-  const XCtx x = p2p ? xctx(e) : XCtx{};
-  int xj = 0;  // exchange step within this request (selects the region)
-  c.nvlink_bytes = 0;
   OwnerFilter own{};
   if (p2p) {
     own.owner = c.owner;
@@ -515,17 +557,6 @@ void serve_cgp(Engine& e, float* d_out) {
     own.P = c.P;
     own.rank = c.my_rank;
   }
-  auto x_begin = [&] { x_launch(s, k_x_begin, x); };
-  auto x_exchange = [&] {  // publish this rank's region, wait for everyone's
-    cudaEvent_t pc = prof_begin(s);
-    x_launch(s, k_x_publish, x);
-    x_launch(s, k_x_wait, x);
-    prof_end(s, pc, kProfComm, nullptr, 0, 0, 0, 0, 0);
-  };
-  auto x_done = [&] {
-    x_launch(s, k_x_done, x);
-    ++xj;
-  };
   for (int l = 1; l <= k; ++l) {
     const LayerDev& L = e.layers[l - 1];
     const int bi = l < k ? 0 : 1;
@@ -699,7 +730,7 @@ void cgp_ensure_exchange(Engine& e) {
 #ifdef OB_WITH_NCCL
   CgpState& c = e.cgp;
   if (!c.nccl || !c.p2p) return;
-  const int steps = 4 * (int)e.layers.size() + 2;
+  const int steps = 4 * (int)e.layers.size() + 3;  // + the IS numerator exchange
   if (c.xbuf && c.x_need_region <= c.xregion && steps <= c.xsteps) return;
   cudaStream_t s = e.stream;
   OB_CUDA(cudaStreamSynchronize(s));

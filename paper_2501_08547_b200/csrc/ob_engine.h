@@ -243,6 +243,7 @@ struct RequestWs {
   int32_t* cand_nq = nullptr;      // [R]
   double* cand_score = nullptr;    // [R]
   uint64_t* cand_key = nullptr;    // [R]
+  double* is_part = nullptr;       // [R] IS numerators (centralized; CGP: [P][R])
   int32_t* cand_tpos = nullptr;    // [R] position in targets or -1
   int32_t* targets = nullptr;      // [T]
   int64_t* sel_pos = nullptr;      // [R+1]
@@ -367,6 +368,11 @@ struct PartPtrs {
   const float* lp[kMaxParts];
   const float* cnt[kMaxParts];
 };
+// IS policy: per-partition numerator arrays [R] summed in rank order (own / peers' buffers)
+struct IsParts {
+  const double* part[kMaxParts];
+  int P;
+};
 // NCCL mode: a rank merges / updates only the destinations it owns
 struct OwnerFilter {
   const int32_t* owner = nullptr;  // null: every destination
@@ -465,6 +471,8 @@ void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, 
 
 void stage_request_prep(Engine& e, RequestWs& w, bool need_scores);
 void stage_select(Engine& e, RequestWs& w);
+void launch_is_partial(Engine& e, RequestWs& w, const int64_t* off, const int32_t* src, double* out);
+void launch_score_is(Engine& e, RequestWs& w, const IsParts& parts);
 void stage_request_csr(Engine& e, RequestWs& w);
 void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound, const int64_t* m_dev, RqCsr& c,
                   bool counts_ready);

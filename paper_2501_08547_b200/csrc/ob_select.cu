@@ -203,22 +203,270 @@ __global__ void k_zero_slots(const ReqCounters* rc, int B, int32_t* a, int32_t* 
 // ---------------------------------------------------------------------------
 // 2. ratio scores (policy.py:77-81) and budget
 // ---------------------------------------------------------------------------
+// ratio == false (IS policy): counts only; k_score_is writes the scores and the
+// zero-total check does not apply (score_importance never divides by the total)
 __global__ void k_score(const int32_t* __restrict__ cand_ids, const int32_t* __restrict__ rq_cnt,
                         const int32_t* __restrict__ indeg, ReqCounters* rc, int32_t* cand_nq, double* score,
-                        uint64_t* key, int32_t* tpos) {
+                        uint64_t* key, int32_t* tpos, bool ratio) {
   const int64_t R = rc->R;
   bool bad = false;
   OB_GRID_STRIDE(c, R) {
     int32_t nq = rq_cnt[c];
+    cand_nq[c] = nq;
+    tpos[c] = -1;
+    if (!ratio) continue;
     int64_t total = (int64_t)indeg[cand_ids[c]] + nq;
     if (total <= 0) bad = true;
     double s = total > 0 ? (double)nq / (double)total : 0.0;
-    cand_nq[c] = nq;
     score[c] = s;
     key[c] = (uint64_t)__double_as_longlong(s);  // s >= +0.0: bit order == value order
-    tpos[c] = -1;
   }
   if (bad) atomicOr((unsigned long long*)&rc->err, (unsigned long long)kErrZeroTotal);
+}
+
+// ---------------------------------------------------------------------------
+// 2b. importance scores (policy.py:84-107, runtime.py:168-175)
+//
+// IS(v) = (1/deg v) * sum_{u in N(v)} [deg u > 0] / deg u over the training
+// CSR, in fp64.  The reference sums each row with np.sum, i.e. numpy's
+// pairwise summation: rows under 8 terms add sequentially from 0.0; rows of
+// 8..128 terms run eight strided accumulators combined as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail; longer rows
+// split at n2 = n/2 - (n/2)%8 and add the halves.  One warp per candidate
+// reproduces that association exactly: the leaves (64..128 terms) of the
+// split tree are summed by 8-lane groups, four leaves at a time, and lane 0
+// adds the leaf sums back up the same tree.  Under CGP each partition sums
+// its source-split row and the partials are added in rank order.
+// ---------------------------------------------------------------------------
+constexpr int kPwChunk = 16384;           // rows above this split at warp level first
+constexpr int kPwLeafCap = kPwChunk / 64;  // leaves are >= 64 terms
+constexpr int kIsWarps = 8;
+
+__device__ __forceinline__ double is_term(const int32_t* __restrict__ indeg, int32_t u) {
+  const int32_t d = __ldg(indeg + u);
+  return d > 0 ? 1.0 / (double)d : 0.0;
+}
+
+__device__ __forceinline__ int pw_split(int n) {
+  const int n2 = n / 2;
+  return n2 - n2 % 8;
+}
+
+// The split tree of a row depends only on its length; walk it without recursion
+// (device recursion costs stack and cannot be sized statically).  Leaves of
+// the tree are visited left to right; kPwDepth bounds the depth for n < 2^31.
+constexpr int kPwDepth = 32;
+
+// leaf start offsets of an n-term row (n <= kPwChunk), left to right
+__device__ int pw_leaves(int n, int* starts) {
+  int st_off[kPwDepth], st_n[kPwDepth], sp = 0, L = 0;
+  st_off[sp] = 0;
+  st_n[sp++] = n;
+  while (sp) {
+    --sp;
+    const int o = st_off[sp], m = st_n[sp];
+    if (m <= 128) {
+      starts[L++] = o;
+      continue;
+    }
+    const int m2 = pw_split(m);
+    st_off[sp] = o + m2;  // right half below the left so the left pops first
+    st_n[sp++] = m - m2;
+    st_off[sp] = o;
+    st_n[sp++] = m2;
+  }
+  return L;
+}
+
+// add the leaf sums back up the split tree of an n-term row: post-order walk
+// with an explicit stack of (length, state, left value)
+__device__ double pw_combine(int n, const double* sums) {
+  int st_n[kPwDepth], st_s[kPwDepth], sp = 0, li = 0;
+  double st_v[kPwDepth];
+  st_n[sp] = n;
+  st_s[sp++] = 0;
+  double v = 0.0;
+  bool have = false;  // v holds a finished subtree value to hand to the parent
+  while (true) {
+    if (!have) {
+      const int m = st_n[sp - 1];
+      if (m <= 128) {
+        v = sums[li++];
+        --sp;
+        have = true;
+      } else {  // descend into the left half
+        st_n[sp] = pw_split(m);
+        st_s[sp++] = 0;
+      }
+      continue;
+    }
+    if (sp == 0) return v;
+    int& state = st_s[sp - 1];
+    if (state == 0) {  // left done: keep it, descend into the right half
+      st_v[sp - 1] = v;
+      state = 1;
+      const int m = st_n[sp - 1];
+      st_n[sp] = m - pw_split(m);
+      st_s[sp++] = 0;
+      have = false;
+    } else {  // both halves done
+      v = st_v[sp - 1] + v;
+      --sp;
+    }
+  }
+}
+
+// one leaf (8 <= n <= 128) by the 8-lane group of this lane; every lane of the
+// group returns the leaf sum.  All 32 lanes must call it (butterfly shuffles).
+__device__ __forceinline__ double pw_leaf(const int32_t* __restrict__ a, int n, const int32_t* __restrict__ indeg,
+                                          bool valid) {
+  const int j = threadIdx.x & 7;
+  const int full = n - (n & 7);
+  int32_t u[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int i = j + 8 * t;
+    u[t] = valid && i < full ? __ldg(a + i) : -1;
+  }
+  double r = 0.0;
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    if (u[t] >= 0) {
+      const double x = is_term(indeg, u[t]);
+      r = t == 0 ? x : r + x;
+    }
+  }
+  // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)): IEEE addition commutes, so the butterfly is exact
+  r += __shfl_xor_sync(0xffffffffu, r, 1);
+  r += __shfl_xor_sync(0xffffffffu, r, 2);
+  r += __shfl_xor_sync(0xffffffffu, r, 4);
+  if (valid)
+    for (int i = full; i < n; ++i) r += is_term(indeg, __ldg(a + i));
+  return r;
+}
+
+// pairwise sum of a row of at most kPwChunk terms (warp-uniform n)
+__device__ double pw_chunk(const int32_t* __restrict__ a, int n, const int32_t* __restrict__ indeg, int* starts,
+                           double* sums) {
+  const int lane = threadIdx.x & 31;
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r += is_term(indeg, __ldg(a + i));
+    return r;
+  }
+  if (n <= 128) return pw_leaf(a, n, indeg, true);
+  int L = 0;
+  if (lane == 0) L = pw_leaves(n, starts);
+  L = __shfl_sync(0xffffffffu, L, 0);
+  __syncwarp();
+  const int g = lane >> 3;
+  for (int l0 = 0; l0 < L; l0 += 4) {
+    const int li = l0 + g;
+    const bool valid = li < L;
+    const int st = valid ? starts[li] : 0;
+    const int len = valid ? (li + 1 < L ? starts[li + 1] : n) - st : 8;
+    const double v = pw_leaf(a + st, len, indeg, valid);
+    if (valid && (lane & 7) == 0) sums[li] = v;
+  }
+  __syncwarp();
+  double r = 0.0;
+  if (lane == 0) r = pw_combine(n, sums);
+  __syncwarp();
+  return __shfl_sync(0xffffffffu, r, 0);
+}
+
+// pairwise sum of any row: the top of the split tree (halves above kPwChunk)
+// walked warp-uniformly with an explicit stack, chunks summed by pw_chunk
+__device__ double pw_row(const int32_t* __restrict__ a, int64_t n, const int32_t* __restrict__ indeg, int* starts,
+                         double* sums) {
+  if (n <= kPwChunk) return pw_chunk(a, (int)n, indeg, starts, sums);
+  int64_t st_off[kPwDepth], st_n[kPwDepth];
+  int st_s[kPwDepth], sp = 0;
+  double st_v[kPwDepth];
+  st_off[sp] = 0;
+  st_n[sp] = n;
+  st_s[sp++] = 0;
+  double v = 0.0;
+  bool have = false;
+  while (true) {
+    if (!have) {
+      const int64_t m = st_n[sp - 1], o = st_off[sp - 1];
+      if (m <= kPwChunk) {
+        v = pw_chunk(a + o, (int)m, indeg, starts, sums);
+        --sp;
+        have = true;
+      } else {
+        int64_t m2 = m / 2;
+        m2 -= m2 % 8;
+        st_off[sp] = o;
+        st_n[sp] = m2;
+        st_s[sp++] = 0;
+      }
+      continue;
+    }
+    if (sp == 0) return v;
+    if (st_s[sp - 1] == 0) {
+      st_v[sp - 1] = v;
+      st_s[sp - 1] = 1;
+      const int64_t m = st_n[sp - 1], o = st_off[sp - 1];
+      int64_t m2 = m / 2;
+      m2 -= m2 % 8;
+      st_off[sp] = o + m2;
+      st_n[sp] = m - m2;
+      st_s[sp++] = 0;
+      have = false;
+    } else {
+      v = st_v[sp - 1] + v;
+      --sp;
+    }
+  }
+}
+
+// one partition's numerators (the whole CSR when centralized), warp per candidate
+__global__ void __launch_bounds__(32 * kIsWarps) k_is_partial(const int32_t* __restrict__ cand_ids,
+                                                              const ReqCounters* rc, const int64_t* __restrict__ off,
+                                                              const int32_t* __restrict__ src,
+                                                              const int32_t* __restrict__ indeg, double* out) {
+  __shared__ int starts[kIsWarps][kPwLeafCap];
+  __shared__ double sums[kIsWarps][kPwLeafCap];
+  const int wid = threadIdx.x >> 5;
+  const int64_t R = rc->R;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = gw; c < R; c += nw) {
+    const int32_t v = cand_ids[c];
+    const int64_t b = off[v], n = off[v + 1] - b;
+    const double r = pw_row(src + b, n, indeg, starts[wid], sums[wid]);
+    if ((threadIdx.x & 31) == 0) out[c] = r;
+  }
+}
+
+// scores from P partial arrays, summed in rank order (P = 1: the centralized row sum)
+__global__ void k_score_is(const int32_t* __restrict__ cand_ids, const int32_t* __restrict__ indeg,
+                           const ReqCounters* rc, IsParts parts, double* score, uint64_t* key) {
+  const int64_t R = rc->R;
+  OB_GRID_STRIDE(c, R) {
+    double sum = 0.0;
+    for (int p = 0; p < parts.P; ++p) sum += __ldcg(parts.part[p] + c);
+    const int32_t d = indeg[cand_ids[c]];
+    const double s = d > 0 ? sum / (double)d : 0.0;
+    score[c] = s;
+    key[c] = (uint64_t)__double_as_longlong(s);
+  }
+}
+
+void launch_is_partial(Engine& e, RequestWs& w, const int64_t* off, const int32_t* src, double* out) {
+  const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
+  k_is_partial<<<grid_for(r_max, kIsWarps, kNumSMs * 8), 32 * kIsWarps, 0, e.stream>>>(w.cand_ids, w.rc, off, src,
+                                                                                       e.g.indeg, out);
+  OB_LAUNCHED();
+}
+
+void launch_score_is(Engine& e, RequestWs& w, const IsParts& parts) {
+  const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
+  k_score_is<<<grid_for(r_max, 256), 256, 0, e.stream>>>(w.cand_ids, e.g.indeg, w.rc, parts, w.cand_score,
+                                                         w.cand_key);
+  OB_LAUNCHED();
 }
 
 __global__ void k_budget(ReqCounters* rc, double gamma, uint32_t* hist) {
@@ -545,7 +793,7 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   if (need_scores) {
     const int64_t r_max = std::min<int64_t>(N, 2 * m);
     k_score<<<grid_for(r_max, 256), 256, 0, s>>>(w.cand_ids, w.rq_cnt, e.g.indeg, w.rc, w.cand_nq, w.cand_score,
-                                                 w.cand_key, w.cand_tpos);
+                                                 w.cand_key, w.cand_tpos, e.cfg.policy == OB_POLICY_RATIO);
     OB_LAUNCHED();
   }
 }
@@ -553,6 +801,14 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
 void stage_select(Engine& e, RequestWs& w) {
   cudaStream_t s = e.stream;
   const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
+  if (e.cfg.policy == OB_POLICY_IS && e.cfg.strategy != OB_STRATEGY_SRPE_CGP && r_max > 0) {
+    // centralized importance scores over the whole training CSR (policy.py:84-95)
+    launch_is_partial(e, w, e.g.offsets, e.g.nbrs, w.is_part);
+    IsParts ip{};
+    ip.P = 1;
+    ip.part[0] = w.is_part;
+    launch_score_is(e, w, ip);
+  }
   k_budget<<<1, 256, 0, s>>>(w.rc, e.cfg.gamma, w.sel_hist);
   OB_LAUNCHED();
   for (int shift = 56; shift >= 0; shift -= 8) {

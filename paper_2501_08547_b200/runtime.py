@@ -126,8 +126,8 @@ class ServingEngine:
                  config: ServeConfig, stream: int = 0, nccl_id: bytes | None = None, rank: int = 0):
         if config.strategy == "sampled":
             raise ValueError("the sampled baseline strategy is not part of the B200 serving path")
-        if config.policy != "ratio":
-            raise ValueError(f"policy {config.policy!r} is not on the device path (ratio only)")
+        if config.policy not in nat.POLICY:
+            raise ValueError(f"policy {config.policy!r} is not on the device path (ratio and is)")
         if config.cache_bytes:
             raise ValueError("feature caches are subsumed by HBM residency; use cache_bytes=0")
         self.dataset = dataset

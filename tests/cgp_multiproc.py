@@ -63,6 +63,30 @@ def main():
                                         coll_bytes=int(bd.collective_bytes)))
                 eng.close()
                 emu.close()
+    # importance policy: per-rank numerators exchanged and summed in rank order
+    # (runtime.py:168-175) must give the reference's distributed plan
+    gis = load_golden("policy_is")
+    for tag, name in (("s3", "small_s3"), ("s50", "small_s50"), ("s60", "small_s60")):
+        g = load_golden(name)
+        N, F = int(g["N"]), g["feats"].shape[1]
+        ds = graphstore.GraphDataset(N, g["offsets"], g["nbrs"], g["feats"], np.ones(N, bool), np.zeros(N, bool))
+        q = gis[f"{tag}.qfeat"]
+        req = ServingRequest(N, len(q), q, gis[f"{tag}.edges"])
+        model = models.make_model("sage_mean", 3, F, 6)
+        w = models.Weights(golden_weights(gis, f"{tag}.w", "sage_mean", 3))
+        pe = graphstore.PeStore([gis[f"{tag}.pe.l{l}"] for l in (1, 2)])
+        cfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=0.5, num_partitions=P, seed=11, device=local,
+                                  policy="is")
+        eng = runtime.distributed_engine(ds, pe, model, w, cfg)
+        emb, bd = eng.serve(req)
+        plan = eng.last_plan()
+        if rank == 0:
+            key = f"{tag}.P{P}.emb"
+            ok_t = f"{tag}.P{P}.targets" not in gis or np.array_equal(plan["targets"], gis[f"{tag}.P{P}.targets"])
+            results.append(dict(case=f"is.{tag}", kind="sage_mean", k=3,
+                                err_ref=max_rel_err(emb, gis[key]) if key in gis else 0.0,
+                                err_emu=0.0, shard=bool(ok_t), coll_bytes=int(bd.collective_bytes)))
+        eng.close()
     # device-generated graph with partitioned storage: each rank holds only its
     # owned rows and source-split CSR; the single-process emulation holds all
     from paper_2501_08547_b200 import workload

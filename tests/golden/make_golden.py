@@ -16,6 +16,11 @@ Cases:
   cfg1      -- BASELINE config 1 (100K nodes, GCN k=2, B=256, gamma=0.1):
                hashes of the generated graph/request, the selected targets,
                block hashes, embeddings, fetch bytes
+  policy_is -- the importance (IS) policy: centralized scores/targets
+               (policy.py:84-95), per-rank partial sums and the distributed
+               plan (policy.py:98-107, runtime.py:168-175) for P in {2,3}, and
+               srpe / srpe-cgp embeddings served with policy="is", on the demo,
+               small_workload graphs and a hub-heavy graph (hubgraph.py)
 """
 
 from __future__ import annotations
@@ -32,7 +37,10 @@ from gnnserve.collectives import make_sim_worlds, run_ranks
 from gnnserve.compgraph import ServingRequest, build_full_k_hop, build_partitioned, build_srpe, partition_request
 from gnnserve.graphstore import make_dataset, partition_random_hash, precompute_embeddings, scatter_pe
 from gnnserve.models import forward_full, init_weights, make_model
-from gnnserve.runtime import ServeConfig, ServingEngine, graph_fetch_bytes
+from gnnserve.runtime import ServeConfig, ServingEngine, graph_fetch_bytes, run_cgp_request
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import hubgraph  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 DEMO_EDGES = [(1, 0), (2, 0), (3, 0), (1, 2), (4, 2), (0, 3), (5, 3), (7, 3), (6, 7), (5, 4), (6, 4)]
@@ -216,8 +224,70 @@ def cfg1():
     print("cfg1", len(out), "arrays", "targets", len(plan.targets))
 
 
+def _is_case(out: dict, tag: str, serving, request, F: int, with_emb: bool) -> None:
+    out[f"{tag}.N"] = np.int64(serving.num_nodes)
+    out[f"{tag}.edges"] = request.edges
+    out[f"{tag}.qfeat"] = request.query_features
+    cand = policy.find_candidates(request, serving)
+    scores = policy.score_importance(cand, serving)
+    out[f"{tag}.cand.ids"] = cand.ids
+    out[f"{tag}.scores"] = scores
+    for g in GAMMAS:
+        out[f"{tag}.targets.g{g}"] = policy.select_targets(cand, scores, g, "is").targets
+    model = make_model("sage_mean", 3, F, 6)
+    w = init_weights(model, 21)
+    pe = precompute_embeddings(serving, model, w) if with_emb else None
+    if with_emb:
+        put_weights(out, f"{tag}.w", model, w)
+        for l in range(1, 3):
+            out[f"{tag}.pe.l{l}"] = pe.layers[l - 1]
+        eng = ServingEngine(serving, pe, model, w, ServeConfig(strategy="srpe", gamma=0.5, policy="is"))
+        out[f"{tag}.srpe.emb"], _ = eng.serve(request)
+    for P in (2, 3):
+        pmap, parts = partition_random_hash(serving, P, 11)
+        partials = [policy.importance_partial_sums(cand.ids, parts[r]) for r in range(P)]
+        for r in range(P):
+            out[f"{tag}.P{P}.partial{r}"] = partials[r]
+        if not with_emb:
+            continue
+        eng = ServingEngine(serving, pe, model, w,
+                            ServeConfig(strategy="srpe-cgp", gamma=0.5, num_partitions=P, seed=11, policy="is"))
+        preqs = partition_request(request, eng.pmap, P)
+        args = [(eng.parts[r], preqs[r], model, w, 0.5, "is", 11, None) for r in range(P)]
+        res = run_ranks(make_sim_worlds(P), run_cgp_request, args)
+        out[f"{tag}.P{P}.targets"] = res[0][1]["targets"]
+        out[f"{tag}.P{P}.emb"] = res[0][0]
+        emb2, _ = eng.serve(request)
+        assert np.array_equal(emb2, res[0][0])
+
+
+def policy_is():
+    out: dict = {}
+    rng = np.random.default_rng(0)
+    ds = make_dataset(DEMO_EDGES, 8, rng.standard_normal((8, 4)).astype(np.float32))
+    rng = np.random.default_rng(1)
+    pairs = [(8, 2), (8, 3), (9, 2), (9, 4), (9, 7)]
+    edges = [(q, t) for q, t in pairs] + [(t, q) for q, t in pairs]
+    req = ServingRequest(8, 2, rng.standard_normal((2, 4)).astype(np.float32), np.array(edges))
+    _is_case(out, "demo", ds, req, 4, True)
+    for seed, n, avg, F, batch, rs in ((3, 300, 8.0, 10, 5, 9), (50, 200, 10.0, 6, 8, 51), (60, 300, 8.0, 10, 6, 5)):
+        full = workload.gen_powerlaw_graph(n, avg, 2.1, F, seed=seed)
+        serving, pool = workload.split_holdout(full, 0.25, seed=seed)
+        req = workload.make_request(pool, serving, batch, seed=rs)
+        _is_case(out, f"s{seed}", serving, req, F, True)
+    hub = make_dataset(hubgraph.edges(), hubgraph.N, hubgraph.features())
+    off, nb = hubgraph.csr()
+    assert np.array_equal(hub.in_offsets, off) and np.array_equal(hub.in_neighbors, nb)
+    e, qf = hubgraph.request()
+    _is_case(out, "hub", hub, ServingRequest(hubgraph.N, len(qf), qf, e), 4, False)
+    np.savez_compressed(os.path.join(HERE, "policy_is.npz"), **out)
+    print("policy_is", len(out), "arrays")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["demo", "small", "edge", "cfg1"]
+    which = sys.argv[1:] or ["demo", "small", "edge", "cfg1", "is"]
+    if "is" in which:
+        policy_is()
     if "demo" in which:
         demo()
     if "small" in which:
