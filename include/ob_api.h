@@ -50,8 +50,13 @@ enum ob_status {
   OB_ESTATE = 6      /* call out of order (e.g. serve before load) -> RuntimeError  */
 };
 
-/* ServeConfig.strategy (runtime.py:51); "sampled" is out of scope. */
-enum ob_strategy { OB_STRATEGY_FULL = 0, OB_STRATEGY_SRPE = 2, OB_STRATEGY_SRPE_CGP = 3 };
+/* ServeConfig.strategy (runtime.py:51).  "sampled" is build_sampled
+   (compgraph.py:248-284): build_full_k_hop with each destination's sources cut to
+   fanouts[l-1] by numpy's SeedSequence(seed, (l, v)) -> PCG64 -> choice stream,
+   reproduced per destination on the device (fanouts <= OB_MAX_FANOUT). */
+enum ob_strategy { OB_STRATEGY_FULL = 0, OB_STRATEGY_SAMPLED = 1, OB_STRATEGY_SRPE = 2, OB_STRATEGY_SRPE_CGP = 3 };
+#define OB_MAX_FANOUT 200
+#define OB_MAX_LAYERS 8
 
 /* ServeConfig.policy (policy.py:29-32): ratio (policy.py:77-81) and importance
    (policy.py:84-107; under srpe-cgp the per-partition numerators are summed in
@@ -79,6 +84,8 @@ typedef struct {
   uint64_t stream;         /* cudaStream_t to launch on; 0 = engine-owned stream */
   const void* nccl_id;     /* 128-byte ncclUniqueId: one process per GPU / rank;
                               NULL with P > 1 = all P partitions on this device  */
+  int32_t num_fanouts;     /* sampled: one fanout per layer (== k), else 0      */
+  int32_t fanouts[OB_MAX_LAYERS]; /* ServeConfig.fanouts, outermost hop first     */
 } ob_config;
 
 typedef struct {

@@ -212,7 +212,7 @@ def precompute(layers, weights, offsets, nbrs, feats):
 
 
 def serve(strategy, layers, weights, num_base, num_queries, offsets, nbrs, feats, qfeat, edges,
-          pe_layers=None, gamma=0.0):
+          pe_layers=None, gamma=0.0, fanouts=None, seed=0):
     """ServingEngine.serve for the centralized strategies (runtime.py:290-335).
 
     Returns a dict with the plan, the blocks, the query embeddings and the
@@ -223,6 +223,10 @@ def serve(strategy, layers, weights, num_base, num_queries, offsets, nbrs, feats
     plan = None
     if strategy == "full":
         blocks = st.build_full(num_base, num_queries, offsets, nbrs, edges, k)
+    elif strategy == "sampled":
+        if fanouts is None or len(fanouts) != k:
+            raise ValueError("sampled strategy needs one fanout per layer")
+        blocks = st.build_sampled(num_base, num_queries, offsets, nbrs, edges, fanouts, seed)
     elif strategy == "srpe":
         if pe_layers is None:
             raise ValueError("reuse strategy needs stored embeddings")

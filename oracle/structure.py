@@ -281,6 +281,44 @@ def build_srpe(num_base, num_queries, offsets, nbrs, edges, targets, k, pe_layer
     return blocks
 
 
+def build_sampled(num_base, num_queries, offsets, nbrs, edges, fanouts, seed) -> list[Block]:
+    """build_sampled (compgraph.py:248-284): build_full_k_hop with fanout-capped source lists.
+
+    Block l keeps at most fanouts[l-1] of each destination's serving in-sources,
+    chosen by numpy's SeedSequence(seed, (l, v)) stream (oracle/sampling.py).
+    """
+    fanouts = [int(f) for f in fanouts]
+    if any(f < 1 for f in fanouts):
+        raise ValueError("fanouts must be >= 1")
+    k = len(fanouts)
+    edges = np.asarray(edges, dtype=_I64).reshape(-1, 2)
+    train_deg = np.diff(offsets).astype(_I64)
+    q_deg = query_in_degrees(edges, num_base, num_queries)
+    ridx = RequestIndex(edges)
+    dst = np.arange(num_base, num_base + num_queries, dtype=_I64)
+    blocks: list[Block] = [None] * k  # type: ignore[list-item]
+    for l in range(k, 0, -1):
+        fan = fanouts[l - 1]
+        flat, cnt = _serving_sources(dst, num_base, offsets, nbrs, ridx)
+        ptr = np.zeros(len(dst) + 1, dtype=_I64)
+        np.cumsum(cnt, out=ptr[1:])
+        parts, counts = [], []
+        for i, v in enumerate(dst):
+            row = flat[ptr[i]:ptr[i + 1]]
+            if len(row) > fan:
+                rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(l, int(v))))
+                row = np.sort(row[rng.choice(len(row), size=fan, replace=False)])
+            parts.append(row)
+            counts.append(len(row))
+        flat = np.concatenate(parts) if parts else np.empty(0, dtype=_I64)
+        blocks[l - 1] = _assemble(
+            dst, flat, np.asarray(counts, dtype=_I64), num_base, lambda s, _l=l: _uniform_binding(s, _l),
+            train_deg, q_deg,
+        )
+        dst = blocks[l - 1].src_ids
+    return blocks
+
+
 def build_full(num_base, num_queries, offsets, nbrs, edges, k) -> list[Block]:
     """build_full_k_hop (compgraph.py:224-245)."""
     if k < 1:

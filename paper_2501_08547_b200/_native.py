@@ -16,7 +16,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libomega_b200.so")
 
 OB_OK, OB_EINVAL, OB_ENOTFOUND, OB_ECOMM, OB_ECUDA, OB_ENOMEM, OB_ESTATE = range(7)
-STRATEGY = {"full": 0, "srpe": 2, "srpe-cgp": 3}
+STRATEGY = {"full": 0, "sampled": 1, "srpe": 2, "srpe-cgp": 3}
+MAX_FANOUT = 200  # OB_MAX_FANOUT
+MAX_LAYERS = 8
 POLICY = {"ratio": 0, "is": 1}
 KIND_TAGS = {"gcn": 0, "sage_mean": 1, "gat": 2, "power_mean": 3, "moments": 4, "sage_max": 5}
 
@@ -36,6 +38,8 @@ class ObConfig(C.Structure):
         ("seed", C.c_uint64),
         ("stream", C.c_uint64),
         ("nccl_id", C.c_void_p),
+        ("num_fanouts", C.c_int32),
+        ("fanouts", C.c_int32 * 8),
     ]
 
 

@@ -70,12 +70,14 @@ static Plan plan_request(const Engine& e, int B, int64_t m) {
     b.has_self = self;
     return b;
   };
-  if (e.cfg.strategy == OB_STRATEGY_FULL) {
+  if (khop(e.cfg)) {
     p.blocks.resize(k);
     int64_t D = B;
+    const bool samp = e.cfg.strategy == OB_STRATEGY_SAMPLED;
     for (int l = k; l >= 1; --l) {
       int64_t E = topdeg(e.g, std::min<int64_t>(N, D)) + m;
       E = std::min<int64_t>(E, e.g.E + m);
+      if (samp) E = std::min<int64_t>(E, D * e.cfg.fanouts[l - 1]);  // at most fan sources per destination
       p.blocks[l - 1] = mk(D, E, true);
       D = p.blocks[l - 1].S_max;
     }
@@ -141,7 +143,12 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     sc.span_rl = a.take<int32_t>(D);
   };
   take_scratch(w.bs[0], Dmax, Emax);
-  if (e.cfg.strategy != OB_STRATEGY_FULL) take_scratch(w.bs[1], p.blocks[1].D_max, p.blocks[1].E_max);  // query block
+  if (e.cfg.strategy == OB_STRATEGY_SAMPLED) {  // kept sources of the sampled rows, one block at a time
+    int64_t n = 1;
+    for (int l = 1; l <= k; ++l) n = std::max<int64_t>(n, p.blocks[l - 1].D_max * e.cfg.fanouts[l - 1]);
+    w.bs[0].samp = a.take<int32_t>(n);
+  }
+  if (!khop(e.cfg)) take_scratch(w.bs[1], p.blocks[1].D_max, p.blocks[1].E_max);  // query block
   else w.bs[1] = w.bs[0];
   w.blocks = p.blocks;
   for (size_t i = 0; i < w.blocks.size(); ++i) {
@@ -158,11 +165,11 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     // full: block l-1's dst list aliases block l's src_ids (set below)
     b.dst_ids = a.take<int32_t>(b.D_max);
   }
-  if (e.cfg.strategy == OB_STRATEGY_FULL)  // block l-1's destinations are block l's sources
+  if (khop(e.cfg))  // block l-1's destinations are block l's sources
     for (int l = k - 1; l >= 1; --l) w.blocks[l - 1].dst_ids = w.blocks[l].src_ids;
   w.block_of_layer.assign(k, 0);
   for (int l = 1; l <= k; ++l)
-    w.block_of_layer[l - 1] = (e.cfg.strategy == OB_STRATEGY_FULL) ? l - 1 : (l < k ? 0 : 1);
+    w.block_of_layer[l - 1] = khop(e.cfg) ? l - 1 : (l < k ? 0 : 1);
   w.rowp = a.take<const float*>(Smax);
   w.gscale = a.take<float>(Smax);
   bool gat = false, mom = false, wide = false;
@@ -242,7 +249,9 @@ static void check_ready(Engine& e) {
   OB_CHECK(e.g.N > 0, OB_ESTATE, "no graph loaded");
   OB_CHECK(!e.layers.empty(), OB_ESTATE, "no model loaded");
   OB_CHECK(e.layers[0].spec.in_dim == e.g.F, OB_EINVAL, "input width does not match layer in_dim");
-  if (e.cfg.strategy != OB_STRATEGY_FULL) {
+  if (e.cfg.strategy == OB_STRATEGY_SAMPLED)
+    OB_CHECK(e.cfg.num_fanouts == (int)e.layers.size(), OB_EINVAL, "sampled strategy needs one fanout per layer");
+  if (!khop(e.cfg)) {
     OB_CHECK((int)e.layers.size() >= 2, OB_EINVAL, "reuse graphs need k >= 2");
     OB_CHECK((int)e.pe.size() >= (int)e.layers.size() - 1 && !e.pe.empty(), OB_EINVAL,
              "reuse strategy needs stored embeddings");
@@ -267,7 +276,7 @@ static int64_t fetch_bytes(const Engine& e, const RequestWs& w, const std::vecto
     const BlockCounters& c = per_layer[l - 1];
     total += 16 * c.E;
     total += 4 * (int64_t)e.g.F * c.feat_src;
-    if (l > 1 && !e.pe_dim.empty() && e.cfg.strategy != OB_STRATEGY_FULL) total += 4 * (int64_t)e.pe_dim[l - 2] * c.pe_src;
+    if (l > 1 && !e.pe_dim.empty() && !khop(e.cfg)) total += 4 * (int64_t)e.pe_dim[l - 2] * c.pe_src;
   }
   (void)w;
   return total;
@@ -307,7 +316,7 @@ static void enqueue_request(Engine& e, float* d_out) {
 static void enqueue_stages(Engine& e, float* d_out) {
   cudaStream_t s = e.stream;
   RequestWs& w = e.ws;
-  const bool srpe = e.cfg.strategy != OB_STRATEGY_FULL;
+  const bool srpe = !khop(e.cfg);
   OB_CUDA(cudaMemsetAsync(w.rc, 0, sizeof(ReqCounters), s));
   for (auto& b : w.blocks) OB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(BlockCounters), s));
   if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) {
@@ -408,7 +417,7 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   w.edges = d_edges;
   w.qfeat = d_q;
   const int k = (int)e.layers.size();
-  const bool srpe = e.cfg.strategy != OB_STRATEGY_FULL;
+  const bool srpe = !khop(e.cfg);
   const bool cgp = e.cfg.strategy == OB_STRATEGY_SRPE_CGP;
   // kernel arguments are copied at launch: the block is stream-ordered with no host staging
   k_set_params<<<1, 1, 0, s>>>(e.params, d_edges, d_q, m);
@@ -663,9 +672,16 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
   return guarded([&] {
     OB_CHECK(cfg && out, OB_EINVAL, "null argument");
     OB_CHECK(cfg->gamma >= 0.0 && cfg->gamma <= 1.0, OB_EINVAL, "gamma must lie in [0, 1]");
-    OB_CHECK(cfg->strategy == OB_STRATEGY_FULL || cfg->strategy == OB_STRATEGY_SRPE ||
-                 cfg->strategy == OB_STRATEGY_SRPE_CGP,
+    OB_CHECK(cfg->strategy == OB_STRATEGY_FULL || cfg->strategy == OB_STRATEGY_SAMPLED ||
+                 cfg->strategy == OB_STRATEGY_SRPE || cfg->strategy == OB_STRATEGY_SRPE_CGP,
              OB_EINVAL, "unknown strategy");
+    if (cfg->strategy == OB_STRATEGY_SAMPLED) {
+      OB_CHECK(cfg->num_fanouts >= 1 && cfg->num_fanouts <= OB_MAX_LAYERS, OB_EINVAL, "sampled strategy needs fanouts");
+      for (int l = 0; l < cfg->num_fanouts; ++l) {
+        OB_CHECK(cfg->fanouts[l] >= 1, OB_EINVAL, "fanouts must be >= 1");
+        OB_CHECK(cfg->fanouts[l] <= OB_MAX_FANOUT, OB_EINVAL, "fanout above OB_MAX_FANOUT (200)");
+      }
+    }
     OB_CHECK(cfg->policy == OB_POLICY_RATIO || cfg->policy == OB_POLICY_IS, OB_EINVAL,
              "unknown policy (ratio and is run on the device)");
     OB_CHECK(cfg->num_partitions >= 1, OB_EINVAL, "num_partitions must be >= 1");
@@ -929,7 +945,7 @@ int ob_last_plan(ob_engine* h, int64_t* nc, int64_t* nt, int64_t* ids, int64_t* 
     std::lock_guard<std::mutex> lk(h->mu);
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
-    OB_CHECK(e.have_request && e.cfg.strategy != OB_STRATEGY_FULL, OB_ESTATE, "no srpe request served");
+    OB_CHECK(e.have_request && !khop(e.cfg), OB_ESTATE, "no srpe request served");
     RequestWs& w = e.ws;
     cudaStream_t s = e.stream;
     ReqCounters rc = d2h(w.rc, 1, s)[0];

@@ -18,15 +18,23 @@
 // the bitmap's popcount prefix both as the ascending unique source list and
 // as the global -> local relabel.  Edges come out already ordered by
 // (dst, src), so no sort is needed.
+//
+// Sampled strategy (build_sampled, compgraph.py:248-284): after the spans are
+// known, k_sample_spans replaces every row longer than the block's fanout by
+// the fanout sources numpy would keep -- one thread per destination runs
+// numpy's SeedSequence(seed, (l, v)) -> PCG64 -> Floyd choice stream
+// (restated in oracle/sampling.py) and writes the kept sources, ascending,
+// to a per-block buffer that the fill reads instead of the CSR span.
 #include "ob_engine.h"
 
 namespace ob {
 
 struct SegSpans {
-  int64_t* cs;  // csr start
-  int32_t* cl;  // csr length
+  int64_t* cs;  // csr start (sampled row: start in samp)
+  int32_t* cl;  // csr length (sampled row: -fanout, every source in samp)
   int64_t* rs;  // request-span start
   int32_t* rl;  // request-span length
+  const int32_t* samp;  // sampled rows' kept sources
 };
 
 // spans for a destination list (global ids ascending)
@@ -91,12 +99,14 @@ __global__ void __launch_bounds__(1024) k_block_fill(const BlockCounters* cnt, c
     const int64_t e0 = d0 + (it - __ldg(item_ptr + i)) * kAggChunk;
     const int64_t e1 = min(e0 + kAggChunk, __ldg(dst_ptr + i + 1));
     const int64_t cs = __ldg(sp.cs + i), rs = __ldg(sp.rs + i);
-    const int32_t cl = __ldg(sp.cl + i);
+    const int32_t cl0 = __ldg(sp.cl + i);
+    const int32_t* __restrict__ row = cl0 < 0 ? sp.samp : nbrs;  // a sampled row lives in samp
+    const int32_t cl = cl0 < 0 ? -cl0 : cl0;
     int32_t v[kAggChunk / 32];
 #pragma unroll
     for (int u = 0; u < kAggChunk / 32; ++u) {  // all loads in flight first
       const int64_t e = e0 + u * 32 + lane, j = e - d0;
-      v[u] = e < e1 ? (j < cl ? __ldg(nbrs + cs + j) : __ldg(rq_src + rs + (j - cl))) : -1;
+      v[u] = e < e1 ? (j < cl ? __ldg(row + cs + j) : __ldg(rq_src + rs + (j - cl))) : -1;
     }
 #pragma unroll
     for (int u = 0; u < kAggChunk / 32; ++u) {
@@ -114,6 +124,150 @@ __global__ void __launch_bounds__(1024) k_block_fill(const BlockCounters* cnt, c
     __syncthreads();
     uint32_t* out = part_bits + (int64_t)blockIdx.x * words;
     for (int64_t w = threadIdx.x; w < words; w += blockDim.x) out[w] = sbm[w];
+  }
+}
+
+// --- numpy's per-destination sampling stream -----------------------------------
+// SeedSequence(entropy=seed, spawn_key=(l, v)).generate_state(4, uint64)
+// (numpy/random/bit_generator.pyx): uint32 limbs, entropy zero-padded to the
+// 4-word pool because a spawn key is present, hashmix/mix pool, INIT_B draw.
+__device__ void ss_generate(uint64_t seed, uint32_t l, uint32_t v, uint64_t st[4]) {
+  uint32_t ent[6];
+  int ne = 0;
+  ent[ne++] = (uint32_t)seed;
+  if (seed >> 32) ent[ne++] = (uint32_t)(seed >> 32);
+  while (ne < 4) ent[ne++] = 0u;
+  ent[4] = l;
+  ent[5] = v;
+  uint32_t hc = 0x43b0d7e5u;
+  auto hashmix = [&hc](uint32_t x) {
+    x ^= hc;
+    hc *= 0x931e8875u;
+    x *= hc;
+    return x ^ (x >> 16);
+  };
+  auto mix = [](uint32_t x, uint32_t y) {
+    const uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+    return r ^ (r >> 16);
+  };
+  uint32_t mx[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) mx[i] = hashmix(ent[i]);
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+      if (a != d) mx[d] = mix(mx[d], hashmix(mx[a]));
+#pragma unroll
+  for (int a = 4; a < 6; ++a)
+#pragma unroll
+    for (int d = 0; d < 4; ++d) mx[d] = mix(mx[d], hashmix(ent[a]));
+  uint32_t hb = 0x8b51f9ddu, o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t x = mx[i & 3] ^ hb;
+    hb *= 0x58f38dedu;
+    x *= hb;
+    o[i] = x ^ (x >> 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) st[i] = (uint64_t)o[2 * i] | ((uint64_t)o[2 * i + 1] << 32);
+}
+
+// numpy's PCG64 (XSL-RR 128/64, pcg_setseq_128_srandom_r seeding) with the
+// bit generator's 32-bit draw buffer (low half of a 64-bit output first)
+struct Pcg64 {
+  unsigned __int128 s, inc;
+  uint32_t buf;
+  bool has;
+  __device__ void step() {
+    const unsigned __int128 mult = ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+    s = s * mult + inc;
+  }
+  __device__ explicit Pcg64(const uint64_t st[4]) {
+    const unsigned __int128 seed = ((unsigned __int128)st[0] << 64) | st[1];
+    inc = ((((unsigned __int128)st[2] << 64) | st[3]) << 1) | 1u;
+    s = 0;
+    step();
+    s += seed;
+    step();
+    has = false;
+    buf = 0;
+  }
+  __device__ uint64_t next64() {
+    step();
+    const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    const unsigned rot = (unsigned)(hi >> 58);
+    const uint64_t x = hi ^ lo;
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+  }
+  __device__ uint32_t next32() {
+    if (has) {
+      has = false;
+      return buf;
+    }
+    const uint64_t n = next64();
+    has = true;
+    buf = (uint32_t)(n >> 32);
+    return (uint32_t)n;
+  }
+  // random_bounded_uint64(0, rng) for 0 < rng < 2^32 - 1: Lemire's rejection method
+  __device__ uint32_t bounded(uint32_t rng) {
+    const uint32_t ex = rng + 1u;
+    uint64_t m = (uint64_t)next32() * ex;
+    uint32_t left = (uint32_t)m;
+    if (left < ex) {
+      const uint32_t thr = (0xFFFFFFFFu - rng) % ex;
+      while (left < thr) {
+        m = (uint64_t)next32() * ex;
+        left = (uint32_t)m;
+      }
+    }
+    return (uint32_t)(m >> 32);
+  }
+};
+
+// rows longer than fan keep Generator.choice(n, fan, replace=False)'s set
+// (Floyd: j = n-fan .. n-1, t = bounded(j), keep t unless chosen, else j),
+// ascending; the row's source list is ascending, so the kept values come out
+// in the order np.sort(nbrs[keep]) gives
+__global__ void __launch_bounds__(128) k_sample_spans(const int32_t* __restrict__ dst_ids, const BlockCounters* cnt,
+                                                      SegSpans sp, const int32_t* __restrict__ nbrs,
+                                                      const int32_t* __restrict__ rq_src, int fan, int layer,
+                                                      uint64_t seed, int32_t* samp, int64_t* seg_len) {
+  const int64_t D = cnt->D;
+  OB_GRID_STRIDE(i, D) {
+    const int32_t cl = sp.cl[i], rl = sp.rl[i];
+    const int64_t n = (int64_t)cl + rl;
+    if (n <= fan) continue;
+    uint64_t st[4];
+    ss_generate(seed, (uint32_t)layer, (uint32_t)dst_ids[i], st);
+    Pcg64 g(st);
+    int32_t pick[OB_MAX_FANOUT];
+    int c = 0;
+    for (int64_t j = n - fan; j < n; ++j) {
+      const int32_t t = j > 0 ? (int32_t)g.bounded((uint32_t)j) : 0;
+      bool dup = false;
+      for (int q = 0; q < c; ++q) dup |= pick[q] == t;
+      // insertion into the ascending list of picks
+      int32_t x = dup ? (int32_t)j : t;
+      int q = c++;
+      while (q > 0 && pick[q - 1] > x) {
+        pick[q] = pick[q - 1];
+        --q;
+      }
+      pick[q] = x;
+    }
+    const int64_t cs = sp.cs[i], rs = sp.rs[i];
+    int32_t* out = samp + i * fan;
+    for (int q = 0; q < fan; ++q) {
+      const int32_t j = pick[q];
+      out[q] = j < cl ? nbrs[cs + j] : rq_src[rs + (j - cl)];
+    }
+    sp.cs[i] = i * fan;
+    sp.cl[i] = -fan;
+    sp.rl[i] = 0;
+    seg_len[i] = fan;
   }
 }
 
@@ -186,16 +340,23 @@ __global__ void k_copy_count_D(BlockCounters* dst, const BlockCounters* src) { d
 // generic block assembly over an already written dst list + counts->D.
 // `src` names the CSR the destinations pull from (the whole graph, or a CGP
 // rank's source-split CSR) and the request CSR (whole request or the rank's slice).
-void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const BuildScratch& sc) {
+void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const BuildScratch& sc, int fan,
+              int layer) {
   cudaStream_t s = e.stream;
   SegSpans sp;  // transient, shared by every block of the request
   sp.cs = sc.span_cs;
   sp.cl = sc.span_cl;
   sp.rs = sc.span_rs;
   sp.rl = sc.span_rl;
+  sp.samp = sc.samp;
   k_block_spans<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, e.g.N, src.offsets, src.deg, w.cbits,
                                                         w.cwpre, src.rq_ptr, w.rc, sp, sc.seg_len);
   OB_LAUNCHED();
+  if (fan > 0) {
+    k_sample_spans<<<grid_for(b.D_max, 128), 128, 0, s>>>(b.dst_ids, b.cnt, sp, src.nbrs, src.rq_src, fan, layer,
+                                                           e.cfg.seed, sc.samp, sc.seg_len);
+    OB_LAUNCHED();
+  }
   // dst_ptr / item_ptr / group_ptr (+ E, items, groups) in one pass; the work
   // items double as the fill's edge chunks
   const BlockStore3 st{b.dst_ptr, b.item_ptr, b.group_ptr};
@@ -272,7 +433,8 @@ void stage_build_full(Engine& e, RequestWs& w) {
       k_copy_count_D<<<1, 1, 0, s>>>(b.cnt, up.cnt);
       OB_LAUNCHED();
     }
-    assemble(e, w, b, src, w.bs[0]);
+    const bool samp = e.cfg.strategy == OB_STRATEGY_SAMPLED;
+    assemble(e, w, b, src, w.bs[0], samp ? e.cfg.fanouts[l - 1] : 0, l);
   }
 }
 

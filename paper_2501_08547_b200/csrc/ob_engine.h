@@ -74,6 +74,8 @@ struct BlockDev {
 // Every row table in HBM uses a row stride padded to 4 floats (16 B) so rows
 // can be staged with 16-byte cp.async and read with float4 vectors.
 inline int ld4(int w) { return (w + 3) & ~3; }
+// one block per layer, frontier expansion, no selection: full and sampled
+inline bool khop(const ob_config& c) { return c.strategy == OB_STRATEGY_FULL || c.strategy == OB_STRATEGY_SAMPLED; }
 
 // A row source: per-row pointers (gathered inputs) or a dense strided matrix.
 struct RowSrc {
@@ -224,6 +226,7 @@ struct BuildScratch {
   int32_t* span_cl = nullptr;
   int64_t* span_rs = nullptr;
   int32_t* span_rl = nullptr;
+  int32_t* samp = nullptr;         // sampled: [D][fanout] kept source ids of the sampled rows
 };
 
 // Per-request device workspace for the centralized pipeline.
@@ -484,7 +487,10 @@ struct SpanSrc {
   const int64_t* rq_ptr;   // request CSR (whole request or the rank's slice)
   const int32_t* rq_src;
 };
-void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const BuildScratch& sc);
+// fan > 0 (sampled strategy): rows longer than fan keep the sources numpy's
+// SeedSequence(seed, (layer, v)) choice picks (compgraph.py:266-274)
+void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const BuildScratch& sc, int fan = 0,
+              int layer = 0);
 void build_query_block(Engine& e, RequestWs& w);
 void build_mid_block(Engine& e, RequestWs& w);
 void write_mid_dst(Engine& e, RequestWs& w, BlockDev& b);

@@ -906,7 +906,7 @@ void cgp_update(cudaStream_t s, const LayerDev& L, const int64_t* D_dev, int64_t
 // serving forward over the request's blocks
 // ---------------------------------------------------------------------------
 BindCtx bind_ctx(Engine& e, RequestWs& w, int l) {
-  const bool full = e.cfg.strategy == OB_STRATEGY_FULL;
+  const bool full = khop(e.cfg);
   const LayerDev& L = e.layers[l - 1];
   BindCtx c{};
   c.mode = full ? 1 : 0;

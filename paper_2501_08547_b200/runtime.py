@@ -124,8 +124,14 @@ class ServingEngine:
 
     def __init__(self, dataset: GraphDataset, pe: PeStore | None, model: ModelSpec, weights: Weights,
                  config: ServeConfig, stream: int = 0, nccl_id: bytes | None = None, rank: int = 0):
-        if config.strategy == "sampled":
-            raise ValueError("the sampled baseline strategy is not part of the B200 serving path")
+        if config.strategy == "sampled":  # build_sampled (compgraph.py:248-284)
+            fan = [int(f) for f in config.fanouts]
+            if any(f < 1 for f in fan):
+                raise ValueError("fanouts must be >= 1")
+            if len(fan) != model.k:
+                raise ValueError("model depth does not match the computation graph")
+            if max(fan) > nat.MAX_FANOUT:
+                raise ValueError(f"fanouts above {nat.MAX_FANOUT} are not supported on the device")
         if config.policy not in nat.POLICY:
             raise ValueError(f"policy {config.policy!r} is not on the device path (ratio and is)")
         if config.cache_bytes:
@@ -139,6 +145,12 @@ class ServingEngine:
                            policy=nat.POLICY[config.policy], num_partitions=int(config.num_partitions),
                            rank=int(rank), seed=int(config.seed) & 0xFFFFFFFFFFFFFFFF, stream=int(stream),
                            nccl_id=None)
+        if config.strategy == "sampled":
+            if len(config.fanouts) > nat.MAX_LAYERS:
+                raise ValueError(f"at most {nat.MAX_LAYERS} layers")
+            cfg.num_fanouts = len(config.fanouts)
+            for i, f in enumerate(config.fanouts):
+                cfg.fanouts[i] = int(f)
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -198,7 +210,7 @@ class ServingEngine:
         """runtime.py:308-358."""
         if request.num_base != self.dataset.num_nodes:
             raise ValueError("request numbered against a different dataset")
-        if self.config.strategy != "full" and self.model.k < 2:
+        if self.config.strategy not in ("full", "sampled") and self.model.k < 2:
             raise ValueError("reuse graphs need k >= 2")
         B = int(request.num_queries)
         q = _f32(request.query_features)
@@ -262,7 +274,8 @@ class ServingEngine:
     def last_graph(self, partition: int = 0) -> ComputationGraph:
         blocks = [self.last_block(l, partition) for l in range(1, self.model.k + 1)]
         n = self.dataset.num_nodes
-        tg = self.last_plan()["targets"] if self.config.strategy != "full" else np.empty(0, np.int64)
+        tg = (self.last_plan()["targets"] if self.config.strategy not in ("full", "sampled")
+              else np.empty(0, np.int64))
         B = int(np.sum(blocks[-1].dst_ids >= n))
         return ComputationGraph(blocks, np.arange(n, n + B, dtype=np.int64), self.config.strategy, n, tg)
 

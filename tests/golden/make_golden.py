@@ -16,6 +16,9 @@ Cases:
   cfg1      -- BASELINE config 1 (100K nodes, GCN k=2, B=256, gamma=0.1):
                hashes of the generated graph/request, the selected targets,
                block hashes, embeddings, fetch bytes
+  sampled   -- the sampled strategy (compgraph.py:248-284): blocks and
+               embeddings for several fanouts and seeds (incl. a seed above
+               2^32), small_workload graphs and the hub graph
   policy_is -- the importance (IS) policy: centralized scores/targets
                (policy.py:84-95), per-rank partial sums and the distributed
                plan (policy.py:98-107, runtime.py:168-175) for P in {2,3}, and
@@ -34,7 +37,8 @@ import numpy as np
 from gnnserve import models, policy, workload
 from gnnserve.cgpexec import execute_model
 from gnnserve.collectives import make_sim_worlds, run_ranks
-from gnnserve.compgraph import ServingRequest, build_full_k_hop, build_partitioned, build_srpe, partition_request
+from gnnserve.compgraph import (ServingRequest, build_full_k_hop, build_partitioned, build_sampled, build_srpe,
+                                partition_request)
 from gnnserve.graphstore import make_dataset, partition_random_hash, precompute_embeddings, scatter_pe
 from gnnserve.models import forward_full, init_weights, make_model
 from gnnserve.runtime import ServeConfig, ServingEngine, graph_fetch_bytes, run_cgp_request
@@ -261,6 +265,35 @@ def _is_case(out: dict, tag: str, serving, request, F: int, with_emb: bool) -> N
         assert np.array_equal(emb2, res[0][0])
 
 
+SAMPLED_RUNS = [((3, 2), 0), ((1, 4), 7), ((4, 3, 2), 0), ((5, 1, 3), 12345678901)]
+
+
+def sampled():
+    out: dict = {}
+    for seed, n, avg, F, batch, rs in ((3, 300, 8.0, 10, 5, 9), (50, 200, 10.0, 6, 8, 51), (60, 300, 8.0, 10, 6, 5)):
+        full = workload.gen_powerlaw_graph(n, avg, 2.1, F, seed=seed)
+        serving, pool = workload.split_holdout(full, 0.25, seed=seed)
+        req = workload.make_request(pool, serving, batch, seed=rs)
+        tag = f"s{seed}"
+        for fan, sd in SAMPLED_RUNS:
+            k = len(fan)
+            run = f"{tag}.f{''.join(map(str, fan))}.seed{sd}"
+            put_blocks(out, run, build_sampled(req, serving, fan, sd))
+            for kind, kw in (("sage_mean", {}), ("gcn", {}), ("gat", {})):
+                model = make_model(kind, k, F, 6, **kw)
+                w = init_weights(model, 7 + k)  # the small_* fixtures' weights (case())
+                eng = ServingEngine(serving, None, model, w, ServeConfig(strategy="sampled", fanouts=fan, seed=sd))
+                out[f"{run}.{kind}.emb"], bd = eng.serve(req)
+                out[f"{run}.{kind}.fetch"] = np.int64(bd.fetch_bytes)
+    hub = make_dataset(hubgraph.edges(), hubgraph.N, hubgraph.features())
+    e, qf = hubgraph.request()
+    req = ServingRequest(hubgraph.N, len(qf), qf, e)
+    for fan, sd in (((25, 10), 3), ((150, 200), 99)):
+        put_blocks(out, f"hub.f{fan[0]}_{fan[1]}.seed{sd}", build_sampled(req, hub, fan, sd))
+    np.savez_compressed(os.path.join(HERE, "sampled.npz"), **out)
+    print("sampled", len(out), "arrays")
+
+
 def policy_is():
     out: dict = {}
     rng = np.random.default_rng(0)
@@ -285,7 +318,9 @@ def policy_is():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["demo", "small", "edge", "cfg1", "is"]
+    which = sys.argv[1:] or ["demo", "small", "edge", "cfg1", "is", "sampled"]
+    if "sampled" in which:
+        sampled()
     if "is" in which:
         policy_is()
     if "demo" in which:
