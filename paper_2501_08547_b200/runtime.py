@@ -333,3 +333,75 @@ class ServingEngine:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# Poisson throughput harness (runtime.py:476-534)
+# ---------------------------------------------------------------------------
+
+
+def poisson_interarrivals(rate_per_s: float, count: int, seed: int) -> np.ndarray:
+    """runtime.py:476-480: exponential gaps from numpy's default_rng(seed)."""
+    if rate_per_s <= 0:
+        raise ValueError("rate must be positive")
+    rng = np.random.default_rng(seed)
+    return rng.exponential(1.0 / rate_per_s, size=count)
+
+
+@dataclass
+class ThroughputReport:
+    """runtime.py:483-490."""
+
+    offered_rate: float
+    achieved_rate: float
+    completed: int
+    p50_ms: float
+    p95_ms: float
+    p99_ms: float
+
+
+def throughput_benchmark(serve_fn, request_factory, rate_per_s: float, duration_s: float, seed: int,
+                         service_time_fn=None) -> ThroughputReport:
+    """FIFO single-server queue in virtual time with measured service times (runtime.py:493-534).
+
+    Arrivals follow the reference's exponential gaps (same numpy stream, so the
+    same arrival times for a seed); each admitted request is served for real
+    and its completion placed on the virtual timeline; latency = completion -
+    arrival.  Service time is the wall clock around ``serve_fn`` (a serve is
+    synchronous: it returns host arrays), or ``service_time_fn(result)``
+    seconds when given -- e.g. the device-measured time of the request
+    (``lambda r: r[1].compute_ms / 1e3 + ...``).
+    """
+    import time
+
+    if rate_per_s <= 0:
+        raise ValueError("rate must be positive")
+    rng = np.random.default_rng(seed)
+    arrivals = []
+    t = 0.0
+    while True:
+        t += rng.exponential(1.0 / rate_per_s)
+        if t >= duration_s:
+            break
+        arrivals.append(t)
+    free_at = 0.0
+    latencies = []
+    completed = 0
+    for i, arr in enumerate(arrivals):
+        start = max(arr, free_at)
+        if start >= duration_s:
+            break
+        t0 = time.perf_counter()
+        res = serve_fn(request_factory(i))
+        service = time.perf_counter() - t0 if service_time_fn is None else float(service_time_fn(res))
+        completion = start + service
+        free_at = completion
+        if completion <= duration_s:
+            completed += 1
+            latencies.append((completion - arr) * 1e3)
+    if latencies:
+        p50, p95, p99 = np.percentile(latencies, [50, 95, 99])
+    else:
+        p50 = p95 = p99 = 0.0
+    return ThroughputReport(offered_rate=rate_per_s, achieved_rate=completed / duration_s, completed=completed,
+                            p50_ms=float(p50), p95_ms=float(p95), p99_ms=float(p99))
