@@ -56,6 +56,16 @@ CONFIGS = {
     "cfg4": (111_059_956, 14.55, 128, "sage_mean", 3, 128, 1024, 0.1,
              "3-layer GraphSAGE-mean, ogbn-papers100M-shaped 111M nodes / ~1.6B edges generated on the GPUs, "
              "F=128, H=128, B=1024, SRPE ratio 0.1, CGP-partitioned"),
+    # BASELINE configs[4] (gamma from PAPER.md:560-561): Yelp / Amazon shapes, H = 512;
+    # run with --strategy full | srpe | sampled (and --parallel cgp at N > 1) for the ablation
+    "cfg5-yelp-gcn": (717_000, 19.5, 300, "gcn", 2, 512, 1024, 0.20,
+                      "2-layer GCN, Yelp-shaped 717K nodes / ~14M edges, F=300, H=512, B=1024, SRPE ratio 0.2"),
+    "cfg5-yelp-gat": (717_000, 19.5, 300, "gat", 3, 512, 1024, 0.07,
+                      "3-layer GAT, Yelp-shaped 717K nodes / ~14M edges, F=300, H=512, B=1024, SRPE ratio 0.07"),
+    "cfg5-amazon-gcn": (1_600_000, 165.0, 200, "gcn", 2, 512, 1024, 0.03,
+                        "2-layer GCN, Amazon-shaped 1.6M nodes / ~264M edges, F=200, H=512, B=1024, SRPE ratio 0.03"),
+    "cfg5-amazon-gat": (1_600_000, 165.0, 200, "gat", 3, 512, 1024, 0.01,
+                        "3-layer GAT, Amazon-shaped 1.6M nodes / ~264M edges, F=200, H=512, B=1024, SRPE ratio 0.01"),
 }
 SYNTHETIC = {"cfg4"}  # device-generated graph + synthetic stored embeddings (never on the host)
 METRIC = "queries/s (B-query batches, p50/p99 batch latency in ms alongside)"
@@ -246,6 +256,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--gamma", type=float, default=None)
+    ap.add_argument("--strategy", default="srpe", choices=["srpe", "full", "sampled"],
+                    help="single-GPU / replica strategy (CGP runs srpe-cgp); config 5's ablation axis")
+    ap.add_argument("--fanouts", default="15,10,5",
+                    help="sampled strategy: comma-separated fanouts, outermost hop first (trimmed to k)")
     ap.add_argument("--ref-batch", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
@@ -274,6 +288,8 @@ def main():
     n, avg, F, kind, k, H, B, gamma, desc = CONFIGS[cfg]
     if args.gamma is not None:
         gamma = args.gamma
+    strategy = args.strategy
+    fanouts = tuple(int(f) for f in args.fanouts.split(","))[-k:] if strategy == "sampled" else None
     nreq = args.warmup + args.steps
     synthetic = cfg in SYNTHETIC
     mode = args.parallel or ("cgp" if synthetic and world > 1 else ("replicas" if world > 1 else "single"))
@@ -312,9 +328,9 @@ def main():
         scfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=gamma, num_partitions=P, seed=0, device=local)
         eng = runtime.distributed_engine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream, group=pg)
     else:
-        scfg = runtime.ServeConfig(strategy="srpe", gamma=gamma, device=local)
+        scfg = runtime.ServeConfig(strategy=strategy, gamma=gamma, device=local, fanouts=fanouts)
         eng = runtime.ServingEngine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream)
-    if not synthetic:
+    if not synthetic and (cgp or strategy == "srpe"):
         eng.precompute_pe()
     info = eng.graph_info()
     log(f"[bench] rank {rank}: engine loaded in {time.time() - t0:.1f}s ({info})")
@@ -433,7 +449,7 @@ def main():
     if synthetic:
         cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "port",
                "sample": f"none: the {cfg} graph exists only on the GPUs; see the cfg2 line for the CPU baseline"}
-    elif rank == 0 and world == 1 and not args.no_cpu:
+    elif rank == 0 and world == 1 and not args.no_cpu and strategy == "srpe":
         pe_host = [eng.read_pe(l) for l in range(1, k)]
         qps, nr, cl = cpu_sample(serving, pe_host, model, w, pool, cfg, budget_s=12.0, batch=args.ref_batch)
         cpu = {"value": round(qps, 3), "unit": "queries/s", "cores": 1, "kind": "port",
@@ -459,7 +475,8 @@ def main():
         "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": desc, "batch": B, "policy": "ratio", "gamma": gamma,
-                   "strategy": "srpe-cgp" if cgp else "srpe",
+                   "strategy": "srpe-cgp" if cgp else strategy,
+                   **({"fanouts": list(fanouts)} if fanouts else {}),
                    "parallelism": (f"cgp x{P} (NVLink exchange) x {groups} group(s)" if cgp else
                                    (f"replicas x{world}" if world > 1 else "single")),
                    "l2": "flushed (512 MB write) before every timed step",

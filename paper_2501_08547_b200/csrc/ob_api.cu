@@ -563,7 +563,7 @@ static void load_model(Engine& e, int k, const ob_layer* layers, const float* co
     if (l) OB_CHECK(layers[l - 1].out_dim == sp.in_dim, OB_EINVAL, "adjacent layer dimensions do not chain");
     if (sp.kind == OB_KIND_POWER_MEAN) OB_CHECK(sp.p != 0.f, OB_EINVAL, "power_mean needs p != 0");
     if (sp.kind == OB_KIND_MOMENTS) OB_CHECK(sp.n >= 2, OB_EINVAL, "moments needs n >= 2");
-    OB_CHECK(sp.out_dim <= 256, OB_EINVAL, "layer out_dim above 256 is not supported");
+    OB_CHECK(sp.out_dim <= 2048, OB_EINVAL, "layer out_dim above 2048 is not supported");
     LayerDev& L = out[l];
     L.spec = sp;
     const int in = sp.in_dim, o = sp.out_dim;

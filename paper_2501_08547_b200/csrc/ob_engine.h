@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "ob_common.cuh"
@@ -87,13 +88,18 @@ struct RowSrc {
 
 // Weights staged for the tensor-core GEMM: B^T (Np x Kp, K-major, zero padded)
 // plus its 3xTF32 low part; K is the concatenation of 32-padded segments.
+// Weights staged for the tcgen05 GEMM.  One TMEM accumulator pair covers at
+// most 256 output columns; wider layers (Yelp/Amazon-shaped H = 512) are split
+// into column slabs of <= 256, each its own staged operand and launch.
 struct TcWeights {
   float* hi = nullptr;
   float* lo = nullptr;
   int N = 0, Np = 0, Kp = 0;
+  int n0 = 0;  // first output column of this slab
   alignas(64) unsigned char map_hi[128] = {};  // CUtensorMap (TMA, 128B swizzle, box 32 x Np)
   alignas(64) unsigned char map_lo[128] = {};
   bool map_ready = false;
+  std::shared_ptr<TcWeights> next;  // the following column slab (N > 256)
 };
 
 struct TcGemmArgs {

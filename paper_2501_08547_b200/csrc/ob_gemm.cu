@@ -428,7 +428,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
+static void tc_gemm_slab(cudaStream_t s, const TcGemmArgs& g, int64_t M_max);
+
+// one launch per <= 256-column weight slab (TMEM holds two 256-column accumulators)
 void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max) {
+  OB_CHECK(g.w && g.w->map_ready, OB_ESTATE, "tc_gemm: weights not staged");
+  if (!g.w->next) return tc_gemm_slab(s, g, M_max);
+  for (const TcWeights* w = g.w; w; w = w->next.get()) {
+    TcGemmArgs gs = g;
+    gs.w = w;
+    gs.Bt = w->hi;
+    gs.Bt_lo = w->lo;
+    gs.N = w->N;
+    gs.Np = w->Np;
+    gs.C = g.C + w->n0;
+    gs.E = g.E ? g.E + w->n0 : nullptr;
+    tc_gemm_slab(s, gs, M_max);
+  }
+}
+
+static void tc_gemm_slab(cudaStream_t s, const TcGemmArgs& g, int64_t M_max) {
   OB_CHECK(g.N >= 1 && g.N <= 256, OB_ESTATE, "tc_gemm: N out of range");
   OB_CHECK(g.w && g.w->map_ready, OB_ESTATE, "tc_gemm: weights not staged");
   const int64_t tiles = (M_max + kTcBM - 1) / kTcBM;
@@ -482,11 +501,26 @@ static void make_map(void* out, float* base, int Np, int Kp) {
   OB_CHECK(r == CUDA_SUCCESS, OB_ECUDA, "cuTensorMapEncodeTiled failed");
 }
 
+static void prep_slab(Engine& e, const std::vector<const float*>& segs, const std::vector<int>& seg_k, int Ntot,
+                      int n0, TcWeights* out);
+
 void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std::vector<int>& seg_k, int N,
                      TcWeights* out) {
   tc_gemm_configure();
+  TcWeights* cur = out;
+  for (int n0 = 0; n0 < N; n0 += 256) {  // column slabs of <= 256
+    if (n0) {
+      cur->next = std::make_shared<TcWeights>();
+      cur = cur->next.get();
+    }
+    prep_slab(e, segs, seg_k, N, n0, cur);
+  }
+}
+
+static void prep_slab(Engine& e, const std::vector<const float*>& segs, const std::vector<int>& seg_k, int Ntot,
+                      int n0, TcWeights* out) {
+  const int N = std::min(256, Ntot - n0);
   int Np = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
-  OB_CHECK(N <= 256, OB_EINVAL, "layer width above 256 is not supported by the tensor-core path");
   int Kp = 0;
   for (int k : seg_k) Kp += (k + kTcBK - 1) / kTcBK * kTcBK;
   std::vector<float> hi((size_t)Np * Kp, 0.f), lo((size_t)Np * Kp, 0.f);
@@ -496,7 +530,7 @@ void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std
     const int K = seg_k[si];
     for (int k = 0; k < K; ++k)
       for (int n = 0; n < N; ++n) {
-        float v = W[(size_t)k * N + n];
+        float v = W[(size_t)k * Ntot + n0 + n];
         uint32_t b;
         std::memcpy(&b, &v, 4);
         b &= 0xFFFFE000u;
@@ -510,6 +544,7 @@ void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std
   out->N = N;
   out->Np = Np;
   out->Kp = Kp;
+  out->n0 = n0;
   out->hi = (float*)e.dalloc(sizeof(float) * hi.size());
   out->lo = (float*)e.dalloc(sizeof(float) * lo.size());
   OB_CUDA(cudaMemcpy(out->hi, hi.data(), sizeof(float) * hi.size(), cudaMemcpyHostToDevice));
