@@ -437,13 +437,59 @@ def main():
             h2d += bd.h2d_bytes
             d2h += bd.d2h_bytes
         et = float(np.sum(e2e_ms))
+        # pipelined: the same requests through ob_serve_submit / ob_serve_wait (two in flight), so
+        # request t+1's inputs cross PCIe and t-1's rows return while t runs; every step still copies
+        # its inputs H2D from pinned memory and its rows D2H inside the timed region
+        outs_p = [torch.empty((B, H), dtype=torch.float32).pin_memory() for _ in range(2)]
+
+        def submit(i, slot):
+            t = C.c_int64()
+            nat.check(lib.ob_serve_submit(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
+                                          C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(outs_p[slot].data_ptr()),
+                                          C.byref(t)))
+            return t.value
+
+        def wait(t):
+            bdw = nat.ObBreakdown()
+            nat.check(lib.ob_serve_wait(eng._h, t, C.byref(bdw)))
+            return bdw
+
+        for i in above + [0, 1]:  # both slots' graphs captured before timing
+            wait(submit(i, i & 1))
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t_sub, t_done, pend = {}, {}, []
+        p0 = time.perf_counter()
+        for j in range(args.steps):
+            if len(pend) == 2:
+                tk, jj = pend.pop(0)
+                wait(tk)
+                t_done[jj] = time.perf_counter()
+            t_sub[j] = time.perf_counter()
+            pend.append((submit(args.warmup + j, j & 1), j))
+        for tk, jj in pend:
+            wait(tk)
+            t_done[jj] = time.perf_counter()
+        pt = (time.perf_counter() - p0) * 1e3
+        if world > 1:
+            t = torch.tensor([pt], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            pt = float(t.item())
+        plat = [(t_done[j] - t_sub[j]) * 1e3 for j in range(args.steps)]
         if world > 1:
             t = torch.tensor([et], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             et = float(t.item())
-        e2e = {"value": round(served * args.steps / (et / 1e3), 3), "unit": "queries/s",
+        e2e = {"value": round(served * args.steps / (pt / 1e3), 3), "unit": "queries/s",
                "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
-               "p50_ms": float(np.percentile(e2e_ms, 50)), "p99_ms": float(np.percentile(e2e_ms, 99))}
+               "mode": "pipelined host API (ob_serve_submit/ob_serve_wait, 2 requests in flight, pinned host "
+                       "buffers); wall clock over the K steps; no L2 flush (each request gathers > 0.5 GB)",
+               "p50_ms": float(np.percentile(plat, 50)), "p99_ms": float(np.percentile(plat, 99)),
+               "sync": {"value": round(served * args.steps / (et / 1e3), 3), "unit": "queries/s",
+                        "mode": "one ob_serve call per step (H2D, request, D2H, synchronise), CUDA events, "
+                                "L2 flushed before each step",
+                        "p50_ms": float(np.percentile(e2e_ms, 50)), "p99_ms": float(np.percentile(e2e_ms, 99))}}
 
     cpu = None
     if synthetic:

@@ -168,6 +168,18 @@ int ob_serve(ob_engine* e, int32_t num_queries, const float* query_features, int
 int ob_serve_device(ob_engine* e, int32_t num_queries, const float* d_query_features,
                     int64_t num_edges, const int64_t* d_edges, float* d_out, ob_breakdown* bd);
 
+/* Pipelined host path (production serving loop): submit copies the request's
+ * host inputs to one of two device staging slots on a copy stream and enqueues
+ * the request; the rows come back on a second copy stream.  While request t
+ * runs, request t+1's inputs cross PCIe and request t-1's rows return.  At most
+ * two requests are outstanding (OB_ESTATE otherwise); ob_serve_wait(ticket)
+ * blocks until request `ticket`'s rows are in its `out` and reports its errors
+ * and breakdown (compute_ms = device time of the request).  Host buffers must
+ * stay valid until the wait; pinned buffers give full overlap. */
+int ob_serve_submit(ob_engine* e, int32_t num_queries, const float* query_features, int64_t num_edges,
+                    const int64_t* edges, float* out, int64_t* ticket);
+int ob_serve_wait(ob_engine* e, int64_t ticket, ob_breakdown* bd);
+
 /* Parity hooks over the last served request (synchronising). */
 int ob_last_plan(ob_engine* e, int64_t* num_candidates, int64_t* num_targets, int64_t* cand_ids,
                  int64_t* cand_nq, int64_t* cand_total, double* cand_scores, int64_t* targets);

@@ -402,9 +402,19 @@ static RequestGraph& request_graph(Engine& e, float* d_out) {
   return e.graphs.back();
 }
 
-// The request pipeline.  Inputs/outputs are device pointers.
-static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const int64_t* d_edges, float* d_out,
-                         ob_breakdown* bd) {
+// blocks whose counters a breakdown reads: centralized blocks, or every partition's (mid, last)
+static std::vector<BlockDev*> counted_blocks(Engine& e) {
+  std::vector<BlockDev*> all;
+  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) {
+    for (auto& pw : e.cgp.ws) all.insert(all.end(), {&pw.blocks[0], &pw.blocks[1]});
+  } else {
+    for (auto& b : e.ws.blocks) all.push_back(&b);
+  }
+  return all;
+}
+
+// The request pipeline, enqueued on the engine stream.  Inputs/outputs are device pointers.
+static void enqueue_serve(Engine& e, int B, const float* d_q, int64_t m, const int64_t* d_edges, float* d_out) {
   check_ready(e);
   OB_CHECK(B >= 0 && m >= 0, OB_EINVAL, "negative request size");
   OB_CHECK(e.g.N + B < ((int64_t)1 << 31) - 1, OB_EINVAL, "id space exceeds int32");
@@ -416,9 +426,6 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   w.rp = e.params;
   w.edges = d_edges;
   w.qfeat = d_q;
-  const int k = (int)e.layers.size();
-  const bool srpe = !khop(e.cfg);
-  const bool cgp = e.cfg.strategy == OB_STRATEGY_SRPE_CGP;
   // kernel arguments are copied at launch: the block is stream-ordered with no host staging
   k_set_params<<<1, 1, 0, s>>>(e.params, d_edges, d_q, m);
   OB_LAUNCHED();
@@ -444,25 +451,19 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   }
   OB_CUDA(cudaEventRecord(e.ev[2], s));
   e.have_request = true;
+}
+
+// errors and the breakdown from the request's counters (read back to the host)
+static void finish_breakdown(Engine& e, const ReqCounters& rc, const std::vector<BlockCounters>& hc, float t01,
+                             float t12, ob_breakdown* bd) {
+  RequestWs& w = e.ws;
+  const int k = (int)e.layers.size();
+  const bool srpe = !khop(e.cfg);
+  const bool cgp = e.cfg.strategy == OB_STRATEGY_SRPE_CGP;
+  std::vector<BlockDev*> all = counted_blocks(e);
+  for (size_t i = 0; i < all.size() && i < hc.size(); ++i) all[i]->host = hc[i];
+  raise_request_errors(rc);
   if (!bd) return;
-  PinnedReadback hb{};
-  OB_CUDA(cudaMemcpyAsync(&hb.rc, w.rc, sizeof(ReqCounters), cudaMemcpyDeviceToHost, s));
-  std::vector<BlockDev*> all;  // centralized blocks, or every partition's (mid, last)
-  if (cgp) {
-    for (auto& pw : e.cgp.ws) all.insert(all.end(), {&pw.blocks[0], &pw.blocks[1]});
-  } else {
-    for (auto& b : w.blocks) all.push_back(&b);
-  }
-  std::vector<BlockCounters> hc(all.size());
-  for (size_t i = 0; i < all.size(); ++i)
-    OB_CUDA(cudaMemcpyAsync(&hc[i], all[i]->cnt, sizeof(BlockCounters), cudaMemcpyDeviceToHost, s));
-  OB_CUDA(cudaStreamSynchronize(s));
-  OB_CUDA(cudaGetLastError());
-  for (size_t i = 0; i < all.size(); ++i) all[i]->host = hc[i];
-  raise_request_errors(hb.rc);
-  float t01 = 0, t12 = 0;
-  OB_CUDA(cudaEventElapsedTime(&t01, e.ev[0], e.ev[1]));
-  OB_CUDA(cudaEventElapsedTime(&t12, e.ev[1], e.ev[2]));
   // graph_fetch_bytes per block set (runtime.py:105-120; CGP: _shard_fetch_bytes summed, :224-247)
   auto set_bytes = [&](const BlockCounters* blocks_of_layer[], const BlockCounters& mid) {
     std::vector<BlockCounters> per_layer(k);
@@ -493,9 +494,28 @@ static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const in
   bd->fetch_bytes = fb;
   bd->collective_bytes = e.cgp.collective_bytes;
   bd->transfer_ms = (double)bd->fetch_bytes / 12e9 * 1e3;
-  bd->num_candidates = hb.rc.R;
-  bd->num_targets = hb.rc.T;
+  bd->num_candidates = rc.R;
+  bd->num_targets = rc.T;
   bd->total_device_ms = t01 + t12;
+}
+
+static void serve_device(Engine& e, int B, const float* d_q, int64_t m, const int64_t* d_edges, float* d_out,
+                         ob_breakdown* bd) {
+  enqueue_serve(e, B, d_q, m, d_edges, d_out);
+  if (!bd) return;
+  cudaStream_t s = e.stream;
+  PinnedReadback hb{};
+  OB_CUDA(cudaMemcpyAsync(&hb.rc, e.ws.rc, sizeof(ReqCounters), cudaMemcpyDeviceToHost, s));
+  std::vector<BlockDev*> all = counted_blocks(e);
+  std::vector<BlockCounters> hc(all.size());
+  for (size_t i = 0; i < all.size(); ++i)
+    OB_CUDA(cudaMemcpyAsync(&hc[i], all[i]->cnt, sizeof(BlockCounters), cudaMemcpyDeviceToHost, s));
+  OB_CUDA(cudaStreamSynchronize(s));
+  OB_CUDA(cudaGetLastError());
+  float t01 = 0, t12 = 0;
+  OB_CUDA(cudaEventElapsedTime(&t01, e.ev[0], e.ev[1]));
+  OB_CUDA(cudaEventElapsedTime(&t12, e.ev[1], e.ev[2]));
+  finish_breakdown(e, hb.rc, hc, t01, t12, bd);
 }
 
 // ---------------------------------------------------------------------------
@@ -626,6 +646,25 @@ static std::vector<T> d2h(const T* d, int64_t n, cudaStream_t s) {
 // =============================================================================
 using namespace ob;
 
+// One slot of the pipelined host path: device staging for one request's
+// inputs/outputs, pinned counter readback, and the events that order its H2D
+// copy -> request graph -> D2H copy across the three streams.
+struct PipeSlot {
+  int64_t* d_edges = nullptr;
+  float* d_q = nullptr;
+  float* d_out = nullptr;
+  size_t cap_edges = 0, cap_q = 0, cap_out = 0;
+  ReqCounters* h_rc = nullptr;        // pinned
+  BlockCounters* h_bc = nullptr;      // pinned [kMaxCounted]
+  int n_bc = 0;
+  cudaEvent_t h2d_done = nullptr, start = nullptr, comp_done = nullptr, d2h_done = nullptr;
+  bool busy = false;
+  int64_t ticket = -1;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
+  int64_t collective_bytes = 0;
+};
+constexpr int kMaxCounted = 64;
+
 struct ob_engine {
   Engine impl;
   std::mutex mu;  // one in-flight request per engine
@@ -634,6 +673,11 @@ struct ob_engine {
   float* d_q = nullptr;
   float* d_out = nullptr;
   size_t cap_edges = 0, cap_q = 0, cap_out = 0;
+  // pipelined host path (ob_serve_submit / ob_serve_wait): two slots, so request
+  // t+1's inputs cross PCIe while request t runs and t-1's rows come back
+  PipeSlot slot[2];
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  int64_t next_ticket = 0;
 };
 
 template <class F>
@@ -725,9 +769,23 @@ int ob_engine_destroy(ob_engine* h) {
   return guarded([&] {
     if (!h) return;
     cudaSetDevice(h->impl.cfg.device);
+    if (h->h2d) cudaStreamSynchronize(h->h2d);
+    if (h->d2h) cudaStreamSynchronize(h->d2h);
+    cudaStreamSynchronize(h->impl.stream);
     if (h->d_edges) cudaFree(h->d_edges);
     if (h->d_q) cudaFree(h->d_q);
     if (h->d_out) cudaFree(h->d_out);
+    for (auto& sl : h->slot) {
+      if (sl.d_edges) cudaFree(sl.d_edges);
+      if (sl.d_q) cudaFree(sl.d_q);
+      if (sl.d_out) cudaFree(sl.d_out);
+      if (sl.h_rc) cudaFreeHost(sl.h_rc);
+      if (sl.h_bc) cudaFreeHost(sl.h_bc);
+      for (cudaEvent_t ev : {sl.h2d_done, sl.start, sl.comp_done, sl.d2h_done})
+        if (ev) cudaEventDestroy(ev);
+    }
+    if (h->h2d) cudaStreamDestroy(h->h2d);
+    if (h->d2h) cudaStreamDestroy(h->d2h);
     delete h;
   });
 }
@@ -924,6 +982,98 @@ int ob_serve(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* 
     OB_CUDA(cudaStreamSynchronize(s));
     local.h2d_bytes = 16 * m + 4 * (int64_t)B * e.g.F;
     local.d2h_bytes = 4 * (int64_t)B * H;
+    if (bd) *bd = local;
+  });
+}
+
+// Pipelined host path.  Request t uses slot t % 2: its H2D copy runs on the h2d
+// stream (after slot t's previous request finished on the device), its request
+// graph on the engine stream (after the copy and after the slot's previous D2H),
+// its D2H copy and counter readback on the d2h stream.  Up to two requests are
+// outstanding; ob_serve_wait(t) returns request t's rows in `out` and its
+// breakdown (errors of request t are raised there).
+int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* edges, float* out,
+                    int64_t* ticket) {
+  return guarded([&] {
+    OB_CHECK(h && ticket, OB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    check_ready(e);
+    OB_CHECK(B >= 0 && m >= 0, OB_EINVAL, "negative request size");
+    OB_CHECK(m == 0 || edges, OB_EINVAL, "null edges");
+    OB_CHECK(out, OB_EINVAL, "null output");
+    const int64_t t = h->next_ticket;
+    PipeSlot& sl = h->slot[t & 1];
+    OB_CHECK(!sl.busy, OB_ESTATE, "two requests already outstanding: wait for the oldest first");
+    if (!h->h2d) {
+      OB_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+      OB_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+    }
+    if (!sl.h2d_done) {
+      for (cudaEvent_t* ev : {&sl.h2d_done, &sl.start, &sl.comp_done, &sl.d2h_done}) OB_CUDA(cudaEventCreate(ev));
+      OB_CUDA(cudaMallocHost(&sl.h_rc, sizeof(ReqCounters)));
+      OB_CUDA(cudaMallocHost(&sl.h_bc, sizeof(BlockCounters) * kMaxCounted));
+    }
+    const int H = e.layers.back().spec.out_dim;
+    // the slot is idle: its previous request was waited for, so its buffers can be resized
+    ensure(sl.d_edges, sl.cap_edges, (size_t)(2 * m));
+    ensure(sl.d_q, sl.cap_q, (size_t)B * e.g.F);
+    ensure(sl.d_out, sl.cap_out, (size_t)B * H);
+    if (m) OB_CUDA(cudaMemcpyAsync(sl.d_edges, edges, sizeof(int64_t) * 2 * m, cudaMemcpyHostToDevice, h->h2d));
+    if ((int64_t)B * e.g.F)
+      OB_CUDA(cudaMemcpyAsync(sl.d_q, q, sizeof(float) * B * e.g.F, cudaMemcpyHostToDevice, h->h2d));
+    OB_CUDA(cudaEventRecord(sl.h2d_done, h->h2d));
+    cudaStream_t s = e.stream;
+    OB_CUDA(cudaStreamWaitEvent(s, sl.h2d_done, 0));
+    OB_CUDA(cudaEventRecord(sl.start, s));
+    enqueue_serve(e, B, sl.d_q, m, sl.d_edges, sl.d_out);
+    std::vector<BlockDev*> all = counted_blocks(e);
+    OB_CHECK((int)all.size() <= kMaxCounted, OB_ESTATE, "too many blocks for the pipelined readback");
+    OB_CUDA(cudaMemcpyAsync(sl.h_rc, e.ws.rc, sizeof(ReqCounters), cudaMemcpyDeviceToHost, s));
+    for (size_t i = 0; i < all.size(); ++i)
+      OB_CUDA(cudaMemcpyAsync(sl.h_bc + i, all[i]->cnt, sizeof(BlockCounters), cudaMemcpyDeviceToHost, s));
+    OB_CUDA(cudaEventRecord(sl.comp_done, s));
+    OB_CUDA(cudaStreamWaitEvent(h->d2h, sl.comp_done, 0));
+    if ((int64_t)B * H) OB_CUDA(cudaMemcpyAsync(out, sl.d_out, sizeof(float) * B * H, cudaMemcpyDeviceToHost, h->d2h));
+    OB_CUDA(cudaEventRecord(sl.d2h_done, h->d2h));
+    sl.n_bc = (int)all.size();
+    sl.busy = true;
+    sl.ticket = t;
+    sl.h2d_bytes = 16 * m + 4 * (int64_t)B * e.g.F;
+    sl.d2h_bytes = 4 * (int64_t)B * H;
+    sl.collective_bytes = e.cgp.collective_bytes;
+    h->next_ticket = t + 1;
+    *ticket = t;
+  });
+}
+
+int ob_serve_wait(ob_engine* h, int64_t ticket, ob_breakdown* bd) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(ticket >= 0, OB_EINVAL, "bad ticket");
+    PipeSlot& sl = h->slot[ticket & 1];
+    OB_CHECK(sl.busy && sl.ticket == ticket, OB_ESTATE, "ticket is not outstanding");
+    // the next slot's request keeps running; only this one's D2H is awaited
+    OB_CUDA(cudaEventSynchronize(sl.d2h_done));
+    sl.busy = false;
+    OB_CUDA(cudaGetLastError());
+    float ms = 0;
+    OB_CUDA(cudaEventElapsedTime(&ms, sl.start, sl.comp_done));
+    std::vector<BlockCounters> hc(sl.h_bc, sl.h_bc + sl.n_bc);
+    ob_breakdown local{};
+    // counters of the request that was last enqueued describe the workspace
+    // layout; both slots share one plan once the shape is reserved
+    finish_breakdown(e, *sl.h_rc, hc, 0.f, ms, &local);
+    local.fetch_ms = 0.0;  // the stage split is not recorded per slot
+    local.compute_ms = ms;
+    local.total_device_ms = ms;
+    local.collective_bytes = sl.collective_bytes;
+    local.h2d_bytes = sl.h2d_bytes;
+    local.d2h_bytes = sl.d2h_bytes;
     if (bd) *bd = local;
   });
 }

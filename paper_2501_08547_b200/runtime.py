@@ -206,8 +206,7 @@ class ServingEngine:
         return out
 
     # -- serving ---------------------------------------------------------------
-    def serve(self, request: ServingRequest) -> tuple[np.ndarray, LatencyBreakdown]:
-        """runtime.py:308-358."""
+    def _request_arrays(self, request: ServingRequest):
         if request.num_base != self.dataset.num_nodes:
             raise ValueError("request numbered against a different dataset")
         if self.config.strategy not in ("full", "sampled") and self.model.k < 2:
@@ -218,9 +217,53 @@ class ServingEngine:
             raise ValueError("query features must be B x F")
         e = np.ascontiguousarray(request.edges, dtype=np.int64)
         out = np.empty((B, self.model.layers[-1].out_dim), dtype=np.float32)
+        return B, q, e, out
+
+    def serve(self, request: ServingRequest) -> tuple[np.ndarray, LatencyBreakdown]:
+        """runtime.py:308-358."""
+        B, q, e, out = self._request_arrays(request)
         bd = nat.ObBreakdown()
         nat.check(self._lib.ob_serve(self._h, B, nat.ptr(q), int(e.shape[0]), nat.ptr(e), nat.ptr(out),
                                      C.byref(bd)))
+        return out, self._breakdown(bd)
+
+    def serve_stream(self, requests):
+        """Pipelined serving over an iterable of requests: yields (emb, LatencyBreakdown) in order.
+
+        Request t+1's inputs cross PCIe and request t-1's rows come back while
+        request t runs on the device (ob_serve_submit / ob_serve_wait, two
+        staging slots).  Each result equals ``serve(request)``'s; ``compute_ms``
+        is the request's device time.
+        """
+        pending = []  # (ticket, out, keep-alive arrays)
+        it = iter(requests)
+        done = False
+        try:
+            while True:
+                while not done and len(pending) < 2:
+                    try:
+                        req = next(it)
+                    except StopIteration:
+                        done = True
+                        break
+                    B, q, e, out = self._request_arrays(req)
+                    t = C.c_int64()
+                    nat.check(self._lib.ob_serve_submit(self._h, B, nat.ptr(q), int(e.shape[0]), nat.ptr(e),
+                                                        nat.ptr(out), C.byref(t)))
+                    pending.append((t.value, out, (q, e)))
+                if not pending:
+                    return
+                t, out, keep = pending[0]
+                bd = nat.ObBreakdown()
+                st = self._lib.ob_serve_wait(self._h, t, C.byref(bd))
+                pending.pop(0)
+                nat.check(st)
+                yield out, self._breakdown(bd)
+        finally:  # an error or an abandoned stream: retire what is still in flight
+            for t, _, _ in pending:
+                self._lib.ob_serve_wait(self._h, t, None)
+
+    def _breakdown(self, bd) -> LatencyBreakdown:
         self.last_breakdown = bd
         parts = self.config.num_partitions if self.config.strategy == "srpe-cgp" else 1
         lb = LatencyBreakdown(
