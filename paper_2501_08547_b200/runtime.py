@@ -273,7 +273,7 @@ class ServingEngine:
             collective_bytes=int(bd.collective_bytes),
             fetch_bytes=int(bd.fetch_bytes),
         )
-        return out, lb
+        return lb
 
     def serve_device(self, num_queries: int, d_query_features: int, num_edges: int, d_edges: int, d_out: int,
                      sync: bool = False):
