@@ -185,6 +185,9 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.agg = a.take<float>(Dmax * wl);
   w.mean = mom ? a.take<float>(2 * Dmax * wl) : nullptr;
   w.z = wide ? a.take<float>(Smax * wl) : nullptr;
+  w.yrow = wide ? a.take<const float*>(Smax) : nullptr;
+  w.dyn_src = wide ? a.take<int32_t>(Smax) : nullptr;
+  w.ndyn = wide ? a.take<int64_t>(1) : nullptr;
   w.s_src = gat ? a.take<float>(Smax) : nullptr;
   w.s_dst = gat ? a.take<float>(Dmax) : nullptr;
   for (int l = 1; l < k; ++l) {
@@ -419,6 +422,7 @@ static void enqueue_serve(Engine& e, int B, const float* d_q, int64_t m, const i
   OB_CHECK(B >= 0 && m >= 0, OB_EINVAL, "negative request size");
   OB_CHECK(e.g.N + B < ((int64_t)1 << 31) - 1, OB_EINVAL, "id space exceeds int32");
   cgp_localize_storage(e);  // NCCL CGP: keep only the owned rows (no-op otherwise)
+  build_stored_transforms(e);  // once per (model, PE) state, outside any capture
   cudaStream_t s = e.stream;
   prepare_workspace(e, B, std::max(bucket_m(m), e.m_reserved));
   RequestWs& w = e.ws;
@@ -796,6 +800,7 @@ int ob_load_graph(ob_engine* h, int64_t N, const int64_t* off, const int64_t* nb
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
     load_graph(h->impl, N, off, nb, E, feats, F);
     if (h->impl.cfg.strategy == OB_STRATEGY_SRPE_CGP) cgp_build_partitions(h->impl);
   });
@@ -806,6 +811,7 @@ int ob_generate_graph(ob_engine* h, int64_t N, double avg_degree, double exponen
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
     generate_graph(h->impl, N, avg_degree, exponent, F, seed);
   });
 }
@@ -815,6 +821,7 @@ int ob_generate_pe(ob_engine* h, int32_t layer, int32_t dim, uint64_t seed) {
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
     generate_pe(h->impl, layer, dim, seed);
   });
 }
@@ -899,6 +906,7 @@ int ob_load_pe(ob_engine* h, int32_t layer, const float* rows, int64_t n, int32_
     std::lock_guard<std::mutex> lk(h->mu);
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
+    e.drop_ytab();  // stored transforms follow the weights, features and PE
     OB_CHECK(e.g.N > 0, OB_ESTATE, "load the graph before stored embeddings");
     OB_CHECK(layer >= 1 && layer <= 7, OB_EINVAL, "bad stored-embedding layer");
     OB_CHECK(n == e.g.N, OB_EINVAL, "stored embeddings must cover every node");
@@ -925,6 +933,7 @@ int ob_load_model(ob_engine* h, int32_t k, const ob_layer* layers, const float* 
     OB_CHECK(h && layers && mats, OB_EINVAL, "null argument");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
     load_model(h->impl, k, layers, mats);
   });
 }
@@ -934,6 +943,7 @@ int ob_precompute_pe(ob_engine* h) {
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
     OB_CHECK(!h->impl.layers.empty(), OB_ESTATE, "load a model first");
     OB_CHECK(h->impl.layers[0].spec.in_dim == h->impl.g.F, OB_EINVAL, "input width does not match layer in_dim");
     OB_CHECK(h->impl.g.offsets && !h->impl.g.pos, OB_ESTATE,

@@ -286,6 +286,9 @@ struct RequestWs {
   std::vector<int> block_of_layer; // layer -> index into blocks
   // execution scratch
   const float** rowp = nullptr;    // [S_max] input row per source
+  const float** yrow = nullptr;    // [S_max] stored-transform row per source (wide layers)
+  int32_t* dyn_src = nullptr;      // [S_max] sources whose transformed row is computed per request
+  int64_t* ndyn = nullptr;
   float* gscale = nullptr;         // [S_max] gcn source normaliser
   float* partial = nullptr;        // [items_max][w + 2]
   float* partial2 = nullptr;       // [groups_max][w + 2] second-level partials of hub destinations
@@ -351,6 +354,14 @@ struct BindCtx {
   const int32_t* tpos;
   const int32_t* indeg;
   const int32_t* qdeg;
+  // stored transforms (layers that gather X W rows): static rows of FEATURE /
+  // PE-bound sources come from the table, the rest are listed for a GEMM
+  const float* ytab;    // [N][y_ld] or null
+  int64_t y_ld;
+  const float** yrow;   // [S] row pointer of each source's transformed row
+  float* ydyn;          // [dyn][y_ld] transformed rows of the listed sources
+  int32_t* dyn_src;     // [dyn] source index per listed row
+  int64_t* ndyn;        // device count of listed rows (zeroed before k_resolve)
 };
 
 struct LayerRun {
@@ -367,6 +378,11 @@ struct LayerRun {
   RowSrc x;                  // bound inputs
   const float* gscale;       // gcn
   const int64_t* group_ptr;  // second-level partial groups (hub destinations)
+  // stored transforms: Y rows by pointer, only the listed (dynamic) sources go through the GEMM
+  const float** yrow = nullptr;
+  const int32_t* dyn_src = nullptr;
+  const int64_t* ndyn = nullptr;
+  int64_t dyn_max = 0;
 };
 
 // CGP merge inputs: partition p's raw partial rows and local in-edge counts
@@ -407,6 +423,7 @@ struct LayerScratch {
 
 void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc, float* out,
                int64_t ldo);
+void build_stored_transforms(Engine& e);
 void launch_resolve(cudaStream_t s, const BindCtx& c, BlockCounters* cnt, int64_t S_max, const int32_t* src_ids,
                     const float** rowp, float* gscale);
 // CGP: this partition's raw per-destination partial (cgpexec.py:111-164, not normalised)
@@ -618,6 +635,17 @@ struct Engine {
   std::vector<LayerDev> layers;
   std::vector<float*> pe;        // per stored layer, N x ld4(dim)
   std::vector<int> pe_dim;
+  // stored transforms: per layer that gathers transformed rows (GAT z = x W,
+  // transform-first X W_neigh / X W), the table x_v W over every training node
+  // whose layer input is static (features at layer 1, stored embeddings above);
+  // built lazily before the first request, dropped when weights / PE change
+  std::vector<float*> ytab;
+  bool ytab_ready = false;
+  void drop_ytab() {
+    for (float* t : ytab) dfree(t);
+    ytab.clear();
+    ytab_ready = false;
+  }
   Arena arena;
   ScanScratch scan;
   RequestWs ws;

@@ -24,6 +24,8 @@
 // cuts the gathered bytes by in/out.
 #include <type_traits>
 
+#include <cstdlib>
+
 #include "ob_engine.h"
 
 namespace ob {
@@ -81,6 +83,23 @@ __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restri
     int pl;
     int k = bind_row(c, T, s, g, &r, &pl);
     rowp[s] = r;
+    if (c.yrow) {
+      // FEATURE rows of training nodes and PE rows are static: their x W is in the table
+      const bool stat = (k == 0 && g < c.N) || k == 1;
+      if (stat) {
+        c.yrow[s] = c.ytab + g * c.y_ld;
+      } else {
+        const unsigned act = __activemask();
+        const unsigned b = __ballot_sync(act, 1);
+        const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+        int64_t base = 0;
+        if (lane == leader) base = (int64_t)atomicAdd((unsigned long long*)c.ndyn, (unsigned long long)__popc(b));
+        base = __shfl_sync(act, base, leader);
+        const int64_t slot = base + __popc(b & ((1u << lane) - 1u));
+        c.dyn_src[slot] = (int32_t)s;
+        c.yrow[s] = c.ydyn + slot * c.y_ld;
+      }
+    }
     if (gscale) {
       int64_t d = g < c.N ? c.indeg[g] : c.qdeg[g - c.N];
       gscale[s] = (float)(1.0 / sqrt((double)d + 1.0));
@@ -418,14 +437,15 @@ __global__ void __launch_bounds__(256) k_finalize_moments(const BlockCounters* c
 }
 
 // GAT attention scores: s[r] = z[row(r)] . a  (one warp per row)
-__global__ void k_rowdot(const int64_t* M_dev, const float* __restrict__ z, int64_t ldz, const int32_t* self, int w,
-                         const float* __restrict__ av, float* out) {
+// out[r] = z_row(self[r] or r) . av  (GAT source / destination scores)
+__global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* self, int w,
+                              const float* __restrict__ av, float* out) {
   const int64_t M = *M_dev;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = gw; r < M; r += nw) {
-    const float* row = z + (self ? (int64_t)self[r] : r) * ldz;
+    const float* row = z.row(self ? (int64_t)self[r] : r);
     float s = 0.f;
     for (int c = lane; c < w; c += 32) s = fmaf(row[c], av[c], s);
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -517,7 +537,20 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   f.out = sc.agg;
   f.ldo = ld4(in);
 
-  if (sp.kind == OB_KIND_GAT || L.transform_first) {
+  if ((sp.kind == OB_KIND_GAT || L.transform_first) && r.yrow) {
+    // stored transforms: only the listed sources (queries, recomputed rows) need x W now
+    TcGemmArgs g = gemm_args(r.ndyn, L.tw_main, sc.z, ld_out, false);
+    g.a1 = r.x;
+    g.self = r.dyn_src;
+    g.K1 = in;
+    gemm(s, g, r.dyn_max, nullptr);
+    a.x = RowSrc{r.yrow, nullptr, 0};
+    a.width = outd;
+    a.pw = ld4(outd);
+    f.width = outd;
+    f.pw = ld4(outd);
+    f.ldo = ld_out;
+  } else if (sp.kind == OB_KIND_GAT || L.transform_first) {
     // Y = X W over every source row (GAT: z; transform-first: X W_neigh or X W)
     TcGemmArgs g = gemm_args(r.S_dev, L.tw_main, sc.z, ld_out, false);
     g.a1 = r.x;
@@ -531,8 +564,9 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     f.ldo = ld_out;
   }
   if (sp.kind == OB_KIND_GAT) {
-    k_rowdot<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, sc.z, ld_out, nullptr, outd, L.a_src, sc.s_src);
-    k_rowdot<<<grid_for(r.D_max, 8), 256, 0, s>>>(r.D_dev, sc.z, ld_out, r.self, outd, L.a_dst, sc.s_dst);
+    const RowSrc z = r.yrow ? RowSrc{r.yrow, nullptr, 0} : RowSrc{nullptr, sc.z, ld_out};
+    k_rowdot_rows<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, z, nullptr, outd, L.a_src, sc.s_src);
+    k_rowdot_rows<<<grid_for(r.D_max, 8), 256, 0, s>>>(r.D_dev, z, r.self, outd, L.a_dst, sc.s_dst);
     g_launches += 2;
     a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
@@ -805,7 +839,8 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
     return;
   }
   if (sp.kind == OB_KIND_GAT) {
-    k_rowdot<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, sc.z, ld_out, nullptr, outd, L.a_src, sc.s_src);
+    k_rowdot_rows<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, RowSrc{nullptr, sc.z, ld_out}, nullptr, outd,
+                                                       L.a_src, sc.s_src);
     OB_LAUNCHED();
     a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
@@ -948,9 +983,25 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     const LayerDev& L = e.layers[l - 1];
     BlockDev& b = w.blocks[w.block_of_layer[l - 1]];
     BindCtx c = bind_ctx(e, w, l);
+    const bool yt = e.ytab_ready && l - 1 < (int)e.ytab.size() && e.ytab[l - 1];
+    if (yt) {
+      c.ytab = e.ytab[l - 1];
+      c.y_ld = ld4(L.spec.out_dim);
+      c.yrow = w.yrow;
+      c.ydyn = w.z;
+      c.dyn_src = w.dyn_src;
+      c.ndyn = w.ndyn;
+      OB_CUDA(cudaMemsetAsync(w.ndyn, 0, sizeof(int64_t), s));
+    }
     k_resolve<<<grid_for(b.S_max, 256), 256, 0, s>>>(c, b.cnt, b.src_ids, w.rowp, w.gscale, nullptr, nullptr);
     OB_LAUNCHED();
     LayerRun r{};
+    if (yt) {
+      r.yrow = w.yrow;
+      r.dyn_src = w.dyn_src;
+      r.ndyn = w.ndyn;
+      r.dyn_max = b.S_max;
+    }
     r.cnt = b.cnt;
     r.D_dev = &b.cnt->D;
     r.S_dev = &b.cnt->S;
@@ -983,6 +1034,50 @@ void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d
   BindCtx c = bind_ctx(e, w, layer);
   k_resolve<<<grid_for(b.S_max, 256), 256, 0, e.stream>>>(c, b.cnt, b.src_ids, w.rowp, nullptr, d_kind, d_pe_layer);
   OB_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
+// stored transforms: x_v W for every training node whose layer input is static
+// ---------------------------------------------------------------------------
+void build_stored_transforms(Engine& e) {
+  if (e.ytab_ready) return;
+  e.ytab_ready = true;  // decided once per (model, PE) state; tables may stay empty
+  const char* off = std::getenv("OB_NO_STORED_TRANSFORMS");
+  if (off && off[0] && off[0] != '0') return;
+  if (e.g.pos || e.cfg.strategy == OB_STRATEGY_SRPE_CGP || !e.g.feats) return;  // centralized, full tables
+  const int k = (int)e.layers.size();
+  const int64_t N = e.g.N;
+  std::vector<int> want(k, 0);
+  size_t bytes = 0;
+  for (int l = 1; l <= k; ++l) {
+    const LayerDev& L = e.layers[l - 1];
+    if (!(L.spec.kind == OB_KIND_GAT || L.transform_first)) continue;
+    const bool stat_in = l == 1 || (!khop(e.cfg) && (int)e.pe.size() >= l - 1 && e.pe[l - 2]);
+    if (!stat_in) continue;
+    want[l - 1] = 1;
+    bytes += (size_t)N * ld4(L.spec.out_dim) * 4;
+  }
+  if (!bytes) return;
+  size_t free_b = 0, total_b = 0;
+  OB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if (bytes > free_b / 3) return;  // keep room for request workspaces
+  cudaStream_t s = e.stream;
+  int64_t* n_dev = (int64_t*)e.dalloc(sizeof(int64_t));
+  OB_CUDA(cudaMemcpyAsync(n_dev, &N, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  e.ytab.assign(k, nullptr);
+  for (int l = 1; l <= k; ++l) {
+    if (!want[l - 1]) continue;
+    const LayerDev& L = e.layers[l - 1];
+    const int64_t ld = ld4(L.spec.out_dim);
+    float* t = (float*)e.dalloc(sizeof(float) * N * ld);
+    TcGemmArgs g = gemm_args(n_dev, L.tw_main, t, ld, false);
+    g.a1 = l == 1 ? RowSrc{nullptr, e.g.feats, e.g.F_ld} : RowSrc{nullptr, e.pe[l - 2], ld4(L.spec.in_dim)};
+    g.K1 = L.spec.in_dim;
+    tc_gemm(s, g, N);
+    e.ytab[l - 1] = t;
+  }
+  OB_CUDA(cudaStreamSynchronize(s));
+  e.dfree(n_dev);
 }
 
 // ---------------------------------------------------------------------------
