@@ -383,6 +383,12 @@ struct LayerRun {
   const int32_t* dyn_src = nullptr;
   const int64_t* ndyn = nullptr;
   int64_t dyn_max = 0;
+  // stored aggregates (layer 1 of sum kinds): static CSR-part sums per training node
+  const float* stat = nullptr;
+  int64_t stat_ld = 0;
+  const int32_t* dst_ids = nullptr;
+  const int32_t* indeg = nullptr;
+  int64_t N = 0;
 };
 
 // CGP merge inputs: partition p's raw partial rows and local in-edge counts
@@ -640,10 +646,16 @@ struct Engine {
   // whose layer input is static (features at layer 1, stored embeddings above);
   // built lazily before the first request, dropped when weights / PE change
   std::vector<float*> ytab;
+  // stored aggregates: for sum kinds (gcn, sage_mean) the layer-1 aggregate of a
+  // training node's CSR in-neighbours is static (only request edges, whose
+  // sources are queries, change it): sagg1[v] = sum_u w_u x_u (W), raw, unnormalised
+  float* sagg1 = nullptr;
   bool ytab_ready = false;
   void drop_ytab() {
     for (float* t : ytab) dfree(t);
     ytab.clear();
+    dfree(sagg1);
+    sagg1 = nullptr;
     ytab_ready = false;
   }
   Arena arena;

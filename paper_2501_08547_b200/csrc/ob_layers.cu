@@ -144,6 +144,11 @@ struct AggArgs {
   const float* s_dst;
   float* partial;        // [items][pw]
   int pw;                // partial row stride: ld4(width), softmax kSmHdr + ld4(width)
+  // stored aggregates (layer 1): a training destination's CSR part is in the
+  // table, so only its request span (the row's suffix of query sources) is gathered
+  const int32_t* skip_dst_ids = nullptr;
+  const int32_t* skip_indeg = nullptr;
+  int64_t skip_N = 0;
 };
 
 template <int OP, int NV>
@@ -159,8 +164,12 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = __ldg(a.item_dst + it);
     const int64_t j = it - a.item_ptr[i];
-    const int64_t e0 = a.dst_ptr[i] + j * kAggChunk;
+    int64_t e0 = a.dst_ptr[i] + j * kAggChunk;
     const int64_t e1 = min(e0 + kAggChunk, a.dst_ptr[i + 1]);
+    if (a.skip_indeg) {
+      const int64_t v = __ldg(a.skip_dst_ids + i);
+      if (v < a.skip_N) e0 = max(e0, a.dst_ptr[i] + (int64_t)__ldg(a.skip_indeg + v));
+    }
     AT acc[NV][4];
     float m_run = -INFINITY, den = 0.f;
 #pragma unroll
@@ -257,6 +266,11 @@ __global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
 // merge a destination's partials in item order and normalise (warp per dst)
 // ---------------------------------------------------------------------------
 struct FinArgs {
+  // stored aggregates: raw CSR-part sum of each training destination, added before normalising
+  const float* stat = nullptr;
+  int64_t stat_ld = 0;
+  const int32_t* stat_dst_ids = nullptr;
+  int64_t stat_N = 0;
   const BlockCounters* cnt;
   const int64_t* dst_ptr;
   const int64_t* item_ptr;
@@ -393,8 +407,17 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
     float ms = 0.f, den = 0.f;
     // (max, sum exp, sum exp*z) merge in item order (cgpexec.py:225-239)
     if (mk == kMergeSoftmax) sm_header(part, a.pw, i0, i1, ms, den);
+    const float* st = nullptr;
+    if (a.stat) {
+      const int64_t v = a.stat_dst_ids[i];
+      if (v < a.stat_N) st = a.stat + v * a.stat_ld;
+    }
     for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
-      const float4 v = merge_cols(mk, part, a.pw, i0, i1, hdr, c4, ms);
+      float4 v = merge_cols(mk, part, a.pw, i0, i1, hdr, c4, ms);
+      if (st) {
+        const float4 q = ld4f(st + c4);
+        v = make_float4(q.x + v.x, q.y + v.y, q.z + v.z, q.w + v.w);
+      }
       const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -536,6 +559,15 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   f.n = sp.n;
   f.out = sc.agg;
   f.ldo = ld4(in);
+  if (r.stat) {  // stored aggregates: gather only the request spans, add the static CSR part
+    a.skip_dst_ids = r.dst_ids;
+    a.skip_indeg = r.indeg;
+    a.skip_N = r.N;
+    f.stat = r.stat;
+    f.stat_ld = r.stat_ld;
+    f.stat_dst_ids = r.dst_ids;
+    f.stat_N = r.N;
+  }
 
   if ((sp.kind == OB_KIND_GAT || L.transform_first) && r.yrow) {
     // stored transforms: only the listed sources (queries, recomputed rows) need x W now
@@ -1002,6 +1034,13 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       r.ndyn = w.ndyn;
       r.dyn_max = b.S_max;
     }
+    if (l == 1 && e.sagg1) {
+      r.stat = e.sagg1;
+      r.stat_ld = ld4(L.transform_first ? L.spec.out_dim : L.spec.in_dim);
+      r.dst_ids = b.dst_ids;
+      r.indeg = e.g.indeg;
+      r.N = e.g.N;
+    }
     r.cnt = b.cnt;
     r.D_dev = &b.cnt->D;
     r.S_dev = &b.cnt->S;
@@ -1036,6 +1075,32 @@ void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d
   OB_LAUNCHED();
 }
 
+// raw CSR-part sum per node: out[v] = sum_{u in N(v)} w_u x_u (w_u = 1/sqrt(deg u + 1) for gcn),
+// warp per node, 4 columns per lane, rows in CSR order
+__global__ void k_sagg_build(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
+                             RowSrc x, int width, const int32_t* __restrict__ indeg, bool gcn, float* out,
+                             int64_t ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = gw; v < N; v += nw) {
+    for (int c4 = lane * 4; c4 < ld; c4 += 128) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+        const int32_t u = __ldg(nbrs + e);
+        const float wgt = gcn ? (float)(1.0 / sqrt((double)__ldg(indeg + u) + 1.0)) : 1.f;
+        const float4 q = c4 < width ? __ldg(reinterpret_cast<const float4*>(x.row(u) + c4))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        acc.x = fmaf(wgt, q.x, acc.x);
+        acc.y = fmaf(wgt, q.y, acc.y);
+        acc.z = fmaf(wgt, q.z, acc.z);
+        acc.w = fmaf(wgt, q.w, acc.w);
+      }
+      *reinterpret_cast<float4*>(out + v * ld + c4) = acc;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // stored transforms: x_v W for every training node whose layer input is static
 // ---------------------------------------------------------------------------
@@ -1057,10 +1122,9 @@ void build_stored_transforms(Engine& e) {
     want[l - 1] = 1;
     bytes += (size_t)N * ld4(L.spec.out_dim) * 4;
   }
-  if (!bytes) return;
   size_t free_b = 0, total_b = 0;
   OB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  if (bytes > free_b / 3) return;  // keep room for request workspaces
+  if (bytes > free_b / 3) want.assign(k, 0);  // keep room for request workspaces
   cudaStream_t s = e.stream;
   int64_t* n_dev = (int64_t*)e.dalloc(sizeof(int64_t));
   OB_CUDA(cudaMemcpyAsync(n_dev, &N, sizeof(int64_t), cudaMemcpyHostToDevice, s));
@@ -1075,6 +1139,25 @@ void build_stored_transforms(Engine& e) {
     g.K1 = L.spec.in_dim;
     tc_gemm(s, g, N);
     e.ytab[l - 1] = t;
+  }
+  // stored aggregates of layer 1 (sum kinds, srpe / full: block-1 rows are CSR ++ request)
+  const LayerDev& L1 = e.layers[0];
+  const bool sum_kind = L1.spec.kind == OB_KIND_GCN || L1.spec.kind == OB_KIND_SAGE_MEAN;
+  const bool rows_full = e.cfg.strategy == OB_STRATEGY_SRPE || e.cfg.strategy == OB_STRATEGY_FULL;
+  const char* off_sa = std::getenv("OB_NO_STORED_AGGREGATES");
+  const bool sa_off = off_sa && off_sa[0] && off_sa[0] != '0';
+  if (sum_kind && rows_full && !sa_off && e.g.offsets && (!L1.transform_first || e.ytab[0])) {
+    const int w = L1.transform_first ? L1.spec.out_dim : L1.spec.in_dim;
+    const int64_t ld = ld4(w);
+    size_t fb = 0, tb = 0;
+    OB_CUDA(cudaMemGetInfo(&fb, &tb));
+    if ((size_t)N * ld * 4 <= fb / 3) {
+      e.sagg1 = (float*)e.dalloc(sizeof(float) * N * ld);
+      const RowSrc x = L1.transform_first ? RowSrc{nullptr, e.ytab[0], ld} : RowSrc{nullptr, e.g.feats, e.g.F_ld};
+      k_sagg_build<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, x, w, e.g.indeg,
+                                                                   L1.spec.kind == OB_KIND_GCN, e.sagg1, ld);
+      OB_LAUNCHED();
+    }
   }
   OB_CUDA(cudaStreamSynchronize(s));
   e.dfree(n_dev);

@@ -1,4 +1,6 @@
-"""Stored transforms: x_v W precomputed for every training node whose layer input is static
+"""Stored transforms and stored aggregates.
+
+Stored transforms: x_v W precomputed for every training node whose layer input is static
 (features at layer 1, stored embeddings above) replace the per-request GEMM over those sources;
 only queries and recomputed rows are transformed per request.  Results must equal the
 per-request path bit for bit (same GEMM kernel per row) and the oracle within 1e-4."""
@@ -23,21 +25,24 @@ def graph():
     return serving, reqs
 
 
-def _serve(serving, reqs, model, w, pe, strategy, disable):
+def _serve(serving, reqs, model, w, pe, strategy, no_transforms=False, no_aggregates=False):
     from paper_2501_08547_b200 import runtime
 
-    old = os.environ.get("OB_NO_STORED_TRANSFORMS")
-    os.environ["OB_NO_STORED_TRANSFORMS"] = "1" if disable else "0"
+    keys = {"OB_NO_STORED_TRANSFORMS": no_transforms, "OB_NO_STORED_AGGREGATES": no_aggregates}
+    old = {k: os.environ.get(k) for k in keys}
+    for k, v in keys.items():
+        os.environ[k] = "1" if v else "0"
     try:
         cfg = runtime.ServeConfig(strategy=strategy, gamma=0.3, fanouts=(6, 4, 3) if strategy == "sampled" else None)
         eng = runtime.ServingEngine(serving, pe, model, w, cfg)
         out = [eng.serve(r)[0] for r in reqs]
         eng.close()
     finally:
-        if old is None:
-            os.environ.pop("OB_NO_STORED_TRANSFORMS", None)
-        else:
-            os.environ["OB_NO_STORED_TRANSFORMS"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     return out
 
 
@@ -53,10 +58,12 @@ def test_stored_transforms_bitwise(graph, kind, strategy):
     layers = [dict(kind=s.kind, in_dim=s.in_dim, out_dim=s.out_dim) for s in model.layers]
     pe = graphstore.PeStore(OL.precompute(layers, w.layers, serving.in_offsets, serving.in_neighbors,
                                           serving.features)) if strategy == "srpe" else None
-    a = _serve(serving, reqs, model, w, pe, strategy, disable=False)
-    b = _serve(serving, reqs, model, w, pe, strategy, disable=True)
-    for x, y in zip(a, b):
-        assert np.array_equal(x, y)
+    a = _serve(serving, reqs, model, w, pe, strategy)  # stored transforms + stored aggregates
+    b = _serve(serving, reqs, model, w, pe, strategy, no_aggregates=True)  # stored transforms only
+    c = _serve(serving, reqs, model, w, pe, strategy, no_transforms=True, no_aggregates=True)
+    for x, y, z in zip(a, b, c):
+        assert np.array_equal(y, z)  # same GEMM per row: bitwise
+        assert OL.max_rel_err(x, z) <= 1e-5  # layer-1 sums re-associated (static CSR part + request span)
     if strategy != "sampled":
         r = reqs[0]
         ref = OL.serve(strategy, layers, w.layers, serving.num_nodes, r.num_queries, serving.in_offsets,
