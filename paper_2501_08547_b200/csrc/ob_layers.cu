@@ -152,7 +152,7 @@ struct AggArgs {
 };
 
 template <int OP, int NV>
-__global__ void __launch_bounds__(32 * kAggWarps) k_agg(AggArgs a) {
+__global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : 1)) k_agg(AggArgs a) {
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   const int lane = threadIdx.x & 31;
@@ -412,9 +412,24 @@ __global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
       const int64_t v = a.stat_dst_ids[i];
       if (v < a.stat_N) st = a.stat + v * a.stat_ld;
     }
+    // softmax: the static (max, sum exp, sum exp z) triple joins the item partials
+    float sc_items = 1.f, sc_stat = 0.f;
+    if (st && mk == kMergeSoftmax) {
+      const float2 h = __ldg(reinterpret_cast<const float2*>(st));
+      if (h.y > 0.f) {
+        const float M = den > 0.f ? fmaxf(ms, h.x) : h.x;
+        sc_items = den > 0.f ? __expf(ms - M) : 0.f;
+        sc_stat = __expf(h.x - M);
+        den = den * sc_items + h.y * sc_stat;
+      }
+    }
     for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
       float4 v = merge_cols(mk, part, a.pw, i0, i1, hdr, c4, ms);
-      if (st) {
+      if (st && mk == kMergeSoftmax) {
+        const float4 q = ld4f(st + hdr + c4);
+        v = make_float4(fmaf(sc_stat, q.x, v.x * sc_items), fmaf(sc_stat, q.y, v.y * sc_items),
+                        fmaf(sc_stat, q.z, v.z * sc_items), fmaf(sc_stat, q.w, v.w * sc_items));
+      } else if (st) {
         const float4 q = ld4f(st + c4);
         v = make_float4(q.x + v.x, q.y + v.y, q.z + v.z, q.w + v.w);
       }
@@ -1036,7 +1051,8 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     }
     if (l == 1 && e.sagg1) {
       r.stat = e.sagg1;
-      r.stat_ld = ld4(L.transform_first ? L.spec.out_dim : L.spec.in_dim);
+      r.stat_ld = L.spec.kind == OB_KIND_GAT ? kSmHdr + ld4(L.spec.out_dim)
+                                             : ld4(L.transform_first ? L.spec.out_dim : L.spec.in_dim);
       r.dst_ids = b.dst_ids;
       r.indeg = e.g.indeg;
       r.N = e.g.N;
@@ -1101,6 +1117,54 @@ __global__ void k_sagg_build(int64_t N, const int64_t* __restrict__ off, const i
   }
 }
 
+// GAT layer 1: the CSR part's softmax triple per node (max logit, sum exp,
+// sum exp * z_u) with logit = leaky_relu_0.2(s_src[u] + z_v . a_dst) -- the
+// destination score of a training node is static at layer 1 (models.py:199-206)
+__global__ void k_sagg_gat_build(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
+                                 const float* __restrict__ z, int64_t zld, int width, const float* __restrict__ ssrc,
+                                 const float* __restrict__ a_dst, float* out, int64_t ld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = gw; v < N; v += nw) {
+    float sd = 0.f;
+    for (int c = lane; c < width; c += 32) sd = fmaf(z[v * zld + c], a_dst[c], sd);
+    for (int o = 16; o; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+    const int64_t e0 = off[v], e1 = off[v + 1];
+    float m = -INFINITY;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const float lg = ssrc[nbrs[e]] + sd;
+      m = fmaxf(m, lg >= 0.f ? lg : 0.2f * lg);
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float den = 0.f;
+    for (int c4 = lane * 4; c4 < ld - kSmHdr; c4 += 128) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float dd = 0.f;
+      for (int64_t e = e0; e < e1; ++e) {
+        const int32_t u = __ldg(nbrs + e);
+        const float lg0 = ssrc[u] + sd;
+        const float p = __expf((lg0 >= 0.f ? lg0 : 0.2f * lg0) - m);
+        dd += p;
+        const float4 q = c4 < width ? __ldg(reinterpret_cast<const float4*>(z + (int64_t)u * zld + c4))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        acc.x = fmaf(p, q.x, acc.x);
+        acc.y = fmaf(p, q.y, acc.y);
+        acc.z = fmaf(p, q.z, acc.z);
+        acc.w = fmaf(p, q.w, acc.w);
+      }
+      den = dd;
+      *reinterpret_cast<float4*>(out + v * ld + kSmHdr + c4) = acc;
+    }
+    if (lane == 0) {
+      out[v * ld] = e1 > e0 ? m : -INFINITY;
+      out[v * ld + 1] = e1 > e0 ? den : 0.f;
+      out[v * ld + 2] = 0.f;
+      out[v * ld + 3] = 0.f;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // stored transforms: x_v W for every training node whose layer input is static
 // ---------------------------------------------------------------------------
@@ -1140,8 +1204,31 @@ void build_stored_transforms(Engine& e) {
     tc_gemm(s, g, N);
     e.ytab[l - 1] = t;
   }
-  // stored aggregates of layer 1 (sum kinds, srpe / full: block-1 rows are CSR ++ request)
+  // stored aggregates of layer 1 (srpe / full: block-1 rows are CSR ++ request)
   const LayerDev& L1 = e.layers[0];
+  {
+    const char* off_g = std::getenv("OB_NO_STORED_AGGREGATES");
+    const bool rows_full_g = e.cfg.strategy == OB_STRATEGY_SRPE || e.cfg.strategy == OB_STRATEGY_FULL;
+    if (L1.spec.kind == OB_KIND_GAT && rows_full_g && !(off_g && off_g[0] && off_g[0] != '0') && e.g.offsets &&
+        e.ytab[0]) {  // softmax triple over the CSR part
+      const int w = L1.spec.out_dim;
+      const int64_t zld = ld4(w), ld = kSmHdr + ld4(w);
+      size_t fb = 0, tb = 0;
+      OB_CUDA(cudaMemGetInfo(&fb, &tb));
+      if ((size_t)N * (ld + 1) * 4 <= fb / 3) {
+        float* ssrc = (float*)e.dalloc(sizeof(float) * N);
+        k_rowdot_rows<<<grid_for(N, 8), 256, 0, s>>>(n_dev, RowSrc{nullptr, e.ytab[0], zld}, nullptr, w, L1.a_src,
+                                                      ssrc);
+        OB_LAUNCHED();
+        e.sagg1 = (float*)e.dalloc(sizeof(float) * N * ld);
+        k_sagg_gat_build<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, e.ytab[0], zld, w,
+                                                                        ssrc, L1.a_dst, e.sagg1, ld);
+        OB_LAUNCHED();
+        OB_CUDA(cudaStreamSynchronize(s));
+        e.dfree(ssrc);
+      }
+    }
+  }
   const bool sum_kind = L1.spec.kind == OB_KIND_GCN || L1.spec.kind == OB_KIND_SAGE_MEAN;
   const bool rows_full = e.cfg.strategy == OB_STRATEGY_SRPE || e.cfg.strategy == OB_STRATEGY_FULL;
   const char* off_sa = std::getenv("OB_NO_STORED_AGGREGATES");
