@@ -180,6 +180,17 @@ int ob_serve_submit(ob_engine* e, int32_t num_queries, const float* query_featur
                     const int64_t* edges, float* out, int64_t* ticket);
 int ob_serve_wait(ob_engine* e, int64_t ticket, ob_breakdown* bd);
 
+/* Request lanes: with n = 2, consecutive ob_serve_device calls (and the two
+ * slots of ob_serve_submit) alternate between two independent request
+ * workspaces on two streams, so one request's graph construction (many small
+ * latency-bound kernels) overlaps the other's aggregation gathers.  Lane 0 uses
+ * the engine stream; ob_lanes_fork orders the other lanes after lane 0's
+ * enqueued work and ob_lanes_join orders lane 0 after theirs (bracket a batch
+ * of device serves with them to time it on lane 0's stream).  Not for CGP. */
+int ob_set_lanes(ob_engine* e, int32_t n);
+int ob_lanes_fork(ob_engine* e);
+int ob_lanes_join(ob_engine* e);
+
 /* Parity hooks over the last served request (synchronising). */
 int ob_last_plan(ob_engine* e, int64_t* num_candidates, int64_t* num_targets, int64_t* cand_ids,
                  int64_t* cand_nq, int64_t* cand_total, double* cand_scores, int64_t* targets);

@@ -89,6 +89,9 @@ _SIGS = {
     "ob_serve_device": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(ObBreakdown)]),
     "ob_serve_submit": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(C.c_int64)]),
     "ob_serve_wait": (C.c_int, [_P, C.c_int64, C.POINTER(ObBreakdown)]),
+    "ob_set_lanes": (C.c_int, [_P, C.c_int32]),
+    "ob_lanes_fork": (C.c_int, [_P]),
+    "ob_lanes_join": (C.c_int, [_P]),
     "ob_last_plan": (C.c_int, [_P, _I64P, _I64P, _P, _P, _P, _P, _P]),
     "ob_last_block_sizes": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P, _I64P, _I64P]),
     "ob_last_block": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),

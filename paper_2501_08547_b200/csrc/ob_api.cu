@@ -24,6 +24,19 @@ namespace ob {
 static thread_local std::string t_err;
 
 Engine::~Engine() {
+  for (auto& L : lanes) {
+    for (auto& gr : L.graphs)
+      if (gr.exec) cudaGraphExecDestroy(gr.exec);
+    if (L.arena.base) cudaFree(L.arena.base);
+    if (L.scan.pool) cudaFree(L.scan.pool);
+    for (auto& ev_ : L.ev)
+      if (ev_) cudaEventDestroy(ev_);
+    for (cudaEvent_t ev_ : {L.fork_ev, L.join_ev, L.csr_ev, L.done_ev})
+      if (ev_) cudaEventDestroy(ev_);
+    if (L.stream) cudaStreamDestroy(L.stream);
+    if (L.side) cudaStreamDestroy(L.side);
+  }
+  if (lane_fork_ev) cudaEventDestroy(lane_fork_ev);
   drop_graphs();
   cgp_destroy(*this);
   if (arena.base) cudaFree(arena.base);
@@ -37,6 +50,36 @@ Engine::~Engine() {
   if (join_ev) cudaEventDestroy(join_ev);
   if (csr_ev) cudaEventDestroy(csr_ev);
 }
+
+// swap a lane's request state with the engine's current one (lane 0 lives in the engine)
+static void swap_lane(Engine& e, Lane& L) {
+  std::swap(e.ws, L.ws);
+  std::swap(e.arena, L.arena);
+  std::swap(e.scan, L.scan);
+  std::swap(e.params, L.params);
+  std::swap(e.graphs, L.graphs);
+  std::swap(e.stream, L.stream);
+  std::swap(e.side, L.side);
+  std::swap(e.fork_ev, L.fork_ev);
+  std::swap(e.join_ev, L.join_ev);
+  std::swap(e.csr_ev, L.csr_ev);
+  for (int i = 0; i < 6; ++i) std::swap(e.ev[i], L.ev[i]);
+}
+
+// RAII: lane `lane` is the engine's request state for the guard's lifetime
+struct LaneGuard {
+  Engine& e;
+  Lane* L = nullptr;
+  LaneGuard(Engine& e_, int lane) : e(e_) {
+    if (lane > 0) {
+      L = &e.lanes[lane - 1];
+      swap_lane(e, *L);
+    }
+  }
+  ~LaneGuard() {
+    if (L) swap_lane(e, *L);
+  }
+};
 
 // sum of the r largest in-degrees: bound on the CSR edges r destinations can pull
 static int64_t topdeg(const GraphDev& g, int64_t r) {
@@ -988,6 +1031,7 @@ int ob_serve(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* 
     if ((int64_t)B * e.g.F) OB_CUDA(cudaMemcpyAsync(h->d_q, q, sizeof(float) * B * e.g.F, cudaMemcpyHostToDevice, s));
     ob_breakdown local{};
     serve_device(e, B, h->d_q, m, h->d_edges, h->d_out, &local);
+    e.last_lane = 0;
     if ((int64_t)B * H) OB_CUDA(cudaMemcpyAsync(out, h->d_out, sizeof(float) * B * H, cudaMemcpyDeviceToHost, s));
     OB_CUDA(cudaStreamSynchronize(s));
     local.h2d_bytes = 16 * m + 4 * (int64_t)B * e.g.F;
@@ -1034,6 +1078,9 @@ int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const in
     if ((int64_t)B * e.g.F)
       OB_CUDA(cudaMemcpyAsync(sl.d_q, q, sizeof(float) * B * e.g.F, cudaMemcpyHostToDevice, h->h2d));
     OB_CUDA(cudaEventRecord(sl.h2d_done, h->h2d));
+    const int lane = (int)(t & 1) % e.nlanes;  // with two lanes the two slots' requests overlap
+    LaneGuard lg(e, lane);
+    e.last_lane = lane;
     cudaStream_t s = e.stream;
     OB_CUDA(cudaStreamWaitEvent(s, sl.h2d_done, 0));
     OB_CUDA(cudaEventRecord(sl.start, s));
@@ -1074,6 +1121,7 @@ int ob_serve_wait(ob_engine* h, int64_t ticket, ob_breakdown* bd) {
     float ms = 0;
     OB_CUDA(cudaEventElapsedTime(&ms, sl.start, sl.comp_done));
     std::vector<BlockCounters> hc(sl.h_bc, sl.h_bc + sl.n_bc);
+    LaneGuard lg(e, (int)(ticket & 1) % e.nlanes);
     ob_breakdown local{};
     // counters of the request that was last enqueued describe the workspace
     // layout; both slots share one plan once the shape is reserved
@@ -1093,8 +1141,65 @@ int ob_serve_device(ob_engine* h, int32_t B, const float* d_q, int64_t m, const 
   return guarded([&] {
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
-    OB_CUDA(cudaSetDevice(h->impl.cfg.device));
-    serve_device(h->impl, B, d_q, m, d_edges, d_out, bd);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    const int lane = e.nlanes > 1 ? (int)(e.lane_rr++ % e.nlanes) : 0;
+    LaneGuard g(e, lane);
+    serve_device(e, B, d_q, m, d_edges, d_out, bd);
+    e.last_lane = lane;
+  });
+}
+
+int ob_set_lanes(ob_engine* h, int32_t n) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    OB_CHECK(n >= 1 && n <= 4, OB_EINVAL, "lanes must be 1..4");
+    OB_CHECK(n == 1 || e.cfg.strategy != OB_STRATEGY_SRPE_CGP, OB_EINVAL,
+             "CGP engines serve one request at a time (the NVLink exchange is per engine)");
+    OB_CHECK(n == 1 || !e.prof.on, OB_ESTATE, "profiling runs on one lane");
+    OB_CUDA(cudaDeviceSynchronize());
+    if (!e.lane_fork_ev) OB_CUDA(cudaEventCreateWithFlags(&e.lane_fork_ev, cudaEventDisableTiming));
+    while ((int)e.lanes.size() < n - 1) {
+      e.lanes.emplace_back();
+      Lane& L = e.lanes.back();
+      OB_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+      OB_CUDA(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking));
+      for (auto& ev_ : L.ev) OB_CUDA(cudaEventCreate(&ev_));
+      for (cudaEvent_t* ev_ : {&L.fork_ev, &L.join_ev, &L.csr_ev, &L.done_ev})
+        OB_CUDA(cudaEventCreateWithFlags(ev_, cudaEventDisableTiming));
+    }
+    e.nlanes = n;
+    e.lane_rr = 0;
+  });
+}
+
+// order every lane after the work enqueued so far on lane 0's stream
+int ob_lanes_fork(ob_engine* h) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    if (e.nlanes < 2) return;
+    OB_CUDA(cudaEventRecord(e.lane_fork_ev, e.stream));
+    for (int i = 0; i + 1 < e.nlanes; ++i) OB_CUDA(cudaStreamWaitEvent(e.lanes[i].stream, e.lane_fork_ev, 0));
+  });
+}
+
+// order lane 0's stream after everything enqueued on the other lanes
+int ob_lanes_join(ob_engine* h) {
+  return guarded([&] {
+    OB_CHECK(h, OB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lk(h->mu);
+    Engine& e = h->impl;
+    OB_CUDA(cudaSetDevice(e.cfg.device));
+    for (int i = 0; i + 1 < e.nlanes; ++i) {
+      OB_CUDA(cudaEventRecord(e.lanes[i].done_ev, e.lanes[i].stream));
+      OB_CUDA(cudaStreamWaitEvent(e.stream, e.lanes[i].done_ev, 0));
+    }
   });
 }
 
@@ -1106,6 +1211,8 @@ int ob_last_plan(ob_engine* h, int64_t* nc, int64_t* nt, int64_t* ids, int64_t* 
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
     OB_CHECK(e.have_request && !khop(e.cfg), OB_ESTATE, "no srpe request served");
+    LaneGuard lg(e, e.last_lane);
+    OB_CUDA(cudaDeviceSynchronize());
     RequestWs& w = e.ws;
     cudaStream_t s = e.stream;
     ReqCounters rc = d2h(w.rc, 1, s)[0];
@@ -1157,6 +1264,8 @@ int ob_last_block_sizes(ob_engine* h, int32_t part, int32_t layer, int64_t* ns, 
     std::lock_guard<std::mutex> lk(h->mu);
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
+    LaneGuard lg(e, e.last_lane);
+    OB_CUDA(cudaDeviceSynchronize());
     BlockDev& b = block_of(e, part, layer);
     BlockCounters c = d2h(b.cnt, 1, e.stream)[0];
     *ns = c.S;
@@ -1173,6 +1282,8 @@ int ob_last_block(ob_engine* h, int32_t part, int32_t layer, int64_t* src_ids, i
     std::lock_guard<std::mutex> lk(h->mu);
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
+    LaneGuard lg(e, e.last_lane);
+    OB_CUDA(cudaDeviceSynchronize());
     RequestWs& w = e.ws;
     BlockDev& b = block_of(e, part, layer);
     cudaStream_t s = e.stream;

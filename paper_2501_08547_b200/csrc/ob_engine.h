@@ -628,6 +628,24 @@ inline void record_mark(cudaEvent_t ev, cudaStream_t s) {
   else OB_CUDA(cudaEventRecord(ev, s));
 }
 
+// A request lane: everything a request writes (workspace arena, scan state,
+// parameter block, captured graphs, streams, stage events).  The engine's own
+// fields are lane 0; extra lanes are swapped in around a request, so two
+// requests can be in flight on two streams at once (one's graph construction
+// -- latency-bound small kernels -- overlapping the other's gathers).  The
+// loaded graph, weights, stored embeddings and tables are shared read-only.
+struct RequestGraph;
+struct Lane {
+  RequestWs ws;
+  Arena arena;
+  ScanScratch scan;
+  ReqParams* params = nullptr;
+  std::vector<RequestGraph> graphs;
+  cudaStream_t stream = nullptr, side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, csr_ev = nullptr, done_ev = nullptr;
+  cudaEvent_t ev[6] = {};
+};
+
 struct Engine {
   ob_config cfg{};
   CgpState cgp;
@@ -693,6 +711,12 @@ struct Engine {
       }
   }
   bool localized = false;  // NCCL-mode CGP storage reduced to the owned rows
+  // request lanes beyond lane 0 (ob_set_lanes); lane_rr round-robins device serves
+  std::vector<Lane> lanes;
+  int nlanes = 1;
+  int64_t lane_rr = 0;
+  int last_lane = 0;
+  cudaEvent_t lane_fork_ev = nullptr;
   ~Engine();
 };
 

@@ -361,6 +361,10 @@ class ServingEngine:
     def launch_count(self) -> int:
         return int(self._lib.ob_launch_count(self._h))
 
+    def set_lanes(self, n: int) -> None:
+        """Request lanes (1 or 2): two requests in flight on two streams (serve_stream / serve_device)."""
+        nat.check(self._lib.ob_set_lanes(self._h, int(n)))
+
     def set_graphs(self, enable: bool) -> None:
         """Replay captured per-shape CUDA graphs (default) or launch every stage eagerly."""
         nat.check(self._lib.ob_set_graphs(self._h, int(bool(enable))))

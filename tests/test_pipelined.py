@@ -61,3 +61,25 @@ def test_stream_error_is_raised_in_order_and_engine_recovers(setup):
     got = [r[0] for r in eng.serve_stream([reqs[1]])]
     assert np.array_equal(got[0], emb)
     eng.close()
+
+
+@pytest.mark.parametrize("strategy", ["srpe", "full"])
+def test_two_lanes_equal_serve(setup, strategy):
+    """Two request lanes (two workspaces on two streams, requests in flight together) change nothing."""
+    from paper_2501_08547_b200 import runtime
+
+    serving, model, w, pe, reqs = setup
+    eng = runtime.ServingEngine(serving, pe, model, w, runtime.ServeConfig(strategy=strategy, gamma=0.2))
+    ref = [eng.serve(r) for r in reqs]
+    plan_ref = eng.last_plan() if strategy == "srpe" else None
+    eng.set_lanes(2)
+    for _ in range(2):
+        got = list(eng.serve_stream(reqs))
+        for (a, ba), (b, bb) in zip(got, ref):
+            assert np.array_equal(a, b)
+            assert ba.fetch_bytes == bb.fetch_bytes
+    if strategy == "srpe":  # parity hooks read the lane that served the last request
+        assert np.array_equal(eng.last_plan()["targets"], plan_ref["targets"])
+    eng.set_lanes(1)
+    assert np.array_equal(eng.serve(reqs[2])[0], ref[2][0])
+    eng.close()
