@@ -258,7 +258,7 @@ def main():
     ap.add_argument("--gamma", type=float, default=None)
     ap.add_argument("--strategy", default="srpe", choices=["srpe", "full", "sampled"],
                     help="single-GPU / replica strategy (CGP runs srpe-cgp); config 5's ablation axis")
-    ap.add_argument("--lanes", type=int, default=2,
+    ap.add_argument("--lanes", type=int, default=4,
                     help="request lanes for the throughput pass (1 = one request at a time)")
     ap.add_argument("--fanouts", default="15,10,5",
                     help="sampled strategy: comma-separated fanouts, outermost hop first (trimmed to k)")
@@ -477,7 +477,8 @@ def main():
         # pipelined: the same requests through ob_serve_submit / ob_serve_wait (two in flight), so
         # request t+1's inputs cross PCIe and t-1's rows return while t runs; every step still copies
         # its inputs H2D from pinned memory and its rows D2H inside the timed region
-        outs_p = [torch.empty((B, H), dtype=torch.float32).pin_memory() for _ in range(2)]
+        depth = 4 if lanes > 1 else 2  # requests in flight on the pipelined path
+        outs_p = [torch.empty((B, H), dtype=torch.float32).pin_memory() for _ in range(depth)]
 
         def submit(i, slot):
             t = C.c_int64()
@@ -491,21 +492,21 @@ def main():
             nat.check(lib.ob_serve_wait(eng._h, t, C.byref(bdw)))
             return bdw
 
-        for i in above + [0]:  # both slots' (lanes') graphs captured before timing
-            for sl in range(2):
-                wait(submit(i, sl))
+        for i in above + [0]:  # every slot's (lane's) graph captured before timing
+            for sl in range(4):
+                wait(submit(i, sl % depth))
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         t_sub, t_done, pend = {}, {}, []
         p0 = time.perf_counter()
         for j in range(args.steps):
-            if len(pend) == 2:
+            if len(pend) == depth:
                 tk, jj = pend.pop(0)
                 wait(tk)
                 t_done[jj] = time.perf_counter()
             t_sub[j] = time.perf_counter()
-            pend.append((submit(args.warmup + j, j & 1), j))
+            pend.append((submit(args.warmup + j, j % depth), j))
         for tk, jj in pend:
             wait(tk)
             t_done[jj] = time.perf_counter()
@@ -521,8 +522,9 @@ def main():
             et = float(t.item())
         e2e = {"value": round(served * args.steps / (pt / 1e3), 3), "unit": "queries/s",
                "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
-               "mode": "pipelined host API (ob_serve_submit/ob_serve_wait, 2 requests in flight, pinned host "
-                       "buffers); wall clock over the K steps; no L2 flush (each request gathers > 0.5 GB)",
+               "mode": f"pipelined host API (ob_serve_submit/ob_serve_wait, {depth} requests in flight over "
+                       f"{lanes} request lane(s), pinned host buffers); wall clock over the K steps; no L2 flush "
+                       "(each request gathers > 0.5 GB)",
                "p50_ms": float(np.percentile(plat, 50)), "p99_ms": float(np.percentile(plat, 99)),
                "sync": {"value": round(served * args.steps / (et / 1e3), 3), "unit": "queries/s",
                         "mode": "one ob_serve call per step (H2D, request, D2H, synchronise), CUDA events, "

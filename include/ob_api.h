@@ -169,10 +169,11 @@ int ob_serve_device(ob_engine* e, int32_t num_queries, const float* d_query_feat
                     int64_t num_edges, const int64_t* d_edges, float* d_out, ob_breakdown* bd);
 
 /* Pipelined host path (production serving loop): submit copies the request's
- * host inputs to one of two device staging slots on a copy stream and enqueues
+ * host inputs to one of four device staging slots on a copy stream and enqueues
  * the request; the rows come back on a second copy stream.  While request t
- * runs, request t+1's inputs cross PCIe and request t-1's rows return.  At most
- * two requests are outstanding (OB_ESTATE otherwise); ob_serve_wait(ticket)
+ * runs, request t+1's inputs cross PCIe and request t-1's rows return (with
+ * request lanes, slot s runs on lane s % lanes).  At most four requests are
+ * outstanding (OB_ESTATE otherwise); ob_serve_wait(ticket)
  * blocks until request `ticket`'s rows are in its `out` and reports its errors
  * and breakdown (compute_ms = device time of the request).  Host buffers must
  * stay valid until the wait; pinned buffers give full overlap. */
@@ -180,9 +181,9 @@ int ob_serve_submit(ob_engine* e, int32_t num_queries, const float* query_featur
                     const int64_t* edges, float* out, int64_t* ticket);
 int ob_serve_wait(ob_engine* e, int64_t ticket, ob_breakdown* bd);
 
-/* Request lanes: with n = 2, consecutive ob_serve_device calls (and the two
- * slots of ob_serve_submit) alternate between two independent request
- * workspaces on two streams, so one request's graph construction (many small
+/* Request lanes: with n > 1, consecutive ob_serve_device calls (and the
+ * slots of ob_serve_submit) rotate over n independent request workspaces on n
+ * streams, so one request's graph construction (many small
  * latency-bound kernels) overlaps the other's aggregation gathers.  Lane 0 uses
  * the engine stream; ob_lanes_fork orders the other lanes after lane 0's
  * enqueued work and ob_lanes_join orders lane 0 after theirs (bracket a batch

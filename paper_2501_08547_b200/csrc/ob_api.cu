@@ -711,6 +711,7 @@ struct PipeSlot {
   int64_t collective_bytes = 0;
 };
 constexpr int kMaxCounted = 64;
+constexpr int kPipeSlots = 4;  // requests in flight on the pipelined host path
 
 struct ob_engine {
   Engine impl;
@@ -722,7 +723,7 @@ struct ob_engine {
   size_t cap_edges = 0, cap_q = 0, cap_out = 0;
   // pipelined host path (ob_serve_submit / ob_serve_wait): two slots, so request
   // t+1's inputs cross PCIe while request t runs and t-1's rows come back
-  PipeSlot slot[2];
+  PipeSlot slot[kPipeSlots];
   cudaStream_t h2d = nullptr, d2h = nullptr;
   int64_t next_ticket = 0;
 };
@@ -1058,8 +1059,8 @@ int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const in
     OB_CHECK(m == 0 || edges, OB_EINVAL, "null edges");
     OB_CHECK(out, OB_EINVAL, "null output");
     const int64_t t = h->next_ticket;
-    PipeSlot& sl = h->slot[t & 1];
-    OB_CHECK(!sl.busy, OB_ESTATE, "two requests already outstanding: wait for the oldest first");
+    PipeSlot& sl = h->slot[t % kPipeSlots];
+    OB_CHECK(!sl.busy, OB_ESTATE, "four requests already outstanding: wait for the oldest first");
     if (!h->h2d) {
       OB_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
       OB_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
@@ -1078,7 +1079,7 @@ int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const in
     if ((int64_t)B * e.g.F)
       OB_CUDA(cudaMemcpyAsync(sl.d_q, q, sizeof(float) * B * e.g.F, cudaMemcpyHostToDevice, h->h2d));
     OB_CUDA(cudaEventRecord(sl.h2d_done, h->h2d));
-    const int lane = (int)(t & 1) % e.nlanes;  // with two lanes the two slots' requests overlap
+    const int lane = (int)(t % kPipeSlots) % e.nlanes;  // with several lanes the slots' requests overlap
     LaneGuard lg(e, lane);
     e.last_lane = lane;
     cudaStream_t s = e.stream;
@@ -1112,7 +1113,7 @@ int ob_serve_wait(ob_engine* h, int64_t ticket, ob_breakdown* bd) {
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
     OB_CHECK(ticket >= 0, OB_EINVAL, "bad ticket");
-    PipeSlot& sl = h->slot[ticket & 1];
+    PipeSlot& sl = h->slot[ticket % kPipeSlots];
     OB_CHECK(sl.busy && sl.ticket == ticket, OB_ESTATE, "ticket is not outstanding");
     // the next slot's request keeps running; only this one's D2H is awaited
     OB_CUDA(cudaEventSynchronize(sl.d2h_done));
@@ -1121,7 +1122,7 @@ int ob_serve_wait(ob_engine* h, int64_t ticket, ob_breakdown* bd) {
     float ms = 0;
     OB_CUDA(cudaEventElapsedTime(&ms, sl.start, sl.comp_done));
     std::vector<BlockCounters> hc(sl.h_bc, sl.h_bc + sl.n_bc);
-    LaneGuard lg(e, (int)(ticket & 1) % e.nlanes);
+    LaneGuard lg(e, (int)(ticket % kPipeSlots) % e.nlanes);
     ob_breakdown local{};
     // counters of the request that was last enqueued describe the workspace
     // layout; both slots share one plan once the shape is reserved
@@ -1156,7 +1157,7 @@ int ob_set_lanes(ob_engine* h, int32_t n) {
     std::lock_guard<std::mutex> lk(h->mu);
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
-    OB_CHECK(n >= 1 && n <= 4, OB_EINVAL, "lanes must be 1..4");
+    OB_CHECK(n >= 1 && n <= 8, OB_EINVAL, "lanes must be 1..8");
     OB_CHECK(n == 1 || e.cfg.strategy != OB_STRATEGY_SRPE_CGP, OB_EINVAL,
              "CGP engines serve one request at a time (the NVLink exchange is per engine)");
     OB_CHECK(n == 1 || !e.prof.on, OB_ESTATE, "profiling runs on one lane");

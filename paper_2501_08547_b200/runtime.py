@@ -227,12 +227,12 @@ class ServingEngine:
                                      C.byref(bd)))
         return out, self._breakdown(bd)
 
-    def serve_stream(self, requests):
+    def serve_stream(self, requests, depth: int = 2):
         """Pipelined serving over an iterable of requests: yields (emb, LatencyBreakdown) in order.
 
         Request t+1's inputs cross PCIe and request t-1's rows come back while
-        request t runs on the device (ob_serve_submit / ob_serve_wait, two
-        staging slots).  Each result equals ``serve(request)``'s; ``compute_ms``
+        request t runs on the device (ob_serve_submit / ob_serve_wait; up to
+        ``depth`` <= 4 requests in flight, spread over the request lanes).  Each result equals ``serve(request)``'s; ``compute_ms``
         is the request's device time.
         """
         pending = []  # (ticket, out, keep-alive arrays)
@@ -240,7 +240,7 @@ class ServingEngine:
         done = False
         try:
             while True:
-                while not done and len(pending) < 2:
+                while not done and len(pending) < max(1, min(int(depth), 4)):
                     try:
                         req = next(it)
                     except StopIteration:
@@ -362,7 +362,7 @@ class ServingEngine:
         return int(self._lib.ob_launch_count(self._h))
 
     def set_lanes(self, n: int) -> None:
-        """Request lanes (1 or 2): two requests in flight on two streams (serve_stream / serve_device)."""
+        """Request lanes (1..8): requests in flight on separate workspaces and streams (serve_stream / serve_device)."""
         nat.check(self._lib.ob_set_lanes(self._h, int(n)))
 
     def set_graphs(self, enable: bool) -> None:

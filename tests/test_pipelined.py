@@ -72,9 +72,9 @@ def test_two_lanes_equal_serve(setup, strategy):
     eng = runtime.ServingEngine(serving, pe, model, w, runtime.ServeConfig(strategy=strategy, gamma=0.2))
     ref = [eng.serve(r) for r in reqs]
     plan_ref = eng.last_plan() if strategy == "srpe" else None
-    eng.set_lanes(2)
-    for _ in range(2):
-        got = list(eng.serve_stream(reqs))
+    for lanes, depth in ((2, 2), (3, 4), (4, 4)):
+        eng.set_lanes(lanes)
+        got = list(eng.serve_stream(reqs, depth=depth))
         for (a, ba), (b, bb) in zip(got, ref):
             assert np.array_equal(a, b)
             assert ba.fetch_bytes == bb.fetch_bytes
