@@ -258,6 +258,8 @@ def main():
     ap.add_argument("--gamma", type=float, default=None)
     ap.add_argument("--strategy", default="srpe", choices=["srpe", "full", "sampled"],
                     help="single-GPU / replica strategy (CGP runs srpe-cgp); config 5's ablation axis")
+    ap.add_argument("--policy", default="ratio", choices=["ratio", "is"],
+                    help="SRPE scoring policy (policy.py:29-32)")
     ap.add_argument("--lanes", type=int, default=4,
                     help="request lanes for the throughput pass (1 = one request at a time)")
     ap.add_argument("--fanouts", default="15,10,5",
@@ -327,10 +329,12 @@ def main():
     stream = torch.cuda.Stream(device=local)
     t0 = time.time()
     if cgp:
-        scfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=gamma, num_partitions=P, seed=0, device=local)
+        scfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=gamma, num_partitions=P, seed=0, device=local,
+                                   policy=args.policy)
         eng = runtime.distributed_engine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream, group=pg)
     else:
-        scfg = runtime.ServeConfig(strategy=strategy, gamma=gamma, device=local, fanouts=fanouts)
+        scfg = runtime.ServeConfig(strategy=strategy, gamma=gamma, device=local, fanouts=fanouts,
+                                   policy=args.policy)
         eng = runtime.ServingEngine(serving, pe_src, model, w, scfg, stream=stream.cuda_stream)
     if not synthetic and (cgp or strategy == "srpe"):
         eng.precompute_pe()
@@ -562,7 +566,7 @@ def main():
         "higher_is_better": True, "scaling": "strong" if (cgp and groups == 1) else "weak", "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": desc, "batch": B, "policy": "ratio", "gamma": gamma,
+        "config": {"workload": desc, "batch": B, "policy": args.policy, "gamma": gamma,
                    "strategy": "srpe-cgp" if cgp else strategy,
                    **({"fanouts": list(fanouts)} if fanouts else {}),
                    "parallelism": (f"cgp x{P} (NVLink exchange) x {groups} group(s)" if cgp else
