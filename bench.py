@@ -413,7 +413,7 @@ def main():
     served = groups * B  # CGP: the P ranks of a group serve one batch together
     value_single = served * args.steps / (total_ms / 1e3)
     value, lanes_ms, launches_lanes, clk_lanes = value_single, None, None, None
-    lanes = 1 if (cgp or args.lanes < 2) else args.lanes
+    lanes = 1 if args.lanes < 2 else args.lanes
     if lanes > 1:
         # throughput with two request lanes: consecutive requests alternate between two request
         # workspaces on two streams, so one's graph construction overlaps the other's gathers.

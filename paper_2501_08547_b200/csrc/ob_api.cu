@@ -64,6 +64,7 @@ static void swap_lane(Engine& e, Lane& L) {
   std::swap(e.join_ev, L.join_ev);
   std::swap(e.csr_ev, L.csr_ev);
   for (int i = 0; i < 6; ++i) std::swap(e.ev[i], L.ev[i]);
+  std::swap(static_cast<CgpLaneState&>(e.cgp), L.cg);
 }
 
 // RAII: lane `lane` is the engine's request state for the guard's lifetime
@@ -817,6 +818,10 @@ int ob_engine_destroy(ob_engine* h) {
   return guarded([&] {
     if (!h) return;
     cudaSetDevice(h->impl.cfg.device);
+    for (int i = 1; i <= (int)h->impl.lanes.size(); ++i) {  // every lane's NVLink exchange, with the peers
+      LaneGuard lg(h->impl, i);
+      cgp_release_exchange(h->impl);
+    }
     if (h->h2d) cudaStreamSynchronize(h->h2d);
     if (h->d2h) cudaStreamSynchronize(h->d2h);
     cudaStreamSynchronize(h->impl.stream);
@@ -1158,8 +1163,8 @@ int ob_set_lanes(ob_engine* h, int32_t n) {
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
     OB_CHECK(n >= 1 && n <= 8, OB_EINVAL, "lanes must be 1..8");
-    OB_CHECK(n == 1 || e.cfg.strategy != OB_STRATEGY_SRPE_CGP, OB_EINVAL,
-             "CGP engines serve one request at a time (the NVLink exchange is per engine)");
+    OB_CHECK(n == 1 || e.cfg.strategy != OB_STRATEGY_SRPE_CGP || !e.cgp.nccl || e.cgp.p2p, OB_EINVAL,
+             "CGP lanes need the NVLink exchange (each lane has its own; OB_CGP_NCCL=1 serialises on one comm)");
     OB_CHECK(n == 1 || !e.prof.on, OB_ESTATE, "profiling runs on one lane");
     OB_CUDA(cudaDeviceSynchronize());
     if (!e.lane_fork_ev) OB_CUDA(cudaEventCreateWithFlags(&e.lane_fork_ev, cudaEventDisableTiming));

@@ -726,6 +726,23 @@ static void close_exchange(Engine& e) {
   c.xsteps = 0;
 }
 
+void cgp_release_exchange(Engine& e) {
+#ifdef OB_WITH_NCCL
+  if (e.cgp.comm && e.cgp.xbuf) {
+    try {
+      cudaStreamSynchronize(e.stream);
+      comm_barrier(e);  // no peer still reads this lane's buffer
+      close_exchange(e);
+      comm_barrier(e);
+    } catch (...) {
+      close_exchange(e);
+    }
+  }
+#else
+  (void)e;
+#endif
+}
+
 void cgp_ensure_exchange(Engine& e) {
 #ifdef OB_WITH_NCCL
   CgpState& c = e.cgp;
@@ -795,16 +812,7 @@ void cgp_init_comm(Engine& e) {
 
 void cgp_destroy(Engine& e) {
 #ifdef OB_WITH_NCCL
-  if (e.cgp.comm && e.cgp.xbuf) {
-    try {
-      cudaStreamSynchronize(e.stream);
-      comm_barrier(e);  // no peer still reads this rank's buffer
-      close_exchange(e);
-      comm_barrier(e);
-    } catch (...) {
-      close_exchange(e);
-    }
-  }
+  cgp_release_exchange(e);
   if (e.cgp.comm) ncclCommDestroy((ncclComm_t)e.cgp.comm);
 #endif
   e.cgp.comm = nullptr;

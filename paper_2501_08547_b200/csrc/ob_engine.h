@@ -546,13 +546,10 @@ struct CgpPartWs {
   BlockDev blocks[2];         // mid (layers 1..k-1), last (layer k); no self rows
 };
 
-struct CgpState {
-  int P = 1;
-  int my_rank = 0;
-  bool nccl = false;
-  void* comm = nullptr;       // ncclComm_t
-  int32_t* owner = nullptr;   // [N]
-  std::vector<PartitionDev> parts;  // emulation: all P; NCCL: this rank's
+// CGP state of one request lane: the request's workspace pieces and the lane's
+// own NVLink exchange (buffer, peer mappings, device step counter), so lanes on
+// different streams never share exchange regions or flags
+struct CgpLaneState {
   std::vector<CgpPartWs> ws;
   // per request
   const float** hvp = nullptr;  // [D_max] destination rows h_v (owned; zero row otherwise)
@@ -568,7 +565,6 @@ struct CgpState {
   // NVLink exchange (NCCL mode): every rank's exchange buffer is mapped into
   // every peer (CUDA IPC); partials move with P2P loads, step flags with
   // system-scope stores -- only real rows, no padding, owner-only merges
-  bool p2p = false;             // use the exchange (else padded ncclAllReduce)
   char* xbuf = nullptr;         // [flags 256 B][steps x region]
   size_t xregion = 0;           // bytes per step region
   int xsteps = 0;               // regions
@@ -578,6 +574,19 @@ struct CgpState {
   int64_t* xerr = nullptr;      // device error word (flag wait timeouts)
   int64_t nvlink_bytes = 0;     // per request, real-row bytes read from peers (host estimate)
 };
+
+struct CgpState : CgpLaneState {
+  int P = 1;
+  int my_rank = 0;
+  bool nccl = false;
+  void* comm = nullptr;       // ncclComm_t
+  int32_t* owner = nullptr;   // [N]
+  std::vector<PartitionDev> parts;  // emulation: all P; NCCL: this rank's
+  bool p2p = false;             // use the exchange (else padded ncclAllReduce)
+};
+
+// release the current lane's exchange buffers (barrier with every peer first)
+void cgp_release_exchange(Engine& e);
 
 // (re)build the NVLink exchange when the plan needs bigger regions (all ranks
 // call it at the same request: plans are identical); outside any capture
@@ -644,6 +653,7 @@ struct Lane {
   cudaStream_t stream = nullptr, side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, csr_ev = nullptr, done_ev = nullptr;
   cudaEvent_t ev[6] = {};
+  CgpLaneState cg;
 };
 
 struct Engine {

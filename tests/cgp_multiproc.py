@@ -102,8 +102,10 @@ def main():
         info = eng.graph_info()
         rows = torch.tensor([info["local_rows"], info["local_edges"]], dtype=torch.int64)
         dist.all_reduce(rows)
+        reqs_l = []
         for seed in (1, 2):
             req = workload.make_request_synthetic(gds.num_nodes, gds.avg_degree, gds.exponent, 32, 256, seed)
+            reqs_l.append(req)
             emb, bd = eng.serve(req)
             emb_emu, _ = emu.serve(req)
             if rank == 0:
@@ -113,6 +115,15 @@ def main():
                                                      and int(rows[0]) == gds.num_nodes
                                                      and int(rows[1]) == info["num_edges"]),
                                     coll_bytes=int(bd.collective_bytes)))
+        if kind == "sage_mean":  # request lanes: each lane has its own NVLink exchange
+            one = [eng.serve(r)[0] for r in reqs_l * 2]
+            eng.set_lanes(2)
+            two = [x[0] for x in eng.serve_stream(reqs_l * 2, depth=4)]
+            eng.set_lanes(1)
+            if rank == 0:
+                results.append(dict(case="lanes", kind=kind, k=3, err_ref=0.0 if all(
+                    np.array_equal(a, b) for a, b in zip(one, two)) else 1.0, err_emu=0.0, shard=True,
+                    coll_bytes=0))
         eng.close()
         emu.close()
     if rank == 0:
