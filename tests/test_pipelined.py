@@ -83,3 +83,17 @@ def test_two_lanes_equal_serve(setup, strategy):
     eng.set_lanes(1)
     assert np.array_equal(eng.serve(reqs[2])[0], ref[2][0])
     eng.close()
+
+
+def test_lanes_under_cgp_emulation(setup):
+    """All P partitions on one device (no NCCL): lanes swap the CGP request state too."""
+    from paper_2501_08547_b200 import runtime
+
+    serving, model, w, pe, reqs = setup
+    eng = runtime.ServingEngine(serving, pe, model, w,
+                                runtime.ServeConfig(strategy="srpe-cgp", gamma=0.2, num_partitions=3, seed=5))
+    ref = [eng.serve(r)[0] for r in reqs]
+    eng.set_lanes(3)
+    got = [x[0] for x in eng.serve_stream(reqs, depth=4)]
+    assert all(np.array_equal(a, b) for a, b in zip(got, ref))
+    eng.close()
