@@ -449,6 +449,24 @@ static RequestGraph& request_graph(Engine& e, float* d_out) {
   return e.graphs.back();
 }
 
+// IS numerator tables (once per graph; outside any capture)
+void ensure_is_tables(Engine& e) {
+  if (e.cfg.policy != OB_POLICY_IS || !e.is_tab.empty()) return;
+  const int64_t N = e.g.N;
+  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) {
+    for (auto& part : e.cgp.parts) {
+      double* t = (double*)e.dalloc(sizeof(double) * N);
+      build_is_table(e, part.off, part.src, t);
+      e.is_tab.push_back(t);
+    }
+  } else {
+    OB_CHECK(e.g.offsets, OB_ESTATE, "the IS policy needs the graph's CSR");
+    double* t = (double*)e.dalloc(sizeof(double) * N);
+    build_is_table(e, e.g.offsets, e.g.nbrs, t);
+    e.is_tab.push_back(t);
+  }
+}
+
 // blocks whose counters a breakdown reads: centralized blocks, or every partition's (mid, last)
 static std::vector<BlockDev*> counted_blocks(Engine& e) {
   std::vector<BlockDev*> all;
@@ -467,6 +485,7 @@ static void enqueue_serve(Engine& e, int B, const float* d_q, int64_t m, const i
   OB_CHECK(e.g.N + B < ((int64_t)1 << 31) - 1, OB_EINVAL, "id space exceeds int32");
   cgp_localize_storage(e);  // NCCL CGP: keep only the owned rows (no-op otherwise)
   build_stored_transforms(e);  // once per (model, PE) state, outside any capture
+  ensure_is_tables(e);
   cudaStream_t s = e.stream;
   prepare_workspace(e, B, std::max(bucket_m(m), e.m_reserved));
   RequestWs& w = e.ws;

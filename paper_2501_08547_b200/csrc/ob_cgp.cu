@@ -503,7 +503,7 @@ void serve_cgp(Engine& e, float* d_out) {
     ip.P = c.P;
     if (p2p) {
       x_begin();
-      launch_is_partial(e, w, c.parts[0].off, c.parts[0].src, reinterpret_cast<double*>(xregion_ptr(c, xj)));
+      launch_is_gather(e, w, e.is_tab[0], reinterpret_cast<double*>(xregion_ptr(c, xj)));
       x_exchange();
       for (int q = 0; q < c.P; ++q)
         ip.part[q] = reinterpret_cast<const double*>(c.xpeer[q] + kXFlags + xoff(c, xj));
@@ -512,7 +512,7 @@ void serve_cgp(Engine& e, float* d_out) {
       c.nvlink_bytes += r_max * 8 * (c.P - 1);
     } else {
       for (int p = 0; p < np; ++p)
-        launch_is_partial(e, w, c.parts[p].off, c.parts[p].src, w.is_part + (int64_t)c.parts[p].rank * r_max);
+        launch_is_gather(e, w, e.is_tab[p], w.is_part + (int64_t)c.parts[p].rank * r_max);
 #ifdef OB_WITH_NCCL
       if (c.nccl) {
         OB_NCCL(ncclAllGather(w.is_part + (int64_t)c.my_rank * r_max, w.is_part, (size_t)r_max, ncclDouble,

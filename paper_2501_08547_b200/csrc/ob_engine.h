@@ -503,7 +503,9 @@ void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, 
 
 void stage_request_prep(Engine& e, RequestWs& w, bool need_scores);
 void stage_select(Engine& e, RequestWs& w);
-void launch_is_partial(Engine& e, RequestWs& w, const int64_t* off, const int32_t* src, double* out);
+void launch_is_gather(Engine& e, RequestWs& w, const double* tab, double* out);
+void build_is_table(Engine& e, const int64_t* off, const int32_t* src, double* out);
+void ensure_is_tables(Engine& e);
 void launch_score_is(Engine& e, RequestWs& w, const IsParts& parts);
 void stage_request_csr(Engine& e, RequestWs& w);
 void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound, const int64_t* m_dev, RqCsr& c,
@@ -678,12 +680,17 @@ struct Engine {
   // training node's CSR in-neighbours is static (only request edges, whose
   // sources are queries, change it): sagg1[v] = sum_u w_u x_u (W), raw, unnormalised
   float* sagg1 = nullptr;
+  // IS policy: per-node numerators of the whole CSR (centralized) or of each
+  // local partition's source-split CSR (CGP), computed once per graph
+  std::vector<double*> is_tab;
   bool ytab_ready = false;
   void drop_ytab() {
     for (float* t : ytab) dfree(t);
     ytab.clear();
     dfree(sagg1);
     sagg1 = nullptr;
+    for (double* t : is_tab) dfree(t);
+    is_tab.clear();
     ytab_ready = false;
   }
   Arena arena;

@@ -422,23 +422,149 @@ __device__ double pw_row(const int32_t* __restrict__ a, int64_t n, const int32_t
   }
 }
 
-// one partition's numerators (the whole CSR when centralized), warp per candidate
-__global__ void __launch_bounds__(32 * kIsWarps) k_is_partial(const int32_t* __restrict__ cand_ids,
-                                                              const ReqCounters* rc, const int64_t* __restrict__ off,
-                                                              const int32_t* __restrict__ src,
-                                                              const int32_t* __restrict__ indeg, double* out) {
+// IS numerators depend only on the training graph (and a partition's source
+// split), so they are computed once per graph for every node and gathered per
+// request.  Rows up to kPwChunk terms: a warp each; longer rows are queued for
+// k_is_big, where a CTA's warps sum the top-level chunks and one thread adds
+// them back up the split tree.
+__global__ void __launch_bounds__(32 * kIsWarps) k_is_rows(int64_t N, const int64_t* __restrict__ off,
+                                                           const int32_t* __restrict__ src,
+                                                           const int32_t* __restrict__ indeg, double* out,
+                                                           int32_t* big, int32_t* nbig) {
   __shared__ int starts[kIsWarps][kPwLeafCap];
   __shared__ double sums[kIsWarps][kPwLeafCap];
   const int wid = threadIdx.x >> 5;
-  const int64_t R = rc->R;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t c = gw; c < R; c += nw) {
-    const int32_t v = cand_ids[c];
+  for (int64_t v = gw; v < N; v += nw) {
     const int64_t b = off[v], n = off[v + 1] - b;
-    const double r = pw_row(src + b, n, indeg, starts[wid], sums[wid]);
-    if ((threadIdx.x & 31) == 0) out[c] = r;
+    if (n > kPwChunk) {
+      if ((threadIdx.x & 31) == 0) big[atomicAdd(nbig, 1)] = (int32_t)v;
+      continue;
+    }
+    const double r = pw_chunk(src + b, (int)n, indeg, starts[wid], sums[wid]);
+    if ((threadIdx.x & 31) == 0) out[v] = r;
   }
+}
+
+constexpr int kIsBigChunks = 1024;  // rows up to 1024 top-level chunks (~16.7M terms)
+
+__global__ void __launch_bounds__(32 * kIsWarps) k_is_big(const int32_t* __restrict__ big, const int32_t* nbig,
+                                                          const int64_t* __restrict__ off,
+                                                          const int32_t* __restrict__ src,
+                                                          const int32_t* __restrict__ indeg, double* out) {
+  __shared__ int starts[kIsWarps][kPwLeafCap];
+  __shared__ double sums[kIsWarps][kPwLeafCap];
+  __shared__ int64_t c_off[kIsBigChunks];
+  __shared__ int c_len[kIsBigChunks];
+  __shared__ double c_val[kIsBigChunks];
+  __shared__ int nchunks;
+  const int wid = threadIdx.x >> 5;
+  for (int bi = blockIdx.x; bi < *nbig; bi += gridDim.x) {
+    const int32_t v = big[bi];
+    const int64_t b = off[v], n = off[v + 1] - b;
+    if (threadIdx.x == 0) {  // top-level chunks of the split tree, left to right
+      int64_t st_off[kPwDepth], st_n[kPwDepth];
+      int sp = 0, L = 0;
+      st_off[sp] = 0;
+      st_n[sp++] = n;
+      while (sp) {
+        --sp;
+        const int64_t o = st_off[sp], m = st_n[sp];
+        if (m <= kPwChunk) {
+          if (L < kIsBigChunks) {
+            c_off[L] = o;
+            c_len[L] = (int)m;
+          }
+          ++L;
+          continue;
+        }
+        int64_t m2 = m / 2;
+        m2 -= m2 % 8;
+        st_off[sp] = o + m2;
+        st_n[sp++] = m - m2;
+        st_off[sp] = o;
+        st_n[sp++] = m2;
+      }
+      nchunks = L;
+    }
+    __syncthreads();
+    const int L = min(nchunks, kIsBigChunks);
+    for (int c = wid; c < L; c += kIsWarps) {
+      const double r = pw_chunk(src + b + c_off[c], c_len[c], indeg, starts[wid], sums[wid]);
+      if ((threadIdx.x & 31) == 0) c_val[c] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // add the chunk sums back up the same tree (post-order)
+      int64_t st_n[kPwDepth];
+      int st_s[kPwDepth], sp = 0, li = 0;
+      double st_v[kPwDepth];
+      st_n[sp] = n;
+      st_s[sp++] = 0;
+      double val = 0.0;
+      bool have = false;
+      while (true) {
+        if (!have) {
+          const int64_t m = st_n[sp - 1];
+          if (m <= kPwChunk) {
+            val = c_val[li++];
+            --sp;
+            have = true;
+          } else {
+            int64_t m2 = m / 2;
+            m2 -= m2 % 8;
+            st_n[sp] = m2;
+            st_s[sp++] = 0;
+          }
+          continue;
+        }
+        if (sp == 0) break;
+        if (st_s[sp - 1] == 0) {
+          st_v[sp - 1] = val;
+          st_s[sp - 1] = 1;
+          const int64_t m = st_n[sp - 1];
+          int64_t m2 = m / 2;
+          m2 -= m2 % 8;
+          st_n[sp] = m - m2;
+          st_s[sp++] = 0;
+          have = false;
+        } else {
+          val = st_v[sp - 1] + val;
+          --sp;
+        }
+      }
+      out[v] = nchunks <= kIsBigChunks ? val : __longlong_as_double(0x7FF8000000000000ll);  // NaN: too long
+    }
+    __syncthreads();
+  }
+}
+
+// numerator table of one CSR (the whole graph, or a partition's source split) over all N nodes
+void build_is_table(Engine& e, const int64_t* off, const int32_t* src, double* out) {
+  cudaStream_t s = e.stream;
+  const int64_t N = e.g.N;
+  int32_t* big = (int32_t*)e.dalloc(sizeof(int32_t) * (N + 1));
+  int32_t* nbig = (int32_t*)e.dalloc(sizeof(int32_t));
+  OB_CUDA(cudaMemsetAsync(nbig, 0, sizeof(int32_t), s));
+  k_is_rows<<<grid_for(N, kIsWarps, kNumSMs * 8), 32 * kIsWarps, 0, s>>>(N, off, src, e.g.indeg, out, big, nbig);
+  OB_LAUNCHED();
+  k_is_big<<<kNumSMs, 32 * kIsWarps, 0, s>>>(big, nbig, off, src, e.g.indeg, out);
+  OB_LAUNCHED();
+  OB_CUDA(cudaStreamSynchronize(s));
+  e.dfree(big);
+  e.dfree(nbig);
+}
+
+__global__ void k_is_gather(const int32_t* __restrict__ cand_ids, const ReqCounters* rc,
+                            const double* __restrict__ tab, double* out) {
+  const int64_t R = rc->R;
+  OB_GRID_STRIDE(c, R) out[c] = tab[cand_ids[c]];
+}
+
+void launch_is_gather(Engine& e, RequestWs& w, const double* tab, double* out) {
+  const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
+  k_is_gather<<<grid_for(r_max, 256), 256, 0, e.stream>>>(w.cand_ids, w.rc, tab, out);
+  OB_LAUNCHED();
 }
 
 // scores from P partial arrays, summed in rank order (P = 1: the centralized row sum)
@@ -453,13 +579,6 @@ __global__ void k_score_is(const int32_t* __restrict__ cand_ids, const int32_t* 
     score[c] = s;
     key[c] = (uint64_t)__double_as_longlong(s);
   }
-}
-
-void launch_is_partial(Engine& e, RequestWs& w, const int64_t* off, const int32_t* src, double* out) {
-  const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
-  k_is_partial<<<grid_for(r_max, kIsWarps, kNumSMs * 8), 32 * kIsWarps, 0, e.stream>>>(w.cand_ids, w.rc, off, src,
-                                                                                       e.g.indeg, out);
-  OB_LAUNCHED();
 }
 
 void launch_score_is(Engine& e, RequestWs& w, const IsParts& parts) {
@@ -803,7 +922,7 @@ void stage_select(Engine& e, RequestWs& w) {
   const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
   if (e.cfg.policy == OB_POLICY_IS && e.cfg.strategy != OB_STRATEGY_SRPE_CGP && r_max > 0) {
     // centralized importance scores over the whole training CSR (policy.py:84-95)
-    launch_is_partial(e, w, e.g.offsets, e.g.nbrs, w.is_part);
+    launch_is_gather(e, w, e.is_tab[0], w.is_part);
     IsParts ip{};
     ip.P = 1;
     ip.part[0] = w.is_part;
