@@ -395,6 +395,7 @@ static void enqueue_stages(Engine& e, float* d_out) {
     }
     e.stream = s;
   }
+  stage_request_post(e, w, srpe);
   if (srpe) stage_select(e, w);
   prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
   OB_CUDA(cudaStreamWaitEvent(s, e.csr_ev, 0));

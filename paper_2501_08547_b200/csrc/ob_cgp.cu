@@ -495,6 +495,7 @@ void serve_cgp(Engine& e, float* d_out) {
   // identical plan on every rank from the whole request (runtime.py:151-192)
   cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, true);
+  stage_request_post(e, w, true);
   const int64_t r_max = std::min<int64_t>(N, 2 * w.m);
   if (e.cfg.policy == OB_POLICY_IS && r_max > 0) {
     // importance numerators per partition over its source-split CSR

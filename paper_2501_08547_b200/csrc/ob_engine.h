@@ -502,6 +502,7 @@ void stage_qpad(Engine& e, RequestWs& w);
 void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, int64_t words, int32_t* out);
 
 void stage_request_prep(Engine& e, RequestWs& w, bool need_scores);
+void stage_request_post(Engine& e, RequestWs& w, bool need_scores);
 void stage_select(Engine& e, RequestWs& w);
 void launch_is_gather(Engine& e, RequestWs& w, const double* tab, double* out);
 void build_is_table(Engine& e, const int64_t* off, const int32_t* src, double* out);

@@ -889,10 +889,6 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
     k_request_mark<<<grid_for(m, kEdgeTile, kNumSMs * 4), 256, sq, s>>>(w.rp, N, w.B, w.cbits, w.qdeg, w.rc);
     OB_LAUNCHED();
   }
-  if ((int64_t)w.B * e.g.F > 0) {
-    k_check_finite<<<grid_for((int64_t)w.B * e.g.F, 256), 256, 0, s>>>(w.rp, (int64_t)w.B * e.g.F, w.rc);
-    OB_LAUNCHED();
-  }
   // candidate set: popcount prefix, ascending ids
   device_scan(s, e.scan, LoadPopc{w.cbits}, StoreI64{w.cwpre}, nullptr, w.words_N, w.words_N, &w.rc->R, w.cwpre);
   k_bitmap_compact<<<grid_for(w.words_N, 256), 256, 0, s>>>(w.cbits, w.cwpre, w.words_N, w.cand_ids);
@@ -907,6 +903,19 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
     else
       k_rq_count<uint32_t><<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt,
                                                             reinterpret_cast<uint32_t*>(w.rq_keys), f);
+    OB_LAUNCHED();
+  }
+  (void)need_scores;
+}
+
+// the request's checks and scores: off the request-index sort's critical path
+// (launched on the main stream after the fork; only the selection needs them)
+void stage_request_post(Engine& e, RequestWs& w, bool need_scores) {
+  cudaStream_t s = e.stream;
+  const int64_t N = e.g.N;
+  const int64_t m = w.m;
+  if ((int64_t)w.B * e.g.F > 0) {
+    k_check_finite<<<grid_for((int64_t)w.B * e.g.F, 256), 256, 0, s>>>(w.rp, (int64_t)w.B * e.g.F, w.rc);
     OB_LAUNCHED();
   }
   if (need_scores) {
