@@ -1186,6 +1186,7 @@ int ob_set_lanes(ob_engine* h, int32_t n) {
     OB_CHECK(n == 1 || e.cfg.strategy != OB_STRATEGY_SRPE_CGP || !e.cgp.nccl || e.cgp.p2p, OB_EINVAL,
              "CGP lanes need the NVLink exchange (each lane has its own; OB_CGP_NCCL=1 serialises on one comm)");
     OB_CHECK(n == 1 || !e.prof.on, OB_ESTATE, "profiling runs on one lane");
+    for (auto& sl : h->slot) OB_CHECK(!sl.busy, OB_ESTATE, "wait for the outstanding pipelined requests first");
     OB_CUDA(cudaDeviceSynchronize());
     if (!e.lane_fork_ev) OB_CUDA(cudaEventCreateWithFlags(&e.lane_fork_ev, cudaEventDisableTiming));
     while ((int)e.lanes.size() < n - 1) {
@@ -1385,6 +1386,7 @@ int ob_profile(ob_engine* h, int32_t enable) {
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
+    OB_CHECK(!enable || h->impl.nlanes == 1, OB_ESTATE, "profiling runs on one lane (ob_set_lanes(e, 1))");
     OB_CUDA(cudaStreamSynchronize(h->impl.stream));
     h->impl.prof.reset();
     h->impl.prof.on = enable != 0;

@@ -97,3 +97,31 @@ def test_lanes_under_cgp_emulation(setup):
     got = [x[0] for x in eng.serve_stream(reqs, depth=4)]
     assert all(np.array_equal(a, b) for a, b in zip(got, ref))
     eng.close()
+
+
+def test_lane_api_errors(setup):
+    import ctypes as C
+
+    from paper_2501_08547_b200 import _native as nat
+    from paper_2501_08547_b200 import runtime
+
+    serving, model, w, pe, reqs = setup
+    eng = runtime.ServingEngine(serving, pe, model, w, runtime.ServeConfig(strategy="srpe", gamma=0.2))
+    with pytest.raises(ValueError):
+        eng.set_lanes(0)
+    with pytest.raises(ValueError):
+        eng.set_lanes(9)
+    eng.set_lanes(2)
+    with pytest.raises(RuntimeError):  # profiling needs one lane
+        nat.check(nat.lib.ob_profile(eng._h, 1))
+    it = eng.serve_stream(reqs, depth=2)
+    next(it)  # one request retired, one still in flight
+    with pytest.raises(RuntimeError):
+        eng.set_lanes(1)
+    rest = list(it)
+    assert len(rest) == len(reqs) - 1
+    eng.set_lanes(1)
+    nat.check(nat.lib.ob_profile(eng._h, 1))
+    nat.check(nat.lib.ob_profile(eng._h, 0))
+    _ = C
+    eng.close()
