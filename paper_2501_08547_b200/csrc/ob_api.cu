@@ -1198,6 +1198,14 @@ int ob_set_lanes(ob_engine* h, int32_t n) {
       for (cudaEvent_t* ev_ : {&L.fork_ev, &L.join_ev, &L.csr_ev, &L.done_ev})
         OB_CUDA(cudaEventCreateWithFlags(ev_, cudaEventDisableTiming));
     }
+    if (n != e.nlanes) {  // the gather plan depends on the lane count: re-capture every lane's graphs
+      e.drop_graphs();
+      for (auto& L : e.lanes) {
+        for (auto& gr : L.graphs)
+          if (gr.exec) cudaGraphExecDestroy(gr.exec);
+        L.graphs.clear();
+      }
+    }
     e.nlanes = n;
     e.lane_rr = 0;
   });

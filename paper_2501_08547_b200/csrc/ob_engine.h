@@ -389,6 +389,7 @@ struct LayerRun {
   const int32_t* dst_ids = nullptr;
   const int32_t* indeg = nullptr;
   int64_t N = 0;
+  bool split_gather = false;  // sum gathers as L2-sized source-range passes (request lanes)
 };
 
 // CGP merge inputs: partition p's raw partial rows and local in-edge counts

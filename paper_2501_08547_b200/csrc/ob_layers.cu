@@ -149,6 +149,10 @@ struct AggArgs {
   const int32_t* skip_dst_ids = nullptr;
   const int32_t* skip_indeg = nullptr;
   int64_t skip_N = 0;
+  // source-range pass (sum): only sources [src_lo, src_hi) of each row (a row's
+  // sources are ascending, so that is a contiguous run of every 32-edge group);
+  // accumulate adds to the partials of the previous pass
+  int pass = 0, passes = 1;  // pass p covers sources [S p / passes, S (p+1) / passes)
 };
 
 template <int OP, int NV>
@@ -161,6 +165,12 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : 1)) k_agg(AggAr
   const int col0 = blockIdx.y * (32 * 4 * NV);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int32_t src_lo = 0, src_hi = 0x7fffffff;
+  if (a.passes > 1) {
+    const int64_t S = a.cnt->S;
+    src_lo = (int32_t)(S * a.pass / a.passes);
+    src_hi = a.pass + 1 == a.passes ? 0x7fffffff : (int32_t)(S * (a.pass + 1) / a.passes);
+  }
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = __ldg(a.item_dst + it);
     const int64_t j = it - a.item_ptr[i];
@@ -181,22 +191,27 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : 1)) k_agg(AggAr
       // lane-cooperative edge fetch, then broadcast
       const int64_t my = eb + lane;
       const int32_t s_l = my < e1 ? a.edge_src[my] : 0;
-      const float* r_l = my < e1 ? a.x.row(s_l) : nullptr;
+      const bool in_l = my < e1 && s_l >= src_lo && s_l < src_hi;
+      const float* r_l = in_l ? a.x.row(s_l) : nullptr;
       float w_l = 1.f;
-      if (my < e1) {
+      if (in_l) {
         if (OP == kOpSum && a.gscale) w_l = a.gscale[s_l];
         if (OP == kOpSoftmax) {
           float lg = a.s_src[s_l] + sd;
           w_l = lg >= 0.f ? lg : 0.2f * lg;  // leaky_relu(0.2)
         }
       }
-      const int cnt = (int)min((int64_t)32, e1 - eb);
+      // the group's in-range edges are contiguous (ascending sources): [first, first + cnt)
+      const unsigned inb = __ballot_sync(0xffffffffu, in_l);
+      if (!inb) continue;
+      const int first = __ffs(inb) - 1;
+      const int cnt = __popc(inb);
       for (int u = 0; u < cnt; u += kU) {
         float4 v[kU][NV];
         float wg[kU];
 #pragma unroll
         for (int x = 0; x < kU; ++x) {  // issue kU row loads before consuming any
-          const int uu = min(u + x, cnt - 1);
+          const int uu = first + min(u + x, cnt - 1);
           const float* r = (const float*)__shfl_sync(0xffffffffu, (unsigned long long)r_l, uu);
           wg[x] = __shfl_sync(0xffffffffu, w_l, uu);
 #pragma unroll
@@ -257,7 +272,7 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : 1)) k_agg(AggAr
       const int col = col0 + (q * 32 + lane) * 4;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (col + t < a.width) out[col + t] = acc[q][t];
+        if (col + t < a.width) out[col + t] = a.pass > 0 ? out[col + t] + acc[q][t] : acc[q][t];
     }
   }
 }
@@ -494,16 +509,31 @@ __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* sel
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
+// Sum gathers over a source-row set larger than ~half the L2 run as source-range
+// passes, each touching a slice of the rows that stays L2-resident.
+constexpr int64_t kAggPassBytes = 64ll << 20;
+
 template <int OP>
-static void launch_agg(cudaStream_t s, const AggArgs& a, int64_t items_max) {
-  const int nv = a.width <= 128 ? 1 : (a.width <= 256 ? 2 : 4);
-  dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a.width + 128 * nv - 1) / (128 * nv));
+static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int64_t S_max = 0) {
+  const int nv = a0.width <= 128 ? 1 : (a0.width <= 256 ? 2 : 4);
+  dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a0.width + 128 * nv - 1) / (128 * nv));
+  int passes = 1;
+  if (OP == kOpSum && S_max > 0 && !a0.skip_indeg) {
+    const int64_t rows_bytes = S_max * (int64_t)ld4(a0.width) * 4;
+    passes = (int)std::min<int64_t>(4, (rows_bytes + kAggPassBytes - 1) / kAggPassBytes);
+    if (passes < 1) passes = 1;
+  }
   cudaEvent_t pa = prof_begin(s);
-  if (nv == 1) k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a);
-  else if (nv == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a);
-  else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a);
-  OB_LAUNCHED();
-  prof_end(s, pa, kProfAgg, a.cnt, a.width, a.pw, 0, 0, 0);
+  for (int p = 0; p < passes; ++p) {
+    AggArgs a = a0;
+    a.pass = p;
+    a.passes = passes;
+    if (nv == 1) k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a);
+    else if (nv == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a);
+    else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a);
+    OB_LAUNCHED();
+  }
+  prof_end(s, pa, kProfAgg, a0.cnt, a0.width, a0.pw, 0, 0, 0);
 }
 
 static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t items_max) {
@@ -628,7 +658,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   }
   if (sp.kind == OB_KIND_GCN) {
     a.gscale = r.gscale;
-    launch_agg<kOpSum>(s, a, r.items_max);
+    launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
     f.gcn_norm = true;
     if (L.transform_first) {  // relu(sum_u (x_u W) / sqrt(d_u+1) / sqrt(c+1))
       f.out = out;
@@ -646,7 +676,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     return;
   }
   if (sp.kind == OB_KIND_SAGE_MEAN && L.transform_first) {
-    launch_agg<kOpSum>(s, a, r.items_max);
+    launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
     finalize(s, f, r.D_max, r.items_max);  // mean over Y = X W_neigh rows -> agg [D][ld_out]
     TcGemmArgs g = gemm_args(r.D_dev, L.tw_self, out, ldo, true);
     g.a1 = r.x;
@@ -674,7 +704,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
         r.cnt, r.dst_ptr, r.item_ptr, (const double*)sc.partial, in, 2, sp.n, nullptr, sc.agg, ld4(in));
     g_launches += 2;
   } else {  // sage_mean aggregate-first
-    launch_agg<kOpSum>(s, a, r.items_max);
+    launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
     finalize(s, f, r.D_max, r.items_max);
   }
   // relu([h_v | agg] @ [W_self; W_neigh])
@@ -1072,6 +1102,8 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     r.x = RowSrc{w.rowp, nullptr, 0};
     r.gscale = w.gscale;
     r.group_ptr = b.group_ptr;
+    // with several requests in flight, big sum gathers run as L2-sized source-range passes
+    r.split_gather = e.nlanes > 1;
     LayerScratch sc{w.partial, w.partial2, w.agg, w.mean, w.z, w.s_src, w.s_dst};
     const bool last = l == k;
     float* out = last ? d_out : w.outs[l];
