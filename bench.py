@@ -555,7 +555,10 @@ def main():
             "gathered_row_gbs": round(agg["flops"] / (agg["ms"] / 1e3) / 1e9, 1) if agg["ms"] > 0 else None,
             "gather_ceiling_gbs": 15200.0,  # measured random 512-B row gather, L2-sized table (profiles/r01_gather_ceiling.md)
             "note": "rows are re-read once per edge (avg source out-degree in the block), mostly from L2; "
-                    "gathered_row_gbs is that served traffic, the kernel's real limiter (L2 fabric)",
+                    "gathered_row_gbs is that served traffic, the kernel's real limiter (L2 fabric). The "
+                    "layer-1 launch under stored aggregates gathers only the request spans, which the block "
+                    "counters do not size: it contributes its edge list and partials but no row bytes "
+                    "(both figures are conservative)",
             "share_of_step": round(agg["ms"] / max(reqp["ms"], 1e-9), 3)}
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,

@@ -1420,7 +1420,11 @@ int ob_profile_read(ob_engine* h, int32_t cls, double* total_ms, int64_t* launch
       ++n;
       if (r.slot < 0) continue;
       const BlockCounters& c = e.prof.pinned[r.slot];
-      if (cls == kProfAgg) {
+      if (cls == kProfAgg && r.K < 0) {
+        // stored-aggregate launch: rows gathered for the request spans only (not sized by the
+        // block counters) -- count the edge list and the partials, no rows (conservative)
+        by += 4.0 * c.E + 4.0 * r.pw * c.items;
+      } else if (cls == kProfAgg) {
         // edge list + every source row once + partial rows out
         by += 4.0 * c.E + 4.0 * r.width * c.S + 4.0 * r.pw * c.items;
         fl += 4.0 * r.width * c.E;  // gathered row bytes (rows are re-read once per edge, mostly from L2)

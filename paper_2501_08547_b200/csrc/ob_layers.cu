@@ -533,7 +533,9 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
     else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a);
     OB_LAUNCHED();
   }
-  prof_end(s, pa, kProfAgg, a0.cnt, a0.width, a0.pw, 0, 0, 0);
+  // K = -1 marks a stored-aggregate launch: it gathers only the request spans, which the
+  // block counters do not size, so the profiler counts its edge list and partials only
+  prof_end(s, pa, kProfAgg, a0.cnt, a0.width, a0.pw, a0.skip_indeg ? -1 : 0, 0, 0);
 }
 
 static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t items_max) {
