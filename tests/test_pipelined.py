@@ -125,3 +125,29 @@ def test_lane_api_errors(setup):
     nat.check(nat.lib.ob_profile(eng._h, 0))
     _ = C
     eng.close()
+
+
+def test_source_range_passes_match_oracle():
+    """Lanes on + a source-row set above 64 MB: the sum gathers run as source-range passes."""
+    from oracle import layers as OL
+    from paper_2501_08547_b200 import graphstore, models, runtime, workload
+
+    full = workload.gen_powerlaw_graph(200_000, 12.0, 2.1, 16, seed=21)
+    serving, pool = workload.split_holdout(full, 0.25, seed=21)
+    model = models.make_model("sage_mean", 3, 16, 128)  # 512-byte rows: 200K rows exceed 64 MB
+    w = models.init_weights(model, 3)
+    layers = [dict(kind=s.kind, in_dim=s.in_dim, out_dim=s.out_dim) for s in model.layers]
+    pe = graphstore.precompute_embeddings(serving, model, w)
+    reqs = [workload.make_request(pool, serving, 64, seed=s) for s in (1, 2, 3)]
+    eng = runtime.ServingEngine(serving, pe, model, w, runtime.ServeConfig(strategy="srpe", gamma=0.3))
+    one = [eng.serve(r)[0] for r in reqs]
+    eng.set_lanes(2)
+    two = [x[0] for x in eng.serve_stream(reqs, depth=2)]
+    for r, a, b in zip(reqs, one, two):
+        ref = OL.serve("srpe", layers, w.layers, serving.num_nodes, r.num_queries, serving.in_offsets,
+                       serving.in_neighbors, serving.features, r.query_features, r.edges, pe_layers=pe.layers,
+                       gamma=0.3)
+        assert OL.max_rel_err(a, ref["emb"]) <= 1e-4
+        assert OL.max_rel_err(b, ref["emb"]) <= 1e-4
+        assert OL.max_rel_err(a, b) <= 1e-5
+    eng.close()
