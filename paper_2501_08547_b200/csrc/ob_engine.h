@@ -390,6 +390,12 @@ struct LayerRun {
   const int32_t* indeg = nullptr;
   int64_t N = 0;
   bool split_gather = false;  // sum gathers as L2-sized source-range passes (request lanes)
+  // layer-1 SAGE update from the stored own-row transform: only the B query rows need a GEMM
+  const float* self_tab = nullptr;
+  const float* qpad = nullptr;
+  int64_t q_ld = 0;
+  const int64_t* B_dev = nullptr;
+  int64_t B = 0;
 };
 
 // CGP merge inputs: partition p's raw partial rows and local in-edge counts
@@ -682,6 +688,8 @@ struct Engine {
   // training node's CSR in-neighbours is static (only request edges, whose
   // sources are queries, change it): sagg1[v] = sum_u w_u x_u (W), raw, unnormalised
   float* sagg1 = nullptr;
+  // SAGE-mean transform-first layer 1: x_v W_self per training node (the update's own-row term)
+  float* yself1 = nullptr;
   // IS policy: per-node numerators of the whole CSR (centralized) or of each
   // local partition's source-split CSR (CGP), computed once per graph
   std::vector<double*> is_tab;
@@ -691,6 +699,8 @@ struct Engine {
     ytab.clear();
     dfree(sagg1);
     sagg1 = nullptr;
+    dfree(yself1);
+    yself1 = nullptr;
     for (double* t : is_tab) dfree(t);
     is_tab.clear();
     ytab_ready = false;

@@ -574,6 +574,24 @@ static TcGemmArgs gemm_args(const int64_t* M_dev, const TcWeights& w, float* C, 
   return g;
 }
 
+// out[i] = relu(own[i] + agg[i]) with own = the stored x_v W_self of a training destination or the
+// query's GEMM row -- the same fp32 sum the GEMM epilogue forms (acc + addend, then relu)
+__global__ void k_self_update(const BlockCounters* cnt, const int32_t* __restrict__ dst_ids, int64_t N,
+                              const float* __restrict__ tab, const float* __restrict__ qrows, int64_t ld,
+                              const float* __restrict__ agg, int width, float* out, int64_t ldo) {
+  const int64_t D = cnt->D;
+  const int64_t n = D * ld;
+  OB_GRID_STRIDE(t, n) {
+    const int64_t i = t / ld;
+    const int c = (int)(t - i * ld);
+    if (c >= width) continue;
+    const int64_t v = dst_ids[i];
+    float o = v < N ? tab[v * ld + c] : qrows[(v - N) * ld + c];
+    o += agg[i * ld + c];
+    out[i * ldo + c] = fmaxf(o, 0.f);
+  }
+}
+
 void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc, float* out,
                int64_t ldo) {
   const ob_layer& sp = L.spec;
@@ -675,6 +693,19 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     g.lda2 = ld4(in);
     g.K2 = in;
     gemm(s, g, r.D_max, r.cnt);
+    return;
+  }
+  if (sp.kind == OB_KIND_SAGE_MEAN && L.transform_first && r.self_tab) {
+    launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
+    finalize(s, f, r.D_max, r.items_max);  // mean over Y = X W_neigh rows -> agg [D][ld_out]
+    // own-row term: training destinations from the stored table, the queries by a B-row GEMM
+    TcGemmArgs g = gemm_args(r.B_dev, L.tw_self, sc.z, ld_out, false);
+    g.a1 = RowSrc{nullptr, r.qpad, r.q_ld};
+    g.K1 = in;
+    gemm(s, g, r.B, nullptr);
+    k_self_update<<<grid_for(r.D_max * ld_out, 256), 256, 0, s>>>(r.cnt, r.dst_ids, r.N, r.self_tab, sc.z, ld_out,
+                                                                    sc.agg, outd, out, ldo);
+    OB_LAUNCHED();
     return;
   }
   if (sp.kind == OB_KIND_SAGE_MEAN && L.transform_first) {
@@ -1081,6 +1112,15 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       r.ndyn = w.ndyn;
       r.dyn_max = b.S_max;
     }
+    if (l == 1 && e.yself1) {
+      r.self_tab = e.yself1;
+      r.dst_ids = b.dst_ids;
+      r.N = e.g.N;
+      r.qpad = w.qpad;
+      r.q_ld = e.g.F_ld;
+      r.B_dev = &w.blocks[(int)w.blocks.size() - 1].cnt->D;  // the query block: D = B
+      r.B = w.B;
+    }
     if (l == 1 && e.sagg1) {
       r.stat = e.sagg1;
       r.stat_ld = L.spec.kind == OB_KIND_GAT ? kSmHdr + ld4(L.spec.out_dim)
@@ -1238,8 +1278,22 @@ void build_stored_transforms(Engine& e) {
     tc_gemm(s, g, N);
     e.ytab[l - 1] = t;
   }
-  // stored aggregates of layer 1 (srpe / full: block-1 rows are CSR ++ request)
+  // own-row transform of a transform-first SAGE layer 1 (its destinations' x_v W_self)
   const LayerDev& L1 = e.layers[0];
+  if (L1.spec.kind == OB_KIND_SAGE_MEAN && L1.transform_first && e.ytab[0] &&
+      (e.cfg.strategy == OB_STRATEGY_SRPE || e.cfg.strategy == OB_STRATEGY_FULL)) {
+    const int64_t ld = ld4(L1.spec.out_dim);
+    size_t fb = 0, tb = 0;
+    OB_CUDA(cudaMemGetInfo(&fb, &tb));
+    if ((size_t)N * ld * 4 <= fb / 3) {
+      e.yself1 = (float*)e.dalloc(sizeof(float) * N * ld);
+      TcGemmArgs g = gemm_args(n_dev, L1.tw_self, e.yself1, ld, false);
+      g.a1 = RowSrc{nullptr, e.g.feats, e.g.F_ld};
+      g.K1 = L1.spec.in_dim;
+      tc_gemm(s, g, N);
+    }
+  }
+  // stored aggregates of layer 1 (srpe / full: block-1 rows are CSR ++ request)
   {
     const char* off_g = std::getenv("OB_NO_STORED_AGGREGATES");
     const bool rows_full_g = e.cfg.strategy == OB_STRATEGY_SRPE || e.cfg.strategy == OB_STRATEGY_FULL;
