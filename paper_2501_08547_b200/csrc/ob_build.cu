@@ -398,17 +398,9 @@ void write_query_dst(Engine& e, RequestWs& w, BlockDev& b) {
   OB_LAUNCHED();
 }
 
-void stage_build_srpe(Engine& e, RequestWs& w) {
-  // blocks[0] = shared mid block (layers 1..k-1), blocks[1] = last block (layer k)
-  const SpanSrc src{e.g.offsets, e.g.nbrs, e.g.indeg, w.rq_ptr, w.rq_src};
-  write_mid_dst(e, w, w.blocks[0]);
-  assemble(e, w, w.blocks[0], src, w.bs[0]);
-  write_query_dst(e, w, w.blocks[1]);
-  assemble(e, w, w.blocks[1], src, w.bs[1]);
-}
 
 // the two srpe blocks separately: the query block needs only the request index,
-// the mid block also the targets (stage_build_srpe = both, in order)
+// the mid block also the targets
 void build_query_block(Engine& e, RequestWs& w) {
   const SpanSrc src{e.g.offsets, e.g.nbrs, e.g.indeg, w.rq_ptr, w.rq_src};
   write_query_dst(e, w, w.blocks[1]);

@@ -534,7 +534,6 @@ void build_query_block(Engine& e, RequestWs& w);
 void build_mid_block(Engine& e, RequestWs& w);
 void write_mid_dst(Engine& e, RequestWs& w, BlockDev& b);
 void write_query_dst(Engine& e, RequestWs& w, BlockDev& b);
-void stage_build_srpe(Engine& e, RequestWs& w);
 void stage_build_full(Engine& e, RequestWs& w);
 void stage_forward(Engine& e, RequestWs& w, float* d_out);
 void stage_precompute(Engine& e);

@@ -3,6 +3,7 @@
 // Reference (paths relative to /root/reference/pkg/src/gnnserve):
 //   candidate_arrays / find_candidates  compgraph.py:108-121, policy.py:64-67
 //   score_query_edge_ratio              policy.py:77-81   (IEEE fp64 nq / total)
+//   score_importance / partial sums     policy.py:84-107, runtime.py:168-175 (numpy pairwise fp64 sums)
 //   select_targets                      policy.py:110-135 (floor(gamma*|R|), score desc, id asc)
 //   _EdgeIndex                          compgraph.py:155-171 (request edges by dst, src ascending)
 //
