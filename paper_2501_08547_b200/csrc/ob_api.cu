@@ -230,6 +230,8 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.mean = mom ? a.take<float>(2 * Dmax * wl) : nullptr;
   w.z = wide ? a.take<float>(Smax * wl) : nullptr;
   w.yrow = wide ? a.take<const float*>(Smax) : nullptr;
+  w.qxw = wide ? a.take<float>((int64_t)(B + 1) * wl) : nullptr;
+  w.qself = wide ? a.take<float>((int64_t)(B + 1) * wl) : nullptr;
   w.dyn_src = wide ? a.take<int32_t>(Smax) : nullptr;
   w.ndyn = wide ? a.take<int64_t>(1) : nullptr;
   w.s_src = gat ? a.take<float>(Smax) : nullptr;
@@ -337,10 +339,11 @@ static int64_t bucket_m(int64_t m) {
   return b;
 }
 
-__global__ void k_set_params(ReqParams* p, const int64_t* edges, const float* q, int64_t m) {
+__global__ void k_set_params(ReqParams* p, const int64_t* edges, const float* q, int64_t m, int64_t B) {
   p->edges = edges;
   p->qfeat = q;
   p->m = m;
+  p->B = B;
 }
 
 // every stage of one request, enqueued on e.stream (eagerly or under capture)
@@ -364,6 +367,7 @@ static void enqueue_stages(Engine& e, float* d_out) {
   cudaStream_t s = e.stream;
   RequestWs& w = e.ws;
   const bool srpe = !khop(e.cfg);
+  w.qrows_ready = w.qpad_ready = false;
   OB_CUDA(cudaMemsetAsync(w.rc, 0, sizeof(ReqCounters), s));
   for (auto& b : w.blocks) OB_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(BlockCounters), s));
   if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) {
@@ -398,6 +402,8 @@ static void enqueue_stages(Engine& e, float* d_out) {
   stage_request_post(e, w, srpe);
   if (srpe) stage_select(e, w);
   prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
+  // query rows of layer 1 (padding, stored-transform rows) while the request index sorts
+  stage_query_rows(e, w);
   OB_CUDA(cudaStreamWaitEvent(s, e.csr_ev, 0));
   p0 = prof_begin(s);
   if (srpe) build_mid_block(e, w);
@@ -495,7 +501,7 @@ static void enqueue_serve(Engine& e, int B, const float* d_q, int64_t m, const i
   w.edges = d_edges;
   w.qfeat = d_q;
   // kernel arguments are copied at launch: the block is stream-ordered with no host staging
-  k_set_params<<<1, 1, 0, s>>>(e.params, d_edges, d_q, m);
+  k_set_params<<<1, 1, 0, s>>>(e.params, d_edges, d_q, m, B);
   OB_LAUNCHED();
   OB_CUDA(cudaEventRecord(e.ev[0], s));
   if (e.prof.on || !e.use_graphs) {

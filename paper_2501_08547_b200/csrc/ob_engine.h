@@ -205,7 +205,7 @@ struct ReqParams {
   const int64_t* edges;  // device [m][2]
   const float* qfeat;    // device [B][F]
   int64_t m;             // edge count of this request
-  int64_t pad;
+  int64_t B;             // query count (GEMM row count of the early query transforms)
 };
 
 // one (src, dst) request edge: a single 16-byte load when the array allows it
@@ -289,6 +289,10 @@ struct RequestWs {
   const float** yrow = nullptr;    // [S_max] stored-transform row per source (wide layers)
   int32_t* dyn_src = nullptr;      // [S_max] sources whose transformed row is computed per request
   int64_t* ndyn = nullptr;
+  float* qxw = nullptr;            // [B][ld] layer-1 x_q W of the queries (stored-transform layers)
+  float* qself = nullptr;          // [B][ld] layer-1 x_q W_self (SAGE own-row table)
+  bool qrows_ready = false;        // host: this enqueue staged qxw / qself early
+  bool qpad_ready = false;         // host: this enqueue staged qpad early
   float* gscale = nullptr;         // [S_max] gcn source normaliser
   float* partial = nullptr;        // [items_max][w + 2]
   float* partial2 = nullptr;       // [groups_max][w + 2] second-level partials of hub destinations
@@ -362,6 +366,7 @@ struct BindCtx {
   float* ydyn;          // [dyn][y_ld] transformed rows of the listed sources
   int32_t* dyn_src;     // [dyn] source index per listed row
   int64_t* ndyn;        // device count of listed rows (zeroed before k_resolve)
+  const float* qxw;     // layer 1: the queries' transformed rows, computed early (no listing)
 };
 
 struct LayerRun {
@@ -396,6 +401,8 @@ struct LayerRun {
   int64_t q_ld = 0;
   const int64_t* B_dev = nullptr;
   int64_t B = 0;
+  const float* self_q = nullptr;   // the queries' own-row transforms, computed early
+  bool no_dyn = false;             // every transformed row is a table row: skip the listed-row GEMM
 };
 
 // CGP merge inputs: partition p's raw partial rows and local in-edge counts
@@ -505,6 +512,7 @@ void expand_items(cudaStream_t s, const BlockCounters* cnt, int64_t D_max, const
 void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d_kind, int32_t* d_pe_layer);
 BindCtx bind_ctx(Engine& e, RequestWs& w, int l);
 void stage_qpad(Engine& e, RequestWs& w);
+void stage_query_rows(Engine& e, RequestWs& w);
 
 void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, int64_t words, int32_t* out);
 

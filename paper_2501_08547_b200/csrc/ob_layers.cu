@@ -88,6 +88,8 @@ __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restri
       const bool stat = (k == 0 && g < c.N) || k == 1;
       if (stat) {
         c.yrow[s] = c.ytab + g * c.y_ld;
+      } else if (c.qxw && g >= c.N) {
+        c.yrow[s] = c.qxw + (g - c.N) * c.y_ld;
       } else {
         const unsigned act = __activemask();
         const unsigned b = __ballot_sync(act, 1);
@@ -699,11 +701,16 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
     finalize(s, f, r.D_max, r.items_max);  // mean over Y = X W_neigh rows -> agg [D][ld_out]
     // own-row term: training destinations from the stored table, the queries by a B-row GEMM
-    TcGemmArgs g = gemm_args(r.B_dev, L.tw_self, sc.z, ld_out, false);
-    g.a1 = RowSrc{nullptr, r.qpad, r.q_ld};
-    g.K1 = in;
-    gemm(s, g, r.B, nullptr);
-    k_self_update<<<grid_for(r.D_max * ld_out, 256), 256, 0, s>>>(r.cnt, r.dst_ids, r.N, r.self_tab, sc.z, ld_out,
+    // (done early, beside the request-index sort, when the query rows were staged ahead)
+    const float* qs = r.self_q;
+    if (!qs) {
+      TcGemmArgs g = gemm_args(r.B_dev, L.tw_self, sc.z, ld_out, false);
+      g.a1 = RowSrc{nullptr, r.qpad, r.q_ld};
+      g.K1 = in;
+      gemm(s, g, r.B, nullptr);
+      qs = sc.z;
+    }
+    k_self_update<<<grid_for(r.D_max * ld_out, 256), 256, 0, s>>>(r.cnt, r.dst_ids, r.N, r.self_tab, qs, ld_out,
                                                                     sc.agg, outd, out, ldo);
     OB_LAUNCHED();
     return;
@@ -1086,9 +1093,11 @@ __global__ void k_pad_rows(const ReqParams* rp, int64_t rows, int w, float* dst,
 void stage_forward(Engine& e, RequestWs& w, float* d_out) {
   cudaStream_t s = e.stream;
   const int k = (int)e.layers.size();
-  // stage query features with 16 B aligned rows
-  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, s>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
-  OB_LAUNCHED();
+  // stage query features with 16 B aligned rows (unless staged early, stage_query_rows)
+  if (!w.qpad_ready) {
+    k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, s>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
+    OB_LAUNCHED();
+  }
   for (int l = 1; l <= k; ++l) {
     const LayerDev& L = e.layers[l - 1];
     BlockDev& b = w.blocks[w.block_of_layer[l - 1]];
@@ -1101,6 +1110,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       c.ydyn = w.z;
       c.dyn_src = w.dyn_src;
       c.ndyn = w.ndyn;
+      if (l == 1 && w.qrows_ready) c.qxw = w.qxw;  // layer 1: queries are the only non-table sources
       OB_CUDA(cudaMemsetAsync(w.ndyn, 0, sizeof(int64_t), s));
     }
     k_resolve<<<grid_for(b.S_max, 256), 256, 0, s>>>(c, b.cnt, b.src_ids, w.rowp, w.gscale, nullptr, nullptr);
@@ -1111,6 +1121,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       r.dyn_src = w.dyn_src;
       r.ndyn = w.ndyn;
       r.dyn_max = b.S_max;
+      r.no_dyn = l == 1 && w.qrows_ready;
     }
     if (l == 1 && e.yself1) {
       r.self_tab = e.yself1;
@@ -1120,6 +1131,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       r.q_ld = e.g.F_ld;
       r.B_dev = &w.blocks[(int)w.blocks.size() - 1].cnt->D;  // the query block: D = B
       r.B = w.B;
+      if (w.qrows_ready) r.self_q = w.qself;
     }
     if (l == 1 && e.sagg1) {
       r.stat = e.sagg1;
@@ -1151,6 +1163,33 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     float* out = last ? d_out : w.outs[l];
     run_layer(s, L, r, sc, out, last ? L.spec.out_dim : ld4(L.spec.out_dim));
   }
+}
+
+// Layer-1 query rows ahead of the block builds: padded features and, for layers with
+// stored transforms, x_q W (and x_q W_self for the SAGE own-row table) over the B queries.
+// Launched on the main stream beside the request-index sort, off the critical path.
+void stage_query_rows(Engine& e, RequestWs& w) {
+  cudaStream_t s = e.stream;
+  w.qrows_ready = false;
+  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, s>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
+  OB_LAUNCHED();
+  w.qpad_ready = true;
+  const LayerDev& L = e.layers[0];
+  const bool yt = e.ytab_ready && !e.ytab.empty() && e.ytab[0] && w.qxw;
+  const int64_t ld = ld4(L.spec.out_dim);
+  if (yt) {
+    TcGemmArgs g = gemm_args(&w.rp->B, L.tw_main, w.qxw, ld, false);
+    g.a1 = RowSrc{nullptr, w.qpad, e.g.F_ld};
+    g.K1 = L.spec.in_dim;
+    gemm(s, g, w.B, nullptr);
+  }
+  if (yt && e.yself1) {
+    TcGemmArgs g = gemm_args(&w.rp->B, L.tw_self, w.qself, ld, false);
+    g.a1 = RowSrc{nullptr, w.qpad, e.g.F_ld};
+    g.K1 = L.spec.in_dim;
+    gemm(s, g, w.B, nullptr);
+  }
+  w.qrows_ready = yt;
 }
 
 void stage_qpad(Engine& e, RequestWs& w) {
