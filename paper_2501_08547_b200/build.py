@@ -25,6 +25,7 @@ SOURCES = ["ob_select.cu", "ob_build.cu", "ob_layers.cu", "ob_gemm.cu", "ob_cgp.
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+FLAGS += os.environ.get("OB_NVCC_EXTRA", "").split()  # e.g. -DOB_RX_MINB=3 for tuning sweeps
 
 
 def _nccl_flags() -> tuple[list[str], list[str]]:

@@ -699,6 +699,9 @@ struct SelTotal {
 //    writes the decoded source ids straight into the CSR.
 // ---------------------------------------------------------------------------
 constexpr int kRxThreads = 512;
+#ifndef OB_RX_MINB
+#define OB_RX_MINB 2  // scatter CTAs resident per SM (caps registers at 64)
+#endif
 constexpr int kRxWarps = kRxThreads / 32;
 constexpr int kRxItems = kRxTile / kRxThreads;  // 8 keys per thread, warp-striped
 
@@ -722,7 +725,7 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* __restrict__ ke
 }
 
 template <class K, bool FINAL>
-__global__ void __launch_bounds__(kRxThreads) k_rx_scatter(const K* __restrict__ in, K* out, int32_t* src_out,
+__global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* __restrict__ in, K* out, int32_t* src_out,
                                                            const int64_t* m_dev, int shift, int64_t tiles_b,
                                                            const int64_t* __restrict__ off,
                                                            const int32_t* __restrict__ cnt, RqKeyFmt f, int64_t N,
@@ -835,7 +838,7 @@ template <class K>
 static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int64_t m_bound, const RqKeyFmt& f) {
   cudaStream_t s = e.stream;
   const int64_t tiles_b = rx_tiles(m_bound);
-  const int g = grid_for(tiles_b, 1, kNumSMs * 2);
+  const int g = grid_for(tiles_b, 1, kNumSMs * (OB_RX_MINB > 2 ? OB_RX_MINB : 2));
   K* a = reinterpret_cast<K*>(c.keys);
   K* b = reinterpret_cast<K*>(c.keys2);
   const int passes = f.passes();
