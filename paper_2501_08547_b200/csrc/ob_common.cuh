@@ -98,6 +98,9 @@ __device__ __forceinline__ int64_t bm_rank(const uint32_t* bits, const int64_t* 
 constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
+#ifndef OB_SCAN_MINB
+#define OB_SCAN_MINB 2  // int64 scan CTAs resident per SM (I3 scans keep one: 3x the registers)
+#endif
 
 // three running sums scanned together (block assembly: edges, items, groups)
 struct I3 {
@@ -129,7 +132,7 @@ struct ScanTiles {
 };
 
 template <class T, int ITEMS, class Load, class Store, class Total>
-__global__ void __launch_bounds__(kScanThreads) k_scan(Load load, Store store, Total total, const int64_t* n_dev,
+__global__ void __launch_bounds__(kScanThreads, sizeof(T) == 8 ? OB_SCAN_MINB : 1) k_scan(Load load, Store store, Total total, const int64_t* n_dev,
                                                        int64_t n_host, ScanTiles<T> st) {
   using BS = cub::BlockScan<T, kScanThreads>;
   using BX = cub::BlockExchange<T, kScanThreads, ITEMS>;
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Load load, const i
 __global__ void __launch_bounds__(1024) k_scan_spine(const int64_t* n_dev, int64_t n_host, int64_t* tile_sums);
 
 template <class Load, class Store, class Total>
-__global__ void __launch_bounds__(kScanThreads) k_scan_down(Load load, Store store, Total total,
+__global__ void __launch_bounds__(kScanThreads, OB_SCAN_MINB) k_scan_down(Load load, Store store, Total total,
                                                             const int64_t* n_dev, int64_t n_host,
                                                             const int64_t* tile_off) {
   using BS = cub::BlockScan<int64_t, kScanThreads>;

@@ -1,9 +1,16 @@
+# Tuning sweep for residency macros (-DOB_RX_MINB / -DOB_SCAN_MINB): rebuild, bench cfg1-3, then GPU tests.
+# usage: bash tools/rx_sweep.sh TAG "FLAGS1" "FLAGS2" ...
 set -x
+tag=$1; shift
 mkdir -p gpurun_out
-for mb in 1 2 3; do
-  OB_NVCC_EXTRA="-DOB_RX_MINB=$mb" python -c "from paper_2501_08547_b200.build import build; build(force=True)" > gpurun_out/c2_build_$mb.log 2>&1
-  timeout 300 python bench.py --no-cpu > gpurun_out/c2_bench_cfg2_mb$mb.json 2> gpurun_out/c2_bench_cfg2_mb$mb.err
-  timeout 300 python bench.py --no-cpu --config cfg3 > gpurun_out/c2_bench_cfg3_mb$mb.json 2> gpurun_out/c2_bench_cfg3_mb$mb.err
+i=0
+for fl in "$@"; do
+  i=$((i+1))
+  OB_NVCC_EXTRA="$fl" python -c "from paper_2501_08547_b200.build import build; build(force=True)" > gpurun_out/${tag}_build_$i.log 2>&1
+  echo "$fl" > gpurun_out/${tag}_flags_$i.txt
+  for c in cfg2 cfg3 cfg1; do
+    timeout 300 python bench.py --no-cpu --config $c > gpurun_out/${tag}_bench_${c}_$i.json 2> gpurun_out/${tag}_bench_${c}_$i.err
+  done
 done
-OB_NVCC_EXTRA="-DOB_RX_MINB=2" python -c "from paper_2501_08547_b200.build import build; build(force=True)" > gpurun_out/c2_build_final.log 2>&1
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/c2_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/c2_pytest.log
+python -c "from paper_2501_08547_b200.build import build; build(force=True)" > gpurun_out/${tag}_build_final.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/${tag}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${tag}_pytest.log
