@@ -405,7 +405,10 @@ __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a, float* partial
   }
 }
 
-__global__ void __launch_bounds__(256) k_finalize(FinArgs a) {
+#ifndef OB_FIN_MINB
+#define OB_FIN_MINB 4  // k_finalize CTAs resident per SM (64 registers, no spills)
+#endif
+__global__ void __launch_bounds__(256, OB_FIN_MINB) k_finalize(FinArgs a) {
   const int64_t D = a.cnt->D;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
