@@ -158,7 +158,10 @@ struct AggArgs {
 };
 
 template <int OP, int NV>
-__global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : 1)) k_agg(AggArgs a) {
+#ifndef OB_AGG_MINB_WIDE
+#define OB_AGG_MINB_WIDE 1  // k_agg CTAs per SM for rows wider than 128 columns (NV = 2, 4)
+#endif
+__global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WIDE)) k_agg(AggArgs a) {
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   const int lane = threadIdx.x & 31;

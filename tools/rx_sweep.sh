@@ -8,7 +8,7 @@ for fl in "$@"; do
   i=$((i+1))
   OB_NVCC_EXTRA="$fl" python -c "from paper_2501_08547_b200.build import build; build(force=True)" > gpurun_out/${tag}_build_$i.log 2>&1
   echo "$fl" > gpurun_out/${tag}_flags_$i.txt
-  for c in cfg2 cfg3 cfg1; do
+  for c in ${SWEEP_CONFIGS:-cfg2 cfg3 cfg1}; do
     timeout 300 python bench.py --no-cpu --config $c > gpurun_out/${tag}_bench_${c}_$i.json 2> gpurun_out/${tag}_bench_${c}_$i.err
   done
 done
