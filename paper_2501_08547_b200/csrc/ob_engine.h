@@ -179,6 +179,8 @@ struct RqCsr {
   uint64_t* keys2 = nullptr;    // [m] radix pong
   int32_t* rx_cnt = nullptr;    // [256 x tiles] digit counts per 4096-key tile (digit-major)
   int64_t* rx_off = nullptr;    // [256 x tiles + 1] their exclusive scan
+  uint32_t* rx_st = nullptr;    // one-sweep: [8 passes][tiles][256] look-back words, 8 tickets,
+                                // [8][256] digit totals (rx_st_words); nullptr: hist + scan passes
   int64_t* ctr = nullptr;       // device [4]: m (slice edge count), spare
 };
 
@@ -197,6 +199,7 @@ struct RqKeyFmt {
 };
 constexpr int kRxTile = 4096;  // keys per radix tile (512 threads x 8)
 inline int64_t rx_tiles(int64_t m_bound) { return m_bound / kRxTile + 1; }
+inline int64_t rx_st_words(int64_t m_bound) { return 8 * 256 * rx_tiles(m_bound) + 8 + 8 * 256; }
 
 // Request inputs as seen by the kernels: written (16 bytes of pointers + m) before
 // each request so a captured CUDA graph can be replayed for any request whose
@@ -266,6 +269,7 @@ struct RequestWs {
   uint64_t* rq_keys2 = nullptr;    // [m] radix keys (pong)
   int32_t* rx_cnt = nullptr;       // radix digit counts
   int64_t* rx_off = nullptr;       // radix digit offsets
+  uint32_t* rx_st = nullptr;       // one-sweep look-back state (RqCsr::rx_st)
   int64_t* rq_ctr = nullptr;       // [4] csr counters
   RqCsr rq_view() const {
     RqCsr c;
@@ -277,6 +281,7 @@ struct RequestWs {
     c.keys2 = rq_keys2;
     c.rx_cnt = rx_cnt;
     c.rx_off = rx_off;
+    c.rx_st = rx_st;
     c.ctr = rq_ctr;
     return c;
   }

@@ -17,6 +17,7 @@
 // 8-bit passes over 32-bit keys -- which handles hub queries with 10^5 in-edges
 // and the ~10^5 tiny candidate slots alike.  Everything runs off device-side
 // counts.
+#include <cstdlib>
 #include <cub/block/block_scan.cuh>
 
 #include "ob_engine.h"
@@ -724,13 +725,34 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* __restrict__ ke
   }
 }
 
+// one-sweep: every pass's digit totals from one read of the keys ([pass][256])
+template <class K>
+__global__ void __launch_bounds__(kRxThreads) k_rx_ghist(const K* __restrict__ keys, const int64_t* m_dev, int passes,
+                                                         uint32_t* ghist) {
+  __shared__ uint32_t h[8 * 256];
+  for (int i = threadIdx.x; i < passes * 256; i += kRxThreads) h[i] = 0;
+  __syncthreads();
+  const int64_t m = *m_dev;
+  OB_GRID_STRIDE(e, m) {
+    const K k = keys[e];
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p * 256 + (int)((k >> (8 * p)) & 255)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += kRxThreads)
+    if (h[i]) atomicAdd(ghist + i, h[i]);
+}
+
+// look-back word: flag in the top two bits (1 tile count, 2 inclusive prefix), count below
+constexpr uint32_t kRxAgg = 1u << 30, kRxInc = 2u << 30, kRxCount = kRxAgg - 1u;
+
 template <class K, bool FINAL>
 __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* __restrict__ in, K* out, int32_t* src_out,
                                                            const int64_t* m_dev, int shift, int64_t tiles_b,
                                                            const int64_t* __restrict__ off,
                                                            const int32_t* __restrict__ cnt, RqKeyFmt f, int64_t N,
                                                            const int32_t* __restrict__ cand_ids,
-                                                           const ReqCounters* rc) {
+                                                           const ReqCounters* rc, uint32_t* st, uint32_t* ticket,
+                                                           const uint32_t* __restrict__ ghist) {
   using BS = cub::BlockScan<int32_t, kRxThreads>;
   using BS64 = cub::BlockScan<int64_t, kRxThreads>;
   __shared__ typename BS64::TempStorage scan_tmp64;
@@ -741,11 +763,25 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
   __shared__ typename BS::TempStorage scan_tmp;
   __shared__ int32_t bstart[256];
   __shared__ int64_t gofs[256];
+  __shared__ int64_t gbase[256];  // one-sweep: keys of smaller digits (whole input)
+  __shared__ int64_t s_t;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t m = *m_dev;
   const int64_t tiles = (m + kRxTile - 1) / kRxTile;
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+  if (st) {
+    int64_t g = threadIdx.x < 256 ? (int64_t)ghist[threadIdx.x] : 0, gx;
+    BS64(scan_tmp64).ExclusiveSum(g, gx);
+    if (threadIdx.x < 256) gbase[threadIdx.x] = gx;
+  }
+  for (int64_t t = blockIdx.x;; t += gridDim.x) {
+    // one-sweep tiles come from a ticket, so every look-back target is already running
+    if (st) {
+      if (threadIdx.x == 0) s_t = (int64_t)atomicAdd(ticket, 1u);
+      __syncthreads();
+      t = s_t;
+    }
+    if (t >= tiles) break;
     for (int i = threadIdx.x; i < kRxWarps * 256; i += kRxThreads) (&u.wcnt[0][0])[i] = 0;
     __syncthreads();
     const int64_t base = t * kRxTile + warp * 256;
@@ -780,7 +816,26 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
     }
     int32_t start;
     BS(scan_tmp).ExclusiveSum(tot, start);
-    if (off) {
+    if (st) {
+      if (threadIdx.x < 256) {  // publish this tile's digit count, then look back for the prefix
+        const int d = threadIdx.x;
+        volatile uint32_t* vs = st;
+        vs[t * 256 + d] = (t == 0 ? kRxInc : kRxAgg) | (uint32_t)tot;
+        uint32_t excl = 0;
+        if (t > 0) {
+          for (int64_t j = t - 1;; --j) {
+            uint32_t v;
+            do v = vs[j * 256 + d];
+            while ((v & ~kRxCount) == 0);
+            excl += v & kRxCount;
+            if (v & kRxInc) break;
+          }
+          vs[t * 256 + d] = kRxInc | (excl + (uint32_t)tot);
+        }
+        bstart[d] = start;
+        gofs[d] = gbase[d] + excl;
+      }
+    } else if (off) {
       if (threadIdx.x < 256) {
         bstart[threadIdx.x] = start;
         gofs[threadIdx.x] = off[(int64_t)threadIdx.x * tiles_b + t];
@@ -834,6 +889,10 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
   }
 }
 
+#ifndef OB_RX_ONESWEEP
+#define OB_RX_ONESWEEP 0  // measured: cfg2 p50 +2 % (look-back spins contend with the side stream), cfg1/cfg3 ±1 %
+#endif
+
 template <class K>
 static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int64_t m_bound, const RqKeyFmt& f) {
   cudaStream_t s = e.stream;
@@ -842,6 +901,34 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
   K* a = reinterpret_cast<K*>(c.keys);
   K* b = reinterpret_cast<K*>(c.keys2);
   const int passes = f.passes();
+  // OB_RX_ONESWEEP in the environment overrides the build default (read per sort;
+  // a captured request graph keeps the path it was captured with)
+  const char* os_env = std::getenv("OB_RX_ONESWEEP");
+  const bool onesweep = os_env ? std::atoi(os_env) != 0 : OB_RX_ONESWEEP != 0;
+  if (onesweep && c.rx_st && m_bound < (int64_t)kRxCount) {
+    // one sweep per pass: digit totals for every pass from one read, then each
+    // scatter tile publishes its digit counts and looks back for its offsets
+    uint32_t* st = c.rx_st;
+    uint32_t* ticket = st + 8 * 256 * tiles_b;
+    uint32_t* ghist = ticket + 8;
+    OB_CUDA(cudaMemsetAsync(st, 0, sizeof(uint32_t) * rx_st_words(m_bound), s));
+    k_rx_ghist<K><<<grid_for(m_bound, kRxThreads * 8, kNumSMs * 2), kRxThreads, 0, s>>>(a, m_dev, passes, ghist);
+    OB_LAUNCHED();
+    for (int p = 0; p < passes; ++p) {
+      const int shift = 8 * p;
+      uint32_t* sp = st + (int64_t)p * 256 * tiles_b;
+      if (p + 1 == passes) {
+        k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
+                                                        e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p);
+      } else {
+        k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
+                                                         e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p);
+        std::swap(a, b);
+      }
+      OB_LAUNCHED();
+    }
+    return;
+  }
   const bool fused = tiles_b <= 32;  // few tiles: offsets come straight from the counts
   const int64_t* off = fused ? nullptr : c.rx_off;
   for (int p = 0; p < passes; ++p) {
@@ -852,10 +939,10 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
       device_scan(s, e.scan, LoadI32{c.rx_cnt}, StoreI64{c.rx_off}, nullptr, 256 * tiles_b, 256 * tiles_b, nullptr);
     if (p + 1 == passes) {
       k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, off, c.rx_cnt, f,
-                                                      e.g.N, w.cand_ids, w.rc);
+                                                      e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr);
     } else {
       k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, off, c.rx_cnt, f,
-                                                       e.g.N, w.cand_ids, w.rc);
+                                                       e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr);
       std::swap(a, b);
     }
     OB_LAUNCHED();
