@@ -179,7 +179,52 @@ def ncu_traffic(cfg):
         return None
 
 
-def cpu_sample(serving, pe_layers, model, weights, pool, cfg, budget_s=12.0, batch=16):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def ref_gnnserve():
+    """The unmodified reference package (pip-installed into baseline/_ref), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "gnnserve")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import gnnserve.graphstore
+    import gnnserve.models
+    import gnnserve.runtime
+    import gnnserve.compgraph
+
+    return gnnserve
+
+
+def ref_sample(gn, serving, pe_layers, pool, cfg, budget_s=12.0, batch=16, max_requests=None, seed=777):
+    """The reference's own ServingEngine.serve (gnnserve, runtime.py:308-335) on bounded sub-batches of
+    the same workload: same graph, stored embeddings and weights (init_weights(seed=2), the reference's
+    own), requests drawn from the same hold-out pool by make_request."""
+    from paper_2501_08547_b200 import workload
+
+    n, avg, F, kind, k, H, B, gamma, _ = CONFIGS[cfg]
+    G, M, R, CG = gn.graphstore, gn.models, gn.runtime, gn.compgraph
+    ds = G.GraphDataset(serving.num_nodes, serving.in_offsets, serving.in_neighbors, serving.features,
+                        np.ones(serving.num_nodes, bool), np.zeros(serving.num_nodes, bool))
+    model = M.make_model(kind, k, F, H)
+    eng = R.ServingEngine(ds, G.PeStore(pe_layers), model, M.init_weights(model, 2),
+                          R.ServeConfig(strategy="srpe", gamma=gamma))
+    done, t_all, lat = 0, 0.0, []
+    while True:
+        r = workload.make_request(pool, serving, batch, seed=seed + done)
+        req = CG.ServingRequest(r.num_base, r.num_queries, r.query_features, r.edges)
+        t0 = time.perf_counter()
+        eng.serve(req)
+        dt = time.perf_counter() - t0
+        lat.append(dt * 1e3)
+        t_all += dt
+        done += 1
+        if t_all >= budget_s or (max_requests and done >= max_requests):
+            break
+    return batch * done / t_all, done, lat
+
+
+def port_sample(serving, pe_layers, model, weights, pool, cfg, budget_s=12.0, batch=16, seed=777):
     """The oracle (numpy/scipy port of the reference) on bounded sub-batches of the same workload."""
     from oracle import layers as OL
     from paper_2501_08547_b200 import workload
@@ -188,7 +233,7 @@ def cpu_sample(serving, pe_layers, model, weights, pool, cfg, budget_s=12.0, bat
     specs = [dict(kind=s.kind, in_dim=s.in_dim, out_dim=s.out_dim, p=s.p, n=s.n) for s in model.layers]
     done, q, t_all, lat = 0, 0, 0.0, []
     while True:
-        req = workload.make_request(pool, serving, batch, seed=777 + done)
+        req = workload.make_request(pool, serving, batch, seed=seed + done)
         t0 = time.perf_counter()
         OL.serve("srpe", specs, weights.layers, serving.num_nodes, batch, serving.in_offsets, serving.in_neighbors,
                  serving.features, req.query_features, req.edges, pe_layers=pe_layers, gamma=gamma)
@@ -202,8 +247,41 @@ def cpu_sample(serving, pe_layers, model, weights, pool, cfg, budget_s=12.0, bat
     return q / t_all, done, lat
 
 
+def parity_check(eng, serving, pe_layers, model, weights, req, gamma, k):
+    """One of the timed B-query requests through the public host API, checked against the oracle:
+    plan (ids, nq, totals, fp64 score bits, targets), every block array and the fetch bytes bit-exact,
+    embeddings by max|a-r|/max|r| (north_star bar 1e-4).  The oracle's wall time is the port's
+    full-batch CPU time (same request, same config)."""
+    from oracle import layers as OL
+
+    specs = [dict(kind=s.kind, in_dim=s.in_dim, out_dim=s.out_dim, p=s.p, n=s.n) for s in model.layers]
+    emb, bd = eng.serve(req)
+    t0 = time.perf_counter()
+    ref = OL.serve("srpe", specs, weights.layers, serving.num_nodes, req.num_queries, serving.in_offsets,
+                   serving.in_neighbors, serving.features, req.query_features, req.edges, pe_layers=pe_layers,
+                   gamma=gamma)
+    t_port = time.perf_counter() - t0
+    plan, rp = eng.last_plan(), ref["plan"]
+    eq = all(np.array_equal(plan[f], rp[f]) for f in ("ids", "nq", "total", "targets"))
+    eq = eq and np.array_equal(plan["scores"].view(np.uint64), rp["scores"].view(np.uint64))
+    fields = ("src_ids", "dst_ids", "edge_src", "edge_dst", "bind_kind", "bind_pe_layer", "src_degree",
+              "dst_self_src")
+    for l in range(1, k + 1):
+        got, exp = eng.last_block(l), ref["blocks"][l - 1]
+        for f in fields:
+            eq = eq and np.array_equal(np.asarray(getattr(got, f)).astype(np.int64),
+                                       np.asarray(getattr(exp, f)).astype(np.int64))
+    eq = eq and int(bd.fetch_bytes) == int(ref["fetch_bytes"])
+    err = OL.max_rel_err(emb, ref["emb"])
+    return {"request": "the first timed request (B=%d, m=%d)" % (req.num_queries, req.edges.shape[0]),
+            "structure_equal": bool(eq), "max_rel_err": float(err), "tolerance": 1e-4,
+            "checked": "candidates/nq/totals/score bits/targets, all 8 arrays of every block, fetch bytes; "
+                       "embeddings vs oracle (numpy/scipy fp64 restatement of gnnserve)"}, t_port
+
+
 def run_reference(args):
-    """--impl reference: the oracle port of the reference CPU path, rank 0 only."""
+    """--impl reference: the reference's own CPU path (gnnserve from baseline/_ref; the oracle port when
+    it is not installed), rank 0 only, all host cores numpy uses."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -213,26 +291,34 @@ def run_reference(args):
     n, avg, F, kind, k, H, B, gamma, desc = CONFIGS[cfg]
     if cfg in SYNTHETIC:
         print(json.dumps({"impl": "reference", "unavailable": f"{cfg}: the ~1.6B-edge graph exists only on the GPUs "
-                                                             "(generated per rank); the CPU port cannot hold it"}))
+                                                             "(generated per rank); the CPU reference cannot hold it"}))
         return
     serving, pool, _ = make_inputs(cfg, 0, 1, 0)
     model = models.make_model(kind, k, F, H)
     w = models.init_weights(model, 2)
     rng = np.random.default_rng(9)
-    # stored embeddings: value-independent for timing; fabricated as in SURVEY.md 6 (reference precompute
-    # would need E x F float64 temporaries)
+    # stored embeddings: value-independent for timing (the reference's precompute would need E x F float64
+    # temporaries), so fabricated N(0, 0.01) rows of the right shape
     pe = [rng.standard_normal((serving.num_nodes, H)).astype(np.float32) * 0.1 for _ in range(k - 1)]
     batch = args.ref_batch
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_sample(serving, pe, model, w, pool, cfg, budget_s=0.0, batch=batch)
-    qps, nreq, lat = [], 0, []
+    gn = ref_gnnserve()
+    if gn is not None:
+        kind_ = "reference"
+        what = "gnnserve.runtime.ServingEngine.serve (the unmodified reference, baseline/_ref)"
+        one = lambda i: ref_sample(gn, serving, pe, pool, cfg, budget_s=0.0, batch=batch, seed=777 + 100 * i)
+    else:
+        kind_ = "port"
+        what = "numpy/scipy port of the reference (oracle/); baseline/_ref not installed"
+        one = lambda i: port_sample(serving, pe, model, w, pool, cfg, budget_s=0.0, batch=batch, seed=777 + 100 * i)
+    for i in range(min(args.warmup, 1)):
+        one(1000 + i)
+    lat = []
     t_total, q_total = 0.0, 0
-    for _ in range(args.steps):
-        v, nr, l = cpu_sample(serving, pe, model, w, pool, cfg, budget_s=0.0, batch=batch)
+    for i in range(args.steps):
+        v, nr, l = one(i)
         lat += l
         t_total += sum(l) / 1e3
         q_total += batch * nr
-        nreq += nr
     value = q_total / t_total
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "queries/s",
@@ -240,9 +326,10 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "sample_batch": batch, "policy": "ratio", "gamma": gamma},
         "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
-        "cpu_baseline": {"value": round(value, 3), "unit": "queries/s", "cores": os.cpu_count(), "kind": "port",
+        "cpu_baseline": {"value": round(value, 3), "unit": "queries/s", "cores": os.cpu_count(), "kind": kind_,
                          "sample": f"{args.steps} requests of {batch} queries each (bounded sub-batches of the "
-                                   f"{cfg} workload; numpy/scipy port of the reference, oracle/)"},
+                                   f"{cfg} workload, same graph and weights, fabricated stored rows); {what}; "
+                                   f"numpy free to use every host core"},
         "e2e": {"value": round(value, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -536,15 +623,27 @@ def main():
                         "p50_ms": float(np.percentile(e2e_ms, 50)), "p99_ms": float(np.percentile(e2e_ms, 99))}}
 
     cpu = None
+    parity = None
     if synthetic:
         cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "port",
                "sample": f"none: the {cfg} graph exists only on the GPUs; see the cfg2 line for the CPU baseline"}
-    elif rank == 0 and world == 1 and not args.no_cpu and strategy == "srpe":
+    elif rank == 0 and world == 1 and not args.no_cpu and strategy == "srpe" and args.policy == "ratio":
         pe_host = [eng.read_pe(l) for l in range(1, k)]
-        qps, nr, cl = cpu_sample(serving, pe_host, model, w, pool, cfg, budget_s=12.0, batch=args.ref_batch)
-        cpu = {"value": round(qps, 3), "unit": "queries/s", "cores": 1, "kind": "port",
-               "sample": f"{nr} requests of {args.ref_batch} queries (bounded sub-batches of the {cfg} workload, "
-                         f"same graph/PE/weights; numpy+scipy port of the reference, oracle/)"}
+        # served with the throughput configuration still set (request lanes, source-range passes)
+        parity, t_port = parity_check(eng, serving, pe_host, model, w, reqs[args.warmup], gamma, k)
+        gn = ref_gnnserve()
+        port = {"value": round(B / t_port, 3), "unit": "queries/s", "cores": 1,
+                "sample": f"1 request of {B} queries (the parity request above: the bench config itself)"}
+        if gn is not None:
+            qps, nr, cl = ref_sample(gn, serving, pe_host, pool, cfg, budget_s=12.0, batch=args.ref_batch)
+            cpu = {"value": round(qps, 3), "unit": "queries/s", "cores": 1, "kind": "reference",
+                   "sample": f"{nr} requests of {args.ref_batch} queries (bounded sub-batches of the {cfg} workload, "
+                             f"same graph/stored rows/weights); gnnserve.runtime.ServingEngine.serve, the unmodified "
+                             f"reference from baseline/_ref; its hot loops (np.add.at, Python loops) are single-core",
+                   "port_full_batch": port}
+        else:
+            cpu = dict(port, kind="port")
+            cpu["sample"] += "; numpy/scipy port of the reference (oracle/), baseline/_ref not installed"
 
     hbm, tf, which = peaks()
     agg_gbs = agg["bytes"] / (agg["ms"] / 1e3) / 1e9 if agg["ms"] > 0 else 0.0
@@ -587,7 +686,7 @@ def main():
                                 "finalize": round(fin["ms"] / args.steps, 4),
                                 **{name: round(st[name]["ms"] / args.steps, 4) for name in st}},
         "gemm_tflops": round(gemm["flops"] / (gemm["ms"] / 1e3) / 1e12, 2) if gemm["ms"] > 0 else None,
-        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk_lanes or clk,
+        "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "clocks": clk_lanes or clk,
         "gpu_launches": int(launches_lanes if launches_lanes is not None else launches),
         "request": {"edges": int(reqs[0].edges.shape[0]), "candidates": int(bd0.num_candidates),
                     "targets": int(bd0.num_targets), "fetch_bytes": int(bd0.fetch_bytes),

@@ -51,6 +51,37 @@ Engine::~Engine() {
   if (csr_ev) cudaEventDestroy(csr_ev);
 }
 
+void Engine::invalidate_state() {
+  OB_CUDA(cudaDeviceSynchronize());
+  drop_graphs();
+  for (auto& L : lanes) {
+    for (auto& gr : L.graphs)
+      if (gr.exec) cudaGraphExecDestroy(gr.exec);
+    L.graphs.clear();
+  }
+  drop_ytab();
+}
+
+// release a layer's device buffers (weights replaced by ob_load_model)
+static void free_tc(Engine& e, TcWeights& t) {
+  e.dfree(t.hi);
+  e.dfree(t.lo);
+  t.hi = t.lo = nullptr;
+  for (auto n = t.next; n; n = n->next) {
+    e.dfree(n->hi);
+    e.dfree(n->lo);
+    n->hi = n->lo = nullptr;
+  }
+}
+static void free_layer(Engine& e, LayerDev& L) {
+  free_tc(e, L.tw_main);
+  free_tc(e, L.tw_self);
+  e.dfree(L.a_src);
+  e.dfree(L.a_dst);
+  e.dfree(L.wa_dst);
+  L.a_src = L.a_dst = L.wa_dst = nullptr;
+}
+
 // swap a lane's request state with the engine's current one (lane 0 lives in the engine)
 static void swap_lane(Engine& e, Lane& L) {
   std::swap(e.ws, L.ws);
@@ -315,7 +346,7 @@ static void raise_request_errors(const ReqCounters& rc) {
   if (rc.err & kErrNoQuery) throw Error(OB_EINVAL, "every request edge needs a query endpoint");
   if (rc.err & kErrNonFinite) throw Error(OB_EINVAL, "query features must be finite");
   if (rc.err & kErrZeroTotal) throw Error(OB_EINVAL, "candidate with zero total degree");
-  if (rc.err & kErrComm) throw Error(OB_ECOMM, "CGP exchange: a peer rank did not signal within 2 s");
+  if (rc.err & kErrComm) throw Error(OB_ECOMM, "CGP exchange: a peer rank did not signal in time (OB_CGP_TIMEOUT_MS)");
 }
 
 // fetch-byte accounting per layer (graph_fetch_bytes, runtime.py:105-120)
@@ -489,6 +520,8 @@ static std::vector<BlockDev*> counted_blocks(Engine& e) {
 // The request pipeline, enqueued on the engine stream.  Inputs/outputs are device pointers.
 static void enqueue_serve(Engine& e, int B, const float* d_q, int64_t m, const int64_t* d_edges, float* d_out) {
   check_ready(e);
+  OB_CHECK(!e.comm_failed, OB_ECOMM,
+           "a CGP exchange timed out on an earlier request: the exchange state is unusable, recreate the engines");
   OB_CHECK(B >= 0 && m >= 0, OB_EINVAL, "negative request size");
   OB_CHECK(e.g.N + B < ((int64_t)1 << 31) - 1, OB_EINVAL, "id space exceeds int32");
   cgp_localize_storage(e);  // NCCL CGP: keep only the owned rows (no-op otherwise)
@@ -537,6 +570,7 @@ static void finish_breakdown(Engine& e, const ReqCounters& rc, const std::vector
   const bool cgp = e.cfg.strategy == OB_STRATEGY_SRPE_CGP;
   std::vector<BlockDev*> all = counted_blocks(e);
   for (size_t i = 0; i < all.size() && i < hc.size(); ++i) all[i]->host = hc[i];
+  if (rc.err & kErrComm) e.comm_failed = true;  // sticky: the exchange state is skewed
   raise_request_errors(rc);
   if (!bd) return;
   // graph_fetch_bytes per block set (runtime.py:105-120; CGP: _shard_fetch_bytes summed, :224-247)
@@ -691,6 +725,7 @@ static void load_model(Engine& e, int k, const ob_layer* layers, const float* co
     }
     mi += nmats(sp.kind);
   }
+  for (auto& L : e.layers) free_layer(e, L);  // the old weights (no request can still use them)
   e.layers = out;
 }
 
@@ -737,6 +772,13 @@ struct PipeSlot {
   int64_t ticket = -1;
   int64_t h2d_bytes = 0, d2h_bytes = 0;
   int64_t collective_bytes = 0;
+  // pageable `out`: the rows come back into this pinned buffer and are copied
+  // to the caller's array in ob_serve_wait (a D2H copy into pageable memory
+  // would block the submit until the request finished on the device)
+  float* h_out = nullptr;
+  size_t cap_h_out = 0;
+  float* user_out = nullptr;
+  size_t out_bytes = 0;
 };
 constexpr int kMaxCounted = 64;
 constexpr int kPipeSlots = 4;  // requests in flight on the pipelined host path
@@ -861,6 +903,7 @@ int ob_engine_destroy(ob_engine* h) {
       if (sl.d_out) cudaFree(sl.d_out);
       if (sl.h_rc) cudaFreeHost(sl.h_rc);
       if (sl.h_bc) cudaFreeHost(sl.h_bc);
+      if (sl.h_out) cudaFreeHost(sl.h_out);
       for (cudaEvent_t ev : {sl.h2d_done, sl.start, sl.comp_done, sl.d2h_done})
         if (ev) cudaEventDestroy(ev);
     }
@@ -876,7 +919,7 @@ int ob_load_graph(ob_engine* h, int64_t N, const int64_t* off, const int64_t* nb
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
-    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
+    h->impl.invalidate_state();  // graphs and stored tables follow the weights, features and PE
     load_graph(h->impl, N, off, nb, E, feats, F);
     if (h->impl.cfg.strategy == OB_STRATEGY_SRPE_CGP) cgp_build_partitions(h->impl);
   });
@@ -887,7 +930,7 @@ int ob_generate_graph(ob_engine* h, int64_t N, double avg_degree, double exponen
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
-    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
+    h->impl.invalidate_state();  // graphs and stored tables follow the weights, features and PE
     generate_graph(h->impl, N, avg_degree, exponent, F, seed);
   });
 }
@@ -897,7 +940,7 @@ int ob_generate_pe(ob_engine* h, int32_t layer, int32_t dim, uint64_t seed) {
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
-    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
+    h->impl.invalidate_state();  // graphs and stored tables follow the weights, features and PE
     generate_pe(h->impl, layer, dim, seed);
   });
 }
@@ -982,7 +1025,7 @@ int ob_load_pe(ob_engine* h, int32_t layer, const float* rows, int64_t n, int32_
     std::lock_guard<std::mutex> lk(h->mu);
     Engine& e = h->impl;
     OB_CUDA(cudaSetDevice(e.cfg.device));
-    e.drop_ytab();  // stored transforms follow the weights, features and PE
+    e.invalidate_state();  // graphs and stored tables follow the weights, features and PE
     OB_CHECK(e.g.N > 0, OB_ESTATE, "load the graph before stored embeddings");
     OB_CHECK(layer >= 1 && layer <= 7, OB_EINVAL, "bad stored-embedding layer");
     OB_CHECK(n == e.g.N, OB_EINVAL, "stored embeddings must cover every node");
@@ -1009,7 +1052,7 @@ int ob_load_model(ob_engine* h, int32_t k, const ob_layer* layers, const float* 
     OB_CHECK(h && layers && mats, OB_EINVAL, "null argument");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
-    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
+    h->impl.invalidate_state();  // graphs and stored tables follow the weights, features and PE
     load_model(h->impl, k, layers, mats);
   });
 }
@@ -1019,7 +1062,7 @@ int ob_precompute_pe(ob_engine* h) {
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
     OB_CUDA(cudaSetDevice(h->impl.cfg.device));
-    h->impl.drop_ytab();  // stored transforms follow the weights, features and PE
+    h->impl.invalidate_state();  // graphs and stored tables follow the weights, features and PE
     OB_CHECK(!h->impl.layers.empty(), OB_ESTATE, "load a model first");
     OB_CHECK(h->impl.layers[0].spec.in_dim == h->impl.g.F, OB_EINVAL, "input width does not match layer in_dim");
     OB_CHECK(h->impl.g.offsets && !h->impl.g.pos, OB_ESTATE,
@@ -1073,12 +1116,14 @@ int ob_serve(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* 
   });
 }
 
-// Pipelined host path.  Request t uses slot t % 2: its H2D copy runs on the h2d
-// stream (after slot t's previous request finished on the device), its request
-// graph on the engine stream (after the copy and after the slot's previous D2H),
-// its D2H copy and counter readback on the d2h stream.  Up to two requests are
-// outstanding; ob_serve_wait(t) returns request t's rows in `out` and its
-// breakdown (errors of request t are raised there).
+// Pipelined host path.  Request t uses slot t % kPipeSlots (four slots): its
+// H2D copy runs on the h2d stream (after slot t's previous request finished on
+// the device), its request graph on its request lane's stream (after the copy
+// and after the slot's previous D2H), its D2H copy and counter readback on the
+// d2h stream.  Up to kPipeSlots requests are outstanding; ob_serve_wait(t)
+// returns request t's rows in `out` and its breakdown (errors of request t are
+// raised there).  The D2H into `out` overlaps only when `out` is pinned
+// (page-locked) host memory; a pageable `out` makes the submit wait for it.
 int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* edges, float* out,
                     int64_t* ticket) {
   return guarded([&] {
@@ -1125,7 +1170,21 @@ int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const in
       OB_CUDA(cudaMemcpyAsync(sl.h_bc + i, all[i]->cnt, sizeof(BlockCounters), cudaMemcpyDeviceToHost, s));
     OB_CUDA(cudaEventRecord(sl.comp_done, s));
     OB_CUDA(cudaStreamWaitEvent(h->d2h, sl.comp_done, 0));
-    if ((int64_t)B * H) OB_CUDA(cudaMemcpyAsync(out, sl.d_out, sizeof(float) * B * H, cudaMemcpyDeviceToHost, h->d2h));
+    // pinned (page-locked or registered) `out` takes the copy directly, pageable goes through h_out
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    sl.out_bytes = sizeof(float) * (size_t)B * H;
+    sl.user_out = pinned ? nullptr : out;
+    if (!pinned && sl.out_bytes > sl.cap_h_out) {
+      if (sl.h_out) OB_CUDA(cudaFreeHost(sl.h_out));
+      sl.h_out = nullptr;
+      sl.cap_h_out = 0;
+      OB_CUDA(cudaMallocHost(&sl.h_out, sl.out_bytes));
+      sl.cap_h_out = sl.out_bytes;
+    }
+    if (sl.out_bytes)
+      OB_CUDA(cudaMemcpyAsync(pinned ? out : sl.h_out, sl.d_out, sl.out_bytes, cudaMemcpyDeviceToHost, h->d2h));
     OB_CUDA(cudaEventRecord(sl.d2h_done, h->d2h));
     sl.n_bc = (int)all.size();
     sl.busy = true;
@@ -1150,6 +1209,7 @@ int ob_serve_wait(ob_engine* h, int64_t ticket, ob_breakdown* bd) {
     // the next slot's request keeps running; only this one's D2H is awaited
     OB_CUDA(cudaEventSynchronize(sl.d2h_done));
     sl.busy = false;
+    if (sl.user_out && sl.out_bytes) std::memcpy(sl.user_out, sl.h_out, sl.out_bytes);
     OB_CUDA(cudaGetLastError());
     float ms = 0;
     OB_CUDA(cudaEventElapsedTime(&ms, sl.start, sl.comp_done));

@@ -15,11 +15,13 @@
 // slice) with the same device builder as the centralized path, aggregates
 // locally into one raw partial per destination (sum / max / softmax triple), and
 // the partials are combined across ranks:
-//   * NCCL mode (one process per GPU, ob_config.nccl_id): ncclAllReduce over
-//     NVLink/NVSwitch on destination-indexed buffers padded to the request bound
-//     (sum; max for sage_max; max-then-rescaled-sum for the softmax triple), so no
-//     host-side sizes are needed; owners then update their destinations and the
-//     query rows reduce to rank 0;
+//   * NCCL mode (one process per GPU, ob_config.nccl_id): by default every
+//     rank writes its partial rows into its own CUDA-IPC exchange region and the
+//     owners read the peers' regions in place over NVLink ("NVLink exchange"
+//     below: device step counters, release/acquire flags, owner-only merges);
+//     OB_CGP_NCCL=1 selects ncclAllReduce on destination-indexed buffers padded
+//     to the request bound instead; owners then update their destinations and
+//     the query rows go to rank 0;
 //   * emulation (nccl_id == NULL, P > 1): all P partitions run on this device and
 //     the merge walks the P partials in ascending rank order (cgpexec.py:189-240).
 #include <algorithm>
@@ -367,15 +369,21 @@ void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
 //   consumer   kernels read peers' regions with ld.global.cg over NVLink
 //   x_done     done[me] = k at every peer
 // The step counter lives on the device, so a replayed CUDA graph keeps
-// counting; spins give up after ~2 s and raise OB_ECOMM instead of hanging.
+// counting; spins give up after OB_CGP_TIMEOUT_MS (default 2 s of %globaltimer
+// wall time) and raise OB_ECOMM instead of hanging.  The failure is sticky: the
+// lane's failure word skips every later step and the timed-out rank poisons its
+// peers' flags, so no rank carries on with a skewed step counter.
 // ---------------------------------------------------------------------------
 struct XCtx {
   char* peer[kMaxParts];
   int P, rank;
   int64_t* ep;
   int64_t* err;     // the request's error word (kErrComm on a flag timeout)
+  int64_t* sticky;  // the lane's persistent failure word: once set, every later step is skipped
+  int64_t timeout_ns;
 };
-constexpr size_t kXFlags = 256;  // ready[8] @0, done[8] @64
+constexpr size_t kXFlags = 256;   // ready[8] @0, done[8] @64, poison @128
+constexpr size_t kXPoison = 128;  // set by a peer that timed out: this exchange is unusable
 
 __device__ __forceinline__ int64_t ld_acq_sys(const int64_t* p) {
   int64_t v;
@@ -385,22 +393,45 @@ __device__ __forceinline__ int64_t ld_acq_sys(const int64_t* p) {
 __device__ __forceinline__ void st_rel_sys(int64_t* p, int64_t v) {
   asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void spin_geq(const int64_t* f, int64_t k, int64_t* err) {
-  const long long t0 = clock64();
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// the exchange failed earlier (this lane timed out, or a peer poisoned our flags)
+__device__ __forceinline__ bool x_failed(const XCtx& x) {
+  return *reinterpret_cast<volatile int64_t*>(x.sticky) != 0 ||
+         ld_acq_sys(reinterpret_cast<const int64_t*>(x.peer[x.rank] + kXPoison)) != 0;
+}
+// Sticky failure: flag this request, remember it for the lane and poison every
+// peer's flags so their spins end with kErrComm too instead of reading regions
+// this rank may overwrite (no rank proceeds on a skewed step counter silently)
+__device__ __noinline__ void x_fail(const XCtx& x) {
+  atomicOr((unsigned long long*)x.err, (unsigned long long)kErrComm);
+  atomicExch((unsigned long long*)x.sticky, 1ull);
+  for (int q = 0; q < x.P; ++q)
+    if (q != x.rank) st_rel_sys(reinterpret_cast<int64_t*>(x.peer[q] + kXPoison), 1);
+}
+__device__ __forceinline__ void spin_geq(const XCtx& x, const int64_t* f, int64_t k) {
+  const uint64_t t0 = globaltimer_ns();
   while (ld_acq_sys(f) < k) {
-    if (clock64() - t0 > (1ll << 32)) {  // ~2 s at 1.9 GHz: a peer is gone
-      atomicOr((unsigned long long*)err, (unsigned long long)kErrComm);
+    if (x_failed(x) || globaltimer_ns() - t0 > (uint64_t)x.timeout_ns) {  // a peer is gone
+      x_fail(x);
       return;
     }
-    __nanosleep(64);
+    __nanosleep(256);
   }
 }
 
 __global__ void k_x_begin(XCtx x) {  // peers done with the previous step
   const int q = threadIdx.x;
   if (q >= x.P || q == x.rank) return;
+  if (x_failed(x)) {
+    atomicOr((unsigned long long*)x.err, (unsigned long long)kErrComm);
+    return;
+  }
   const int64_t k = *x.ep;
-  if (k > 0) spin_geq(reinterpret_cast<const int64_t*>(x.peer[x.rank] + 64) + q, k, x.err);
+  if (k > 0) spin_geq(x, reinterpret_cast<const int64_t*>(x.peer[x.rank] + 64) + q, k);
 }
 __global__ void k_x_publish(XCtx x) {
   __threadfence_system();
@@ -413,7 +444,11 @@ __global__ void k_x_publish(XCtx x) {
 __global__ void k_x_wait(XCtx x) {
   const int p = threadIdx.x;
   if (p >= x.P || p == x.rank) return;
-  spin_geq(reinterpret_cast<const int64_t*>(x.peer[x.rank]) + p, *x.ep, x.err);
+  if (x_failed(x)) {
+    atomicOr((unsigned long long*)x.err, (unsigned long long)kErrComm);
+    return;
+  }
+  spin_geq(x, reinterpret_cast<const int64_t*>(x.peer[x.rank]) + p, *x.ep);
 }
 __global__ void k_x_done(XCtx x) {
   const int q = threadIdx.x;
@@ -444,6 +479,8 @@ static XCtx xctx(Engine& e) {
   x.rank = c.my_rank;
   x.ep = c.xep;
   x.err = &e.ws.rc->err;
+  x.sticky = c.xerr;
+  x.timeout_ns = c.x_timeout_ns;
   return x;
 }
 static void x_launch(cudaStream_t s, void (*kern)(XCtx), const XCtx& x) {
@@ -806,6 +843,10 @@ void cgp_init_comm(Engine& e) {
   // the padded ncclAllReduce path
   const char* v = std::getenv("OB_CGP_NCCL");
   e.cgp.p2p = !(v && v[0] && v[0] != '0') && e.cfg.num_partitions <= kMaxParts;
+  // flag-wait timeout of the NVLink exchange (wall time, %globaltimer)
+  const char* t = std::getenv("OB_CGP_TIMEOUT_MS");
+  const double ms = t && t[0] ? std::atof(t) : 2000.0;
+  e.cgp.x_timeout_ns = (int64_t)(std::max(ms, 1.0) * 1e6);
 #else
   throw Error(OB_ECOMM, "built without NCCL");
 #endif

@@ -593,7 +593,7 @@ struct CgpLaneState {
   size_t x_need_region = 0;     // this plan's region bytes (carve_cgp)
   char* xpeer[kMaxParts] = {};  // every rank's buffer in this address space (own = xbuf)
   int64_t* xep = nullptr;       // device step counter
-  int64_t* xerr = nullptr;      // device error word (flag wait timeouts)
+  int64_t* xerr = nullptr;      // device failure word of this lane's exchange (sticky after a timeout)
   int64_t nvlink_bytes = 0;     // per request, real-row bytes read from peers (host estimate)
 };
 
@@ -605,6 +605,7 @@ struct CgpState : CgpLaneState {
   int32_t* owner = nullptr;   // [N]
   std::vector<PartitionDev> parts;  // emulation: all P; NCCL: this rank's
   bool p2p = false;             // use the exchange (else padded ncclAllReduce)
+  int64_t x_timeout_ns = 2000000000;  // flag-wait timeout of the exchange (OB_CGP_TIMEOUT_MS)
 };
 
 // release the current lane's exchange buffers (barrier with every peer first)
@@ -734,6 +735,11 @@ struct Engine {
       if (gr.exec) cudaGraphExecDestroy(gr.exec);
     graphs.clear();
   }
+  // A state change (graph, features, stored embeddings, weights) frees or
+  // replaces buffers that captured request graphs and the stored tables point
+  // at: wait for every in-flight request on every lane, then drop the graphs
+  // of every lane and the derived tables (ob_api.cu)
+  void invalidate_state();
   std::vector<void*> owned;      // device allocations to free
   void* dalloc(size_t bytes) {
     void* p = nullptr;
@@ -751,6 +757,7 @@ struct Engine {
         return;
       }
   }
+  bool comm_failed = false;  // a CGP exchange timed out: the engine refuses further requests
   bool localized = false;  // NCCL-mode CGP storage reduced to the owned rows
   // request lanes beyond lane 0 (ob_set_lanes); lane_rr round-robins device serves
   std::vector<Lane> lanes;

@@ -1440,6 +1440,7 @@ void stage_precompute(Engine& e) {
     const BlockStore3 bst{nullptr, item_ptr, group_ptr};
     device_scan_t<I3>(s, sc_scan, OffsetsLoad3{e.g.offsets}, bst, BlockTotal3{bst, cnt}, nullptr, N, N);
     expand_items(s, cnt, N, item_ptr, group_ptr, item_dst, group_dst);
+    for (float* t : e.pe) e.dfree(t);  // replaced below
     e.pe.assign(k - 1, nullptr);
     e.pe_dim.assign(k - 1, 0);
     const float* h = e.g.feats;

@@ -124,6 +124,11 @@ class ServingEngine:
 
     def __init__(self, dataset: GraphDataset, pe: PeStore | None, model: ModelSpec, weights: Weights,
                  config: ServeConfig, stream: int = 0, nccl_id: bytes | None = None, rank: int = 0):
+        """runtime.py:258-288.  The arguments are duck-typed: the reference's own ``GraphDataset``,
+        ``PeStore``, ``ModelSpec``, ``Weights`` and ``ServeConfig`` objects are accepted unchanged
+        (tests/test_gpu_dropin.py), as are this package's mirrors of them."""
+        if config.strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {config.strategy!r}")
         if config.strategy == "sampled":  # build_sampled (compgraph.py:248-284)
             fan = [int(f) for f in config.fanouts]
             if any(f < 1 for f in fan):
@@ -134,14 +139,15 @@ class ServingEngine:
                 raise ValueError(f"fanouts above {nat.MAX_FANOUT} are not supported on the device")
         if config.policy not in nat.POLICY:
             raise ValueError(f"policy {config.policy!r} is not on the device path (ratio and is)")
-        if config.cache_bytes:
+        if getattr(config, "cache_bytes", 0):
             raise ValueError("feature caches are subsumed by HBM residency; use cache_bytes=0")
         self.dataset = dataset
         self.pe = pe
         self.model = model
         self.weights = weights
         self.config = config
-        cfg = nat.ObConfig(device=config.device, strategy=nat.STRATEGY[config.strategy], gamma=float(config.gamma),
+        device = int(getattr(config, "device", 0))  # gnnserve's own ServeConfig has no device field
+        cfg = nat.ObConfig(device=device, strategy=nat.STRATEGY[config.strategy], gamma=float(config.gamma),
                            policy=nat.POLICY[config.policy], num_partitions=int(config.num_partitions),
                            rank=int(rank), seed=int(config.seed) & 0xFFFFFFFFFFFFFFFF, stream=int(stream),
                            nccl_id=None)
@@ -177,6 +183,10 @@ class ServingEngine:
             feats = _f32(ds.features)
             nat.check(self._lib.ob_load_graph(self._h, int(ds.num_nodes), nat.ptr(off), nat.ptr(nb),
                                               int(nb.shape[0]), nat.ptr(feats), int(feats.shape[1])))
+        self._load_model(model, weights)
+        self._load_pe(pe)
+
+    def _load_model(self, model, weights):
         layers = (nat.ObLayer * model.k)()
         mats = []
         for i, spec in enumerate(model.layers):
@@ -185,6 +195,8 @@ class ServingEngine:
                 mats.append(_f32(weights.layers[i][name]))
         arr = (C.c_void_p * len(mats))(*[m.ctypes.data for m in mats])
         nat.check(self._lib.ob_load_model(self._h, model.k, layers, arr))
+
+    def _load_pe(self, pe):
         if isinstance(pe, SyntheticPe):
             for l, dim in enumerate(pe.dims, start=1):
                 nat.check(self._lib.ob_generate_pe(self._h, l, int(dim), int(pe.seed) + l))
@@ -194,6 +206,21 @@ class ServingEngine:
             for l in range(1, pe.num_layers + 1):
                 rows = _f32(pe.layers[l - 1])
                 nat.check(self._lib.ob_load_pe(self._h, l, nat.ptr(rows), int(rows.shape[0]), int(rows.shape[1])))
+
+    def reload(self, model=None, weights=None, pe=None) -> None:
+        """Replace the weights (model + weights) and/or the stored embeddings in place.
+
+        Captured request graphs and the derived stored tables are dropped (after every in-flight
+        request finished) and rebuilt on the next request, so later serves equal a fresh engine's.
+        """
+        if (model is None) != (weights is None):
+            raise ValueError("reload the model and its weights together")
+        if model is not None:
+            self._load_model(model, weights)
+            self.model, self.weights = model, weights
+        if pe is not None:
+            self._load_pe(pe)
+            self.pe = pe
 
     def precompute_pe(self) -> None:
         """GPU precompute_embeddings into HBM (graphstore.py:330-365)."""
