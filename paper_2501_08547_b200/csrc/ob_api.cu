@@ -266,6 +266,7 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.qself = wide ? a.take<float>((int64_t)(B + 1) * wl) : nullptr;
   w.dyn_src = wide ? a.take<int32_t>(Smax) : nullptr;
   w.ndyn = wide ? a.take<int64_t>(1) : nullptr;
+  w.delta = (!khop(e.cfg) && k >= 3) ? a.take<float>(p.blocks[0].D_max * wl) : nullptr;
   w.s_src = gat ? a.take<float>(Smax) : nullptr;
   w.s_dst = gat ? a.take<float>(Dmax) : nullptr;
   for (int l = 1; l < k; ++l) {
@@ -1487,7 +1488,11 @@ int ob_profile_read(ob_engine* h, int32_t cls, double* total_ms, int64_t* launch
       ++n;
       if (r.slot < 0) continue;
       const BlockCounters& c = e.prof.pinned[r.slot];
-      if (cls == kProfAgg && r.K < 0) {
+      if (cls == kProfAgg && r.K == -2) {
+        // delta launch: edge list, the recomputed rows it gathers (at most the D block rows) and
+        // the partials
+        by += 4.0 * c.E + 4.0 * r.width * c.D + 4.0 * r.pw * c.items;
+      } else if (cls == kProfAgg && r.K < 0) {
         // stored-aggregate launch: rows gathered for the request spans only (not sized by the
         // block counters) -- count the edge list and the partials, no rows (conservative)
         by += 4.0 * c.E + 4.0 * r.pw * c.items;

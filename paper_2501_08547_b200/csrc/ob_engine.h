@@ -307,6 +307,7 @@ struct RequestWs {
   float* s_src = nullptr;          // gat: [S_max]
   float* s_dst = nullptr;          // gat: [D_max]
   float* mean = nullptr;           // moments: [D_max][in]
+  float* delta = nullptr;          // [D_max][ld] delta rows h - PE of the targets (mid-block layers >= 2)
   int64_t words_N = 0, words_NB = 0;
   BuildScratch bs[2];
 };
@@ -394,6 +395,12 @@ struct LayerRun {
   const int64_t* ndyn = nullptr;
   int64_t dyn_max = 0;
   // stored aggregates (layer 1 of sum kinds): static CSR-part sums per training node
+  // (delta mode, srpe mid-block layers >= 2: the stored rows' CSR-part sums; the
+  // gather then visits only recomputed CSR sources, as (h - PE) delta rows)
+  bool delta = false;
+  const float* dprev = nullptr;  // previous layer's rows [T targets | B queries]
+  const int64_t* dT = nullptr;   // device T
+  const float* dbuf = nullptr;   // delta rows h - PE of the T targets (same row index)
   const float* stat = nullptr;
   int64_t stat_ld = 0;
   const int32_t* dst_ids = nullptr;
@@ -706,8 +713,13 @@ struct Engine {
   // IS policy: per-node numerators of the whole CSR (centralized) or of each
   // local partition's source-split CSR (CGP), computed once per graph
   std::vector<double*> is_tab;
+  // delta aggregates (srpe mid-block layers l >= 2 of sum kinds): sagg_l[l-1][v] =
+  // sum_{u in N(v)} w_u PE_{l-1}(u), raw, unnormalised; null where unused
+  std::vector<float*> sagg_l;
   bool ytab_ready = false;
   void drop_ytab() {
+    for (float* t : sagg_l) dfree(t);
+    sagg_l.clear();
     for (float* t : ytab) dfree(t);
     ytab.clear();
     dfree(sagg1);

@@ -151,6 +151,13 @@ struct AggArgs {
   const int32_t* skip_dst_ids = nullptr;
   const int32_t* skip_indeg = nullptr;
   int64_t skip_N = 0;
+  // delta mode (skip_dst_ids set too): CSR-part edges are kept only when their row
+  // lies in dprev[0, T) (a recomputed target) and then read from the delta row at
+  // the same index (dbuf); the request suffix is gathered as is
+  const float* dprev = nullptr;
+  const int64_t* dT = nullptr;
+  const float* dbuf = nullptr;
+  int64_t dld = 0;
   // source-range pass (sum): only sources [src_lo, src_hi) of each row (a row's
   // sources are ascending, so that is a contiguous run of every 32-edge group);
   // accumulate adds to the partials of the previous pass
@@ -176,14 +183,24 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
     src_lo = (int32_t)(S * a.pass / a.passes);
     src_hi = a.pass + 1 == a.passes ? 0x7fffffff : (int32_t)(S * (a.pass + 1) / a.passes);
   }
+  // delta mode: recomputed rows are prev[0, T); their delta rows sit at the same offset in dbuf
+  const float* d_lo = a.dprev;
+  const float* d_hi = a.dprev ? a.dprev + (*a.dT) * a.dld : nullptr;
+  const ptrdiff_t d_shift = a.dprev ? a.dbuf - a.dprev : 0;
+  __shared__ const float* c_row[kAggWarps][32];  // delta mode: the group's kept edges, compacted
+  __shared__ float c_w[kAggWarps][32];
+  const int wib = threadIdx.x >> 5;
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = __ldg(a.item_dst + it);
     const int64_t j = it - a.item_ptr[i];
     int64_t e0 = a.dst_ptr[i] + j * kAggChunk;
     const int64_t e1 = min(e0 + kAggChunk, a.dst_ptr[i + 1]);
+    int64_t csr_end = e0;  // delta mode: edges below this are the destination's CSR part
     if (a.skip_indeg) {
       const int64_t v = __ldg(a.skip_dst_ids + i);
-      if (v < a.skip_N) e0 = max(e0, a.dst_ptr[i] + (int64_t)__ldg(a.skip_indeg + v));
+      const int64_t ce = v < a.skip_N ? a.dst_ptr[i] + (int64_t)__ldg(a.skip_indeg + v) : a.dst_ptr[i];
+      if (d_lo) csr_end = ce;
+      else e0 = max(e0, ce);
     }
     AT acc[NV][4];
     float m_run = -INFINITY, den = 0.f;
@@ -196,8 +213,12 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
       // lane-cooperative edge fetch, then broadcast
       const int64_t my = eb + lane;
       const int32_t s_l = my < e1 ? a.edge_src[my] : 0;
-      const bool in_l = my < e1 && s_l >= src_lo && s_l < src_hi;
+      bool in_l = my < e1 && s_l >= src_lo && s_l < src_hi;
       const float* r_l = in_l ? a.x.row(s_l) : nullptr;
+      if (d_lo && in_l && my < csr_end) {  // CSR part: recomputed sources only, as delta rows
+        in_l = r_l >= d_lo && r_l < d_hi;
+        r_l += d_shift;
+      }
       float w_l = 1.f;
       if (in_l) {
         if (OP == kOpSum && a.gscale) w_l = a.gscale[s_l];
@@ -206,11 +227,24 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
           w_l = lg >= 0.f ? lg : 0.2f * lg;  // leaky_relu(0.2)
         }
       }
-      // the group's in-range edges are contiguous (ascending sources): [first, first + cnt)
+      // the group's in-range edges are contiguous (ascending sources): [first, first + cnt);
+      // in delta mode they are compacted through shared memory first (same edge order)
       const unsigned inb = __ballot_sync(0xffffffffu, in_l);
       if (!inb) continue;
-      const int first = __ffs(inb) - 1;
+      int first = __ffs(inb) - 1;
       const int cnt = __popc(inb);
+      if (d_lo) {
+        if (in_l) {
+          const int slot = __popc(inb & ((1u << lane) - 1u));
+          c_row[wib][slot] = r_l;
+          c_w[wib][slot] = w_l;
+        }
+        __syncwarp();
+        r_l = c_row[wib][lane];
+        w_l = c_w[wib][lane];
+        __syncwarp();
+        first = 0;
+      }
       for (int u = 0; u < cnt; u += kU) {
         float4 v[kU][NV];
         float wg[kU];
@@ -526,7 +560,7 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
   const int nv = a0.width <= 128 ? 1 : (a0.width <= 256 ? 2 : 4);
   dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a0.width + 128 * nv - 1) / (128 * nv));
   int passes = 1;
-  if (OP == kOpSum && S_max > 0 && !a0.skip_indeg) {
+  if (OP == kOpSum && S_max > 0 && !a0.skip_indeg && !a0.dprev) {
     const int64_t rows_bytes = S_max * (int64_t)ld4(a0.width) * 4;
     passes = (int)std::min<int64_t>(4, (rows_bytes + kAggPassBytes - 1) / kAggPassBytes);
     if (passes < 1) passes = 1;
@@ -543,7 +577,8 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
   }
   // K = -1 marks a stored-aggregate launch: it gathers only the request spans, which the
   // block counters do not size, so the profiler counts its edge list and partials only
-  prof_end(s, pa, kProfAgg, a0.cnt, a0.width, a0.pw, a0.skip_indeg ? -1 : 0, 0, 0);
+  // (K = -2: delta launch -- edge list, the recomputed rows (<= D) and the partials)
+  prof_end(s, pa, kProfAgg, a0.cnt, a0.width, a0.pw, a0.dprev ? -2 : (a0.skip_indeg ? -1 : 0), 0, 0);
 }
 
 static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t items_max) {
@@ -636,6 +671,12 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     a.skip_dst_ids = r.dst_ids;
     a.skip_indeg = r.indeg;
     a.skip_N = r.N;
+    if (r.delta) {
+      a.dprev = r.dprev;
+      a.dT = r.dT;
+      a.dbuf = r.dbuf;
+      a.dld = ld4(in);
+    }
     f.stat = r.stat;
     f.stat_ld = r.stat_ld;
     f.stat_dst_ids = r.dst_ids;
@@ -1096,6 +1137,17 @@ __global__ void k_pad_rows(const ReqParams* rp, int64_t rows, int w, float* dst,
   }
 }
 
+// delta rows of the recomputed targets: dbuf[t] = prev[t] - PE[targets[t]] (t < T)
+__global__ void k_delta_rows(const int64_t* T_dev, const int32_t* __restrict__ targets, const float* __restrict__ prev,
+                             const float* __restrict__ pe, int64_t ld, float* dbuf) {
+  const int64_t n = (*T_dev) * ld;
+  OB_GRID_STRIDE(t, n) {
+    const int64_t i = t / ld;
+    const int64_t c = t - i * ld;
+    dbuf[t] = prev[t] - pe[(int64_t)targets[i] * ld + c];
+  }
+}
+
 void stage_forward(Engine& e, RequestWs& w, float* d_out) {
   cudaStream_t s = e.stream;
   const int k = (int)e.layers.size();
@@ -1138,6 +1190,22 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       r.B_dev = &w.blocks[(int)w.blocks.size() - 1].cnt->D;  // the query block: D = B
       r.B = w.B;
       if (w.qrows_ready) r.self_q = w.qself;
+    }
+    if (l > 1 && l < k && (int)e.sagg_l.size() >= l && e.sagg_l[l - 1] && w.delta) {
+      // delta aggregates: static CSR-part sums of the stored rows + (h - PE) of recomputed sources
+      const int64_t ld = ld4(L.spec.in_dim);
+      k_delta_rows<<<grid_for(b.D_max * ld, 256), 256, 0, s>>>(&w.rc->T, w.targets, w.outs[l - 1], e.pe[l - 2], ld,
+                                                                 w.delta);
+      OB_LAUNCHED();
+      r.delta = true;
+      r.dprev = w.outs[l - 1];
+      r.dT = &w.rc->T;
+      r.dbuf = w.delta;
+      r.stat = e.sagg_l[l - 1];
+      r.stat_ld = ld;
+      r.dst_ids = b.dst_ids;
+      r.indeg = e.g.indeg;
+      r.N = e.g.N;
     }
     if (l == 1 && e.sagg1) {
       r.stat = e.sagg1;
@@ -1378,6 +1446,26 @@ void build_stored_transforms(Engine& e) {
                                                                    L1.spec.kind == OB_KIND_GCN, e.sagg1, ld);
       OB_LAUNCHED();
     }
+  }
+  // delta aggregates of srpe mid-block layers l = 2..k-1 (aggregate-first sum kinds): the CSR-part
+  // sum of the stored rows PE_{l-1} per node; a request then gathers only recomputed sources
+  const char* off_d = std::getenv("OB_NO_DELTA_AGGREGATES");
+  const bool d_off = sa_off || (off_d && off_d[0] && off_d[0] != '0');
+  e.sagg_l.assign(k, nullptr);
+  for (int l = 2; l < k && e.cfg.strategy == OB_STRATEGY_SRPE && !d_off && e.g.offsets; ++l) {
+    const LayerDev& L = e.layers[l - 1];
+    if (!(L.spec.kind == OB_KIND_GCN || L.spec.kind == OB_KIND_SAGE_MEAN) || L.transform_first) continue;
+    if ((int)e.pe.size() < l - 1 || !e.pe[l - 2]) continue;
+    const int w = L.spec.in_dim;
+    const int64_t ld = ld4(w);
+    size_t fb = 0, tb = 0;
+    OB_CUDA(cudaMemGetInfo(&fb, &tb));
+    if ((size_t)N * ld * 4 > fb / 3) continue;
+    e.sagg_l[l - 1] = (float*)e.dalloc(sizeof(float) * N * ld);
+    k_sagg_build<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, RowSrc{nullptr, e.pe[l - 2], ld},
+                                                                 w, e.g.indeg, L.spec.kind == OB_KIND_GCN,
+                                                                 e.sagg_l[l - 1], ld);
+    OB_LAUNCHED();
   }
   OB_CUDA(cudaStreamSynchronize(s));
   e.dfree(n_dev);

@@ -70,3 +70,50 @@ def test_stored_transforms_bitwise(graph, kind, strategy):
                        serving.in_neighbors, serving.features, r.query_features, r.edges,
                        pe_layers=pe.layers if pe else None, gamma=0.3)
         assert OL.max_rel_err(a[0], ref["emb"]) <= 1e-4
+
+
+def _serve_env(serving, reqs, model, w, pe, env, lanes=1):
+    from paper_2501_08547_b200 import runtime
+
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        eng = runtime.ServingEngine(serving, pe, model, w, runtime.ServeConfig(strategy="srpe", gamma=0.3))
+        if lanes > 1:
+            eng.set_lanes(lanes)
+            out = [o for o, _ in eng.serve_stream(reqs, depth=4)]
+        else:
+            out = [eng.serve(r)[0] for r in reqs]
+        eng.close()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return out
+
+
+@pytest.mark.parametrize("kind", ["sage_mean", "gcn"])
+@pytest.mark.parametrize("k,hidden", [(3, 16), (4, 16), (3, 48)])
+@pytest.mark.parametrize("lanes", [1, 2])
+def test_delta_aggregates(graph, kind, k, hidden, lanes):
+    """Mid-block layers >= 2 of sum kinds: static CSR-part sums of the stored rows plus (h - PE) delta
+    rows of the recomputed sources, against the full gather (OB_NO_DELTA_AGGREGATES=1) and the oracle."""
+    from oracle import layers as OL
+    from paper_2501_08547_b200 import graphstore, models
+
+    serving, reqs = graph
+    model = models.make_model(kind, k, serving.feature_dim, hidden)
+    w = models.init_weights(model, 4)
+    layers = [dict(kind=s.kind, in_dim=s.in_dim, out_dim=s.out_dim) for s in model.layers]
+    pe = graphstore.PeStore(OL.precompute(layers, w.layers, serving.in_offsets, serving.in_neighbors,
+                                          serving.features))
+    a = _serve_env(serving, reqs, model, w, pe, {"OB_NO_DELTA_AGGREGATES": "0"}, lanes)
+    b = _serve_env(serving, reqs, model, w, pe, {"OB_NO_DELTA_AGGREGATES": "1"}, lanes)
+    for i, r in enumerate(reqs):
+        assert OL.max_rel_err(a[i], b[i]) <= 1e-5
+        ref = OL.serve("srpe", layers, w.layers, serving.num_nodes, r.num_queries, serving.in_offsets,
+                       serving.in_neighbors, serving.features, r.query_features, r.edges, pe_layers=pe.layers,
+                       gamma=0.3)
+        assert OL.max_rel_err(a[i], ref["emb"]) <= 1e-4
