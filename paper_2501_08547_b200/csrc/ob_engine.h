@@ -308,6 +308,7 @@ struct RequestWs {
   float* s_dst = nullptr;          // gat: [D_max]
   float* mean = nullptr;           // moments: [D_max][in]
   float* delta = nullptr;          // [D_max][ld] delta rows h - PE of the targets (mid-block layers >= 2)
+  int32_t* fcnt = nullptr;         // arrival counters of the fused merge (fin_counters of the largest block)
   int64_t words_N = 0, words_NB = 0;
   BuildScratch bs[2];
 };
@@ -415,6 +416,11 @@ struct LayerRun {
   int64_t B = 0;
   const float* self_q = nullptr;   // the queries' own-row transforms, computed early
   bool no_dyn = false;             // every transformed row is a table row: skip the listed-row GEMM
+  // the next layer's delta rows (dnext[i] = out[i] - dnext_pe[dst i], i < T), written by the
+  // merge epilogue when this layer's output comes from it
+  float* dnext = nullptr;
+  const float* dnext_pe = nullptr;
+  const int64_t* dnext_T = nullptr;
 };
 
 // CGP merge inputs: partition p's raw partial rows and local in-edge counts
@@ -451,9 +457,11 @@ struct LayerScratch {
   float* z;       // [S][ld4(out)]
   float* s_src;
   float* s_dst;
+  int32_t* fcnt = nullptr;  // arrival counters of the merge fused into k_agg (null: separate finalize)
 };
 
-void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc, float* out,
+// returns true when the merge epilogue also wrote the next layer's delta rows (r.dnext)
+bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc, float* out,
                int64_t ldo);
 void build_stored_transforms(Engine& e);
 void launch_resolve(cudaStream_t s, const BindCtx& c, BlockCounters* cnt, int64_t S_max, const int32_t* src_ids,

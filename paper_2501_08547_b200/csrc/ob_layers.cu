@@ -125,11 +125,236 @@ __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restri
 }
 
 // ---------------------------------------------------------------------------
-// edge-chunk aggregation: one warp per (work item, 512-column slice)
+// merge of a destination's partials (item order) and its normalisation /
+// epilogue -- run by k_finalize (a separate pass) or fused into k_agg, where
+// the warp that completes a destination's last work item merges it
 // ---------------------------------------------------------------------------
 constexpr int kAggWarps = 4;
 constexpr int kSmHdr = 4;    // softmax partial rows: [max logit, sum exp, pad, pad | values]
 
+struct FinArgs {
+  // stored aggregates: raw CSR-part sum of each training destination, added before normalising
+  const float* stat = nullptr;
+  int64_t stat_ld = 0;
+  const int32_t* stat_dst_ids = nullptr;
+  int64_t stat_N = 0;
+  const BlockCounters* cnt;
+  const int64_t* dst_ptr;
+  const int64_t* item_ptr;
+  const int32_t* group_dst;  // destination per second-level group
+  const float* partial;
+  const int64_t* group_ptr;  // hub destinations: second-level partials in partial2
+  float* partial2;
+  int pw;     // partial row stride: ld4(width) (+ kSmHdr for softmax)
+  int width;
+  int kind;   // ob_kind
+  float p;
+  int n;
+  float* out;  // [D][ldo]
+  int64_t ldo;
+  bool relu;
+  bool gcn_norm;  // divide by sqrt(count + 1) (gcn)
+  // own-row update of a transform-first SAGE layer 1 (k_self_update fused):
+  // out = relu(own + mean), own = the stored x_v W_self of a training destination or the query's row
+  const float* self_tab = nullptr;
+  const float* self_q = nullptr;
+  int64_t self_ld = 0;
+  const int32_t* self_dst_ids = nullptr;
+  int64_t self_N = 0;
+  // delta rows for the next layer (k_delta_rows fused): dbuf[i] = out[i] - dpe[dst_ids[i]] for i < T
+  float* dbuf = nullptr;
+  const float* dpe = nullptr;
+  const int64_t* dT = nullptr;
+  // fused into k_agg: arrival counters (zeroed before the launch), per destination
+  // (items, or groups for hub destinations) and per group (items)
+  int32_t* dcnt = nullptr;
+  int32_t* gcnt = nullptr;
+};
+
+// partial-row loads: the non-coherent path for a separate pass, L2 (.cg) when the
+// partials were written by other warps of the same kernel
+template <bool CG>
+__device__ __forceinline__ float4 ldp4(const float* p) {
+  return CG ? __ldcg(reinterpret_cast<const float4*>(p)) : __ldg(reinterpret_cast<const float4*>(p));
+}
+template <bool CG>
+__device__ __forceinline__ float2 ldp2(const float* p) {
+  return CG ? __ldcg(reinterpret_cast<const float2*>(p)) : __ldg(reinterpret_cast<const float2*>(p));
+}
+__device__ __forceinline__ float4 ld4f(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// softmax partial header over items [i0, i1): running max logit and the
+// rescaled sum of exps, lanes over items, fixed butterfly order
+template <bool CG>
+__device__ __forceinline__ void sm_header(const float* part, int64_t pw, int64_t i0, int64_t i1, float& ms,
+                                          float& den) {
+  const int lane = threadIdx.x & 31;
+  float m = -INFINITY;
+  for (int64_t it = i0 + lane; it < i1; it += 32) {
+    const float2 h = ldp2<CG>(part + it * pw);
+    if (h.y > 0.f) m = fmaxf(m, h.x);
+  }
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float d = 0.f;
+  for (int64_t it = i0 + lane; it < i1; it += 32) {
+    const float2 h = ldp2<CG>(part + it * pw);
+    if (h.y > 0.f) d += h.y * __expf(h.x - m);
+  }
+  for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  ms = m;
+  den = d;
+}
+
+enum MergeKind { kMergeSum = 0, kMergeMax = 1, kMergeSoftmax = 2 };
+
+__device__ __forceinline__ float4 f4_op(int mk, float4 a, float4 v, float sc) {
+  if (mk == kMergeMax) return make_float4(fmaxf(a.x, v.x), fmaxf(a.y, v.y), fmaxf(a.z, v.z), fmaxf(a.w, v.w));
+  if (mk == kMergeSoftmax) return make_float4(fmaf(sc, v.x, a.x), fmaf(sc, v.y, a.y), fmaf(sc, v.z, a.z), fmaf(sc, v.w, a.w));
+  return make_float4(a.x + v.x, a.y + v.y, a.z + v.z, a.w + v.w);
+}
+
+// four columns [c4, c4+4) of items [i0, i1) merged with a fixed association:
+// four interleaved accumulators, 4 rows in flight per lane
+template <bool CG>
+__device__ __forceinline__ float4 merge_cols(int mk, const float* part, int64_t pw, int64_t i0, int64_t i1, int hdr,
+                                             int c4, float ms) {
+  const float z = mk == kMergeMax ? -INFINITY : 0.f;
+  float4 acc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = make_float4(z, z, z, z);
+  int64_t it = i0;
+  for (; it + 3 < i1; it += 4) {
+    float4 v[4];
+    float sc[4] = {1.f, 1.f, 1.f, 1.f};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = ldp4<CG>(part + (it + j) * pw + hdr + c4);
+    if (mk == kMergeSoftmax) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 h = ldp2<CG>(part + (it + j) * pw);
+        sc[j] = h.y > 0.f ? __expf(h.x - ms) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = f4_op(mk, acc[j], v[j], sc[j]);
+  }
+  for (; it < i1; ++it) {
+    float sc = 1.f;
+    if (mk == kMergeSoftmax) {
+      const float2 h = ldp2<CG>(part + it * pw);
+      sc = h.y > 0.f ? __expf(h.x - ms) : 0.f;
+    }
+    acc[0] = f4_op(mk, acc[0], ldp4<CG>(part + it * pw + hdr + c4), sc);
+  }
+  const int cm = mk == kMergeMax ? kMergeMax : kMergeSum;
+  return f4_op(cm, f4_op(cm, acc[0], acc[1], 1.f), f4_op(cm, acc[2], acc[3], 1.f), 1.f);
+}
+
+__device__ __forceinline__ int merge_kind(int kind) {
+  return kind == OB_KIND_GAT ? kMergeSoftmax : (kind == OB_KIND_SAGE_MAX ? kMergeMax : kMergeSum);
+}
+
+// Hub destinations (more than kItemGroup items): group g = kItemGroup consecutive
+// items merged into one second-level partial of the same form (sum / max / softmax
+// header + values), fixed association.
+template <bool CG>
+__device__ __forceinline__ void reduce_group(const FinArgs& a, int64_t g) {
+  const int lane = threadIdx.x & 31;
+  const int mk = merge_kind(a.kind);
+  const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
+  const int64_t i = __ldg(a.group_dst + g);
+  const int64_t it0 = a.item_ptr[i] + (g - a.group_ptr[i]) * kItemGroup;
+  const int64_t it1 = min(it0 + kItemGroup, a.item_ptr[i + 1]);
+  float* out = a.partial2 + g * (int64_t)a.pw;
+  float ms = 0.f, den = 0.f;
+  if (mk == kMergeSoftmax) {
+    sm_header<CG>(a.partial, a.pw, it0, it1, ms, den);
+    if (lane == 0) {
+      out[0] = ms;
+      out[1] = den;
+    }
+  }
+  for (int c4 = lane * 4; c4 < a.width; c4 += 128)
+    *reinterpret_cast<float4*>(out + hdr + c4) = merge_cols<CG>(mk, a.partial, a.pw, it0, it1, hdr, c4, ms);
+}
+
+// destination i: merge its items (or hub groups) in order, add the stored CSR
+// part, normalise, then the layer's epilogue (activation, own-row update, delta rows)
+template <bool CG>
+__device__ __forceinline__ void finalize_dst(const FinArgs& a, int64_t i) {
+  const int lane = threadIdx.x & 31;
+  const int mk = merge_kind(a.kind);
+  const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
+  int64_t i0 = a.item_ptr[i], i1 = a.item_ptr[i + 1];
+  const int64_t cnt = a.dst_ptr[i + 1] - a.dst_ptr[i];
+  const float* part = a.partial;
+  if (a.group_ptr && a.group_ptr[i + 1] > a.group_ptr[i]) {  // hub: merge the group partials
+    i0 = a.group_ptr[i];
+    i1 = a.group_ptr[i + 1];
+    part = a.partial2;
+  }
+  float ms = 0.f, den = 0.f;
+  // (max, sum exp, sum exp*z) merge in item order (cgpexec.py:225-239)
+  if (mk == kMergeSoftmax) sm_header<CG>(part, a.pw, i0, i1, ms, den);
+  const float* st = nullptr;
+  if (a.stat) {
+    const int64_t v = a.stat_dst_ids[i];
+    if (v < a.stat_N) st = a.stat + v * a.stat_ld;
+  }
+  // softmax: the static (max, sum exp, sum exp z) triple joins the item partials
+  float sc_items = 1.f, sc_stat = 0.f;
+  if (st && mk == kMergeSoftmax) {
+    const float2 h = __ldg(reinterpret_cast<const float2*>(st));
+    if (h.y > 0.f) {
+      const float M = den > 0.f ? fmaxf(ms, h.x) : h.x;
+      sc_items = den > 0.f ? __expf(ms - M) : 0.f;
+      sc_stat = __expf(h.x - M);
+      den = den * sc_items + h.y * sc_stat;
+    }
+  }
+  const float* own = nullptr;
+  if (a.self_tab) {
+    const int64_t v = a.self_dst_ids[i];
+    own = v < a.self_N ? a.self_tab + v * a.self_ld : a.self_q + (v - a.self_N) * a.self_ld;
+  }
+  const float* dpe = nullptr;
+  float* drow = nullptr;
+  if (a.dbuf && i < *a.dT) {
+    const int64_t ld = (a.width + 3) & ~3;
+    dpe = a.dpe + (int64_t)a.self_dst_ids[i] * ld;
+    drow = a.dbuf + i * ld;
+  }
+  for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
+    float4 v = merge_cols<CG>(mk, part, a.pw, i0, i1, hdr, c4, ms);
+    if (st && mk == kMergeSoftmax) {
+      const float4 q = ld4f(st + hdr + c4);
+      v = make_float4(fmaf(sc_stat, q.x, v.x * sc_items), fmaf(sc_stat, q.y, v.y * sc_items),
+                      fmaf(sc_stat, q.z, v.z * sc_items), fmaf(sc_stat, q.w, v.w * sc_items));
+    } else if (st) {
+      const float4 q = ld4f(st + c4);
+      v = make_float4(q.x + v.x, q.y + v.y, q.z + v.z, q.w + v.w);
+    }
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (c4 + t >= a.width) break;
+      float r;
+      if (mk == kMergeSoftmax) r = den > 0.f ? vv[t] / den : 0.f;
+      else if (mk == kMergeMax) r = cnt > 0 ? vv[t] : 0.f;
+      else if (a.gcn_norm) r = vv[t] / sqrtf((float)cnt + 1.f);  // agg / sqrt(|N(v)|+1) (models.py:217-218)
+      else if (a.kind == OB_KIND_POWER_MEAN) r = cnt > 0 ? powf(vv[t] / (float)cnt, 1.f / a.p) : 0.f;
+      else r = cnt > 0 ? vv[t] / (float)cnt : 0.f;  // mean
+      if (own) r = fmaxf(own[c4 + t] + r, 0.f);  // the same fp32 sum k_self_update formed
+      if (a.relu) r = fmaxf(r, 0.f);
+      a.out[i * a.ldo + c4 + t] = r;
+      if (drow) drow[c4 + t] = r - dpe[c4 + t];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// edge-chunk aggregation: one warp per (work item, 512-column slice)
+// ---------------------------------------------------------------------------
 struct AggArgs {
   const BlockCounters* cnt;
   const int64_t* dst_ptr;
@@ -162,17 +387,19 @@ struct AggArgs {
   // sources are ascending, so that is a contiguous run of every 32-edge group);
   // accumulate adds to the partials of the previous pass
   int pass = 0, passes = 1;  // pass p covers sources [S p / passes, S (p+1) / passes)
+  // fused merge (last pass, one column slice): the warp completing a destination's
+  // last item (or a hub destination's last group) merges and finalizes it
+  bool fused = false;
 };
 
 template <int OP, int NV>
 #ifndef OB_AGG_MINB_WIDE
 #define OB_AGG_MINB_WIDE 1  // k_agg CTAs per SM for rows wider than 128 columns (NV = 2, 4)
 #endif
-__global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WIDE)) k_agg(AggArgs a) {
+__global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WIDE)) k_agg(AggArgs a, FinArgs f) {
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   const int lane = threadIdx.x & 31;
-  const int64_t D = a.cnt->D;
   const int64_t items = a.cnt->items;
   const int col0 = blockIdx.y * (32 * 4 * NV);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -313,133 +540,49 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
       for (int t = 0; t < 4; ++t)
         if (col + t < a.width) out[col + t] = a.pass > 0 ? out[col + t] + acc[q][t] : acc[q][t];
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// merge a destination's partials in item order and normalise (warp per dst)
-// ---------------------------------------------------------------------------
-struct FinArgs {
-  // stored aggregates: raw CSR-part sum of each training destination, added before normalising
-  const float* stat = nullptr;
-  int64_t stat_ld = 0;
-  const int32_t* stat_dst_ids = nullptr;
-  int64_t stat_N = 0;
-  const BlockCounters* cnt;
-  const int64_t* dst_ptr;
-  const int64_t* item_ptr;
-  const int32_t* group_dst;  // destination per second-level group
-  const float* partial;
-  const int64_t* group_ptr;  // hub destinations: second-level partials in partial2
-  const float* partial2;
-  int pw;     // partial row stride: ld4(width) (+ kSmHdr for softmax)
-  int width;
-  int kind;   // ob_kind
-  float p;
-  int n;
-  float* out;  // [D][ldo]
-  int64_t ldo;
-  bool relu;
-  bool gcn_norm;  // divide by sqrt(count + 1) (gcn)
-};
-
-__device__ __forceinline__ float4 ld4f(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-
-// softmax partial header over items [i0, i1): running max logit and the
-// rescaled sum of exps, lanes over items, fixed butterfly order
-__device__ __forceinline__ void sm_header(const float* part, int64_t pw, int64_t i0, int64_t i1, float& ms,
-                                          float& den) {
-  const int lane = threadIdx.x & 31;
-  float m = -INFINITY;
-  for (int64_t it = i0 + lane; it < i1; it += 32) {
-    const float2 h = __ldg(reinterpret_cast<const float2*>(part + it * pw));
-    if (h.y > 0.f) m = fmaxf(m, h.x);
-  }
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float d = 0.f;
-  for (int64_t it = i0 + lane; it < i1; it += 32) {
-    const float2 h = __ldg(reinterpret_cast<const float2*>(part + it * pw));
-    if (h.y > 0.f) d += h.y * __expf(h.x - m);
-  }
-  for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-  ms = m;
-  den = d;
-}
-
-enum MergeKind { kMergeSum = 0, kMergeMax = 1, kMergeSoftmax = 2 };
-
-__device__ __forceinline__ float4 f4_op(int mk, float4 a, float4 v, float sc) {
-  if (mk == kMergeMax) return make_float4(fmaxf(a.x, v.x), fmaxf(a.y, v.y), fmaxf(a.z, v.z), fmaxf(a.w, v.w));
-  if (mk == kMergeSoftmax) return make_float4(fmaf(sc, v.x, a.x), fmaf(sc, v.y, a.y), fmaf(sc, v.z, a.z), fmaf(sc, v.w, a.w));
-  return make_float4(a.x + v.x, a.y + v.y, a.z + v.z, a.w + v.w);
-}
-
-// four columns [c4, c4+4) of items [i0, i1) merged with a fixed association:
-// four interleaved accumulators, 4 rows in flight per lane
-__device__ __forceinline__ float4 merge_cols(int mk, const float* part, int64_t pw, int64_t i0, int64_t i1, int hdr,
-                                             int c4, float ms) {
-  const float z = mk == kMergeMax ? -INFINITY : 0.f;
-  float4 acc[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j] = make_float4(z, z, z, z);
-  int64_t it = i0;
-  for (; it + 3 < i1; it += 4) {
-    float4 v[4];
-    float sc[4] = {1.f, 1.f, 1.f, 1.f};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] = ld4f(part + (it + j) * pw + hdr + c4);
-    if (mk == kMergeSoftmax) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 h = __ldg(reinterpret_cast<const float2*>(part + (it + j) * pw));
-        sc[j] = h.y > 0.f ? __expf(h.x - ms) : 0.f;
+    if constexpr (OP != kOpDSum && OP != kOpMom2) {
+      if (a.fused) {
+        // publish this item; the warp that completes the destination (or the hub
+        // destination's group, then the destination) merges in item order
+        __threadfence();
+        __syncwarp();
+        const int64_t gn = f.group_ptr ? f.group_ptr[i + 1] - f.group_ptr[i] : 0;
+        int last = 0;
+        if (lane == 0) {
+          if (gn > 0) {
+            const int64_t g = f.group_ptr[i] + j / kItemGroup;
+            const int64_t it0 = a.item_ptr[i] + (j / kItemGroup) * kItemGroup;
+            const int64_t n_in = min((int64_t)kItemGroup, a.item_ptr[i + 1] - it0);
+            last = atomicAdd(f.gcnt + g, 1) == n_in - 1 ? 1 : 0;
+          } else {
+            const int64_t n_it = a.item_ptr[i + 1] - a.item_ptr[i];
+            last = atomicAdd(f.dcnt + i, 1) == n_it - 1 ? 2 : 0;
+          }
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last == 1) {  // this group is complete: its second-level partial, then count it
+          __threadfence();
+          reduce_group<true>(f, f.group_ptr[i] + j / kItemGroup);
+          __threadfence();
+          __syncwarp();
+          int lg = 0;
+          if (lane == 0) lg = atomicAdd(f.dcnt + i, 1) == gn - 1;
+          last = __shfl_sync(0xffffffffu, lg, 0) ? 2 : 0;
+        }
+        if (last == 2) {
+          __threadfence();
+          finalize_dst<true>(f, i);
+        }
       }
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] = f4_op(mk, acc[j], v[j], sc[j]);
   }
-  for (; it < i1; ++it) {
-    float sc = 1.f;
-    if (mk == kMergeSoftmax) {
-      const float2 h = __ldg(reinterpret_cast<const float2*>(part + it * pw));
-      sc = h.y > 0.f ? __expf(h.x - ms) : 0.f;
-    }
-    acc[0] = f4_op(mk, acc[0], ld4f(part + it * pw + hdr + c4), sc);
-  }
-  const int cm = mk == kMergeMax ? kMergeMax : kMergeSum;
-  return f4_op(cm, f4_op(cm, acc[0], acc[1], 1.f), f4_op(cm, acc[2], acc[3], 1.f), 1.f);
 }
 
-__device__ __forceinline__ int merge_kind(int kind) {
-  return kind == OB_KIND_GAT ? kMergeSoftmax : (kind == OB_KIND_SAGE_MAX ? kMergeMax : kMergeSum);
-}
-
-// Hub destinations (more than kItemGroup items): merge each group of
-// kItemGroup consecutive items into one second-level partial of the same form
-// (sum / max / softmax header + values), one warp per group, fixed association.
-__global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a, float* partial2) {
-  const int64_t D = a.cnt->D, G = a.cnt->groups;
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
+  const int64_t G = a.cnt->groups;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int mk = merge_kind(a.kind);
-  const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
-  for (int64_t g = gw; g < G; g += nw) {
-    const int64_t i = __ldg(a.group_dst + g);
-    const int64_t it0 = a.item_ptr[i] + (g - a.group_ptr[i]) * kItemGroup;
-    const int64_t it1 = min(it0 + kItemGroup, a.item_ptr[i + 1]);
-    float* out = partial2 + g * (int64_t)a.pw;
-    float ms = 0.f, den = 0.f;
-    if (mk == kMergeSoftmax) {
-      sm_header(a.partial, a.pw, it0, it1, ms, den);
-      if (lane == 0) {
-        out[0] = ms;
-        out[1] = den;
-      }
-    }
-    for (int c4 = lane * 4; c4 < a.width; c4 += 128)
-      *reinterpret_cast<float4*>(out + hdr + c4) = merge_cols(mk, a.partial, a.pw, it0, it1, hdr, c4, ms);
-  }
+  for (int64_t g = gw; g < G; g += nw) reduce_group<false>(a, g);
 }
 
 #ifndef OB_FIN_MINB
@@ -447,64 +590,9 @@ __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a, float* partial
 #endif
 __global__ void __launch_bounds__(256, OB_FIN_MINB) k_finalize(FinArgs a) {
   const int64_t D = a.cnt->D;
-  const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int mk = merge_kind(a.kind);
-  const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
-  for (int64_t i = gw; i < D; i += nw) {
-    int64_t i0 = a.item_ptr[i], i1 = a.item_ptr[i + 1];
-    const int64_t cnt = a.dst_ptr[i + 1] - a.dst_ptr[i];
-    const float* part = a.partial;
-    if (a.group_ptr && a.group_ptr[i + 1] > a.group_ptr[i]) {  // hub: merge the group partials
-      i0 = a.group_ptr[i];
-      i1 = a.group_ptr[i + 1];
-      part = a.partial2;
-    }
-    float ms = 0.f, den = 0.f;
-    // (max, sum exp, sum exp*z) merge in item order (cgpexec.py:225-239)
-    if (mk == kMergeSoftmax) sm_header(part, a.pw, i0, i1, ms, den);
-    const float* st = nullptr;
-    if (a.stat) {
-      const int64_t v = a.stat_dst_ids[i];
-      if (v < a.stat_N) st = a.stat + v * a.stat_ld;
-    }
-    // softmax: the static (max, sum exp, sum exp z) triple joins the item partials
-    float sc_items = 1.f, sc_stat = 0.f;
-    if (st && mk == kMergeSoftmax) {
-      const float2 h = __ldg(reinterpret_cast<const float2*>(st));
-      if (h.y > 0.f) {
-        const float M = den > 0.f ? fmaxf(ms, h.x) : h.x;
-        sc_items = den > 0.f ? __expf(ms - M) : 0.f;
-        sc_stat = __expf(h.x - M);
-        den = den * sc_items + h.y * sc_stat;
-      }
-    }
-    for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
-      float4 v = merge_cols(mk, part, a.pw, i0, i1, hdr, c4, ms);
-      if (st && mk == kMergeSoftmax) {
-        const float4 q = ld4f(st + hdr + c4);
-        v = make_float4(fmaf(sc_stat, q.x, v.x * sc_items), fmaf(sc_stat, q.y, v.y * sc_items),
-                        fmaf(sc_stat, q.z, v.z * sc_items), fmaf(sc_stat, q.w, v.w * sc_items));
-      } else if (st) {
-        const float4 q = ld4f(st + c4);
-        v = make_float4(q.x + v.x, q.y + v.y, q.z + v.z, q.w + v.w);
-      }
-      const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if (c4 + t >= a.width) break;
-        float r;
-        if (mk == kMergeSoftmax) r = den > 0.f ? vv[t] / den : 0.f;
-        else if (mk == kMergeMax) r = cnt > 0 ? vv[t] : 0.f;
-        else if (a.gcn_norm) r = vv[t] / sqrtf((float)cnt + 1.f);  // agg / sqrt(|N(v)|+1) (models.py:217-218)
-        else if (a.kind == OB_KIND_POWER_MEAN) r = cnt > 0 ? powf(vv[t] / (float)cnt, 1.f / a.p) : 0.f;
-        else r = cnt > 0 ? vv[t] / (float)cnt : 0.f;  // mean
-        if (a.relu) r = fmaxf(r, 0.f);
-        a.out[i * a.ldo + c4 + t] = r;
-      }
-    }
-  }
+  for (int64_t i = gw; i < D; i += nw) finalize_dst<false>(a, i);
 }
 
 // moments finalize in float64: phase 1 -> mean (double), phase 2 -> signed root (float)
@@ -556,7 +644,8 @@ __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* sel
 constexpr int64_t kAggPassBytes = 64ll << 20;
 
 template <int OP>
-static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int64_t S_max = 0) {
+static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int64_t S_max = 0,
+                       const FinArgs* fused = nullptr) {
   const int nv = a0.width <= 128 ? 1 : (a0.width <= 256 ? 2 : 4);
   dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a0.width + 128 * nv - 1) / (128 * nv));
   int passes = 1;
@@ -565,14 +654,16 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
     passes = (int)std::min<int64_t>(4, (rows_bytes + kAggPassBytes - 1) / kAggPassBytes);
     if (passes < 1) passes = 1;
   }
+  const FinArgs f = fused ? *fused : FinArgs{};
   cudaEvent_t pa = prof_begin(s);
   for (int p = 0; p < passes; ++p) {
     AggArgs a = a0;
     a.pass = p;
     a.passes = passes;
-    if (nv == 1) k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a);
-    else if (nv == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a);
-    else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a);
+    a.fused = fused && p + 1 == passes;
+    if (nv == 1) k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a, f);
+    else if (nv == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a, f);
+    else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a, f);
     OB_LAUNCHED();
   }
   // K = -1 marks a stored-aggregate launch: it gathers only the request spans, which the
@@ -584,12 +675,39 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
 static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t items_max) {
   cudaEvent_t pa = prof_begin(s);
   if (f.group_ptr) {
-    k_reduce_groups<<<grid_for(items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f, (float*)f.partial2);
+    k_reduce_groups<<<grid_for(items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f);
     OB_LAUNCHED();
   }
   k_finalize<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(f);
   OB_LAUNCHED();
   prof_end(s, pa, kProfFinalize, f.cnt, f.width, f.pw, 0, 0, 0);
+}
+
+// arrival counters of a fused merge: [D_max + 1] per destination, then per group
+inline int64_t fin_counters(int64_t D_max, int64_t items_max) { return 2 * D_max + items_max / kItemGroup + 2; }
+
+static bool fused_finalize_on() {
+  static const bool off = [] {
+    const char* v = std::getenv("OB_NO_FUSED_FINALIZE");
+    return v && v[0] && v[0] != '0';
+  }();
+  return !off;
+}
+
+// aggregation + merge/normalise: one k_agg launch whose last-arriving warps merge
+// each destination (fcnt given, one column slice), else k_agg then k_finalize
+template <int OP>
+static void agg_fin(cudaStream_t s, const AggArgs& a, FinArgs f, int32_t* fcnt, int64_t items_max, int64_t D_max,
+                    int64_t S_split = 0) {
+  if (fcnt && a.width <= 512 && fused_finalize_on()) {
+    OB_CUDA(cudaMemsetAsync(fcnt, 0, sizeof(int32_t) * fin_counters(D_max, items_max), s));
+    f.dcnt = fcnt;
+    f.gcnt = fcnt + D_max + 1;
+    launch_agg<OP>(s, a, items_max, S_split, &f);
+    return;
+  }
+  launch_agg<OP>(s, a, items_max, S_split);
+  finalize(s, f, D_max, items_max);
 }
 
 static void gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max, const BlockCounters* cnt) {
@@ -617,25 +735,9 @@ static TcGemmArgs gemm_args(const int64_t* M_dev, const TcWeights& w, float* C, 
   return g;
 }
 
-// out[i] = relu(own[i] + agg[i]) with own = the stored x_v W_self of a training destination or the
-// query's GEMM row -- the same fp32 sum the GEMM epilogue forms (acc + addend, then relu)
-__global__ void k_self_update(const BlockCounters* cnt, const int32_t* __restrict__ dst_ids, int64_t N,
-                              const float* __restrict__ tab, const float* __restrict__ qrows, int64_t ld,
-                              const float* __restrict__ agg, int width, float* out, int64_t ldo) {
-  const int64_t D = cnt->D;
-  const int64_t n = D * ld;
-  OB_GRID_STRIDE(t, n) {
-    const int64_t i = t / ld;
-    const int c = (int)(t - i * ld);
-    if (c >= width) continue;
-    const int64_t v = dst_ids[i];
-    float o = v < N ? tab[v * ld + c] : qrows[(v - N) * ld + c];
-    o += agg[i * ld + c];
-    out[i * ldo + c] = fmaxf(o, 0.f);
-  }
-}
-
-void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc, float* out,
+// Returns true when the layer's finalize also wrote the next layer's delta rows
+// (r.dnext): the output then comes from the merge epilogue, not a GEMM.
+bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc, float* out,
                int64_t ldo) {
   const ob_layer& sp = L.spec;
   const int in = sp.in_dim, outd = sp.out_dim;
@@ -682,6 +784,16 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     f.stat_dst_ids = r.dst_ids;
     f.stat_N = r.N;
   }
+  // the next layer's delta rows from this layer's merge epilogue (when it writes the output)
+  auto with_dnext = [&](FinArgs& ff) {
+    if (!r.dnext) return false;
+    ff.dbuf = r.dnext;
+    ff.dpe = r.dnext_pe;
+    ff.dT = r.dnext_T;
+    ff.self_dst_ids = r.dst_ids;
+    return true;
+  };
+  const int64_t split = r.split_gather ? r.S_max : 0;
 
   if ((sp.kind == OB_KIND_GAT || L.transform_first) && r.yrow) {
     // stored transforms: only the listed sources (queries, recomputed rows) need x W now
@@ -689,7 +801,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     g.a1 = r.x;
     g.self = r.dyn_src;
     g.K1 = in;
-    gemm(s, g, r.dyn_max, nullptr);
+    if (!r.no_dyn) gemm(s, g, r.dyn_max, nullptr);
     a.x = RowSrc{r.yrow, nullptr, 0};
     a.width = outd;
     a.pw = ld4(outd);
@@ -717,38 +829,37 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
     a.s_dst = sc.s_dst;
-    launch_agg<kOpSoftmax>(s, a, r.items_max);
     f.pw = a.pw;
     f.out = out;
     f.ldo = ldo;
     f.relu = true;
-    finalize(s, f, r.D_max, r.items_max);
-    return;
+    const bool d = with_dnext(f);
+    agg_fin<kOpSoftmax>(s, a, f, sc.fcnt, r.items_max, r.D_max);
+    return d;
   }
   if (sp.kind == OB_KIND_GCN) {
     a.gscale = r.gscale;
-    launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
     f.gcn_norm = true;
     if (L.transform_first) {  // relu(sum_u (x_u W) / sqrt(d_u+1) / sqrt(c+1))
       f.out = out;
       f.ldo = ldo;
       f.relu = true;
-      finalize(s, f, r.D_max, r.items_max);
-      return;
+      const bool d = with_dnext(f);
+      agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);
+      return d;
     }
-    finalize(s, f, r.D_max, r.items_max);
+    agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);
     TcGemmArgs g = gemm_args(r.D_dev, L.tw_main, out, ldo, true);
     g.a2 = sc.agg;
     g.lda2 = ld4(in);
     g.K2 = in;
     gemm(s, g, r.D_max, r.cnt);
-    return;
+    return false;
   }
   if (sp.kind == OB_KIND_SAGE_MEAN && L.transform_first && r.self_tab) {
-    launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
-    finalize(s, f, r.D_max, r.items_max);  // mean over Y = X W_neigh rows -> agg [D][ld_out]
     // own-row term: training destinations from the stored table, the queries by a B-row GEMM
-    // (done early, beside the request-index sort, when the query rows were staged ahead)
+    // (done early, beside the request-index sort, when the query rows were staged ahead);
+    // relu(own + mean) is the merge epilogue
     const float* qs = r.self_q;
     if (!qs) {
       TcGemmArgs g = gemm_args(r.B_dev, L.tw_self, sc.z, ld_out, false);
@@ -757,14 +868,19 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
       gemm(s, g, r.B, nullptr);
       qs = sc.z;
     }
-    k_self_update<<<grid_for(r.D_max * ld_out, 256), 256, 0, s>>>(r.cnt, r.dst_ids, r.N, r.self_tab, qs, ld_out,
-                                                                    sc.agg, outd, out, ldo);
-    OB_LAUNCHED();
-    return;
+    f.self_tab = r.self_tab;
+    f.self_q = qs;
+    f.self_ld = ld_out;
+    f.self_dst_ids = r.dst_ids;
+    f.self_N = r.N;
+    f.out = out;
+    f.ldo = ldo;
+    const bool d = with_dnext(f);
+    agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);
+    return d;
   }
   if (sp.kind == OB_KIND_SAGE_MEAN && L.transform_first) {
-    launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
-    finalize(s, f, r.D_max, r.items_max);  // mean over Y = X W_neigh rows -> agg [D][ld_out]
+    agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);  // mean over Y = X W_neigh -> agg
     TcGemmArgs g = gemm_args(r.D_dev, L.tw_self, out, ldo, true);
     g.a1 = r.x;
     g.self = r.self;
@@ -772,14 +888,12 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     g.E = sc.agg;
     g.lde = ld_out;
     gemm(s, g, r.D_max, r.cnt);
-    return;
+    return false;
   }
   if (sp.kind == OB_KIND_SAGE_MAX) {
-    launch_agg<kOpMax>(s, a, r.items_max);
-    finalize(s, f, r.D_max, r.items_max);
+    agg_fin<kOpMax>(s, a, f, sc.fcnt, r.items_max, r.D_max);
   } else if (sp.kind == OB_KIND_POWER_MEAN) {
-    launch_agg<kOpPow>(s, a, r.items_max);
-    finalize(s, f, r.D_max, r.items_max);
+    agg_fin<kOpPow>(s, a, f, sc.fcnt, r.items_max, r.D_max);
   } else if (sp.kind == OB_KIND_MOMENTS) {
     double* mean = reinterpret_cast<double*>(sc.mean);
     launch_agg<kOpDSum>(s, a, r.items_max);
@@ -791,8 +905,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
         r.cnt, r.dst_ptr, r.item_ptr, (const double*)sc.partial, in, 2, sp.n, nullptr, sc.agg, ld4(in));
     g_launches += 2;
   } else {  // sage_mean aggregate-first
-    launch_agg<kOpSum>(s, a, r.items_max, r.split_gather ? r.S_max : 0);
-    finalize(s, f, r.D_max, r.items_max);
+    agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);
   }
   // relu([h_v | agg] @ [W_self; W_neigh])
   TcGemmArgs g = gemm_args(r.D_dev, L.tw_main, out, ldo, true);
@@ -803,6 +916,7 @@ void run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   g.lda2 = ld4(in);
   g.K2 = in;
   gemm(s, g, r.D_max, r.cnt);
+  return false;
 }
 
 // ---------------------------------------------------------------------------
@@ -836,14 +950,14 @@ __global__ void __launch_bounds__(256) k_local_raw(FinArgs a, float* lp, int64_t
     const int oh = mk == kMergeSoftmax ? 2 : 0;  // rank-partial layout: [max, sum exp | values]
     float ms = 0.f, den = 0.f;
     if (mk == kMergeSoftmax) {
-      sm_header(part, a.pw, i0, i1, ms, den);
+      sm_header<false>(part, a.pw, i0, i1, ms, den);
       if (lane == 0) {
         o[0] = ms;
         o[1] = den;
       }
     }
     for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
-      const float4 v = merge_cols(mk, part, a.pw, i0, i1, hdr, c4, ms);
+      const float4 v = merge_cols<false>(mk, part, a.pw, i0, i1, hdr, c4, ms);
       const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -1031,7 +1145,7 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   f.pw = a.pw;
   f.width = a.width;
   f.kind = sp.kind;
-  k_reduce_groups<<<grid_for(r.items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f, sc.partial2);
+  k_reduce_groups<<<grid_for(r.items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f);
   k_local_raw<<<grid_for(r.D_max, 8, kNumSMs * 16), 256, 0, s>>>(f, lp, ldp, lcnt);
   g_launches += 2;
 }
@@ -1156,6 +1270,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, s>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
     OB_LAUNCHED();
   }
+  bool delta_ready = false;  // the previous layer's epilogue wrote this layer's delta rows
   for (int l = 1; l <= k; ++l) {
     const LayerDev& L = e.layers[l - 1];
     BlockDev& b = w.blocks[w.block_of_layer[l - 1]];
@@ -1194,9 +1309,11 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     if (l > 1 && l < k && (int)e.sagg_l.size() >= l && e.sagg_l[l - 1] && w.delta) {
       // delta aggregates: static CSR-part sums of the stored rows + (h - PE) of recomputed sources
       const int64_t ld = ld4(L.spec.in_dim);
-      k_delta_rows<<<grid_for(b.D_max * ld, 256), 256, 0, s>>>(&w.rc->T, w.targets, w.outs[l - 1], e.pe[l - 2], ld,
-                                                                 w.delta);
-      OB_LAUNCHED();
+      if (!delta_ready) {
+        k_delta_rows<<<grid_for(b.D_max * ld, 256), 256, 0, s>>>(&w.rc->T, w.targets, w.outs[l - 1], e.pe[l - 2],
+                                                                   ld, w.delta);
+        OB_LAUNCHED();
+      }
       r.delta = true;
       r.dprev = w.outs[l - 1];
       r.dT = &w.rc->T;
@@ -1206,6 +1323,13 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       r.dst_ids = b.dst_ids;
       r.indeg = e.g.indeg;
       r.N = e.g.N;
+    }
+    // the next layer aggregates by deltas: this layer's merge epilogue may write them
+    if (l + 1 < k && (int)e.sagg_l.size() > l && e.sagg_l[l] && w.delta) {
+      r.dnext = w.delta;
+      r.dnext_pe = e.pe[l - 1];
+      r.dnext_T = &w.rc->T;
+      r.dst_ids = b.dst_ids;
     }
     if (l == 1 && e.sagg1) {
       r.stat = e.sagg1;
@@ -1232,10 +1356,10 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     r.group_ptr = b.group_ptr;
     // with several requests in flight, big sum gathers run as L2-sized source-range passes
     r.split_gather = e.nlanes > 1;
-    LayerScratch sc{w.partial, w.partial2, w.agg, w.mean, w.z, w.s_src, w.s_dst};
+    LayerScratch sc{w.partial, w.partial2, w.agg, w.mean, w.z, w.s_src, w.s_dst, w.fcnt};
     const bool last = l == k;
     float* out = last ? d_out : w.outs[l];
-    run_layer(s, L, r, sc, out, last ? L.spec.out_dim : ld4(L.spec.out_dim));
+    delta_ready = run_layer(s, L, r, sc, out, last ? L.spec.out_dim : ld4(L.spec.out_dim));
   }
 }
 
@@ -1518,6 +1642,7 @@ void stage_precompute(Engine& e) {
     float* s_src = (float*)talloc(sizeof(float) * N);
     float* s_dst = (float*)talloc(sizeof(float) * N);
     float* gscale = (float*)talloc(sizeof(float) * N);
+    int32_t* fcnt = (int32_t*)talloc(sizeof(int32_t) * fin_counters(N, items_max));
     k_node_scale<<<grid_for(N, 256), 256, 0, s>>>(e.g.indeg, N, gscale);
     OB_LAUNCHED();
     ScanScratch sc_scan;
@@ -1556,7 +1681,7 @@ void stage_precompute(Engine& e) {
       r.x = RowSrc{nullptr, h, hld};
       r.gscale = gscale;
       r.group_ptr = group_ptr;
-      LayerScratch scr{partial, partial2, agg, mean, z, s_src, s_dst};
+      LayerScratch scr{partial, partial2, agg, mean, z, s_src, s_dst, fcnt};
       run_layer(s, L, r, scr, out, old);
       e.pe[l - 1] = out;
       e.pe_dim[l - 1] = L.spec.out_dim;
