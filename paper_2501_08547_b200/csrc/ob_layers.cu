@@ -352,6 +352,12 @@ __device__ __forceinline__ void finalize_dst(const FinArgs& a, int64_t i) {
   }
 }
 
+__device__ __forceinline__ int atom_add_release(int32_t* p) {
+  int old;
+  asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 // ---------------------------------------------------------------------------
 // edge-chunk aggregation: one warp per (work item, 512-column slice)
 // ---------------------------------------------------------------------------
@@ -543,8 +549,11 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
     if constexpr (OP != kOpDSum && OP != kOpMom2) {
       if (a.fused) {
         // publish this item; the warp that completes the destination (or the hub
-        // destination's group, then the destination) merges in item order
-        __threadfence();
+        // destination's group, then the destination) merges in item order.  The
+        // counter add is a gpu-scope release (MEMBAR, no L1 invalidation: a full
+        // __threadfence would flush this SM's L1 of gathered rows on every item);
+        // the merging warp reads the partials with L2 loads (ld.global.cg) that are
+        // control-dependent on the count it observed
         __syncwarp();
         const int64_t gn = f.group_ptr ? f.group_ptr[i + 1] - f.group_ptr[i] : 0;
         int last = 0;
@@ -553,26 +562,21 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
             const int64_t g = f.group_ptr[i] + j / kItemGroup;
             const int64_t it0 = a.item_ptr[i] + (j / kItemGroup) * kItemGroup;
             const int64_t n_in = min((int64_t)kItemGroup, a.item_ptr[i + 1] - it0);
-            last = atomicAdd(f.gcnt + g, 1) == n_in - 1 ? 1 : 0;
+            last = atom_add_release(f.gcnt + g) == n_in - 1 ? 1 : 0;
           } else {
             const int64_t n_it = a.item_ptr[i + 1] - a.item_ptr[i];
-            last = atomicAdd(f.dcnt + i, 1) == n_it - 1 ? 2 : 0;
+            last = atom_add_release(f.dcnt + i) == n_it - 1 ? 2 : 0;
           }
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last == 1) {  // this group is complete: its second-level partial, then count it
-          __threadfence();
           reduce_group<true>(f, f.group_ptr[i] + j / kItemGroup);
-          __threadfence();
           __syncwarp();
           int lg = 0;
-          if (lane == 0) lg = atomicAdd(f.dcnt + i, 1) == gn - 1;
+          if (lane == 0) lg = atom_add_release(f.dcnt + i) == gn - 1;
           last = __shfl_sync(0xffffffffu, lg, 0) ? 2 : 0;
         }
-        if (last == 2) {
-          __threadfence();
-          finalize_dst<true>(f, i);
-        }
+        if (last == 2) finalize_dst<true>(f, i);
       }
     }
   }
