@@ -267,7 +267,6 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.dyn_src = wide ? a.take<int32_t>(Smax) : nullptr;
   w.ndyn = wide ? a.take<int64_t>(1) : nullptr;
   w.delta = (!khop(e.cfg) && k >= 3) ? a.take<float>(p.blocks[0].D_max * wl) : nullptr;
-  w.fcnt = a.take<int32_t>(2 * Dmax + Imax / kItemGroup + 2);
   w.s_src = gat ? a.take<float>(Smax) : nullptr;
   w.s_dst = gat ? a.take<float>(Dmax) : nullptr;
   for (int l = 1; l < k; ++l) {

@@ -308,7 +308,6 @@ struct RequestWs {
   float* s_dst = nullptr;          // gat: [D_max]
   float* mean = nullptr;           // moments: [D_max][in]
   float* delta = nullptr;          // [D_max][ld] delta rows h - PE of the targets (mid-block layers >= 2)
-  int32_t* fcnt = nullptr;         // arrival counters of the fused merge (fin_counters of the largest block)
   int64_t words_N = 0, words_NB = 0;
   BuildScratch bs[2];
 };
@@ -457,7 +456,6 @@ struct LayerScratch {
   float* z;       // [S][ld4(out)]
   float* s_src;
   float* s_dst;
-  int32_t* fcnt = nullptr;  // arrival counters of the merge fused into k_agg (null: separate finalize)
 };
 
 // returns true when the merge epilogue also wrote the next layer's delta rows (r.dnext)

@@ -165,10 +165,9 @@ struct FinArgs {
   float* dbuf = nullptr;
   const float* dpe = nullptr;
   const int64_t* dT = nullptr;
-  // fused into k_agg: arrival counters (zeroed before the launch), per destination
-  // (items, or groups for hub destinations) and per group (items)
-  int32_t* dcnt = nullptr;
-  int32_t* gcnt = nullptr;
+  // destinations with at most direct_items work items were gathered by one warp
+  // and finalized from its registers inside k_agg (0: none)
+  int direct_items = 0;
 };
 
 // partial-row loads: the non-coherent path for a separate pass, L2 (.cg) when the
@@ -278,14 +277,69 @@ __device__ __forceinline__ void reduce_group(const FinArgs& a, int64_t g) {
     *reinterpret_cast<float4*>(out + hdr + c4) = merge_cols<CG>(mk, a.partial, a.pw, it0, it1, hdr, c4, ms);
 }
 
-// destination i: merge its items (or hub groups) in order, add the stored CSR
-// part, normalise, then the layer's epilogue (activation, own-row update, delta rows)
-template <bool CG>
+// columns [c4, c4 + 4) of destination i from its merged raw aggregate v (softmax:
+// the sum exp * z with its header (ms, den)): add the stored CSR part, normalise,
+// then the layer epilogue (activation, own-row update, the next layer's delta rows)
+__device__ __forceinline__ void fin_cols(const FinArgs& a, int64_t i, int64_t cnt, int c4, float4 v, float ms,
+                                         float den) {
+  if (c4 >= a.width) return;
+  const int mk = merge_kind(a.kind);
+  const float* st = nullptr;
+  if (a.stat) {
+    const int64_t u = a.stat_dst_ids[i];
+    if (u < a.stat_N) st = a.stat + u * a.stat_ld;
+  }
+  if (st && mk == kMergeSoftmax) {  // the static (max, sum exp, sum exp z) triple joins the items
+    const float2 h = __ldg(reinterpret_cast<const float2*>(st));
+    if (h.y > 0.f) {
+      const float M = den > 0.f ? fmaxf(ms, h.x) : h.x;
+      const float sc_items = den > 0.f ? __expf(ms - M) : 0.f;
+      const float sc_stat = __expf(h.x - M);
+      den = den * sc_items + h.y * sc_stat;
+      const float4 q = ld4f(st + kSmHdr + c4);
+      v = make_float4(fmaf(sc_stat, q.x, v.x * sc_items), fmaf(sc_stat, q.y, v.y * sc_items),
+                      fmaf(sc_stat, q.z, v.z * sc_items), fmaf(sc_stat, q.w, v.w * sc_items));
+    }
+  } else if (st) {
+    const float4 q = ld4f(st + c4);
+    v = make_float4(q.x + v.x, q.y + v.y, q.z + v.z, q.w + v.w);
+  }
+  const float* own = nullptr;
+  if (a.self_tab) {
+    const int64_t u = a.self_dst_ids[i];
+    own = (u < a.self_N ? a.self_tab + u * a.self_ld : a.self_q + (u - a.self_N) * a.self_ld) + c4;
+  }
+  const float* dpe = nullptr;
+  float* drow = nullptr;
+  if (a.dbuf && i < *a.dT) {
+    const int64_t ld = (a.width + 3) & ~3;
+    dpe = a.dpe + (int64_t)a.self_dst_ids[i] * ld + c4;
+    drow = a.dbuf + i * ld + c4;
+  }
+  const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    if (c4 + t >= a.width) break;
+    float r;
+    if (mk == kMergeSoftmax) r = den > 0.f ? vv[t] / den : 0.f;
+    else if (mk == kMergeMax) r = cnt > 0 ? vv[t] : 0.f;
+    else if (a.gcn_norm) r = vv[t] / sqrtf((float)cnt + 1.f);  // agg / sqrt(|N(v)|+1) (models.py:217-218)
+    else if (a.kind == OB_KIND_POWER_MEAN) r = cnt > 0 ? powf(vv[t] / (float)cnt, 1.f / a.p) : 0.f;
+    else r = cnt > 0 ? vv[t] / (float)cnt : 0.f;  // mean
+    if (own) r = fmaxf(own[t] + r, 0.f);  // the fp32 sum the own-row update formed (then relu)
+    if (a.relu) r = fmaxf(r, 0.f);
+    a.out[i * a.ldo + c4 + t] = r;
+    if (drow) drow[t] = r - dpe[t];
+  }
+}
+
+// destination i: merge its items (or hub groups) in item order, then fin_cols
 __device__ __forceinline__ void finalize_dst(const FinArgs& a, int64_t i) {
   const int lane = threadIdx.x & 31;
   const int mk = merge_kind(a.kind);
   const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
   int64_t i0 = a.item_ptr[i], i1 = a.item_ptr[i + 1];
+  if (a.direct_items && i1 - i0 <= a.direct_items) return;  // finalized by k_agg from registers
   const int64_t cnt = a.dst_ptr[i + 1] - a.dst_ptr[i];
   const float* part = a.partial;
   if (a.group_ptr && a.group_ptr[i + 1] > a.group_ptr[i]) {  // hub: merge the group partials
@@ -295,67 +349,9 @@ __device__ __forceinline__ void finalize_dst(const FinArgs& a, int64_t i) {
   }
   float ms = 0.f, den = 0.f;
   // (max, sum exp, sum exp*z) merge in item order (cgpexec.py:225-239)
-  if (mk == kMergeSoftmax) sm_header<CG>(part, a.pw, i0, i1, ms, den);
-  const float* st = nullptr;
-  if (a.stat) {
-    const int64_t v = a.stat_dst_ids[i];
-    if (v < a.stat_N) st = a.stat + v * a.stat_ld;
-  }
-  // softmax: the static (max, sum exp, sum exp z) triple joins the item partials
-  float sc_items = 1.f, sc_stat = 0.f;
-  if (st && mk == kMergeSoftmax) {
-    const float2 h = __ldg(reinterpret_cast<const float2*>(st));
-    if (h.y > 0.f) {
-      const float M = den > 0.f ? fmaxf(ms, h.x) : h.x;
-      sc_items = den > 0.f ? __expf(ms - M) : 0.f;
-      sc_stat = __expf(h.x - M);
-      den = den * sc_items + h.y * sc_stat;
-    }
-  }
-  const float* own = nullptr;
-  if (a.self_tab) {
-    const int64_t v = a.self_dst_ids[i];
-    own = v < a.self_N ? a.self_tab + v * a.self_ld : a.self_q + (v - a.self_N) * a.self_ld;
-  }
-  const float* dpe = nullptr;
-  float* drow = nullptr;
-  if (a.dbuf && i < *a.dT) {
-    const int64_t ld = (a.width + 3) & ~3;
-    dpe = a.dpe + (int64_t)a.self_dst_ids[i] * ld;
-    drow = a.dbuf + i * ld;
-  }
-  for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
-    float4 v = merge_cols<CG>(mk, part, a.pw, i0, i1, hdr, c4, ms);
-    if (st && mk == kMergeSoftmax) {
-      const float4 q = ld4f(st + hdr + c4);
-      v = make_float4(fmaf(sc_stat, q.x, v.x * sc_items), fmaf(sc_stat, q.y, v.y * sc_items),
-                      fmaf(sc_stat, q.z, v.z * sc_items), fmaf(sc_stat, q.w, v.w * sc_items));
-    } else if (st) {
-      const float4 q = ld4f(st + c4);
-      v = make_float4(q.x + v.x, q.y + v.y, q.z + v.z, q.w + v.w);
-    }
-    const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (c4 + t >= a.width) break;
-      float r;
-      if (mk == kMergeSoftmax) r = den > 0.f ? vv[t] / den : 0.f;
-      else if (mk == kMergeMax) r = cnt > 0 ? vv[t] : 0.f;
-      else if (a.gcn_norm) r = vv[t] / sqrtf((float)cnt + 1.f);  // agg / sqrt(|N(v)|+1) (models.py:217-218)
-      else if (a.kind == OB_KIND_POWER_MEAN) r = cnt > 0 ? powf(vv[t] / (float)cnt, 1.f / a.p) : 0.f;
-      else r = cnt > 0 ? vv[t] / (float)cnt : 0.f;  // mean
-      if (own) r = fmaxf(own[c4 + t] + r, 0.f);  // the same fp32 sum k_self_update formed
-      if (a.relu) r = fmaxf(r, 0.f);
-      a.out[i * a.ldo + c4 + t] = r;
-      if (drow) drow[c4 + t] = r - dpe[c4 + t];
-    }
-  }
-}
-
-__device__ __forceinline__ int atom_add_release(int32_t* p) {
-  int old;
-  asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
-  return old;
+  if (mk == kMergeSoftmax) sm_header<false>(part, a.pw, i0, i1, ms, den);
+  for (int c4 = lane * 4; c4 < a.width; c4 += 128)
+    fin_cols(a, i, cnt, c4, merge_cols<false>(mk, part, a.pw, i0, i1, hdr, c4, ms), ms, den);
 }
 
 // ---------------------------------------------------------------------------
@@ -393,9 +389,11 @@ struct AggArgs {
   // sources are ascending, so that is a contiguous run of every 32-edge group);
   // accumulate adds to the partials of the previous pass
   int pass = 0, passes = 1;  // pass p covers sources [S p / passes, S (p+1) / passes)
-  // fused merge (last pass, one column slice): the warp completing a destination's
-  // last item (or a hub destination's last group) merges and finalizes it
-  bool fused = false;
+  // direct mode: a destination with at most direct_items work items is one unit of
+  // work (its first item's warp gathers the whole row, the others skip); on the
+  // last pass that warp finalizes it from registers (fin_cols), no partial row
+  int direct_items = 0;
+  bool fused = false;  // last pass of a direct-mode launch
 };
 
 template <int OP, int NV>
@@ -426,8 +424,10 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = __ldg(a.item_dst + it);
     const int64_t j = it - a.item_ptr[i];
+    const bool whole = a.direct_items && a.item_ptr[i + 1] - a.item_ptr[i] <= a.direct_items;
+    if (whole && j > 0) continue;  // the first item's warp gathers the whole row
     int64_t e0 = a.dst_ptr[i] + j * kAggChunk;
-    const int64_t e1 = min(e0 + kAggChunk, a.dst_ptr[i + 1]);
+    const int64_t e1 = whole ? a.dst_ptr[i + 1] : min(e0 + kAggChunk, a.dst_ptr[i + 1]);
     int64_t csr_end = e0;  // delta mode: edges below this are the destination's CSR part
     if (a.skip_indeg) {
       const int64_t v = __ldg(a.skip_dst_ids + i);
@@ -532,6 +532,25 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
       }
     }
     AT* out = reinterpret_cast<AT*>(a.partial) + it * (int64_t)a.pw;
+    if constexpr (OP != kOpDSum && OP != kOpMom2) {
+      if (whole && a.fused) {  // the whole row is in registers: finalize it here
+        const int64_t cnt = a.dst_ptr[i + 1] - a.dst_ptr[i];
+        const float ms = e1 > e0 ? m_run : -INFINITY;
+        if (OP == kOpSoftmax) out += kSmHdr;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const int col = col0 + (q * 32 + lane) * 4;
+          if (col >= a.width) continue;
+          float4 v = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+          if (a.pass > 0) {  // the earlier source-range passes' sums of this row
+            const float4 o = __ldcg(reinterpret_cast<const float4*>(out + col));
+            v = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+          }
+          fin_cols(f, i, cnt, col, v, ms, den);
+        }
+        continue;
+      }
+    }
     if (OP == kOpSoftmax) {
       if (blockIdx.y == 0 && lane == 0) {
         out[0] = (e1 > e0) ? m_run : -INFINITY;
@@ -545,39 +564,6 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
 #pragma unroll
       for (int t = 0; t < 4; ++t)
         if (col + t < a.width) out[col + t] = a.pass > 0 ? out[col + t] + acc[q][t] : acc[q][t];
-    }
-    if constexpr (OP != kOpDSum && OP != kOpMom2) {
-      if (a.fused) {
-        // publish this item; the warp that completes the destination (or the hub
-        // destination's group, then the destination) merges in item order.  The
-        // counter add is a gpu-scope release (MEMBAR, no L1 invalidation: a full
-        // __threadfence would flush this SM's L1 of gathered rows on every item);
-        // the merging warp reads the partials with L2 loads (ld.global.cg) that are
-        // control-dependent on the count it observed
-        __syncwarp();
-        const int64_t gn = f.group_ptr ? f.group_ptr[i + 1] - f.group_ptr[i] : 0;
-        int last = 0;
-        if (lane == 0) {
-          if (gn > 0) {
-            const int64_t g = f.group_ptr[i] + j / kItemGroup;
-            const int64_t it0 = a.item_ptr[i] + (j / kItemGroup) * kItemGroup;
-            const int64_t n_in = min((int64_t)kItemGroup, a.item_ptr[i + 1] - it0);
-            last = atom_add_release(f.gcnt + g) == n_in - 1 ? 1 : 0;
-          } else {
-            const int64_t n_it = a.item_ptr[i + 1] - a.item_ptr[i];
-            last = atom_add_release(f.dcnt + i) == n_it - 1 ? 2 : 0;
-          }
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last == 1) {  // this group is complete: its second-level partial, then count it
-          reduce_group<true>(f, f.group_ptr[i] + j / kItemGroup);
-          __syncwarp();
-          int lg = 0;
-          if (lane == 0) lg = atom_add_release(f.dcnt + i) == gn - 1;
-          last = __shfl_sync(0xffffffffu, lg, 0) ? 2 : 0;
-        }
-        if (last == 2) finalize_dst<true>(f, i);
-      }
     }
   }
 }
@@ -596,7 +582,7 @@ __global__ void __launch_bounds__(256, OB_FIN_MINB) k_finalize(FinArgs a) {
   const int64_t D = a.cnt->D;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = gw; i < D; i += nw) finalize_dst<false>(a, i);
+  for (int64_t i = gw; i < D; i += nw) finalize_dst(a, i);
 }
 
 // moments finalize in float64: phase 1 -> mean (double), phase 2 -> signed root (float)
@@ -687,30 +673,28 @@ static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t it
   prof_end(s, pa, kProfFinalize, f.cnt, f.width, f.pw, 0, 0, 0);
 }
 
-// arrival counters of a fused merge: [D_max + 1] per destination, then per group
-inline int64_t fin_counters(int64_t D_max, int64_t items_max) { return 2 * D_max + items_max / kItemGroup + 2; }
-
-static bool fused_finalize_on() {
-  static const bool off = [] {
-    const char* v = std::getenv("OB_NO_FUSED_FINALIZE");
-    return v && v[0] && v[0] != '0';
+// direct mode: destinations of at most this many work items are gathered by one
+// warp and finalized from its registers (OB_DIRECT_ITEMS, 0 = off)
+static int direct_items() {
+  static const int n = [] {
+    const char* v = std::getenv("OB_DIRECT_ITEMS");
+    return v && v[0] ? std::max(0, std::atoi(v)) : 4;
   }();
-  return !off;
+  return n;
 }
 
-// aggregation + merge/normalise: one k_agg launch whose last-arriving warps merge
-// each destination (fcnt given, one column slice), else k_agg then k_finalize
+// aggregation + merge/normalise: in direct mode (one column slice) small
+// destinations are finalized inside k_agg and k_finalize merges only the rest
 template <int OP>
-static void agg_fin(cudaStream_t s, const AggArgs& a, FinArgs f, int32_t* fcnt, int64_t items_max, int64_t D_max,
+static void agg_fin(cudaStream_t s, const AggArgs& a0, FinArgs f, int64_t items_max, int64_t D_max,
                     int64_t S_split = 0) {
-  if (fcnt && a.width <= 512 && fused_finalize_on()) {
-    OB_CUDA(cudaMemsetAsync(fcnt, 0, sizeof(int32_t) * fin_counters(D_max, items_max), s));
-    f.dcnt = fcnt;
-    f.gcnt = fcnt + D_max + 1;
+  AggArgs a = a0;
+  if (a.width <= 512 && direct_items() > 0) {
+    a.direct_items = f.direct_items = direct_items();
     launch_agg<OP>(s, a, items_max, S_split, &f);
-    return;
+  } else {
+    launch_agg<OP>(s, a, items_max, S_split);
   }
-  launch_agg<OP>(s, a, items_max, S_split);
   finalize(s, f, D_max, items_max);
 }
 
@@ -838,7 +822,7 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     f.ldo = ldo;
     f.relu = true;
     const bool d = with_dnext(f);
-    agg_fin<kOpSoftmax>(s, a, f, sc.fcnt, r.items_max, r.D_max);
+    agg_fin<kOpSoftmax>(s, a, f, r.items_max, r.D_max);
     return d;
   }
   if (sp.kind == OB_KIND_GCN) {
@@ -849,10 +833,10 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
       f.ldo = ldo;
       f.relu = true;
       const bool d = with_dnext(f);
-      agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);
+      agg_fin<kOpSum>(s, a, f, r.items_max, r.D_max, split);
       return d;
     }
-    agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);
+    agg_fin<kOpSum>(s, a, f, r.items_max, r.D_max, split);
     TcGemmArgs g = gemm_args(r.D_dev, L.tw_main, out, ldo, true);
     g.a2 = sc.agg;
     g.lda2 = ld4(in);
@@ -880,11 +864,11 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     f.out = out;
     f.ldo = ldo;
     const bool d = with_dnext(f);
-    agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);
+    agg_fin<kOpSum>(s, a, f, r.items_max, r.D_max, split);
     return d;
   }
   if (sp.kind == OB_KIND_SAGE_MEAN && L.transform_first) {
-    agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);  // mean over Y = X W_neigh -> agg
+    agg_fin<kOpSum>(s, a, f, r.items_max, r.D_max, split);  // mean over Y = X W_neigh -> agg
     TcGemmArgs g = gemm_args(r.D_dev, L.tw_self, out, ldo, true);
     g.a1 = r.x;
     g.self = r.self;
@@ -895,9 +879,9 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
     return false;
   }
   if (sp.kind == OB_KIND_SAGE_MAX) {
-    agg_fin<kOpMax>(s, a, f, sc.fcnt, r.items_max, r.D_max);
+    agg_fin<kOpMax>(s, a, f, r.items_max, r.D_max);
   } else if (sp.kind == OB_KIND_POWER_MEAN) {
-    agg_fin<kOpPow>(s, a, f, sc.fcnt, r.items_max, r.D_max);
+    agg_fin<kOpPow>(s, a, f, r.items_max, r.D_max);
   } else if (sp.kind == OB_KIND_MOMENTS) {
     double* mean = reinterpret_cast<double*>(sc.mean);
     launch_agg<kOpDSum>(s, a, r.items_max);
@@ -909,7 +893,7 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
         r.cnt, r.dst_ptr, r.item_ptr, (const double*)sc.partial, in, 2, sp.n, nullptr, sc.agg, ld4(in));
     g_launches += 2;
   } else {  // sage_mean aggregate-first
-    agg_fin<kOpSum>(s, a, f, sc.fcnt, r.items_max, r.D_max, split);
+    agg_fin<kOpSum>(s, a, f, r.items_max, r.D_max, split);
   }
   // relu([h_v | agg] @ [W_self; W_neigh])
   TcGemmArgs g = gemm_args(r.D_dev, L.tw_main, out, ldo, true);
@@ -1360,7 +1344,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
     r.group_ptr = b.group_ptr;
     // with several requests in flight, big sum gathers run as L2-sized source-range passes
     r.split_gather = e.nlanes > 1;
-    LayerScratch sc{w.partial, w.partial2, w.agg, w.mean, w.z, w.s_src, w.s_dst, w.fcnt};
+    LayerScratch sc{w.partial, w.partial2, w.agg, w.mean, w.z, w.s_src, w.s_dst};
     const bool last = l == k;
     float* out = last ? d_out : w.outs[l];
     delta_ready = run_layer(s, L, r, sc, out, last ? L.spec.out_dim : ld4(L.spec.out_dim));
@@ -1646,7 +1630,6 @@ void stage_precompute(Engine& e) {
     float* s_src = (float*)talloc(sizeof(float) * N);
     float* s_dst = (float*)talloc(sizeof(float) * N);
     float* gscale = (float*)talloc(sizeof(float) * N);
-    int32_t* fcnt = (int32_t*)talloc(sizeof(int32_t) * fin_counters(N, items_max));
     k_node_scale<<<grid_for(N, 256), 256, 0, s>>>(e.g.indeg, N, gscale);
     OB_LAUNCHED();
     ScanScratch sc_scan;
@@ -1685,7 +1668,7 @@ void stage_precompute(Engine& e) {
       r.x = RowSrc{nullptr, h, hld};
       r.gscale = gscale;
       r.group_ptr = group_ptr;
-      LayerScratch scr{partial, partial2, agg, mean, z, s_src, s_dst, fcnt};
+      LayerScratch scr{partial, partial2, agg, mean, z, s_src, s_dst};
       run_layer(s, L, r, scr, out, old);
       e.pe[l - 1] = out;
       e.pe_dim[l - 1] = L.spec.out_dim;
