@@ -126,8 +126,10 @@ __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restri
 
 // ---------------------------------------------------------------------------
 // merge of a destination's partials (item order) and its normalisation /
-// epilogue -- run by k_finalize (a separate pass) or fused into k_agg, where
-// the warp that completes a destination's last work item merges it
+// epilogue (k_reduce_groups + k_finalize after k_agg).  Merging inside k_agg was
+// measured slower both ways it was tried: a per-item release fence + arrival
+// counter (fences stall the gather), and one warp per small destination (load
+// imbalance under the static item schedule); DESIGN.md "Tried".
 // ---------------------------------------------------------------------------
 constexpr int kAggWarps = 4;
 constexpr int kSmHdr = 4;    // softmax partial rows: [max logit, sum exp, pad, pad | values]
@@ -165,13 +167,9 @@ struct FinArgs {
   float* dbuf = nullptr;
   const float* dpe = nullptr;
   const int64_t* dT = nullptr;
-  // destinations with at most direct_items work items were gathered by one warp
-  // and finalized from its registers inside k_agg (0: none)
-  int direct_items = 0;
 };
 
-// partial-row loads: the non-coherent path for a separate pass, L2 (.cg) when the
-// partials were written by other warps of the same kernel
+// partial-row loads (non-coherent path; CG = L2 loads for partials written by the same kernel)
 template <bool CG>
 __device__ __forceinline__ float4 ldp4(const float* p) {
   return CG ? __ldcg(reinterpret_cast<const float4*>(p)) : __ldg(reinterpret_cast<const float4*>(p));
@@ -339,7 +337,6 @@ __device__ __forceinline__ void finalize_dst(const FinArgs& a, int64_t i) {
   const int mk = merge_kind(a.kind);
   const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
   int64_t i0 = a.item_ptr[i], i1 = a.item_ptr[i + 1];
-  if (a.direct_items && i1 - i0 <= a.direct_items) return;  // finalized by k_agg from registers
   const int64_t cnt = a.dst_ptr[i + 1] - a.dst_ptr[i];
   const float* part = a.partial;
   if (a.group_ptr && a.group_ptr[i + 1] > a.group_ptr[i]) {  // hub: merge the group partials
@@ -389,18 +386,13 @@ struct AggArgs {
   // sources are ascending, so that is a contiguous run of every 32-edge group);
   // accumulate adds to the partials of the previous pass
   int pass = 0, passes = 1;  // pass p covers sources [S p / passes, S (p+1) / passes)
-  // direct mode: a destination with at most direct_items work items is one unit of
-  // work (its first item's warp gathers the whole row, the others skip); on the
-  // last pass that warp finalizes it from registers (fin_cols), no partial row
-  int direct_items = 0;
-  bool fused = false;  // last pass of a direct-mode launch
 };
 
 template <int OP, int NV>
 #ifndef OB_AGG_MINB_WIDE
 #define OB_AGG_MINB_WIDE 1  // k_agg CTAs per SM for rows wider than 128 columns (NV = 2, 4)
 #endif
-__global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WIDE)) k_agg(AggArgs a, FinArgs f) {
+__global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WIDE)) k_agg(AggArgs a) {
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   const int lane = threadIdx.x & 31;
@@ -424,10 +416,8 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = __ldg(a.item_dst + it);
     const int64_t j = it - a.item_ptr[i];
-    const bool whole = a.direct_items && a.item_ptr[i + 1] - a.item_ptr[i] <= a.direct_items;
-    if (whole && j > 0) continue;  // the first item's warp gathers the whole row
     int64_t e0 = a.dst_ptr[i] + j * kAggChunk;
-    const int64_t e1 = whole ? a.dst_ptr[i + 1] : min(e0 + kAggChunk, a.dst_ptr[i + 1]);
+    const int64_t e1 = min(e0 + kAggChunk, a.dst_ptr[i + 1]);
     int64_t csr_end = e0;  // delta mode: edges below this are the destination's CSR part
     if (a.skip_indeg) {
       const int64_t v = __ldg(a.skip_dst_ids + i);
@@ -532,25 +522,6 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
       }
     }
     AT* out = reinterpret_cast<AT*>(a.partial) + it * (int64_t)a.pw;
-    if constexpr (OP != kOpDSum && OP != kOpMom2) {
-      if (whole && a.fused) {  // the whole row is in registers: finalize it here
-        const int64_t cnt = a.dst_ptr[i + 1] - a.dst_ptr[i];
-        const float ms = e1 > e0 ? m_run : -INFINITY;
-        if (OP == kOpSoftmax) out += kSmHdr;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          const int col = col0 + (q * 32 + lane) * 4;
-          if (col >= a.width) continue;
-          float4 v = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
-          if (a.pass > 0) {  // the earlier source-range passes' sums of this row
-            const float4 o = __ldcg(reinterpret_cast<const float4*>(out + col));
-            v = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
-          }
-          fin_cols(f, i, cnt, col, v, ms, den);
-        }
-        continue;
-      }
-    }
     if (OP == kOpSoftmax) {
       if (blockIdx.y == 0 && lane == 0) {
         out[0] = (e1 > e0) ? m_run : -INFINITY;
@@ -634,8 +605,7 @@ __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* sel
 constexpr int64_t kAggPassBytes = 64ll << 20;
 
 template <int OP>
-static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int64_t S_max = 0,
-                       const FinArgs* fused = nullptr) {
+static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int64_t S_max = 0) {
   const int nv = a0.width <= 128 ? 1 : (a0.width <= 256 ? 2 : 4);
   dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a0.width + 128 * nv - 1) / (128 * nv));
   int passes = 1;
@@ -644,16 +614,14 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
     passes = (int)std::min<int64_t>(4, (rows_bytes + kAggPassBytes - 1) / kAggPassBytes);
     if (passes < 1) passes = 1;
   }
-  const FinArgs f = fused ? *fused : FinArgs{};
   cudaEvent_t pa = prof_begin(s);
   for (int p = 0; p < passes; ++p) {
     AggArgs a = a0;
     a.pass = p;
     a.passes = passes;
-    a.fused = fused && p + 1 == passes;
-    if (nv == 1) k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a, f);
-    else if (nv == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a, f);
-    else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a, f);
+    if (nv == 1) k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a);
+    else if (nv == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a);
+    else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a);
     OB_LAUNCHED();
   }
   // K = -1 marks a stored-aggregate launch: it gathers only the request spans, which the
@@ -673,28 +641,11 @@ static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t it
   prof_end(s, pa, kProfFinalize, f.cnt, f.width, f.pw, 0, 0, 0);
 }
 
-// direct mode: destinations of at most this many work items are gathered by one
-// warp and finalized from its registers (OB_DIRECT_ITEMS, 0 = off)
-static int direct_items() {
-  static const int n = [] {
-    const char* v = std::getenv("OB_DIRECT_ITEMS");
-    return v && v[0] ? std::max(0, std::atoi(v)) : 4;
-  }();
-  return n;
-}
-
-// aggregation + merge/normalise: in direct mode (one column slice) small
-// destinations are finalized inside k_agg and k_finalize merges only the rest
+// aggregation, then the merge of each destination's partials and its epilogue
 template <int OP>
-static void agg_fin(cudaStream_t s, const AggArgs& a0, FinArgs f, int64_t items_max, int64_t D_max,
+static void agg_fin(cudaStream_t s, const AggArgs& a, const FinArgs& f, int64_t items_max, int64_t D_max,
                     int64_t S_split = 0) {
-  AggArgs a = a0;
-  if (a.width <= 512 && direct_items() > 0) {
-    a.direct_items = f.direct_items = direct_items();
-    launch_agg<OP>(s, a, items_max, S_split, &f);
-  } else {
-    launch_agg<OP>(s, a, items_max, S_split);
-  }
+  launch_agg<OP>(s, a, items_max, S_split);
   finalize(s, f, D_max, items_max);
 }
 
