@@ -160,6 +160,45 @@ class Clocks:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+class NvlinkCounter:
+    """NVML NVLink data counters of this rank's GPU (cumulative KiB, all links): bytes sent and received
+    between two reads, so the exchange's real NVLink traffic can sit next to its computed bytes."""
+
+    TX, RX = 138, 139  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+
+    def __init__(self, device):
+        self.h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[device]) if vis and vis.split(",")[device].isdigit() else device
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.links = [l for l in range(18) if self._link_ok(l)]
+        except Exception:
+            self.h = None
+
+    def _link_ok(self, l):
+        try:
+            return self.nv.nvmlDeviceGetNvLinkState(self.h, l) == 1
+        except Exception:
+            return False
+
+    def read(self):
+        if self.h is None or not self.links:
+            return None
+        ids = [(f, l) for l in self.links for f in (self.TX, self.RX)]
+        try:
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
+        except Exception:
+            return None
+        tx = sum(int(v.value.ullVal) for v, (f, _) in zip(vals, ids) if f == self.TX and v.nvmlReturn == 0)
+        rx = sum(int(v.value.ullVal) for v, (f, _) in zip(vals, ids) if f == self.RX and v.nvmlReturn == 0)
+        return tx * 1024, rx * 1024
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -500,6 +539,7 @@ def main():
     served = groups * B  # CGP: the P ranks of a group serve one batch together
     value_single = served * args.steps / (total_ms / 1e3)
     value, lanes_ms, launches_lanes, clk_lanes = value_single, None, None, None
+    nvl_measured = None
     lanes = 1 if args.lanes < 2 else args.lanes
     if lanes > 1:
         # throughput with two request lanes: consecutive requests alternate between two request
@@ -516,6 +556,8 @@ def main():
             torch.distributed.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
+        nvl = NvlinkCounter(local) if cgp else None
+        nvl0 = nvl.read() if nvl else None
         clocks = Clocks(local)
         l0 = eng.launch_count()
         with torch.cuda.stream(stream):
@@ -527,6 +569,13 @@ def main():
             b.record(stream)
         torch.cuda.synchronize()
         clk_lanes = clocks.stop()
+        nvl1 = nvl.read() if nvl else None
+        if nvl0 is not None and nvl1 is not None:
+            t = torch.tensor([float(nvl1[0] - nvl0[0]), float(nvl1[1] - nvl0[1])], device=dev)
+            torch.distributed.all_reduce(t)  # every rank's counters
+            nvl_measured = {"tx_bytes": int(t[0].item()), "rx_bytes": int(t[1].item()), "steps": args.steps,
+                            "per_step_bytes": int(t[1].item() / args.steps / max(groups, 1)),
+                            "source": "NVML NVLink data counters (all links, all ranks) around the throughput pass"}
         launches_lanes = eng.launch_count() - l0
         lanes_ms = a.elapsed_time(b)
         if world > 1:
@@ -690,7 +739,12 @@ def main():
         "gpu_launches": int(launches_lanes if launches_lanes is not None else launches),
         "request": {"edges": int(reqs[0].edges.shape[0]), "candidates": int(bd0.num_candidates),
                     "targets": int(bd0.num_targets), "fetch_bytes": int(bd0.fetch_bytes),
-                    "nvlink_bytes_per_step": int(bd0.collective_bytes) if cgp else 0},
+                    "nvlink_bytes_per_step": int(bd0.collective_bytes) if cgp else 0,
+                    **({"allgather_rows_bytes": int(bd0.allgather_bytes),
+                        "nvlink_note": "per request of one CGP group, all ranks: the exchange's bytes from the "
+                                       "request's actual destination counts; allgather_rows_bytes = the all-gather-"
+                                       "of-source-rows alternative sum_l (P-1) S_l row_bytes_l",
+                        "nvlink_measured": nvl_measured} if cgp else {})},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -101,13 +101,16 @@ typedef struct {
   double fetch_ms;          /* selection + graph construction (device time)          */
   double transfer_ms;       /* fetch_bytes / bandwidth, as the reference models it   */
   double compute_ms;        /* per-layer execution (device time)                     */
-  int64_t collective_bytes; /* bytes this engine sent to peers (NVLink)              */
+  int64_t collective_bytes; /* CGP: bytes moved between GPUs for the request, all ranks
+                               (NVLink exchange: from the request's actual sizes)      */
   int64_t fetch_bytes;      /* graph_fetch_bytes (runtime.py:105-120)                */
   int64_t num_candidates;
   int64_t num_targets;
   int64_t h2d_bytes;        /* request bytes copied host -> device                   */
   int64_t d2h_bytes;        /* result bytes copied device -> host                    */
   double total_device_ms;   /* whole request on the device                           */
+  int64_t allgather_bytes;  /* CGP: the all-gather-of-source-rows alternative,
+                               sum_l (P-1) S_l row_bytes_l           */
 } ob_breakdown;
 
 const char* ob_last_error(void);

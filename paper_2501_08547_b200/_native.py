@@ -65,6 +65,7 @@ class ObBreakdown(C.Structure):
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
         ("total_device_ms", C.c_double),
+        ("allgather_bytes", C.c_int64),
     ]
 
 

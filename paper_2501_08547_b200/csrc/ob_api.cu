@@ -603,6 +603,12 @@ static void finish_breakdown(Engine& e, const ReqCounters& rc, const std::vector
   bd->compute_ms = t12;
   bd->fetch_bytes = fb;
   bd->collective_bytes = e.cgp.collective_bytes;
+  if (cgp && e.cgp.nccl && e.cgp.p2p) {  // NVLink exchange: actual rows moved (all ranks)
+    cgp_traffic(e, rc, hc, &bd->collective_bytes, &bd->allgather_bytes);
+  } else if (cgp) {
+    int64_t nv = 0;
+    cgp_traffic(e, rc, hc, &nv, &bd->allgather_bytes);
+  }
   bd->transfer_ms = (double)bd->fetch_bytes / 12e9 * 1e3;
   bd->num_candidates = rc.R;
   bd->num_targets = rc.T;
@@ -1223,7 +1229,7 @@ int ob_serve_wait(ob_engine* h, int64_t ticket, ob_breakdown* bd) {
     local.fetch_ms = 0.0;  // the stage split is not recorded per slot
     local.compute_ms = ms;
     local.total_device_ms = ms;
-    local.collective_bytes = sl.collective_bytes;
+    if (!(e.cfg.strategy == OB_STRATEGY_SRPE_CGP && e.cgp.nccl && e.cgp.p2p)) local.collective_bytes = sl.collective_bytes;
     local.h2d_bytes = sl.h2d_bytes;
     local.d2h_bytes = sl.d2h_bytes;
     if (bd) *bd = local;

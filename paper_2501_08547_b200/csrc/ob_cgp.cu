@@ -517,7 +517,6 @@ void serve_cgp(Engine& e, float* d_out) {
   const bool p2p = c.nccl && c.p2p;
   const XCtx x = p2p ? xctx(e) : XCtx{};
   int xj = 0;  // exchange step within this request (selects the region)
-  c.nvlink_bytes = 0;
   auto x_begin = [&] { x_launch(s, k_x_begin, x); };
   auto x_exchange = [&] {  // publish this rank's region, wait for everyone's
     cudaEvent_t pc = prof_begin(s);
@@ -547,7 +546,6 @@ void serve_cgp(Engine& e, float* d_out) {
         ip.part[q] = reinterpret_cast<const double*>(c.xpeer[q] + kXFlags + xoff(c, xj));
       launch_score_is(e, w, ip);
       x_done();
-      c.nvlink_bytes += r_max * 8 * (c.P - 1);
     } else {
       for (int p = 0; p < np; ++p)
         launch_is_gather(e, w, e.is_tab[p], w.is_part + (int64_t)c.parts[p].rank * r_max);
@@ -621,7 +619,6 @@ void serve_cgp(Engine& e, float* d_out) {
                                                              c.sdst);
         OB_LAUNCHED();
         x_done();
-        c.nvlink_bytes += (int64_t)(D_max * 4 * (c.P - 1) / c.P);
       } else {
         k_rowdot_ptr<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.hvp, L.spec.in_dim, L.wa_dst, c.sdst);
         OB_LAUNCHED();
@@ -639,10 +636,36 @@ void serve_cgp(Engine& e, float* d_out) {
         lp0 = reinterpret_cast<float*>(reg);
         cnt0 = reinterpret_cast<float*>(reg + (((size_t)c.D_max * c.ldp * (mom ? 8 : 4) + 255) & ~(size_t)255));
       }
+      // layer 1 from the stored tables: transformed rows of the stored features, and the
+      // partitions' CSR-part sums (sum kinds)
+      const bool yt = l == 1 && e.ytab_ready && !e.ytab.empty() && e.ytab[0] && w.yrow;
+      if (yt) {
+        bc.ytab = e.ytab[0];
+        bc.y_ld = ld4(L.spec.out_dim);
+        bc.yrow = w.yrow;
+        bc.ydyn = w.z;
+        bc.dyn_src = w.dyn_src;
+        bc.ndyn = w.ndyn;
+      }
+      const bool sa = l == 1 && (int)e.cgp_sagg1.size() == np;
       for (int p = 0; p < np; ++p) {
         const BlockDev& b = c.ws[p].blocks[bi];
+        if (yt) OB_CUDA(cudaMemsetAsync(w.ndyn, 0, sizeof(int64_t), s));
         launch_resolve(s, bc, b.cnt, b.S_max, b.src_ids, w.rowp, w.gscale);
         LayerRun r{};
+        if (yt) {
+          r.yrow = w.yrow;
+          r.dyn_src = w.dyn_src;
+          r.ndyn = w.ndyn;
+          r.dyn_max = b.S_max;
+        }
+        if (sa) {
+          r.stat = e.cgp_sagg1[p];
+          r.stat_ld = ld4(L.transform_first ? L.spec.out_dim : L.spec.in_dim);
+          r.dst_ids = b.dst_ids;
+          r.indeg = c.parts[p].deg;
+          r.N = N;
+        }
         r.cnt = b.cnt;
         r.D_dev = &b.cnt->D;
         r.S_dev = &b.cnt->S;
@@ -672,7 +695,6 @@ void serve_cgp(Engine& e, float* d_out) {
           pp.lp[q] = reinterpret_cast<const float*>(reg);
           pp.cnt[q] = reinterpret_cast<const float*>(reg + cnt_off);
         }
-        c.nvlink_bytes += (int64_t)((double)D_max / c.P * (c.P - 1) * ((double)cgp_partial_width(L) * (mom ? 8 : 4) + 4));
       } else {
         if (c.nccl) {
           const int64_t pw = cgp_partial_width(L);
@@ -712,7 +734,6 @@ void serve_cgp(Engine& e, float* d_out) {
                                                                       8, mw, reinterpret_cast<float*>(c.mean));
         OB_LAUNCHED();
         x_done();
-        c.nvlink_bytes += (int64_t)(D_max * mw * 8 * (c.P - 1) / c.P);
       }
       if (ph == phases) cgp_update(s, L, D_dev, D_max, c.hvp, w.agg, out, ldo);
     }
@@ -729,8 +750,6 @@ void serve_cgp(Engine& e, float* d_out) {
       OB_LAUNCHED();
     }
     x_done();
-    c.nvlink_bytes += (int64_t)w.B * H * 4 * (c.P - 1) / c.P;
-    c.collective_bytes = c.nvlink_bytes;
   } else if (c.nccl) {
     const int H = e.layers.back().spec.out_dim;
     k_zero_foreign_queries<<<grid_for((int64_t)w.B * H, 256), 256, 0, s>>>(c.fin, w.B, H, c.P, c.my_rank);
@@ -739,6 +758,43 @@ void serve_cgp(Engine& e, float* d_out) {
     c.collective_bytes += (int64_t)w.B * H * 4;
   }
 #endif
+}
+
+// NVLink traffic of one request from its actual sizes (the block counters read
+// back after the request), summed over the P ranks, next to the all-gather-of-
+// source-rows alternative sum_l (P-1) S_l row_bytes_l.  The
+// exchange reads only real rows: an owner reads P-1 peers' partial rows of each
+// destination it owns (+ a 4-byte count); GAT destination scores and moments
+// means are read by every rank from the owners; rank 0 reads the query rows.
+void cgp_traffic(const Engine& e, const ReqCounters& rc, const std::vector<BlockCounters>& hc, int64_t* nvlink,
+                 int64_t* allgather) {
+  const CgpState& c = e.cgp;
+  const int k = (int)e.layers.size();
+  const double P = c.P, q = c.P - 1;
+  *nvlink = 0;
+  *allgather = 0;
+  if (c.P < 2 || hc.size() < 2) return;
+  const int np = (int)hc.size() / 2;  // (mid, last) per local partition
+  auto S_of = [&](int bi) {         // union of the partitions' sources (NCCL: P x this rank's)
+    double S = 0;
+    for (int p = 0; p < np; ++p) S += (double)hc[2 * p + bi].S;
+    return np == c.P ? S : S * P / np;
+  };
+  double nv = 0, ag = 0;
+  if (e.cfg.policy == OB_POLICY_IS) nv += P * q * (double)rc.R * 8;  // every rank reads every peer's numerators
+  for (int l = 1; l <= k; ++l) {
+    const LayerDev& L = e.layers[l - 1];
+    const int bi = l < k ? 0 : 1;
+    const double D = (double)hc[bi].D;
+    const bool mom = L.spec.kind == OB_KIND_MOMENTS;
+    if (L.spec.kind == OB_KIND_GAT) nv += q * D * 4;                       // s_dst from the owners
+    nv += (mom ? 2 : 1) * q * D * ((double)cgp_partial_width(L) * (mom ? 8 : 4) + 4);  // partials to owners
+    if (mom) nv += q * D * L.spec.in_dim * 8.0;                            // owners' means to every rank
+    ag += q * S_of(bi) * L.spec.in_dim * 4.0;
+  }
+  nv += q / P * (double)hc[1].D * e.layers.back().spec.out_dim * 4;       // query rows to rank 0
+  *nvlink = (int64_t)nv;
+  *allgather = (int64_t)ag;
 }
 
 #ifdef OB_WITH_NCCL

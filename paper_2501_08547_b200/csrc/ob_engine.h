@@ -607,7 +607,6 @@ struct CgpLaneState {
   char* xpeer[kMaxParts] = {};  // every rank's buffer in this address space (own = xbuf)
   int64_t* xep = nullptr;       // device step counter
   int64_t* xerr = nullptr;      // device failure word of this lane's exchange (sticky after a timeout)
-  int64_t nvlink_bytes = 0;     // per request, real-row bytes read from peers (host estimate)
 };
 
 struct CgpState : CgpLaneState {
@@ -646,6 +645,9 @@ void generate_graph(Engine& e, int64_t N, double avg, double exponent, int F, ui
 void generate_pe(Engine& e, int layer, int dim, uint64_t seed);
 __global__ void k_owner(int64_t N, int P, uint64_t seed, int32_t* owner);
 void carve_cgp(Engine& e, RequestWs& w, Arena& a);
+// NVLink bytes of a request from its counters (all ranks) and the all-gather-of-rows alternative
+void cgp_traffic(const Engine& e, const ReqCounters& rc, const std::vector<BlockCounters>& hc, int64_t* nvlink,
+                 int64_t* allgather);
 void serve_cgp(Engine& e, float* d_out);
 void cgp_destroy(Engine& e);
 void cgp_init_comm(Engine& e);
@@ -722,10 +724,14 @@ struct Engine {
   // delta aggregates (srpe mid-block layers l >= 2 of sum kinds): sagg_l[l-1][v] =
   // sum_{u in N(v)} w_u PE_{l-1}(u), raw, unnormalised; null where unused
   std::vector<float*> sagg_l;
+  // CGP: layer-1 stored aggregates per local partition (its source-split CSR)
+  std::vector<float*> cgp_sagg1;
   bool ytab_ready = false;
   void drop_ytab() {
     for (float* t : sagg_l) dfree(t);
     sagg_l.clear();
+    for (float* t : cgp_sagg1) dfree(t);
+    cgp_sagg1.clear();
     for (float* t : ytab) dfree(t);
     ytab.clear();
     dfree(sagg1);

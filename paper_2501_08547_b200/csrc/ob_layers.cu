@@ -87,7 +87,7 @@ __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restri
       // FEATURE rows of training nodes and PE rows are static: their x W is in the table
       const bool stat = (k == 0 && g < c.N) || k == 1;
       if (stat) {
-        c.yrow[s] = c.ytab + g * c.y_ld;
+        c.yrow[s] = c.ytab + (c.pos ? (int64_t)c.pos[g] : g) * c.y_ld;
       } else if (c.qxw && g >= c.N) {
         c.yrow[s] = c.qxw + (g - c.N) * c.y_ld;
       } else {
@@ -895,8 +895,17 @@ __global__ void __launch_bounds__(256) k_local_raw(FinArgs a, float* lp, int64_t
         o[1] = den;
       }
     }
+    const float* st = nullptr;  // this partition's stored CSR-part sum (sum kinds, layer 1)
+    if (a.stat) {
+      const int64_t v = a.stat_dst_ids[i];
+      if (v < a.stat_N) st = a.stat + v * a.stat_ld;
+    }
     for (int c4 = lane * 4; c4 < a.width; c4 += 128) {
-      const float4 v = merge_cols<false>(mk, part, a.pw, i0, i1, hdr, c4, ms);
+      float4 v = merge_cols<false>(mk, part, a.pw, i0, i1, hdr, c4, ms);
+      if (st) {
+        const float4 q = ld4f(st + c4);
+        v = make_float4(q.x + v.x, q.y + v.y, q.z + v.z, q.w + v.w);
+      }
       const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -1036,12 +1045,30 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   a.partial = sc.partial;
   a.p = sp.p;
   a.n = sp.n;
-  if (sp.kind == OB_KIND_GAT || L.transform_first) {
+  if (r.stat) {  // stored CSR-part sums of this partition: gather only the request suffix
+    a.skip_dst_ids = r.dst_ids;
+    a.skip_indeg = r.indeg;
+    a.skip_N = r.N;
+  }
+  RowSrc zrows{nullptr, sc.z, ld_out};
+  if ((sp.kind == OB_KIND_GAT || L.transform_first) && r.yrow) {
+    // stored transforms: owned training rows from the table, the listed rows (this
+    // partition's queries) through a GEMM
+    TcGemmArgs g = gemm_args(r.ndyn, L.tw_main, sc.z, ld_out, false);
+    g.a1 = r.x;
+    g.self = r.dyn_src;
+    g.K1 = in;
+    gemm(s, g, r.dyn_max, nullptr);
+    zrows = RowSrc{r.yrow, nullptr, 0};
+    a.x = zrows;
+    a.width = outd;
+    a.pw = ld4(outd);
+  } else if (sp.kind == OB_KIND_GAT || L.transform_first) {
     TcGemmArgs g = gemm_args(r.S_dev, L.tw_main, sc.z, ld_out, false);
     g.a1 = r.x;
     g.K1 = in;
     gemm(s, g, r.S_max, r.cnt);
-    a.x = RowSrc{nullptr, sc.z, ld_out};
+    a.x = zrows;
     a.width = outd;
     a.pw = ld4(outd);
   }
@@ -1056,8 +1083,7 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
     return;
   }
   if (sp.kind == OB_KIND_GAT) {
-    k_rowdot_rows<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, RowSrc{nullptr, sc.z, ld_out}, nullptr, outd,
-                                                       L.a_src, sc.s_src);
+    k_rowdot_rows<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, zrows, nullptr, outd, L.a_src, sc.s_src);
     OB_LAUNCHED();
     a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
@@ -1084,6 +1110,12 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   f.pw = a.pw;
   f.width = a.width;
   f.kind = sp.kind;
+  if (r.stat) {
+    f.stat = r.stat;
+    f.stat_ld = r.stat_ld;
+    f.stat_dst_ids = r.dst_ids;
+    f.stat_N = r.N;
+  }
   k_reduce_groups<<<grid_for(r.items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f);
   k_local_raw<<<grid_for(r.D_max, 8, kNumSMs * 16), 256, 0, s>>>(f, lp, ldp, lcnt);
   g_launches += 2;
@@ -1345,7 +1377,7 @@ void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d
 // warp per node, 4 columns per lane, rows in CSR order
 __global__ void k_sagg_build(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
                              RowSrc x, int width, const int32_t* __restrict__ indeg, bool gcn, float* out,
-                             int64_t ld) {
+                             int64_t ld, const int32_t* __restrict__ pos = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1355,7 +1387,8 @@ __global__ void k_sagg_build(int64_t N, const int64_t* __restrict__ off, const i
       for (int64_t e = off[v]; e < off[v + 1]; ++e) {
         const int32_t u = __ldg(nbrs + e);
         const float wgt = gcn ? (float)(1.0 / sqrt((double)__ldg(indeg + u) + 1.0)) : 1.f;
-        const float4 q = c4 < width ? __ldg(reinterpret_cast<const float4*>(x.row(u) + c4))
+        const int64_t ru = pos ? (int64_t)__ldg(pos + u) : u;  // stored row of u (owned rows under CGP)
+        const float4 q = c4 < width ? __ldg(reinterpret_cast<const float4*>(x.row(ru) + c4))
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
         acc.x = fmaf(wgt, q.x, acc.x);
         acc.y = fmaf(wgt, q.y, acc.y);
@@ -1416,6 +1449,61 @@ __global__ void k_sagg_gat_build(int64_t N, const int64_t* __restrict__ off, con
 }
 
 // ---------------------------------------------------------------------------
+// CGP ranks: layer-1 tables over the rows and edges a partition stores
+//   * stored transforms (GAT / transform-first layer 1): x_u W for every stored
+//     feature row (owned rows under NCCL partitioned storage, through pos)
+//   * stored aggregates (sum kinds, layer 1): per local partition p, the CSR-part
+//     sum over its source-split CSR, sum_{u in N_p(v)} w_u x_u (W), for every
+//     destination v; a request then gathers only its slice's request spans
+// Tables are skipped when they would take more than a third of free HBM (the
+// papers-shaped cfg4: N x H per partition does not fit).
+// ---------------------------------------------------------------------------
+static void build_cgp_tables(Engine& e) {
+  const char* off = std::getenv("OB_NO_STORED_TRANSFORMS");
+  if ((off && off[0] && off[0] != '0') || !e.g.feats || e.layers.empty()) return;
+  cudaStream_t s = e.stream;
+  const LayerDev& L1 = e.layers[0];
+  const int64_t N = e.g.N;
+  const int64_t rows = e.g.pos ? e.g.N_local : N;
+  const int k = (int)e.layers.size();
+  e.ytab.assign(k, nullptr);
+  size_t fb = 0, tb = 0;
+  int64_t* n_dev = (int64_t*)e.dalloc(sizeof(int64_t));
+  OB_CUDA(cudaMemcpyAsync(n_dev, &rows, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  if (L1.spec.kind == OB_KIND_GAT || L1.transform_first) {
+    const int64_t ld = ld4(L1.spec.out_dim);
+    OB_CUDA(cudaMemGetInfo(&fb, &tb));
+    if ((size_t)rows * ld * 4 <= fb / 3) {
+      e.ytab[0] = (float*)e.dalloc(sizeof(float) * std::max<int64_t>(rows, 1) * ld);
+      TcGemmArgs g = gemm_args(n_dev, L1.tw_main, e.ytab[0], ld, false);
+      g.a1 = RowSrc{nullptr, e.g.feats, e.g.F_ld};
+      g.K1 = L1.spec.in_dim;
+      tc_gemm(s, g, rows);
+    }
+  }
+  const char* off_sa = std::getenv("OB_NO_STORED_AGGREGATES");
+  const bool sa_off = off_sa && off_sa[0] && off_sa[0] != '0';
+  const bool sum_kind = L1.spec.kind == OB_KIND_GCN || L1.spec.kind == OB_KIND_SAGE_MEAN;
+  if (sum_kind && !sa_off && (!L1.transform_first || e.ytab[0])) {
+    const int w = L1.transform_first ? L1.spec.out_dim : L1.spec.in_dim;
+    const int64_t ld = ld4(w);
+    OB_CUDA(cudaMemGetInfo(&fb, &tb));
+    if ((size_t)N * ld * 4 * e.cgp.parts.size() <= fb / 3) {
+      const RowSrc x = L1.transform_first ? RowSrc{nullptr, e.ytab[0], ld} : RowSrc{nullptr, e.g.feats, e.g.F_ld};
+      for (auto& part : e.cgp.parts) {
+        float* t = (float*)e.dalloc(sizeof(float) * N * ld);
+        k_sagg_build<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, part.off, part.src, x, w, e.g.indeg,
+                                                                     L1.spec.kind == OB_KIND_GCN, t, ld, e.g.pos);
+        OB_LAUNCHED();
+        e.cgp_sagg1.push_back(t);
+      }
+    }
+  }
+  OB_CUDA(cudaStreamSynchronize(s));
+  e.dfree(n_dev);
+}
+
+// ---------------------------------------------------------------------------
 // stored transforms: x_v W for every training node whose layer input is static
 // ---------------------------------------------------------------------------
 void build_stored_transforms(Engine& e) {
@@ -1423,7 +1511,8 @@ void build_stored_transforms(Engine& e) {
   e.ytab_ready = true;  // decided once per (model, PE) state; tables may stay empty
   const char* off = std::getenv("OB_NO_STORED_TRANSFORMS");
   if (off && off[0] && off[0] != '0') return;
-  if (e.g.pos || e.cfg.strategy == OB_STRATEGY_SRPE_CGP || !e.g.feats) return;  // centralized, full tables
+  if (e.cfg.strategy == OB_STRATEGY_SRPE_CGP) return build_cgp_tables(e);
+  if (e.g.pos || !e.g.feats) return;  // centralized, full tables
   const int k = (int)e.layers.size();
   const int64_t N = e.g.N;
   std::vector<int> want(k, 0);

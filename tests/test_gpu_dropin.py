@@ -83,8 +83,9 @@ def test_reference_objects_unchanged(gn, workload, kind, k, strategy, gamma):
         eng.close()
 
 
-def test_reference_objects_cgp(gn, workload):
-    """srpe-cgp with P = 2 partitions (single-process emulation) against the reference's simulated ranks."""
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_reference_objects_cgp(gn, workload, P):
+    """srpe-cgp with P partitions (single-process emulation) against the reference's simulated ranks."""
     from paper_2501_08547_b200 import runtime as ours
 
     serving, reqs = workload
@@ -92,7 +93,7 @@ def test_reference_objects_cgp(gn, workload):
     model = M.make_model("sage_mean", 3, serving.feature_dim, 16)
     w = M.init_weights(model, 2)
     pe = G.precompute_embeddings(serving, model, w)
-    cfg = R.ServeConfig(strategy="srpe-cgp", gamma=0.1, num_partitions=2, seed=0)
+    cfg = R.ServeConfig(strategy="srpe-cgp", gamma=0.1, num_partitions=P, seed=0)
     ref = R.ServingEngine(serving, pe, model, w, cfg)
     eng = ours.ServingEngine(serving, pe, model, w, cfg)
     try:
@@ -100,6 +101,7 @@ def test_reference_objects_cgp(gn, workload):
         emb, bd = eng.serve(reqs[0])
         assert _rel(emb, r_emb) <= TOL
         assert bd.fetch_bytes == r_bd.fetch_bytes
+        assert np.array_equal(eng.partition_owner(), ref.pmap.owner)
     finally:
         eng.close()
 
