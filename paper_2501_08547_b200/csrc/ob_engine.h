@@ -98,7 +98,11 @@ struct TcWeights {
   int n0 = 0;  // first output column of this slab
   alignas(64) unsigned char map_hi[128] = {};  // CUtensorMap (TMA, 128B swizzle, box 32 x Np)
   alignas(64) unsigned char map_lo[128] = {};
-  bool map_ready = false;
+  alignas(64) unsigned char map_hi64[128] = {};  // 64- and 32-row boxes: column slabs of small-M launches
+  alignas(64) unsigned char map_lo64[128] = {};
+  alignas(64) unsigned char map_hi32[128] = {};
+  alignas(64) unsigned char map_lo32[128] = {};
+  bool map_ready = false, map64_ready = false, map32_ready = false;
   std::shared_ptr<TcWeights> next;  // the following column slab (N > 256)
 };
 
@@ -119,6 +123,7 @@ struct TcGemmArgs {
   const float* E;         // optional addend [M][lde] (before the activation)
   int64_t lde;
   bool relu;
+  int nslab = 1;          // column slabs of Np / nslab per work unit (set by tc_gemm)
 };
 
 struct LayerDev {

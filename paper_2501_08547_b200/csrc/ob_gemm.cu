@@ -214,6 +214,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t M = *g.M_dev;
   const int64_t tiles = (M + kTcBM - 1) / kTcBM;
+  // work units: (row tile, column slab); small-M GEMMs split the columns across
+  // CTAs (nslab > 1) so more SMs share the tile's MMAs and epilogue
+  const int ns = g.nslab;
+  const int64_t units = tiles * ns;
   const int KB1 = (g.K1 + kTcBK - 1) / kTcBK, KB2 = (g.K2 + kTcBK - 1) / kTcBK, KB = KB1 + KB2;
 
   if (tid == 0) {
@@ -250,7 +254,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     constexpr int kRowsPer = kTcBM / (kWarpsProd * 32 / 8);  // 8 rows per thread
     const int c = tid & 7, r0 = tid >> 3;
     uint32_t gk = 0;
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int64_t tile = u / ns;
       const float* p1[kRowsPer];
       const float* p2[kRowsPer];
 #pragma unroll
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // row r = this warp's TMEM lane quadrant x 32 + lane: read the (swizzled)
       // 128-byte row, write A_lo to this stage's TMEM columns
       const int q = warp & 3, r = q * 32 + lane;
-      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         for (int kb = 0; kb < KB; ++kb, ++gk) {
           const int s = gk % SA;
           mbar_wait(full_a + s, (gk / SA) & 1);
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     } else {
       // in place: trunc_tf32(a) in the A tile, A_lo in the stage's second tile
       const int t = tid - kWarpsProd * 32;
-      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
         for (int kb = 0; kb < KB; ++kb, ++gk) {
           const int s = gk % SA;
           mbar_wait(full_a + s, (gk / SA) & 1);
@@ -335,7 +340,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int q = warp - (kWarpsProd + kWarpsXf);  // TMEM lane quadrant (warp % 4)
     float* buf = epi_buf + q * 1024;
     uint32_t ti = 0;
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++ti) {
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++ti) {
+      const int64_t tile = u / ns;
+      const int n0 = (int)(u % ns) * NP;  // first column of this unit's slab
       const int acc = ti & 1;
       mbar_wait(tfull + acc, (ti >> 1) & 1);
       tc_fence_after();
@@ -347,7 +354,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) buf[lane * 32 + (j ^ lane)] = v[j];
         __syncwarp();
-        const int col = c0 + lane;
+        const int col = n0 + c0 + lane;
         const int64_t r0 = m0 + q * 32;
         if (g.E) {  // all 32 addend loads in flight before any is consumed
 #pragma unroll
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       const uint32_t idesc = tf32_idesc(NP);
       uint32_t gk = 0, ti = 0;
-      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++ti) {
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++ti) {
         const int acc = ti & 1;
         if (ti >= 2) mbar_wait(tempty + acc, ((ti >> 1) - 1) & 1);
         tc_fence_after();
@@ -407,14 +414,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- weight tiles: TMA into the B ring ----------------
     if (lane == 0) {
       uint32_t gk = 0;
-      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int n0 = (int)(u % ns) * NP;
         for (int kb = 0; kb < KB; ++kb, ++gk) {
           const int s = gk % SB;
           if (gk >= (uint32_t)SB) mbar_wait(empty_b + s, ((gk / SB) - 1) & 1);
           const uint32_t b_s = smem_u32(ring_b + s * SM::kStageB);
           mbar_expect_tx(full_b + s, SM::kStageB);
-          tma_load_2d(b_s, &map_hi, kb * kTcBK, 0, full_b + s);
-          tma_load_2d(b_s + SM::kTileB, &map_lo, kb * kTcBK, 0, full_b + s);
+          tma_load_2d(b_s, &map_hi, kb * kTcBK, n0, full_b + s);
+          tma_load_2d(b_s + SM::kTileB, &map_lo, kb * kTcBK, n0, full_b + s);
         }
       }
     }
@@ -447,14 +455,35 @@ void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max) {
   }
 }
 
-static void tc_gemm_slab(cudaStream_t s, const TcGemmArgs& g, int64_t M_max) {
-  OB_CHECK(g.N >= 1 && g.N <= 256, OB_ESTATE, "tc_gemm: N out of range");
-  OB_CHECK(g.w && g.w->map_ready, OB_ESTATE, "tc_gemm: weights not staged");
+static void tc_gemm_slab(cudaStream_t s, const TcGemmArgs& g0, int64_t M_max) {
+  OB_CHECK(g0.N >= 1 && g0.N <= 256, OB_ESTATE, "tc_gemm: N out of range");
+  OB_CHECK(g0.w && g0.w->map_ready, OB_ESTATE, "tc_gemm: weights not staged");
   const int64_t tiles = (M_max + kTcBM - 1) / kTcBM;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs));
-  const int np = g.Np;
-  const CUtensorMap& mh = *reinterpret_cast<const CUtensorMap*>(g.w->map_hi);
-  const CUtensorMap& ml = *reinterpret_cast<const CUtensorMap*>(g.w->map_lo);
+  TcGemmArgs g = g0;
+  // column slabs: pick the split with the fewest unit rounds on 148 SMs per unit of
+  // work, charging 15 % per extra slab for re-gathering the A rows
+  int np = g.Np, ns = 1;
+  double best = 1e30;
+  for (int sw : {g.Np, 64, 32}) {
+    if (sw > g.Np || (sw != g.Np && !(sw == 64 ? g.w->map64_ready : g.w->map32_ready))) continue;
+    const int n = g.Np / sw;
+    const double rounds = (double)((tiles * n + kNumSMs - 1) / kNumSMs);
+    const double cost = rounds / n * (1.0 + 0.15 * (n - 1));
+    if (cost < best - 1e-9) {
+      best = cost;
+      np = sw;
+      ns = n;
+    }
+  }
+  if (const char* v = std::getenv("OB_GEMM_NO_SLABS")) {
+    if (v[0] && v[0] != '0') np = g.Np, ns = 1;
+  }
+  g.nslab = ns;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * ns, kNumSMs));
+  const unsigned char* mh_raw = np == g.Np ? g.w->map_hi : (np == 64 ? g.w->map_hi64 : g.w->map_hi32);
+  const unsigned char* ml_raw = np == g.Np ? g.w->map_lo : (np == 64 ? g.w->map_lo64 : g.w->map_lo32);
+  const CUtensorMap& mh = *reinterpret_cast<const CUtensorMap*>(mh_raw);
+  const CUtensorMap& ml = *reinterpret_cast<const CUtensorMap*>(ml_raw);
   // smem opt-in is set at weight preparation (tc_gemm_configure), never while a
   // request is being captured into a CUDA graph
   auto go = [&](auto kern, int bytes) { kern<<<grid, kTcThreads, bytes, s>>>(g, mh, ml); };
@@ -489,11 +518,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static void make_map(void* out, float* base, int Np, int Kp) {
+static void make_map(void* out, float* base, int Np, int Kp, int box_rows = 0) {
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out);
   const cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)Np};
   const cuuint64_t strides[1] = {(cuuint64_t)Kp * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)Np};
+  const cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)(box_rows ? box_rows : Np)};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -551,6 +580,16 @@ static void prep_slab(Engine& e, const std::vector<const float*>& segs, const st
   OB_CUDA(cudaMemcpy(out->lo, lo.data(), sizeof(float) * lo.size(), cudaMemcpyHostToDevice));
   make_map(out->map_hi, out->hi, Np, Kp);
   make_map(out->map_lo, out->lo, Np, Kp);
+  if (Np > 64) {  // column-slab boxes for small-M launches
+    make_map(out->map_hi64, out->hi, Np, Kp, 64);
+    make_map(out->map_lo64, out->lo, Np, Kp, 64);
+    out->map64_ready = true;
+  }
+  if (Np > 32) {
+    make_map(out->map_hi32, out->hi, Np, Kp, 32);
+    make_map(out->map_lo32, out->lo, Np, Kp, 32);
+    out->map32_ready = true;
+  }
   out->map_ready = true;
 }
 
