@@ -528,6 +528,7 @@ static void enqueue_serve(Engine& e, int B, const float* d_q, int64_t m, const i
   cgp_localize_storage(e);  // NCCL CGP: keep only the owned rows (no-op otherwise)
   build_stored_transforms(e);  // once per (model, PE) state, outside any capture
   ensure_is_tables(e);
+  set_gemm_slabs(e.nlanes == 1);  // baked into the captured graph (graphs are re-captured on ob_set_lanes)
   cudaStream_t s = e.stream;
   prepare_workspace(e, B, std::max(bucket_m(m), e.m_reserved));
   RequestWs& w = e.ws;

@@ -531,6 +531,39 @@ void serve_cgp(Engine& e, float* d_out) {
   // identical plan on every rank from the whole request (runtime.py:151-192)
   cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, true);
+  // the slices' request-index sorts and query blocks (side stream) need only the
+  // request and the candidate set: they run beside the selection (main stream);
+  // the mid blocks follow the targets (as in the centralized pipeline)
+  OB_CUDA(cudaEventRecord(e.fork_ev, s));
+  OB_CUDA(cudaStreamWaitEvent(e.side, e.fork_ev, 0));
+  {
+    e.stream = e.side;
+    try {
+      cudaEvent_t pc = prof_begin(e.side);
+      for (int p = 0; p < np; ++p) {
+        CgpPartWs& pw = c.ws[p];
+        const PartitionDev& part = c.parts[p];
+        OB_CUDA(cudaMemsetAsync(pw.rq.ctr, 0, sizeof(int64_t) * 4, e.side));
+        OB_CUDA(cudaMemsetAsync(pw.blocks[0].cnt, 0, sizeof(BlockCounters), e.side));
+        OB_CUDA(cudaMemsetAsync(pw.blocks[1].cnt, 0, sizeof(BlockCounters), e.side));
+        if (w.m > 0) {
+          k_filter_slice<<<grid_for(w.m, 256), 256, 0, e.side>>>(w.rp, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
+                                                                  pw.rq.ctr);
+          OB_LAUNCHED();
+        }
+        build_rq_csr(e, w, pw.ledges, w.m, pw.rq.ctr, pw.rq, /*counts_ready=*/false);
+        const SpanSrc src{part.off, part.src, part.deg, pw.rq.ptr, pw.rq.src};
+        write_query_dst(e, w, pw.blocks[1]);
+        assemble(e, w, pw.blocks[1], src, w.bs[1]);
+      }
+      prof_end(e.side, pc, kProfBuild, nullptr, 0, 0, 0, 0, 0);
+      OB_CUDA(cudaEventRecord(e.csr_ev, e.side));
+    } catch (...) {
+      e.stream = s;
+      throw;
+    }
+    e.stream = s;
+  }
   stage_request_post(e, w, true);
   const int64_t r_max = std::min<int64_t>(N, 2 * w.m);
   if (e.cfg.policy == OB_POLICY_IS && r_max > 0) {
@@ -562,24 +595,14 @@ void serve_cgp(Engine& e, float* d_out) {
   }
   stage_select(e, w);
   prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
+  OB_CUDA(cudaStreamWaitEvent(s, e.csr_ev, 0));
   p0 = prof_begin(s);
   for (int p = 0; p < np; ++p) {
     CgpPartWs& pw = c.ws[p];
     const PartitionDev& part = c.parts[p];
-    OB_CUDA(cudaMemsetAsync(pw.rq.ctr, 0, sizeof(int64_t) * 4, s));
-    OB_CUDA(cudaMemsetAsync(pw.blocks[0].cnt, 0, sizeof(BlockCounters), s));
-    OB_CUDA(cudaMemsetAsync(pw.blocks[1].cnt, 0, sizeof(BlockCounters), s));
-    if (w.m > 0) {
-      k_filter_slice<<<grid_for(w.m, 256), 256, 0, s>>>(w.rp, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
-                                                         pw.rq.ctr);
-      OB_LAUNCHED();
-    }
-    build_rq_csr(e, w, pw.ledges, w.m, pw.rq.ctr, pw.rq, /*counts_ready=*/false);
     const SpanSrc src{part.off, part.src, part.deg, pw.rq.ptr, pw.rq.src};
     write_mid_dst(e, w, pw.blocks[0]);
     assemble(e, w, pw.blocks[0], src, w.bs[0]);
-    write_query_dst(e, w, pw.blocks[1]);
-    assemble(e, w, pw.blocks[1], src, w.bs[0]);
   }
   prof_end(s, p0, kProfBuild, nullptr, 0, 0, 0, 0, 0);
   record_mark(e.ev[1], s);

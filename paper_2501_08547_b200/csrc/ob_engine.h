@@ -154,6 +154,7 @@ struct GraphDev {
 };
 
 void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max);
+void set_gemm_slabs(bool on);  // column-slab splitting of small-M GEMMs (single-lane engines)
 struct Engine;
 void prep_tc_weights(Engine& e, const std::vector<const float*>& segs, const std::vector<int>& seg_k, int N,
                      TcWeights* out);

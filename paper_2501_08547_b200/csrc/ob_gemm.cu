@@ -455,6 +455,12 @@ void tc_gemm(cudaStream_t s, const TcGemmArgs& g, int64_t M_max) {
   }
 }
 
+// Column slabs spread a small-M GEMM over more SMs: lower latency for one request
+// at a time, but with request lanes the wider grids take whole SMs (smem, TMEM)
+// from the other lanes' kernels, so engines with lanes launch one slab per tile
+static thread_local bool t_gemm_slabs = true;
+void set_gemm_slabs(bool on) { t_gemm_slabs = on; }
+
 static void tc_gemm_slab(cudaStream_t s, const TcGemmArgs& g0, int64_t M_max) {
   OB_CHECK(g0.N >= 1 && g0.N <= 256, OB_ESTATE, "tc_gemm: N out of range");
   OB_CHECK(g0.w && g0.w->map_ready, OB_ESTATE, "tc_gemm: weights not staged");
@@ -478,6 +484,7 @@ static void tc_gemm_slab(cudaStream_t s, const TcGemmArgs& g0, int64_t M_max) {
   if (const char* v = std::getenv("OB_GEMM_NO_SLABS")) {
     if (v[0] && v[0] != '0') np = g.Np, ns = 1;
   }
+  if (!t_gemm_slabs) np = g.Np, ns = 1;
   g.nslab = ns;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles * ns, kNumSMs));
   const unsigned char* mh_raw = np == g.Np ? g.w->map_hi : (np == 64 ? g.w->map_hi64 : g.w->map_hi32);
