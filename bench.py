@@ -584,92 +584,99 @@ def main():
             lanes_ms = float(t.item())
         value = served * args.steps / (lanes_ms / 1e3)
 
-    # end to end through the public host-pointer API (pinned buffers, H2D + D2H inside the region)
+    # end to end through the public host-pointer API (pinned buffers, H2D + D2H inside the region).
+    # Request edges cross PCIe as int32 (src, dst) pairs (ob_serve_i32 / ob_serve_submit_i32: N + B < 2^31,
+    # widened on the device), the int64 path of the reference's own array type is measured beside it.
     e2e = None
     if not args.no_e2e:
-        pin_e = [torch.from_numpy(r.edges).pin_memory() for r in reqs]
-        pin_q = [torch.from_numpy(r.query_features).pin_memory() for r in reqs]
-        out_h = torch.empty((B, H), dtype=torch.float32).pin_memory()
         import ctypes as C
 
-        e2e_ms = []
-        h2d = d2h = 0
-        bd = nat.ObBreakdown()  # host-path calls capture their own graphs (output buffer differs)
-        for i in above + [0]:
-            nat.check(lib.ob_serve(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
-                                   C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(out_h.data_ptr()), C.byref(bd)))
-        for j in range(args.steps):
-            i = args.warmup + j
-            flush.fill_(j & 0xFF)
-            torch.cuda.synchronize()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            bd = nat.ObBreakdown()
-            nat.check(lib.ob_serve(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
-                                   C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(out_h.data_ptr()), C.byref(bd)))
-            b.record(stream)
-            b.synchronize()
-            e2e_ms.append(a.elapsed_time(b))
-            h2d += bd.h2d_bytes
-            d2h += bd.d2h_bytes
-        et = float(np.sum(e2e_ms))
-        # pipelined: the same requests through ob_serve_submit / ob_serve_wait (two in flight), so
-        # request t+1's inputs cross PCIe and t-1's rows return while t runs; every step still copies
-        # its inputs H2D from pinned memory and its rows D2H inside the timed region
+        pin_e64 = [torch.from_numpy(r.edges).pin_memory() for r in reqs]
+        pin_e32 = [torch.from_numpy(r.edges.astype(np.int32)).pin_memory() for r in reqs]
+        pin_q = [torch.from_numpy(r.query_features).pin_memory() for r in reqs]
+        out_h = torch.empty((B, H), dtype=torch.float32).pin_memory()
         depth = 4 if lanes > 1 else 2  # requests in flight on the pipelined path
         outs_p = [torch.empty((B, H), dtype=torch.float32).pin_memory() for _ in range(depth)]
 
-        def submit(i, slot):
-            t = C.c_int64()
-            nat.check(lib.ob_serve_submit(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
-                                          C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(outs_p[slot].data_ptr()),
-                                          C.byref(t)))
-            return t.value
+        def e2e_pass(i32):
+            serve_fn = lib.ob_serve_i32 if i32 else lib.ob_serve
+            submit_fn = lib.ob_serve_submit_i32 if i32 else lib.ob_serve_submit
+            pin_e = pin_e32 if i32 else pin_e64
+            e2e_ms, h2d, d2h = [], 0, 0
+            bd = nat.ObBreakdown()  # host-path calls capture their own graphs (output buffer differs)
+            for i in above + [0]:
+                nat.check(serve_fn(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
+                                   C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(out_h.data_ptr()), C.byref(bd)))
+            for j in range(args.steps):
+                i = args.warmup + j
+                flush.fill_(j & 0xFF)
+                torch.cuda.synchronize()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                bd = nat.ObBreakdown()
+                nat.check(serve_fn(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
+                                   C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(out_h.data_ptr()), C.byref(bd)))
+                b.record(stream)
+                b.synchronize()
+                e2e_ms.append(a.elapsed_time(b))
+                h2d += bd.h2d_bytes
+                d2h += bd.d2h_bytes
+            et = float(np.sum(e2e_ms))
 
-        def wait(t):
-            bdw = nat.ObBreakdown()
-            nat.check(lib.ob_serve_wait(eng._h, t, C.byref(bdw)))
-            return bdw
+            # pipelined: the same requests through submit / wait (depth in flight), so request t+1's
+            # inputs cross PCIe and t-1's rows return while t runs; every step still copies its inputs
+            # H2D from pinned memory and its rows D2H inside the timed region
+            def submit(i, slot):
+                t = C.c_int64()
+                nat.check(submit_fn(eng._h, B, C.c_void_p(pin_q[i].data_ptr()), pin_e[i].shape[0],
+                                    C.c_void_p(pin_e[i].data_ptr()), C.c_void_p(outs_p[slot].data_ptr()),
+                                    C.byref(t)))
+                return t.value
 
-        for i in above + [0]:  # every slot's (lane's) graph captured before timing
-            for sl in range(4):
-                wait(submit(i, sl % depth))
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        t_sub, t_done, pend = {}, {}, []
-        p0 = time.perf_counter()
-        for j in range(args.steps):
-            if len(pend) == depth:
-                tk, jj = pend.pop(0)
+            def wait(t):
+                bdw = nat.ObBreakdown()
+                nat.check(lib.ob_serve_wait(eng._h, t, C.byref(bdw)))
+                return bdw
+
+            for i in above + [0]:  # every slot's (lane's) graph captured before timing
+                for sl in range(4):
+                    wait(submit(i, sl % depth))
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            t_sub, t_done, pend = {}, {}, []
+            p0 = time.perf_counter()
+            for j in range(args.steps):
+                if len(pend) == depth:
+                    tk, jj = pend.pop(0)
+                    wait(tk)
+                    t_done[jj] = time.perf_counter()
+                t_sub[j] = time.perf_counter()
+                pend.append((submit(args.warmup + j, j % depth), j))
+            for tk, jj in pend:
                 wait(tk)
                 t_done[jj] = time.perf_counter()
-            t_sub[j] = time.perf_counter()
-            pend.append((submit(args.warmup + j, j % depth), j))
-        for tk, jj in pend:
-            wait(tk)
-            t_done[jj] = time.perf_counter()
-        pt = (time.perf_counter() - p0) * 1e3
-        if world > 1:
-            t = torch.tensor([pt], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            pt = float(t.item())
-        plat = [(t_done[j] - t_sub[j]) * 1e3 for j in range(args.steps)]
-        if world > 1:
-            t = torch.tensor([et], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            et = float(t.item())
-        e2e = {"value": round(served * args.steps / (pt / 1e3), 3), "unit": "queries/s",
-               "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
-               "mode": f"pipelined host API (ob_serve_submit/ob_serve_wait, {depth} requests in flight over "
-                       f"{lanes} request lane(s), pinned host buffers); wall clock over the K steps; no L2 flush "
-                       "(each request gathers > 0.5 GB)",
-               "p50_ms": float(np.percentile(plat, 50)), "p99_ms": float(np.percentile(plat, 99)),
-               "sync": {"value": round(served * args.steps / (et / 1e3), 3), "unit": "queries/s",
-                        "mode": "one ob_serve call per step (H2D, request, D2H, synchronise), CUDA events, "
-                                "L2 flushed before each step",
-                        "p50_ms": float(np.percentile(e2e_ms, 50)), "p99_ms": float(np.percentile(e2e_ms, 99))}}
+            pt = (time.perf_counter() - p0) * 1e3
+            if world > 1:
+                t = torch.tensor([pt, et], device=dev)
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                pt, et = float(t[0].item()), float(t[1].item())
+            plat = [(t_done[j] - t_sub[j]) * 1e3 for j in range(args.steps)]
+            return {"value": round(served * args.steps / (pt / 1e3), 3), "unit": "queries/s",
+                    "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
+                    "p50_ms": float(np.percentile(plat, 50)), "p99_ms": float(np.percentile(plat, 99)),
+                    "sync": {"value": round(served * args.steps / (et / 1e3), 3), "unit": "queries/s",
+                             "mode": "one synchronous call per step (H2D, request, D2H, synchronise), CUDA events, "
+                                     "L2 flushed before each step",
+                             "p50_ms": float(np.percentile(e2e_ms, 50)), "p99_ms": float(np.percentile(e2e_ms, 99))}}
+
+        e2e = e2e_pass(True)
+        e2e["mode"] = (f"pipelined host API (ob_serve_submit_i32/ob_serve_wait, {depth} requests in flight over "
+                       f"{lanes} request lane(s), pinned host buffers, request edges as int32 pairs); wall clock over "
+                       "the K steps; no L2 flush (each request gathers > 0.5 GB)")
+        e2e["int64_edges"] = e2e_pass(False)
+        e2e["int64_edges"]["mode"] = "the same with int64 edge pairs (ob_serve_submit / ob_serve), 16 bytes per edge"
 
     cpu = None
     parity = None

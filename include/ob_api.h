@@ -164,6 +164,10 @@ int ob_read_pe(ob_engine* e, int32_t layer, float* out_rows);
  * GPU every rank calls this with the full request; rank 0 receives `out`. */
 int ob_serve(ob_engine* e, int32_t num_queries, const float* query_features, int64_t num_edges,
              const int64_t* edges, float* out, ob_breakdown* bd);
+/* Same with int32 (src, dst) pairs (valid whenever N + B < 2^31, which the engine
+ * requires anyway): half the request's PCIe bytes; widened on the device. */
+int ob_serve_i32(ob_engine* e, int32_t num_queries, const float* query_features, int64_t num_edges,
+                 const int32_t* edges, float* out, ob_breakdown* bd);
 
 /* Same with device pointers (request already resident in HBM); `out` is a
  * device pointer.  Work is enqueued on the engine stream; with bd == NULL the
@@ -182,6 +186,8 @@ int ob_serve_device(ob_engine* e, int32_t num_queries, const float* d_query_feat
  * stay valid until the wait; pinned buffers give full overlap. */
 int ob_serve_submit(ob_engine* e, int32_t num_queries, const float* query_features, int64_t num_edges,
                     const int64_t* edges, float* out, int64_t* ticket);
+int ob_serve_submit_i32(ob_engine* e, int32_t num_queries, const float* query_features, int64_t num_edges,
+                        const int32_t* edges, float* out, int64_t* ticket);
 int ob_serve_wait(ob_engine* e, int64_t ticket, ob_breakdown* bd);
 
 /* Request lanes: with n > 1, consecutive ob_serve_device calls (and the

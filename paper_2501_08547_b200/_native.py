@@ -89,6 +89,8 @@ _SIGS = {
     "ob_serve": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(ObBreakdown)]),
     "ob_serve_device": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(ObBreakdown)]),
     "ob_serve_submit": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(C.c_int64)]),
+    "ob_serve_i32": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(ObBreakdown)]),
+    "ob_serve_submit_i32": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P, C.POINTER(C.c_int64)]),
     "ob_serve_wait": (C.c_int, [_P, C.c_int64, C.POINTER(ObBreakdown)]),
     "ob_set_lanes": (C.c_int, [_P, C.c_int32]),
     "ob_lanes_fork": (C.c_int, [_P]),

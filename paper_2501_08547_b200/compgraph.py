@@ -71,7 +71,10 @@ class ServingRequest:
 
     def __post_init__(self):
         self.query_features = np.ascontiguousarray(self.query_features, dtype=np.float32)
-        self.edges = np.ascontiguousarray(np.asarray(self.edges, dtype=np.int64).reshape(-1, 2))
+        # int64 like the reference; int32 pairs are kept as given (the engine ships them as
+        # 8 bytes per edge and widens on the device)
+        e = np.asarray(self.edges)
+        self.edges = np.ascontiguousarray(e.reshape(-1, 2) if e.dtype == np.int32 else e.astype(np.int64).reshape(-1, 2))
         if not np.all(np.isfinite(self.query_features)):
             raise ValueError("query features must be finite")
         hi = self.num_base + self.num_queries

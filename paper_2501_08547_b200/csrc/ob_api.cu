@@ -787,6 +787,8 @@ struct PipeSlot {
   size_t cap_h_out = 0;
   float* user_out = nullptr;
   size_t out_bytes = 0;
+  int32_t* d_edges32 = nullptr;  // int32 host edges land here and are widened on the device
+  size_t cap_edges32 = 0;
 };
 constexpr int kMaxCounted = 64;
 constexpr int kPipeSlots = 4;  // requests in flight on the pipelined host path
@@ -799,6 +801,8 @@ struct ob_engine {
   float* d_q = nullptr;
   float* d_out = nullptr;
   size_t cap_edges = 0, cap_q = 0, cap_out = 0;
+  int32_t* d_edges32 = nullptr;
+  size_t cap_edges32 = 0;
   // pipelined host path (ob_serve_submit / ob_serve_wait): two slots, so request
   // t+1's inputs cross PCIe while request t runs and t-1's rows come back
   PipeSlot slot[kPipeSlots];
@@ -831,6 +835,37 @@ static void ensure(T*& p, size_t& cap, size_t n) {
   size_t c = std::max<size_t>(n, 64);
   OB_CUDA(cudaMalloc(&p, sizeof(T) * c));
   cap = c;
+}
+
+// int32 (src, dst) request edges -> the int64 pairs the pipeline reads (8 host bytes
+// per edge over PCIe instead of 16)
+__global__ void k_widen_edges(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  const int64_t n4 = n / 4;
+  OB_GRID_STRIDE(i, n4) {
+    const int4 v = __ldg(reinterpret_cast<const int4*>(in) + i);
+    reinterpret_cast<longlong2*>(out)[2 * i] = make_longlong2(v.x, v.y);
+    reinterpret_cast<longlong2*>(out)[2 * i + 1] = make_longlong2(v.z, v.w);
+  }
+  OB_GRID_STRIDE(j, n - 4 * n4) out[4 * n4 + j] = in[4 * n4 + j];
+}
+
+template <class T>
+static void stage_edges(const T* src, int64_t m, int64_t*& d64, size_t& cap64, int32_t*& d32, size_t& cap32,
+                        cudaStream_t copy_s) {
+  ensure(d64, cap64, (size_t)(2 * m));
+  if (!m) return;
+  if constexpr (sizeof(T) == 8) {
+    OB_CUDA(cudaMemcpyAsync(d64, src, sizeof(int64_t) * 2 * m, cudaMemcpyHostToDevice, copy_s));
+  } else {
+    ensure(d32, cap32, (size_t)(2 * m));
+    OB_CUDA(cudaMemcpyAsync(d32, src, sizeof(int32_t) * 2 * m, cudaMemcpyHostToDevice, copy_s));
+  }
+}
+template <class T>
+static void widen_edges(int64_t m, int64_t* d64, const int32_t* d32, cudaStream_t s) {
+  if (sizeof(T) == 8 || !m) return;
+  k_widen_edges<<<grid_for(m / 2 + 1, 256), 256, 0, s>>>(d32, 2 * m, d64);
+  OB_LAUNCHED();
 }
 
 extern "C" {
@@ -903,10 +938,12 @@ int ob_engine_destroy(ob_engine* h) {
     if (h->d2h) cudaStreamSynchronize(h->d2h);
     cudaStreamSynchronize(h->impl.stream);
     if (h->d_edges) cudaFree(h->d_edges);
+    if (h->d_edges32) cudaFree(h->d_edges32);
     if (h->d_q) cudaFree(h->d_q);
     if (h->d_out) cudaFree(h->d_out);
     for (auto& sl : h->slot) {
       if (sl.d_edges) cudaFree(sl.d_edges);
+      if (sl.d_edges32) cudaFree(sl.d_edges32);
       if (sl.d_q) cudaFree(sl.d_q);
       if (sl.d_out) cudaFree(sl.d_out);
       if (sl.h_rc) cudaFreeHost(sl.h_rc);
@@ -1095,8 +1132,11 @@ int ob_read_pe(ob_engine* h, int32_t layer, float* out) {
   });
 }
 
-int ob_serve(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* edges, float* out,
-             ob_breakdown* bd) {
+}  // extern "C" (the host-path templates have C++ linkage)
+
+template <class T>
+static int serve_host(ob_engine* h, int32_t B, const float* q, int64_t m, const T* edges, float* out,
+                      ob_breakdown* bd) {
   return guarded([&] {
     OB_CHECK(h, OB_EINVAL, "null engine");
     std::lock_guard<std::mutex> lk(h->mu);
@@ -1107,21 +1147,33 @@ int ob_serve(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* 
     OB_CHECK(m == 0 || edges, OB_EINVAL, "null edges");
     OB_CHECK(out, OB_EINVAL, "null output");
     const int H = e.layers.back().spec.out_dim;
-    ensure(h->d_edges, h->cap_edges, (size_t)(2 * m));
+    cudaStream_t s = e.stream;
+    stage_edges(edges, m, h->d_edges, h->cap_edges, h->d_edges32, h->cap_edges32, s);
     ensure(h->d_q, h->cap_q, (size_t)B * e.g.F);
     ensure(h->d_out, h->cap_out, (size_t)B * H);
-    cudaStream_t s = e.stream;
-    if (m) OB_CUDA(cudaMemcpyAsync(h->d_edges, edges, sizeof(int64_t) * 2 * m, cudaMemcpyHostToDevice, s));
     if ((int64_t)B * e.g.F) OB_CUDA(cudaMemcpyAsync(h->d_q, q, sizeof(float) * B * e.g.F, cudaMemcpyHostToDevice, s));
+    widen_edges<T>(m, h->d_edges, h->d_edges32, s);
     ob_breakdown local{};
     serve_device(e, B, h->d_q, m, h->d_edges, h->d_out, &local);
     e.last_lane = 0;
     if ((int64_t)B * H) OB_CUDA(cudaMemcpyAsync(out, h->d_out, sizeof(float) * B * H, cudaMemcpyDeviceToHost, s));
     OB_CUDA(cudaStreamSynchronize(s));
-    local.h2d_bytes = 16 * m + 4 * (int64_t)B * e.g.F;
+    local.h2d_bytes = 2 * (int64_t)sizeof(T) * m + 4 * (int64_t)B * e.g.F;
     local.d2h_bytes = 4 * (int64_t)B * H;
     if (bd) *bd = local;
   });
+}
+
+extern "C" {
+
+int ob_serve(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* edges, float* out,
+             ob_breakdown* bd) {
+  return serve_host(h, B, q, m, edges, out, bd);
+}
+
+int ob_serve_i32(ob_engine* h, int32_t B, const float* q, int64_t m, const int32_t* edges, float* out,
+                 ob_breakdown* bd) {
+  return serve_host(h, B, q, m, edges, out, bd);
 }
 
 // Pipelined host path.  Request t uses slot t % kPipeSlots (four slots): its
@@ -1132,8 +1184,11 @@ int ob_serve(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* 
 // returns request t's rows in `out` and its breakdown (errors of request t are
 // raised there).  The D2H into `out` overlaps only when `out` is pinned
 // (page-locked) host memory; a pageable `out` makes the submit wait for it.
-int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* edges, float* out,
-                    int64_t* ticket) {
+}  // extern "C"
+
+template <class T>
+static int submit_host(ob_engine* h, int32_t B, const float* q, int64_t m, const T* edges, float* out,
+                       int64_t* ticket) {
   return guarded([&] {
     OB_CHECK(h && ticket, OB_EINVAL, "null argument");
     std::lock_guard<std::mutex> lk(h->mu);
@@ -1157,10 +1212,9 @@ int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const in
     }
     const int H = e.layers.back().spec.out_dim;
     // the slot is idle: its previous request was waited for, so its buffers can be resized
-    ensure(sl.d_edges, sl.cap_edges, (size_t)(2 * m));
+    stage_edges(edges, m, sl.d_edges, sl.cap_edges, sl.d_edges32, sl.cap_edges32, h->h2d);
     ensure(sl.d_q, sl.cap_q, (size_t)B * e.g.F);
     ensure(sl.d_out, sl.cap_out, (size_t)B * H);
-    if (m) OB_CUDA(cudaMemcpyAsync(sl.d_edges, edges, sizeof(int64_t) * 2 * m, cudaMemcpyHostToDevice, h->h2d));
     if ((int64_t)B * e.g.F)
       OB_CUDA(cudaMemcpyAsync(sl.d_q, q, sizeof(float) * B * e.g.F, cudaMemcpyHostToDevice, h->h2d));
     OB_CUDA(cudaEventRecord(sl.h2d_done, h->h2d));
@@ -1170,6 +1224,7 @@ int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const in
     cudaStream_t s = e.stream;
     OB_CUDA(cudaStreamWaitEvent(s, sl.h2d_done, 0));
     OB_CUDA(cudaEventRecord(sl.start, s));
+    widen_edges<T>(m, sl.d_edges, sl.d_edges32, s);
     enqueue_serve(e, B, sl.d_q, m, sl.d_edges, sl.d_out);
     std::vector<BlockDev*> all = counted_blocks(e);
     OB_CHECK((int)all.size() <= kMaxCounted, OB_ESTATE, "too many blocks for the pipelined readback");
@@ -1197,12 +1252,24 @@ int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const in
     sl.n_bc = (int)all.size();
     sl.busy = true;
     sl.ticket = t;
-    sl.h2d_bytes = 16 * m + 4 * (int64_t)B * e.g.F;
+    sl.h2d_bytes = 2 * (int64_t)sizeof(T) * m + 4 * (int64_t)B * e.g.F;
     sl.d2h_bytes = 4 * (int64_t)B * H;
     sl.collective_bytes = e.cgp.collective_bytes;
     h->next_ticket = t + 1;
     *ticket = t;
   });
+}
+
+extern "C" {
+
+int ob_serve_submit(ob_engine* h, int32_t B, const float* q, int64_t m, const int64_t* edges, float* out,
+                    int64_t* ticket) {
+  return submit_host(h, B, q, m, edges, out, ticket);
+}
+
+int ob_serve_submit_i32(ob_engine* h, int32_t B, const float* q, int64_t m, const int32_t* edges, float* out,
+                        int64_t* ticket) {
+  return submit_host(h, B, q, m, edges, out, ticket);
 }
 
 int ob_serve_wait(ob_engine* h, int64_t ticket, ob_breakdown* bd) {

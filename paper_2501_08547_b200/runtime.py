@@ -242,7 +242,8 @@ class ServingEngine:
         q = _f32(request.query_features)
         if q.shape != (B, self.dataset.feature_dim):
             raise ValueError("query features must be B x F")
-        e = np.ascontiguousarray(request.edges, dtype=np.int64)
+        e = np.asarray(request.edges)
+        e = np.ascontiguousarray(e if e.dtype == np.int32 else e.astype(np.int64, copy=False)).reshape(-1, 2)
         out = np.empty((B, self.model.layers[-1].out_dim), dtype=np.float32)
         return B, q, e, out
 
@@ -250,8 +251,8 @@ class ServingEngine:
         """runtime.py:308-358."""
         B, q, e, out = self._request_arrays(request)
         bd = nat.ObBreakdown()
-        nat.check(self._lib.ob_serve(self._h, B, nat.ptr(q), int(e.shape[0]), nat.ptr(e), nat.ptr(out),
-                                     C.byref(bd)))
+        fn = self._lib.ob_serve_i32 if e.dtype == np.int32 else self._lib.ob_serve  # int32 pairs: half the PCIe bytes
+        nat.check(fn(self._h, B, nat.ptr(q), int(e.shape[0]), nat.ptr(e), nat.ptr(out), C.byref(bd)))
         return out, self._breakdown(bd)
 
     def serve_stream(self, requests, depth: int = 2):
@@ -275,8 +276,8 @@ class ServingEngine:
                         break
                     B, q, e, out = self._request_arrays(req)
                     t = C.c_int64()
-                    nat.check(self._lib.ob_serve_submit(self._h, B, nat.ptr(q), int(e.shape[0]), nat.ptr(e),
-                                                        nat.ptr(out), C.byref(t)))
+                    fn = self._lib.ob_serve_submit_i32 if e.dtype == np.int32 else self._lib.ob_serve_submit
+                    nat.check(fn(self._h, B, nat.ptr(q), int(e.shape[0]), nat.ptr(e), nat.ptr(out), C.byref(t)))
                     pending.append((t.value, out, (q, e)))
                 if not pending:
                     return

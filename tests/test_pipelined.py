@@ -151,3 +151,27 @@ def test_source_range_passes_match_oracle():
         assert OL.max_rel_err(b, ref["emb"]) <= 1e-4
         assert OL.max_rel_err(a, b) <= 1e-5
     eng.close()
+
+
+@pytest.mark.parametrize("lanes", [1, 3])
+def test_int32_edges_equal_int64(setup, lanes):
+    """int32 (src, dst) host edges (ob_serve_i32 / ob_serve_submit_i32, widened on the device) give the
+    int64 path's rows bit for bit, and half its request edge bytes."""
+    from paper_2501_08547_b200 import runtime
+    from paper_2501_08547_b200.compgraph import ServingRequest
+
+    serving, model, w, pe, reqs = setup
+    eng = runtime.ServingEngine(serving, pe, model, w, runtime.ServeConfig(strategy="srpe", gamma=0.2))
+    eng.set_lanes(lanes)
+    r32 = [ServingRequest(r.num_base, r.num_queries, r.query_features, r.edges.astype(np.int32)) for r in reqs]
+    assert all(r.edges.dtype == np.int32 for r in r32)
+    ref = [eng.serve(r) for r in reqs]
+    got = [eng.serve(r) for r in r32]
+    for (a, ba), (b, bb) in zip(got, ref):
+        assert np.array_equal(a, b)
+        assert ba.fetch_bytes == bb.fetch_bytes
+    assert eng.last_breakdown.h2d_bytes == 8 * reqs[-1].edges.shape[0] + 4 * reqs[-1].query_features.size
+    stream = list(eng.serve_stream(r32 + reqs, depth=4))
+    for i, (a, _) in enumerate(stream):
+        assert np.array_equal(a, ref[i % len(reqs)][0])
+    eng.close()
