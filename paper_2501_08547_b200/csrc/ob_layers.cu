@@ -604,9 +604,20 @@ __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* sel
 // passes, each touching a slice of the rows that stays L2-resident.
 constexpr int64_t kAggPassBytes = 64ll << 20;
 
+// widest column slice per warp (OB_AGG_NV_MAX: 4 = 512 columns; 2 splits 512-wide rows into two
+// 256-column slices on blockIdx.y, each warp then needs ~40 % fewer registers)
+static int agg_nv_max() {
+  static const int n = [] {
+    const char* v = std::getenv("OB_AGG_NV_MAX");
+    const int x = v && v[0] ? std::atoi(v) : 4;
+    return x >= 4 ? 4 : (x >= 2 ? 2 : 1);
+  }();
+  return n;
+}
+
 template <int OP>
 static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int64_t S_max = 0) {
-  const int nv = a0.width <= 128 ? 1 : (a0.width <= 256 ? 2 : 4);
+  const int nv = std::min(agg_nv_max(), a0.width <= 128 ? 1 : (a0.width <= 256 ? 2 : 4));
   dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a0.width + 128 * nv - 1) / (128 * nv));
   int passes = 1;
   if (OP == kOpSum && S_max > 0 && !a0.skip_indeg && !a0.dprev) {
