@@ -531,23 +531,28 @@ void serve_cgp(Engine& e, float* d_out) {
   // identical plan on every rank from the whole request (runtime.py:151-192)
   cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, true);
+  static const bool serial = [] {  // OB_CGP_SERIAL=1: slice sorts on the main stream (A/B)
+    const char* v = std::getenv("OB_CGP_SERIAL");
+    return v && v[0] && v[0] != '0';
+  }();
+  cudaStream_t side = serial ? s : e.side;
   // the slices' request-index sorts and query blocks (side stream) need only the
   // request and the candidate set: they run beside the selection (main stream);
   // the mid blocks follow the targets (as in the centralized pipeline)
   OB_CUDA(cudaEventRecord(e.fork_ev, s));
-  OB_CUDA(cudaStreamWaitEvent(e.side, e.fork_ev, 0));
+  OB_CUDA(cudaStreamWaitEvent(side, e.fork_ev, 0));
   {
-    e.stream = e.side;
+    e.stream = side;
     try {
-      cudaEvent_t pc = prof_begin(e.side);
+      cudaEvent_t pc = prof_begin(side);
       for (int p = 0; p < np; ++p) {
         CgpPartWs& pw = c.ws[p];
         const PartitionDev& part = c.parts[p];
-        OB_CUDA(cudaMemsetAsync(pw.rq.ctr, 0, sizeof(int64_t) * 4, e.side));
-        OB_CUDA(cudaMemsetAsync(pw.blocks[0].cnt, 0, sizeof(BlockCounters), e.side));
-        OB_CUDA(cudaMemsetAsync(pw.blocks[1].cnt, 0, sizeof(BlockCounters), e.side));
+        OB_CUDA(cudaMemsetAsync(pw.rq.ctr, 0, sizeof(int64_t) * 4, side));
+        OB_CUDA(cudaMemsetAsync(pw.blocks[0].cnt, 0, sizeof(BlockCounters), side));
+        OB_CUDA(cudaMemsetAsync(pw.blocks[1].cnt, 0, sizeof(BlockCounters), side));
         if (w.m > 0) {
-          k_filter_slice<<<grid_for(w.m, 256), 256, 0, e.side>>>(w.rp, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
+          k_filter_slice<<<grid_for(w.m, 256), 256, 0, side>>>(w.rp, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
                                                                   pw.rq.ctr);
           OB_LAUNCHED();
         }
@@ -556,8 +561,8 @@ void serve_cgp(Engine& e, float* d_out) {
         write_query_dst(e, w, pw.blocks[1]);
         assemble(e, w, pw.blocks[1], src, w.bs[1]);
       }
-      prof_end(e.side, pc, kProfBuild, nullptr, 0, 0, 0, 0, 0);
-      OB_CUDA(cudaEventRecord(e.csr_ev, e.side));
+      prof_end(side, pc, kProfBuild, nullptr, 0, 0, 0, 0, 0);
+      OB_CUDA(cudaEventRecord(e.csr_ev, side));
     } catch (...) {
       e.stream = s;
       throw;

@@ -617,7 +617,10 @@ static int agg_nv_max() {
 
 template <int OP>
 static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int64_t S_max = 0) {
-  const int nv = std::min(agg_nv_max(), a0.width <= 128 ? 1 : (a0.width <= 256 ? 2 : 4));
+  // sum gathers of 512-wide rows run as two 256-column slices (measured +1-3 % on the
+  // H = 512 GCN configs; the softmax kind keeps one 512-column warp, -4 % otherwise)
+  const int nv_cap = OP == kOpSum ? std::min(agg_nv_max(), 2) : agg_nv_max();
+  const int nv = std::min(nv_cap, a0.width <= 128 ? 1 : (a0.width <= 256 ? 2 : 4));
   dim3 grid(grid_for(items_max, kAggWarps, kNumSMs * 16), (a0.width + 128 * nv - 1) / (128 * nv));
   int passes = 1;
   if (OP == kOpSum && S_max > 0 && !a0.skip_indeg && !a0.dprev) {
