@@ -709,11 +709,12 @@ def main():
             "launches": agg["n"], "avg_launch_us": round(agg["ms"] * 1e3 / max(agg["n"], 1), 2),
             "gathered_row_gbs": round(agg["flops"] / (agg["ms"] / 1e3) / 1e9, 1) if agg["ms"] > 0 else None,
             "gather_ceiling_gbs": 15200.0,  # measured random 512-B row gather, L2-sized table (profiles/r01_gather_ceiling.md)
-            "note": "rows are re-read once per edge (avg source out-degree in the block), mostly from L2; "
-                    "gathered_row_gbs is that served traffic, the kernel's real limiter (L2 fabric). The "
-                    "layer-1 launch under stored aggregates gathers only the request spans, which the block "
-                    "counters do not size: it contributes its edge list and partials but no row bytes "
-                    "(both figures are conservative)",
+            "note": "k_agg is bound by the per-SM L2->SM return path, not HBM: rows are re-read once per "
+                    "edge, ~70-80 % from L2 (gathered_row_gbs = the row bytes the launches actually gathered, "
+                    "against the measured 15.2 TB/s random-row gather ceiling). achieved counts algorithmic "
+                    "bytes (each unique row once): the layer-1 launch (stored aggregates) its edge list and "
+                    "partials, the layer-2 launch (delta aggregates) its edge list, the recomputed rows (<= D) "
+                    "and partials, the query-block launch its edge list, every source row once and partials",
             "share_of_step": round(agg["ms"] / max(reqp["ms"], 1e-9), 3)}
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,

@@ -1566,6 +1566,7 @@ int ob_profile_read(ob_engine* h, int32_t cls, double* total_ms, int64_t* launch
         // delta launch: edge list, the recomputed rows it gathers (at most the D block rows) and
         // the partials
         by += 4.0 * c.E + 4.0 * r.width * c.D + 4.0 * r.pw * c.items;
+        fl += 4.0 * r.width * c.gathered;  // rows it actually gathered (device count)
       } else if (cls == kProfAgg && r.K < 0) {
         // stored-aggregate launch: rows gathered for the request spans only (not sized by the
         // block counters) -- count the edge list and the partials, no rows (conservative)

@@ -51,7 +51,7 @@ struct BlockCounters {
   int64_t feat_src;    // FEATURE-bound training sources (fetch bytes)
   int64_t pe_src;      // PE-bound sources (fetch bytes)
   int64_t groups;      // second-level partial groups (hub destinations)
-  int64_t pad;
+  int64_t gathered;    // rows gathered by delta-mode aggregations over this block (profiler)
 };
 
 // A computation block in device memory (CSR over destinations).

@@ -413,6 +413,7 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
   __shared__ const float* c_row[kAggWarps][32];  // delta mode: the group's kept edges, compacted
   __shared__ float c_w[kAggWarps][32];
   const int wib = threadIdx.x >> 5;
+  int64_t kept = 0;  // delta mode: rows this warp gathered (for the profiler's byte count)
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = __ldg(a.item_dst + it);
     const int64_t j = it - a.item_ptr[i];
@@ -457,6 +458,7 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
       int first = __ffs(inb) - 1;
       const int cnt = __popc(inb);
       if (d_lo) {
+        kept += cnt;
         if (in_l) {
           const int slot = __popc(inb & ((1u << lane) - 1u));
           c_row[wib][slot] = r_l;
@@ -537,6 +539,8 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
         if (col + t < a.width) out[col + t] = a.pass > 0 ? out[col + t] + acc[q][t] : acc[q][t];
     }
   }
+  if (d_lo && lane == 0 && kept && blockIdx.y == 0)
+    atomicAdd((unsigned long long*)&const_cast<BlockCounters*>(a.cnt)->gathered, (unsigned long long)kept);
 }
 
 __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
