@@ -384,7 +384,7 @@ def main():
     ap.add_argument("--gamma", type=float, default=None)
     ap.add_argument("--strategy", default="srpe", choices=["srpe", "full", "sampled"],
                     help="single-GPU / replica strategy (CGP runs srpe-cgp); config 5's ablation axis")
-    ap.add_argument("--policy", default="ratio", choices=["ratio", "is"],
+    ap.add_argument("--policy", default="ratio", choices=["ratio", "is", "random"],
                     help="SRPE scoring policy (policy.py:29-32)")
     ap.add_argument("--lanes", type=int, default=4,
                     help="request lanes for the throughput pass (1 = one request at a time)")

@@ -61,7 +61,9 @@ enum ob_strategy { OB_STRATEGY_FULL = 0, OB_STRATEGY_SAMPLED = 1, OB_STRATEGY_SR
 /* ServeConfig.policy (policy.py:29-32): ratio (policy.py:77-81) and importance
    (policy.py:84-107; under srpe-cgp the per-partition numerators are summed in
    rank order, runtime.py:168-175). */
-enum ob_policy { OB_POLICY_RATIO = 0, OB_POLICY_IS = 1 };
+/* ratio: query-edge ratio (policy.py:77-81); is: importance (policy.py:84-107);
+ * random: default_rng(seed).permutation of the candidates (policy.py:122-124) */
+enum ob_policy { OB_POLICY_RATIO = 0, OB_POLICY_IS = 1, OB_POLICY_RANDOM = 2 };
 
 /* Layer kinds use the reference's on-disk tags (models.py:36 KIND_TAGS). */
 enum ob_kind {

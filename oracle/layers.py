@@ -212,7 +212,7 @@ def precompute(layers, weights, offsets, nbrs, feats):
 
 
 def serve(strategy, layers, weights, num_base, num_queries, offsets, nbrs, feats, qfeat, edges,
-          pe_layers=None, gamma=0.0, fanouts=None, seed=0):
+          pe_layers=None, gamma=0.0, fanouts=None, seed=0, policy="ratio"):
     """ServingEngine.serve for the centralized strategies (runtime.py:290-335).
 
     Returns a dict with the plan, the blocks, the query embeddings and the
@@ -231,8 +231,12 @@ def serve(strategy, layers, weights, num_base, num_queries, offsets, nbrs, feats
         if pe_layers is None:
             raise ValueError("reuse strategy needs stored embeddings")
         ids, nq, total = st.candidates(edges, num_base, deg)
-        scores = st.ratio_scores(nq, total)
-        targets = st.select_top(ids, scores, gamma)
+        if policy == "random":  # runtime.py:182-183, policy.py:122-124
+            scores = np.zeros(len(ids))
+            targets = st.select_random(ids, gamma, seed)
+        else:
+            scores = st.ratio_scores(nq, total)
+            targets = st.select_top(ids, scores, gamma)
         plan = dict(ids=ids, nq=nq, total=total, scores=scores, targets=targets)
         blocks = st.build_srpe(num_base, num_queries, offsets, nbrs, edges, targets, k, len(pe_layers))
     else:

@@ -149,3 +149,67 @@ def numpy_choice_set(n: int, size: int, seed: int, layer: int, v: int) -> np.nda
     """The reference's own call (compgraph.py:272-273), for pinning the restatement."""
     rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(layer, int(v))))
     return np.sort(rng.choice(n, size=size, replace=False))
+
+
+# ---------------------------------------------------------------------------
+# RANDOM selection policy (policy.py:122-124): default_rng(tie_seed).permutation(|R|)
+# ---------------------------------------------------------------------------
+
+
+def random_interval(g: Pcg64, mx: int) -> int:
+    """numpy's random_interval (distributions.c): masked rejection on 32-bit draws (mx < 2^32)."""
+    if mx == 0:
+        return 0
+    mask = mx
+    for s in (1, 2, 4, 8, 16):
+        mask |= mask >> s
+    while True:
+        v = g.next32() & mask
+        if v <= mx:
+            return v
+
+
+def permutation_prefix(m: int, budget: int, seed: int) -> list[int]:
+    """default_rng(seed).permutation(m)[:budget]: numpy's Fisher-Yates shuffle of arange(m)
+    (Generator.shuffle: for i = m-1 .. 1, j = random_interval(i), swap a[i], a[j])."""
+    g = Pcg64(seed_state(seed, ()))
+    a = list(range(m))
+    for i in range(m - 1, 0, -1):
+        j = random_interval(g, i)
+        a[i], a[j] = a[j], a[i]
+    return a[:budget]
+
+
+def swap_draws(m: int, seed: int) -> list[int]:
+    """j_i for i = 1 .. m-1 (index i), the draws the shuffle makes (drawn for i = m-1 first)."""
+    g = Pcg64(seed_state(seed, ()))
+    j = [0] * max(m, 1)
+    for i in range(m - 1, 0, -1):
+        j[i] = random_interval(g, i)
+    return j
+
+
+def permutation_prefix_traced(m: int, budget: int, seed: int) -> list[int]:
+    """The same prefix without performing the swaps -- the order the CUDA path evaluates it in.
+
+    The shuffle applies transpositions t_i = (i, j_i) for i = m-1 down to 1, so the final array
+    is a[p] = t_1(t_2(... t_{m-1}(p) ...)) read right to left as "apply t_{m-1} last":
+    a[p] = (t_{m-1} o ... o t_1)(p).  Tracing p forward through i = 1 .. m-1: nothing moves it
+    before step p (j_i <= i < p); at step p it becomes j_p; afterwards it moves only when a
+    later step draws exactly its current value x, and then to that step's index.  So a[p] is
+    found by hopping to the first later step whose draw equals the current value.
+    """
+    j = swap_draws(m, seed)
+    occ: dict[int, list[int]] = {}
+    for i in range(1, m):
+        occ.setdefault(j[i], []).append(i)  # ascending steps per drawn value
+    out = []
+    for p in range(budget):
+        x, s = (j[p], p) if p > 0 else (0, 0)
+        while True:
+            nxt = [i for i in occ.get(x, []) if i > s]
+            if not nxt:
+                break
+            x = s = nxt[0]
+        out.append(x)
+    return out

@@ -234,6 +234,18 @@ def importance_scores_distributed(ids: np.ndarray, partials: list, train_deg: np
     return np.where(deg > 0, sums / np.maximum(deg, 1.0), 0.0)
 
 
+def select_random(ids: np.ndarray, gamma: float, seed: int) -> np.ndarray:
+    """select_targets with policy RANDOM (policy.py:118-135): the first floor(gamma*|R|) of
+    default_rng(seed).permutation(|R|), sorted; the permutation restated in oracle/sampling.py."""
+    from .sampling import permutation_prefix
+
+    if not 0.0 <= gamma <= 1.0:
+        raise ValueError("gamma must lie in [0, 1]")
+    budget = int(np.floor(float(gamma) * len(ids)))
+    order = np.asarray(permutation_prefix(len(ids), budget, int(seed)), dtype=_I64)
+    return np.sort(np.asarray(ids, dtype=_I64)[order]).astype(_I64)
+
+
 def select_top(ids: np.ndarray, scores: np.ndarray, gamma: float) -> np.ndarray:
     """select_targets (policy.py:110-135): top floor(gamma*|R|), score desc, id asc."""
     if not 0.0 <= gamma <= 1.0:

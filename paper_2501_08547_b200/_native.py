@@ -19,7 +19,7 @@ OB_OK, OB_EINVAL, OB_ENOTFOUND, OB_ECOMM, OB_ECUDA, OB_ENOMEM, OB_ESTATE = range
 STRATEGY = {"full": 0, "sampled": 1, "srpe": 2, "srpe-cgp": 3}
 MAX_FANOUT = 200  # OB_MAX_FANOUT
 MAX_LAYERS = 8
-POLICY = {"ratio": 0, "is": 1}
+POLICY = {"ratio": 0, "is": 1, "random": 2}
 KIND_TAGS = {"gcn": 0, "sage_mean": 1, "gat": 2, "power_mean": 3, "moments": 4, "sage_max": 5}
 
 

@@ -187,6 +187,14 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   // IS numerators: one array centralized, one per partition under CGP emulation,
   // [P][R] for the NCCL all-gather fallback
   w.is_part = e.cfg.policy == OB_POLICY_IS ? a.take<double>(p.R_max * std::max(1, e.cfg.num_partitions)) : nullptr;
+  if (e.cfg.policy == OB_POLICY_RANDOM) {
+    w.rnd_raw = a.take<uint32_t>(4 * p.R_max + 4096);
+    w.rnd_j = a.take<int32_t>(p.R_max + 1);
+    w.rnd_cnt = a.take<int32_t>(p.R_max + 2);
+    w.rnd_fill = a.take<int32_t>(p.R_max + 2);
+    w.rnd_off = a.take<int64_t>(p.R_max + 2);
+    w.rnd_lst = a.take<int32_t>(p.R_max + 1);
+  }
   w.cand_tpos = a.take<int32_t>(p.R_max);
   w.targets = a.take<int32_t>(p.T_max + 1);
   w.sel_hist = a.take<uint32_t>(257);  // [256] = round completion counter
@@ -347,6 +355,7 @@ static void raise_request_errors(const ReqCounters& rc) {
   if (rc.err & kErrNoQuery) throw Error(OB_EINVAL, "every request edge needs a query endpoint");
   if (rc.err & kErrNonFinite) throw Error(OB_EINVAL, "query features must be finite");
   if (rc.err & kErrZeroTotal) throw Error(OB_EINVAL, "candidate with zero total degree");
+  if (rc.err & kErrRandom) throw Error(OB_ECUDA, "random policy: draw stream exhausted");
   if (rc.err & kErrComm) throw Error(OB_ECOMM, "CGP exchange: a peer rank did not signal in time (OB_CGP_TIMEOUT_MS)");
 }
 
@@ -887,8 +896,8 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
         OB_CHECK(cfg->fanouts[l] <= OB_MAX_FANOUT, OB_EINVAL, "fanout above OB_MAX_FANOUT (200)");
       }
     }
-    OB_CHECK(cfg->policy == OB_POLICY_RATIO || cfg->policy == OB_POLICY_IS, OB_EINVAL,
-             "unknown policy (ratio and is run on the device)");
+    OB_CHECK(cfg->policy == OB_POLICY_RATIO || cfg->policy == OB_POLICY_IS || cfg->policy == OB_POLICY_RANDOM,
+             OB_EINVAL, "unknown policy (ratio, is and random run on the device)");
     OB_CHECK(cfg->num_partitions >= 1, OB_EINVAL, "num_partitions must be >= 1");
     OB_CHECK(cfg->strategy == OB_STRATEGY_SRPE_CGP || cfg->num_partitions == 1, OB_EINVAL,
              "num_partitions > 1 needs strategy srpe-cgp");

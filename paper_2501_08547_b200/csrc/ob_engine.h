@@ -26,6 +26,7 @@ enum ErrBits : int64_t {
   kErrZeroTotal = 4,    // candidate with zero total degree (policy.py:79-80)
   kErrNonFinite = 8,    // query feature not finite
   kErrComm = 16,        // a CGP peer never signalled (NVLink exchange timeout)
+  kErrRandom = 32,      // RANDOM policy: the generated draw stream ran out (not reached in practice)
 };
 
 // Device-side counters of one request (one allocation, read back once).
@@ -262,6 +263,13 @@ struct RequestWs {
   double* cand_score = nullptr;    // [R]
   uint64_t* cand_key = nullptr;    // [R]
   double* is_part = nullptr;       // [R] IS numerators (centralized; CGP: [P][R])
+  // RANDOM policy: raw 32-bit draws, per-step draws j_i, per-value step lists
+  uint32_t* rnd_raw = nullptr;     // [4 R_max + 4096]
+  int32_t* rnd_j = nullptr;        // [R_max]
+  int32_t* rnd_cnt = nullptr;      // [R_max + 1]
+  int32_t* rnd_fill = nullptr;     // [R_max + 1]
+  int64_t* rnd_off = nullptr;      // [R_max + 1]
+  int32_t* rnd_lst = nullptr;      // [R_max]
   int32_t* cand_tpos = nullptr;    // [R] position in targets or -1
   int32_t* targets = nullptr;      // [T]
   int64_t* sel_pos = nullptr;      // [R+1]

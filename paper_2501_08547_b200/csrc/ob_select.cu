@@ -1017,6 +1017,8 @@ void stage_request_post(Engine& e, RequestWs& w, bool need_scores) {
   }
 }
 
+static void select_random(Engine& e, RequestWs& w, int64_t r_max);  // RANDOM policy (below)
+
 void stage_select(Engine& e, RequestWs& w) {
   cudaStream_t s = e.stream;
   const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
@@ -1030,7 +1032,12 @@ void stage_select(Engine& e, RequestWs& w) {
   }
   k_budget<<<1, 256, 0, s>>>(w.rc, e.cfg.gamma, w.sel_hist);
   OB_LAUNCHED();
-  for (int shift = 56; shift >= 0; shift -= 8) {
+  if (e.cfg.policy == OB_POLICY_RANDOM) {
+    // zero scores (runtime.py:182-183); the chosen ranks' keys are 1 against threshold 0
+    OB_CUDA(cudaMemsetAsync(w.cand_score, 0, sizeof(double) * std::max<int64_t>(r_max, 1), s));
+    select_random(e, w, r_max);
+  }
+  for (int shift = 56; shift >= 0 && e.cfg.policy != OB_POLICY_RANDOM; shift -= 8) {
     k_sel_round<<<grid_for(r_max, 256, kNumSMs * 2), 256, 0, s>>>(w.cand_key, w.rc, shift, w.sel_hist);
     OB_LAUNCHED();
   }
@@ -1038,6 +1045,273 @@ void stage_select(Engine& e, RequestWs& w) {
   const SelLoad ld{w.cand_key, w.rc};
   device_scan_t<I3>(s, e.scan, ld, SelStore3{ld, w.cand_ids, w.targets, w.cand_tpos}, SelTotal{w.rc}, &w.rc->R, 0,
                     r_max);
+}
+
+// ---------------------------------------------------------------------------
+// 2c. RANDOM policy (policy.py:122-124): order = default_rng(tie_seed).permutation(|R|),
+//     targets = sort(ids[order[:budget]]).
+//
+// numpy's permutation is a Fisher-Yates shuffle of arange(R): for i = R-1 .. 1,
+// j_i = random_interval(i) (masked rejection on the PCG64 stream's 32-bit draws, low
+// half of each 64-bit output first), swap a[i], a[j_i].  The device never performs the
+// swaps:
+//   1. k_rnd_raw: the raw 32-bit draw stream, each thread jumping the 128-bit LCG
+//      ahead to its chunk (O(log n) affine-map squaring) -- fully parallel;
+//   2. k_rnd_draws: one warp assigns draws to steps.  Acceptance of draw r depends on
+//      how many earlier draws were rejected, so each lane evaluates its draw under 16
+//      hypotheses (k earlier rejections) and the warp resolves the chain with one
+//      ballot per hypothesis: ~32 draws per iteration instead of one;
+//   3. position p's final value is found by tracing p through the transpositions
+//      (oracle/sampling.py permutation_prefix_traced): it becomes j_p at step p and
+//      afterwards hops to the first later step whose draw equals its current value --
+//      per-value step lists (count, scan, fill, sort the short lists), one thread per
+//      p < budget;
+//   4. the chosen ranks are flagged in the selection keys and the existing ordered
+//      compaction writes the targets ascending.
+// ---------------------------------------------------------------------------
+constexpr int kRndHyp = 16;  // rejections one warp iteration can resolve
+constexpr int kRndChunk = 64;  // 64-bit outputs per thread in k_rnd_raw
+
+__host__ __device__ inline int64_t rnd_raw_len(int64_t R) { return 4 * R + 4096; }  // 32-bit draws generated
+
+struct Pcg128 {
+  unsigned __int128 s, inc;
+};
+
+__device__ __forceinline__ unsigned __int128 pcg_mult() {
+  return ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+}
+
+// state after `delta` steps of s <- a s + inc (pcg's affine-map squaring)
+__device__ __forceinline__ unsigned __int128 pcg_advance(unsigned __int128 st, unsigned __int128 inc, uint64_t delta) {
+  unsigned __int128 acc_m = 1, acc_p = 0, cur_m = pcg_mult(), cur_p = inc;
+  while (delta) {
+    if (delta & 1) {
+      acc_m *= cur_m;
+      acc_p = acc_p * cur_m + cur_p;
+    }
+    cur_p = (cur_m + 1) * cur_p;
+    cur_m *= cur_m;
+    delta >>= 1;
+  }
+  return acc_m * st + acc_p;
+}
+
+__device__ __forceinline__ uint64_t pcg_out(unsigned __int128 st) {  // XSL-RR
+  const uint64_t hi = (uint64_t)(st >> 64), lo = (uint64_t)st;
+  const unsigned rot = (unsigned)(hi >> 58);
+  const uint64_t x = hi ^ lo;
+  return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+__global__ void k_rnd_raw(Pcg128 g, const ReqCounters* rc, uint32_t* raw) {
+  const int64_t n64 = rnd_raw_len(rc->R) / 2;
+  const int64_t chunks = (n64 + kRndChunk - 1) / kRndChunk;
+  OB_GRID_STRIDE(c, chunks) {
+    const int64_t o0 = c * kRndChunk;
+    unsigned __int128 st = pcg_advance(g.s, g.inc, (uint64_t)o0);
+    const int64_t o1 = min(o0 + kRndChunk, n64);
+    for (int64_t o = o0; o < o1; ++o) {
+      st = st * pcg_mult() + g.inc;  // next64: step, then output
+      const uint64_t v = pcg_out(st);
+      raw[2 * o] = (uint32_t)v;  // the bit generator's 32-bit buffer: low half first
+      raw[2 * o + 1] = (uint32_t)(v >> 32);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t interval_mask(uint32_t m) {
+  m |= m >> 1;
+  m |= m >> 2;
+  m |= m >> 4;
+  m |= m >> 8;
+  m |= m >> 16;
+  return m;
+}
+
+// one warp: j[i] for i = R-1 .. 1 from the raw stream
+__global__ void __launch_bounds__(32) k_rnd_draws(const uint32_t* __restrict__ raw, ReqCounters* rc, int32_t* jd) {
+  __shared__ uint32_t buf[2048];
+  const int lane = threadIdx.x;
+  const int64_t R = rc->R;
+  const int64_t L = rnd_raw_len(R);
+  int64_t i = R - 1, r = 0, base = 0;
+  for (int k = lane; k < 2048; k += 32) buf[k] = k < L ? raw[k] : 0u;
+  __syncwarp();
+  while (i >= 1) {
+    if (r + 32 > base + 2048) {  // refill the window at r
+      __syncwarp();
+      base = r;
+      for (int k = lane; k < 2048; k += 32) buf[k] = base + k < L ? raw[base + k] : 0u;
+      __syncwarp();
+    }
+    if (r + 32 > L) {  // not reached in practice: 4R + 4096 draws for <= R-1 acceptances of p >= 1/2
+      if (lane == 0) atomicOr((unsigned long long*)&rc->err, (unsigned long long)kErrRandom);
+      return;
+    }
+    const uint32_t x = buf[r - base + lane];
+    // hypothesis h: h rejections among the earlier lanes -> this lane's step is i - lane + h
+    unsigned rej[kRndHyp];
+    uint32_t vh[kRndHyp];
+#pragma unroll
+    for (int h = 0; h < kRndHyp; ++h) {
+      const int64_t st = i - lane + h;
+      bool acc = false;
+      uint32_t v = 0;
+      if (st >= 1 && st <= i) {
+        v = x & interval_mask((uint32_t)st);
+        acc = v <= (uint32_t)st;
+      }
+      vh[h] = v;
+      rej[h] = __ballot_sync(0xffffffffu, !acc);
+    }
+    // resolve: lanes up to the first rejection under h = 0 are accepted with h = 0, the next
+    // run up to the first rejection under h = 1 with h = 1, ...
+    int cur = -1, h = 0, myh = -1;
+    for (; h < kRndHyp; ++h) {
+      const unsigned above = cur >= 31 ? 0u : (0xffffffffu << (cur + 1));
+      const unsigned b = rej[h] & above;
+      const int f = b ? __ffs(b) - 1 : 32;
+      if (lane > cur && lane < f) myh = h;
+      cur = f;
+      if (f >= 32) break;
+    }
+    const int consumed = cur >= 32 ? 32 : cur + 1;  // through the last resolved rejection
+    // lanes past the last resolved rejection are re-read next iteration
+    bool wrote = false;
+    if (myh >= 0 && lane < consumed) {
+      int64_t st = i - lane + myh;
+      uint32_t v = 0;
+#pragma unroll
+      for (int hh = 0; hh < kRndHyp; ++hh)
+        if (hh == myh) v = vh[hh];
+      if (st >= 1) {
+        jd[st] = (int32_t)v;
+        wrote = true;
+      }
+    }
+    const int acc_n = __popc(__ballot_sync(0xffffffffu, wrote));
+    i -= acc_n;
+    r += consumed;
+  }
+}
+
+__global__ void k_rnd_count(const ReqCounters* rc, const int32_t* __restrict__ jd, int32_t* cnt) {
+  const int64_t R = rc->R;
+  OB_GRID_STRIDE(t, R) {
+    if (t >= 1) atomicAdd(cnt + jd[t], 1);
+  }
+}
+
+__global__ void k_rnd_fill(const ReqCounters* rc, const int32_t* __restrict__ jd, const int64_t* __restrict__ off,
+                           int32_t* fill, int32_t* lst) {
+  const int64_t R = rc->R;
+  OB_GRID_STRIDE(t, R) {
+    if (t >= 1) {
+      const int32_t v = jd[t];
+      lst[off[v] + atomicAdd(fill + v, 1)] = (int32_t)t;
+    }
+  }
+}
+
+// sort each value's (short) step list, then trace the chosen positions
+__global__ void k_rnd_sort_lists(const ReqCounters* rc, const int64_t* __restrict__ off, int32_t* lst) {
+  const int64_t R = rc->R;
+  OB_GRID_STRIDE(v, R) {
+    const int64_t a = off[v], b = off[v + 1];
+    for (int64_t x = a + 1; x < b; ++x) {  // insertion sort (expected length <= ln R + 1)
+      const int32_t key = lst[x];
+      int64_t y = x - 1;
+      while (y >= a && lst[y] > key) {
+        lst[y + 1] = lst[y];
+        --y;
+      }
+      lst[y + 1] = key;
+    }
+  }
+}
+
+__global__ void k_rnd_trace(ReqCounters* rc, const int32_t* __restrict__ jd, const int64_t* __restrict__ off,
+                            const int32_t* __restrict__ lst, uint64_t* key) {
+  const int64_t R = rc->R, budget = rc->budget;
+  if (budget <= 0 || budget >= R) return;  // SelLoad takes none / all
+  OB_GRID_STRIDE(p, budget) {
+    int64_t x = p > 0 ? jd[p] : 0, s = p;
+    for (int64_t guard = 0; guard < R; ++guard) {
+      // first step > s whose draw equals x
+      int64_t lo = off[x], hi = off[x + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (lst[mid] <= s) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo == off[x + 1]) break;
+      x = s = lst[lo];
+    }
+    key[x] = 1;  // candidate rank x is chosen (ranks follow ids: the compaction sorts by id)
+  }
+}
+
+// host: SeedSequence(seed).generate_state(4, uint64) (numpy/random/bit_generator.pyx) and
+// PCG64's seeding (pcg_setseq_128_srandom_r)
+static Pcg128 pcg64_from_seed(uint64_t seed) {
+  const uint32_t INIT_A = 0x43B0D7E5u, MULT_A = 0x931E8875u, INIT_B = 0x8B51F9DDu, MULT_B = 0x58F38DEDu;
+  const uint32_t MIX_L = 0xCA01F9DDu, MIX_R = 0x4973F715u;
+  std::vector<uint32_t> ent;
+  if (seed == 0) ent.push_back(0);
+  for (uint64_t x = seed; x; x >>= 32) ent.push_back((uint32_t)x);
+  uint32_t hc = INIT_A;
+  auto hashmix = [&](uint32_t v) {
+    v ^= hc;
+    hc *= MULT_A;
+    v *= hc;
+    return v ^ (v >> 16);
+  };
+  auto mix = [&](uint32_t x, uint32_t y) {
+    uint32_t r = MIX_L * x - MIX_R * y;
+    return r ^ (r >> 16);
+  };
+  uint32_t pool[4];
+  for (int i = 0; i < 4; ++i) pool[i] = hashmix(i < (int)ent.size() ? ent[i] : 0u);
+  for (int a = 0; a < 4; ++a)
+    for (int d = 0; d < 4; ++d)
+      if (a != d) pool[d] = mix(pool[d], hashmix(pool[a]));
+  for (size_t a = 4; a < ent.size(); ++a)
+    for (int d = 0; d < 4; ++d) pool[d] = mix(pool[d], hashmix(ent[a]));
+  uint32_t hb = INIT_B, o[8];
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = pool[i % 4] ^ hb;
+    hb *= MULT_B;
+    v *= hb;
+    o[i] = v ^ (v >> 16);
+  }
+  uint64_t st[4];
+  for (int i = 0; i < 4; ++i) st[i] = (uint64_t)o[2 * i] | ((uint64_t)o[2 * i + 1] << 32);
+  const unsigned __int128 mult = ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+  Pcg128 g;
+  g.inc = ((((unsigned __int128)st[2] << 64) | st[3]) << 1) | 1u;
+  g.s = 0;
+  g.s = g.s * mult + g.inc;
+  g.s += ((unsigned __int128)st[0] << 64) | st[1];
+  g.s = g.s * mult + g.inc;
+  return g;
+}
+
+static void select_random(Engine& e, RequestWs& w, int64_t r_max) {
+  cudaStream_t s = e.stream;
+  const Pcg128 g = pcg64_from_seed(e.cfg.seed);
+  OB_CUDA(cudaMemsetAsync(w.cand_key, 0, sizeof(uint64_t) * std::max<int64_t>(r_max, 1), s));
+  OB_CUDA(cudaMemsetAsync(w.rnd_cnt, 0, sizeof(int32_t) * (r_max + 1), s));
+  OB_CUDA(cudaMemsetAsync(w.rnd_fill, 0, sizeof(int32_t) * (r_max + 1), s));
+  k_rnd_raw<<<grid_for(rnd_raw_len(r_max) / 2, kRndChunk * 128, kNumSMs * 4), 128, 0, s>>>(g, w.rc, w.rnd_raw);
+  k_rnd_draws<<<1, 32, 0, s>>>(w.rnd_raw, w.rc, w.rnd_j);
+  k_rnd_count<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_j, w.rnd_cnt);
+  g_launches += 3;
+  device_scan(s, e.scan, LoadI32{w.rnd_cnt}, StoreI64{w.rnd_off}, nullptr, r_max + 1, r_max + 1, nullptr);
+  k_rnd_fill<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_j, w.rnd_off, w.rnd_fill, w.rnd_lst);
+  k_rnd_sort_lists<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_off, w.rnd_lst);
+  k_rnd_trace<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_j, w.rnd_off, w.rnd_lst, w.cand_key);
+  g_launches += 3;
 }
 
 // Request CSR over an edge set (the whole request via the parameter block when

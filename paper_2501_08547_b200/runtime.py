@@ -138,7 +138,7 @@ class ServingEngine:
             if max(fan) > nat.MAX_FANOUT:
                 raise ValueError(f"fanouts above {nat.MAX_FANOUT} are not supported on the device")
         if config.policy not in nat.POLICY:
-            raise ValueError(f"policy {config.policy!r} is not on the device path (ratio and is)")
+            raise ValueError(f"policy {config.policy!r} is not on the device path (ratio, is, random)")
         if getattr(config, "cache_bytes", 0):
             raise ValueError("feature caches are subsumed by HBM residency; use cache_bytes=0")
         self.dataset = dataset

@@ -19,6 +19,9 @@ Cases:
   sampled   -- the sampled strategy (compgraph.py:248-284): blocks and
                embeddings for several fanouts and seeds (incl. a seed above
                2^32), small_workload graphs and the hub graph
+  policy_random -- the RANDOM policy (policy.py:122-124, default_rng(tie_seed)
+               .permutation): candidates and targets for several seeds and gammas,
+               incl. a 20K-candidate request; srpe embeddings served with it
   policy_is -- the importance (IS) policy: centralized scores/targets
                (policy.py:84-95), per-rank partial sums and the distributed
                plan (policy.py:98-107, runtime.py:168-175) for P in {2,3}, and
@@ -317,8 +320,48 @@ def policy_is():
     print("policy_is", len(out), "arrays")
 
 
+def policy_random():
+    out: dict = {}
+    cases = [(3, 300, 8.0, 10, 5, 9), (50, 200, 10.0, 6, 8, 51), (60, 300, 8.0, 10, 6, 5), (7, 40000, 12.0, 8, 512, 3)]
+    for seed, n, avg, F, batch, rs in cases:
+        full = workload.gen_powerlaw_graph(n, avg, 2.1, F, seed=seed)
+        serving, pool = workload.split_holdout(full, 0.25, seed=seed)
+        req = workload.make_request(pool, serving, batch, seed=rs)
+        tag = f"s{seed}"
+        out[f"{tag}.offsets"] = serving.in_offsets
+        out[f"{tag}.nbrs"] = serving.in_neighbors
+        out[f"{tag}.feats"] = serving.features
+        out[f"{tag}.N"] = np.int64(serving.num_nodes)
+        out[f"{tag}.B"] = np.int64(batch)
+        out[f"{tag}.qfeat"] = req.query_features
+        out[f"{tag}.edges"] = req.edges
+        cand = policy.find_candidates(req, serving)
+        out[f"{tag}.cand"] = cand.ids
+        for tie in (0, 1, 7, (1 << 40) + 3):
+            for g in (0.1, 0.5, 1.0):
+                plan = policy.select_targets(cand, np.zeros(len(cand)), g, policy.POLICY_RANDOM, tie_seed=tie)
+                out[f"{tag}.t{tie}.g{g}.targets"] = plan.targets
+        if n <= 300:  # srpe served with the random policy (sage_mean k=3)
+            model = make_model("sage_mean", 3, F, 6)
+            w = init_weights(model, 4)
+            pe = precompute_embeddings(serving, model, w)
+            for li, lw in enumerate(w.layers, start=1):
+                for nm, m in lw.items():
+                    out[f"{tag}.w.l{li}.{nm}"] = m
+            for l in range(1, 3):
+                out[f"{tag}.pe.l{l}"] = pe.layers[l - 1]
+            eng = ServingEngine(serving, pe, model, w, ServeConfig(strategy="srpe", gamma=0.5, policy="random", seed=7))
+            emb, bd = eng.serve(req)
+            out[f"{tag}.emb"] = emb
+            out[f"{tag}.fetch"] = np.int64(bd.fetch_bytes)
+    np.savez_compressed(os.path.join(HERE, "policy_random.npz"), **out)
+    print("policy_random", len(out), "arrays")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["demo", "small", "edge", "cfg1", "is", "sampled"]
+    which = sys.argv[1:] or ["demo", "small", "edge", "cfg1", "is", "sampled", "random"]
+    if "random" in which:
+        policy_random()
     if "sampled" in which:
         sampled()
     if "is" in which:
