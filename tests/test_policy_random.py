@@ -55,7 +55,7 @@ def _engine(golden, case, tie, gamma, strategy="srpe", P=1):
     ds = graphstore.GraphDataset(N, g[f"{case}.offsets"], g[f"{case}.nbrs"], g[f"{case}.feats"], np.ones(N, bool),
                                  np.zeros(N, bool))
     model = models.make_model("sage_mean", 3, F, 6)
-    if f"{case}.w.l1.W_self" in g:
+    if f"{case}.w.l1.w_self" in g:
         w = models.Weights([{n: g[f"{case}.w.l{l}.{n}"] for n in WEIGHT_NAMES["sage_mean"]} for l in (1, 2, 3)])
         pe = graphstore.PeStore([g[f"{case}.pe.l{l}"] for l in (1, 2)])
     else:
