@@ -1120,14 +1120,8 @@ __global__ void k_rnd_raw(Pcg128 g, const ReqCounters* rc, uint32_t* raw) {
   }
 }
 
-__device__ __forceinline__ uint32_t interval_mask(uint32_t m) {
-  m |= m >> 1;
-  m |= m >> 2;
-  m |= m >> 4;
-  m |= m >> 8;
-  m |= m >> 16;
-  return m;
-}
+// random_interval's mask: the smallest all-ones value >= m (m >= 1)
+__device__ __forceinline__ uint32_t interval_mask(uint32_t m) { return 0xFFFFFFFFu >> __clz(m); }
 
 // one warp: j[i] for i = R-1 .. 1 from the raw stream
 __global__ void __launch_bounds__(32) k_rnd_draws(const uint32_t* __restrict__ raw, ReqCounters* rc, int32_t* jd) {
@@ -1166,15 +1160,17 @@ __global__ void __launch_bounds__(32) k_rnd_draws(const uint32_t* __restrict__ r
       rej[h] = __ballot_sync(0xffffffffu, !acc);
     }
     // resolve: lanes up to the first rejection under h = 0 are accepted with h = 0, the next
-    // run up to the first rejection under h = 1 with h = 1, ...
-    int cur = -1, h = 0, myh = -1;
-    for (; h < kRndHyp; ++h) {
-      const unsigned above = cur >= 31 ? 0u : (0xffffffffu << (cur + 1));
-      const unsigned b = rej[h] & above;
-      const int f = b ? __ffs(b) - 1 : 32;
-      if (lane > cur && lane < f) myh = h;
-      cur = f;
-      if (f >= 32) break;
+    // run up to the first rejection under h = 1 with h = 1, ... (unrolled, predicated)
+    int cur = -1, myh = -1;
+#pragma unroll
+    for (int h = 0; h < kRndHyp; ++h) {
+      if (cur < 32) {
+        const unsigned above = cur >= 31 ? 0u : (0xffffffffu << (cur + 1));
+        const unsigned b = rej[h] & above;
+        const int f = b ? __ffs(b) - 1 : 32;
+        if (lane > cur && lane < f) myh = h;
+        cur = f;
+      }
     }
     const int consumed = cur >= 32 ? 32 : cur + 1;  // through the last resolved rejection
     // lanes past the last resolved rejection are re-read next iteration
