@@ -205,5 +205,5 @@ def test_policy_validation_on_host():
     """Unknown policies fail on the host side before touching the device (ServeConfig mirrors runtime.py:74-82)."""
     from paper_2501_08547_b200 import _native as nat
 
-    assert nat.POLICY == {"ratio": 0, "is": 1}
+    assert nat.POLICY == {"ratio": 0, "is": 1, "random": 2}
     _ = os
