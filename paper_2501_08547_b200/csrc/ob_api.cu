@@ -35,10 +35,6 @@ Engine::~Engine() {
       if (ev_) cudaEventDestroy(ev_);
     if (L.stream) cudaStreamDestroy(L.stream);
     if (L.side) cudaStreamDestroy(L.side);
-    for (int i = 0; i < 2; ++i) {
-      if (L.aux[i]) cudaStreamDestroy(L.aux[i]);
-      if (L.aux_ev[i]) cudaEventDestroy(L.aux_ev[i]);
-    }
   }
   if (lane_fork_ev) cudaEventDestroy(lane_fork_ev);
   drop_graphs();
@@ -50,10 +46,6 @@ Engine::~Engine() {
     if (ev_) cudaEventDestroy(ev_);
   if (own_stream && stream) cudaStreamDestroy(stream);
   if (side) cudaStreamDestroy(side);
-  for (int i = 0; i < 2; ++i) {
-    if (aux[i]) cudaStreamDestroy(aux[i]);
-    if (aux_ev[i]) cudaEventDestroy(aux_ev[i]);
-  }
   if (fork_ev) cudaEventDestroy(fork_ev);
   if (join_ev) cudaEventDestroy(join_ev);
   if (csr_ev) cudaEventDestroy(csr_ev);
@@ -99,10 +91,6 @@ static void swap_lane(Engine& e, Lane& L) {
   std::swap(e.graphs, L.graphs);
   std::swap(e.stream, L.stream);
   std::swap(e.side, L.side);
-  for (int i = 0; i < 2; ++i) {
-    std::swap(e.aux[i], L.aux[i]);
-    std::swap(e.aux_ev[i], L.aux_ev[i]);
-  }
   std::swap(e.fork_ev, L.fork_ev);
   std::swap(e.join_ev, L.join_ev);
   std::swap(e.csr_ev, L.csr_ev);
@@ -216,12 +204,8 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.rq_src = a.take<int32_t>(m + 1);
   w.rq_keys = a.take<uint64_t>(m + 1);
   w.rq_keys2 = a.take<uint64_t>(m + 1);
-  w.rq_keys3 = a.take<uint64_t>(m + 1);
-  w.rq_keys4 = a.take<uint64_t>(m + 1);
   w.rx_cnt = a.take<int32_t>(256 * rx_tiles(m));
   w.rx_off = a.take<int64_t>(256 * rx_tiles(m) + 1);
-  w.rx_cnt2 = a.take<int32_t>(256 * rx_tiles(m));
-  w.rx_off2 = a.take<int64_t>(256 * rx_tiles(m) + 1);
   w.rx_st = a.take<uint32_t>(rx_st_words(m));
   w.rq_ctr = a.take<int64_t>(4);
   int64_t Emax = 1, Dmax = 1, Smax = 1, Imax = 1;
@@ -434,20 +418,16 @@ static void enqueue_stages(Engine& e, float* d_out) {
   }
   cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, srpe);
-  // From here four streams share only read-only inputs: the query half of the
-  // request-index sort and the query block (side), the candidate half of the sort
-  // (aux[0]), the layer-1 query rows -- padding and the early query GEMMs -- (aux[1]),
-  // and the checks, scores and top-k selection (main); the mid block joins them
+  // the request-index sort (side stream) and the top-k selection (main stream)
+  // only share read-only inputs from here on: run them side by side
+  // and, under srpe, the query block (it needs only the index) follows the sort there
   OB_CUDA(cudaEventRecord(e.fork_ev, s));
-  for (cudaStream_t t : {e.side, e.aux[0], e.aux[1]}) OB_CUDA(cudaStreamWaitEvent(t, e.fork_ev, 0));
+  OB_CUDA(cudaStreamWaitEvent(e.side, e.fork_ev, 0));
   {
+    e.stream = e.side;  // stage functions launch on e.stream
     try {
-      e.stream = e.aux[1];
-      stage_query_rows(e, w);
-      OB_CUDA(cudaEventRecord(e.aux_ev[1], e.aux[1]));
-      e.stream = e.side;  // stage functions launch on e.stream
       cudaEvent_t pc = prof_begin(e.side);
-      stage_request_csr(e, w, e.aux[0], e.aux_ev[0]);
+      stage_request_csr(e, w);
       prof_end(e.side, pc, kProfCsr, nullptr, 0, 0, 0, 0, 0);
       OB_CUDA(cudaEventRecord(e.csr_ev, e.side));
       if (srpe) {
@@ -464,15 +444,15 @@ static void enqueue_stages(Engine& e, float* d_out) {
   stage_request_post(e, w, srpe);
   if (srpe) stage_select(e, w);
   prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
+  // query rows of layer 1 (padding, stored-transform rows) while the request index sorts
+  stage_query_rows(e, w);
   OB_CUDA(cudaStreamWaitEvent(s, e.csr_ev, 0));
-  OB_CUDA(cudaStreamWaitEvent(s, e.aux_ev[0], 0));
   p0 = prof_begin(s);
   if (srpe) build_mid_block(e, w);
   else stage_build_full(e, w);
   prof_end(s, p0, kProfBuild, nullptr, 0, 0, 0, 0, 0);
   OB_CUDA(cudaEventRecord(e.join_ev, e.side));
   OB_CUDA(cudaStreamWaitEvent(s, e.join_ev, 0));
-  OB_CUDA(cudaStreamWaitEvent(s, e.aux_ev[1], 0));
   record_mark(e.ev[1], s);
   stage_forward(e, w, d_out);
 }
@@ -938,10 +918,6 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
     }
     for (auto& ev_ : e.ev) OB_CUDA(cudaEventCreate(&ev_));
     OB_CUDA(cudaStreamCreateWithFlags(&e.side, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
-      OB_CUDA(cudaStreamCreateWithFlags(&e.aux[i], cudaStreamNonBlocking));
-      OB_CUDA(cudaEventCreateWithFlags(&e.aux_ev[i], cudaEventDisableTiming));
-    }
     OB_CUDA(cudaEventCreateWithFlags(&e.fork_ev, cudaEventDisableTiming));
     OB_CUDA(cudaEventCreateWithFlags(&e.join_ev, cudaEventDisableTiming));
     OB_CUDA(cudaEventCreateWithFlags(&e.csr_ev, cudaEventDisableTiming));
@@ -1369,10 +1345,6 @@ int ob_set_lanes(ob_engine* h, int32_t n) {
       Lane& L = e.lanes.back();
       OB_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
       OB_CUDA(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking));
-      for (int i = 0; i < 2; ++i) {
-        OB_CUDA(cudaStreamCreateWithFlags(&L.aux[i], cudaStreamNonBlocking));
-        OB_CUDA(cudaEventCreateWithFlags(&L.aux_ev[i], cudaEventDisableTiming));
-      }
       for (auto& ev_ : L.ev) OB_CUDA(cudaEventCreate(&ev_));
       for (cudaEvent_t* ev_ : {&L.fork_ev, &L.join_ev, &L.csr_ev, &L.done_ev})
         OB_CUDA(cudaEventCreateWithFlags(ev_, cudaEventDisableTiming));

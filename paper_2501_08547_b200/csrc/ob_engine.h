@@ -281,10 +281,6 @@ struct RequestWs {
   int32_t* rq_src = nullptr;       // [m] sources, ascending within a slot after sort
   uint64_t* rq_keys = nullptr;     // [m] radix keys (ping)
   uint64_t* rq_keys2 = nullptr;    // [m] radix keys (pong)
-  uint64_t* rq_keys3 = nullptr;    // [m] query-slot half of the keys (ping) -- sorted beside the candidate half
-  uint64_t* rq_keys4 = nullptr;    // [m] query-slot half (pong)
-  int32_t* rx_cnt2 = nullptr;      // query-slot half's radix digit counts / offsets
-  int64_t* rx_off2 = nullptr;
   int32_t* rx_cnt = nullptr;       // radix digit counts
   int64_t* rx_off = nullptr;       // radix digit offsets
   uint32_t* rx_st = nullptr;       // one-sweep look-back state (RqCsr::rx_st)
@@ -559,7 +555,7 @@ void launch_is_gather(Engine& e, RequestWs& w, const double* tab, double* out);
 void build_is_table(Engine& e, const int64_t* off, const int32_t* src, double* out);
 void ensure_is_tables(Engine& e);
 void launch_score_is(Engine& e, RequestWs& w, const IsParts& parts);
-void stage_request_csr(Engine& e, RequestWs& w, cudaStream_t cand_stream, cudaEvent_t cand_done);
+void stage_request_csr(Engine& e, RequestWs& w);
 void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound, const int64_t* m_dev, RqCsr& c,
                   bool counts_ready);
 // where a block's destinations pull their sources from
@@ -707,8 +703,6 @@ struct Lane {
   ReqParams* params = nullptr;
   std::vector<RequestGraph> graphs;
   cudaStream_t stream = nullptr, side = nullptr;
-  cudaStream_t aux[2] = {};        // candidate-half sort, layer-1 query rows
-  cudaEvent_t aux_ev[2] = {};
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, csr_ev = nullptr, done_ev = nullptr;
   cudaEvent_t ev[6] = {};
   CgpLaneState cg;
@@ -722,10 +716,6 @@ struct Engine {
   // side stream for independent request stages (request-index sort next to the
   // top-k selection); forked and joined with events, so captured graphs branch
   cudaStream_t side = nullptr;
-  // two more request streams: the candidate half of the request-index sort and the
-  // layer-1 query rows run beside the query half (side) and the selection (stream)
-  cudaStream_t aux[2] = {};
-  cudaEvent_t aux_ev[2] = {};
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, csr_ev = nullptr;
   GraphDev g;
   std::vector<LayerDev> layers;

@@ -161,37 +161,18 @@ __device__ __forceinline__ K rq_key(int64_t s, int64_t d, int64_t N, const uint3
   return ((K)1 << f.body) | ((K)(d - N) << f.bN) | (K)sr;
 }
 
-// candidate-slot counts (query slots take qdeg) + one radix key per edge, split by
-// population: keys into candidate slots go to keys_a[0, Mc), keys into query slots
-// to keys_b[0, Mq) (counters ctr[1], ctr[2]), so the two halves sort side by side.
-// The order inside each half is arbitrary: equal keys are identical (slot, source)
-// pairs, so the sorted CSR does not depend on it.
+// candidate-slot counts (query slots take qdeg) + one radix key per edge
 template <class K>
 __global__ void k_rq_count(const ReqParams* rp, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
-                           const ReqCounters* rc, int32_t* rq_cnt, K* keys_a, K* keys_b, int64_t* ctr, RqKeyFmt f) {
+                           const ReqCounters* rc, int32_t* rq_cnt, K* keys, RqKeyFmt f) {
   if (rc->err & (kErrRange | kErrNoQuery)) return;
   const int64_t* __restrict__ edges = rp->edges;
   const int64_t m = rp->m;
-  const int lane = threadIdx.x & 31;
-  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < m; e0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = e0 + threadIdx.x;
-    const bool live = e < m;
-    int64_t s = 0, d = 0;
-    if (live) ld_edge(edges, e, s, d);
-    const bool cand = live && d < N;
-    if (cand) warp_agg_inc(rq_cnt, bm_rank(cbits, cwpre, d));
-    const K k = live ? rq_key<K>(s, d, N, cbits, cwpre, rc->R, f) : (K)0;
-    const unsigned bc = __ballot_sync(0xffffffffu, cand), bq = __ballot_sync(0xffffffffu, live && !cand);
-    unsigned long long base_c = 0, base_q = 0;
-    if (lane == 0) {
-      if (bc) base_c = atomicAdd((unsigned long long*)(ctr + 1), (unsigned long long)__popc(bc));
-      if (bq) base_q = atomicAdd((unsigned long long*)(ctr + 2), (unsigned long long)__popc(bq));
-    }
-    base_c = __shfl_sync(0xffffffffu, base_c, 0);
-    base_q = __shfl_sync(0xffffffffu, base_q, 0);
-    const unsigned lt = (1u << lane) - 1u;
-    if (cand) keys_a[base_c + __popc(bc & lt)] = k;
-    else if (live) keys_b[base_q + __popc(bq & lt)] = k;
+  OB_GRID_STRIDE(e, m) {
+    int64_t s, d;
+    ld_edge(edges, e, s, d);
+    if (d < N) warp_agg_inc(rq_cnt, bm_rank(cbits, cwpre, d));
+    keys[e] = rq_key<K>(s, d, N, cbits, cwpre, rc->R, f);
   }
 }
 
@@ -771,8 +752,7 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
                                                            const int32_t* __restrict__ cnt, RqKeyFmt f, int64_t N,
                                                            const int32_t* __restrict__ cand_ids,
                                                            const ReqCounters* rc, uint32_t* st, uint32_t* ticket,
-                                                           const uint32_t* __restrict__ ghist,
-                                                           const int64_t* __restrict__ out_base) {
+                                                           const uint32_t* __restrict__ ghist) {
   using BS = cub::BlockScan<int32_t, kRxThreads>;
   using BS64 = cub::BlockScan<int64_t, kRxThreads>;
   __shared__ typename BS64::TempStorage scan_tmp64;
@@ -889,11 +869,10 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
       if (dg[i] < 256) u.exch[rk[i]] = k[i];
     __syncthreads();
     const int n = (int)min((int64_t)kRxTile, m - t * kRxTile);
-    const int64_t ob = FINAL && out_base ? *out_base : 0;  // the query-slot half lands after the candidate half
     for (int p = threadIdx.x; p < n; p += kRxThreads) {
       const K kk = u.exch[p];
       const int d = (int)((kk >> shift) & 255);
-      const int64_t pos = ob + gofs[d] + (p - bstart[d]);
+      const int64_t pos = gofs[d] + (p - bstart[d]);
       if (FINAL) {
         const bool query_slot = (kk >> f.body) & 1;
         if (query_slot) {
@@ -915,8 +894,7 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
 #endif
 
 template <class K>
-static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int64_t m_bound, const RqKeyFmt& f,
-                    const int64_t* out_base = nullptr) {
+static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int64_t m_bound, const RqKeyFmt& f) {
   cudaStream_t s = e.stream;
   const int64_t tiles_b = rx_tiles(m_bound);
   const int g = grid_for(tiles_b, 1, kNumSMs * (OB_RX_MINB > 2 ? OB_RX_MINB : 2));
@@ -927,7 +905,7 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
   // a captured request graph keeps the path it was captured with)
   const char* os_env = std::getenv("OB_RX_ONESWEEP");
   const bool onesweep = os_env ? std::atoi(os_env) != 0 : OB_RX_ONESWEEP != 0;
-  if (onesweep && c.rx_st && m_bound < (int64_t)kRxCount && !out_base) {
+  if (onesweep && c.rx_st && m_bound < (int64_t)kRxCount) {
     // one sweep per pass: digit totals for every pass from one read, then each
     // scatter tile publishes its digit counts and looks back for its offsets
     uint32_t* st = c.rx_st;
@@ -941,12 +919,10 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
       uint32_t* sp = st + (int64_t)p * 256 * tiles_b;
       if (p + 1 == passes) {
         k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
-                                                        e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p,
-                                                        nullptr);
+                                                        e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p);
       } else {
         k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
-                                                         e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p,
-                                                         nullptr);
+                                                         e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p);
         std::swap(a, b);
       }
       OB_LAUNCHED();
@@ -963,10 +939,10 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
       device_scan(s, e.scan, LoadI32{c.rx_cnt}, StoreI64{c.rx_off}, nullptr, 256 * tiles_b, 256 * tiles_b, nullptr);
     if (p + 1 == passes) {
       k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, off, c.rx_cnt, f,
-                                                      e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr, out_base);
+                                                      e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr);
     } else {
       k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, off, c.rx_cnt, f,
-                                                       e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr, nullptr);
+                                                       e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr);
       std::swap(a, b);
     }
     OB_LAUNCHED();
@@ -1013,14 +989,11 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   OB_LAUNCHED();
   if (m > 0) {  // candidate-slot counts + the request CSR's radix keys
     const RqKeyFmt f = rq_key_fmt(e, w);
-    OB_CUDA(cudaMemsetAsync(w.rq_ctr, 0, sizeof(int64_t) * 4, s));
     if (f.wide())
-      k_rq_count<uint64_t><<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt, w.rq_keys,
-                                                            w.rq_keys3, w.rq_ctr, f);
+      k_rq_count<uint64_t><<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt, w.rq_keys, f);
     else
       k_rq_count<uint32_t><<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt,
-                                                            reinterpret_cast<uint32_t*>(w.rq_keys),
-                                                            reinterpret_cast<uint32_t*>(w.rq_keys3), w.rq_ctr, f);
+                                                            reinterpret_cast<uint32_t*>(w.rq_keys), f);
     OB_LAUNCHED();
   }
   (void)need_scores;
@@ -1365,36 +1338,9 @@ void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound
   else rx_sort<uint32_t>(e, w, c, m_dev, m_bound, f);
 }
 
-// The whole request's index (centralized): slot offsets from the counts, then the
-// two populations' radix sorts -- query slots on e.stream, candidate slots on
-// `cand_stream` -- writing the sources into one CSR (candidate half first)
-void stage_request_csr(Engine& e, RequestWs& w, cudaStream_t cand_stream, cudaEvent_t cand_done) {
-  const int64_t rb_max = std::min<int64_t>(e.g.N, 2 * w.m) + w.B;
-  const RqKeyFmt f = rq_key_fmt(e, w);
-  cudaStream_t s = e.stream;
-  device_scan(s, e.scan, LoadI32{w.rq_cnt}, StoreI64{w.rq_ptr}, &w.rc->RB, 0, rb_max, nullptr, w.rq_ptr);
-  if (w.m <= 0) {
-    OB_CUDA(cudaEventRecord(cand_done, cand_stream));
-    return;
-  }
-  RqCsr ca = w.rq_view();  // candidate half: keys / keys2, rx_cnt / rx_off
-  RqCsr cq = w.rq_view();  // query half: keys3 / keys4, rx_cnt2 / rx_off2
-  cq.keys = w.rq_keys3;
-  cq.keys2 = w.rq_keys4;
-  cq.rx_cnt = w.rx_cnt2;
-  cq.rx_off = w.rx_off2;
-  e.stream = cand_stream;
-  try {
-    if (f.wide()) rx_sort<uint64_t>(e, w, ca, w.rq_ctr + 1, w.m, f);
-    else rx_sort<uint32_t>(e, w, ca, w.rq_ctr + 1, w.m, f);
-  } catch (...) {
-    e.stream = s;
-    throw;
-  }
-  e.stream = s;
-  OB_CUDA(cudaEventRecord(cand_done, cand_stream));
-  if (f.wide()) rx_sort<uint64_t>(e, w, cq, w.rq_ctr + 2, w.m, f, w.rq_ctr + 1);
-  else rx_sort<uint32_t>(e, w, cq, w.rq_ctr + 2, w.m, f, w.rq_ctr + 1);
+void stage_request_csr(Engine& e, RequestWs& w) {
+  RqCsr c = w.rq_view();
+  build_rq_csr(e, w, nullptr, w.m, nullptr, c, /*counts_ready=*/true);
 }
 
 }  // namespace ob
