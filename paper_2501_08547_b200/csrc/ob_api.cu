@@ -194,6 +194,10 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     w.rnd_fill = a.take<int32_t>(p.R_max + 2);
     w.rnd_off = a.take<int64_t>(p.R_max + 2);
     w.rnd_lst = a.take<int32_t>(p.R_max + 1);
+    const int64_t chunks = (4 * p.R_max + 4096 + 2047) / 2048;
+    w.rnd_lo = a.take<int64_t>(chunks + 1);
+    w.rnd_exit = a.take<int32_t>((chunks + 1) * 4096);
+    w.rnd_enter = a.take<int64_t>(chunks + 1);
   }
   w.cand_tpos = a.take<int32_t>(p.R_max);
   w.targets = a.take<int32_t>(p.T_max + 1);

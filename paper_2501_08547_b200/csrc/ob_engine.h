@@ -270,6 +270,9 @@ struct RequestWs {
   int32_t* rnd_fill = nullptr;     // [R_max + 1]
   int64_t* rnd_off = nullptr;      // [R_max + 1]
   int32_t* rnd_lst = nullptr;      // [R_max]
+  int64_t* rnd_lo = nullptr;       // chunked draw assignment: per chunk, the first evaluated entering step
+  int32_t* rnd_exit = nullptr;     //   [chunks][4096] exit step per entering step
+  int64_t* rnd_enter = nullptr;    //   [chunks] the true entering step
   int32_t* cand_tpos = nullptr;    // [R] position in targets or -1
   int32_t* targets = nullptr;      // [T]
   int64_t* sel_pos = nullptr;      // [R+1]

@@ -1192,6 +1192,97 @@ __global__ void __launch_bounds__(32) k_rnd_draws(const uint32_t* __restrict__ r
   }
 }
 
+// Chunked draw assignment (replaces the one-warp walk for large |R|).  Draws are cut
+// into chunks of kRndW; a chunk maps the step it is entered with to the step it
+// leaves with.  Phase A evaluates that map for a window of kRndK entering steps
+// around the expected one (one thread per entering step, the chunk's draws
+// broadcast from shared memory); phase B walks the chunks on one thread with the
+// maps (falling back to simulating a chunk when the true step left its window);
+// phase C re-runs every chunk from its true entering step and writes the draws.
+constexpr int kRndW = 2048;      // draws per chunk
+constexpr int kRndK = 4096;      // entering steps evaluated per chunk (4.7 sigma of the random walk at |R| = 2e5)
+constexpr int kRndKCta = 1024;
+
+__device__ __forceinline__ int64_t rnd_step_exit(const uint32_t* d, int n, int64_t s) {
+  for (int r = 0; r < n && s >= 1; ++r) {
+    const uint32_t v = d[r] & interval_mask((uint32_t)s);
+    s -= v <= (uint32_t)s;
+  }
+  return s;
+}
+
+// the expected entering step of every chunk (deterministic: expected acceptances)
+__global__ void k_rnd_estimate(const ReqCounters* rc, int64_t chunks, int64_t* lo) {
+  if (threadIdx.x || blockIdx.x) return;
+  double i = (double)rc->R - 1.0;
+  int64_t tail = 4;  // chunks evaluated past the expected end of the walk
+  for (int64_t c = 0; c < chunks; ++c) {
+    if (i < 1.0 && --tail < 0) {
+      lo[c] = INT64_MIN;  // never reached in expectation: k_rnd_chunkmap skips it
+      continue;
+    }
+    lo[c] = (int64_t)llround(i) - kRndK / 2;
+    for (int q = 0; q < 16; ++q) {  // 16 sub-steps of kRndW / 16 draws at the local acceptance rate
+      if (i < 1.0) break;
+      const double m = (double)interval_mask((uint32_t)i) + 1.0;
+      i -= (kRndW / 16) * (i + 1.0) / m;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRndKCta) k_rnd_chunkmap(const uint32_t* __restrict__ raw, const ReqCounters* rc,
+                                                           const int64_t* __restrict__ lo, int32_t* exit_) {
+  __shared__ uint32_t d[kRndW];
+  const int64_t R = rc->R;
+  const int64_t L = rnd_raw_len(R);
+  const int64_t c = blockIdx.x / (kRndK / kRndKCta);
+  const int k = (int)(blockIdx.x % (kRndK / kRndKCta)) * kRndKCta + threadIdx.x;
+  const int64_t r0 = c * kRndW;
+  if (r0 >= L || lo[c] == INT64_MIN) return;
+  const int n = (int)min((int64_t)kRndW, L - r0);
+  for (int r = threadIdx.x; r < n; r += kRndKCta) d[r] = raw[r0 + r];
+  __syncthreads();
+  const int64_t s0 = lo[c] + k;
+  exit_[c * kRndK + k] = s0 >= 1 && s0 < R ? (int32_t)rnd_step_exit(d, n, s0) : -1;
+}
+
+__global__ void k_rnd_walk(const uint32_t* __restrict__ raw, ReqCounters* rc, int64_t chunks,
+                           const int64_t* __restrict__ lo, const int32_t* __restrict__ exit_, int64_t* enter) {
+  if (threadIdx.x || blockIdx.x) return;
+  const int64_t R = rc->R;
+  const int64_t L = rnd_raw_len(R);
+  int64_t i = R - 1;
+  for (int64_t c = 0; c < chunks; ++c) {
+    enter[c] = i;
+    if (i < 1) continue;
+    const int64_t r0 = c * kRndW;
+    if (r0 >= L) {  // not reached in practice: the stream holds 4R + 4096 draws
+      atomicOr((unsigned long long*)&rc->err, (unsigned long long)kErrRandom);
+      return;
+    }
+    const int64_t k = lo[c] == INT64_MIN ? -1 : i - lo[c];
+    if (k >= 0 && k < kRndK && exit_[c * kRndK + k] >= 0) i = exit_[c * kRndK + k];
+    else i = rnd_step_exit(raw + r0, (int)min((int64_t)kRndW, L - r0), i);  // outside the window: walk it
+  }
+  if (i >= 1) atomicOr((unsigned long long*)&rc->err, (unsigned long long)kErrRandom);
+}
+
+__global__ void k_rnd_emit(const uint32_t* __restrict__ raw, const ReqCounters* rc, int64_t chunks,
+                           const int64_t* __restrict__ enter, int32_t* jd) {
+  const int64_t L = rnd_raw_len(rc->R);
+  OB_GRID_STRIDE(c, chunks) {
+    int64_t s = enter[c];
+    const int64_t r0 = c * kRndW, r1 = min(r0 + kRndW, L);
+    for (int64_t r = r0; r < r1 && s >= 1; ++r) {
+      const uint32_t v = __ldg(raw + r) & interval_mask((uint32_t)s);
+      if (v <= (uint32_t)s) {
+        jd[s] = (int32_t)v;
+        --s;
+      }
+    }
+  }
+}
+
 __global__ void k_rnd_count(const ReqCounters* rc, const int32_t* __restrict__ jd, int32_t* cnt) {
   const int64_t R = rc->R;
   OB_GRID_STRIDE(t, R) {
@@ -1300,9 +1391,21 @@ static void select_random(Engine& e, RequestWs& w, int64_t r_max) {
   OB_CUDA(cudaMemsetAsync(w.rnd_cnt, 0, sizeof(int32_t) * (r_max + 1), s));
   OB_CUDA(cudaMemsetAsync(w.rnd_fill, 0, sizeof(int32_t) * (r_max + 1), s));
   k_rnd_raw<<<grid_for(rnd_raw_len(r_max) / 2, kRndChunk * 128, kNumSMs * 4), 128, 0, s>>>(g, w.rc, w.rnd_raw);
-  k_rnd_draws<<<1, 32, 0, s>>>(w.rnd_raw, w.rc, w.rnd_j);
+  // draws -> steps: the chunk maps + one walk + re-emission (large |R|); the one-warp walk
+  // over the whole stream below kRndSmall candidates (a few chunks are not worth three launches)
+  const int64_t chunks = (rnd_raw_len(r_max) + kRndW - 1) / kRndW;
+  if (r_max > 8192) {
+    k_rnd_estimate<<<1, 32, 0, s>>>(w.rc, chunks, w.rnd_lo);
+    k_rnd_chunkmap<<<(unsigned)(chunks * (kRndK / kRndKCta)), kRndKCta, 0, s>>>(w.rnd_raw, w.rc, w.rnd_lo, w.rnd_exit);
+    k_rnd_walk<<<1, 32, 0, s>>>(w.rnd_raw, w.rc, chunks, w.rnd_lo, w.rnd_exit, w.rnd_enter);
+    k_rnd_emit<<<grid_for(chunks, 64), 64, 0, s>>>(w.rnd_raw, w.rc, chunks, w.rnd_enter, w.rnd_j);
+    g_launches += 4;
+  } else {
+    k_rnd_draws<<<1, 32, 0, s>>>(w.rnd_raw, w.rc, w.rnd_j);
+    OB_LAUNCHED();
+  }
   k_rnd_count<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_j, w.rnd_cnt);
-  g_launches += 3;
+  OB_LAUNCHED();
   device_scan(s, e.scan, LoadI32{w.rnd_cnt}, StoreI64{w.rnd_off}, nullptr, r_max + 1, r_max + 1, nullptr);
   k_rnd_fill<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_j, w.rnd_off, w.rnd_fill, w.rnd_lst);
   k_rnd_sort_lists<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_off, w.rnd_lst);
