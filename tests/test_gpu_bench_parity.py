@@ -150,3 +150,23 @@ def test_cfg3_gat_request_vs_oracle():
         assert _rel(emb, ref["emb"]) <= TOL
     finally:
         ctx["eng"].close()
+
+
+def test_cfg2_random_policy_targets(cfg2):
+    """The RANDOM policy at the benchmarked size (|R| = 191K candidates: the chunked draw assignment):
+    targets equal sort(ids[default_rng(seed).permutation(|R|)[:budget]]) (policy.py:122-124)."""
+    from oracle import structure as ST
+    from paper_2501_08547_b200 import graphstore, runtime
+
+    s = cfg2["serving"]
+    pe = graphstore.PeStore(cfg2["pe"])
+    for seed in (0, 7):
+        eng = runtime.ServingEngine(s, pe, cfg2["model"], cfg2["w"],
+                                    runtime.ServeConfig(strategy="srpe", gamma=0.1, policy="random", seed=seed))
+        req = cfg2["reqs"][0]
+        eng.serve(req)
+        plan = eng.last_plan()
+        assert len(plan["ids"]) > 100_000
+        assert np.all(plan["scores"] == 0.0)
+        assert np.array_equal(plan["targets"], ST.select_random(plan["ids"], 0.1, seed))
+        eng.close()
