@@ -1204,28 +1204,41 @@ constexpr int kRndK = 4096;      // entering steps evaluated per chunk (4.7 sigm
 constexpr int kRndKCta = 1024;
 
 __device__ __forceinline__ int64_t rnd_step_exit(const uint32_t* d, int n, int64_t s) {
-  for (int r = 0; r < n && s >= 1; ++r) {
+  int r = 0;
+  for (; r + 8 <= n && s >= 1; r += 8) {  // eight draws loaded ahead of the dependent chain
+    uint32_t x[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = d[r + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (s >= 1) {
+        const uint32_t v = x[q] & interval_mask((uint32_t)s);
+        s -= v <= (uint32_t)s;
+      }
+    }
+  }
+  for (; r < n && s >= 1; ++r) {
     const uint32_t v = d[r] & interval_mask((uint32_t)s);
     s -= v <= (uint32_t)s;
   }
   return s;
 }
 
-// the expected entering step of every chunk (deterministic: expected acceptances)
+// the expected entering step of every chunk (deterministic: expected acceptances,
+// four sub-steps per chunk at the local acceptance rate (i + 1) / (mask(i) + 1))
 __global__ void k_rnd_estimate(const ReqCounters* rc, int64_t chunks, int64_t* lo) {
   if (threadIdx.x || blockIdx.x) return;
-  double i = (double)rc->R - 1.0;
+  float i = (float)(rc->R - 1);
   int64_t tail = 4;  // chunks evaluated past the expected end of the walk
   for (int64_t c = 0; c < chunks; ++c) {
-    if (i < 1.0 && --tail < 0) {
+    if (i < 1.f && --tail < 0) {
       lo[c] = INT64_MIN;  // never reached in expectation: k_rnd_chunkmap skips it
       continue;
     }
-    lo[c] = (int64_t)llround(i) - kRndK / 2;
-    for (int q = 0; q < 16; ++q) {  // 16 sub-steps of kRndW / 16 draws at the local acceptance rate
-      if (i < 1.0) break;
-      const double m = (double)interval_mask((uint32_t)i) + 1.0;
-      i -= (kRndW / 16) * (i + 1.0) / m;
+    lo[c] = (int64_t)lrintf(i) - kRndK / 2;
+    for (int q = 0; q < 4 && i >= 1.f; ++q) {
+      const float m = (float)interval_mask((uint32_t)i) + 1.f;
+      i -= (kRndW / 4) * (i + 1.f) / m;
     }
   }
 }
@@ -1267,17 +1280,25 @@ __global__ void k_rnd_walk(const uint32_t* __restrict__ raw, ReqCounters* rc, in
   if (i >= 1) atomicOr((unsigned long long*)&rc->err, (unsigned long long)kErrRandom);
 }
 
-__global__ void k_rnd_emit(const uint32_t* __restrict__ raw, const ReqCounters* rc, int64_t chunks,
-                           const int64_t* __restrict__ enter, int32_t* jd) {
+__global__ void __launch_bounds__(32) k_rnd_emit(const uint32_t* __restrict__ raw, const ReqCounters* rc,
+                                                 int64_t chunks, const int64_t* __restrict__ enter, int32_t* jd) {
+  __shared__ uint32_t d[kRndW];
   const int64_t L = rnd_raw_len(rc->R);
-  OB_GRID_STRIDE(c, chunks) {
+  for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     int64_t s = enter[c];
-    const int64_t r0 = c * kRndW, r1 = min(r0 + kRndW, L);
-    for (int64_t r = r0; r < r1 && s >= 1; ++r) {
-      const uint32_t v = __ldg(raw + r) & interval_mask((uint32_t)s);
-      if (v <= (uint32_t)s) {
-        jd[s] = (int32_t)v;
-        --s;
+    if (s < 1) continue;
+    const int64_t r0 = c * kRndW;
+    const int n = (int)max((int64_t)0, min((int64_t)kRndW, L - r0));
+    __syncwarp();
+    for (int r = threadIdx.x; r < n; r += 32) d[r] = raw[r0 + r];
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      for (int r = 0; r < n && s >= 1; ++r) {
+        const uint32_t v = d[r] & interval_mask((uint32_t)s);
+        if (v <= (uint32_t)s) {
+          jd[s] = (int32_t)v;
+          --s;
+        }
       }
     }
   }
@@ -1398,7 +1419,8 @@ static void select_random(Engine& e, RequestWs& w, int64_t r_max) {
     k_rnd_estimate<<<1, 32, 0, s>>>(w.rc, chunks, w.rnd_lo);
     k_rnd_chunkmap<<<(unsigned)(chunks * (kRndK / kRndKCta)), kRndKCta, 0, s>>>(w.rnd_raw, w.rc, w.rnd_lo, w.rnd_exit);
     k_rnd_walk<<<1, 32, 0, s>>>(w.rnd_raw, w.rc, chunks, w.rnd_lo, w.rnd_exit, w.rnd_enter);
-    k_rnd_emit<<<grid_for(chunks, 64), 64, 0, s>>>(w.rnd_raw, w.rc, chunks, w.rnd_enter, w.rnd_j);
+    k_rnd_emit<<<(unsigned)std::min<int64_t>(chunks, kNumSMs * 16), 32, 0, s>>>(w.rnd_raw, w.rc, chunks, w.rnd_enter,
+                                                                                 w.rnd_j);
     g_launches += 4;
   } else {
     k_rnd_draws<<<1, 32, 0, s>>>(w.rnd_raw, w.rc, w.rnd_j);
