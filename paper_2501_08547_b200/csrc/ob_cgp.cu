@@ -531,10 +531,14 @@ void serve_cgp(Engine& e, float* d_out) {
   // identical plan on every rank from the whole request (runtime.py:151-192)
   cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, true);
-  static const bool serial = [] {  // OB_CGP_SERIAL=1: slice sorts on the main stream (A/B)
+  static const bool serial_env = [] {  // OB_CGP_SERIAL=1: slice sorts on the main stream (A/B)
     const char* v = std::getenv("OB_CGP_SERIAL");
     return v && v[0] && v[0] != '0';
   }();
+  // With request lanes on more than two ranks the two-stream request graphs stall each
+  // other across ranks (measured cfg4 P = 4, 4 lanes: 0.72 M vs 3.57 M queries/s serial);
+  // at P = 2 the overlap still pays with lanes (4.51 vs 4.17 M), and always without them
+  const bool serial = serial_env || (e.nlanes > 1 && c.P > 2);
   cudaStream_t side = serial ? s : e.side;
   // the slices' request-index sorts and query blocks (side stream) need only the
   // request and the candidate set: they run beside the selection (main stream);
