@@ -716,6 +716,29 @@ def main():
                     "partials, the layer-2 launch (delta aggregates) its edge list, the recomputed rows (<= D) "
                     "and partials, the query-block launch its edge list, every source row once and partials",
             "share_of_step": round(agg["ms"] / max(reqp["ms"], 1e-9), 3)}
+    # the whole request against HBM, with SURVEY.md 8(d)'s per-unit figure: bytes(G) =
+    # graph_fetch_bytes(G) + sum_l 4 H_l D_l + 4 F B + 16 m per query batch, over the per-request
+    # time of the throughput pass (lanes) -- the bytes the reference's path would move
+    try:
+        import ctypes as C
+
+        outs_b = 0
+        for l in range(1, k + 1):
+            ns, nd, ne = C.c_int64(), C.c_int64(), C.c_int64()
+            nat.check(lib.ob_last_block_sizes(eng._h, 0, l, C.byref(ns), C.byref(nd), C.byref(ne)))
+            outs_b += 4 * model.layers[l - 1].out_dim * nd.value
+        req0 = reqs[0]
+        bytes_g = int(bd0.fetch_bytes) + outs_b + 4 * F * B + 16 * int(req0.edges.shape[0])
+        # each GPU (a CGP group: P GPUs sharing one request) serves `steps` requests in the pass
+        ms_req = (lanes_ms if lanes_ms is not None else total_ms) / args.steps
+        gbs = bytes_g / (P if cgp else 1) / (ms_req / 1e3) / 1e9
+        roof["request"] = {"bytes_per_request": bytes_g, "ms_per_request": round(ms_req, 4),
+                           "achieved": round(gbs, 1), "frac": round(gbs / hbm, 4), "unit": "GB/s per GPU",
+                           "definition": "SURVEY.md 8(d) bytes(G) of one request (divided over the P GPUs of a CGP "
+                                         "group) over the throughput pass's time per request: every request stage, "
+                                         "not one kernel"}
+    except Exception as ex:  # pragma: no cover - reporting only
+        roof["request"] = {"error": str(ex)[:200]}
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
