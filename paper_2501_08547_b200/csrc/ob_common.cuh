@@ -48,6 +48,30 @@ constexpr int kPersistCTAs = kNumSMs * 8;
 extern int64_t g_launches;
 #define OB_LAUNCHED() (++::ob::g_launches)
 
+// Programmatic dependent launch for the per-layer kernel chain: the next kernel's
+// CTAs are scheduled onto SMs as the previous kernel's tail drains and run their
+// prologue; every such kernel calls pdl_wait() before it touches its
+// predecessors' results (griddepcontrol.wait: returns once the prerequisite grid
+// has completed and flushed; a no-op for an ordinary launch).  OB_NO_PDL=1 turns
+// the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  OB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  OB_LAUNCHED();
+}
+
 inline int grid_for(int64_t work, int per_cta, int cap = kPersistCTAs) {
   int64_t g = (work + per_cta - 1) / per_cta;
   if (g < 1) g = 1;

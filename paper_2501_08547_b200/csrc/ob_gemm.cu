@@ -212,12 +212,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t M = *g.M_dev;
-  const int64_t tiles = (M + kTcBM - 1) / kTcBM;
-  // work units: (row tile, column slab); small-M GEMMs split the columns across
-  // CTAs (nslab > 1) so more SMs share the tile's MMAs and epilogue
-  const int ns = g.nslab;
-  const int64_t units = tiles * ns;
   const int KB1 = (g.K1 + kTcBK - 1) / kTcBK, KB2 = (g.K2 + kTcBK - 1) / kTcBK, KB = KB1 + KB2;
 
   if (tid == 0) {
@@ -245,6 +239,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the set-up above (barriers, TMEM allocation) overlaps the previous kernel's tail;
+  // everything below may read its results (the row count M is one of them)
+  pdl_wait();
+  const int64_t M = *g.M_dev;
+  const int64_t tiles = (M + kTcBM - 1) / kTcBM;
+  // work units: (row tile, column slab); small-M GEMMs split the columns across
+  // CTAs (nslab > 1) so more SMs share the tile's MMAs and epilogue
+  const int ns = g.nslab;
+  const int64_t units = tiles * ns;
 
   if (warp < kWarpsProd) {
     // ---------------- A producers ----------------
@@ -493,13 +496,12 @@ static void tc_gemm_slab(cudaStream_t s, const TcGemmArgs& g0, int64_t M_max) {
   const CUtensorMap& ml = *reinterpret_cast<const CUtensorMap*>(ml_raw);
   // smem opt-in is set at weight preparation (tc_gemm_configure), never while a
   // request is being captured into a CUDA graph
-  auto go = [&](auto kern, int bytes) { kern<<<grid, kTcThreads, bytes, s>>>(g, mh, ml); };
+  auto go = [&](auto kern, int bytes) { launch_pdl(kern, dim3(grid), dim3(kTcThreads), (size_t)bytes, s, g, mh, ml); };
   if (np == 32) go(k_tc_gemm<32>, TcSmem<32>::kBytes);
   else if (np == 64) go(k_tc_gemm<64>, TcSmem<64>::kBytes);
   else if (np == 128) go(k_tc_gemm<128>, TcSmem<128>::kBytes);
   else if (np == 256) go(k_tc_gemm<256>, TcSmem<256>::kBytes);
   else throw Error(OB_ESTATE, "tc_gemm: padded N must be 32/64/128/256");
-  OB_LAUNCHED();
 }
 
 static void tc_gemm_configure() {

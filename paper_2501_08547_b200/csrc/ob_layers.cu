@@ -74,6 +74,7 @@ __device__ __forceinline__ int bind_row(const BindCtx& c, int64_t T, int64_t s, 
 
 __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restrict__ src_ids, const float** rowp,
                           float* gscale, uint8_t* kind_out, int32_t* pe_layer_out) {
+  pdl_wait();
   const int64_t S = cnt->S;
   const int64_t T = c.T_dev ? *c.T_dev : 0;
   int64_t nfeat = 0, npe = 0;
@@ -395,6 +396,7 @@ template <int OP, int NV>
 __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WIDE)) k_agg(AggArgs a) {
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t items = a.cnt->items;
   const int col0 = blockIdx.y * (32 * 4 * NV);
@@ -544,6 +546,7 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
 }
 
 __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
+  pdl_wait();
   const int64_t G = a.cnt->groups;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -554,6 +557,7 @@ __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
 #define OB_FIN_MINB 4  // k_finalize CTAs resident per SM (64 registers, no spills)
 #endif
 __global__ void __launch_bounds__(256, OB_FIN_MINB) k_finalize(FinArgs a) {
+  pdl_wait();
   const int64_t D = a.cnt->D;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -637,10 +641,9 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
     AggArgs a = a0;
     a.pass = p;
     a.passes = passes;
-    if (nv == 1) k_agg<OP, 1><<<grid, 32 * kAggWarps, 0, s>>>(a);
-    else if (nv == 2) k_agg<OP, 2><<<grid, 32 * kAggWarps, 0, s>>>(a);
-    else k_agg<OP, 4><<<grid, 32 * kAggWarps, 0, s>>>(a);
-    OB_LAUNCHED();
+    if (nv == 1) launch_pdl(k_agg<OP, 1>, grid, dim3(32 * kAggWarps), 0, s, a);
+    else if (nv == 2) launch_pdl(k_agg<OP, 2>, grid, dim3(32 * kAggWarps), 0, s, a);
+    else launch_pdl(k_agg<OP, 4>, grid, dim3(32 * kAggWarps), 0, s, a);
   }
   // K = -1 marks a stored-aggregate launch: it gathers only the request spans, which the
   // block counters do not size, so the profiler counts its edge list and partials only
@@ -651,11 +654,9 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
 static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t items_max) {
   cudaEvent_t pa = prof_begin(s);
   if (f.group_ptr) {
-    k_reduce_groups<<<grid_for(items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f);
-    OB_LAUNCHED();
+    launch_pdl(k_reduce_groups, dim3(grid_for(items_max / kItemGroup + 1, 8, kNumSMs * 16)), dim3(256), 0, s, f);
   }
-  k_finalize<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(f);
-  OB_LAUNCHED();
+  launch_pdl(k_finalize, dim3(grid_for(D_max, 8, kNumSMs * 16)), dim3(256), 0, s, f);
   prof_end(s, pa, kProfFinalize, f.cnt, f.width, f.pw, 0, 0, 0);
 }
 
@@ -1275,8 +1276,8 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       if (l == 1 && w.qrows_ready) c.qxw = w.qxw;  // layer 1: queries are the only non-table sources
       OB_CUDA(cudaMemsetAsync(w.ndyn, 0, sizeof(int64_t), s));
     }
-    k_resolve<<<grid_for(b.S_max, 256), 256, 0, s>>>(c, b.cnt, b.src_ids, w.rowp, w.gscale, nullptr, nullptr);
-    OB_LAUNCHED();
+    launch_pdl(k_resolve, dim3(grid_for(b.S_max, 256)), dim3(256), 0, s, c, b.cnt, (const int32_t*)b.src_ids, w.rowp,
+               w.gscale, (uint8_t*)nullptr, (int32_t*)nullptr);
     LayerRun r{};
     if (yt) {
       r.yrow = w.yrow;

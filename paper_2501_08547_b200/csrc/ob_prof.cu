@@ -4,11 +4,21 @@
 // the block counters they ran over are snapshotted into pinned memory at the
 // end of each request so the algorithmic bytes of every launch can be
 // computed after the fact without a host round trip inside the request.
+#include <cstdlib>
+
 #include "ob_engine.h"
 
 namespace ob {
 
 Profiler* g_prof = nullptr;
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("OB_NO_PDL");
+    return !(v && v[0] && v[0] != '0');
+  }();
+  return on;
+}
 
 cudaEvent_t Profiler::take() {
   if (next == pool.size()) {
