@@ -42,6 +42,7 @@ __global__ void k_block_spans(const int32_t* __restrict__ dst_ids, const BlockCo
                               const int64_t* __restrict__ offsets, const int32_t* __restrict__ indeg,
                               const uint32_t* cbits, const int64_t* cwpre, const int64_t* rq_ptr,
                               const ReqCounters* rc, SegSpans sp, int64_t* seg_len) {
+  pdl_wait();
   const int64_t D = cnt->D;
   const int64_t R = rc->R;
   const bool bad = rc->err & (kErrRange | kErrNoQuery);
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(1024) k_block_fill(const BlockCounters* cnt, c
                                                      const int32_t* __restrict__ nbrs,
                                                      const int32_t* __restrict__ rq_src, int32_t* src_global,
                                                      uint32_t* sbits, int64_t words, uint32_t* part_bits) {
+  pdl_wait();
   extern __shared__ uint32_t sbm[];
   const int64_t items = cnt->items;
   const int lane = threadIdx.x & 31;
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(128) k_sample_spans(const int32_t* __restrict_
                                                       SegSpans sp, const int32_t* __restrict__ nbrs,
                                                       const int32_t* __restrict__ rq_src, int fan, int layer,
                                                       uint64_t seed, int32_t* samp, int64_t* seg_len) {
+  pdl_wait();
   const int64_t D = cnt->D;
   OB_GRID_STRIDE(i, D) {
     const int32_t cl = sp.cl[i], rl = sp.rl[i];
@@ -272,6 +275,7 @@ __global__ void __launch_bounds__(128) k_sample_spans(const int32_t* __restrict_
 }
 
 __global__ void k_bitmap_or(const uint32_t* __restrict__ part_bits, int nparts, int64_t words, uint32_t* sbits) {
+  pdl_wait();
   OB_GRID_STRIDE(w, words) {
     uint32_t v = 0;
     for (int p = 0; p < nparts; ++p) v |= __ldg(part_bits + (int64_t)p * words + w);
@@ -289,6 +293,7 @@ void configure_fill() {
 __global__ void __launch_bounds__(256) k_expand_items(const BlockCounters* cnt, const int64_t* __restrict__ item_ptr,
                                                       const int64_t* __restrict__ group_ptr, int32_t* item_dst,
                                                       int32_t* group_dst) {
+  pdl_wait();
   const int64_t D = cnt->D;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -301,23 +306,25 @@ __global__ void __launch_bounds__(256) k_expand_items(const BlockCounters* cnt, 
 
 void expand_items(cudaStream_t s, const BlockCounters* cnt, int64_t D_max, const int64_t* item_ptr,
                   const int64_t* group_ptr, int32_t* item_dst, int32_t* group_dst) {
-  k_expand_items<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(cnt, item_ptr, group_ptr, item_dst, group_dst);
-  OB_LAUNCHED();
+  launch_pdl(k_expand_items, dim3(grid_for(D_max, 8, kNumSMs * 16)), dim3(256), 0, s, cnt, item_ptr, group_ptr, item_dst, group_dst);
 }
 
 __global__ void k_mark_ids(const int32_t* __restrict__ ids, const BlockCounters* cnt, uint32_t* sbits) {
+  pdl_wait();
   const int64_t D = cnt->D;
   OB_GRID_STRIDE(i, D) bm_set(sbits, ids[i]);
 }
 
 __global__ void k_relabel(const BlockCounters* cnt, const int32_t* __restrict__ src_global, const uint32_t* sbits,
                           const int64_t* swpre, int32_t* edge_src) {
+  pdl_wait();
   const int64_t E = cnt->E;
   OB_GRID_STRIDE(e, E) edge_src[e] = (int32_t)bm_rank(sbits, swpre, src_global[e]);
 }
 
 __global__ void k_self_rows(const BlockCounters* cnt, const int32_t* __restrict__ dst_ids, const uint32_t* sbits,
                             const int64_t* swpre, int32_t* self_src) {
+  pdl_wait();
   const int64_t D = cnt->D;
   OB_GRID_STRIDE(i, D) self_src[i] = (int32_t)bm_rank(sbits, swpre, dst_ids[i]);
 }
@@ -325,17 +332,20 @@ __global__ void k_self_rows(const BlockCounters* cnt, const int32_t* __restrict_
 // srpe destination lists ------------------------------------------------------
 __global__ void k_mid_dst(const ReqCounters* rc, int64_t N, int B, const int32_t* targets, int32_t* dst_ids,
                           BlockCounters* cnt) {
+  pdl_wait();
   const int64_t T = rc->T, D = T + B;
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt->D = D;
   OB_GRID_STRIDE(i, D) dst_ids[i] = i < T ? targets[i] : (int32_t)(N + (i - T));
 }
 
 __global__ void k_query_dst(int64_t N, int B, int32_t* dst_ids, BlockCounters* cnt) {
+  pdl_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt->D = B;
   OB_GRID_STRIDE(i, (int64_t)B) dst_ids[i] = (int32_t)(N + i);
 }
 
-__global__ void k_copy_count_D(BlockCounters* dst, const BlockCounters* src) { dst->D = src->S; }
+__global__ void k_copy_count_D(BlockCounters* dst, const BlockCounters* src) {
+  pdl_wait(); dst->D = src->S; }
 
 // generic block assembly over an already written dst list + counts->D.
 // `src` names the CSR the destinations pull from (the whole graph, or a CGP
@@ -349,13 +359,11 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const Bu
   sp.rs = sc.span_rs;
   sp.rl = sc.span_rl;
   sp.samp = sc.samp;
-  k_block_spans<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, e.g.N, src.offsets, src.deg, w.cbits,
+  launch_pdl(k_block_spans, dim3(grid_for(b.D_max, 256)), dim3(256), 0, s, b.dst_ids, b.cnt, e.g.N, src.offsets, src.deg, w.cbits,
                                                         w.cwpre, src.rq_ptr, w.rc, sp, sc.seg_len);
-  OB_LAUNCHED();
   if (fan > 0) {
-    k_sample_spans<<<grid_for(b.D_max, 128), 128, 0, s>>>(b.dst_ids, b.cnt, sp, src.nbrs, src.rq_src, fan, layer,
+    launch_pdl(k_sample_spans, dim3(grid_for(b.D_max, 128)), dim3(128), 0, s, b.dst_ids, b.cnt, sp, src.nbrs, src.rq_src, fan, layer,
                                                            e.cfg.seed, sc.samp, sc.seg_len);
-    OB_LAUNCHED();
   }
   // dst_ptr / item_ptr / group_ptr (+ E, items, groups) in one pass; the work
   // items double as the fill's edge chunks
@@ -364,38 +372,31 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const Bu
   expand_items(s, b.cnt, b.D_max, b.item_ptr, b.group_ptr, b.item_dst, b.group_dst);
   if (w.words_NB <= kFillSmemWords) {  // per-CTA shared bitmaps, then one OR pass
     const int64_t words = w.words_NB + 1;
-    k_block_fill<true><<<kNumSMs, 1024, words * 4, s>>>(b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs,
+    launch_pdl(k_block_fill<true>, dim3(kNumSMs), dim3(1024), words * 4, s, b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs,
                                                         src.rq_src, sc.src_global, nullptr, words, sc.fill_bits);
-    k_bitmap_or<<<grid_for(words, 256), 256, 0, s>>>(sc.fill_bits, kNumSMs, words, sc.sbits);
-    g_launches += 2;
+    launch_pdl(k_bitmap_or, dim3(grid_for(words, 256)), dim3(256), 0, s, sc.fill_bits, kNumSMs, words, sc.sbits);
   } else {
     OB_CUDA(cudaMemsetAsync(sc.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
-    k_block_fill<false><<<grid_for(b.items_max, 32, kNumSMs * 2), 1024, 0, s>>>(
+    launch_pdl(k_block_fill<false>, dim3(grid_for(b.items_max, 32, kNumSMs * 2)), dim3(1024), 0, s, 
         b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs, src.rq_src, sc.src_global, sc.sbits, 0, nullptr);
-    OB_LAUNCHED();
   }
   if (b.has_self) {
-    k_mark_ids<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.dst_ids, b.cnt, sc.sbits);
-    OB_LAUNCHED();
+    launch_pdl(k_mark_ids, dim3(grid_for(b.D_max, 256)), dim3(256), 0, s, b.dst_ids, b.cnt, sc.sbits);
   }
   device_scan(s, e.scan, LoadPopc{sc.sbits}, StoreI64{sc.swpre}, nullptr, w.words_NB, w.words_NB, &b.cnt->S, sc.swpre);
   k_bitmap_compact_ext(e, sc.sbits, sc.swpre, w.words_NB, b.src_ids);
-  k_relabel<<<grid_for(b.E_max, 256), 256, 0, s>>>(b.cnt, sc.src_global, sc.sbits, sc.swpre, b.edge_src);
-  OB_LAUNCHED();
+  launch_pdl(k_relabel, dim3(grid_for(b.E_max, 256)), dim3(256), 0, s, b.cnt, sc.src_global, sc.sbits, sc.swpre, b.edge_src);
   if (b.has_self) {
-    k_self_rows<<<grid_for(b.D_max, 256), 256, 0, s>>>(b.cnt, b.dst_ids, sc.sbits, sc.swpre, b.self_src);
-    OB_LAUNCHED();
+    launch_pdl(k_self_rows, dim3(grid_for(b.D_max, 256)), dim3(256), 0, s, b.cnt, b.dst_ids, sc.sbits, sc.swpre, b.self_src);
   }
 }
 
 void write_mid_dst(Engine& e, RequestWs& w, BlockDev& b) {
-  k_mid_dst<<<grid_for(b.D_max, 256), 256, 0, e.stream>>>(w.rc, e.g.N, w.B, w.targets, b.dst_ids, b.cnt);
-  OB_LAUNCHED();
+  launch_pdl(k_mid_dst, dim3(grid_for(b.D_max, 256)), dim3(256), 0, e.stream, w.rc, e.g.N, w.B, w.targets, b.dst_ids, b.cnt);
 }
 
 void write_query_dst(Engine& e, RequestWs& w, BlockDev& b) {
-  k_query_dst<<<grid_for(w.B, 256), 256, 0, e.stream>>>(e.g.N, w.B, b.dst_ids, b.cnt);
-  OB_LAUNCHED();
+  launch_pdl(k_query_dst, dim3(grid_for(w.B, 256)), dim3(256), 0, e.stream, e.g.N, w.B, b.dst_ids, b.cnt);
 }
 
 
@@ -422,8 +423,7 @@ void stage_build_full(Engine& e, RequestWs& w) {
     BlockDev& b = w.blocks[l - 1];
     if (l < k) {
       BlockDev& up = w.blocks[l];  // b.dst_ids aliases up.src_ids (carve)
-      k_copy_count_D<<<1, 1, 0, s>>>(b.cnt, up.cnt);
-      OB_LAUNCHED();
+      launch_pdl(k_copy_count_D, dim3(1), dim3(1), 0, s, b.cnt, up.cnt);
     }
     const bool samp = e.cfg.strategy == OB_STRATEGY_SAMPLED;
     assemble(e, w, b, src, w.bs[0], samp ? e.cfg.fanouts[l - 1] : 0, l);

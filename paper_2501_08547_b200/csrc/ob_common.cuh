@@ -158,6 +158,7 @@ struct ScanTiles {
 template <class T, int ITEMS, class Load, class Store, class Total>
 __global__ void __launch_bounds__(kScanThreads, sizeof(T) == 8 ? OB_SCAN_MINB : 1) k_scan(Load load, Store store, Total total, const int64_t* n_dev,
                                                        int64_t n_host, ScanTiles<T> st) {
+  pdl_wait();
   using BS = cub::BlockScan<T, kScanThreads>;
   using BX = cub::BlockExchange<T, kScanThreads, ITEMS>;
   // 8-byte values move warp-striped (coalesced loads and stores) and are
@@ -310,6 +311,7 @@ struct TotalI64 {
 template <class Load>
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Load load, const int64_t* n_dev, int64_t n_host,
                                                               int64_t* tile_sums) {
+  pdl_wait();
   using BR = cub::BlockReduce<int64_t, kScanThreads>;
   __shared__ typename BR::TempStorage tmp;
   const int64_t n = dev_count(n_dev, n_host);
@@ -333,6 +335,7 @@ template <class Load, class Store, class Total>
 __global__ void __launch_bounds__(kScanThreads, OB_SCAN_MINB) k_scan_down(Load load, Store store, Total total,
                                                             const int64_t* n_dev, int64_t n_host,
                                                             const int64_t* tile_off) {
+  pdl_wait();
   using BS = cub::BlockScan<int64_t, kScanThreads>;
   using BX = cub::BlockExchange<int64_t, kScanThreads, kScanItems>;
   __shared__ union {
@@ -380,15 +383,15 @@ void device_scan_t(cudaStream_t s, ScanScratch& sc, Load load, Store store, Tota
   if constexpr (std::is_same<T, int64_t>::value) {
     if (tiles > 4 * kNumSMs) {  // long input: reduce, spine, downsweep
       int64_t* sums = reinterpret_cast<int64_t*>(st.agg);
-      k_scan_reduce<<<g, kScanThreads, 0, s>>>(load, n_dev, n_host, sums);
-      k_scan_spine<<<1, 1024, 0, s>>>(n_dev, n_host, sums);
-      k_scan_down<<<g, kScanThreads, 0, s>>>(load, store, total, n_dev, n_host, sums);
-      g_launches += 3;
+      launch_pdl(k_scan_reduce<Load>, dim3(g), dim3(kScanThreads), 0, s, load, n_dev, n_host, sums);
+      launch_pdl(k_scan_spine, dim3(1), dim3(1024), 0, s, n_dev, n_host, sums);
+      launch_pdl(k_scan_down<Load, Store, Total>, dim3(g), dim3(kScanThreads), 0, s, load, store, total, n_dev, n_host,
+                 (const int64_t*)sums);
       return;
     }
   }
-  k_scan<T, kScanItems><<<g, kScanThreads, 0, s>>>(load, store, total, n_dev, n_host, st);
-  ++g_launches;
+  launch_pdl(k_scan<T, kScanItems, Load, Store, Total>, dim3(g), dim3(kScanThreads), 0, s, load, store, total, n_dev,
+             n_host, st);
 }
 
 // int64 scan; out_arr (optional): the plain array behind `store`, out_arr[n] = total.

@@ -28,6 +28,7 @@ int64_t g_launches = 0;
 
 // exclusive scan of the tile sums in place (one CTA; long scans only)
 __global__ void __launch_bounds__(1024) k_scan_spine(const int64_t* n_dev, int64_t n_host, int64_t* tile_sums) {
+  pdl_wait();
   using BS = cub::BlockScan<int64_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int64_t carry;
@@ -66,6 +67,7 @@ constexpr int kMaxSmemQueries = 12288;
 
 __global__ void __launch_bounds__(256) k_request_mark(const ReqParams* rp, int64_t N, int B, uint32_t* cbits,
                                                       int32_t* qdeg, ReqCounters* rc) {
+  pdl_wait();
   extern __shared__ int32_t sq[];  // per-CTA query in-degree histogram (B entries) when B fits
   const int64_t* __restrict__ edges = rp->edges;
   const int64_t m = rp->m;
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(256) k_request_mark(const ReqParams* rp, int64
 }
 
 __global__ void k_check_finite(const ReqParams* rp, int64_t n, ReqCounters* rc) {
+  pdl_wait();
   const float* __restrict__ q = rp->qfeat;
   bool bad = false;
   OB_GRID_STRIDE(i, n) bad |= !isfinite(q[i]);
@@ -122,6 +125,7 @@ __global__ void k_check_finite(const ReqParams* rp, int64_t n, ReqCounters* rc) 
 // ids of set bits in ascending order (bitmap -> sorted unique list)
 __global__ void k_bitmap_compact(const uint32_t* __restrict__ bits, const int64_t* __restrict__ wpre, int64_t words,
                                  int32_t* out) {
+  pdl_wait();
   OB_GRID_STRIDE(w, words) {
     uint32_t b = bits[w];
     int64_t pos = wpre[w];
@@ -134,12 +138,12 @@ __global__ void k_bitmap_compact(const uint32_t* __restrict__ bits, const int64_
 }
 
 void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, int64_t words, int32_t* out) {
-  k_bitmap_compact<<<grid_for(words, 256), 256, 0, e.stream>>>(bits, wpre, words, out);
-  OB_LAUNCHED();
+  launch_pdl(k_bitmap_compact, dim3(grid_for(words, 256)), dim3(256), 0, e.stream, bits, wpre, words, out);
 }
 
 // RB = R + B slots; query slots take their counts from the per-query in-degrees
 __global__ void k_slots_init(ReqCounters* rc, int B, const int32_t* qdeg, int32_t* rq_cnt, int32_t* rq_fill) {
+  pdl_wait();
   const int64_t R = rc->R;
   if (blockIdx.x == 0 && threadIdx.x == 0) rc->RB = R + B;
   const int64_t RB = R + B;
@@ -165,6 +169,7 @@ __device__ __forceinline__ K rq_key(int64_t s, int64_t d, int64_t N, const uint3
 template <class K>
 __global__ void k_rq_count(const ReqParams* rp, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
                            const ReqCounters* rc, int32_t* rq_cnt, K* keys, RqKeyFmt f) {
+  pdl_wait();
   if (rc->err & (kErrRange | kErrNoQuery)) return;
   const int64_t* __restrict__ edges = rp->edges;
   const int64_t m = rp->m;
@@ -187,6 +192,7 @@ template <class K>
 __global__ void k_rq_count_all(const int64_t* __restrict__ edges, const int64_t* m_dev, int64_t N,
                                const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt,
                                K* keys, RqKeyFmt f) {
+  pdl_wait();
   if (rc->err & (kErrRange | kErrNoQuery)) return;
   const int64_t R = rc->R, m = *m_dev;  // a CGP slice: edges live in the arena
   OB_GRID_STRIDE(e, m) {
@@ -198,6 +204,7 @@ __global__ void k_rq_count_all(const int64_t* __restrict__ edges, const int64_t*
 }
 
 __global__ void k_zero_slots(const ReqCounters* rc, int B, int32_t* a, int32_t* b) {
+  pdl_wait();
   const int64_t RB = rc->R + B;
   OB_GRID_STRIDE(i, RB) a[i] = b[i] = 0;
 }
@@ -210,6 +217,7 @@ __global__ void k_zero_slots(const ReqCounters* rc, int B, int32_t* a, int32_t* 
 __global__ void k_score(const int32_t* __restrict__ cand_ids, const int32_t* __restrict__ rq_cnt,
                         const int32_t* __restrict__ indeg, ReqCounters* rc, int32_t* cand_nq, double* score,
                         uint64_t* key, int32_t* tpos, bool ratio) {
+  pdl_wait();
   const int64_t R = rc->R;
   bool bad = false;
   OB_GRID_STRIDE(c, R) {
@@ -433,6 +441,7 @@ __global__ void __launch_bounds__(32 * kIsWarps) k_is_rows(int64_t N, const int6
                                                            const int32_t* __restrict__ src,
                                                            const int32_t* __restrict__ indeg, double* out,
                                                            int32_t* big, int32_t* nbig) {
+  pdl_wait();
   __shared__ int starts[kIsWarps][kPwLeafCap];
   __shared__ double sums[kIsWarps][kPwLeafCap];
   const int wid = threadIdx.x >> 5;
@@ -455,6 +464,7 @@ __global__ void __launch_bounds__(32 * kIsWarps) k_is_big(const int32_t* __restr
                                                           const int64_t* __restrict__ off,
                                                           const int32_t* __restrict__ src,
                                                           const int32_t* __restrict__ indeg, double* out) {
+  pdl_wait();
   __shared__ int starts[kIsWarps][kPwLeafCap];
   __shared__ double sums[kIsWarps][kPwLeafCap];
   __shared__ int64_t c_off[kIsBigChunks];
@@ -548,10 +558,8 @@ void build_is_table(Engine& e, const int64_t* off, const int32_t* src, double* o
   int32_t* big = (int32_t*)e.dalloc(sizeof(int32_t) * (N + 1));
   int32_t* nbig = (int32_t*)e.dalloc(sizeof(int32_t));
   OB_CUDA(cudaMemsetAsync(nbig, 0, sizeof(int32_t), s));
-  k_is_rows<<<grid_for(N, kIsWarps, kNumSMs * 8), 32 * kIsWarps, 0, s>>>(N, off, src, e.g.indeg, out, big, nbig);
-  OB_LAUNCHED();
-  k_is_big<<<kNumSMs, 32 * kIsWarps, 0, s>>>(big, nbig, off, src, e.g.indeg, out);
-  OB_LAUNCHED();
+  launch_pdl(k_is_rows, dim3(grid_for(N, kIsWarps, kNumSMs * 8)), dim3(32 * kIsWarps), 0, s, N, off, src, e.g.indeg, out, big, nbig);
+  launch_pdl(k_is_big, dim3(kNumSMs), dim3(32 * kIsWarps), 0, s, big, nbig, off, src, e.g.indeg, out);
   OB_CUDA(cudaStreamSynchronize(s));
   e.dfree(big);
   e.dfree(nbig);
@@ -559,19 +567,20 @@ void build_is_table(Engine& e, const int64_t* off, const int32_t* src, double* o
 
 __global__ void k_is_gather(const int32_t* __restrict__ cand_ids, const ReqCounters* rc,
                             const double* __restrict__ tab, double* out) {
+  pdl_wait();
   const int64_t R = rc->R;
   OB_GRID_STRIDE(c, R) out[c] = tab[cand_ids[c]];
 }
 
 void launch_is_gather(Engine& e, RequestWs& w, const double* tab, double* out) {
   const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
-  k_is_gather<<<grid_for(r_max, 256), 256, 0, e.stream>>>(w.cand_ids, w.rc, tab, out);
-  OB_LAUNCHED();
+  launch_pdl(k_is_gather, dim3(grid_for(r_max, 256)), dim3(256), 0, e.stream, w.cand_ids, w.rc, tab, out);
 }
 
 // scores from P partial arrays, summed in rank order (P = 1: the centralized row sum)
 __global__ void k_score_is(const int32_t* __restrict__ cand_ids, const int32_t* __restrict__ indeg,
                            const ReqCounters* rc, IsParts parts, double* score, uint64_t* key) {
+  pdl_wait();
   const int64_t R = rc->R;
   OB_GRID_STRIDE(c, R) {
     double sum = 0.0;
@@ -585,12 +594,12 @@ __global__ void k_score_is(const int32_t* __restrict__ cand_ids, const int32_t* 
 
 void launch_score_is(Engine& e, RequestWs& w, const IsParts& parts) {
   const int64_t r_max = std::min<int64_t>(e.g.N, 2 * w.m);
-  k_score_is<<<grid_for(r_max, 256), 256, 0, e.stream>>>(w.cand_ids, e.g.indeg, w.rc, parts, w.cand_score,
+  launch_pdl(k_score_is, dim3(grid_for(r_max, 256)), dim3(256), 0, e.stream, w.cand_ids, e.g.indeg, w.rc, parts, w.cand_score,
                                                          w.cand_key);
-  OB_LAUNCHED();
 }
 
 __global__ void k_budget(ReqCounters* rc, double gamma, uint32_t* hist) {
+  pdl_wait();
   // budget = int(np.floor(gamma * m)) with gamma a Python float: one IEEE fp64 multiply
   const int64_t R = rc->R;
   const int64_t b = (int64_t)floor(gamma * (double)R);
@@ -612,6 +621,7 @@ __global__ void k_budget(ReqCounters* rc, double gamma, uint32_t* hist) {
 // picks this round's digit (scan from the top digit) and clears hist.
 __global__ void __launch_bounds__(256) k_sel_round(const uint64_t* __restrict__ key, ReqCounters* rc, int shift,
                                                    uint32_t* hist) {
+  pdl_wait();
   using BS = cub::BlockScan<int64_t, 256>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ uint32_t h[256];
@@ -709,6 +719,7 @@ constexpr int kRxItems = kRxTile / kRxThreads;  // 8 keys per thread, warp-strip
 template <class K>
 __global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* __restrict__ keys, const int64_t* m_dev, int shift,
                                                         int64_t tiles_b, int32_t* cnt) {
+  pdl_wait();
   __shared__ int32_t h[256];
   const int64_t m = *m_dev;
   const int64_t tiles = (m + kRxTile - 1) / kRxTile;
@@ -729,6 +740,7 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* __restrict__ ke
 template <class K>
 __global__ void __launch_bounds__(kRxThreads) k_rx_ghist(const K* __restrict__ keys, const int64_t* m_dev, int passes,
                                                          uint32_t* ghist) {
+  pdl_wait();
   __shared__ uint32_t h[8 * 256];
   for (int i = threadIdx.x; i < passes * 256; i += kRxThreads) h[i] = 0;
   __syncthreads();
@@ -753,6 +765,7 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
                                                            const int32_t* __restrict__ cand_ids,
                                                            const ReqCounters* rc, uint32_t* st, uint32_t* ticket,
                                                            const uint32_t* __restrict__ ghist) {
+  pdl_wait();
   using BS = cub::BlockScan<int32_t, kRxThreads>;
   using BS64 = cub::BlockScan<int64_t, kRxThreads>;
   __shared__ typename BS64::TempStorage scan_tmp64;
@@ -912,16 +925,15 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
     uint32_t* ticket = st + 8 * 256 * tiles_b;
     uint32_t* ghist = ticket + 8;
     OB_CUDA(cudaMemsetAsync(st, 0, sizeof(uint32_t) * rx_st_words(m_bound), s));
-    k_rx_ghist<K><<<grid_for(m_bound, kRxThreads * 8, kNumSMs * 2), kRxThreads, 0, s>>>(a, m_dev, passes, ghist);
-    OB_LAUNCHED();
+    launch_pdl(k_rx_ghist<K>, dim3(grid_for(m_bound, kRxThreads * 8, kNumSMs * 2)), dim3(kRxThreads), 0, s, a, m_dev, passes, ghist);
     for (int p = 0; p < passes; ++p) {
       const int shift = 8 * p;
       uint32_t* sp = st + (int64_t)p * 256 * tiles_b;
       if (p + 1 == passes) {
-        k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
+        launch_pdl(k_rx_scatter<K, true>, dim3(g), dim3(kRxThreads), 0, s, a, nullptr, c.src, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
                                                         e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p);
       } else {
-        k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
+        launch_pdl(k_rx_scatter<K, false>, dim3(g), dim3(kRxThreads), 0, s, a, b, nullptr, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
                                                          e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p);
         std::swap(a, b);
       }
@@ -933,15 +945,14 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
   const int64_t* off = fused ? nullptr : c.rx_off;
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
-    k_rx_hist<K><<<g, kRxThreads, 0, s>>>(a, m_dev, shift, tiles_b, c.rx_cnt);
-    OB_LAUNCHED();
+    launch_pdl(k_rx_hist<K>, dim3(g), dim3(kRxThreads), 0, s, a, m_dev, shift, tiles_b, c.rx_cnt);
     if (!fused)
       device_scan(s, e.scan, LoadI32{c.rx_cnt}, StoreI64{c.rx_off}, nullptr, 256 * tiles_b, 256 * tiles_b, nullptr);
     if (p + 1 == passes) {
-      k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(a, nullptr, c.src, m_dev, shift, tiles_b, off, c.rx_cnt, f,
+      launch_pdl(k_rx_scatter<K, true>, dim3(g), dim3(kRxThreads), 0, s, a, nullptr, c.src, m_dev, shift, tiles_b, off, c.rx_cnt, f,
                                                       e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr);
     } else {
-      k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(a, b, nullptr, m_dev, shift, tiles_b, off, c.rx_cnt, f,
+      launch_pdl(k_rx_scatter<K, false>, dim3(g), dim3(kRxThreads), 0, s, a, b, nullptr, m_dev, shift, tiles_b, off, c.rx_cnt, f,
                                                        e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr);
       std::swap(a, b);
     }
@@ -977,24 +988,20 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   OB_CUDA(cudaMemsetAsync(w.qdeg, 0, sizeof(int32_t) * (w.B + 1), s));
   const size_t sq = w.B <= kMaxSmemQueries ? sizeof(int32_t) * w.B : 0;
   if (m > 0) {
-    k_request_mark<<<grid_for(m, kEdgeTile, kNumSMs * 4), 256, sq, s>>>(w.rp, N, w.B, w.cbits, w.qdeg, w.rc);
-    OB_LAUNCHED();
+    launch_pdl(k_request_mark, dim3(grid_for(m, kEdgeTile, kNumSMs * 4)), dim3(256), sq, s, w.rp, N, w.B, w.cbits, w.qdeg, w.rc);
   }
   // candidate set: popcount prefix, ascending ids
   device_scan(s, e.scan, LoadPopc{w.cbits}, StoreI64{w.cwpre}, nullptr, w.words_N, w.words_N, &w.rc->R, w.cwpre);
-  k_bitmap_compact<<<grid_for(w.words_N, 256), 256, 0, s>>>(w.cbits, w.cwpre, w.words_N, w.cand_ids);
-  OB_LAUNCHED();
+  launch_pdl(k_bitmap_compact, dim3(grid_for(w.words_N, 256)), dim3(256), 0, s, w.cbits, w.cwpre, w.words_N, w.cand_ids);
   const int64_t rb_max = std::min<int64_t>(N, 2 * m) + w.B;
-  k_slots_init<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rc, w.B, w.qdeg, w.rq_cnt, w.rq_fill);
-  OB_LAUNCHED();
+  launch_pdl(k_slots_init, dim3(grid_for(rb_max, 256)), dim3(256), 0, s, w.rc, w.B, w.qdeg, w.rq_cnt, w.rq_fill);
   if (m > 0) {  // candidate-slot counts + the request CSR's radix keys
     const RqKeyFmt f = rq_key_fmt(e, w);
     if (f.wide())
-      k_rq_count<uint64_t><<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt, w.rq_keys, f);
+      launch_pdl(k_rq_count<uint64_t>, dim3(grid_for(m, 256)), dim3(256), 0, s, w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt, w.rq_keys, f);
     else
-      k_rq_count<uint32_t><<<grid_for(m, 256), 256, 0, s>>>(w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt,
+      launch_pdl(k_rq_count<uint32_t>, dim3(grid_for(m, 256)), dim3(256), 0, s, w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt,
                                                             reinterpret_cast<uint32_t*>(w.rq_keys), f);
-    OB_LAUNCHED();
   }
   (void)need_scores;
 }
@@ -1006,14 +1013,12 @@ void stage_request_post(Engine& e, RequestWs& w, bool need_scores) {
   const int64_t N = e.g.N;
   const int64_t m = w.m;
   if ((int64_t)w.B * e.g.F > 0) {
-    k_check_finite<<<grid_for((int64_t)w.B * e.g.F, 256), 256, 0, s>>>(w.rp, (int64_t)w.B * e.g.F, w.rc);
-    OB_LAUNCHED();
+    launch_pdl(k_check_finite, dim3(grid_for((int64_t)w.B * e.g.F, 256)), dim3(256), 0, s, w.rp, (int64_t)w.B * e.g.F, w.rc);
   }
   if (need_scores) {
     const int64_t r_max = std::min<int64_t>(N, 2 * m);
-    k_score<<<grid_for(r_max, 256), 256, 0, s>>>(w.cand_ids, w.rq_cnt, e.g.indeg, w.rc, w.cand_nq, w.cand_score,
+    launch_pdl(k_score, dim3(grid_for(r_max, 256)), dim3(256), 0, s, w.cand_ids, w.rq_cnt, e.g.indeg, w.rc, w.cand_nq, w.cand_score,
                                                  w.cand_key, w.cand_tpos, e.cfg.policy == OB_POLICY_RATIO);
-    OB_LAUNCHED();
   }
 }
 
@@ -1030,16 +1035,14 @@ void stage_select(Engine& e, RequestWs& w) {
     ip.part[0] = w.is_part;
     launch_score_is(e, w, ip);
   }
-  k_budget<<<1, 256, 0, s>>>(w.rc, e.cfg.gamma, w.sel_hist);
-  OB_LAUNCHED();
+  launch_pdl(k_budget, dim3(1), dim3(256), 0, s, w.rc, e.cfg.gamma, w.sel_hist);
   if (e.cfg.policy == OB_POLICY_RANDOM) {
     // zero scores (runtime.py:182-183); the chosen ranks' keys are 1 against threshold 0
     OB_CUDA(cudaMemsetAsync(w.cand_score, 0, sizeof(double) * std::max<int64_t>(r_max, 1), s));
     select_random(e, w, r_max);
   }
   for (int shift = 56; shift >= 0 && e.cfg.policy != OB_POLICY_RANDOM; shift -= 8) {
-    k_sel_round<<<grid_for(r_max, 256, kNumSMs * 2), 256, 0, s>>>(w.cand_key, w.rc, shift, w.sel_hist);
-    OB_LAUNCHED();
+    launch_pdl(k_sel_round, dim3(grid_for(r_max, 256, kNumSMs * 2)), dim3(256), 0, s, w.cand_key, w.rc, shift, w.sel_hist);
   }
   // ordered compaction: ties at the threshold resolved by ascending id
   const SelLoad ld{w.cand_key, w.rc};
@@ -1105,6 +1108,7 @@ __device__ __forceinline__ uint64_t pcg_out(unsigned __int128 st) {  // XSL-RR
 }
 
 __global__ void k_rnd_raw(Pcg128 g, const ReqCounters* rc, uint32_t* raw) {
+  pdl_wait();
   const int64_t n64 = rnd_raw_len(rc->R) / 2;
   const int64_t chunks = (n64 + kRndChunk - 1) / kRndChunk;
   OB_GRID_STRIDE(c, chunks) {
@@ -1125,6 +1129,7 @@ __device__ __forceinline__ uint32_t interval_mask(uint32_t m) { return 0xFFFFFFF
 
 // one warp: j[i] for i = R-1 .. 1 from the raw stream
 __global__ void __launch_bounds__(32) k_rnd_draws(const uint32_t* __restrict__ raw, ReqCounters* rc, int32_t* jd) {
+  pdl_wait();
   __shared__ uint32_t buf[2048];
   const int lane = threadIdx.x;
   const int64_t R = rc->R;
@@ -1227,6 +1232,7 @@ __device__ __forceinline__ int64_t rnd_step_exit(const uint32_t* d, int n, int64
 // the expected entering step of every chunk (deterministic: expected acceptances,
 // four sub-steps per chunk at the local acceptance rate (i + 1) / (mask(i) + 1))
 __global__ void k_rnd_estimate(const ReqCounters* rc, int64_t chunks, int64_t* lo) {
+  pdl_wait();
   if (threadIdx.x || blockIdx.x) return;
   float i = (float)(rc->R - 1);
   int64_t tail = 4;  // chunks evaluated past the expected end of the walk
@@ -1245,6 +1251,7 @@ __global__ void k_rnd_estimate(const ReqCounters* rc, int64_t chunks, int64_t* l
 
 __global__ void __launch_bounds__(kRndKCta) k_rnd_chunkmap(const uint32_t* __restrict__ raw, const ReqCounters* rc,
                                                            const int64_t* __restrict__ lo, int32_t* exit_) {
+  pdl_wait();
   __shared__ uint32_t d[kRndW];
   const int64_t R = rc->R;
   const int64_t L = rnd_raw_len(R);
@@ -1261,6 +1268,7 @@ __global__ void __launch_bounds__(kRndKCta) k_rnd_chunkmap(const uint32_t* __res
 
 __global__ void k_rnd_walk(const uint32_t* __restrict__ raw, ReqCounters* rc, int64_t chunks,
                            const int64_t* __restrict__ lo, const int32_t* __restrict__ exit_, int64_t* enter) {
+  pdl_wait();
   if (threadIdx.x || blockIdx.x) return;
   const int64_t R = rc->R;
   const int64_t L = rnd_raw_len(R);
@@ -1282,6 +1290,7 @@ __global__ void k_rnd_walk(const uint32_t* __restrict__ raw, ReqCounters* rc, in
 
 __global__ void __launch_bounds__(32) k_rnd_emit(const uint32_t* __restrict__ raw, const ReqCounters* rc,
                                                  int64_t chunks, const int64_t* __restrict__ enter, int32_t* jd) {
+  pdl_wait();
   __shared__ uint32_t d[kRndW];
   const int64_t L = rnd_raw_len(rc->R);
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
@@ -1305,6 +1314,7 @@ __global__ void __launch_bounds__(32) k_rnd_emit(const uint32_t* __restrict__ ra
 }
 
 __global__ void k_rnd_count(const ReqCounters* rc, const int32_t* __restrict__ jd, int32_t* cnt) {
+  pdl_wait();
   const int64_t R = rc->R;
   OB_GRID_STRIDE(t, R) {
     if (t >= 1) atomicAdd(cnt + jd[t], 1);
@@ -1313,6 +1323,7 @@ __global__ void k_rnd_count(const ReqCounters* rc, const int32_t* __restrict__ j
 
 __global__ void k_rnd_fill(const ReqCounters* rc, const int32_t* __restrict__ jd, const int64_t* __restrict__ off,
                            int32_t* fill, int32_t* lst) {
+  pdl_wait();
   const int64_t R = rc->R;
   OB_GRID_STRIDE(t, R) {
     if (t >= 1) {
@@ -1324,6 +1335,7 @@ __global__ void k_rnd_fill(const ReqCounters* rc, const int32_t* __restrict__ jd
 
 // sort each value's (short) step list, then trace the chosen positions
 __global__ void k_rnd_sort_lists(const ReqCounters* rc, const int64_t* __restrict__ off, int32_t* lst) {
+  pdl_wait();
   const int64_t R = rc->R;
   OB_GRID_STRIDE(v, R) {
     const int64_t a = off[v], b = off[v + 1];
@@ -1341,6 +1353,7 @@ __global__ void k_rnd_sort_lists(const ReqCounters* rc, const int64_t* __restric
 
 __global__ void k_rnd_trace(ReqCounters* rc, const int32_t* __restrict__ jd, const int64_t* __restrict__ off,
                             const int32_t* __restrict__ lst, uint64_t* key) {
+  pdl_wait();
   const int64_t R = rc->R, budget = rc->budget;
   if (budget <= 0 || budget >= R) return;  // SelLoad takes none / all
   OB_GRID_STRIDE(p, budget) {
@@ -1411,28 +1424,24 @@ static void select_random(Engine& e, RequestWs& w, int64_t r_max) {
   OB_CUDA(cudaMemsetAsync(w.cand_key, 0, sizeof(uint64_t) * std::max<int64_t>(r_max, 1), s));
   OB_CUDA(cudaMemsetAsync(w.rnd_cnt, 0, sizeof(int32_t) * (r_max + 1), s));
   OB_CUDA(cudaMemsetAsync(w.rnd_fill, 0, sizeof(int32_t) * (r_max + 1), s));
-  k_rnd_raw<<<grid_for(rnd_raw_len(r_max) / 2, kRndChunk * 128, kNumSMs * 4), 128, 0, s>>>(g, w.rc, w.rnd_raw);
+  launch_pdl(k_rnd_raw, dim3(grid_for(rnd_raw_len(r_max) / 2, kRndChunk * 128, kNumSMs * 4)), dim3(128), 0, s, g, w.rc, w.rnd_raw);
   // draws -> steps: the chunk maps + one walk + re-emission (large |R|); the one-warp walk
   // over the whole stream below kRndSmall candidates (a few chunks are not worth three launches)
   const int64_t chunks = (rnd_raw_len(r_max) + kRndW - 1) / kRndW;
   if (r_max > 8192) {
-    k_rnd_estimate<<<1, 32, 0, s>>>(w.rc, chunks, w.rnd_lo);
-    k_rnd_chunkmap<<<(unsigned)(chunks * (kRndK / kRndKCta)), kRndKCta, 0, s>>>(w.rnd_raw, w.rc, w.rnd_lo, w.rnd_exit);
-    k_rnd_walk<<<1, 32, 0, s>>>(w.rnd_raw, w.rc, chunks, w.rnd_lo, w.rnd_exit, w.rnd_enter);
-    k_rnd_emit<<<(unsigned)std::min<int64_t>(chunks, kNumSMs * 16), 32, 0, s>>>(w.rnd_raw, w.rc, chunks, w.rnd_enter,
+    launch_pdl(k_rnd_estimate, dim3(1), dim3(32), 0, s, w.rc, chunks, w.rnd_lo);
+    launch_pdl(k_rnd_chunkmap, dim3((unsigned)(chunks * (kRndK / kRndKCta))), dim3(kRndKCta), 0, s, w.rnd_raw, w.rc, w.rnd_lo, w.rnd_exit);
+    launch_pdl(k_rnd_walk, dim3(1), dim3(32), 0, s, w.rnd_raw, w.rc, chunks, w.rnd_lo, w.rnd_exit, w.rnd_enter);
+    launch_pdl(k_rnd_emit, dim3((unsigned)std::min<int64_t>(chunks, kNumSMs * 16)), dim3(32), 0, s, w.rnd_raw, w.rc, chunks, w.rnd_enter,
                                                                                  w.rnd_j);
-    g_launches += 4;
   } else {
-    k_rnd_draws<<<1, 32, 0, s>>>(w.rnd_raw, w.rc, w.rnd_j);
-    OB_LAUNCHED();
+    launch_pdl(k_rnd_draws, dim3(1), dim3(32), 0, s, w.rnd_raw, w.rc, w.rnd_j);
   }
-  k_rnd_count<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_j, w.rnd_cnt);
-  OB_LAUNCHED();
+  launch_pdl(k_rnd_count, dim3(grid_for(r_max, 256)), dim3(256), 0, s, w.rc, w.rnd_j, w.rnd_cnt);
   device_scan(s, e.scan, LoadI32{w.rnd_cnt}, StoreI64{w.rnd_off}, nullptr, r_max + 1, r_max + 1, nullptr);
-  k_rnd_fill<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_j, w.rnd_off, w.rnd_fill, w.rnd_lst);
-  k_rnd_sort_lists<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_off, w.rnd_lst);
-  k_rnd_trace<<<grid_for(r_max, 256), 256, 0, s>>>(w.rc, w.rnd_j, w.rnd_off, w.rnd_lst, w.cand_key);
-  g_launches += 3;
+  launch_pdl(k_rnd_fill, dim3(grid_for(r_max, 256)), dim3(256), 0, s, w.rc, w.rnd_j, w.rnd_off, w.rnd_fill, w.rnd_lst);
+  launch_pdl(k_rnd_sort_lists, dim3(grid_for(r_max, 256)), dim3(256), 0, s, w.rc, w.rnd_off, w.rnd_lst);
+  launch_pdl(k_rnd_trace, dim3(grid_for(r_max, 256)), dim3(256), 0, s, w.rc, w.rnd_j, w.rnd_off, w.rnd_lst, w.cand_key);
 }
 
 // Request CSR over an edge set (the whole request via the parameter block when
@@ -1445,16 +1454,14 @@ void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound
   const RqKeyFmt f = rq_key_fmt(e, w);
   if (!edges) m_dev = &w.rp->m;  // the whole request: its edge count lives in the parameter block
   if (!counts_ready) {
-    k_zero_slots<<<grid_for(rb_max, 256), 256, 0, s>>>(w.rc, w.B, c.cnt, c.fill);
-    OB_LAUNCHED();
+    launch_pdl(k_zero_slots, dim3(grid_for(rb_max, 256)), dim3(256), 0, s, w.rc, w.B, c.cnt, c.fill);
     if (m_bound > 0) {
       if (f.wide())
-        k_rq_count_all<uint64_t><<<grid_for(m_bound, 256), 256, 0, s>>>(edges, m_dev, e.g.N, w.cbits, w.cwpre, w.rc,
+        launch_pdl(k_rq_count_all<uint64_t>, dim3(grid_for(m_bound, 256)), dim3(256), 0, s, edges, m_dev, e.g.N, w.cbits, w.cwpre, w.rc,
                                                                           c.cnt, c.keys, f);
       else
-        k_rq_count_all<uint32_t><<<grid_for(m_bound, 256), 256, 0, s>>>(
+        launch_pdl(k_rq_count_all<uint32_t>, dim3(grid_for(m_bound, 256)), dim3(256), 0, s, 
             edges, m_dev, e.g.N, w.cbits, w.cwpre, w.rc, c.cnt, reinterpret_cast<uint32_t*>(c.keys), f);
-      OB_LAUNCHED();
     }
   }
   device_scan(s, e.scan, LoadI32{c.cnt}, StoreI64{c.ptr}, &w.rc->RB, 0, rb_max, nullptr, c.ptr);
