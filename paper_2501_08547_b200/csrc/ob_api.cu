@@ -386,6 +386,7 @@ static int64_t bucket_m(int64_t m) {
 }
 
 __global__ void k_set_params(ReqParams* p, const int64_t* edges, const float* q, int64_t m, int64_t B) {
+  pdl_wait();
   p->edges = edges;
   p->qfeat = q;
   p->m = m;
@@ -550,8 +551,7 @@ static void enqueue_serve(Engine& e, int B, const float* d_q, int64_t m, const i
   w.edges = d_edges;
   w.qfeat = d_q;
   // kernel arguments are copied at launch: the block is stream-ordered with no host staging
-  k_set_params<<<1, 1, 0, s>>>(e.params, d_edges, d_q, m, B);
-  OB_LAUNCHED();
+  launch_pdl(k_set_params, dim3(1), dim3(1), 0, s, e.params, d_edges, d_q, m, B);
   OB_CUDA(cudaEventRecord(e.ev[0], s));
   if (e.prof.on || !e.use_graphs) {
     g_prof = e.prof.on ? &e.prof : nullptr;
@@ -755,6 +755,7 @@ static void load_model(Engine& e, int k, const ob_layer* layers, const float* co
 // ---------------------------------------------------------------------------
 __global__ void k_src_degree(const int32_t* __restrict__ src_ids, const BlockCounters* cnt, int64_t N,
                              const int32_t* indeg, const int32_t* qdeg, int64_t* out) {
+  pdl_wait();
   const int64_t S = cnt->S;
   OB_GRID_STRIDE(s, S) {
     int64_t g = src_ids[s];
@@ -853,6 +854,7 @@ static void ensure(T*& p, size_t& cap, size_t n) {
 // int32 (src, dst) request edges -> the int64 pairs the pipeline reads (8 host bytes
 // per edge over PCIe instead of 16)
 __global__ void k_widen_edges(const int32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+  pdl_wait();
   const int64_t n4 = n / 4;
   OB_GRID_STRIDE(i, n4) {
     const int4 v = __ldg(reinterpret_cast<const int4*>(in) + i);
@@ -877,8 +879,7 @@ static void stage_edges(const T* src, int64_t m, int64_t*& d64, size_t& cap64, i
 template <class T>
 static void widen_edges(int64_t m, int64_t* d64, const int32_t* d32, cudaStream_t s) {
   if (sizeof(T) == 8 || !m) return;
-  k_widen_edges<<<grid_for(m / 2 + 1, 256), 256, 0, s>>>(d32, 2 * m, d64);
-  OB_LAUNCHED();
+  launch_pdl(k_widen_edges, dim3(grid_for(m / 2 + 1, 256)), dim3(256), 0, s, d32, 2 * m, d64);
 }
 
 extern "C" {
@@ -1500,9 +1501,8 @@ int ob_last_block(ob_engine* h, int32_t part, int32_t layer, int64_t* src_ids, i
       OB_CUDA(cudaMalloc(&dp, sizeof(int32_t) * std::max<int64_t>(c.S, 1)));
       OB_CUDA(cudaMalloc(&dd, sizeof(int64_t) * std::max<int64_t>(c.S, 1)));
       export_bindings(e, w, b, layer, dk, dp);
-      k_src_degree<<<grid_for(std::max<int64_t>(c.S, 1), 256), 256, 0, s>>>(b.src_ids, b.cnt, e.g.N, e.g.indeg,
+      launch_pdl(k_src_degree, dim3(grid_for(std::max<int64_t>(c.S, 1), 256)), dim3(256), 0, s, b.src_ids, b.cnt, e.g.N, e.g.indeg,
                                                                              w.qdeg, dd);
-      OB_LAUNCHED();
       auto k1 = d2h(dk, c.S, s);
       auto k2 = d2h(dp, c.S, s);
       auto k3 = d2h(dd, c.S, s);

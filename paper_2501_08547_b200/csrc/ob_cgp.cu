@@ -43,7 +43,8 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
   return z ^ (z >> 31);
 }
 
-__global__ void k_owner(int64_t N, int P, uint64_t seed, int32_t* owner) {  // declared in ob_engine.h
+__global__ void k_owner(int64_t N, int P, uint64_t seed, int32_t* owner) {
+  pdl_wait();  // declared in ob_engine.h
   const uint64_t key = mix64(seed);
   OB_GRID_STRIDE(v, N) owner[v] = (int32_t)(mix64((uint64_t)v ^ key) % (uint64_t)P);
 }
@@ -51,6 +52,7 @@ __global__ void k_owner(int64_t N, int P, uint64_t seed, int32_t* owner) {  // d
 // per destination row: number of in-neighbours owned by partition r (warp per row)
 __global__ void k_part_deg(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
                            const int32_t* __restrict__ owner, int r, int32_t* deg) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -66,6 +68,7 @@ __global__ void k_part_deg(int64_t N, const int64_t* __restrict__ off, const int
 __global__ void k_part_fill(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
                             const int32_t* __restrict__ owner, int r, const int64_t* __restrict__ poff,
                             int32_t* psrc) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -89,8 +92,7 @@ void cgp_build_partitions(Engine& e) {
   c.nccl = e.cfg.nccl_id != nullptr;
   c.my_rank = c.nccl ? e.cfg.rank : 0;
   c.owner = (int32_t*)e.dalloc(sizeof(int32_t) * N);
-  k_owner<<<grid_for(N, 256), 256, 0, s>>>(N, c.P, e.cfg.seed, c.owner);
-  OB_LAUNCHED();
+  launch_pdl(k_owner, dim3(grid_for(N, 256)), dim3(256), 0, s, N, c.P, e.cfg.seed, c.owner);
   ScanScratch sc;
   sc.cap = ScanScratch::bytes_for(N, c.P);
   sc.pool = (char*)e.dalloc(sc.cap);
@@ -103,27 +105,28 @@ void cgp_build_partitions(Engine& e) {
     p.rank = r;
     p.deg = (int32_t*)e.dalloc(sizeof(int32_t) * N);
     p.off = (int64_t*)e.dalloc(sizeof(int64_t) * (N + 1));
-    k_part_deg<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, c.owner, r, p.deg);
-    OB_LAUNCHED();
+    launch_pdl(k_part_deg, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, N, e.g.offsets, e.g.nbrs, c.owner, r, p.deg);
     device_scan(s, sc, LoadI32{p.deg}, StoreI64{p.off}, nullptr, N, N, total, p.off);
     OB_CUDA(cudaMemcpyAsync(&p.E, total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     OB_CUDA(cudaStreamSynchronize(s));
     p.src = (int32_t*)e.dalloc(sizeof(int32_t) * std::max<int64_t>(p.E, 1));
-    k_part_fill<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, c.owner, r, p.off, p.src);
-    OB_LAUNCHED();
+    launch_pdl(k_part_fill, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, N, e.g.offsets, e.g.nbrs, c.owner, r, p.off, p.src);
     c.parts.push_back(p);
   }
   OB_CUDA(cudaStreamSynchronize(s));
 }
 
 __global__ void k_flag_owned(int64_t N, const int32_t* owner, int rank, int32_t* flag) {
+  pdl_wait();
   OB_GRID_STRIDE(v, N) flag[v] = owner[v] == rank;
 }
 __global__ void k_pos_owned(int64_t N, const int32_t* owner, int rank, const int64_t* excl, int32_t* pos) {
+  pdl_wait();
   OB_GRID_STRIDE(v, N) pos[v] = owner[v] == rank ? (int32_t)excl[v] : -1;
 }
 __global__ void k_gather_owned(int64_t N, int64_t ld, const int32_t* __restrict__ pos, const float* __restrict__ full,
                                float* local) {
+  pdl_wait();
   const int64_t n = N * ld;
   OB_GRID_STRIDE(i, n) {
     const int64_t v = i / ld;
@@ -143,11 +146,10 @@ void owned_positions(Engine& e) {
   sc.cap = ScanScratch::bytes_for(N, 1);
   sc.pool = (char*)e.dalloc(sc.cap);
   OB_CUDA(cudaMemsetAsync(sc.pool, 0, sc.cap, s));
-  k_flag_owned<<<grid_for(N, 256), 256, 0, s>>>(N, c.owner, c.my_rank, flag);
+  launch_pdl(k_flag_owned, dim3(grid_for(N, 256)), dim3(256), 0, s, N, c.owner, c.my_rank, flag);
   device_scan(s, sc, LoadI32{flag}, StoreI64{excl}, nullptr, N, N, nullptr, excl);
   e.g.pos = (int32_t*)e.dalloc(sizeof(int32_t) * N);
-  k_pos_owned<<<grid_for(N, 256), 256, 0, s>>>(N, c.owner, c.my_rank, excl, e.g.pos);
-  g_launches += 2;
+  launch_pdl(k_pos_owned, dim3(grid_for(N, 256)), dim3(256), 0, s, N, c.owner, c.my_rank, excl, e.g.pos);
   OB_CUDA(cudaMemcpyAsync(&e.g.N_local, excl + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   OB_CUDA(cudaStreamSynchronize(s));
   e.dfree(flag);
@@ -161,8 +163,7 @@ void localize_table(Engine& e, float*& table, int64_t ld) {
   cudaStream_t s = e.stream;
   const int64_t N = e.g.N;
   float* local = (float*)e.dalloc(sizeof(float) * std::max<int64_t>(e.g.N_local, 1) * ld);
-  k_gather_owned<<<grid_for(N * ld, 256), 256, 0, s>>>(N, ld, e.g.pos, table, local);
-  OB_LAUNCHED();
+  launch_pdl(k_gather_owned, dim3(grid_for(N * ld, 256)), dim3(256), 0, s, N, ld, e.g.pos, table, local);
   OB_CUDA(cudaStreamSynchronize(s));
   e.dfree(table);
   table = local;
@@ -194,6 +195,7 @@ void cgp_localize_storage(Engine& e) {
 // request slice of partition r: edges whose source it owns (queries: round robin)
 __global__ void k_filter_slice(const ReqParams* rp, int64_t N, int P, int r, const int32_t* __restrict__ owner,
                                const ReqCounters* rc, int64_t* out, int64_t* count) {
+  pdl_wait();
   if (rc->err & (kErrRange | kErrNoQuery)) return;
   const int64_t* __restrict__ edges = rp->edges;
   const int64_t m = rp->m;
@@ -222,6 +224,7 @@ __global__ void k_dst_rows(const int32_t* __restrict__ dst_ids, const int64_t* D
                            const float* prev, int64_t in_ld,
                            const int64_t* T_dev, const int32_t* owner, int P, int rank, const float* zero,
                            const float** hvp) {
+  pdl_wait();
   const int64_t D = *D_dev, T = *T_dev;
   OB_GRID_STRIDE(i, D) {
     const int64_t g = dst_ids[i];
@@ -238,6 +241,7 @@ __global__ void k_dst_rows(const int32_t* __restrict__ dst_ids, const int64_t* D
 
 __global__ void k_rowdot_ptr(const int64_t* M_dev, const float* const* rows, int w, const float* __restrict__ av,
                              float* out) {
+  pdl_wait();
   const int64_t M = *M_dev;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -254,10 +258,12 @@ __global__ void k_rowdot_ptr(const int64_t* M_dev, const float* const* rows, int
 // softmax exchange: pull the max-logit column out, then rescale (den, num) to the
 // global max so the triples can be summed (cgpexec.py:225-239)
 __global__ void k_sm_extract(const int64_t* D_dev, const float* lp, int64_t ldp, float* lmax) {
+  pdl_wait();
   const int64_t D = *D_dev;
   OB_GRID_STRIDE(i, D) lmax[i] = lp[i * ldp + 1] > 0.f ? lp[i * ldp] : -INFINITY;
 }
 __global__ void k_sm_rescale(const int64_t* D_dev, float* lp, int64_t ldp, int w, const float* gmax) {
+  pdl_wait();
   const int64_t D = *D_dev;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -275,12 +281,14 @@ __global__ void k_sm_rescale(const int64_t* D_dev, float* lp, int64_t ldp, int w
   }
 }
 __global__ void k_sm_restore(const int64_t* D_dev, float* lp, int64_t ldp, const float* gmax) {
+  pdl_wait();
   const int64_t D = *D_dev;
   OB_GRID_STRIDE(i, D) lp[i * ldp] = gmax[i];
 }
 
 // final rows: zero the queries this rank does not own before the reduce to rank 0
 __global__ void k_zero_foreign_queries(float* rows, int B, int H, int P, int rank) {
+  pdl_wait();
   const int64_t n = (int64_t)B * H;
   OB_GRID_STRIDE(i, n) if ((int)((i / H) % P) != rank) rows[i] = 0.f;
 }
@@ -423,7 +431,8 @@ __device__ __forceinline__ void spin_geq(const XCtx& x, const int64_t* f, int64_
   }
 }
 
-__global__ void k_x_begin(XCtx x) {  // peers done with the previous step
+__global__ void k_x_begin(XCtx x) {
+  pdl_wait();  // peers done with the previous step
   const int q = threadIdx.x;
   if (q >= x.P || q == x.rank) return;
   if (x_failed(x)) {
@@ -434,6 +443,7 @@ __global__ void k_x_begin(XCtx x) {  // peers done with the previous step
   if (k > 0) spin_geq(x, reinterpret_cast<const int64_t*>(x.peer[x.rank] + 64) + q, k);
 }
 __global__ void k_x_publish(XCtx x) {
+  pdl_wait();
   __threadfence_system();
   const int64_t k = *x.ep + 1;
   __syncthreads();
@@ -442,6 +452,7 @@ __global__ void k_x_publish(XCtx x) {
   if (q < x.P && q != x.rank) st_rel_sys(reinterpret_cast<int64_t*>(x.peer[q]) + x.rank, k);
 }
 __global__ void k_x_wait(XCtx x) {
+  pdl_wait();
   const int p = threadIdx.x;
   if (p >= x.P || p == x.rank) return;
   if (x_failed(x)) {
@@ -451,6 +462,7 @@ __global__ void k_x_wait(XCtx x) {
   spin_geq(x, reinterpret_cast<const int64_t*>(x.peer[x.rank]) + p, *x.ep);
 }
 __global__ void k_x_done(XCtx x) {
+  pdl_wait();
   const int q = threadIdx.x;
   if (q < x.P && q != x.rank)
     st_rel_sys(reinterpret_cast<int64_t*>(x.peer[q] + 64) + x.rank, *x.ep);
@@ -459,6 +471,7 @@ __global__ void k_x_done(XCtx x) {
 // rows[i] of destination i from its owner's copy (s_dst, moments means, final rows)
 __global__ void k_x_gather_rows(XCtx x, size_t off, const int32_t* dst_ids, const int64_t* D_dev, int64_t D_fixed,
                                 int64_t N, const int32_t* owner, int esize, int64_t width_el, float* out) {
+  pdl_wait();
   const int64_t D = D_dev ? *D_dev : D_fixed;
   const int64_t words = width_el * esize / 4;  // 4-byte words per row
   const int64_t n = D * words;
@@ -484,8 +497,7 @@ static XCtx xctx(Engine& e) {
   return x;
 }
 static void x_launch(cudaStream_t s, void (*kern)(XCtx), const XCtx& x) {
-  kern<<<1, 32, 0, s>>>(x);
-  OB_LAUNCHED();
+  launch_pdl(kern, dim3(1), dim3(32), 0, s, x);
 }
 
 // offset (from the region base past the flags) of step j's region
@@ -556,9 +568,8 @@ void serve_cgp(Engine& e, float* d_out) {
         OB_CUDA(cudaMemsetAsync(pw.blocks[0].cnt, 0, sizeof(BlockCounters), side));
         OB_CUDA(cudaMemsetAsync(pw.blocks[1].cnt, 0, sizeof(BlockCounters), side));
         if (w.m > 0) {
-          k_filter_slice<<<grid_for(w.m, 256), 256, 0, side>>>(w.rp, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
+          launch_pdl(k_filter_slice, dim3(grid_for(w.m, 256)), dim3(256), 0, side, w.rp, N, c.P, part.rank, c.owner, w.rc, pw.ledges,
                                                                   pw.rq.ctr);
-          OB_LAUNCHED();
         }
         build_rq_csr(e, w, pw.ledges, w.m, pw.rq.ctr, pw.rq, /*counts_ready=*/false);
         const SpanSrc src{part.off, part.src, part.deg, pw.rq.ptr, pw.rq.src};
@@ -636,24 +647,20 @@ void serve_cgp(Engine& e, float* d_out) {
     BindCtx bc = bind_ctx(e, w, l);
     own.dst_ids = b0.dst_ids;
     // destination rows h_v (owned ones; zero row elsewhere under NCCL)
-    k_dst_rows<<<grid_for(D_max, 256), 256, 0, s>>>(b0.dst_ids, D_dev, N, l, k, e.g.pos, e.g.feats, w.qpad, e.g.F_ld,
+    launch_pdl(k_dst_rows, dim3(grid_for(D_max, 256)), dim3(256), 0, s, b0.dst_ids, D_dev, N, l, k, e.g.pos, e.g.feats, w.qpad, e.g.F_ld,
                                                     l > 1 ? w.outs[l - 1] : nullptr, ld4(L.spec.in_dim), &w.rc->T,
                                                     c.nccl ? c.owner : nullptr, c.P, c.my_rank, c.zero_row, c.hvp);
-    OB_LAUNCHED();
     if (L.spec.kind == OB_KIND_GAT) {  // s_dst = h_v . (W a_dst), computed by the owner
       if (p2p) {
         x_begin();
         float* reg = reinterpret_cast<float*>(xregion_ptr(c, xj));
-        k_rowdot_ptr<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.hvp, L.spec.in_dim, L.wa_dst, reg);
-        OB_LAUNCHED();
+        launch_pdl(k_rowdot_ptr, dim3(grid_for(D_max, 8)), dim3(256), 0, s, D_dev, c.hvp, L.spec.in_dim, L.wa_dst, reg);
         x_exchange();
-        k_x_gather_rows<<<grid_for(D_max, 256), 256, 0, s>>>(x, xoff(c, xj), b0.dst_ids, D_dev, 0, N, c.owner, 4, 1,
+        launch_pdl(k_x_gather_rows, dim3(grid_for(D_max, 256)), dim3(256), 0, s, x, xoff(c, xj), b0.dst_ids, D_dev, 0, N, c.owner, 4, 1,
                                                              c.sdst);
-        OB_LAUNCHED();
         x_done();
       } else {
-        k_rowdot_ptr<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.hvp, L.spec.in_dim, L.wa_dst, c.sdst);
-        OB_LAUNCHED();
+        launch_pdl(k_rowdot_ptr, dim3(grid_for(D_max, 8)), dim3(256), 0, s, D_dev, c.hvp, L.spec.in_dim, L.wa_dst, c.sdst);
         if (c.nccl) allreduce(e, c.sdst, D_max, false, false);
       }
     }
@@ -731,14 +738,11 @@ void serve_cgp(Engine& e, float* d_out) {
         if (c.nccl) {
           const int64_t pw = cgp_partial_width(L);
           if (L.spec.kind == OB_KIND_GAT) {
-            k_sm_extract<<<grid_for(D_max, 256), 256, 0, s>>>(D_dev, c.lp, c.ldp, c.lmax);
-            OB_LAUNCHED();
+            launch_pdl(k_sm_extract, dim3(grid_for(D_max, 256)), dim3(256), 0, s, D_dev, c.lp, c.ldp, c.lmax);
             allreduce(e, c.lmax, D_max, false, true);
-            k_sm_rescale<<<grid_for(D_max, 8), 256, 0, s>>>(D_dev, c.lp, c.ldp, (int)pw - 2, c.lmax);
-            OB_LAUNCHED();
+            launch_pdl(k_sm_rescale, dim3(grid_for(D_max, 8)), dim3(256), 0, s, D_dev, c.lp, c.ldp, (int)pw - 2, c.lmax);
             allreduce(e, c.lp, D_max * c.ldp, false, false);
-            k_sm_restore<<<grid_for(D_max, 256), 256, 0, s>>>(D_dev, c.lp, c.ldp, c.lmax);
-            OB_LAUNCHED();
+            launch_pdl(k_sm_restore, dim3(grid_for(D_max, 256)), dim3(256), 0, s, D_dev, c.lp, c.ldp, c.lmax);
           } else if (L.spec.kind == OB_KIND_SAGE_MAX) {
             allreduce(e, c.lp, D_max * c.ldp, false, true);  // empty partials hold -inf
           } else {
@@ -762,9 +766,8 @@ void serve_cgp(Engine& e, float* d_out) {
         const int64_t mw = L.spec.in_dim;  // mean rows are in_dim float64 wide (k_merge_moments)
         OB_CUDA(cudaMemcpyAsync(xregion_ptr(c, xj), c.mean, sizeof(double) * D_max * mw, cudaMemcpyDeviceToDevice, s));
         x_exchange();
-        k_x_gather_rows<<<grid_for(D_max * mw * 2, 256), 256, 0, s>>>(x, xoff(c, xj), b0.dst_ids, D_dev, 0, N, c.owner,
+        launch_pdl(k_x_gather_rows, dim3(grid_for(D_max * mw * 2, 256)), dim3(256), 0, s, x, xoff(c, xj), b0.dst_ids, D_dev, 0, N, c.owner,
                                                                       8, mw, reinterpret_cast<float*>(c.mean));
-        OB_LAUNCHED();
         x_done();
       }
       if (ph == phases) cgp_update(s, L, D_dev, D_max, c.hvp, w.agg, out, ldo);
@@ -777,15 +780,13 @@ void serve_cgp(Engine& e, float* d_out) {
     OB_CUDA(cudaMemcpyAsync(xregion_ptr(c, xj), c.fin, sizeof(float) * w.B * H, cudaMemcpyDeviceToDevice, s));
     x_exchange();
     if (c.my_rank == 0) {
-      k_x_gather_rows<<<grid_for((int64_t)w.B * H, 256), 256, 0, s>>>(x, xoff(c, xj), nullptr, nullptr, w.B, N,
+      launch_pdl(k_x_gather_rows, dim3(grid_for((int64_t)w.B * H, 256)), dim3(256), 0, s, x, xoff(c, xj), nullptr, nullptr, w.B, N,
                                                                       c.owner, 4, H, d_out);
-      OB_LAUNCHED();
     }
     x_done();
   } else if (c.nccl) {
     const int H = e.layers.back().spec.out_dim;
-    k_zero_foreign_queries<<<grid_for((int64_t)w.B * H, 256), 256, 0, s>>>(c.fin, w.B, H, c.P, c.my_rank);
-    OB_LAUNCHED();
+    launch_pdl(k_zero_foreign_queries, dim3(grid_for((int64_t)w.B * H, 256)), dim3(256), 0, s, c.fin, w.B, H, c.P, c.my_rank);
     OB_NCCL(ncclReduce(c.fin, d_out, (size_t)w.B * H, ncclFloat, ncclSum, 0, (ncclComm_t)c.comm, s));
     c.collective_bytes += (int64_t)w.B * H * 4;
   }

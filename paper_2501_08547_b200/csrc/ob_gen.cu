@@ -55,17 +55,20 @@ __device__ __forceinline__ int64_t gen_src(const GenLaw& L, int64_t v, int64_t j
 }
 
 __global__ void k_zipf_norm(GenLaw L, double* acc) {
+  pdl_wait();
   double s = 0.0;
   OB_GRID_STRIDE(r, L.N) s += pow((double)(r + 1), -L.s);
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(acc, s);
 }
 
-__global__ void k_gen_indeg(GenLaw L, int32_t* indeg) { OB_GRID_STRIDE(v, L.N) indeg[v] = gen_indeg(L, v); }
+__global__ void k_gen_indeg(GenLaw L, int32_t* indeg) {
+  pdl_wait(); OB_GRID_STRIDE(v, L.N) indeg[v] = gen_indeg(L, v); }
 
 // owned in-neighbours per destination row (owner == nullptr: all); warp per row
 __global__ void k_gen_count(GenLaw L, const int32_t* __restrict__ indeg, const int32_t* __restrict__ owner, int rank,
                             int32_t* cnt) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -83,6 +86,7 @@ __global__ void k_gen_count(GenLaw L, const int32_t* __restrict__ indeg, const i
 
 __global__ void k_gen_fill(GenLaw L, const int32_t* __restrict__ indeg, const int32_t* __restrict__ owner, int rank,
                            const int64_t* __restrict__ off, int32_t* src) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -106,6 +110,7 @@ __global__ void k_gen_fill(GenLaw L, const int32_t* __restrict__ indeg, const in
 
 // N(0, 1) rows for the stored nodes (global id -> local row via pos)
 __global__ void k_gen_rows(int64_t N, int F, int ld, uint64_t seed, const int32_t* pos, float* rows) {
+  pdl_wait();
   const int64_t n = N * (int64_t)ld;
   OB_GRID_STRIDE(i, n) {
     const int64_t v = i / ld;
@@ -148,8 +153,7 @@ GenLaw make_law(int64_t N, double avg, double exponent, uint64_t seed, cudaStrea
   L.a = a;
   L.b = (seed * 0xBF58476D1CE4E5B9ull) % (uint64_t)N;
   OB_CUDA(cudaMemsetAsync(d_acc, 0, sizeof(double), s));
-  k_zipf_norm<<<kNumSMs * 8, 256, 0, s>>>(L, d_acc);
-  OB_LAUNCHED();
+  launch_pdl(k_zipf_norm, dim3(kNumSMs * 8), dim3(256), 0, s, L, d_acc);
   OB_CUDA(cudaMemcpyAsync(&L.H, d_acc, sizeof(double), cudaMemcpyDeviceToHost, s));
   OB_CUDA(cudaStreamSynchronize(s));
   return L;
@@ -160,6 +164,7 @@ GenLaw make_law(int64_t N, double avg, double exponent, uint64_t seed, cudaStrea
 namespace ob {
 
 __global__ void k_sum_i32(const int32_t* a, int64_t n, unsigned long long* out) {
+  pdl_wait();
   unsigned long long s = 0;
   OB_GRID_STRIDE(i, n) s += (unsigned long long)a[i];
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -194,13 +199,11 @@ void generate_graph(Engine& e, int64_t N, double avg, double exponent, int F, ui
   g.F_ld = ld4(F);
   g.generated = true;
   g.indeg = (int32_t*)e.dalloc(sizeof(int32_t) * N);
-  k_gen_indeg<<<grid_for(N, 256), 256, 0, s>>>(L, g.indeg);
-  OB_LAUNCHED();
+  launch_pdl(k_gen_indeg, dim3(grid_for(N, 256)), dim3(256), 0, s, L, g.indeg);
   {
     unsigned long long* tot = reinterpret_cast<unsigned long long*>(acc + 1);
     OB_CUDA(cudaMemsetAsync(tot, 0, sizeof(*tot), s));
-    k_sum_i32<<<kNumSMs * 8, 256, 0, s>>>(g.indeg, N, tot);
-    OB_LAUNCHED();
+    launch_pdl(k_sum_i32, dim3(kNumSMs * 8), dim3(256), 0, s, g.indeg, N, tot);
     unsigned long long h = 0;
     OB_CUDA(cudaMemcpyAsync(&h, tot, sizeof(h), cudaMemcpyDeviceToHost, s));
     OB_CUDA(cudaStreamSynchronize(s));
@@ -219,25 +222,21 @@ void generate_graph(Engine& e, int64_t N, double avg, double exponent, int F, ui
     c.nccl = true;
     c.my_rank = e.cfg.rank;
     c.owner = (int32_t*)e.dalloc(sizeof(int32_t) * N);
-    k_owner<<<grid_for(N, 256), 256, 0, s>>>(N, c.P, e.cfg.seed, c.owner);
-    OB_LAUNCHED();
+    launch_pdl(k_owner, dim3(grid_for(N, 256)), dim3(256), 0, s, N, c.P, e.cfg.seed, c.owner);
     owned_positions(e);  // pos map + N_local
     g.feats = (float*)e.dalloc(sizeof(float) * std::max<int64_t>(g.N_local, 1) * g.F_ld);
-    k_gen_rows<<<grid_for(N * g.F_ld, 256), 256, 0, s>>>(N, F, g.F_ld, fseed, g.pos, g.feats);
-    OB_LAUNCHED();
+    launch_pdl(k_gen_rows, dim3(grid_for(N * g.F_ld, 256)), dim3(256), 0, s, N, F, g.F_ld, fseed, g.pos, g.feats);
     // this rank's source-split CSR, rows ascending
     PartitionDev p;
     p.rank = c.my_rank;
     p.deg = (int32_t*)e.dalloc(sizeof(int32_t) * N);
     p.off = (int64_t*)e.dalloc(sizeof(int64_t) * (N + 1));
-    k_gen_count<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(L, g.indeg, c.owner, c.my_rank, p.deg);
-    OB_LAUNCHED();
+    launch_pdl(k_gen_count, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, L, g.indeg, c.owner, c.my_rank, p.deg);
     device_scan(s, sc, LoadI32{p.deg}, StoreI64{p.off}, nullptr, N, N, total, p.off);
     OB_CUDA(cudaMemcpyAsync(&p.E, total, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     OB_CUDA(cudaStreamSynchronize(s));
     p.src = (int32_t*)e.dalloc(sizeof(int32_t) * std::max<int64_t>(p.E, 1));
-    k_gen_fill<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(L, g.indeg, c.owner, c.my_rank, p.off, p.src);
-    OB_LAUNCHED();
+    launch_pdl(k_gen_fill, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, L, g.indeg, c.owner, c.my_rank, p.off, p.src);
     c.parts.clear();
     c.parts.push_back(p);
     e.localized = true;
@@ -245,11 +244,9 @@ void generate_graph(Engine& e, int64_t N, double avg, double exponent, int F, ui
     g.offsets = (int64_t*)e.dalloc(sizeof(int64_t) * (N + 1));
     device_scan(s, sc, LoadI32{g.indeg}, StoreI64{g.offsets}, nullptr, N, N, total, g.offsets);
     g.nbrs = (int32_t*)e.dalloc(sizeof(int32_t) * std::max<int64_t>(g.E, 1));
-    k_gen_fill<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(L, g.indeg, nullptr, 0, g.offsets, g.nbrs);
-    OB_LAUNCHED();
+    launch_pdl(k_gen_fill, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, L, g.indeg, nullptr, 0, g.offsets, g.nbrs);
     g.feats = (float*)e.dalloc(sizeof(float) * N * g.F_ld);
-    k_gen_rows<<<grid_for(N * g.F_ld, 256), 256, 0, s>>>(N, F, g.F_ld, fseed, nullptr, g.feats);
-    OB_LAUNCHED();
+    launch_pdl(k_gen_rows, dim3(grid_for(N * g.F_ld, 256)), dim3(256), 0, s, N, F, g.F_ld, fseed, nullptr, g.feats);
     g.N_local = N;
   }
   OB_CUDA(cudaStreamSynchronize(s));
@@ -274,9 +271,8 @@ void generate_pe(Engine& e, int layer, int dim, uint64_t seed) {
   const int64_t rows = e.g.pos ? std::max<int64_t>(e.g.N_local, 1) : e.g.N;
   e.dfree(e.pe[layer - 1]);
   float* d = (float*)e.dalloc(sizeof(float) * rows * ld);
-  k_gen_rows<<<grid_for(e.g.N * ld, 256), 256, 0, e.stream>>>(e.g.N, dim, ld, seed * 0x9E3779B97F4A7C15ull + layer,
+  launch_pdl(k_gen_rows, dim3(grid_for(e.g.N * ld, 256)), dim3(256), 0, e.stream, e.g.N, dim, ld, seed * 0x9E3779B97F4A7C15ull + layer,
                                                               e.g.pos, d);
-  OB_LAUNCHED();
   OB_CUDA(cudaStreamSynchronize(e.stream));
   e.pe[layer - 1] = d;
   e.pe_dim[layer - 1] = dim;

@@ -394,6 +394,7 @@ template <int OP, int NV>
 #define OB_AGG_MINB_WIDE 1  // k_agg CTAs per SM for rows wider than 128 columns (NV = 2, 4)
 #endif
 __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WIDE)) k_agg(AggArgs a) {
+  pdl_wait();
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   pdl_wait();
@@ -568,6 +569,7 @@ __global__ void __launch_bounds__(256, OB_FIN_MINB) k_finalize(FinArgs a) {
 __global__ void __launch_bounds__(256) k_finalize_moments(const BlockCounters* cnt_, const int64_t* dst_ptr,
                                                           const int64_t* item_ptr, const double* partial, int width,
                                                           int phase, int n, double* mean, float* agg, int64_t ldo) {
+  pdl_wait();
   const int64_t D = cnt_->D;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -592,6 +594,7 @@ __global__ void __launch_bounds__(256) k_finalize_moments(const BlockCounters* c
 // out[r] = z_row(self[r] or r) . av  (GAT source / destination scores)
 __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* self, int w,
                               const float* __restrict__ av, float* out) {
+  pdl_wait();
   const int64_t M = *M_dev;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -781,9 +784,8 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   }
   if (sp.kind == OB_KIND_GAT) {
     const RowSrc z = r.yrow ? RowSrc{r.yrow, nullptr, 0} : RowSrc{nullptr, sc.z, ld_out};
-    k_rowdot_rows<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, z, nullptr, outd, L.a_src, sc.s_src);
-    k_rowdot_rows<<<grid_for(r.D_max, 8), 256, 0, s>>>(r.D_dev, z, r.self, outd, L.a_dst, sc.s_dst);
-    g_launches += 2;
+    launch_pdl(k_rowdot_rows, dim3(grid_for(r.S_max, 8)), dim3(256), 0, s, r.S_dev, z, nullptr, outd, L.a_src, sc.s_src);
+    launch_pdl(k_rowdot_rows, dim3(grid_for(r.D_max, 8)), dim3(256), 0, s, r.D_dev, z, r.self, outd, L.a_dst, sc.s_dst);
     a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
     a.s_dst = sc.s_dst;
@@ -855,13 +857,12 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   } else if (sp.kind == OB_KIND_MOMENTS) {
     double* mean = reinterpret_cast<double*>(sc.mean);
     launch_agg<kOpDSum>(s, a, r.items_max);
-    k_finalize_moments<<<grid_for(r.D_max, 8, kNumSMs * 16), 256, 0, s>>>(
+    launch_pdl(k_finalize_moments, dim3(grid_for(r.D_max, 8, kNumSMs * 16)), dim3(256), 0, s, 
         r.cnt, r.dst_ptr, r.item_ptr, (const double*)sc.partial, in, 1, sp.n, mean, nullptr, 0);
     a.mean = mean;
     launch_agg<kOpMom2>(s, a, r.items_max);
-    k_finalize_moments<<<grid_for(r.D_max, 8, kNumSMs * 16), 256, 0, s>>>(
+    launch_pdl(k_finalize_moments, dim3(grid_for(r.D_max, 8, kNumSMs * 16)), dim3(256), 0, s, 
         r.cnt, r.dst_ptr, r.item_ptr, (const double*)sc.partial, in, 2, sp.n, nullptr, sc.agg, ld4(in));
-    g_launches += 2;
   } else {  // sage_mean aggregate-first
     agg_fin<kOpSum>(s, a, f, r.items_max, r.D_max, split);
   }
@@ -889,6 +890,7 @@ int cgp_partial_width(const LayerDev& L) {
 // merge a destination's items (or hub groups) into one raw partial: sum / max /
 // (max logit, sum exp, sum exp*z); count = local in-edges
 __global__ void __launch_bounds__(256) k_local_raw(FinArgs a, float* lp, int64_t ldp, float* lcnt) {
+  pdl_wait();
   const int64_t D = a.cnt->D;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -937,6 +939,7 @@ __global__ void __launch_bounds__(256) k_local_raw(FinArgs a, float* lp, int64_t
 __global__ void __launch_bounds__(256) k_local_raw_f64(const BlockCounters* cnt_, const int64_t* dst_ptr,
                                                        const int64_t* item_ptr, const double* partial, int width,
                                                        double* lp, int64_t ldp, float* lcnt) {
+  pdl_wait();
   const int64_t D = cnt_->D;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -968,6 +971,7 @@ struct MergeArgs {
 // merge in ascending partition order (cgpexec.py:189-240): sum / mean / max / powmean /
 // softmax rescale, empty destinations aggregate to zero
 __global__ void __launch_bounds__(256) k_merge_parts(MergeArgs m) {
+  pdl_wait();
   const int64_t D = *m.D_dev;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1017,6 +1021,7 @@ __global__ void __launch_bounds__(256) k_merge_parts(MergeArgs m) {
 __global__ void __launch_bounds__(256) k_merge_moments(int P, PartPtrs parts, int64_t ldp, const int64_t* D_dev,
                                                        OwnerFilter own, int width, int phase, int n, double* mean,
                                                        float* agg, int64_t ldo) {
+  pdl_wait();
   const int64_t D = *D_dev;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1042,8 +1047,7 @@ __global__ void __launch_bounds__(256) k_merge_moments(int P, PartPtrs parts, in
 
 void launch_resolve(cudaStream_t s, const BindCtx& c, BlockCounters* cnt, int64_t S_max, const int32_t* src_ids,
                     const float** rowp, float* gscale) {
-  k_resolve<<<grid_for(S_max, 256), 256, 0, s>>>(c, cnt, src_ids, rowp, gscale, nullptr, nullptr);
-  OB_LAUNCHED();
+  launch_pdl(k_resolve, dim3(grid_for(S_max, 256)), dim3(256), 0, s, c, cnt, src_ids, rowp, gscale, nullptr, nullptr);
 }
 
 void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, const LayerScratch& sc,
@@ -1095,15 +1099,13 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
     a.mean = mean;
     if (moments_phase == 1) launch_agg<kOpDSum>(s, a, r.items_max);
     else launch_agg<kOpMom2>(s, a, r.items_max);
-    k_local_raw_f64<<<grid_for(r.D_max, 8, kNumSMs * 16), 256, 0, s>>>(r.cnt, r.dst_ptr, r.item_ptr,
+    launch_pdl(k_local_raw_f64, dim3(grid_for(r.D_max, 8, kNumSMs * 16)), dim3(256), 0, s, r.cnt, r.dst_ptr, r.item_ptr,
                                                                         (const double*)sc.partial, in, (double*)lp,
                                                                         ldp, lcnt);
-    OB_LAUNCHED();
     return;
   }
   if (sp.kind == OB_KIND_GAT) {
-    k_rowdot_rows<<<grid_for(r.S_max, 8), 256, 0, s>>>(r.S_dev, zrows, nullptr, outd, L.a_src, sc.s_src);
-    OB_LAUNCHED();
+    launch_pdl(k_rowdot_rows, dim3(grid_for(r.S_max, 8)), dim3(256), 0, s, r.S_dev, zrows, nullptr, outd, L.a_src, sc.s_src);
     a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
     a.s_dst = s_dst;
@@ -1135,9 +1137,8 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
     f.stat_dst_ids = r.dst_ids;
     f.stat_N = r.N;
   }
-  k_reduce_groups<<<grid_for(r.items_max / kItemGroup + 1, 8, kNumSMs * 16), 256, 0, s>>>(f);
-  k_local_raw<<<grid_for(r.D_max, 8, kNumSMs * 16), 256, 0, s>>>(f, lp, ldp, lcnt);
-  g_launches += 2;
+  launch_pdl(k_reduce_groups, dim3(grid_for(r.items_max / kItemGroup + 1, 8, kNumSMs * 16)), dim3(256), 0, s, f);
+  launch_pdl(k_local_raw, dim3(grid_for(r.D_max, 8, kNumSMs * 16)), dim3(256), 0, s, f, lp, ldp, lcnt);
 }
 
 void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const PartPtrs& parts, int64_t ldp, const OwnerFilter& own,
@@ -1145,9 +1146,8 @@ void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const PartPtrs& parts, 
                double* mean) {
   const ob_layer& sp = L.spec;
   if (sp.kind == OB_KIND_MOMENTS) {  // float64 partials, ldp counts float64 elements
-    k_merge_moments<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(P, parts, ldp, D_dev, own, sp.in_dim,
+    launch_pdl(k_merge_moments, dim3(grid_for(D_max, 8, kNumSMs * 16)), dim3(256), 0, s, P, parts, ldp, D_dev, own, sp.in_dim,
                                                                       moments_phase, sp.n, mean, agg, ld4(sp.in_dim));
-    OB_LAUNCHED();
     return;
   }
   MergeArgs m{};
@@ -1170,8 +1170,7 @@ void cgp_merge(cudaStream_t s, const LayerDev& L, int P, const PartPtrs& parts, 
     m.out = agg;
     m.ldo = ld4(m.width);
   }
-  k_merge_parts<<<grid_for(D_max, 8, kNumSMs * 16), 256, 0, s>>>(m);
-  OB_LAUNCHED();
+  launch_pdl(k_merge_parts, dim3(grid_for(D_max, 8, kNumSMs * 16)), dim3(256), 0, s, m);
 }
 
 void cgp_update(cudaStream_t s, const LayerDev& L, const int64_t* D_dev, int64_t D_max, const float* const* hvp,
@@ -1232,6 +1231,7 @@ BindCtx bind_ctx(Engine& e, RequestWs& w, int l) {
 }
 
 __global__ void k_pad_rows(const ReqParams* rp, int64_t rows, int w, float* dst, int64_t ld) {
+  pdl_wait();
   const float* __restrict__ src = rp->qfeat;
   const int64_t n = rows * ld;
   OB_GRID_STRIDE(i, n) {
@@ -1244,6 +1244,7 @@ __global__ void k_pad_rows(const ReqParams* rp, int64_t rows, int w, float* dst,
 // delta rows of the recomputed targets: dbuf[t] = prev[t] - PE[targets[t]] (t < T)
 __global__ void k_delta_rows(const int64_t* T_dev, const int32_t* __restrict__ targets, const float* __restrict__ prev,
                              const float* __restrict__ pe, int64_t ld, float* dbuf) {
+  pdl_wait();
   const int64_t n = (*T_dev) * ld;
   OB_GRID_STRIDE(t, n) {
     const int64_t i = t / ld;
@@ -1257,8 +1258,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
   const int k = (int)e.layers.size();
   // stage query features with 16 B aligned rows (unless staged early, stage_query_rows)
   if (!w.qpad_ready) {
-    k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, s>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
-    OB_LAUNCHED();
+    launch_pdl(k_pad_rows, dim3(grid_for((int64_t)w.B * e.g.F_ld, 256)), dim3(256), 0, s, w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
   }
   bool delta_ready = false;  // the previous layer's epilogue wrote this layer's delta rows
   for (int l = 1; l <= k; ++l) {
@@ -1300,9 +1300,8 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       // delta aggregates: static CSR-part sums of the stored rows + (h - PE) of recomputed sources
       const int64_t ld = ld4(L.spec.in_dim);
       if (!delta_ready) {
-        k_delta_rows<<<grid_for(b.D_max * ld, 256), 256, 0, s>>>(&w.rc->T, w.targets, w.outs[l - 1], e.pe[l - 2],
+        launch_pdl(k_delta_rows, dim3(grid_for(b.D_max * ld, 256)), dim3(256), 0, s, &w.rc->T, w.targets, w.outs[l - 1], e.pe[l - 2],
                                                                    ld, w.delta);
-        OB_LAUNCHED();
       }
       r.delta = true;
       r.dprev = w.outs[l - 1];
@@ -1359,8 +1358,7 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
 void stage_query_rows(Engine& e, RequestWs& w) {
   cudaStream_t s = e.stream;
   w.qrows_ready = false;
-  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, s>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
-  OB_LAUNCHED();
+  launch_pdl(k_pad_rows, dim3(grid_for((int64_t)w.B * e.g.F_ld, 256)), dim3(256), 0, s, w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
   w.qpad_ready = true;
   const LayerDev& L = e.layers[0];
   const bool yt = e.ytab_ready && !e.ytab.empty() && e.ytab[0] && w.qxw;
@@ -1381,15 +1379,13 @@ void stage_query_rows(Engine& e, RequestWs& w) {
 }
 
 void stage_qpad(Engine& e, RequestWs& w) {
-  k_pad_rows<<<grid_for((int64_t)w.B * e.g.F_ld, 256), 256, 0, e.stream>>>(w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
-  OB_LAUNCHED();
+  launch_pdl(k_pad_rows, dim3(grid_for((int64_t)w.B * e.g.F_ld, 256)), dim3(256), 0, e.stream, w.rp, w.B, e.g.F, w.qpad, e.g.F_ld);
 }
 
 // parity export of bind_kind / bind_pe_layer with the same binding rule
 void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d_kind, int32_t* d_pe_layer) {
   BindCtx c = bind_ctx(e, w, layer);
-  k_resolve<<<grid_for(b.S_max, 256), 256, 0, e.stream>>>(c, b.cnt, b.src_ids, w.rowp, nullptr, d_kind, d_pe_layer);
-  OB_LAUNCHED();
+  launch_pdl(k_resolve, dim3(grid_for(b.S_max, 256)), dim3(256), 0, e.stream, c, b.cnt, b.src_ids, w.rowp, nullptr, d_kind, d_pe_layer);
 }
 
 // raw CSR-part sum per node: out[v] = sum_{u in N(v)} w_u x_u (w_u = 1/sqrt(deg u + 1) for gcn),
@@ -1397,6 +1393,7 @@ void export_bindings(Engine& e, RequestWs& w, BlockDev& b, int layer, uint8_t* d
 __global__ void k_sagg_build(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
                              RowSrc x, int width, const int32_t* __restrict__ indeg, bool gcn, float* out,
                              int64_t ld, const int32_t* __restrict__ pos = nullptr) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1425,6 +1422,7 @@ __global__ void k_sagg_build(int64_t N, const int64_t* __restrict__ off, const i
 __global__ void k_sagg_gat_build(int64_t N, const int64_t* __restrict__ off, const int32_t* __restrict__ nbrs,
                                  const float* __restrict__ z, int64_t zld, int width, const float* __restrict__ ssrc,
                                  const float* __restrict__ a_dst, float* out, int64_t ld) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1511,9 +1509,8 @@ static void build_cgp_tables(Engine& e) {
       const RowSrc x = L1.transform_first ? RowSrc{nullptr, e.ytab[0], ld} : RowSrc{nullptr, e.g.feats, e.g.F_ld};
       for (auto& part : e.cgp.parts) {
         float* t = (float*)e.dalloc(sizeof(float) * N * ld);
-        k_sagg_build<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, part.off, part.src, x, w, e.g.indeg,
+        launch_pdl(k_sagg_build, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, N, part.off, part.src, x, w, e.g.indeg,
                                                                      L1.spec.kind == OB_KIND_GCN, t, ld, e.g.pos);
-        OB_LAUNCHED();
         e.cgp_sagg1.push_back(t);
       }
     }
@@ -1589,13 +1586,11 @@ void build_stored_transforms(Engine& e) {
       OB_CUDA(cudaMemGetInfo(&fb, &tb));
       if ((size_t)N * (ld + 1) * 4 <= fb / 3) {
         float* ssrc = (float*)e.dalloc(sizeof(float) * N);
-        k_rowdot_rows<<<grid_for(N, 8), 256, 0, s>>>(n_dev, RowSrc{nullptr, e.ytab[0], zld}, nullptr, w, L1.a_src,
+        launch_pdl(k_rowdot_rows, dim3(grid_for(N, 8)), dim3(256), 0, s, n_dev, RowSrc{nullptr, e.ytab[0], zld}, nullptr, w, L1.a_src,
                                                       ssrc);
-        OB_LAUNCHED();
         e.sagg1 = (float*)e.dalloc(sizeof(float) * N * ld);
-        k_sagg_gat_build<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, e.ytab[0], zld, w,
+        launch_pdl(k_sagg_gat_build, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, N, e.g.offsets, e.g.nbrs, e.ytab[0], zld, w,
                                                                         ssrc, L1.a_dst, e.sagg1, ld);
-        OB_LAUNCHED();
         OB_CUDA(cudaStreamSynchronize(s));
         e.dfree(ssrc);
       }
@@ -1613,9 +1608,8 @@ void build_stored_transforms(Engine& e) {
     if ((size_t)N * ld * 4 <= fb / 3) {
       e.sagg1 = (float*)e.dalloc(sizeof(float) * N * ld);
       const RowSrc x = L1.transform_first ? RowSrc{nullptr, e.ytab[0], ld} : RowSrc{nullptr, e.g.feats, e.g.F_ld};
-      k_sagg_build<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, x, w, e.g.indeg,
-                                                                   L1.spec.kind == OB_KIND_GCN, e.sagg1, ld);
-      OB_LAUNCHED();
+      launch_pdl(k_sagg_build, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, N, e.g.offsets, e.g.nbrs, x, w, e.g.indeg,
+                                                                   L1.spec.kind == OB_KIND_GCN, e.sagg1, ld, (const int32_t*)nullptr);
     }
   }
   // delta aggregates of srpe mid-block layers l = 2..k-1 (aggregate-first sum kinds): the CSR-part
@@ -1633,10 +1627,9 @@ void build_stored_transforms(Engine& e) {
     OB_CUDA(cudaMemGetInfo(&fb, &tb));
     if ((size_t)N * ld * 4 > fb / 3) continue;
     e.sagg_l[l - 1] = (float*)e.dalloc(sizeof(float) * N * ld);
-    k_sagg_build<<<grid_for(N, 8, kNumSMs * 16), 256, 0, s>>>(N, e.g.offsets, e.g.nbrs, RowSrc{nullptr, e.pe[l - 2], ld},
+    launch_pdl(k_sagg_build, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, N, e.g.offsets, e.g.nbrs, RowSrc{nullptr, e.pe[l - 2], ld},
                                                                  w, e.g.indeg, L.spec.kind == OB_KIND_GCN,
-                                                                 e.sagg_l[l - 1], ld);
-    OB_LAUNCHED();
+                                                                 e.sagg_l[l - 1], ld, (const int32_t*)nullptr);
   }
   OB_CUDA(cudaStreamSynchronize(s));
   e.dfree(n_dev);
@@ -1646,6 +1639,7 @@ void build_stored_transforms(Engine& e) {
 // precompute_embeddings: layers 1..k-1 over the whole graph (graphstore.py:330-365)
 // ---------------------------------------------------------------------------
 __global__ void k_node_scale(const int32_t* __restrict__ indeg, int64_t N, float* sc) {
+  pdl_wait();
   OB_GRID_STRIDE(v, N) sc[v] = (float)(1.0 / sqrt((double)indeg[v] + 1.0));
 }
 
@@ -1689,8 +1683,7 @@ void stage_precompute(Engine& e) {
     float* s_src = (float*)talloc(sizeof(float) * N);
     float* s_dst = (float*)talloc(sizeof(float) * N);
     float* gscale = (float*)talloc(sizeof(float) * N);
-    k_node_scale<<<grid_for(N, 256), 256, 0, s>>>(e.g.indeg, N, gscale);
-    OB_LAUNCHED();
+    launch_pdl(k_node_scale, dim3(grid_for(N, 256)), dim3(256), 0, s, e.g.indeg, N, gscale);
     ScanScratch sc_scan;
     sc_scan.cap = ScanScratch::bytes_for(N, 1);
     sc_scan.pool = (char*)talloc(sc_scan.cap);
