@@ -126,11 +126,51 @@ def main():
                     coll_bytes=0))
         eng.close()
         emu.close()
+    # a peer that stops serving: the waiting rank times out (OB_CGP_TIMEOUT_MS), raises
+    # TransportError and poisons the peer's flags, so the late rank fails too instead of
+    # reading regions that were overwritten; afterwards both engines refuse requests
+    from paper_2501_08547_b200._native import TransportError
+
+    os.environ["OB_CGP_TIMEOUT_MS"] = "300"
+    g = load_golden("small_s3")
+    N, F = int(g["N"]), g["feats"].shape[1]
+    ds = graphstore.GraphDataset(N, g["offsets"], g["nbrs"], g["feats"], np.ones(N, bool), np.zeros(N, bool))
+    req = ServingRequest(N, int(g["B"]), g["qfeat"], g["edges"])
+    model = models.make_model("sage_mean", 3, F, 6)
+    w = models.Weights(golden_weights(g, "w.sage_mean.k3", "sage_mean", 3))
+    pe = graphstore.PeStore([g[f"pe.sage_mean.k3.l{l}"] for l in (1, 2)])
+    cfg = runtime.ServeConfig(strategy="srpe-cgp", gamma=0.5, num_partitions=P, seed=11, device=local)
+    eng = runtime.distributed_engine(ds, pe, model, w, cfg)
+    eng.serve(req)  # both ranks in step
+    outcome = []
+
+    def attempt():
+        try:
+            eng.serve(req)
+            return "ok"
+        except TransportError:
+            return "transport"
+
+    if rank == 0:
+        outcome.append(attempt())  # rank 1 is not serving this one: timeout
+    dist.barrier()
+    if rank != 0:
+        outcome.append(attempt())  # behind by one request, flags poisoned by rank 0
+    dist.barrier()
+    outcome.append(attempt())  # both engines refuse further requests
+    eng.close()
+    os.environ.pop("OB_CGP_TIMEOUT_MS", None)
+    got = [None] * P
+    dist.all_gather_object(got, outcome)
+    if rank == 0:
+        results.append(dict(case="peer_timeout", kind="sage_mean", k=3,
+                            err_ref=0.0 if all(o == ["transport", "transport"] for o in got) else 1.0,
+                            err_emu=0.0, shard=True, coll_bytes=0, outcome=got))
     if rank == 0:
         worst = max(r["err_ref"] for r in results)
         ok = worst <= 1e-4 and all(r["shard"] for r in results) and all(
             r.get("partitioned", True) for r in results)
-        print(json.dumps(dict(ok=ok, P=P, cases=len(results), worst_err=worst, results=results[:4])))
+        print(json.dumps(dict(ok=ok, P=P, cases=len(results), worst_err=worst, results=results[:4] + results[-1:])))
     dist.destroy_process_group()
 
 
