@@ -209,7 +209,7 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.rq_keys = a.take<uint64_t>(m + 1);
   w.rq_keys2 = a.take<uint64_t>(m + 1);
   w.rx_cnt = a.take<int32_t>(256 * rx_tiles(m));
-  w.rx_off = a.take<int64_t>(256 * rx_tiles(m) + 1);
+  w.rx_off = a.take<int64_t>(256 * rx_tiles(m) + 257);  // + per-digit totals
   w.rx_st = a.take<uint32_t>(rx_st_words(m));
   w.rq_ctr = a.take<int64_t>(4);
   int64_t Emax = 1, Dmax = 1, Smax = 1, Imax = 1;

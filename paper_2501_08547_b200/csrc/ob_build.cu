@@ -274,12 +274,30 @@ __global__ void __launch_bounds__(128) k_sample_spans(const int32_t* __restrict_
   }
 }
 
-__global__ void k_bitmap_or(const uint32_t* __restrict__ part_bits, int nparts, int64_t words, uint32_t* sbits) {
+// OR of the per-CTA bitmaps: a CTA takes 32 words; each of its 8 warps ORs every
+// 8th part over those words (a warp reads 32 consecutive words: one coalesced
+// 128-byte line per part), then warp 0 combines the 8 partial words
+__global__ void __launch_bounds__(256) k_bitmap_or(const uint32_t* __restrict__ part_bits, int nparts, int64_t words,
+                                                   uint32_t* sbits) {
   pdl_wait();
-  OB_GRID_STRIDE(w, words) {
+  __shared__ uint32_t acc[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t w0 = (int64_t)blockIdx.x * 32; w0 < words; w0 += (int64_t)gridDim.x * 32) {
+    const int64_t w = w0 + lane;
     uint32_t v = 0;
-    for (int p = 0; p < nparts; ++p) v |= __ldg(part_bits + (int64_t)p * words + w);
-    sbits[w] = v;
+    if (w < words) {
+#pragma unroll 4
+      for (int p = warp; p < nparts; p += 8) v |= __ldg(part_bits + (int64_t)p * words + w);
+    }
+    acc[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0 && w < words) {
+      uint32_t o = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o |= acc[q][lane];
+      sbits[w] = o;
+    }
+    __syncthreads();
   }
 }
 
@@ -374,7 +392,8 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const Bu
     const int64_t words = w.words_NB + 1;
     launch_pdl(k_block_fill<true>, dim3(kNumSMs), dim3(1024), words * 4, s, b.cnt, b.dst_ptr, b.item_ptr, b.item_dst, sp, src.nbrs,
                                                         src.rq_src, sc.src_global, nullptr, words, sc.fill_bits);
-    launch_pdl(k_bitmap_or, dim3(grid_for(words, 256)), dim3(256), 0, s, sc.fill_bits, kNumSMs, words, sc.sbits);
+    launch_pdl(k_bitmap_or, dim3(grid_for(words, 32, kNumSMs * 8)), dim3(256), 0, s, (const uint32_t*)sc.fill_bits,
+               (int)kNumSMs, words, sc.sbits);
   } else {
     OB_CUDA(cudaMemsetAsync(sc.sbits, 0, sizeof(uint32_t) * (w.words_NB + 1), s));
     launch_pdl(k_block_fill<false>, dim3(grid_for(b.items_max, 32, kNumSMs * 2)), dim3(1024), 0, s, 

@@ -310,7 +310,7 @@ void carve_cgp(Engine& e, RequestWs& w, Arena& a) {
     pw.rq.keys = a.take<uint64_t>(w.m + 1);
     pw.rq.keys2 = a.take<uint64_t>(w.m + 1);
     pw.rq.rx_cnt = a.take<int32_t>(256 * rx_tiles(w.m));
-    pw.rq.rx_off = a.take<int64_t>(256 * rx_tiles(w.m) + 1);
+    pw.rq.rx_off = a.take<int64_t>(256 * rx_tiles(w.m) + 257);  // + per-digit totals
     pw.rq.ctr = a.take<int64_t>(4);
     for (int bi = 0; bi < 2; ++bi) {
       BlockDev b = bi == 0 ? mid : last;

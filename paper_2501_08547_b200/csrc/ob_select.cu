@@ -754,6 +754,30 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_ghist(const K* __restrict__ k
     if (h[i]) atomicAdd(ghist + i, h[i]);
 }
 
+// Digit d's tile counts -> their exclusive prefix over tiles (row d of the digit-major
+// count matrix) and the digit's total; one CTA per digit.  The scatter adds the
+// exclusive prefix over digit totals, so no grid-wide scan is needed between passes.
+constexpr int kRowScanThreads = 256;
+__global__ void __launch_bounds__(kRowScanThreads) k_rx_rowscan(const int32_t* __restrict__ cnt, int64_t tiles_b,
+                                                               int64_t* off, int64_t* dtot) {
+  pdl_wait();
+  using BS = cub::BlockScan<int64_t, kRowScanThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  const int d = blockIdx.x;
+  const int32_t* row = cnt + (int64_t)d * tiles_b;
+  int64_t carry = 0;
+  for (int64_t t0 = 0; t0 < tiles_b; t0 += kRowScanThreads) {
+    const int64_t t = t0 + threadIdx.x;
+    const int64_t v = t < tiles_b ? row[t] : 0;
+    int64_t x, agg;
+    BS(tmp).ExclusiveSum(v, x, agg);
+    __syncthreads();
+    if (t < tiles_b) off[(int64_t)d * tiles_b + t] = carry + x;
+    carry += agg;
+  }
+  if (threadIdx.x == 0) dtot[d] = carry;
+}
+
 // look-back word: flag in the top two bits (1 tile count, 2 inclusive prefix), count below
 constexpr uint32_t kRxAgg = 1u << 30, kRxInc = 2u << 30, kRxCount = kRxAgg - 1u;
 
@@ -764,7 +788,8 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
                                                            const int32_t* __restrict__ cnt, RqKeyFmt f, int64_t N,
                                                            const int32_t* __restrict__ cand_ids,
                                                            const ReqCounters* rc, uint32_t* st, uint32_t* ticket,
-                                                           const uint32_t* __restrict__ ghist) {
+                                                           const uint32_t* __restrict__ ghist,
+                                                           const int64_t* __restrict__ dtot) {
   pdl_wait();
   using BS = cub::BlockScan<int32_t, kRxThreads>;
   using BS64 = cub::BlockScan<int64_t, kRxThreads>;
@@ -782,8 +807,8 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
   const unsigned lt = (1u << lane) - 1u;
   const int64_t m = *m_dev;
   const int64_t tiles = (m + kRxTile - 1) / kRxTile;
-  if (st) {
-    int64_t g = threadIdx.x < 256 ? (int64_t)ghist[threadIdx.x] : 0, gx;
+  if (st || dtot) {  // keys of smaller digits: one-sweep totals, or the row scans' digit totals
+    int64_t g = threadIdx.x < 256 ? (st ? (int64_t)ghist[threadIdx.x] : dtot[threadIdx.x]) : 0, gx;
     BS64(scan_tmp64).ExclusiveSum(g, gx);
     if (threadIdx.x < 256) gbase[threadIdx.x] = gx;
   }
@@ -851,7 +876,7 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
     } else if (off) {
       if (threadIdx.x < 256) {
         bstart[threadIdx.x] = start;
-        gofs[threadIdx.x] = off[(int64_t)threadIdx.x * tiles_b + t];
+        gofs[threadIdx.x] = gbase[threadIdx.x] + off[(int64_t)threadIdx.x * tiles_b + t];
       }
     } else {
       // few tiles: derive this tile's global digit offsets from the raw counts
@@ -931,10 +956,10 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
       uint32_t* sp = st + (int64_t)p * 256 * tiles_b;
       if (p + 1 == passes) {
         launch_pdl(k_rx_scatter<K, true>, dim3(g), dim3(kRxThreads), 0, s, a, nullptr, c.src, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
-                                                        e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p);
+                                                        e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p, nullptr);
       } else {
         launch_pdl(k_rx_scatter<K, false>, dim3(g), dim3(kRxThreads), 0, s, a, b, nullptr, m_dev, shift, tiles_b, nullptr, c.rx_cnt, f,
-                                                         e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p);
+                                                         e.g.N, w.cand_ids, w.rc, sp, ticket + p, ghist + 256 * p, nullptr);
         std::swap(a, b);
       }
       OB_LAUNCHED();
@@ -943,20 +968,21 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
   }
   const bool fused = tiles_b <= 32;  // few tiles: offsets come straight from the counts
   const int64_t* off = fused ? nullptr : c.rx_off;
+  const int64_t* dtot = fused ? nullptr : c.rx_off + 256 * tiles_b;  // per-digit totals (row scans)
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
     launch_pdl(k_rx_hist<K>, dim3(g), dim3(kRxThreads), 0, s, a, m_dev, shift, tiles_b, c.rx_cnt);
-    if (!fused)
-      device_scan(s, e.scan, LoadI32{c.rx_cnt}, StoreI64{c.rx_off}, nullptr, 256 * tiles_b, 256 * tiles_b, nullptr);
+    if (!fused)  // each digit's tile counts scanned by its own CTA; the digit prefix is taken in the scatter
+      launch_pdl(k_rx_rowscan, dim3(256), dim3(kRowScanThreads), 0, s, (const int32_t*)c.rx_cnt, tiles_b, c.rx_off,
+                 c.rx_off + 256 * tiles_b);
     if (p + 1 == passes) {
       launch_pdl(k_rx_scatter<K, true>, dim3(g), dim3(kRxThreads), 0, s, a, nullptr, c.src, m_dev, shift, tiles_b, off, c.rx_cnt, f,
-                                                      e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr);
+                                                      e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr, dtot);
     } else {
       launch_pdl(k_rx_scatter<K, false>, dim3(g), dim3(kRxThreads), 0, s, a, b, nullptr, m_dev, shift, tiles_b, off, c.rx_cnt, f,
-                                                       e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr);
+                                                       e.g.N, w.cand_ids, w.rc, nullptr, nullptr, nullptr, dtot);
       std::swap(a, b);
     }
-    OB_LAUNCHED();
   }
 }
 
