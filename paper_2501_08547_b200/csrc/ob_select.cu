@@ -165,36 +165,19 @@ __device__ __forceinline__ K rq_key(int64_t s, int64_t d, int64_t N, const uint3
   return ((K)1 << f.body) | ((K)(d - N) << f.bN) | (K)sr;
 }
 
-// candidate-slot counts (query slots take qdeg) + one radix key per edge, and the
-// first radix pass's digit counts per 4096-key tile (the sort skips that k_rx_hist):
-// a CTA takes whole tiles, 16 keys per thread, and counts their low digits in
-// shared memory.  Every tile row is written, zero for a request rejected earlier.
-constexpr int kRqThreads = 256;
+// candidate-slot counts (query slots take qdeg) + one radix key per edge
 template <class K>
-__global__ void __launch_bounds__(kRqThreads) k_rq_count(const ReqParams* rp, int64_t N, const uint32_t* cbits,
-                                                         const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt,
-                                                         K* keys, RqKeyFmt f, int64_t tiles_b, int32_t* hist0) {
+__global__ void k_rq_count(const ReqParams* rp, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
+                           const ReqCounters* rc, int32_t* rq_cnt, K* keys, RqKeyFmt f) {
   pdl_wait();
-  __shared__ int32_t h[256];
-  const bool bad = rc->err & (kErrRange | kErrNoQuery);
+  if (rc->err & (kErrRange | kErrNoQuery)) return;
   const int64_t* __restrict__ edges = rp->edges;
-  const int64_t m = bad ? 0 : rp->m;
-  const int64_t R = rc->R;
-  for (int64_t t = blockIdx.x; t < tiles_b; t += gridDim.x) {
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t e1 = min((t + 1) * kRxTile, m);
-    for (int64_t e = t * kRxTile + threadIdx.x; e < e1; e += kRqThreads) {
-      int64_t s, d;
-      ld_edge(edges, e, s, d);
-      if (d < N) warp_agg_inc(rq_cnt, bm_rank(cbits, cwpre, d));
-      const K k = rq_key<K>(s, d, N, cbits, cwpre, R, f);
-      keys[e] = k;
-      atomicAdd(&h[(int)(k & 255)], 1);
-    }
-    __syncthreads();
-    hist0[(int64_t)threadIdx.x * tiles_b + t] = h[threadIdx.x];
-    __syncthreads();
+  const int64_t m = rp->m;
+  OB_GRID_STRIDE(e, m) {
+    int64_t s, d;
+    ld_edge(edges, e, s, d);
+    if (d < N) warp_agg_inc(rq_cnt, bm_rank(cbits, cwpre, d));
+    keys[e] = rq_key<K>(s, d, N, cbits, cwpre, rc->R, f);
   }
 }
 
@@ -949,8 +932,7 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
 #endif
 
 template <class K>
-static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int64_t m_bound, const RqKeyFmt& f,
-                    bool hist0_ready = false) {
+static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int64_t m_bound, const RqKeyFmt& f) {
   cudaStream_t s = e.stream;
   const int64_t tiles_b = rx_tiles(m_bound);
   const int g = grid_for(tiles_b, 1, kNumSMs * (OB_RX_MINB > 2 ? OB_RX_MINB : 2));
@@ -989,7 +971,7 @@ static void rx_sort(Engine& e, RequestWs& w, RqCsr& c, const int64_t* m_dev, int
   const int64_t* dtot = fused ? nullptr : c.rx_off + 256 * tiles_b;  // per-digit totals (row scans)
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
-    if (p > 0 || !hist0_ready) launch_pdl(k_rx_hist<K>, dim3(g), dim3(kRxThreads), 0, s, a, m_dev, shift, tiles_b, c.rx_cnt);
+    launch_pdl(k_rx_hist<K>, dim3(g), dim3(kRxThreads), 0, s, a, m_dev, shift, tiles_b, c.rx_cnt);
     if (!fused)  // each digit's tile counts scanned by its own CTA; the digit prefix is taken in the scatter
       launch_pdl(k_rx_rowscan, dim3(256), dim3(kRowScanThreads), 0, s, (const int32_t*)c.rx_cnt, tiles_b, c.rx_off,
                  c.rx_off + 256 * tiles_b);
@@ -1042,13 +1024,10 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
   if (m > 0) {  // candidate-slot counts + the request CSR's radix keys
     const RqKeyFmt f = rq_key_fmt(e, w);
     if (f.wide())
-      launch_pdl(k_rq_count<uint64_t>, dim3(grid_for(rx_tiles(m), 1, kNumSMs * 8)), dim3(kRqThreads), 0, s, w.rp, N,
-                 (const uint32_t*)w.cbits, (const int64_t*)w.cwpre, (const ReqCounters*)w.rc, w.rq_cnt, w.rq_keys, f,
-                 rx_tiles(m), w.rx_cnt);
+      launch_pdl(k_rq_count<uint64_t>, dim3(grid_for(m, 256)), dim3(256), 0, s, w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt, w.rq_keys, f);
     else
-      launch_pdl(k_rq_count<uint32_t>, dim3(grid_for(rx_tiles(m), 1, kNumSMs * 8)), dim3(kRqThreads), 0, s, w.rp, N,
-                 (const uint32_t*)w.cbits, (const int64_t*)w.cwpre, (const ReqCounters*)w.rc, w.rq_cnt,
-                 reinterpret_cast<uint32_t*>(w.rq_keys), f, rx_tiles(m), w.rx_cnt);
+      launch_pdl(k_rq_count<uint32_t>, dim3(grid_for(m, 256)), dim3(256), 0, s, w.rp, N, w.cbits, w.cwpre, w.rc, w.rq_cnt,
+                                                            reinterpret_cast<uint32_t*>(w.rq_keys), f);
   }
   (void)need_scores;
 }
@@ -1513,9 +1492,8 @@ void build_rq_csr(Engine& e, RequestWs& w, const int64_t* edges, int64_t m_bound
   }
   device_scan(s, e.scan, LoadI32{c.cnt}, StoreI64{c.ptr}, &w.rc->RB, 0, rb_max, nullptr, c.ptr);
   if (m_bound <= 0) return;
-  // the whole request's keys came from k_rq_count with the first pass's digit counts
-  if (f.wide()) rx_sort<uint64_t>(e, w, c, m_dev, m_bound, f, counts_ready);
-  else rx_sort<uint32_t>(e, w, c, m_dev, m_bound, f, counts_ready);
+  if (f.wide()) rx_sort<uint64_t>(e, w, c, m_dev, m_bound, f);
+  else rx_sort<uint32_t>(e, w, c, m_dev, m_bound, f);
 }
 
 void stage_request_csr(Engine& e, RequestWs& w) {
