@@ -13,7 +13,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libomega_b200.so")
+# OB_LIB_VARIANT=name loads libomega_b200.<name>.so from the package directory instead
+# (same-box A/B of two builds, tools/ab_variants.sh); the default is the in-tree build
+_VARIANT = os.environ.get("OB_LIB_VARIANT", "")
+LIB_PATH = os.path.join(_HERE, f"libomega_b200.{_VARIANT}.so" if _VARIANT else "libomega_b200.so")
 
 OB_OK, OB_EINVAL, OB_ENOTFOUND, OB_ECOMM, OB_ECUDA, OB_ENOMEM, OB_ESTATE = range(7)
 STRATEGY = {"full": 0, "sampled": 1, "srpe": 2, "srpe-cgp": 3}
