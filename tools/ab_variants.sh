@@ -4,7 +4,7 @@
 out=${1:-gpurun_out/ab}; cfg=${2:-cfg2}; rounds=${3:-2}
 mkdir -p "$out"
 for r in $(seq 1 $rounds); do
-  for v in a b; do
+  for v in ${VARIANTS:-a b}; do
     OB_LIB_VARIANT=$v python bench.py --config $cfg --no-cpu --no-e2e > "$out/${cfg}_${v}_$r.json" 2> "$out/${cfg}_${v}_$r.err"
     python -c "
 import json
