@@ -180,6 +180,8 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
   w.qdeg = a.take<int32_t>(B + 1);
   w.cbits = a.take<uint32_t>(p.words_N + 1);
   w.cwpre = a.take<int64_t>(p.words_N + 1);
+  w.c_gcnt = p.words_N > kSparseRankWords ? a.take<int32_t>(p.words_N / 32 + 2) : nullptr;
+  w.c_gpre = p.words_N > kSparseRankWords ? a.take<int64_t>(p.words_N / 32 + 2) : nullptr;
   w.cand_ids = a.take<int32_t>(p.R_max);
   w.cand_nq = a.take<int32_t>(p.R_max);
   w.cand_score = a.take<double>(p.R_max);
@@ -223,6 +225,8 @@ static void carve(Engine& e, RequestWs& w, Plan& p, Arena& a) {
     sc.sbits = a.take<uint32_t>(p.words_NB + 1);
     sc.fill_bits = p.words_NB <= 48 * 1024 ? a.take<uint32_t>(kNumSMs * (p.words_NB + 1)) : nullptr;
     sc.swpre = a.take<int64_t>(p.words_NB + 1);
+    sc.gcnt = p.words_NB > kSparseRankWords ? a.take<int32_t>(p.words_NB / 32 + 2) : nullptr;
+    sc.gpre = p.words_NB > kSparseRankWords ? a.take<int64_t>(p.words_NB / 32 + 2) : nullptr;
     sc.src_global = a.take<int32_t>(E);
     sc.seg_len = a.take<int64_t>(D);
     sc.span_cs = a.take<int64_t>(D);

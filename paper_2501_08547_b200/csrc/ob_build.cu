@@ -402,8 +402,7 @@ void assemble(Engine& e, RequestWs& w, BlockDev& b, const SpanSrc& src, const Bu
   if (b.has_self) {
     launch_pdl(k_mark_ids, dim3(grid_for(b.D_max, 256)), dim3(256), 0, s, b.dst_ids, b.cnt, sc.sbits);
   }
-  device_scan(s, e.scan, LoadPopc{sc.sbits}, StoreI64{sc.swpre}, nullptr, w.words_NB, w.words_NB, &b.cnt->S, sc.swpre);
-  k_bitmap_compact_ext(e, sc.sbits, sc.swpre, w.words_NB, b.src_ids);
+  bitmap_rank(e, sc.sbits, w.words_NB, sc.swpre, b.src_ids, &b.cnt->S, sc.gcnt, sc.gpre);
   launch_pdl(k_relabel, dim3(grid_for(b.E_max, 256)), dim3(256), 0, s, b.cnt, sc.src_global, sc.sbits, sc.swpre, b.edge_src);
   if (b.has_self) {
     launch_pdl(k_self_rows, dim3(grid_for(b.D_max, 256)), dim3(256), 0, s, b.cnt, b.dst_ids, sc.sbits, sc.swpre, b.self_src);

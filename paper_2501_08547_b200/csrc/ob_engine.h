@@ -236,6 +236,8 @@ struct BuildScratch {
   uint32_t* sbits = nullptr;       // source bitmap over [0, N+B)
   uint32_t* fill_bits = nullptr;   // [148][words_NB+1] per-CTA source bitmaps (small N only)
   int64_t* swpre = nullptr;        // [words_NB+1] popcount prefix
+  int32_t* gcnt = nullptr;         // group-sparse rank: [words_NB/32 + 1] per-group counts (large N only)
+  int64_t* gpre = nullptr;         //   and their prefix
   int32_t* src_global = nullptr;   // [E] global source id per edge
   int64_t* seg_len = nullptr;      // [D] CSR span + request span per destination
   int64_t* span_cs = nullptr;      // [D] CSR start/len, request start/len
@@ -258,6 +260,8 @@ struct RequestWs {
   // candidate set (bitmap-rank over [0, N))
   uint32_t* cbits = nullptr;
   int64_t* cwpre = nullptr;        // [words+1]
+  int32_t* c_gcnt = nullptr;       // group-sparse rank of the candidate bitmap (large N only)
+  int64_t* c_gpre = nullptr;
   int32_t* cand_ids = nullptr;     // [R]
   int32_t* cand_nq = nullptr;      // [R]
   double* cand_score = nullptr;    // [R]
@@ -550,6 +554,10 @@ void stage_qpad(Engine& e, RequestWs& w);
 void stage_query_rows(Engine& e, RequestWs& w);
 
 void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, int64_t words, int32_t* out);
+// bitmaps above this many words take the group-sparse rank (bitmap_rank)
+constexpr int64_t kSparseRankWords = 256 * 1024;  // 8.4M ids
+void bitmap_rank(Engine& e, const uint32_t* bits, int64_t words, int64_t* wpre, int32_t* out, int64_t* total,
+                 int32_t* gcnt, int64_t* gpre);
 
 void stage_request_prep(Engine& e, RequestWs& w, bool need_scores);
 void stage_request_post(Engine& e, RequestWs& w, bool need_scores);

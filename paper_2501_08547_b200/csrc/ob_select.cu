@@ -141,6 +141,72 @@ void k_bitmap_compact_ext(Engine& e, const uint32_t* bits, const int64_t* wpre, 
   launch_pdl(k_bitmap_compact, dim3(grid_for(words, 256)), dim3(256), 0, e.stream, bits, wpre, words, out);
 }
 
+// Bitmap-rank over a huge id space (papers scale: 3.5M words for 111M ids) with
+// few set bits: count per 32-word group (one warp reads a group's 128 bytes), scan
+// the group counts (32x shorter than the words), then only the non-empty groups
+// write their words' prefixes and their ids.  The dense path scans every word and
+// writes an int64 prefix for all of them (~100 MB of traffic at 111M ids); this one
+// reads the bitmap once.  Word prefixes of empty groups are left unwritten: ranks
+// are only taken of set bits.
+__global__ void __launch_bounds__(256) k_bm_group_popc(const uint32_t* __restrict__ bits, int64_t words,
+                                                       int64_t groups, int32_t* gcnt) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = gw; g < groups; g += nw) {
+    const int64_t w = g * 32 + lane;
+    int c = w < words ? __popc(__ldg(bits + w)) : 0;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) gcnt[g] = c;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bm_group_fin(const uint32_t* __restrict__ bits, int64_t words, int64_t groups,
+                                                      const int32_t* __restrict__ gcnt,
+                                                      const int64_t* __restrict__ gpre, int64_t* wpre, int32_t* out) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (gw == 0 && lane == 0) wpre[words] = gpre[groups];  // the total, like the dense scan's out_arr
+  for (int64_t g = gw; g < groups; g += nw) {
+    if (__ldg(gcnt + g) == 0) continue;
+    const int64_t w = g * 32 + lane;
+    uint32_t b = w < words ? __ldg(bits + w) : 0u;
+    const int c = __popc(b);
+    int x = c;  // inclusive warp scan
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    int64_t pos = __ldg(gpre + g) + (x - c);
+    if (w < words) wpre[w] = pos;
+    while (b) {
+      const int t = __ffs(b) - 1;
+      out[pos++] = (int32_t)(w * 32 + t);
+      b &= b - 1;
+    }
+  }
+}
+
+// prefix of set bits per word + the sorted ids of the set bits + their count:
+// the dense scan, or the group-sparse one for large bitmaps
+void bitmap_rank(Engine& e, const uint32_t* bits, int64_t words, int64_t* wpre, int32_t* out, int64_t* total,
+                 int32_t* gcnt, int64_t* gpre) {
+  cudaStream_t s = e.stream;
+  if (words <= kSparseRankWords || !gcnt) {
+    device_scan(s, e.scan, LoadPopc{bits}, StoreI64{wpre}, nullptr, words, words, total, wpre);
+    k_bitmap_compact_ext(e, bits, wpre, words, out);
+    return;
+  }
+  const int64_t groups = (words + 31) / 32;
+  launch_pdl(k_bm_group_popc, dim3(grid_for(groups, 8, kNumSMs * 16)), dim3(256), 0, s, bits, words, groups, gcnt);
+  device_scan(s, e.scan, LoadI32{gcnt}, StoreI64{gpre}, nullptr, groups, groups, total, gpre);
+  launch_pdl(k_bm_group_fin, dim3(grid_for(groups, 8, kNumSMs * 16)), dim3(256), 0, s, bits, words, groups,
+             (const int32_t*)gcnt, (const int64_t*)gpre, wpre, out);
+}
+
 // RB = R + B slots; query slots take their counts from the per-query in-degrees
 __global__ void k_slots_init(ReqCounters* rc, int B, const int32_t* qdeg, int32_t* rq_cnt, int32_t* rq_fill) {
   pdl_wait();
@@ -1017,8 +1083,7 @@ void stage_request_prep(Engine& e, RequestWs& w, bool need_scores) {
     launch_pdl(k_request_mark, dim3(grid_for(m, kEdgeTile, kNumSMs * 4)), dim3(256), sq, s, w.rp, N, w.B, w.cbits, w.qdeg, w.rc);
   }
   // candidate set: popcount prefix, ascending ids
-  device_scan(s, e.scan, LoadPopc{w.cbits}, StoreI64{w.cwpre}, nullptr, w.words_N, w.words_N, &w.rc->R, w.cwpre);
-  launch_pdl(k_bitmap_compact, dim3(grid_for(w.words_N, 256)), dim3(256), 0, s, w.cbits, w.cwpre, w.words_N, w.cand_ids);
+  bitmap_rank(e, w.cbits, w.words_N, w.cwpre, w.cand_ids, &w.rc->R, w.c_gcnt, w.c_gpre);
   const int64_t rb_max = std::min<int64_t>(N, 2 * m) + w.B;
   launch_pdl(k_slots_init, dim3(grid_for(rb_max, 256)), dim3(256), 0, s, w.rc, w.B, w.qdeg, w.rq_cnt, w.rq_fill);
   if (m > 0) {  // candidate-slot counts + the request CSR's radix keys

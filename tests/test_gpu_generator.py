@@ -105,3 +105,34 @@ def test_generated_graph_cgp_emulation_matches_centralized(P):
     assert tot == len(nb)
     cen.close()
     cgp.close()
+
+
+def test_large_id_space_group_sparse_rank():
+    """N = 12M ids: the candidate and block-source bitmaps (375K words) take the group-sparse rank
+    (kSparseRankWords = 256K words); plan and blocks must equal the oracle's on the read-back graph."""
+    from oracle import structure as ST
+    from paper_2501_08547_b200 import graphstore, models, runtime, workload
+
+    N = 12_000_000
+    ds = graphstore.SyntheticGraph(N, 4.0, 2.1, 8, seed=5)
+    model = models.make_model("sage_mean", 3, 8, 8)
+    w = models.init_weights(model, 3)
+    eng = runtime.ServingEngine(ds, graphstore.SyntheticPe([8, 8], seed=9), model, w,
+                                runtime.ServeConfig(strategy="srpe", gamma=0.3))
+    off, nb, _ = eng.graph_csr()
+    deg = np.diff(off)
+    for seed in (4, 5):
+        req = workload.make_request_synthetic(N, 4.0, 2.1, 8, 256, seed=seed)
+        emb, bd = eng.serve(req)
+        assert np.all(np.isfinite(emb))
+        ids, nq, total = ST.candidates(req.edges, N, deg)
+        targets = ST.select_top(ids, ST.ratio_scores(nq, total), 0.3)
+        plan = eng.last_plan()
+        assert np.array_equal(plan["ids"], ids) and np.array_equal(plan["targets"], targets)
+        blocks = ST.build_srpe(N, 256, off, nb, req.edges, targets, 3, 2)
+        for l, rb in enumerate(blocks, start=1):
+            gb = eng.last_block(l)
+            for f in ("src_ids", "dst_ids", "edge_src", "edge_dst", "bind_kind", "src_degree", "dst_self_src"):
+                assert np.array_equal(np.asarray(getattr(gb, f), np.int64), np.asarray(getattr(rb, f), np.int64)), (l, f)
+        assert bd.fetch_bytes == ST.fetch_bytes(blocks, N, 8, [8, 8])
+    eng.close()
