@@ -194,6 +194,8 @@ class NvlinkCounter:
             vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
         except Exception:
             return None
+        if not any(v.nvmlReturn == 0 for v in vals):
+            return None  # NOT_SUPPORTED on these boxes (profiles/r02/n2/nvml_nvlink_probe.txt)
         tx = sum(int(v.value.ullVal) for v, (f, _) in zip(vals, ids) if f == self.TX and v.nvmlReturn == 0)
         rx = sum(int(v.value.ullVal) for v, (f, _) in zip(vals, ids) if f == self.RX and v.nvmlReturn == 0)
         return tx * 1024, rx * 1024
@@ -570,7 +572,10 @@ def main():
         torch.cuda.synchronize()
         clk_lanes = clocks.stop()
         nvl1 = nvl.read() if nvl else None
-        if nvl0 is not None and nvl1 is not None:
+        ok_nvl = torch.tensor([1 if (nvl0 is not None and nvl1 is not None) else 0], device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(ok_nvl, op=torch.distributed.ReduceOp.MIN)  # every rank or none
+        if int(ok_nvl.item()):
             t = torch.tensor([float(nvl1[0] - nvl0[0]), float(nvl1[1] - nvl0[1])], device=dev)
             torch.distributed.all_reduce(t)  # every rank's counters
             nvl_measured = {"tx_bytes": int(t[0].item()), "rx_bytes": int(t[1].item()), "steps": args.steps,
@@ -775,7 +780,8 @@ def main():
                         "nvlink_note": "per request of one CGP group, all ranks: the exchange's bytes from the "
                                        "request's actual destination counts; allgather_rows_bytes = the all-gather-"
                                        "of-source-rows alternative sum_l (P-1) S_l row_bytes_l",
-                        "nvlink_measured": nvl_measured} if cgp else {})},
+                        "nvlink_measured": nvl_measured or "unavailable: NVML NVLink throughput counters return "
+                                                           "NOT_SUPPORTED here"} if cgp else {})},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
