@@ -210,12 +210,12 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-def ncu_traffic(cfg):
+def ncu_traffic(cfg, key="dram_bytes_per_launch"):
     """dram bytes per launch (averaged over one request's launches, like roofline.achieved) of the
     aggregation kernel from the committed ncu capture of this config, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_agg_traffic.json")) as f:
-            return json.load(f).get(cfg, {}).get("dram_bytes_per_launch")
+            return json.load(f).get(cfg, {}).get(key)
     except Exception:
         return None
 
@@ -530,7 +530,8 @@ def main():
     agg = _read_prof(lib, eng, nat, 0)
     gemm = _read_prof(lib, eng, nat, 1)
     fin = _read_prof(lib, eng, nat, 2)
-    reqp = _read_prof(lib, eng, nat, 6)
+    reqp = _read_prof(lib, eng, nat, 6)  # minus the profiler's own row-count kernels (class 9)
+    prof_count_ms = _read_prof(lib, eng, nat, 9)["ms"]
     st = {name: _read_prof(lib, eng, nat, cls) for name, cls in
           (("select", 4), ("request_csr", 7), ("build", 3), ("resolve", 5), ("collectives", 8))}
     nat.check(lib.ob_profile(eng._h, 0))
@@ -711,15 +712,22 @@ def main():
     roof = {"bound": "hbm", "kernel": "k_agg (edge-chunk gather + segment reduce)",
             "achieved": round(agg_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(agg_gbs / hbm, 4),
             "peak_source": which, "traffic": ncu_traffic(cfg),
+            "traffic_live": ncu_traffic(cfg, "dram_bytes_per_launch_live"),
+            "alg_bytes_per_launch": round(agg["bytes"] / max(agg["n"], 1)),
             "launches": agg["n"], "avg_launch_us": round(agg["ms"] * 1e3 / max(agg["n"], 1), 2),
             "gathered_row_gbs": round(agg["flops"] / (agg["ms"] / 1e3) / 1e9, 1) if agg["ms"] > 0 else None,
             "gather_ceiling_gbs": 15200.0,  # measured random 512-B row gather, L2-sized table (profiles/r01_gather_ceiling.md)
             "note": "k_agg is bound by the per-SM L2->SM return path, not HBM: rows are re-read once per "
-                    "edge, ~70-80 % from L2 (gathered_row_gbs = the row bytes the launches actually gathered, "
-                    "against the measured 15.2 TB/s random-row gather ceiling). achieved counts algorithmic "
-                    "bytes (each unique row once): the layer-1 launch (stored aggregates) its edge list and "
-                    "partials, the layer-2 launch (delta aggregates) its edge list, the recomputed rows (<= D) "
-                    "and partials, the query-block launch its edge list, every source row once and partials",
+                    "edge, ~70-80 % from L2 and ~30 % from L1 (gathered_row_gbs = the row bytes the launches "
+                    "loaded, against the measured 15.2 TB/s random-row gather ceiling from L2; L1 hits lift it "
+                    "above). traffic = cold ncu --set full DRAM bytes per launch, traffic_live = the same "
+                    "without cache flushes between kernels. achieved counts algorithmic "
+                    "bytes (each distinct row once): every launch its edge list, the distinct rows it loaded "
+                    "and its partials -- the layer-1 launch (stored aggregates) the request-span sources' "
+                    "rows, the layer-2 launch (delta aggregates) the delta rows of recomputed CSR sources "
+                    "and the request-span sources' rows (distinct rows counted on the device by the "
+                    "profiler's k_prof_rows, outside the timed events), the query-block launch every source "
+                    "row",
             "share_of_step": round(agg["ms"] / max(reqp["ms"], 1e-9), 3)}
     # the whole request against HBM, with SURVEY.md 8(d)'s per-unit figure: bytes(G) =
     # graph_fetch_bytes(G) + sum_l 4 H_l D_l + 4 F B + 16 m per query batch, over the per-request
@@ -766,7 +774,7 @@ def main():
                    if synthetic else "reference generator (bit-identical numpy streams), PE from GPU precompute",
                    "graph": info},
         "roofline": roof,
-        "eager_ms_per_step": round(float(lat_eager.mean()), 4),
+        "eager_ms_per_step": round(float(lat_eager.mean()) - prof_count_ms / args.steps, 4),
         "kernels_ms_per_step": {"agg": round(agg["ms"] / args.steps, 4), "gemm": round(gemm["ms"] / args.steps, 4),
                                 "finalize": round(fin["ms"] / args.steps, 4),
                                 **{name: round(st[name]["ms"] / args.steps, 4) for name in st}},

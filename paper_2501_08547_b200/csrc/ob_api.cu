@@ -38,6 +38,9 @@ Engine::~Engine() {
   }
   if (lane_fork_ev) cudaEventDestroy(lane_fork_ev);
   drop_graphs();
+  for (cudaEvent_t ev_ : prof.pool) cudaEventDestroy(ev_);
+  if (prof.pinned) cudaFreeHost(prof.pinned);
+  if (prof.rowbits) cudaFree(prof.rowbits);
   cgp_destroy(*this);
   if (arena.base) cudaFree(arena.base);
   if (scan.pool) cudaFree(scan.pool);
@@ -1572,6 +1575,12 @@ int ob_profile_read(ob_engine* h, int32_t cls, double* total_ms, int64_t* launch
     double ms = 0, by = 0, fl = 0;
     int64_t n = 0;
     for (const ProfRec& r : e.prof.recs) {
+      if (cls == kProfRequest && r.cls == kProfCount) {  // the profiler's own row counts are not request time
+        float t = 0;
+        OB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        ms -= t;
+        continue;
+      }
       if (r.cls != cls) continue;
       float t = 0;
       OB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
@@ -1579,15 +1588,12 @@ int ob_profile_read(ob_engine* h, int32_t cls, double* total_ms, int64_t* launch
       ++n;
       if (r.slot < 0) continue;
       const BlockCounters& c = e.prof.pinned[r.slot];
-      if (cls == kProfAgg && r.K == -2) {
-        // delta launch: edge list, the recomputed rows it gathers (at most the D block rows) and
-        // the partials
-        by += 4.0 * c.E + 4.0 * r.width * c.D + 4.0 * r.pw * c.items;
-        fl += 4.0 * r.width * c.gathered;  // rows it actually gathered (device count)
-      } else if (cls == kProfAgg && r.K < 0) {
-        // stored-aggregate launch: rows gathered for the request spans only (not sized by the
-        // block counters) -- count the edge list and the partials, no rows (conservative)
-        by += 4.0 * c.E + 4.0 * r.pw * c.items;
+      if (cls == kProfAgg && r.K < 0) {
+        // stored-aggregate (K = -1) or delta (K = -2) launch: edge list, every distinct row it
+        // loaded once (request-span sources, delta rows of recomputed CSR sources; counted on the
+        // device by k_prof_rows) and the partials
+        by += 4.0 * c.E + 4.0 * r.width * c.uniq + 4.0 * r.pw * c.items;
+        fl += 4.0 * r.width * c.gathered;  // row bytes it loaded (one row per kept edge)
       } else if (cls == kProfAgg) {
         // edge list + every source row once + partial rows out
         by += 4.0 * c.E + 4.0 * r.width * c.S + 4.0 * r.pw * c.items;

@@ -52,7 +52,8 @@ struct BlockCounters {
   int64_t feat_src;    // FEATURE-bound training sources (fetch bytes)
   int64_t pe_src;      // PE-bound sources (fetch bytes)
   int64_t groups;      // second-level partial groups (hub destinations)
-  int64_t gathered;    // rows gathered by delta-mode aggregations over this block (profiler)
+  int64_t gathered;    // profiler: row loads of the stored-aggregate / delta aggregation over this block
+  int64_t uniq;        // profiler: distinct rows that aggregation loaded
 };
 
 // A computation block in device memory (CSR over destinations).
@@ -336,7 +337,8 @@ struct RequestWs {
 // in-library kernel profiler (CUDA events on the launching stream) -------------
 // Used by bench.py to time the dominant kernel live inside the timed region.
 enum ProfClass { kProfAgg = 0, kProfGemm = 1, kProfFinalize = 2, kProfBuild = 3, kProfSelect = 4,
-                 kProfResolve = 5, kProfRequest = 6, kProfCsr = 7, kProfComm = 8, kProfClasses = 9 };
+                 kProfResolve = 5, kProfRequest = 6, kProfCsr = 7, kProfComm = 8, kProfCount = 9,
+                 kProfClasses = 10 };
 
 struct ProfRec {
   int cls;
@@ -355,6 +357,9 @@ struct Profiler {
   BlockCounters* pinned = nullptr;  // snapshot slots
   int nslots = 0, used_slots = 0;
   std::vector<std::pair<const BlockCounters*, int>> pending;  // this request's snapshots
+  uint32_t* rowbits = nullptr;  // device bitmap for the gathered-row count (profiler only)
+  int64_t rowbits_words = 0;
+  uint32_t* bits(int64_t words, cudaStream_t s);  // zeroed on s
   cudaEvent_t take();
   int slot_for(const BlockCounters* d);
   void request_end(cudaStream_t s);

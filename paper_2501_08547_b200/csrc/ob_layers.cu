@@ -387,6 +387,7 @@ struct AggArgs {
   // sources are ascending, so that is a contiguous run of every 32-edge group);
   // accumulate adds to the partials of the previous pass
   int pass = 0, passes = 1;  // pass p covers sources [S p / passes, S (p+1) / passes)
+  int64_t S_max = 0;         // host side: bound on the block's sources (the profiler's row count)
 };
 
 template <int OP, int NV>
@@ -394,7 +395,6 @@ template <int OP, int NV>
 #define OB_AGG_MINB_WIDE 1  // k_agg CTAs per SM for rows wider than 128 columns (NV = 2, 4)
 #endif
 __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WIDE)) k_agg(AggArgs a) {
-  pdl_wait();
   using AT = typename std::conditional<(OP == kOpDSum || OP == kOpMom2), double, float>::type;
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   pdl_wait();
@@ -416,7 +416,6 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
   __shared__ const float* c_row[kAggWarps][32];  // delta mode: the group's kept edges, compacted
   __shared__ float c_w[kAggWarps][32];
   const int wib = threadIdx.x >> 5;
-  int64_t kept = 0;  // delta mode: rows this warp gathered (for the profiler's byte count)
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = __ldg(a.item_dst + it);
     const int64_t j = it - a.item_ptr[i];
@@ -461,7 +460,6 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
       int first = __ffs(inb) - 1;
       const int cnt = __popc(inb);
       if (d_lo) {
-        kept += cnt;
         if (in_l) {
           const int slot = __popc(inb & ((1u << lane) - 1u));
           c_row[wib][slot] = r_l;
@@ -542,8 +540,52 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
         if (col + t < a.width) out[col + t] = a.pass > 0 ? out[col + t] + acc[q][t] : acc[q][t];
     }
   }
-  if (d_lo && lane == 0 && kept && blockIdx.y == 0)
-    atomicAdd((unsigned long long*)&const_cast<BlockCounters*>(a.cnt)->gathered, (unsigned long long)kept);
+}
+
+// Profiler only (launched after a stored-aggregate or delta k_agg, outside its events):
+// the rows that launch loaded -- row loads (one per kept edge) into cnt->gathered and
+// distinct rows into cnt->uniq.  Bit 2s + 1 marks source s's delta row, bit 2s its row.
+__global__ void k_prof_rows(AggArgs a, uint32_t* bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t items = a.cnt->items;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float* d_lo = a.dprev;
+  const float* d_hi = a.dprev ? a.dprev + (*a.dT) * a.dld : nullptr;
+  unsigned long long loads = 0;
+  for (int64_t it = gw; it < items; it += nw) {
+    const int64_t i = a.item_dst[it];
+    int64_t e0 = a.dst_ptr[i] + (it - a.item_ptr[i]) * kAggChunk;
+    const int64_t e1 = min(e0 + kAggChunk, a.dst_ptr[i + 1]);
+    int64_t csr_end = e0;
+    if (a.skip_indeg) {
+      const int64_t v = a.skip_dst_ids[i];
+      const int64_t ce = v < a.skip_N ? a.dst_ptr[i] + (int64_t)a.skip_indeg[v] : a.dst_ptr[i];
+      if (d_lo) csr_end = ce;
+      else e0 = max(e0, ce);
+    }
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const int32_t src = a.edge_src[e];
+      int64_t bit = 2 * (int64_t)src;
+      if (d_lo && e < csr_end) {
+        const float* r = a.x.row(src);
+        if (r < d_lo || r >= d_hi) continue;
+        bit += 1;
+      }
+      ++loads;
+      atomicOr(bits + (bit >> 5), 1u << (bit & 31));
+    }
+  }
+  for (int o = 16; o; o >>= 1) loads += __shfl_xor_sync(0xffffffffu, loads, o);
+  if (lane == 0 && loads) atomicAdd((unsigned long long*)&const_cast<BlockCounters*>(a.cnt)->gathered, loads);
+}
+
+__global__ void k_prof_popc(const uint32_t* bits, int64_t words, const BlockCounters* cnt) {
+  unsigned long long n = 0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+    n += __popc(bits[w]);
+  for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd((unsigned long long*)&const_cast<BlockCounters*>(cnt)->uniq, n);
 }
 
 __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
@@ -652,6 +694,15 @@ static void launch_agg(cudaStream_t s, const AggArgs& a0, int64_t items_max, int
   // block counters do not size, so the profiler counts its edge list and partials only
   // (K = -2: delta launch -- edge list, the recomputed rows (<= D) and the partials)
   prof_end(s, pa, kProfAgg, a0.cnt, a0.width, a0.pw, a0.dprev ? -2 : (a0.skip_indeg ? -1 : 0), 0, 0);
+  if (pa && a0.skip_indeg && a0.S_max > 0) {  // count the rows it loaded (profiler only, its own class)
+    cudaEvent_t pc = prof_begin(s);
+    const int64_t words = (2 * a0.S_max + 31) / 32;
+    uint32_t* bits = g_prof->bits(words, s);
+    k_prof_rows<<<grid_for(items_max, 8, kNumSMs * 16), 256, 0, s>>>(a0, bits);
+    k_prof_popc<<<grid_for(words, 256, kNumSMs * 4), 256, 0, s>>>(bits, words, a0.cnt);
+    OB_CUDA(cudaGetLastError());
+    prof_end(s, pc, kProfCount, nullptr, 0, 0, 0, 0, 0);
+  }
 }
 
 static void finalize(cudaStream_t s, const FinArgs& f, int64_t D_max, int64_t items_max) {
@@ -705,6 +756,7 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   const int64_t ld_out = ld4(outd);
   AggArgs a{};
   a.cnt = r.cnt;
+  a.S_max = r.S_max;
   a.dst_ptr = r.dst_ptr;
   a.item_ptr = r.item_ptr;
   a.item_dst = r.item_dst;
@@ -1058,6 +1110,7 @@ void cgp_local_partial(cudaStream_t s, const LayerDev& L, const LayerRun& r, con
   const int64_t ld_out = ld4(outd);
   AggArgs a{};
   a.cnt = r.cnt;
+  a.S_max = r.S_max;
   a.dst_ptr = r.dst_ptr;
   a.item_ptr = r.item_ptr;
   a.item_dst = r.item_dst;

@@ -4,6 +4,7 @@
 // the block counters they ran over are snapshotted into pinned memory at the
 // end of each request so the algorithmic bytes of every launch can be
 // computed after the fact without a host round trip inside the request.
+#include <algorithm>
 #include <cstdlib>
 
 #include "ob_engine.h"
@@ -46,6 +47,16 @@ void Profiler::request_end(cudaStream_t s) {
   for (auto& p : pending)
     OB_CUDA(cudaMemcpyAsync(pinned + p.second, p.first, sizeof(BlockCounters), cudaMemcpyDeviceToHost, s));
   pending.clear();
+}
+
+uint32_t* Profiler::bits(int64_t words, cudaStream_t s) {
+  if (words > rowbits_words) {
+    if (rowbits) OB_CUDA(cudaFree(rowbits));
+    rowbits_words = std::max<int64_t>(words, 2 * rowbits_words);
+    OB_CUDA(cudaMalloc(&rowbits, rowbits_words * 4));
+  }
+  OB_CUDA(cudaMemsetAsync(rowbits, 0, words * 4, s));
+  return rowbits;
 }
 
 void Profiler::prime(size_t events) {
