@@ -56,6 +56,13 @@ extern int64_t g_launches;
 // the attribute off.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool pdl_enabled();
+// programmatic dependent launch on every kernel (OB_NO_PDL=1 turns it off)
+inline int launch_attrs(cudaLaunchAttribute* at) {
+  if (!pdl_enabled()) return 0;
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  return 1;
+}
 template <class... KArgs, class... Args>
 inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
@@ -64,10 +71,8 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = launch_attrs(at);
   OB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
   OB_LAUNCHED();
 }

@@ -18,6 +18,8 @@
 // and the ~10^5 tiny candidate slots alike.  Everything runs off device-side
 // counts.
 #include <cstdlib>
+#include <cooperative_groups.h>
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "ob_engine.h"
@@ -768,6 +770,182 @@ struct SelTotal {
 };
 
 // ---------------------------------------------------------------------------
+// 2d. The whole top-k in one launch of one 16-CTA thread-block cluster: the budget
+// (policy.py:127), the eight 8-bit radix-select rounds over the fp64 score bits and
+// the ordered compaction (ties to the lowest ids, policy.py:131).  Each CTA keeps its
+// contiguous chunk of the keys in shared memory; a round's digit histograms are summed
+// across the cluster through distributed shared memory (every CTA reads all 16 and
+// takes the same decision), one cluster barrier per round.  Replaces k_budget, the
+// eight k_sel_round launches and the compaction scan whenever |R| fits the cluster's
+// shared memory (16 x 24576 keys).
+// ---------------------------------------------------------------------------
+constexpr int kSelCl = 16;
+constexpr int kSelClThreads = 512;
+constexpr int kSelClKeys = 24576;  // keys per CTA (192 KB of shared memory)
+constexpr int64_t kSelClSoloEdges = 1 << 18;  // single-lane engines: requests up to this many edges
+
+__global__ void __launch_bounds__(kSelClThreads, 1)
+    k_select_cluster(const uint64_t* __restrict__ key, const int32_t* __restrict__ cand_ids, ReqCounters* rc,
+                     double gamma, int32_t* targets, int32_t* tpos) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  using Scan = cub::BlockScan<unsigned long long, kSelClThreads>;
+  using Red = cub::BlockReduce<unsigned long long, kSelClThreads>;
+  extern __shared__ uint64_t sk[];
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Red::TempStorage red;
+  } tmp;
+  __shared__ uint32_t hist[2][256];
+  __shared__ int64_t wsum[8];
+  __shared__ uint64_t s_pre, s_msk;
+  __shared__ int64_t s_krem, s_take;
+  __shared__ unsigned long long s_tot;  // this CTA's (above << 32 | equal) counts
+  pdl_wait();
+  const int t = threadIdx.x, lane = t & 31;
+  const int64_t R = rc->R;
+  const int64_t b = (int64_t)floor(gamma * (double)R);  // int(np.floor(gamma * m)): one fp64 multiply
+  const int rank = (int)cl.block_rank();
+  const int64_t chunk = (R + kSelCl - 1) / kSelCl;
+  const int64_t c0 = min(R, (int64_t)rank * chunk), c1 = min(R, c0 + chunk);
+  const int n = (int)(c1 - c0);
+  for (int i = t; i < n; i += kSelClThreads) sk[i] = key[c0 + i];
+  if (t < 256) hist[0][t] = hist[1][t] = 0;
+  if (t == 0) {
+    s_pre = 0;
+    s_msk = 0;
+    s_krem = b;
+    s_take = 0;
+  }
+  __syncthreads();
+  const bool active = b > 0 && b < R;
+  if (active) {
+    for (int r = 0; r < 8; ++r) {
+      const int shift = 56 - 8 * r, buf = r & 1;
+      const uint64_t pre = s_pre, msk = s_msk;
+      for (int base = 0; base < n; base += kSelClThreads) {  // warp-uniform trip count
+        const int i = base + t;
+        const uint64_t k = i < n ? sk[i] : 0;
+        const bool in = i < n && (k & msk) == pre;
+        const int d = (int)((k >> shift) & 255);
+        const unsigned peers = __match_any_sync(0xffffffffu, in ? d : 256 + lane);
+        if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[buf][d], (uint32_t)__popc(peers));
+      }
+      cl.sync();  // every CTA's histogram of this round is complete and visible
+      int64_t c = 0, incl = 0;
+      if (t < 256) {
+        const int d = 255 - t;  // scan from the top digit down
+        for (int q = 0; q < kSelCl; ++q) c += cl.map_shared_rank(&hist[buf][0], q)[d];
+        incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[t >> 5] = incl;
+      }
+      if (t < 256) hist[buf ^ 1][t] = 0;  // the next round's buffer (its last readers passed this barrier)
+      __syncthreads();
+      if (t < 256) {
+        int64_t excl = incl - c;
+        for (int wq = 0; wq < (t >> 5); ++wq) excl += wsum[wq];
+        const int64_t krem = s_krem;
+        if (excl < krem && krem <= excl + c) {
+          const int d = 255 - t;
+          s_pre = pre | ((uint64_t)d << shift);
+          s_msk = msk | ((uint64_t)255 << shift);
+          s_krem = krem - excl;
+          if (shift == 0) s_take = krem - excl;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ordered compaction: c is selected when above the threshold, or equal to it with fewer
+  // than take equal keys before it; its position is (# above before) + min(# equal before, take)
+  const uint64_t thr = s_pre;
+  const int64_t take = s_take;
+  auto flags = [&](int i) -> unsigned long long {
+    if (i >= n || b <= 0) return 0ull;
+    if (b >= R) return 1ull << 32;
+    const uint64_t k = sk[i];
+    return k > thr ? (1ull << 32) : (k == thr ? 1ull : 0ull);
+  };
+  unsigned long long mine = 0;
+  for (int i = t; i < n; i += kSelClThreads) mine += flags(i);
+  const unsigned long long tot = Red(tmp.red).Sum(mine);
+  if (t == 0) s_tot = tot;
+  cl.sync();  // every CTA's totals are visible
+  unsigned long long basep = 0, allp = 0;
+  if (t == 0) {
+    for (int q = 0; q < kSelCl; ++q) {
+      const unsigned long long v = *cl.map_shared_rank(&s_tot, q);
+      if (q < rank) basep += v;
+      allp += v;
+    }
+    if (rank == 0) {
+      const int64_t above = (int64_t)(allp >> 32), eq = (int64_t)(allp & 0xffffffffu);
+      rc->budget = b;
+      rc->sel_prefix = thr;
+      rc->sel_eq_take = take;
+      rc->T = above + (eq < take ? eq : take);
+    }
+  }
+  cl.sync();  // every remote read of s_tot is done before it is reused (and before any CTA exits)
+  if (t == 0) s_tot = basep;  // this CTA's base counts
+  __syncthreads();
+  unsigned long long run = s_tot;
+  for (int base = 0; base < n; base += kSelClThreads) {
+    const int i = base + t;
+    const unsigned long long f = flags(i);
+    unsigned long long ex, tile;
+    Scan(tmp.scan).ExclusiveSum(f, ex, tile);
+    const unsigned long long p = run + ex;
+    const int64_t above_b = (int64_t)(p >> 32), eq_b = (int64_t)(p & 0xffffffffu);
+    const bool sel = (f >> 32) || ((f & 1ull) && eq_b < take);
+    if (sel) {
+      const int64_t pos = above_b + (eq_b < take ? eq_b : take);
+      targets[pos] = cand_ids[c0 + i];
+      tpos[c0 + i] = (int32_t)pos;
+    }
+    run += tile;
+    __syncthreads();  // tmp.scan reuse
+  }
+}
+
+static bool select_cluster_ok() {
+  static const bool ok = [] {
+    const char* v = std::getenv("OB_NO_CLUSTER_SELECT");
+    if (v && v[0] && v[0] != '0') return false;
+    if (cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kSelClKeys * sizeof(uint64_t))) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  }();
+  return ok;
+}
+
+static void launch_select_cluster(cudaStream_t s, const uint64_t* key, const int32_t* cand_ids, ReqCounters* rc,
+                                  double gamma, int32_t* targets, int32_t* tpos) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kSelCl);
+  cfg.blockDim = dim3(kSelClThreads);
+  cfg.dynamicSmemBytes = kSelClKeys * sizeof(uint64_t);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kSelCl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1 + launch_attrs(at + 1);
+  OB_CUDA(cudaLaunchKernelEx(&cfg, k_select_cluster, key, cand_ids, rc, gamma, targets, tpos));
+  OB_LAUNCHED();
+}
+
+// ---------------------------------------------------------------------------
 // 3. request CSR order: stable LSD radix sort of the packed keys, 8-bit digits,
 //    4096-key tiles.  Per pass: digit counts per tile (digit-major), one scan,
 //    then a stable scatter -- keys are ranked inside the tile warp by warp
@@ -1125,6 +1303,14 @@ void stage_select(Engine& e, RequestWs& w) {
     ip.P = 1;
     ip.part[0] = w.is_part;
     launch_score_is(e, w, ip);
+  }
+  // the cluster needs 16 SMs of one GPC at once: with one lane and a long request-index sort
+  // on the side stream (whose CTAs fill the SMs) it waits for them (cfg2: p50 0.76 -> 0.80 ms),
+  // so that case keeps the multi-launch rounds, which slot into whatever SMs free up
+  const bool cluster = e.nlanes > 1 || w.m <= kSelClSoloEdges;
+  if (e.cfg.policy != OB_POLICY_RANDOM && cluster && r_max <= (int64_t)kSelCl * kSelClKeys && select_cluster_ok()) {
+    launch_select_cluster(s, w.cand_key, w.cand_ids, w.rc, e.cfg.gamma, w.targets, w.cand_tpos);
+    return;
   }
   launch_pdl(k_budget, dim3(1), dim3(256), 0, s, w.rc, e.cfg.gamma, w.sel_hist);
   if (e.cfg.policy == OB_POLICY_RANDOM) {
