@@ -41,6 +41,10 @@ import time
 
 import numpy as np
 
+# before any CUDA context: 32 hardware work queues for the engine's per-lane streams
+# (paper_2501_08547_b200/__init__.py sets the same default)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -10,4 +10,13 @@ host-side data types live in ``graphstore``, ``models``, ``compgraph`` and
 ``workload`` exactly where the reference keeps them.
 """
 
+import os as _os
+
+# An engine drives up to 3 streams per request lane (main, request-index sort, query rows)
+# plus the caller's; with CUDA's default 8 hardware work queues, streams share queues and a
+# CGP exchange kernel spinning on a peer's flag stalls unrelated work queued behind it
+# (measured: cfg2 CGP P = 4 with 4 lanes 0.63 M -> 2.26 M queries/s with 32 queues).  Only
+# takes effect if no CUDA context exists yet; C-ABI users set it themselves (INTEGRATION.md).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 __version__ = "0.1.0"

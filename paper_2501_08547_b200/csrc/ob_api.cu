@@ -35,6 +35,9 @@ Engine::~Engine() {
       if (ev_) cudaEventDestroy(ev_);
     if (L.stream) cudaStreamDestroy(L.stream);
     if (L.side) cudaStreamDestroy(L.side);
+    if (L.qside) cudaStreamDestroy(L.qside);
+    for (cudaEvent_t ev_ : {L.qfork_ev, L.qjoin_ev})
+      if (ev_) cudaEventDestroy(ev_);
   }
   if (lane_fork_ev) cudaEventDestroy(lane_fork_ev);
   drop_graphs();
@@ -49,6 +52,9 @@ Engine::~Engine() {
     if (ev_) cudaEventDestroy(ev_);
   if (own_stream && stream) cudaStreamDestroy(stream);
   if (side) cudaStreamDestroy(side);
+  if (qside) cudaStreamDestroy(qside);
+  for (cudaEvent_t ev_ : {qfork_ev, qjoin_ev})
+    if (ev_) cudaEventDestroy(ev_);
   if (fork_ev) cudaEventDestroy(fork_ev);
   if (join_ev) cudaEventDestroy(join_ev);
   if (csr_ev) cudaEventDestroy(csr_ev);
@@ -94,6 +100,9 @@ static void swap_lane(Engine& e, Lane& L) {
   std::swap(e.graphs, L.graphs);
   std::swap(e.stream, L.stream);
   std::swap(e.side, L.side);
+  std::swap(e.qside, L.qside);
+  std::swap(e.qfork_ev, L.qfork_ev);
+  std::swap(e.qjoin_ev, L.qjoin_ev);
   std::swap(e.fork_ev, L.fork_ev);
   std::swap(e.join_ev, L.join_ev);
   std::swap(e.csr_ev, L.csr_ev);
@@ -428,6 +437,26 @@ static void enqueue_stages(Engine& e, float* d_out) {
     serve_cgp(e, d_out);  // marks ev[1] between build and layers
     return;
   }
+  // the layer-1 query rows need only the request's features: third stream from the start
+  // (OB_QROWS_SERIAL=1: on the main stream after the selection, as before)
+  static const bool qserial = [] {
+    const char* v = std::getenv("OB_QROWS_SERIAL");
+    return v && v[0] && v[0] != '0';
+  }();
+  const bool qs = !qserial;
+  if (qs) {
+    OB_CUDA(cudaEventRecord(e.qfork_ev, s));
+    OB_CUDA(cudaStreamWaitEvent(e.qside, e.qfork_ev, 0));
+    e.stream = e.qside;
+    try {
+      stage_query_rows(e, w);
+    } catch (...) {
+      e.stream = s;
+      throw;
+    }
+    e.stream = s;
+    OB_CUDA(cudaEventRecord(e.qjoin_ev, e.qside));
+  }
   cudaEvent_t p0 = prof_begin(s);
   stage_request_prep(e, w, srpe);
   // the request-index sort (side stream) and the top-k selection (main stream)
@@ -457,7 +486,7 @@ static void enqueue_stages(Engine& e, float* d_out) {
   if (srpe) stage_select(e, w);
   prof_end(s, p0, kProfSelect, nullptr, 0, 0, 0, 0, 0);
   // query rows of layer 1 (padding, stored-transform rows) while the request index sorts
-  stage_query_rows(e, w);
+  if (!qs) stage_query_rows(e, w);
   OB_CUDA(cudaStreamWaitEvent(s, e.csr_ev, 0));
   p0 = prof_begin(s);
   if (srpe) build_mid_block(e, w);
@@ -465,6 +494,7 @@ static void enqueue_stages(Engine& e, float* d_out) {
   prof_end(s, p0, kProfBuild, nullptr, 0, 0, 0, 0, 0);
   OB_CUDA(cudaEventRecord(e.join_ev, e.side));
   OB_CUDA(cudaStreamWaitEvent(s, e.join_ev, 0));
+  if (qs) OB_CUDA(cudaStreamWaitEvent(s, e.qjoin_ev, 0));
   record_mark(e.ev[1], s);
   stage_forward(e, w, d_out);
 }
@@ -763,7 +793,7 @@ static void load_model(Engine& e, int k, const ob_layer* layers, const float* co
 __global__ void k_src_degree(const int32_t* __restrict__ src_ids, const BlockCounters* cnt, int64_t N,
                              const int32_t* indeg, const int32_t* qdeg, int64_t* out) {
   pdl_wait();
-  const int64_t S = cnt->S;
+  const int64_t S = ld_state(&cnt->S);
   OB_GRID_STRIDE(s, S) {
     int64_t g = src_ids[s];
     out[s] = g < N ? indeg[g] : qdeg[g - N];
@@ -930,6 +960,9 @@ int ob_engine_create(const ob_config* cfg, ob_engine** out) {
     }
     for (auto& ev_ : e.ev) OB_CUDA(cudaEventCreate(&ev_));
     OB_CUDA(cudaStreamCreateWithFlags(&e.side, cudaStreamNonBlocking));
+    OB_CUDA(cudaStreamCreateWithFlags(&e.qside, cudaStreamNonBlocking));
+    OB_CUDA(cudaEventCreateWithFlags(&e.qfork_ev, cudaEventDisableTiming));
+    OB_CUDA(cudaEventCreateWithFlags(&e.qjoin_ev, cudaEventDisableTiming));
     OB_CUDA(cudaEventCreateWithFlags(&e.fork_ev, cudaEventDisableTiming));
     OB_CUDA(cudaEventCreateWithFlags(&e.join_ev, cudaEventDisableTiming));
     OB_CUDA(cudaEventCreateWithFlags(&e.csr_ev, cudaEventDisableTiming));
@@ -1357,6 +1390,9 @@ int ob_set_lanes(ob_engine* h, int32_t n) {
       Lane& L = e.lanes.back();
       OB_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
       OB_CUDA(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking));
+      OB_CUDA(cudaStreamCreateWithFlags(&L.qside, cudaStreamNonBlocking));
+      OB_CUDA(cudaEventCreateWithFlags(&L.qfork_ev, cudaEventDisableTiming));
+      OB_CUDA(cudaEventCreateWithFlags(&L.qjoin_ev, cudaEventDisableTiming));
       for (auto& ev_ : L.ev) OB_CUDA(cudaEventCreate(&ev_));
       for (cudaEvent_t* ev_ : {&L.fork_ev, &L.join_ev, &L.csr_ev, &L.done_ev})
         OB_CUDA(cudaEventCreateWithFlags(ev_, cudaEventDisableTiming));

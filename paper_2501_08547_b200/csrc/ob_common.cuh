@@ -84,8 +84,15 @@ inline int grid_for(int64_t work, int per_cta, int cap = kPersistCTAs) {
   return (int)g;
 }
 
+// Request state that earlier kernels of the same request update (counters, selection state)
+// is read past L1 (ld.global.cg): an SM's L1 may still hold a sector cached by a CTA of a
+// concurrent kernel from the request's other streams after the writer's update reached L2.
+__device__ __forceinline__ int64_t ld_state(const int64_t* p) { return __ldcg(reinterpret_cast<const long long*>(p)); }
+__device__ __forceinline__ uint64_t ld_state(const uint64_t* p) {
+  return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
 __device__ __forceinline__ int64_t dev_count(const int64_t* p, int64_t fallback) {
-  return p ? *p : fallback;
+  return p ? ld_state(p) : fallback;
 }
 
 // ---------------------------------------------------------------------------

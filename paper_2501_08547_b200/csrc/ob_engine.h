@@ -718,8 +718,9 @@ struct Lane {
   ScanScratch scan;
   ReqParams* params = nullptr;
   std::vector<RequestGraph> graphs;
-  cudaStream_t stream = nullptr, side = nullptr;
+  cudaStream_t stream = nullptr, side = nullptr, qside = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, csr_ev = nullptr, done_ev = nullptr;
+  cudaEvent_t qfork_ev = nullptr, qjoin_ev = nullptr;
   cudaEvent_t ev[6] = {};
   CgpLaneState cg;
 };
@@ -733,6 +734,10 @@ struct Engine {
   // top-k selection); forked and joined with events, so captured graphs branch
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, csr_ev = nullptr;
+  // third stream: the layer-1 query rows (padding, stored-transform GEMMs) need only the
+  // request's features, so they run beside preparation and selection
+  cudaStream_t qside = nullptr;
+  cudaEvent_t qfork_ev = nullptr, qjoin_ev = nullptr;
   GraphDev g;
   std::vector<LayerDev> layers;
   std::vector<float*> pe;        // per stored layer, N x ld4(dim)

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // the set-up above (barriers, TMEM allocation) overlaps the previous kernel's tail;
   // everything below may read its results (the row count M is one of them)
   pdl_wait();
-  const int64_t M = *g.M_dev;
+  const int64_t M = ld_state(g.M_dev);
   const int64_t tiles = (M + kTcBM - 1) / kTcBM;
   // work units: (row tile, column slab); small-M GEMMs split the columns across
   // CTAs (nslab > 1) so more SMs share the tile's MMAs and epilogue

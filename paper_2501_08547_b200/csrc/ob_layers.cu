@@ -75,8 +75,8 @@ __device__ __forceinline__ int bind_row(const BindCtx& c, int64_t T, int64_t s, 
 __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restrict__ src_ids, const float** rowp,
                           float* gscale, uint8_t* kind_out, int32_t* pe_layer_out) {
   pdl_wait();
-  const int64_t S = cnt->S;
-  const int64_t T = c.T_dev ? *c.T_dev : 0;
+  const int64_t S = ld_state(&cnt->S);
+  const int64_t T = c.T_dev ? ld_state(c.T_dev) : 0;
   int64_t nfeat = 0, npe = 0;
   OB_GRID_STRIDE(s, S) {
     int64_t g = src_ids[s];
@@ -310,7 +310,7 @@ __device__ __forceinline__ void fin_cols(const FinArgs& a, int64_t i, int64_t cn
   }
   const float* dpe = nullptr;
   float* drow = nullptr;
-  if (a.dbuf && i < *a.dT) {
+  if (a.dbuf && i < ld_state(a.dT)) {
     const int64_t ld = (a.width + 3) & ~3;
     dpe = a.dpe + (int64_t)a.self_dst_ids[i] * ld + c4;
     drow = a.dbuf + i * ld + c4;
@@ -399,19 +399,19 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   pdl_wait();
   const int lane = threadIdx.x & 31;
-  const int64_t items = a.cnt->items;
+  const int64_t items = ld_state(&a.cnt->items);
   const int col0 = blockIdx.y * (32 * 4 * NV);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int32_t src_lo = 0, src_hi = 0x7fffffff;
   if (a.passes > 1) {
-    const int64_t S = a.cnt->S;
+    const int64_t S = ld_state(&a.cnt->S);
     src_lo = (int32_t)(S * a.pass / a.passes);
     src_hi = a.pass + 1 == a.passes ? 0x7fffffff : (int32_t)(S * (a.pass + 1) / a.passes);
   }
   // delta mode: recomputed rows are prev[0, T); their delta rows sit at the same offset in dbuf
   const float* d_lo = a.dprev;
-  const float* d_hi = a.dprev ? a.dprev + (*a.dT) * a.dld : nullptr;
+  const float* d_hi = a.dprev ? a.dprev + ld_state(a.dT) * a.dld : nullptr;
   const ptrdiff_t d_shift = a.dprev ? a.dbuf - a.dprev : 0;
   __shared__ const float* c_row[kAggWarps][32];  // delta mode: the group's kept edges, compacted
   __shared__ float c_w[kAggWarps][32];
@@ -547,11 +547,11 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
 // distinct rows into cnt->uniq.  Bit 2s + 1 marks source s's delta row, bit 2s its row.
 __global__ void k_prof_rows(AggArgs a, uint32_t* bits) {
   const int lane = threadIdx.x & 31;
-  const int64_t items = a.cnt->items;
+  const int64_t items = ld_state(&a.cnt->items);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const float* d_lo = a.dprev;
-  const float* d_hi = a.dprev ? a.dprev + (*a.dT) * a.dld : nullptr;
+  const float* d_hi = a.dprev ? a.dprev + ld_state(a.dT) * a.dld : nullptr;
   unsigned long long loads = 0;
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = a.item_dst[it];
@@ -590,7 +590,7 @@ __global__ void k_prof_popc(const uint32_t* bits, int64_t words, const BlockCoun
 
 __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
   pdl_wait();
-  const int64_t G = a.cnt->groups;
+  const int64_t G = ld_state(&a.cnt->groups);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = gw; g < G; g += nw) reduce_group<false>(a, g);
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
 #endif
 __global__ void __launch_bounds__(256, OB_FIN_MINB) k_finalize(FinArgs a) {
   pdl_wait();
-  const int64_t D = a.cnt->D;
+  const int64_t D = ld_state(&a.cnt->D);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = gw; i < D; i += nw) finalize_dst(a, i);
@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(256) k_finalize_moments(const BlockCounters* c
                                                           const int64_t* item_ptr, const double* partial, int width,
                                                           int phase, int n, double* mean, float* agg, int64_t ldo) {
   pdl_wait();
-  const int64_t D = cnt_->D;
+  const int64_t D = ld_state(&cnt_->D);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(256) k_finalize_moments(const BlockCounters* c
 __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* self, int w,
                               const float* __restrict__ av, float* out) {
   pdl_wait();
-  const int64_t M = *M_dev;
+  const int64_t M = ld_state(M_dev);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -943,7 +943,7 @@ int cgp_partial_width(const LayerDev& L) {
 // (max logit, sum exp, sum exp*z); count = local in-edges
 __global__ void __launch_bounds__(256) k_local_raw(FinArgs a, float* lp, int64_t ldp, float* lcnt) {
   pdl_wait();
-  const int64_t D = a.cnt->D;
+  const int64_t D = ld_state(&a.cnt->D);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -992,7 +992,7 @@ __global__ void __launch_bounds__(256) k_local_raw_f64(const BlockCounters* cnt_
                                                        const int64_t* item_ptr, const double* partial, int width,
                                                        double* lp, int64_t ldp, float* lcnt) {
   pdl_wait();
-  const int64_t D = cnt_->D;
+  const int64_t D = ld_state(&cnt_->D);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1024,7 +1024,7 @@ struct MergeArgs {
 // softmax rescale, empty destinations aggregate to zero
 __global__ void __launch_bounds__(256) k_merge_parts(MergeArgs m) {
   pdl_wait();
-  const int64_t D = *m.D_dev;
+  const int64_t D = ld_state(m.D_dev);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(256) k_merge_moments(int P, PartPtrs parts, in
                                                        OwnerFilter own, int width, int phase, int n, double* mean,
                                                        float* agg, int64_t ldo) {
   pdl_wait();
-  const int64_t D = *D_dev;
+  const int64_t D = ld_state(D_dev);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1298,7 +1298,7 @@ __global__ void k_pad_rows(const ReqParams* rp, int64_t rows, int w, float* dst,
 __global__ void k_delta_rows(const int64_t* T_dev, const int32_t* __restrict__ targets, const float* __restrict__ prev,
                              const float* __restrict__ pe, int64_t ld, float* dbuf) {
   pdl_wait();
-  const int64_t n = (*T_dev) * ld;
+  const int64_t n = ld_state(T_dev) * ld;
   OB_GRID_STRIDE(t, n) {
     const int64_t i = t / ld;
     const int64_t c = t - i * ld;

@@ -112,6 +112,21 @@ def test_cfg2_lanes_and_source_range_passes(cfg2):
         eng.set_lanes(1)
 
 
+def test_cfg2_repeated_serves_identical(cfg2):
+    """Serving the two requests alternately, many times: every serve equals the first bit for bit.
+
+    Guards the cross-kernel request state (selection rounds, counters): a read served from a
+    stale L1 sector once in ~500 serves picked the rank-1300 key instead of the rank-21128 one
+    before those reads went through L2 (ob_common.cuh ld_state)."""
+    eng, reqs = cfg2["eng"], cfg2["reqs"]
+    first = [eng.serve(r) for r in reqs]
+    for i in range(800):
+        emb, bd = eng.serve(reqs[i % 2])
+        e0, b0 = first[i % 2]
+        assert bd.num_targets == b0.num_targets, (i, bd.num_targets, b0.num_targets)
+        assert np.array_equal(emb, e0), i
+
+
 def test_cfg2_precompute_rows(cfg2):
     """PE rows on a sample of nodes: layer l applied on the host to the GPU's layer l-1 rows."""
     from oracle import layers as OL
