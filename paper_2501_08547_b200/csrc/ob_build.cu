@@ -43,9 +43,10 @@ __global__ void k_block_spans(const int32_t* __restrict__ dst_ids, const BlockCo
                               const uint32_t* cbits, const int64_t* cwpre, const int64_t* rq_ptr,
                               const ReqCounters* rc, SegSpans sp, int64_t* seg_len) {
   pdl_wait();
-  const int64_t D = ld_state(&cnt->D);
-  const int64_t R = ld_state(&rc->R);
-  const bool bad = ld_state(&rc->err) & (kErrRange | kErrNoQuery);
+  const CtaWords st = cta_ldv(&cnt->D, &rc->R, &rc->err);
+  const int64_t D = st.v[0];
+  const int64_t R = st.v[1];
+  const bool bad = st.v[2] & (kErrRange | kErrNoQuery);
   OB_GRID_STRIDE(i, D) {
     int64_t v = dst_ids[i];
     int64_t cs = 0, rs = 0;
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(1024) k_block_fill(const BlockCounters* cnt, c
                                                      uint32_t* sbits, int64_t words, uint32_t* part_bits) {
   pdl_wait();
   extern __shared__ uint32_t sbm[];
-  const int64_t items = ld_state(&cnt->items);
+  const int64_t items = cta_ld(&cnt->items);
   const int lane = threadIdx.x & 31;
   if (SMEM) {
     for (int64_t w = threadIdx.x; w < words; w += blockDim.x) sbm[w] = 0u;
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(128) k_sample_spans(const int32_t* __restrict_
                                                       const int32_t* __restrict__ rq_src, int fan, int layer,
                                                       uint64_t seed, int32_t* samp, int64_t* seg_len) {
   pdl_wait();
-  const int64_t D = ld_state(&cnt->D);
+  const int64_t D = cta_ld(&cnt->D);
   OB_GRID_STRIDE(i, D) {
     const int32_t cl = sp.cl[i], rl = sp.rl[i];
     const int64_t n = (int64_t)cl + rl;
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(256) k_expand_items(const BlockCounters* cnt, 
                                                       const int64_t* __restrict__ group_ptr, int32_t* item_dst,
                                                       int32_t* group_dst) {
   pdl_wait();
-  const int64_t D = ld_state(&cnt->D);
+  const int64_t D = cta_ld(&cnt->D);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -329,21 +330,21 @@ void expand_items(cudaStream_t s, const BlockCounters* cnt, int64_t D_max, const
 
 __global__ void k_mark_ids(const int32_t* __restrict__ ids, const BlockCounters* cnt, uint32_t* sbits) {
   pdl_wait();
-  const int64_t D = ld_state(&cnt->D);
+  const int64_t D = cta_ld(&cnt->D);
   OB_GRID_STRIDE(i, D) bm_set(sbits, ids[i]);
 }
 
 __global__ void k_relabel(const BlockCounters* cnt, const int32_t* __restrict__ src_global, const uint32_t* sbits,
                           const int64_t* swpre, int32_t* edge_src) {
   pdl_wait();
-  const int64_t E = ld_state(&cnt->E);
+  const int64_t E = cta_ld(&cnt->E);
   OB_GRID_STRIDE(e, E) edge_src[e] = (int32_t)bm_rank(sbits, swpre, src_global[e]);
 }
 
 __global__ void k_self_rows(const BlockCounters* cnt, const int32_t* __restrict__ dst_ids, const uint32_t* sbits,
                             const int64_t* swpre, int32_t* self_src) {
   pdl_wait();
-  const int64_t D = ld_state(&cnt->D);
+  const int64_t D = cta_ld(&cnt->D);
   OB_GRID_STRIDE(i, D) self_src[i] = (int32_t)bm_rank(sbits, swpre, dst_ids[i]);
 }
 
@@ -351,7 +352,7 @@ __global__ void k_self_rows(const BlockCounters* cnt, const int32_t* __restrict_
 __global__ void k_mid_dst(const ReqCounters* rc, int64_t N, int B, const int32_t* targets, int32_t* dst_ids,
                           BlockCounters* cnt) {
   pdl_wait();
-  const int64_t T = ld_state(&rc->T), D = T + B;
+  const int64_t T = cta_ld(&rc->T), D = T + B;
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt->D = D;
   OB_GRID_STRIDE(i, D) dst_ids[i] = i < T ? targets[i] : (int32_t)(N + (i - T));
 }

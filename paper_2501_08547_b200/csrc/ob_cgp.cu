@@ -196,9 +196,10 @@ void cgp_localize_storage(Engine& e) {
 __global__ void k_filter_slice(const ReqParams* rp, int64_t N, int P, int r, const int32_t* __restrict__ owner,
                                const ReqCounters* rc, int64_t* out, int64_t* count) {
   pdl_wait();
-  if (ld_state(&rc->err) & (kErrRange | kErrNoQuery)) return;
+  const CtaWords st = cta_ldv(&rc->err, &rp->m);
+  if (st.v[0] & (kErrRange | kErrNoQuery)) return;
   const int64_t* __restrict__ edges = rp->edges;
-  const int64_t m = ld_state(&rp->m);
+  const int64_t m = st.v[1];
   OB_GRID_STRIDE(e, m) {
     const int64_t s = edges[2 * e];
     const int o = s >= N ? (int)((s - N) % P) : owner[s];
@@ -225,7 +226,8 @@ __global__ void k_dst_rows(const int32_t* __restrict__ dst_ids, const int64_t* D
                            const int64_t* T_dev, const int32_t* owner, int P, int rank, const float* zero,
                            const float** hvp) {
   pdl_wait();
-  const int64_t D = ld_state(D_dev), T = ld_state(T_dev);
+  const CtaWords st = cta_ldv(D_dev, T_dev);
+  const int64_t D = st.v[0], T = st.v[1];
   OB_GRID_STRIDE(i, D) {
     const int64_t g = dst_ids[i];
     bool mine = true;
@@ -242,7 +244,7 @@ __global__ void k_dst_rows(const int32_t* __restrict__ dst_ids, const int64_t* D
 __global__ void k_rowdot_ptr(const int64_t* M_dev, const float* const* rows, int w, const float* __restrict__ av,
                              float* out) {
   pdl_wait();
-  const int64_t M = ld_state(M_dev);
+  const int64_t M = cta_ld(M_dev);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -259,12 +261,12 @@ __global__ void k_rowdot_ptr(const int64_t* M_dev, const float* const* rows, int
 // global max so the triples can be summed (cgpexec.py:225-239)
 __global__ void k_sm_extract(const int64_t* D_dev, const float* lp, int64_t ldp, float* lmax) {
   pdl_wait();
-  const int64_t D = ld_state(D_dev);
+  const int64_t D = cta_ld(D_dev);
   OB_GRID_STRIDE(i, D) lmax[i] = lp[i * ldp + 1] > 0.f ? lp[i * ldp] : -INFINITY;
 }
 __global__ void k_sm_rescale(const int64_t* D_dev, float* lp, int64_t ldp, int w, const float* gmax) {
   pdl_wait();
-  const int64_t D = ld_state(D_dev);
+  const int64_t D = cta_ld(D_dev);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -282,7 +284,7 @@ __global__ void k_sm_rescale(const int64_t* D_dev, float* lp, int64_t ldp, int w
 }
 __global__ void k_sm_restore(const int64_t* D_dev, float* lp, int64_t ldp, const float* gmax) {
   pdl_wait();
-  const int64_t D = ld_state(D_dev);
+  const int64_t D = cta_ld(D_dev);
   OB_GRID_STRIDE(i, D) lp[i * ldp] = gmax[i];
 }
 
@@ -472,7 +474,7 @@ __global__ void k_x_done(XCtx x) {
 __global__ void k_x_gather_rows(XCtx x, size_t off, const int32_t* dst_ids, const int64_t* D_dev, int64_t D_fixed,
                                 int64_t N, const int32_t* owner, int esize, int64_t width_el, float* out) {
   pdl_wait();
-  const int64_t D = D_dev ? ld_state(D_dev) : D_fixed;
+  const int64_t D = D_dev ? cta_ld(D_dev) : D_fixed;
   const int64_t words = width_el * esize / 4;  // 4-byte words per row
   const int64_t n = D * words;
   OB_GRID_STRIDE(t, n) {

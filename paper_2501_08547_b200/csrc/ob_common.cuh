@@ -94,6 +94,37 @@ __device__ __forceinline__ uint64_t ld_state(const uint64_t* p) {
 __device__ __forceinline__ int64_t dev_count(const int64_t* p, int64_t fallback) {
   return p ? ld_state(p) : fallback;
 }
+// The same, one L2 read per CTA broadcast through shared memory: every thread of the CTA
+// must reach it (a per-thread ld.global.cg of one hot word from every warp of a large grid
+// queues thousands of requests on a single L2 line)
+__device__ __forceinline__ int64_t cta_ld(const int64_t* p) {
+  __shared__ int64_t s_cta_word;
+  __syncthreads();  // every thread has taken the previous broadcast
+  if (threadIdx.x == 0) s_cta_word = ld_state(p);
+  __syncthreads();
+  return s_cta_word;
+}
+__device__ __forceinline__ uint64_t cta_ld(const uint64_t* p) {
+  return (uint64_t)cta_ld(reinterpret_cast<const int64_t*>(p));
+}
+__device__ __forceinline__ int64_t cta_count(const int64_t* p, int64_t fallback) {
+  return p ? cta_ld(p) : fallback;
+}
+// Up to four words in one round trip (null pointers read as 0)
+struct CtaWords {
+  int64_t v[4];
+};
+__device__ __forceinline__ CtaWords cta_ldv(const void* p0, const void* p1, const void* p2 = nullptr,
+                                            const void* p3 = nullptr) {
+  __shared__ int64_t s_cta_words[4];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const void* p = threadIdx.x == 0 ? p0 : threadIdx.x == 1 ? p1 : threadIdx.x == 2 ? p2 : p3;
+    s_cta_words[threadIdx.x] = p ? ld_state(static_cast<const int64_t*>(p)) : 0;
+  }
+  __syncthreads();
+  return CtaWords{{s_cta_words[0], s_cta_words[1], s_cta_words[2], s_cta_words[3]}};
+}
 
 // ---------------------------------------------------------------------------
 // bitmap-rank set over [0, n_bits)
@@ -167,10 +198,35 @@ struct ScanTiles {
   T* incl;
 };
 
+// Load / Store functors may cache request state once per thread (prepare(), run after
+// pdl_wait on a per-thread copy); functors without it are used in place (no copy)
+template <class F, class = void>
+struct has_prepare : std::false_type {};
+template <class F>
+struct has_prepare<F, std::void_t<decltype(std::declval<F&>().prepare())>> : std::true_type {};
+
+template <class T, int ITEMS, class Load, class Store, class Total>
+__device__ __forceinline__ void scan_tiles(const Load& load, const Store& store, const Total& total,
+                                           const int64_t* n_dev, int64_t n_host, const ScanTiles<T>& st);
+
 template <class T, int ITEMS, class Load, class Store, class Total>
 __global__ void __launch_bounds__(kScanThreads, sizeof(T) == 8 ? OB_SCAN_MINB : 1) k_scan(Load load, Store store, Total total, const int64_t* n_dev,
                                                        int64_t n_host, ScanTiles<T> st) {
   pdl_wait();
+  if constexpr (has_prepare<Load>::value || has_prepare<Store>::value) {
+    Load l = load;
+    Store o = store;
+    if constexpr (has_prepare<Load>::value) l.prepare();
+    if constexpr (has_prepare<Store>::value) o.prepare();
+    scan_tiles<T, ITEMS>(l, o, total, n_dev, n_host, st);
+  } else {
+    scan_tiles<T, ITEMS>(load, store, total, n_dev, n_host, st);
+  }
+}
+
+template <class T, int ITEMS, class Load, class Store, class Total>
+__device__ __forceinline__ void scan_tiles(const Load& load, const Store& store, const Total& total,
+                                           const int64_t* n_dev, int64_t n_host, const ScanTiles<T>& st) {
   using BS = cub::BlockScan<T, kScanThreads>;
   using BX = cub::BlockExchange<T, kScanThreads, ITEMS>;
   // 8-byte values move warp-striped (coalesced loads and stores) and are
@@ -185,7 +241,7 @@ __global__ void __launch_bounds__(kScanThreads, sizeof(T) == 8 ? OB_SCAN_MINB : 
   } tmp;
   __shared__ int64_t s_tile;
   __shared__ T s_prefix;
-  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t n = cta_count(n_dev, n_host);
   const int64_t ntiles = (n + kTile - 1) / kTile;
   const int lane = threadIdx.x & 31;
   if (n <= 0) {
@@ -326,7 +382,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Load load, const i
   pdl_wait();
   using BR = cub::BlockReduce<int64_t, kScanThreads>;
   __shared__ typename BR::TempStorage tmp;
-  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t n = cta_count(n_dev, n_host);
   const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int64_t v = 0;
@@ -354,7 +410,7 @@ __global__ void __launch_bounds__(kScanThreads, OB_SCAN_MINB) k_scan_down(Load l
     typename BS::TempStorage scan;
     typename BX::TempStorage ex;
   } tmp;
-  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t n = cta_count(n_dev, n_host);
   const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
   if (n <= 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) total(0, 0);

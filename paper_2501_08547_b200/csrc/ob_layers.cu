@@ -75,8 +75,9 @@ __device__ __forceinline__ int bind_row(const BindCtx& c, int64_t T, int64_t s, 
 __global__ void k_resolve(BindCtx c, BlockCounters* cnt, const int32_t* __restrict__ src_ids, const float** rowp,
                           float* gscale, uint8_t* kind_out, int32_t* pe_layer_out) {
   pdl_wait();
-  const int64_t S = ld_state(&cnt->S);
-  const int64_t T = c.T_dev ? ld_state(c.T_dev) : 0;
+  const CtaWords st = cta_ldv(&cnt->S, c.T_dev);
+  const int64_t S = st.v[0];
+  const int64_t T = st.v[1];
   int64_t nfeat = 0, npe = 0;
   OB_GRID_STRIDE(s, S) {
     int64_t g = src_ids[s];
@@ -280,7 +281,7 @@ __device__ __forceinline__ void reduce_group(const FinArgs& a, int64_t g) {
 // the sum exp * z with its header (ms, den)): add the stored CSR part, normalise,
 // then the layer epilogue (activation, own-row update, the next layer's delta rows)
 __device__ __forceinline__ void fin_cols(const FinArgs& a, int64_t i, int64_t cnt, int c4, float4 v, float ms,
-                                         float den) {
+                                         float den, int64_t dT) {
   if (c4 >= a.width) return;
   const int mk = merge_kind(a.kind);
   const float* st = nullptr;
@@ -310,7 +311,7 @@ __device__ __forceinline__ void fin_cols(const FinArgs& a, int64_t i, int64_t cn
   }
   const float* dpe = nullptr;
   float* drow = nullptr;
-  if (a.dbuf && i < ld_state(a.dT)) {
+  if (a.dbuf && i < dT) {
     const int64_t ld = (a.width + 3) & ~3;
     dpe = a.dpe + (int64_t)a.self_dst_ids[i] * ld + c4;
     drow = a.dbuf + i * ld + c4;
@@ -333,7 +334,8 @@ __device__ __forceinline__ void fin_cols(const FinArgs& a, int64_t i, int64_t cn
 }
 
 // destination i: merge its items (or hub groups) in item order, then fin_cols
-__device__ __forceinline__ void finalize_dst(const FinArgs& a, int64_t i) {
+// dT: the delta-row count (*a.dT, read once per kernel)
+__device__ __forceinline__ void finalize_dst(const FinArgs& a, int64_t i, int64_t dT) {
   const int lane = threadIdx.x & 31;
   const int mk = merge_kind(a.kind);
   const int hdr = mk == kMergeSoftmax ? kSmHdr : 0;
@@ -349,7 +351,7 @@ __device__ __forceinline__ void finalize_dst(const FinArgs& a, int64_t i) {
   // (max, sum exp, sum exp*z) merge in item order (cgpexec.py:225-239)
   if (mk == kMergeSoftmax) sm_header<false>(part, a.pw, i0, i1, ms, den);
   for (int c4 = lane * 4; c4 < a.width; c4 += 128)
-    fin_cols(a, i, cnt, c4, merge_cols<false>(mk, part, a.pw, i0, i1, hdr, c4, ms), ms, den);
+    fin_cols(a, i, cnt, c4, merge_cols<false>(mk, part, a.pw, i0, i1, hdr, c4, ms), ms, den, dT);
 }
 
 // ---------------------------------------------------------------------------
@@ -399,19 +401,20 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
   constexpr int kU = NV == 1 ? 8 : 4;  // edges whose rows are in flight together
   pdl_wait();
   const int lane = threadIdx.x & 31;
-  const int64_t items = ld_state(&a.cnt->items);
+  const CtaWords st = cta_ldv(&a.cnt->items, a.passes > 1 ? &a.cnt->S : nullptr, a.dprev ? a.dT : nullptr);
+  const int64_t items = st.v[0];
   const int col0 = blockIdx.y * (32 * 4 * NV);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int32_t src_lo = 0, src_hi = 0x7fffffff;
   if (a.passes > 1) {
-    const int64_t S = ld_state(&a.cnt->S);
+    const int64_t S = st.v[1];
     src_lo = (int32_t)(S * a.pass / a.passes);
     src_hi = a.pass + 1 == a.passes ? 0x7fffffff : (int32_t)(S * (a.pass + 1) / a.passes);
   }
   // delta mode: recomputed rows are prev[0, T); their delta rows sit at the same offset in dbuf
   const float* d_lo = a.dprev;
-  const float* d_hi = a.dprev ? a.dprev + ld_state(a.dT) * a.dld : nullptr;
+  const float* d_hi = a.dprev ? a.dprev + st.v[2] * a.dld : nullptr;
   const ptrdiff_t d_shift = a.dprev ? a.dbuf - a.dprev : 0;
   __shared__ const float* c_row[kAggWarps][32];  // delta mode: the group's kept edges, compacted
   __shared__ float c_w[kAggWarps][32];
@@ -547,11 +550,11 @@ __global__ void __launch_bounds__(32 * kAggWarps, (NV == 1 ? 8 : OB_AGG_MINB_WID
 // distinct rows into cnt->uniq.  Bit 2s + 1 marks source s's delta row, bit 2s its row.
 __global__ void k_prof_rows(AggArgs a, uint32_t* bits) {
   const int lane = threadIdx.x & 31;
-  const int64_t items = ld_state(&a.cnt->items);
+  const int64_t items = cta_ld(&a.cnt->items);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const float* d_lo = a.dprev;
-  const float* d_hi = a.dprev ? a.dprev + ld_state(a.dT) * a.dld : nullptr;
+  const float* d_hi = a.dprev ? a.dprev + cta_ld(a.dT) * a.dld : nullptr;
   unsigned long long loads = 0;
   for (int64_t it = gw; it < items; it += nw) {
     const int64_t i = a.item_dst[it];
@@ -590,7 +593,7 @@ __global__ void k_prof_popc(const uint32_t* bits, int64_t words, const BlockCoun
 
 __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
   pdl_wait();
-  const int64_t G = ld_state(&a.cnt->groups);
+  const int64_t G = cta_ld(&a.cnt->groups);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = gw; g < G; g += nw) reduce_group<false>(a, g);
@@ -601,10 +604,13 @@ __global__ void __launch_bounds__(256) k_reduce_groups(FinArgs a) {
 #endif
 __global__ void __launch_bounds__(256, OB_FIN_MINB) k_finalize(FinArgs a) {
   pdl_wait();
-  const int64_t D = ld_state(&a.cnt->D);
+  const int64_t D = cta_ld(&a.cnt->D);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = gw; i < D; i += nw) finalize_dst(a, i);
+  __shared__ int64_t s_dT;  // read once per CTA, from shared memory per row (no register held)
+  if (threadIdx.x == 0) s_dT = a.dbuf ? ld_state(a.dT) : 0;
+  __syncthreads();
+  for (int64_t i = gw; i < D; i += nw) finalize_dst(a, i, s_dT);
 }
 
 // moments finalize in float64: phase 1 -> mean (double), phase 2 -> signed root (float)
@@ -612,7 +618,7 @@ __global__ void __launch_bounds__(256) k_finalize_moments(const BlockCounters* c
                                                           const int64_t* item_ptr, const double* partial, int width,
                                                           int phase, int n, double* mean, float* agg, int64_t ldo) {
   pdl_wait();
-  const int64_t D = ld_state(&cnt_->D);
+  const int64_t D = cta_ld(&cnt_->D);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -637,7 +643,7 @@ __global__ void __launch_bounds__(256) k_finalize_moments(const BlockCounters* c
 __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* self, int w,
                               const float* __restrict__ av, float* out) {
   pdl_wait();
-  const int64_t M = ld_state(M_dev);
+  const int64_t M = cta_ld(M_dev);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -943,7 +949,7 @@ int cgp_partial_width(const LayerDev& L) {
 // (max logit, sum exp, sum exp*z); count = local in-edges
 __global__ void __launch_bounds__(256) k_local_raw(FinArgs a, float* lp, int64_t ldp, float* lcnt) {
   pdl_wait();
-  const int64_t D = ld_state(&a.cnt->D);
+  const int64_t D = cta_ld(&a.cnt->D);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -992,7 +998,7 @@ __global__ void __launch_bounds__(256) k_local_raw_f64(const BlockCounters* cnt_
                                                        const int64_t* item_ptr, const double* partial, int width,
                                                        double* lp, int64_t ldp, float* lcnt) {
   pdl_wait();
-  const int64_t D = ld_state(&cnt_->D);
+  const int64_t D = cta_ld(&cnt_->D);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1024,7 +1030,7 @@ struct MergeArgs {
 // softmax rescale, empty destinations aggregate to zero
 __global__ void __launch_bounds__(256) k_merge_parts(MergeArgs m) {
   pdl_wait();
-  const int64_t D = ld_state(m.D_dev);
+  const int64_t D = cta_ld(m.D_dev);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1074,7 +1080,7 @@ __global__ void __launch_bounds__(256) k_merge_moments(int P, PartPtrs parts, in
                                                        OwnerFilter own, int width, int phase, int n, double* mean,
                                                        float* agg, int64_t ldo) {
   pdl_wait();
-  const int64_t D = ld_state(D_dev);
+  const int64_t D = cta_ld(D_dev);
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1298,7 +1304,7 @@ __global__ void k_pad_rows(const ReqParams* rp, int64_t rows, int w, float* dst,
 __global__ void k_delta_rows(const int64_t* T_dev, const int32_t* __restrict__ targets, const float* __restrict__ prev,
                              const float* __restrict__ pe, int64_t ld, float* dbuf) {
   pdl_wait();
-  const int64_t n = ld_state(T_dev) * ld;
+  const int64_t n = cta_ld(T_dev) * ld;
   OB_GRID_STRIDE(t, n) {
     const int64_t i = t / ld;
     const int64_t c = t - i * ld;

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(1024) k_scan_spine(const int64_t* n_dev, int64
   using BS = cub::BlockScan<int64_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int64_t carry;
-  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t n = cta_count(n_dev, n_host);
   const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) k_request_mark(const ReqParams* rp, int64
   pdl_wait();
   extern __shared__ int32_t sq[];  // per-CTA query in-degree histogram (B entries) when B fits
   const int64_t* __restrict__ edges = rp->edges;
-  const int64_t m = ld_state(&rp->m);
+  const int64_t m = cta_ld(&rp->m);
   const bool smem = B <= kMaxSmemQueries;
   const int64_t hi = N + B;
   int64_t err = 0;
@@ -212,7 +212,7 @@ void bitmap_rank(Engine& e, const uint32_t* bits, int64_t words, int64_t* wpre, 
 // RB = R + B slots; query slots take their counts from the per-query in-degrees
 __global__ void k_slots_init(ReqCounters* rc, int B, const int32_t* qdeg, int32_t* rq_cnt, int32_t* rq_fill) {
   pdl_wait();
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   if (blockIdx.x == 0 && threadIdx.x == 0) rc->RB = R + B;
   const int64_t RB = R + B;
   OB_GRID_STRIDE(i, RB) {
@@ -238,9 +238,10 @@ template <class K>
 __global__ void k_rq_count(const ReqParams* rp, int64_t N, const uint32_t* cbits, const int64_t* cwpre,
                            const ReqCounters* rc, int32_t* rq_cnt, K* keys, RqKeyFmt f) {
   pdl_wait();
-  if (ld_state(&rc->err) & (kErrRange | kErrNoQuery)) return;
+  const CtaWords st = cta_ldv(&rc->err, &rp->m, &rc->R);
+  if (st.v[0] & (kErrRange | kErrNoQuery)) return;
   const int64_t* __restrict__ edges = rp->edges;
-  const int64_t m = ld_state(&rp->m), R = ld_state(&rc->R);
+  const int64_t m = st.v[1], R = st.v[2];
   OB_GRID_STRIDE(e, m) {
     int64_t s, d;
     ld_edge(edges, e, s, d);
@@ -261,8 +262,9 @@ __global__ void k_rq_count_all(const int64_t* __restrict__ edges, const int64_t*
                                const uint32_t* cbits, const int64_t* cwpre, const ReqCounters* rc, int32_t* rq_cnt,
                                K* keys, RqKeyFmt f) {
   pdl_wait();
-  if (ld_state(&rc->err) & (kErrRange | kErrNoQuery)) return;
-  const int64_t R = ld_state(&rc->R), m = ld_state(m_dev);  // a CGP slice: edges live in the arena
+  const CtaWords st = cta_ldv(&rc->err, &rc->R, m_dev);
+  if (st.v[0] & (kErrRange | kErrNoQuery)) return;
+  const int64_t R = st.v[1], m = st.v[2];  // a CGP slice: edges live in the arena
   OB_GRID_STRIDE(e, m) {
     int64_t s, d;
     ld_edge(edges, e, s, d);
@@ -273,7 +275,7 @@ __global__ void k_rq_count_all(const int64_t* __restrict__ edges, const int64_t*
 
 __global__ void k_zero_slots(const ReqCounters* rc, int B, int32_t* a, int32_t* b) {
   pdl_wait();
-  const int64_t RB = ld_state(&rc->R) + B;
+  const int64_t RB = cta_ld(&rc->R) + B;
   OB_GRID_STRIDE(i, RB) a[i] = b[i] = 0;
 }
 
@@ -286,7 +288,7 @@ __global__ void k_score(const int32_t* __restrict__ cand_ids, const int32_t* __r
                         const int32_t* __restrict__ indeg, ReqCounters* rc, int32_t* cand_nq, double* score,
                         uint64_t* key, int32_t* tpos, bool ratio) {
   pdl_wait();
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   bool bad = false;
   OB_GRID_STRIDE(c, R) {
     int32_t nq = rq_cnt[c];
@@ -636,7 +638,7 @@ void build_is_table(Engine& e, const int64_t* off, const int32_t* src, double* o
 __global__ void k_is_gather(const int32_t* __restrict__ cand_ids, const ReqCounters* rc,
                             const double* __restrict__ tab, double* out) {
   pdl_wait();
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   OB_GRID_STRIDE(c, R) out[c] = tab[cand_ids[c]];
 }
 
@@ -649,7 +651,7 @@ void launch_is_gather(Engine& e, RequestWs& w, const double* tab, double* out) {
 __global__ void k_score_is(const int32_t* __restrict__ cand_ids, const int32_t* __restrict__ indeg,
                            const ReqCounters* rc, IsParts parts, double* score, uint64_t* key) {
   pdl_wait();
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   OB_GRID_STRIDE(c, R) {
     double sum = 0.0;
     for (int p = 0; p < parts.P; ++p) sum += __ldcg(parts.part[p] + c);
@@ -669,7 +671,7 @@ void launch_score_is(Engine& e, RequestWs& w, const IsParts& parts) {
 __global__ void k_budget(ReqCounters* rc, double gamma, uint32_t* hist) {
   pdl_wait();
   // budget = int(np.floor(gamma * m)) with gamma a Python float: one IEEE fp64 multiply
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   const int64_t b = (int64_t)floor(gamma * (double)R);
   if (threadIdx.x == 0) {
     rc->budget = b;
@@ -696,10 +698,11 @@ __global__ void __launch_bounds__(256) k_sel_round(const uint64_t* __restrict__ 
   __shared__ bool last;
   h[threadIdx.x] = 0;
   __syncthreads();
-  const int64_t R = ld_state(&rc->R), b = ld_state(&rc->budget);
+  const CtaWords st = cta_ldv(&rc->R, &rc->budget, &rc->sel_prefix, &rc->sel_mask);
+  const int64_t R = st.v[0], b = st.v[1];
   const bool active = b > 0 && b < R;
   if (active) {
-    const uint64_t pre = ld_state(&rc->sel_prefix), msk = ld_state(&rc->sel_mask);
+    const uint64_t pre = (uint64_t)st.v[2], msk = (uint64_t)st.v[3];
     OB_GRID_STRIDE(c, R) {
       const uint64_t k = key[c];
       if ((k & msk) == pre) atomicAdd(&h[(k >> shift) & 255], 1u);
@@ -738,11 +741,18 @@ __global__ void __launch_bounds__(256) k_sel_round(const uint64_t* __restrict__ 
 struct SelLoad {
   const uint64_t* key;
   const ReqCounters* rc;
+  int64_t R = 0, b = 0;  // cached by prepare() (once per thread, after pdl_wait)
+  uint64_t thr = 0;
+  __device__ void prepare() {
+    const CtaWords st = cta_ldv(&rc->R, &rc->budget, &rc->sel_prefix);
+    R = st.v[0];
+    b = st.v[1];
+    thr = (uint64_t)st.v[2];
+  }
   __device__ I3 operator()(int64_t c) const {
-    const int64_t R = ld_state(&rc->R), b = ld_state(&rc->budget);
     if (b <= 0) return I3(0);
     if (b >= R) return I3(1, 0, 0);
-    const uint64_t k = key[c], thr = ld_state(&rc->sel_prefix);
+    const uint64_t k = key[c];
     return I3(k > thr ? 1 : 0, k == thr ? 1 : 0, 0);
   }
 };
@@ -751,9 +761,16 @@ struct SelStore3 {
   const int32_t* cand_ids;
   int32_t* targets;
   int32_t* tpos;
+  int64_t take = 0;
+  __device__ void prepare() {
+    const CtaWords st = cta_ldv(&ld.rc->R, &ld.rc->budget, &ld.rc->sel_prefix, &ld.rc->sel_eq_take);
+    ld.R = st.v[0];
+    ld.b = st.v[1];
+    ld.thr = (uint64_t)st.v[2];
+    take = st.v[3];
+  }
   __device__ void operator()(int64_t c, const I3& pre) const {
     const I3 me = ld(c);
-    const int64_t take = ld_state(&ld.rc->sel_eq_take);
     if (me.a || (me.b && pre.b < take)) {
       const int64_t pos = pre.a + (pre.b < take ? pre.b : take);
       targets[pos] = cand_ids[c];
@@ -803,7 +820,7 @@ __global__ void __launch_bounds__(kSelClThreads, 1)
   __shared__ unsigned long long s_tot;  // this CTA's (above << 32 | equal) counts
   pdl_wait();
   const int t = threadIdx.x, lane = t & 31;
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   const int64_t b = (int64_t)floor(gamma * (double)R);  // int(np.floor(gamma * m)): one fp64 multiply
   const int rank = (int)cl.block_rank();
   const int64_t chunk = (R + kSelCl - 1) / kSelCl;
@@ -965,7 +982,7 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* __restrict__ ke
                                                         int64_t tiles_b, int32_t* cnt) {
   pdl_wait();
   __shared__ int32_t h[256];
-  const int64_t m = ld_state(m_dev);
+  const int64_t m = cta_ld(m_dev);
   const int64_t tiles = (m + kRxTile - 1) / kRxTile;
   for (int64_t t = blockIdx.x; t < tiles_b; t += gridDim.x) {
     if (threadIdx.x < 256) h[threadIdx.x] = 0;
@@ -988,7 +1005,7 @@ __global__ void __launch_bounds__(kRxThreads) k_rx_ghist(const K* __restrict__ k
   __shared__ uint32_t h[8 * 256];
   for (int i = threadIdx.x; i < passes * 256; i += kRxThreads) h[i] = 0;
   __syncthreads();
-  const int64_t m = ld_state(m_dev);
+  const int64_t m = cta_ld(m_dev);
   OB_GRID_STRIDE(e, m) {
     const K k = keys[e];
     for (int p = 0; p < passes; ++p) atomicAdd(&h[p * 256 + (int)((k >> (8 * p)) & 255)], 1u);
@@ -1035,7 +1052,6 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
                                                            const uint32_t* __restrict__ ghist,
                                                            const int64_t* __restrict__ dtot) {
   pdl_wait();
-  const int64_t R_fin = FINAL ? ld_state(&rc->R) : 0;  // query-slot source codes >= R are queries
   using BS = cub::BlockScan<int32_t, kRxThreads>;
   using BS64 = cub::BlockScan<int64_t, kRxThreads>;
   __shared__ typename BS64::TempStorage scan_tmp64;
@@ -1050,7 +1066,7 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
   __shared__ int64_t s_t;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t m = ld_state(m_dev);
+  const int64_t m = cta_ld(m_dev);
   const int64_t tiles = (m + kRxTile - 1) / kRxTile;
   if (st || dtot) {  // keys of smaller digits: one-sweep totals, or the row scans' digit totals
     int64_t g = threadIdx.x < 256 ? (st ? (int64_t)ghist[threadIdx.x] : dtot[threadIdx.x]) : 0, gx;
@@ -1152,6 +1168,7 @@ __global__ void __launch_bounds__(kRxThreads, OB_RX_MINB) k_rx_scatter(const K* 
       if (dg[i] < 256) u.exch[rk[i]] = k[i];
     __syncthreads();
     const int n = (int)min((int64_t)kRxTile, m - t * kRxTile);
+    const int64_t R_fin = FINAL ? ld_state(&rc->R) : 0;  // query-slot source codes >= R are queries
     for (int p = threadIdx.x; p < n; p += kRxThreads) {
       const K kk = u.exch[p];
       const int d = (int)((kk >> shift) & 255);
@@ -1387,7 +1404,7 @@ __device__ __forceinline__ uint64_t pcg_out(unsigned __int128 st) {  // XSL-RR
 
 __global__ void k_rnd_raw(Pcg128 g, const ReqCounters* rc, uint32_t* raw) {
   pdl_wait();
-  const int64_t n64 = rnd_raw_len(ld_state(&rc->R)) / 2;
+  const int64_t n64 = rnd_raw_len(cta_ld(&rc->R)) / 2;
   const int64_t chunks = (n64 + kRndChunk - 1) / kRndChunk;
   OB_GRID_STRIDE(c, chunks) {
     const int64_t o0 = c * kRndChunk;
@@ -1410,7 +1427,7 @@ __global__ void __launch_bounds__(32) k_rnd_draws(const uint32_t* __restrict__ r
   pdl_wait();
   __shared__ uint32_t buf[2048];
   const int lane = threadIdx.x;
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   const int64_t L = rnd_raw_len(R);
   int64_t i = R - 1, r = 0, base = 0;
   for (int k = lane; k < 2048; k += 32) buf[k] = k < L ? raw[k] : 0u;
@@ -1531,7 +1548,7 @@ __global__ void __launch_bounds__(kRndKCta) k_rnd_chunkmap(const uint32_t* __res
                                                            const int64_t* __restrict__ lo, int32_t* exit_) {
   pdl_wait();
   __shared__ uint32_t d[kRndW];
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   const int64_t L = rnd_raw_len(R);
   const int64_t c = blockIdx.x / (kRndK / kRndKCta);
   const int k = (int)(blockIdx.x % (kRndK / kRndKCta)) * kRndKCta + threadIdx.x;
@@ -1570,7 +1587,7 @@ __global__ void __launch_bounds__(32) k_rnd_emit(const uint32_t* __restrict__ ra
                                                  int64_t chunks, const int64_t* __restrict__ enter, int32_t* jd) {
   pdl_wait();
   __shared__ uint32_t d[kRndW];
-  const int64_t L = rnd_raw_len(ld_state(&rc->R));
+  const int64_t L = rnd_raw_len(cta_ld(&rc->R));
   for (int64_t c = blockIdx.x; c < chunks; c += gridDim.x) {
     int64_t s = enter[c];
     if (s < 1) continue;
@@ -1593,7 +1610,7 @@ __global__ void __launch_bounds__(32) k_rnd_emit(const uint32_t* __restrict__ ra
 
 __global__ void k_rnd_count(const ReqCounters* rc, const int32_t* __restrict__ jd, int32_t* cnt) {
   pdl_wait();
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   OB_GRID_STRIDE(t, R) {
     if (t >= 1) atomicAdd(cnt + jd[t], 1);
   }
@@ -1602,7 +1619,7 @@ __global__ void k_rnd_count(const ReqCounters* rc, const int32_t* __restrict__ j
 __global__ void k_rnd_fill(const ReqCounters* rc, const int32_t* __restrict__ jd, const int64_t* __restrict__ off,
                            int32_t* fill, int32_t* lst) {
   pdl_wait();
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   OB_GRID_STRIDE(t, R) {
     if (t >= 1) {
       const int32_t v = jd[t];
@@ -1614,7 +1631,7 @@ __global__ void k_rnd_fill(const ReqCounters* rc, const int32_t* __restrict__ jd
 // sort each value's (short) step list, then trace the chosen positions
 __global__ void k_rnd_sort_lists(const ReqCounters* rc, const int64_t* __restrict__ off, int32_t* lst) {
   pdl_wait();
-  const int64_t R = ld_state(&rc->R);
+  const int64_t R = cta_ld(&rc->R);
   OB_GRID_STRIDE(v, R) {
     const int64_t a = off[v], b = off[v + 1];
     for (int64_t x = a + 1; x < b; ++x) {  // insertion sort (expected length <= ln R + 1)
@@ -1632,7 +1649,8 @@ __global__ void k_rnd_sort_lists(const ReqCounters* rc, const int64_t* __restric
 __global__ void k_rnd_trace(ReqCounters* rc, const int32_t* __restrict__ jd, const int64_t* __restrict__ off,
                             const int32_t* __restrict__ lst, uint64_t* key) {
   pdl_wait();
-  const int64_t R = ld_state(&rc->R), budget = ld_state(&rc->budget);
+  const CtaWords st = cta_ldv(&rc->R, &rc->budget);
+  const int64_t R = st.v[0], budget = st.v[1];
   if (budget <= 0 || budget >= R) return;  // SelLoad takes none / all
   OB_GRID_STRIDE(p, budget) {
     int64_t x = p > 0 ? jd[p] : 0, s = p;
