@@ -782,7 +782,8 @@ def main():
         "kernels_ms_per_step": {"agg": round(agg["ms"] / args.steps, 4), "gemm": round(gemm["ms"] / args.steps, 4),
                                 "finalize": round(fin["ms"] / args.steps, 4),
                                 **{name: round(st[name]["ms"] / args.steps, 4) for name in st}},
-        "gemm_tflops": round(gemm["flops"] / (gemm["ms"] / 1e3) / 1e12, 2) if gemm["ms"] > 0 else None,
+        "gemm_tflops": round(gemm["flops"] / (gemm["ms"] / 1e3) / 1e12, 2) if gemm["ms"] > 0 and gemm["flops"] > 0
+        else None,  # 2 M K N per launch whose M is a block counter (listed-row GEMMs count no flops: a lower bound)
         "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "clocks": clk_lanes or clk,
         "gpu_launches": int(launches_lanes if launches_lanes is not None else launches),
         "request": {"edges": int(reqs[0].edges.shape[0]), "candidates": int(bd0.num_candidates),
