@@ -1325,7 +1325,11 @@ void stage_select(Engine& e, RequestWs& w) {
   // the cluster needs 16 SMs of one GPC at once: with one lane and a long request-index sort
   // on the side stream (whose CTAs fill the SMs) it waits for them (cfg2: p50 0.76 -> 0.80 ms),
   // so that case keeps the multi-launch rounds, which slot into whatever SMs free up
-  const bool cluster = e.nlanes > 1 || w.m <= kSelClSoloEdges;
+  static const int64_t solo_edges = [] {  // OB_SEL_CLUSTER_EDGES overrides the single-lane bound
+    const char* v = std::getenv("OB_SEL_CLUSTER_EDGES");
+    return v && v[0] ? std::atoll(v) : kSelClSoloEdges;
+  }();
+  const bool cluster = e.nlanes > 1 || w.m <= solo_edges;
   if (e.cfg.policy != OB_POLICY_RANDOM && cluster && r_max <= (int64_t)kSelCl * kSelClKeys && select_cluster_ok()) {
     launch_select_cluster(s, w.cand_key, w.cand_ids, w.rc, e.cfg.gamma, w.targets, w.cand_tpos);
     return;
