@@ -1341,7 +1341,11 @@ void stage_select(Engine& e, RequestWs& w) {
     select_random(e, w, r_max);
   }
   for (int shift = 56; shift >= 0 && e.cfg.policy != OB_POLICY_RANDOM; shift -= 8) {
-    launch_pdl(k_sel_round, dim3(grid_for(r_max, 256, kNumSMs * 2)), dim3(256), 0, s, w.cand_key, w.rc, shift, w.sel_hist);
+    static const int sel_cap = [] {  // OB_SEL_GRID: CTAs per radix-select round (A/B)
+      const char* v = std::getenv("OB_SEL_GRID");
+      return v && v[0] ? std::max(1, std::atoi(v)) : kNumSMs * 2;
+    }();
+    launch_pdl(k_sel_round, dim3(grid_for(r_max, 256, sel_cap)), dim3(256), 0, s, w.cand_key, w.rc, shift, w.sel_hist);
   }
   // ordered compaction: ties at the threshold resolved by ascending id
   const SelLoad ld{w.cand_key, w.rc};
