@@ -420,6 +420,11 @@ struct LayerRun {
   const int32_t* dyn_src = nullptr;
   const int64_t* ndyn = nullptr;
   int64_t dyn_max = 0;
+  // GAT: the table's source scores stab[v] = ytab[v] . a_src (rows that point into ytab
+  // take their score from it instead of a dot product per request)
+  const float* ytab = nullptr;
+  int64_t ytab_rows = 0, ytab_ld = 0;
+  const float* stab = nullptr;
   // stored aggregates (layer 1 of sum kinds): static CSR-part sums per training node
   // (delta mode, srpe mid-block layers >= 2: the stored rows' CSR-part sums; the
   // gather then visits only recomputed CSR sources, as (h - PE) delta rows)
@@ -747,6 +752,8 @@ struct Engine {
   // whose layer input is static (features at layer 1, stored embeddings above);
   // built lazily before the first request, dropped when weights / PE change
   std::vector<float*> ytab;
+  // GAT layers with a table: the stored rows' source scores ytab[v] . a_src (N floats)
+  std::vector<float*> stab;
   // stored aggregates: for sum kinds (gcn, sage_mean) the layer-1 aggregate of a
   // training node's CSR in-neighbours is static (only request edges, whose
   // sources are queries, change it): sagg1[v] = sum_u w_u x_u (W), raw, unnormalised
@@ -769,6 +776,8 @@ struct Engine {
     cgp_sagg1.clear();
     for (float* t : ytab) dfree(t);
     ytab.clear();
+    for (float* t : stab) dfree(t);
+    stab.clear();
     dfree(sagg1);
     sagg1 = nullptr;
     dfree(yself1);

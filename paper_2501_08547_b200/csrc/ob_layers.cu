@@ -640,6 +640,8 @@ __global__ void __launch_bounds__(256) k_finalize_moments(const BlockCounters* c
 
 // GAT attention scores: s[r] = z[row(r)] . a  (one warp per row)
 // out[r] = z_row(self[r] or r) . av  (GAT source / destination scores)
+// tab/stab (optional): rows inside the stored-transform table [tab, tab + tab_rows * tab_ld)
+// take the precomputed score stab[row index] -- the same dot product, computed once per table
 __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* self, int w,
                               const float* __restrict__ av, float* out) {
   pdl_wait();
@@ -649,6 +651,28 @@ __global__ void k_rowdot_rows(const int64_t* M_dev, RowSrc z, const int32_t* sel
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = gw; r < M; r += nw) {
     const float* row = z.row(self ? (int64_t)self[r] : r);
+    float s = 0.f;
+    for (int c = lane; c < w; c += 32) s = fmaf(row[c], av[c], s);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[r] = s;
+  }
+}
+
+// the same for source rows bound by pointer, where rows inside the stored-transform table
+// [tab, tab + tab_rows * tab_ld) take the table's precomputed score stab[row index]
+__global__ void k_rowdot_rows_tab(const int64_t* M_dev, RowSrc z, int w, const float* __restrict__ av, float* out,
+                                  const float* tab, int64_t tab_rows, int64_t tab_ld, const float* __restrict__ stab) {
+  pdl_wait();
+  const int64_t M = cta_ld(M_dev);
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw; r < M; r += nw) {
+    const float* row = z.row(r);
+    if (row >= tab && row < tab + tab_rows * tab_ld) {
+      if (lane == 0) out[r] = stab[(row - tab) / tab_ld];
+      continue;
+    }
     float s = 0.f;
     for (int c = lane; c < w; c += 32) s = fmaf(row[c], av[c], s);
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -842,7 +866,11 @@ bool run_layer(cudaStream_t s, const LayerDev& L, const LayerRun& r, const Layer
   }
   if (sp.kind == OB_KIND_GAT) {
     const RowSrc z = r.yrow ? RowSrc{r.yrow, nullptr, 0} : RowSrc{nullptr, sc.z, ld_out};
-    launch_pdl(k_rowdot_rows, dim3(grid_for(r.S_max, 8)), dim3(256), 0, s, r.S_dev, z, nullptr, outd, L.a_src, sc.s_src);
+    if (r.yrow && r.stab)  // stored rows' source scores from the table
+      launch_pdl(k_rowdot_rows_tab, dim3(grid_for(r.S_max, 8)), dim3(256), 0, s, r.S_dev, z, outd, L.a_src, sc.s_src,
+                 r.ytab, r.ytab_rows, r.ytab_ld, r.stab);
+    else
+      launch_pdl(k_rowdot_rows, dim3(grid_for(r.S_max, 8)), dim3(256), 0, s, r.S_dev, z, nullptr, outd, L.a_src, sc.s_src);
     launch_pdl(k_rowdot_rows, dim3(grid_for(r.D_max, 8)), dim3(256), 0, s, r.D_dev, z, r.self, outd, L.a_dst, sc.s_dst);
     a.pw = kSmHdr + ld4(outd);
     a.s_src = sc.s_src;
@@ -1344,6 +1372,12 @@ void stage_forward(Engine& e, RequestWs& w, float* d_out) {
       r.ndyn = w.ndyn;
       r.dyn_max = b.S_max;
       r.no_dyn = l == 1 && w.qrows_ready;
+      if (l - 1 < (int)e.stab.size() && e.stab[l - 1]) {
+        r.ytab = e.ytab[l - 1];
+        r.ytab_rows = e.g.N;
+        r.ytab_ld = ld4(L.spec.out_dim);
+        r.stab = e.stab[l - 1];
+      }
     }
     if (l == 1 && e.yself1) {
       r.self_tab = e.yself1;
@@ -1607,6 +1641,7 @@ void build_stored_transforms(Engine& e) {
   int64_t* n_dev = (int64_t*)e.dalloc(sizeof(int64_t));
   OB_CUDA(cudaMemcpyAsync(n_dev, &N, sizeof(int64_t), cudaMemcpyHostToDevice, s));
   e.ytab.assign(k, nullptr);
+  e.stab.assign(k, nullptr);
   for (int l = 1; l <= k; ++l) {
     if (!want[l - 1]) continue;
     const LayerDev& L = e.layers[l - 1];
@@ -1617,6 +1652,19 @@ void build_stored_transforms(Engine& e) {
     g.K1 = L.spec.in_dim;
     tc_gemm(s, g, N);
     e.ytab[l - 1] = t;
+    // GAT, wide rows: the stored rows' source scores (k_rowdot_rows, same arithmetic).  Measured:
+    // H = 512 (Amazon-shaped) p50 1.04 -> 0.85 ms; at H = 128 (cfg3) the per-request dot products
+    // are cheap and warm L2 with the rows the gather reads next (p50 0.324 -> 0.348 ms without them)
+    static const bool stab_off = [] {
+      const char* v = std::getenv("OB_NO_GAT_SCORE_TABLE");
+      return v && v[0] && v[0] != '0';
+    }();
+    if (L.spec.kind == OB_KIND_GAT && L.spec.out_dim >= 256 && !stab_off) {
+      float* st = (float*)e.dalloc(sizeof(float) * N);
+      launch_pdl(k_rowdot_rows, dim3(grid_for(N, 8)), dim3(256), 0, s, (const int64_t*)n_dev, RowSrc{nullptr, t, ld},
+                 (const int32_t*)nullptr, L.spec.out_dim, (const float*)L.a_src, st);
+      e.stab[l - 1] = st;
+    }
   }
   // own-row transform of a transform-first SAGE layer 1 (its destinations' x_v W_self)
   const LayerDev& L1 = e.layers[0];
@@ -1646,7 +1694,7 @@ void build_stored_transforms(Engine& e) {
       if ((size_t)N * (ld + 1) * 4 <= fb / 3) {
         float* ssrc = (float*)e.dalloc(sizeof(float) * N);
         launch_pdl(k_rowdot_rows, dim3(grid_for(N, 8)), dim3(256), 0, s, n_dev, RowSrc{nullptr, e.ytab[0], zld}, nullptr, w, L1.a_src,
-                                                      ssrc);
+                   ssrc);
         e.sagg1 = (float*)e.dalloc(sizeof(float) * N * ld);
         launch_pdl(k_sagg_gat_build, dim3(grid_for(N, 8, kNumSMs * 16)), dim3(256), 0, s, N, e.g.offsets, e.g.nbrs, e.ytab[0], zld, w,
                                                                         ssrc, L1.a_dst, e.sagg1, ld);
