@@ -1,7 +1,7 @@
 # critical-path probe: a 30 us spin inserted after one stage (variant library "w"); p50 moves by
 # ~30 us only when that stage is on the critical path
 out=${OUT:-gpurun_out/whatif}; mkdir -p $out
-for where in none csr qb sel mid; do
+for where in none csr qb sel qrows; do
   OB_LIB_VARIANT=w OB_WHATIF_WHERE=$where OB_WHATIF_DELAY_US=30 python bench.py --no-cpu --no-e2e --steps 30 > $out/$where.json 2> $out/$where.err
   python -c "
 import json
