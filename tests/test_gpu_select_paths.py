@@ -2,8 +2,11 @@
 
 ``stage_select`` runs the whole selection (budget, eight radix-select rounds,
 ordered compaction) as one 16-CTA thread-block cluster when |R|'s bound
-min(N, 2m) fits the cluster's shared memory (393,216 keys), and as the
-multi-launch radix select otherwise.  Both are checked against the oracle's
+min(N, 2m) fits the cluster's shared memory (393,216 keys) and the engine runs
+request lanes or the request is small (bucketed m <= 2^18), and as the
+multi-launch radix select otherwise.  The "cluster" case below serves through
+two request lanes (m = 256,000 buckets to 296,960 > 2^18, so a single lane would
+take the multi-launch path); the "multi-launch" case exceeds the cluster's keys.  Both are checked against the oracle's
 ``select_top`` (policy.py:110-135: top floor(gamma |R|) by score, ties to the
 lowest ids) on tie-heavy requests: serving in-degrees 1..3 and mostly one
 request edge per candidate leave a handful of distinct ratio scores, so the
@@ -58,6 +61,8 @@ def test_select_paths_vs_oracle(N, path, gamma):
     eng = runtime.ServingEngine(g, None, model, w, runtime.ServeConfig(strategy="srpe", gamma=gamma))
     try:
         eng.precompute_pe()
+        if path == "cluster":
+            eng.set_lanes(2)
         emb, _ = eng.serve(req)
         assert np.all(np.isfinite(emb))
         plan = eng.last_plan()
