@@ -110,7 +110,8 @@ __device__ __forceinline__ uint64_t cta_ld(const uint64_t* p) {
 __device__ __forceinline__ int64_t cta_count(const int64_t* p, int64_t fallback) {
   return p ? cta_ld(p) : fallback;
 }
-// Up to four words in one round trip (null pointers read as 0)
+// Up to four words in one round trip (null pointers read as 0); every thread of the CTA must
+// reach it and the CTA must have at least as many threads as non-null pointers
 struct CtaWords {
   int64_t v[4];
 };
