@@ -667,10 +667,15 @@ __global__ void k_rowdot_rows_tab(const int64_t* M_dev, RowSrc z, int w, const f
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool pow2 = (tab_ld & (tab_ld - 1)) == 0;  // row index by shift, not a 64-bit divide
+  const int sh = pow2 ? __ffsll((long long)tab_ld) - 1 : 0;
   for (int64_t r = gw; r < M; r += nw) {
     const float* row = z.row(r);
     if (row >= tab && row < tab + tab_rows * tab_ld) {
-      if (lane == 0) out[r] = stab[(row - tab) / tab_ld];
+      if (lane == 0) {
+        const int64_t off = row - tab;
+        out[r] = stab[pow2 ? off >> sh : off / tab_ld];
+      }
       continue;
     }
     float s = 0.f;
